@@ -1,0 +1,134 @@
+"""Whole-fit pins for oracle/fit.py: exact MCD brute force, equivariance, flag rates."""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import fit as F
+from oracle.chi2 import consistency_factor
+from oracle.unimcd import unimcd_reweighted
+from paper_1910_05615_b200 import datagen
+
+
+def _exact_mcd_logdet(X, h):
+    best = np.inf
+    for S in itertools.combinations(range(X.shape[0]), h):
+        C = np.cov(X[list(S)], rowvar=False)
+        s, ld = np.linalg.slogdet(C)
+        if s > 0 and ld < best:
+            best = ld
+    return best
+
+
+def _raw_logdet_unscaled(r):
+    b = r.blocks[0]
+    return b.starts[b.chosen].logdet
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_detmcd_objective_at_least_exact_mcd(seed):
+    # north_star: n = 12, p = 2, brute force over all C(12, 7) = 792 subsets
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((12, 2)) @ np.array([[1.0, 0.4], [0.0, 0.7]])
+    X[:2] += 6.0
+    r = F.fit(X, h=7)
+    Xz = (X - r.loc) / r.scale
+    exact = _exact_mcd_logdet(Xz, 7)
+    assert _raw_logdet_unscaled(r) >= exact - 1e-12
+
+
+def test_detmcd_equals_exact_mcd_when_separated():
+    # 9 tight inliers + 3 far points, h = 9 (C(12, 9) = 220 subsets)
+    rng = np.random.default_rng(10)
+    X = np.vstack([rng.standard_normal((9, 2)) * 0.5, [[40.0, 40.0], [-35.0, 50.0], [60.0, -45.0]]])
+    r = F.fit(X, h=9)
+    Xz = (X - r.loc) / r.scale
+    assert _raw_logdet_unscaled(r) == pytest.approx(_exact_mcd_logdet(Xz, 9), abs=1e-12)
+    assert set(r.blocks[0].starts[r.blocks[0].chosen].H.tolist()) == set(range(9))
+
+
+def test_raw_scatter_and_destandardisation():
+    d = datagen.make_config(1)
+    r = F.fit(d.X, h=d.h)
+    b = r.blocks[0]
+    H = b.starts[b.chosen].H
+    XH = d.X[H]
+    # A1: mean of H; c(alpha)/(h-1) SSCP, alpha = h/n — in X units
+    assert np.allclose(r.mu_raw, XH.mean(0), rtol=1e-12, atol=1e-13)
+    assert np.allclose(r.Sigma_raw, consistency_factor(d.h / 1000, 5) * np.cov(XH, rowvar=False), rtol=1e-11)
+    # the standardisation is the univariate reweighted MCD of each column
+    for j in range(5):
+        u = unimcd_reweighted(d.X[:, j])
+        assert r.loc[j] == u.loc and r.scale[j] == u.scale
+
+
+def test_power_of_two_column_scaling_exact():
+    d = datagen.make_config(1)
+    s = 2.0 ** np.array([3, -2, 0, 5, -7])
+    r = F.fit(d.X, h=d.h)
+    r2 = F.fit(d.X * s, h=d.h)
+    assert np.array_equal(r.flags, r2.flags)
+    assert np.array_equal(r.blocks[0].starts[0].H, r2.blocks[0].starts[0].H)
+    assert np.array_equal(r2.mu_rew, r.mu_rew * s)
+    assert np.array_equal(r2.Sigma_rew, r.Sigma_rew * np.outer(s, s))
+
+
+def test_translation_equivariance():
+    d = datagen.make_config(1)
+    a = np.array([10.0, -3.5, 100.25, 0.5, 7.0])
+    r = F.fit(d.X, h=d.h)
+    r2 = F.fit(d.X + a, h=d.h)
+    assert np.array_equal(r.flags, r2.flags)
+    assert np.allclose(r2.mu_rew, r.mu_rew + a, rtol=1e-12, atol=1e-10)
+    assert np.allclose(r2.Sigma_rew, r.Sigma_rew, rtol=1e-9)
+
+
+def test_row_permutation_invariance():
+    d = datagen.make_config(1)
+    P = np.random.default_rng(3).permutation(1000)
+    r = F.fit(d.X, h=d.h)
+    r2 = F.fit(d.X[P], h=d.h)
+    assert np.array_equal(r.flags[P], r2.flags)
+    assert np.allclose(r2.Sigma_rew, r.Sigma_rew, rtol=1e-12)
+    b, b2 = r.blocks[0], r2.blocks[0]
+    assert set(P[b2.starts[b2.chosen].H].tolist()) == set(b.starts[b.chosen].H.tolist())
+
+
+def test_clean_flag_rate_and_shift_outliers():
+    X = datagen.gaussian(20_000, 4, seed=20, sigma=datagen.a09(4))
+    r = F.fit(X, alpha=0.75)
+    assert abs(r.flags.mean() - 0.025) < 0.01
+    d = datagen.make_config(1)
+    r1 = F.fit(d.X, h=d.h)
+    assert r1.flags[d.outliers].all()
+
+
+def test_h_equal_n_gives_classical_raw():
+    X = datagen.gaussian(300, 3, seed=21)
+    r = F.fit(X, h=300)
+    assert np.allclose(r.mu_raw, X.mean(0), rtol=1e-12, atol=1e-14)
+    assert np.allclose(r.Sigma_raw, np.cov(X, rowvar=False), rtol=1e-11)
+
+
+def test_blocked_fit_q1_equals_serial_and_q4_runs():
+    d = datagen.make_config(2, n=20_000)
+    r1 = F.fit(d.X, h=d.h, q=1)
+    r4 = F.fit(d.X, h=d.h, q=4, seed=5)
+    assert len(r4.blocks) == 4 and len(r4.kept_blocks) == 2
+    assert r4.weights.sum() > 0.5 * 20_000
+    # both fits see the same cluster-dominated geometry: the q=4 aggregate is close
+    assert np.linalg.norm(r4.Sigma_rew - r1.Sigma_rew) / np.linalg.norm(r1.Sigma_rew) < 0.2
+
+
+def test_errors():
+    X = datagen.gaussian(50, 3, seed=22)
+    with pytest.raises(F.FitError):
+        F.fit(X[:5], h=4)
+    Y = X.copy(); Y[3, 1] = np.nan
+    with pytest.raises(F.FitError) as e:
+        F.fit(Y, h=30)
+    assert e.value.code == "NONFINITE"
+    Y = X.copy(); Y[:, 2] = 1.0
+    with pytest.raises(F.FitError) as e:
+        F.fit(Y, h=30)
+    assert e.value.code == "DEGENERATE_COLUMN"
