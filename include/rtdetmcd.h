@@ -1,0 +1,194 @@
+/* rtdetmcd.h — C ABI of the B200-native RT-DetMCD hot path (libpaper_1910_05615_b200.so).
+ *
+ * Method: "Real-time outlier detection for large datasets by RT-DetMCD",
+ * De Ketelaere, Hubert, Raymaekers, Rousseeuw, Vranckx (arXiv 1910.05615),
+ * cited as PAPER.md:<line> (section / equation).
+ *
+ * Conventions (all entry points)
+ *   - All floating point is IEEE binary64.  A data matrix X is n x p ROW-MAJOR
+ *     (row = observation), 1 <= p <= 40,
+ *     n > 2p.
+ *   - Pointers marked [dev|host] may be device memory (cudaMalloc / torch CUDA
+ *     tensor) or host memory (pageable or pinned); the library inspects each
+ *     with cudaPointerGetAttributes and copies host buffers itself.  Pointers
+ *     marked [host] must be host memory; [dev] must be device memory.
+ *   - Ownership: the caller owns every input and output buffer.  Inputs are
+ *     read-only.  No pointer is retained after a call returns.  The context
+ *     owns a grow-only device workspace (or uses one handed over with
+ *     rtdetmcd_set_workspace) and its CUDA stream.
+ *   - Synchrony: every call enqueues its work on the context stream and
+ *     returns after it completed; results are valid on return.  A context is
+ *     not re-entrant (one context per thread / per rank).
+ *   - Errors: a call returns a non-zero rtdetmcd_status and stores a message
+ *     retrievable with rtdetmcd_last_error(); output buffers are then
+ *     unspecified.  The library never calls exit/abort and never throws
+ *     across the ABI.  RTD_E_CUDA means a CUDA runtime error (message names
+ *     the call); the context should then be destroyed.
+ */
+#ifndef RTDETMCD_H
+#define RTDETMCD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTDETMCD_ABI_VERSION 1
+
+typedef struct rtdetmcd_ctx rtdetmcd_ctx;
+
+typedef enum {
+  RTD_OK = 0,
+  RTD_E_INVALID_ARG = 1,          /* sizes / options violate the preconditions below */
+  RTD_E_NONFINITE = 2,            /* a NaN/Inf entry (or x <= 0 with log_transform); message names the row */
+  RTD_E_DEGENERATE_COLUMN = 3,    /* univariate MCD scale is zero for a column */
+  RTD_E_BOTH_STARTS_FAILED = 4,   /* q = 1: both initial estimators were dropped */
+  RTD_E_TOO_FEW_VALID_BLOCKS = 5, /* q > 1: more than floor(q/2) blocks failed */
+  RTD_E_NOT_PD = 6,               /* a scatter matrix that must be positive definite is not */
+  RTD_E_CUDA = 7,
+  RTD_E_OOM = 8,
+  RTD_E_INTERNAL = 9
+} rtdetmcd_status;
+
+enum { RTD_PART_PERMUTE = 0, RTD_PART_CONTIGUOUS = 1 };
+
+/* warning bits of rtdetmcd_result.warnings (non-fatal) */
+enum {
+  RTD_W_H_BELOW_BOUND = 1,  /* h < [(n+p+1)/2]; accepted since h > p */
+  RTD_W_MAX_CSTEPS = 2,     /* a chosen start hit max_csteps before H_new == H_old */
+  RTD_W_BLOCK_FAILED = 4,   /* q > 1: at least one block had both starts dropped */
+  RTD_W_START_FAILED = 8    /* at least one start was dropped (ill-conditioned / singular) */
+};
+
+typedef struct {
+  int64_t h;             /* > 0: explicit coverage, p < h <= n; 0: h = floor(alpha * n) */
+  double alpha;          /* used iff h == 0; default 0.5 */
+  int32_t shards;        /* q >= 1 blocks; 0: q = max(floor(n/(p omega)), 1) capped by shard_cap
+                            (eq. partitionsize) */
+  int32_t shard_cap;     /* cap for the q rule; default 64 */
+  int64_t omega;         /* minimum observations per dimension per block; default 4096 */
+  double kappa_max;      /* condition threshold; default 1000 */
+  double quantile;       /* cut-off quantile; default 0.975 */
+  int32_t max_csteps;    /* C-step cap per start; default 100 */
+  int32_t refresh_every; /* update-based C-steps: full recompute of the sums every this many steps; default 32 */
+  uint64_t seed;         /* key of the random partition */
+  int32_t partition;     /* RTD_PART_PERMUTE (keyed Feistel permutation, default) | RTD_PART_CONTIGUOUS */
+  int32_t log_transform; /* 1: fit ln(x) (x must be > 0), as in BASELINE config 5 */
+} rtdetmcd_opts;
+
+/* Fills *o with the defaults above. */
+void rtdetmcd_opts_default(rtdetmcd_opts* o);
+
+typedef struct {
+  /* [host] caller-allocated, nullable; ORIGINAL units of X (de-standardised, after ln when log_transform) */
+  double* loc;        /* p: univariate reweighted MCD location per column */
+  double* scale;      /* p: univariate reweighted MCD scale per column */
+  double* mu_raw;     /* p: raw MCD centre (pooled when q > 1) */
+  double* sigma_raw;  /* p*p row-major: c(alpha)-scaled raw scatter */
+  double* mu_rew;     /* p: reweighted centre */
+  double* sigma_rew;  /* p*p: reweighted scatter, scaled by c(0.975, p) */
+  /* scalars written by the library */
+  double logdet_raw;  /* log det of the unscaled raw scatter of the chosen start (q = 1), standardised units */
+  double cutoff2;     /* chi2_{p, quantile}: a row is flagged iff RD^2 > cutoff2 */
+  int64_t h;          /* coverage used */
+  int64_t h_block;    /* per-block coverage floor(h m / n) */
+  int64_t m;          /* rows per block floor(n/q) */
+  int32_t q_used;
+  int32_t warnings;   /* RTD_W_* bits */
+  int32_t n_valid_blocks;
+  int32_t n_kept_blocks;
+  int64_t n_weighted; /* rows with weight 1 in the reweighting */
+  /* [host] nullable per-block diagnostics, sized q (block_chosen) or 2q (per (block, start)) */
+  int32_t* block_chosen;  /* 0 = wrapping start, 1 = GSSCM start, -1 = block failed */
+  int32_t* start_steps;   /* C-steps run (distance passes) per (block, start) */
+  int32_t* start_status;  /* 1 converged, 2 not PD, 3 condition >= kappa_max, 4 max steps, 5 refinement dropped */
+  double* start_logdet;   /* log det of the converged unscaled scatter per (block, start) */
+  /* [dev|host] nullable, sized n, in ORIGINAL row order */
+  uint8_t* flags;    /* 1 iff RD^2 > cutoff2 under (mu_rew, sigma_rew) */
+  double* rd2;       /* final squared robust distance */
+  uint8_t* weights;  /* reweighting weight (0 for rows discarded by the partition) */
+  uint8_t* hsubset;  /* 1 iff the row is in its block's chosen h-subset */
+} rtdetmcd_result;
+
+/* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t to
+ * enqueue on (e.g. torch.cuda.current_stream().cuda_stream) or NULL for a
+ * private stream. */
+rtdetmcd_status rtdetmcd_create(rtdetmcd_ctx** ctx, int device, void* cuda_stream);
+void rtdetmcd_destroy(rtdetmcd_ctx* ctx);
+const char* rtdetmcd_last_error(const rtdetmcd_ctx* ctx);
+
+/* Hand over a caller-owned device buffer as workspace (e.g. a torch uint8
+ * tensor).  bytes must be >= rtdetmcd_fit_workspace_size(); the context then
+ * never allocates device memory itself.  dev_ptr = NULL reverts to the
+ * context's own grow-only allocation. */
+rtdetmcd_status rtdetmcd_set_workspace(rtdetmcd_ctx* ctx, void* dev_ptr, size_t bytes);
+size_t rtdetmcd_fit_workspace_size(int64_t n, int32_t p, const rtdetmcd_opts* opts);
+
+/* The whole RT-DetMCD fit (serial IDC for q = 1, parallel IDCP_q for q > 1,
+ * PAPER.md:1076-1100) followed by the flag pass over all n rows:
+ *   standardise (§3.1) -> [partition, §4] -> S~1, S~2 (§3.2) -> refinement (§3.3)
+ *   -> C-steps with Cholesky distances and update-based sums (§3.4-3.5)
+ *   -> lowest-determinant start -> [median / KL / pooling, §4 steps 5-7]
+ *   -> reweighting (§2.1, §4 steps 8-9) -> flagging (§4 step 10).
+ * X [dev|host]: n x p row-major.  out: any nullable field may be NULL. */
+rtdetmcd_status rtdetmcd_fit(rtdetmcd_ctx* ctx, const double* X, int64_t n, int32_t p, const rtdetmcd_opts* opts,
+                             rtdetmcd_result* out);
+
+/* Step 10 on its own (the paper's 8.4 ms "flagging" figure,
+ * PAPER.md:1624-1627): rd2_i = (x_i - mu)^T sigma^-1 (x_i - mu) by a Cholesky
+ * solve, flags_i = rd2_i > chi2_{p, quantile}.
+ * X [dev|host] n x p row-major (ln applied first when log_transform);
+ * mu [host] p; sigma [host] p*p row-major SPD (RTD_E_NOT_PD otherwise);
+ * flags, rd2 [dev|host] n, either may be NULL. */
+rtdetmcd_status rtdetmcd_flag(rtdetmcd_ctx* ctx, const double* X, int64_t n, int32_t p, const double* mu,
+                              const double* sigma, double quantile, int32_t log_transform, uint8_t* flags,
+                              double* rd2);
+
+/* ---- stage entry points: the same kernels, exposed for intermediate parity
+ * checks and as building blocks of the multi-process driver ---- */
+
+/* Univariate reweighted MCD with h~ = floor(len/2)+1 of
+ * ncols columns.  cols [dev] column-major (column j at cols + j*len).
+ * Outputs [host] sized ncols, nullable: reweighted loc/scale, raw window mean
+ * and raw variance SQ/(h~-1) (no factor), window start in the sorted column.
+ * RTD_E_DEGENERATE_COLUMN if a scale is zero (message names the column). */
+rtdetmcd_status rtdetmcd_unimcd(rtdetmcd_ctx* ctx, const double* cols, int64_t len, int32_t ncols, double* loc,
+                                double* scale, double* raw_loc, double* raw_var, int64_t* start);
+
+/* S~1 (wrapped covariance) and S~2 (LR-GSSCM)
+ * of a standardised block.  Z [dev] column-major m x p (column k at Z + k*m).
+ * S1, S2 [host] p*p row-major.  *s2_ok = 0 when the norms have zero IQR. */
+rtdetmcd_status rtdetmcd_initial(rtdetmcd_ctx* ctx, const double* Z, int64_t m, int32_t p, double* S1, double* S2,
+                                 int32_t* s2_ok);
+
+/* Refinement of an initial scatter S.  Z as above, S [host]
+ * p*p.  Outputs [host]: mu (p), sigma (p*p), eigenvalues lam (p, nullable);
+ * *ok = 0 when the start is dropped (lambda_p <= 0, lambda_1/lambda_p > kappa_max,
+ * or a degenerate univariate scale). */
+rtdetmcd_status rtdetmcd_refine(rtdetmcd_ctx* ctx, const double* Z, int64_t m, int32_t p, const double* S,
+                                double kappa_max, double* mu, double* sigma, double* lam, int32_t* ok);
+
+/* C-steps to convergence from (mu0, sigma0).
+ * Z as above; mu0, sigma0 [host].  Outputs [host]: mu, sigma (unscaled
+ * covariance of the final h-subset), logdet, steps, status (1 converged,
+ * 2 not PD, 3 condition >= kappa_max, 4 max steps).  hsubset [dev|host] m
+ * bytes, nullable.  logdet_traj [host] nullable, max_steps+1 entries:
+ * log det of the scatter entering C-step s (s = 1..steps). */
+rtdetmcd_status rtdetmcd_csteps(rtdetmcd_ctx* ctx, const double* Z, int64_t m, int32_t p, int64_t h,
+                                const double* mu0, const double* sigma0, double kappa_max, int32_t max_steps,
+                                int32_t refresh_every, double* mu, double* sigma, double* logdet, int32_t* steps,
+                                int32_t* status, uint8_t* hsubset, double* logdet_traj);
+
+/* Host numerics used by the fit, exported for checking. */
+double rtdetmcd_chi2_quantile(double prob, int32_t dof);
+double rtdetmcd_consistency_factor(double alpha, int32_t p);
+int32_t rtdetmcd_choose_q(int64_t n, int32_t p, int64_t omega, int32_t cap); /* eq. partitionsize */
+/* pi(i) of the keyed Feistel partition permutation (reading R13), for i in [0, n). out [host] n. */
+rtdetmcd_status rtdetmcd_partition_perm(rtdetmcd_ctx* ctx, int64_t n, uint64_t seed, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTDETMCD_H */

@@ -1,0 +1,268 @@
+"""Python face of the C ABI (include/rtdetmcd.h): marshalling only.
+
+Inputs may be numpy arrays or torch tensors (CPU or CUDA); the library copies
+host buffers itself.  Per-row outputs land on the device of X when X is a
+CUDA tensor, else in numpy arrays.  There is no CPU path: every call goes
+through libpaper_1910_05615_b200.so and raises if it is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import RTD_STATUS, Opts, Result, lib
+
+
+class RTDError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{RTD_STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = RTD_STATUS.get(code, str(code))
+
+
+def _torch():
+    import torch
+    return torch
+
+
+_CTX: dict = {}
+
+
+def _ctx(device: int = 0):
+    """Context per (device, torch current stream)."""
+    torch = _torch()
+    stream = 0
+    if torch.cuda.is_available():
+        stream = torch.cuda.current_stream(device).cuda_stream
+    key = (device, stream)
+    if key not in _CTX:
+        h = C.c_void_p()
+        rc = lib().rtdetmcd_create(C.byref(h), device, C.c_void_p(stream) if stream else None)
+        if rc != 0:
+            raise RTDError(rc, "rtdetmcd_create failed")
+        _CTX[key] = {"h": h, "ws": None}
+    return _CTX[key]
+
+
+def _check(rc: int, ctx) -> None:
+    if rc != 0:
+        raise RTDError(rc, lib().rtdetmcd_last_error(ctx["h"]).decode())
+
+
+def _as_f64(x):
+    """(pointer, keepalive, is_cuda, device) of a C-contiguous float64 buffer."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        t = x.detach()
+        if t.dtype != torch.float64:
+            t = t.to(torch.float64)
+        t = t.contiguous()
+        return t.data_ptr(), t, t.is_cuda, (t.device.index or 0) if t.is_cuda else 0
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    return a.ctypes.data, a, False, 0
+
+
+def _out_buffer(n: int, dtype, on_cuda: bool, device: int):
+    torch = _torch()
+    if on_cuda:
+        t = torch.empty(n, dtype={np.uint8: torch.uint8, np.float64: torch.float64}[dtype], device=f"cuda:{device}")
+        return t, t.data_ptr()
+    a = np.empty(n, dtype=dtype)
+    return a, a.ctypes.data
+
+
+def default_opts(**kw) -> Opts:
+    o = Opts()
+    lib().rtdetmcd_opts_default(C.byref(o))
+    for k, v in kw.items():
+        if v is None:
+            continue
+        if not hasattr(o, k):
+            raise TypeError(f"unknown option {k}")
+        setattr(o, k, v)
+    return o
+
+
+@dataclass
+class Fit:
+    loc: np.ndarray
+    scale: np.ndarray
+    mu_raw: np.ndarray
+    sigma_raw: np.ndarray
+    mu_rew: np.ndarray
+    sigma_rew: np.ndarray
+    logdet_raw: float
+    cutoff2: float
+    h: int
+    h_block: int
+    m: int
+    q: int
+    warnings: int
+    n_valid_blocks: int
+    n_kept_blocks: int
+    n_weighted: int
+    block_chosen: np.ndarray
+    start_steps: np.ndarray
+    start_status: np.ndarray
+    start_logdet: np.ndarray
+    flags: object = None
+    rd2: object = None
+    weights: object = None
+    hsubset: object = None
+    extra: dict = field(default_factory=dict)
+
+
+def workspace_size(n: int, p: int, **opts) -> int:
+    o = default_opts(**opts)
+    return int(lib().rtdetmcd_fit_workspace_size(n, p, C.byref(o)))
+
+
+def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, kappa_max: float = 1000.0,
+        quantile: float = 0.975, max_csteps: int = 100, refresh_every: int = 32, partition: int = 0,
+        log_transform: bool = False, outputs=("flags", "rd2", "weights", "hsubset"), device: int | None = None,
+        torch_workspace: bool = True) -> Fit:
+    """rtdetmcd_fit on an n x p row-major float64 matrix (numpy or torch, host or device)."""
+    ptr, keep, is_cuda, dev = _as_f64(X)
+    n, p = int(keep.shape[0]), int(keep.shape[1])
+    dev = dev if device is None else device
+    ctx = _ctx(dev)
+    o = default_opts(h=int(h or 0), alpha=float(alpha), shards=int(q), seed=int(seed), kappa_max=float(kappa_max),
+                     quantile=float(quantile), max_csteps=int(max_csteps), refresh_every=int(refresh_every),
+                     partition=int(partition), log_transform=int(bool(log_transform)))
+    L = lib()
+    if torch_workspace:
+        torch = _torch()
+        need = int(L.rtdetmcd_fit_workspace_size(n, p, C.byref(o)))
+        ws = ctx["ws"]
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{dev}")
+            ctx["ws"] = ws
+        _check(L.rtdetmcd_set_workspace(ctx["h"], C.c_void_p(ws.data_ptr()), ws.numel()), ctx)
+    r = Result()
+    host = {k: np.zeros(p) for k in ("loc", "scale", "mu_raw", "mu_rew")}
+    host.update({k: np.zeros((p, p)) for k in ("sigma_raw", "sigma_rew")})
+    qmax = int(q) if q and q > 0 else 1024
+    host["block_chosen"] = np.zeros(qmax, np.int32)
+    host["start_steps"] = np.zeros(2 * qmax, np.int32)
+    host["start_status"] = np.zeros(2 * qmax, np.int32)
+    host["start_logdet"] = np.zeros(2 * qmax, np.float64)
+    for k, a in host.items():
+        setattr(r, k, a.ctypes.data)
+    rows = {}
+    for k, dt in (("flags", np.uint8), ("rd2", np.float64), ("weights", np.uint8), ("hsubset", np.uint8)):
+        if k in outputs:
+            buf, bp = _out_buffer(n, dt, is_cuda, dev)
+            rows[k] = buf
+            setattr(r, k, bp)
+    rc = L.rtdetmcd_fit(ctx["h"], C.c_void_p(ptr), n, p, C.byref(o), C.byref(r))
+    if torch_workspace:
+        L.rtdetmcd_set_workspace(ctx["h"], None, 0)
+    _check(rc, ctx)
+    qu = r.q_used
+    return Fit(loc=host["loc"], scale=host["scale"], mu_raw=host["mu_raw"], sigma_raw=host["sigma_raw"],
+               mu_rew=host["mu_rew"], sigma_rew=host["sigma_rew"], logdet_raw=r.logdet_raw, cutoff2=r.cutoff2,
+               h=r.h, h_block=r.h_block, m=r.m, q=qu, warnings=r.warnings, n_valid_blocks=r.n_valid_blocks,
+               n_kept_blocks=r.n_kept_blocks, n_weighted=r.n_weighted,
+               block_chosen=host["block_chosen"][:qu].copy(), start_steps=host["start_steps"][:2 * qu].copy(),
+               start_status=host["start_status"][:2 * qu].copy(), start_logdet=host["start_logdet"][:2 * qu].copy(),
+               **rows)
+
+
+def flag(X, mu, sigma, quantile: float = 0.975, log_transform: bool = False, want_rd2: bool = True):
+    """rtdetmcd_flag: (flags, rd2) of rows of X under (mu, sigma)."""
+    ptr, keep, is_cuda, dev = _as_f64(X)
+    n, p = int(keep.shape[0]), int(keep.shape[1])
+    ctx = _ctx(dev)
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    sg = np.ascontiguousarray(sigma, dtype=np.float64)
+    fl, fp = _out_buffer(n, np.uint8, is_cuda, dev)
+    rd, rp = _out_buffer(n, np.float64, is_cuda, dev) if want_rd2 else (None, None)
+    _check(lib().rtdetmcd_flag(ctx["h"], C.c_void_p(ptr), n, p, mu.ctypes.data, sg.ctypes.data, float(quantile),
+                               int(bool(log_transform)), C.c_void_p(fp), C.c_void_p(rp) if rp else None), ctx)
+    return fl, rd
+
+
+def unimcd(cols, device: int = 0):
+    """Univariate reweighted MCD of each column of a (ncols, len) device tensor."""
+    ptr, keep, is_cuda, dev = _as_f64(cols)
+    if not is_cuda:
+        raise ValueError("unimcd stage call takes a CUDA tensor (ncols, len)")
+    ncols, ln = int(keep.shape[0]), int(keep.shape[1])
+    ctx = _ctx(dev)
+    out = {k: np.zeros(ncols) for k in ("loc", "scale", "raw_loc", "raw_var")}
+    start = np.zeros(ncols, np.int64)
+    _check(lib().rtdetmcd_unimcd(ctx["h"], C.c_void_p(ptr), ln, ncols, out["loc"].ctypes.data,
+                                 out["scale"].ctypes.data, out["raw_loc"].ctypes.data, out["raw_var"].ctypes.data,
+                                 start.ctypes.data), ctx)
+    out["start"] = start
+    return out
+
+
+def _zcols(Z):
+    """Z given as a (m, p) CUDA tensor -> column-major device buffer."""
+    torch = _torch()
+    if not (isinstance(Z, torch.Tensor) and Z.is_cuda):
+        raise ValueError("stage calls take a CUDA tensor")
+    Zc = Z.detach().to(torch.float64).t().contiguous()
+    return Zc, int(Z.shape[0]), int(Z.shape[1]), Z.device.index or 0
+
+
+def initial(Z):
+    Zc, m, p, dev = _zcols(Z)
+    ctx = _ctx(dev)
+    S1, S2 = np.zeros((p, p)), np.zeros((p, p))
+    ok = C.c_int32()
+    _check(lib().rtdetmcd_initial(ctx["h"], C.c_void_p(Zc.data_ptr()), m, p, S1.ctypes.data, S2.ctypes.data,
+                                  C.byref(ok)), ctx)
+    return S1, S2, bool(ok.value)
+
+
+def refine(Z, S, kappa_max: float = 1000.0):
+    Zc, m, p, dev = _zcols(Z)
+    ctx = _ctx(dev)
+    S = np.ascontiguousarray(S, dtype=np.float64)
+    mu, sg, lam = np.zeros(p), np.zeros((p, p)), np.zeros(p)
+    ok = C.c_int32()
+    _check(lib().rtdetmcd_refine(ctx["h"], C.c_void_p(Zc.data_ptr()), m, p, S.ctypes.data, float(kappa_max),
+                                 mu.ctypes.data, sg.ctypes.data, lam.ctypes.data, C.byref(ok)), ctx)
+    return mu, sg, lam, bool(ok.value)
+
+
+def csteps(Z, mu0, sigma0, h: int, kappa_max: float = 1000.0, max_steps: int = 100, refresh_every: int = 32):
+    torch = _torch()
+    Zc, m, p, dev = _zcols(Z)
+    ctx = _ctx(dev)
+    mu0 = np.ascontiguousarray(mu0, dtype=np.float64)
+    s0 = np.ascontiguousarray(sigma0, dtype=np.float64)
+    mu, sg = np.zeros(p), np.zeros((p, p))
+    ld = C.c_double()
+    steps, status = C.c_int32(), C.c_int32()
+    hs = torch.empty(m, dtype=torch.uint8, device=Zc.device)
+    traj = np.full(max_steps + 1, np.nan)
+    _check(lib().rtdetmcd_csteps(ctx["h"], C.c_void_p(Zc.data_ptr()), m, p, int(h), mu0.ctypes.data, s0.ctypes.data,
+                                 float(kappa_max), int(max_steps), int(refresh_every), mu.ctypes.data, sg.ctypes.data,
+                                 C.byref(ld), C.byref(steps), C.byref(status), C.c_void_p(hs.data_ptr()),
+                                 traj.ctypes.data), ctx)
+    return {"mu": mu, "sigma": sg, "logdet": ld.value, "steps": steps.value, "status": status.value,
+            "hsubset": hs, "logdet_traj": traj}
+
+
+def chi2_quantile(prob: float, dof: int) -> float:
+    return float(lib().rtdetmcd_chi2_quantile(float(prob), int(dof)))
+
+
+def consistency_factor(alpha: float, p: int) -> float:
+    return float(lib().rtdetmcd_consistency_factor(float(alpha), int(p)))
+
+
+def choose_q(n: int, p: int, omega: int = 4096, cap: int = 0) -> int:
+    return int(lib().rtdetmcd_choose_q(int(n), int(p), int(omega), int(cap)))
+
+
+def partition_perm(n: int, seed: int, device: int = 0) -> np.ndarray:
+    ctx = _ctx(device)
+    out = np.zeros(n, np.int64)
+    _check(lib().rtdetmcd_partition_perm(ctx["h"], int(n), C.c_uint64(seed & (2 ** 64 - 1)), out.ctypes.data), ctx)
+    return out

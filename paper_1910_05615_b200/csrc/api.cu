@@ -1,0 +1,1046 @@
+// C ABI and the host orchestrator of the RT-DetMCD hot path.
+// Every arithmetic step runs in the kernels of k_*.cu; this file sequences
+// them, owns the workspace and turns device status words into ABI errors.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../include/rtdetmcd.h"
+#include "rtd_internal.h"
+#include "rtd_linalg.h"
+
+namespace rtd {
+void launch_feistel_fwd(long long n, unsigned long long seed, long long* out, cudaStream_t st);
+void launch_uni_extract(const UniOut* uni, int p, int which, double* out, cudaStream_t st);
+void launch_scatter_u8(const uint8_t* src, const long long* rowmap, long long total, uint8_t* dst, cudaStream_t st);
+void launch_weights_from_d2(const double* d2, long long total, double c2, const long long* rowmap, uint8_t* dst,
+                            cudaStream_t st);
+void launch_scale_copy(const double* src, double* dst, int p, double factor, cudaStream_t st);
+void launch_hsub_from_mem(const uint8_t* mem_all, const int* chosen_inst, int q, long long m, const long long* rowmap,
+                          uint8_t* dst, cudaStream_t st);
+}  // namespace rtd
+
+using namespace rtd;
+
+struct rtdetmcd_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  char* ws = nullptr;
+  size_t ws_cap = 0;
+  bool ws_user = false;
+};
+
+namespace {
+
+struct Fail {
+  rtdetmcd_status code;
+  std::string msg;
+};
+
+static const int NPMAX = RTD_MAXP + RTD_MAXP * (RTD_MAXP + 1) / 2 + 1;
+static const size_t M2 = (size_t)RTD_MAXP * RTD_MAXP;
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void d2h(cudaStream_t st, void* host, const void* dev, size_t bytes) {
+  if (!bytes) return;
+  RTD_CU(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st));
+  RTD_CU(cudaStreamSynchronize(st));
+}
+void h2d(cudaStream_t st, void* dev, const void* host, size_t bytes) {
+  if (!bytes) return;
+  RTD_CU(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st));
+}
+
+void ensure_ws(rtdetmcd_ctx* c, size_t bytes) {
+  if (bytes <= c->ws_cap) return;
+  if (c->ws_user) throw Fail{RTD_E_OOM, "workspace too small: need " + std::to_string(bytes) + " bytes"};
+  if (c->ws) cudaFree(c->ws);
+  c->ws = nullptr;
+  c->ws_cap = 0;
+  if (cudaMalloc(&c->ws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    throw Fail{RTD_E_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed"};
+  }
+  c->ws_cap = bytes;
+}
+
+size_t uni_bytes(long long len, int ncols) {
+  Arena a;  // dry run
+  unimcd_batch(a, nullptr, nullptr, len, ncols, UniConst{}, nullptr);
+  return a.off + 4096;
+}
+
+size_t sort_bytes(long long len) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, b, (const double*)nullptr, (double*)nullptr, (int)len);
+  return b;
+}
+
+UniConst uni_const(long long len) {
+  UniConst u;
+  const long long h = len / 2 + 1;
+  u.c_raw = consistency_factor((double)h / (double)len, 1);
+  u.q1 = chi2_quantile(0.975, 1);
+  u.c_rew = consistency_factor(0.975, 1);
+  return u;
+}
+
+void run_unimcd(cudaStream_t st, char* scratch, size_t scratch_bytes, const double* cols, long long len, int ncols,
+                UniOut* out) {
+  Arena a;
+  a.base = scratch;
+  a.cap = scratch_bytes;
+  unimcd_batch(a, st, cols, len, ncols, uni_const(len), out);
+}
+
+// ------------------------------------------------------------------ C-step engine
+struct CStepBufs {
+  int ninst_max;
+  long long m;
+  int p;
+  double *mu, *sigma, *shift, *sums, *logdet, *cond, *traj, *cstage, *partial, *d2;
+  int* status;
+  int* changed;
+  int* inst_dev;
+  uint8_t *memA, *memB;
+  SelState* sel;
+  unsigned int* hist;
+  int traj_stride;
+  int ctas;
+};
+
+void carve_cstep(Arena& A, CStepBufs& b, int ninst, long long m, int p, int max_steps) {
+  b.ninst_max = ninst;
+  b.m = m;
+  b.p = p;
+  b.mu = A.take<double>(ninst * RTD_MAXP);
+  b.sigma = A.take<double>(ninst * M2);
+  b.shift = A.take<double>(ninst * RTD_MAXP);
+  b.sums = A.take<double>((size_t)ninst * NPMAX);
+  b.logdet = A.take<double>(ninst);
+  b.cond = A.take<double>(ninst);
+  b.traj_stride = max_steps + 2;
+  b.traj = A.take<double>((size_t)ninst * b.traj_stride);
+  b.cstage = A.take<double>(RTD_CONST_DOUBLES + (size_t)ninst * (RTD_MAXP + RTD_MAXP * (RTD_MAXP + 1) / 2));
+  b.ctas = (int)std::max<long long>(1, std::min<long long>(256, (m + 4095) / 4096));
+  b.partial = A.take<double>((size_t)ninst * b.ctas * NPMAX);
+  b.d2 = A.take<double>((size_t)ninst * m);
+  b.status = A.take<int>(ninst);
+  b.changed = A.take<int>(ninst);
+  b.inst_dev = A.take<int>(ninst + 8);
+  b.memA = A.take<uint8_t>((size_t)ninst * m);
+  b.memB = A.take<uint8_t>((size_t)ninst * m);
+  b.sel = A.take<SelState>(ninst);
+  b.hist = A.take<unsigned int>((size_t)ninst * 4096);
+}
+
+MomArgs mom_args(const CStepBufs& b, const double* Z, long long blk_stride, int nstart) {
+  MomArgs a;
+  memset(&a, 0, sizeof(a));
+  a.Z = Z;
+  a.m = b.m;
+  a.blk_stride = blk_stride;
+  a.p = b.p;
+  a.inst = b.inst_dev;
+  a.nstart = nstart;
+  a.shift = b.shift;
+  a.mem_new = b.memA;
+  a.mem_old = b.memB;
+  a.d2 = b.d2;
+  a.partial = b.partial;
+  a.ctas = b.ctas;
+  return a;
+}
+
+// upload distance operators of instances act[g0, g0+cnt) (staged in cstage slots) and run the distance pass
+void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long blk_stride, int nstart, int nact,
+                 int cstride) {
+  const int cap = std::max(1, RTD_CONST_DOUBLES / std::max(1, cstride));
+  for (int g0 = 0; g0 < nact; g0 += cap) {
+    const int cnt = std::min(cap, nact - g0);
+    upload_const(b.cstage + (size_t)g0 * cstride, (size_t)cnt * cstride, st);
+    launch_dist(b.p, Z, b.m, blk_stride, b.inst_dev + g0, nstart, cnt, cstride, b.d2, st);
+  }
+}
+
+// Runs lock-step C-steps for the instances whose status is ST_ACTIVE on entry.
+// On exit: status ST_CONVERGED / ST_MAXSTEPS (usable) or a failure code;
+// mu/sigma = exact mean / covariance of the final h-subset (in memA), logdet.
+void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_stride, int nstart, int ninst, long long h,
+                double kappa_max, int max_steps, int refresh, std::vector<int>& status_h, std::vector<int>& steps_h) {
+  const int p = b.p;
+  const long long m = b.m;
+  const int cstride = p + p * (p + 1) / 2;
+  const int np = mom_np(p);
+  RTD_CU(cudaMemsetAsync(b.memA, 0, (size_t)ninst * m, st));
+  RTD_CU(cudaMemsetAsync(b.memB, 0, (size_t)ninst * m, st));
+  RTD_CU(cudaMemsetAsync(b.hist, 0, (size_t)ninst * 4096 * sizeof(unsigned int), st));
+  h2d(st, b.status, status_h.data(), ninst * sizeof(int));
+  steps_h.assign(ninst, 0);
+  std::vector<int> act, changed(ninst);
+  MomArgs ma = mom_args(b, Z, blk_stride, nstart);
+  uint8_t* memA = b.memA;  // latest membership
+  uint8_t* memB = b.memB;
+  for (int step = 1; step <= max_steps; step++) {
+    act.clear();
+    for (int i = 0; i < ninst; i++)
+      if (status_h[i] == ST_ACTIVE) act.push_back(i);
+    if (act.empty()) break;
+    const int na = (int)act.size();
+    h2d(st, b.inst_dev, act.data(), na * sizeof(int));
+    launch_prepare(b.inst_dev, na, b.mu, b.sigma, p, kappa_max, b.cstage, cstride, b.logdet, b.cond, b.status, b.traj,
+                   b.traj_stride, step, st);
+    dist_groups(st, b, Z, blk_stride, nstart, na, cstride);
+    RTD_CU(cudaMemsetAsync(b.changed, 0, ninst * sizeof(int), st));
+    launch_select(b.d2, m, h, b.inst_dev, na, b.sel, b.hist, memB, memA, b.changed, st);
+    std::swap(memA, memB);  // memA = membership of this step, memB = previous
+    d2h(st, status_h.data(), b.status, ninst * sizeof(int));
+    d2h(st, changed.data(), b.changed, ninst * sizeof(int));
+    std::vector<int> upd, dense;
+    for (int i : act) {
+      steps_h[i] = step;
+      if (status_h[i] != ST_ACTIVE) continue;  // dropped by the condition monitor
+      if (step > 1 && changed[i] == 0) {
+        status_h[i] = ST_CONVERGED;
+        continue;
+      }
+      if (step == 1 || (refresh > 0 && (step - 1) % refresh == 0)) dense.push_back(i); else upd.push_back(i);
+    }
+    // moments for the new subsets: dense recompute about shift = mu_old, or the delta update
+    ma.mem_new = memA;
+    ma.mem_old = memB;
+    if (!dense.empty()) {
+      h2d(st, b.inst_dev, dense.data(), dense.size() * sizeof(int));
+      launch_copy_vec(b.inst_dev, (int)dense.size(), b.mu, b.shift, p, st);
+      launch_moments(MOM_MEMBER, ma, (int)dense.size(), st);
+      launch_mom_reduce(b.partial, (int)dense.size(), b.inst_dev, b.ctas, np, b.sums, 0, st);
+      launch_sums_to_cov(b.inst_dev, (int)dense.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
+    }
+    if (!upd.empty()) {
+      h2d(st, b.inst_dev, upd.data(), upd.size() * sizeof(int));
+      launch_moments(MOM_DELTA, ma, (int)upd.size(), st);
+      launch_mom_reduce(b.partial, (int)upd.size(), b.inst_dev, b.ctas, np, b.sums, 1, st);
+      launch_sums_to_cov(b.inst_dev, (int)upd.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
+    }
+    // keep the device status words in sync with the host decisions
+    h2d(st, b.status, status_h.data(), ninst * sizeof(int));
+  }
+  for (int i = 0; i < ninst; i++)
+    if (status_h[i] == ST_ACTIVE) status_h[i] = ST_MAXSTEPS;
+  // both buffers hold H for converged instances; make memA the final subset for every instance
+  if (memA != b.memA) RTD_CU(cudaMemcpyAsync(b.memA, memA, (size_t)ninst * m, cudaMemcpyDeviceToDevice, st));
+  // exact recompute of mean / covariance over the final subsets (reading R12)
+  std::vector<int> fin;
+  for (int i = 0; i < ninst; i++)
+    if (status_h[i] == ST_CONVERGED || status_h[i] == ST_MAXSTEPS) fin.push_back(i);
+  if (!fin.empty()) {
+    h2d(st, b.inst_dev, fin.data(), fin.size() * sizeof(int));
+    ma.mem_new = b.memA;
+    launch_copy_vec(b.inst_dev, (int)fin.size(), b.mu, b.shift, p, st);
+    launch_moments(MOM_MEMBER, ma, (int)fin.size(), st);
+    launch_mom_reduce(b.partial, (int)fin.size(), b.inst_dev, b.ctas, np, b.sums, 0, st);
+    launch_sums_to_cov(b.inst_dev, (int)fin.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
+    launch_prepare(b.inst_dev, (int)fin.size(), b.mu, b.sigma, p, kappa_max, nullptr, 0, b.logdet, b.cond, nullptr,
+                   nullptr, 0, 0, st);
+  }
+  RTD_CU(cudaStreamSynchronize(st));
+}
+
+// ------------------------------------------------------------------ refinement of one start
+struct RefineBufs {
+  double *T, *V, *lam, *d, *mut, *Sig, *Smh, *Sh, *mu0;
+  int* ok;
+  UniOut* uni;
+  char* uscratch;
+  size_t uscratch_bytes;
+};
+
+void carve_refine(Arena& A, RefineBufs& r, long long m, int p) {
+  r.T = A.take<double>((size_t)p * m);
+  r.V = A.take<double>(M2);
+  r.lam = A.take<double>(RTD_MAXP);
+  r.d = A.take<double>(RTD_MAXP);
+  r.mut = A.take<double>(RTD_MAXP);
+  r.Sig = A.take<double>(M2);
+  r.Smh = A.take<double>(M2);
+  r.Sh = A.take<double>(M2);
+  r.mu0 = A.take<double>(RTD_MAXP);
+  r.ok = A.take<int>(4);
+  r.uni = A.take<UniOut>(RTD_MAXP);
+  r.uscratch_bytes = uni_bytes(m, p);
+  r.uscratch = A.take<char>(r.uscratch_bytes);
+}
+
+// Given V (eigenvectors of the start, already checked), produce (mu0, Sigma0) into mu_out / sig_out.
+// Returns false when a univariate scale is degenerate.
+bool refine_from_V(cudaStream_t st, RefineBufs& r, const double* Zb, long long m, int p, const double* Vdev,
+                   double* mu_out, double* sig_out) {
+  // T = Z V -> D~ = diag(sigma_uni^2(T_j))
+  upload_const(Vdev, (size_t)p * p, st);
+  launch_matmul(p, Zb, m, r.T, st);
+  run_unimcd(st, r.uscratch, r.uscratch_bytes, r.T, m, p, r.uni);
+  std::vector<UniOut> u(p);
+  d2h(st, u.data(), r.uni, p * sizeof(UniOut));
+  for (int j = 0; j < p; j++)
+    if (u[j].status) return false;
+  launch_uni_extract(r.uni, p, 0, r.d, st);
+  launch_vdv(Vdev, r.d, 1, p, 0, sig_out, st);
+  launch_vdv(Vdev, r.d, 1, p, 1, r.Smh, st);
+  launch_vdv(Vdev, r.d, 1, p, 2, r.Sh, st);
+  // Z~ = Z Sigma^-1/2 -> mu~ = mu_uni(Z~_j) -> mu0 = Sigma^1/2 mu~
+  upload_const(r.Smh, (size_t)p * p, st);
+  launch_matmul(p, Zb, m, r.T, st);
+  run_unimcd(st, r.uscratch, r.uscratch_bytes, r.T, m, p, r.uni);
+  d2h(st, u.data(), r.uni, p * sizeof(UniOut));
+  for (int j = 0; j < p; j++)
+    if (u[j].status) return false;
+  launch_uni_extract(r.uni, p, 1, r.mut, st);
+  launch_matvec(r.Sh, r.mut, 1, p, mu_out, st);
+  return true;
+}
+
+// ------------------------------------------------------------------ initial estimators of q blocks
+struct InitBufs {
+  double *S1, *S2, *r, *rs, *AB, *sums, *partial, *mudummy;
+  int* abok;
+  int* inst_dev;
+  char* sort_tmp;
+  size_t sort_bytes;
+  int ctas;
+};
+
+void carve_init(Arena& A, InitBufs& b, int q, long long m, int p) {
+  b.S1 = A.take<double>((size_t)q * M2);
+  b.S2 = A.take<double>((size_t)q * M2);
+  b.r = A.take<double>((size_t)q * m);
+  b.rs = A.take<double>((size_t)q * m);
+  b.AB = A.take<double>(2 * (size_t)q);
+  b.abok = A.take<int>(q);
+  b.ctas = (int)std::max<long long>(1, std::min<long long>(128, (m + 4095) / 4096));
+  b.sums = A.take<double>((size_t)q * NPMAX);
+  b.partial = A.take<double>((size_t)q * b.ctas * NPMAX);
+  b.mudummy = A.take<double>((size_t)q * RTD_MAXP);
+  b.inst_dev = A.take<int>(q + 8);
+  b.sort_bytes = sort_bytes(m);
+  b.sort_tmp = A.take<char>(b.sort_bytes);
+}
+
+void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int p, int q, long long blk_stride) {
+  std::vector<int> ids(q);
+  for (int i = 0; i < q; i++) ids[i] = i;
+  h2d(st, b.inst_dev, ids.data(), q * sizeof(int));
+  const int np = mom_np(p);
+  MomArgs a;
+  memset(&a, 0, sizeof(a));
+  a.Z = Z;
+  a.m = m;
+  a.blk_stride = blk_stride;
+  a.p = p;
+  a.inst = b.inst_dev;
+  a.nstart = 1;
+  a.partial = b.partial;
+  a.ctas = b.ctas;
+  // S~1: covariance of the wrapped data (centred at the wrapped mean, n - 1)
+  launch_moments(MOM_WRAP, a, q, st);
+  launch_mom_reduce(b.partial, q, b.inst_dev, b.ctas, np, b.sums, 0, st);
+  launch_sums_to_cov(b.inst_dev, q, b.sums, np, nullptr, p, (double)m, 1.0, b.mudummy, b.S1, st);
+  // S~2: norms, type-7 cutoffs, xi^2-weighted second moment / n
+  launch_norms(Z, m, p, q, blk_stride, b.r, st);
+  for (int l = 0; l < q; l++) {
+    size_t bytes = b.sort_bytes;
+    RTD_CU(cub::DeviceRadixSort::SortKeys(b.sort_tmp, bytes, b.r + (size_t)l * m, b.rs + (size_t)l * m, (int)m, 0, 64,
+                                          st));
+  }
+  launch_lr_cutoffs(b.rs, q, m, b.AB, b.abok, st);
+  a.r = b.r;
+  a.AB = b.AB;
+  launch_moments(MOM_XI, a, q, st);
+  launch_mom_reduce(b.partial, q, b.inst_dev, b.ctas, np, b.sums, 0, st);
+  launch_sums_to_second(b.sums, q, np, p, (double)m, b.S2, st);
+}
+
+// ------------------------------------------------------------------ the fit
+struct Dims {
+  long long n, m, h, hb;
+  int p, q, perm, log;
+  bool x_host;
+};
+
+struct FitBufs {
+  double *Xd, *Xc, *Z;
+  unsigned long long* bad;
+  UniOut* uni;
+  char* uscratch;
+  size_t uscratch_bytes;
+  long long* rowmap;
+  InitBufs ib;
+  RefineBufs rb;
+  CStepBufs cb;
+  double *V2, *lam2;  // eigen-pairs: [2q]
+  int* jok;
+  double *sigraw_blk, *mu_raw, *sig_raw, *keys, *agg_scratch, *mu_rew, *sig_rew, *sums_rw, *pooled, *muX, *sigX;
+  int *kept, *ids_dev, *st1;
+  double* mu_blk;
+  uint8_t *flags_d, *weights_d, *hsub_d;
+  double* rd2_d;
+  int* chosen_dev;
+};
+
+void carve_fit(Arena& A, FitBufs& f, const Dims& d, const rtdetmcd_opts& o, bool need_flags, bool need_rd2,
+               bool need_w, bool need_h) {
+  const long long n = d.n, m = d.m;
+  const int p = d.p, q = d.q;
+  f.Xd = d.x_host ? A.take<double>((size_t)n * p) : nullptr;
+  f.Xc = A.take<double>((size_t)n * p);
+  f.bad = A.take<unsigned long long>(1);
+  f.uni = A.take<UniOut>(RTD_MAXP);
+  f.uscratch_bytes = uni_bytes(n, p);
+  f.uscratch = A.take<char>(f.uscratch_bytes);
+  f.Z = A.take<double>((size_t)q * m * p);
+  f.rowmap = d.perm ? A.take<long long>((size_t)q * m) : nullptr;
+  carve_init(A, f.ib, q, m, p);
+  carve_refine(A, f.rb, m, p);
+  carve_cstep(A, f.cb, 2 * q, m, p, o.max_csteps);
+  f.V2 = A.take<double>((size_t)2 * q * M2);
+  f.lam2 = A.take<double>((size_t)2 * q * RTD_MAXP);
+  f.jok = A.take<int>(2 * q);
+  f.sigraw_blk = A.take<double>((size_t)q * M2);
+  f.mu_raw = A.take<double>(RTD_MAXP);
+  f.sig_raw = A.take<double>(M2);
+  f.keys = A.take<double>(q);
+  f.agg_scratch = A.take<double>(2 * M2);
+  f.mu_rew = A.take<double>(RTD_MAXP);
+  f.sig_rew = A.take<double>(M2);
+  f.sums_rw = A.take<double>((size_t)q * NPMAX);
+  f.pooled = A.take<double>(NPMAX);
+  f.muX = A.take<double>(4 * RTD_MAXP);
+  f.sigX = A.take<double>(4 * M2);
+  f.kept = A.take<int>(q);
+  f.ids_dev = A.take<int>(q + 8);
+  f.st1 = A.take<int>(8);
+  f.mu_blk = A.take<double>((size_t)q * RTD_MAXP);
+  f.chosen_dev = A.take<int>(q + 8);
+  f.flags_d = need_flags ? A.take<uint8_t>(n) : nullptr;
+  f.rd2_d = need_rd2 ? A.take<double>(n) : nullptr;
+  f.weights_d = need_w ? A.take<uint8_t>(n) : nullptr;
+  f.hsub_d = need_h ? A.take<uint8_t>(n) : nullptr;
+}
+
+Dims make_dims(long long n, int p, const rtdetmcd_opts& o, bool x_host) {
+  if (p < 1 || p > RTD_MAXP) throw Fail{RTD_E_INVALID_ARG, "p must be in [1, 40]"};
+  if (!(n > 2LL * p)) throw Fail{RTD_E_INVALID_ARG, "need n > 2p"};
+  if (n > (1LL << 31) - 1) throw Fail{RTD_E_INVALID_ARG, "n too large for this build"};
+  Dims d;
+  d.n = n;
+  d.p = p;
+  d.h = o.h > 0 ? o.h : (long long)std::floor(o.alpha * (double)n);
+  if (!(d.h > p && d.h <= n)) throw Fail{RTD_E_INVALID_ARG, "need p < h <= n"};
+  d.q = o.shards > 0 ? o.shards : rtdetmcd_choose_q(n, p, o.omega, o.shard_cap);
+  if (d.q < 1 || d.q > 1024) throw Fail{RTD_E_INVALID_ARG, "q must be in [1, 1024]"};
+  d.m = n / d.q;
+  d.hb = (d.h * d.m) / n;
+  if (!(d.hb > p)) throw Fail{RTD_E_INVALID_ARG, "block coverage floor(h m / n) must exceed p"};
+  d.perm = (d.q > 1 && o.partition == RTD_PART_PERMUTE) ? 1 : 0;
+  d.log = o.log_transform ? 1 : 0;
+  d.x_host = x_host;
+  if (o.max_csteps < 1 || o.max_csteps > 10000) throw Fail{RTD_E_INVALID_ARG, "max_csteps out of range"};
+  if (!(o.quantile > 0.0 && o.quantile < 1.0)) throw Fail{RTD_E_INVALID_ARG, "quantile must be in (0,1)"};
+  return d;
+}
+
+void output_copy(cudaStream_t st, void* user, const void* dev, size_t bytes) {
+  if (!user) return;
+  if (is_device_ptr(user)) RTD_CU(cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDeviceToDevice, st));
+  else RTD_CU(cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDeviceToHost, st));
+}
+
+void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetmcd_opts& o, rtdetmcd_result* out) {
+  cudaStream_t st = c->stream;
+  const bool x_host = !is_device_ptr(X);
+  Dims d = make_dims(n, p, o, x_host);
+  const long long m = d.m;
+  const int q = d.q;
+  const bool want_flags = out && (out->flags || out->rd2);
+  Arena dry;
+  FitBufs f;
+  carve_fit(dry, f, d, o, true, true, true, true);
+  ensure_ws(c, dry.off + 4096);
+  Arena A;
+  A.base = c->ws;
+  A.cap = c->ws_cap;
+  carve_fit(A, f, d, o, true, true, true, true);
+  const long long blk_stride = (long long)p * m;
+  int warnings = 0;
+  if (d.h < (n + p + 1) / 2) warnings |= RTD_W_H_BELOW_BOUND;
+
+  // H0: input to device, validate (and ln) while transposing to columns
+  const double* Xdev = X;
+  if (x_host) {
+    h2d(st, f.Xd, X, (size_t)n * p * sizeof(double));
+    Xdev = f.Xd;
+  }
+  RTD_CU(cudaMemsetAsync(f.bad, 0xff, sizeof(unsigned long long), st));
+  launch_transpose(Xdev, n, p, d.log, f.Xc, f.bad, st);
+  unsigned long long bad = 0;
+  d2h(st, &bad, f.bad, sizeof(bad));
+  if (bad != ~0ull) throw Fail{RTD_E_NONFINITE, "row " + std::to_string(bad) + (d.log ? " is not finite and > 0" : " is not finite")};
+
+  // H1: global column standardisation
+  run_unimcd(st, f.uscratch, f.uscratch_bytes, f.Xc, n, p, f.uni);
+  std::vector<UniOut> uni(p);
+  d2h(st, uni.data(), f.uni, p * sizeof(UniOut));
+  for (int j = 0; j < p; j++)
+    if (uni[j].status) throw Fail{RTD_E_DEGENERATE_COLUMN, "column " + std::to_string(j)};
+
+  // partition + Z = (X - loc)/scale per block, column-major
+  launch_build_Z(f.Xc, Xdev, n, p, q, m, d.perm, o.seed, d.log, f.uni, f.Z, f.rowmap, st);
+
+  // H2, H3: S~1, S~2 per block
+  run_initial(st, f.ib, f.Z, m, p, q, blk_stride);
+  std::vector<int> abok(q);
+  // H4 step 1-2: eigen-decomposition + condition check of both starts
+  launch_jacobi(f.ib.S1, q, p, o.kappa_max, f.V2, f.lam2, f.jok, st);
+  launch_jacobi(f.ib.S2, q, p, o.kappa_max, f.V2 + (size_t)q * M2, f.lam2 + (size_t)q * RTD_MAXP, f.jok + q, st);
+  std::vector<int> jok(2 * q);
+  d2h(st, jok.data(), f.jok, 2 * q * sizeof(int));
+  d2h(st, abok.data(), f.ib.abok, q * sizeof(int));
+
+  // H4 steps 3-4: refinement per (block, start); instance id = 2 b + k
+  const int ninst = 2 * q;
+  std::vector<int> status(ninst, ST_ACTIVE), steps(ninst, 0);
+  for (int b = 0; b < q; b++) {
+    for (int k = 0; k < 2; k++) {
+      const int id = 2 * b + k;
+      const bool eig_ok = jok[k * q + b] != 0 && (k == 0 || abok[b] != 0);
+      if (!eig_ok) {
+        status[id] = ST_REFINE;
+        continue;
+      }
+      const double* V = f.V2 + ((size_t)k * q + b) * M2;
+      bool ok = refine_from_V(st, f.rb, f.Z + (size_t)b * blk_stride, m, p, V, f.cb.mu + (size_t)id * RTD_MAXP,
+                              f.cb.sigma + (size_t)id * M2);
+      if (!ok) status[id] = ST_REFINE;
+    }
+  }
+
+  // H5-H9: C-steps for all (block, start) instances in lock step
+  run_csteps(st, f.cb, f.Z, blk_stride, 2, ninst, d.hb, o.kappa_max, o.max_csteps, o.refresh_every, status, steps);
+  std::vector<double> logdet(ninst);
+  d2h(st, logdet.data(), f.cb.logdet, ninst * sizeof(double));
+  const double calpha = consistency_factor((double)d.hb / (double)m, p);
+  std::vector<int> chosen(q, -1), valid_ids;
+  for (int b = 0; b < q; b++) {
+    bool u0 = status[2 * b] == ST_CONVERGED || status[2 * b] == ST_MAXSTEPS;
+    bool u1 = status[2 * b + 1] == ST_CONVERGED || status[2 * b + 1] == ST_MAXSTEPS;
+    if (!u0 || !u1) warnings |= RTD_W_START_FAILED;
+    int ch = -1;
+    if (u0) ch = 0;
+    if (u1 && (!u0 || logdet[2 * b + 1] < logdet[2 * b])) ch = 1;
+    chosen[b] = ch;
+    if (ch >= 0) {
+      valid_ids.push_back(b);
+      if (status[2 * b + ch] == ST_MAXSTEPS) warnings |= RTD_W_MAX_CSTEPS;
+    } else {
+      warnings |= RTD_W_BLOCK_FAILED;
+    }
+  }
+  // per-block raw fits: c(alpha_l) * Sigma
+  std::vector<int> chosen_inst(q, -1);
+  for (int b = 0; b < q; b++) chosen_inst[b] = chosen[b] >= 0 ? 2 * b + chosen[b] : -1;
+  h2d(st, f.chosen_dev, chosen_inst.data(), q * sizeof(int));
+  for (int b : valid_ids)
+    launch_scale_copy(f.cb.sigma + (size_t)chosen_inst[b] * M2, f.sigraw_blk + (size_t)b * M2, p, calpha, st);
+  if (q == 1) {
+    if (valid_ids.empty()) throw Fail{RTD_E_BOTH_STARTS_FAILED, "both starts were dropped"};
+  } else {
+    if ((int)valid_ids.size() < q - q / 2)
+      throw Fail{RTD_E_TOO_FEW_VALID_BLOCKS,
+                 std::to_string(valid_ids.size()) + " of " + std::to_string(q) + " blocks valid"};
+  }
+  int n_kept = 1;
+  if (q == 1) {
+    RTD_CU(cudaMemcpyAsync(f.mu_raw, f.cb.mu + (size_t)chosen_inst[0] * RTD_MAXP, RTD_MAXP * sizeof(double),
+                           cudaMemcpyDeviceToDevice, st));
+    RTD_CU(cudaMemcpyAsync(f.sig_raw, f.sigraw_blk, M2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else {
+    // chosen centres of the valid blocks -> mu_blk[b]; median / KL / pooling on the device (K11)
+    for (int b : valid_ids)
+      RTD_CU(cudaMemcpyAsync(f.mu_blk + (size_t)b * RTD_MAXP, f.cb.mu + (size_t)chosen_inst[b] * RTD_MAXP,
+                             RTD_MAXP * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    h2d(st, f.ids_dev, valid_ids.data(), valid_ids.size() * sizeof(int));
+    launch_aggregate(f.mu_blk, f.sigraw_blk, f.ids_dev, (int)valid_ids.size(), p, (double)m, f.mu_raw, f.sig_raw,
+                     f.kept, f.keys, f.agg_scratch, st);
+    std::vector<int> kept(valid_ids.size());
+    d2h(st, kept.data(), f.kept, kept.size() * sizeof(int));
+    n_kept = 0;
+    for (int v : kept) n_kept += v;
+  }
+
+  // H11: reweighting over the fitted rows, per block then pooled
+  const double c2 = chi2_quantile(o.quantile, p);
+  const int cstride = p + p * (p + 1) / 2;
+  {
+    // distance operator of the raw fit; also its positive-definiteness check
+    int zero2[2] = {0, 0};
+    h2d(st, f.ids_dev, zero2, sizeof(int));
+    h2d(st, f.st1, zero2, sizeof(int));
+    launch_prepare(f.ids_dev, 1, f.mu_raw, f.sig_raw, p, 1e300, f.cb.cstage, cstride, nullptr, nullptr, f.st1,
+                   nullptr, 0, 0, st);
+    int stv = 0;
+    d2h(st, &stv, f.st1, sizeof(int));
+    if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "raw scatter is not positive definite"};
+  }
+  {
+    std::vector<int> blocks(q);
+    for (int b = 0; b < q; b++) blocks[b] = b;
+    h2d(st, f.cb.inst_dev, blocks.data(), q * sizeof(int));
+    upload_const(f.cb.cstage, cstride, st);
+    launch_dist(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, 0, f.cb.d2, st);
+    // shift = mu_raw for every block
+    for (int b = 0; b < q; b++)
+      RTD_CU(cudaMemcpyAsync(f.cb.shift + (size_t)b * RTD_MAXP, f.mu_raw, RTD_MAXP * sizeof(double),
+                             cudaMemcpyDeviceToDevice, st));
+    MomArgs a = mom_args(f.cb, f.Z, blk_stride, 1);
+    a.c2 = c2;
+    const int np = mom_np(p);
+    launch_moments(MOM_REWEIGHT, a, q, st);
+    launch_mom_reduce(f.cb.partial, q, f.cb.inst_dev, f.cb.ctas, np, f.sums_rw, 0, st);
+    launch_pool_sums(f.sums_rw, q, np, f.pooled, st);
+    std::vector<double> pooled(np);
+    d2h(st, pooled.data(), f.pooled, np * sizeof(double));
+    const double kw = pooled[np - 1];
+    if (!(kw > p)) throw Fail{RTD_E_NOT_PD, "too few reweighted inliers"};
+    std::vector<int> zero(1, 0);
+    h2d(st, f.ids_dev, zero.data(), sizeof(int));
+    launch_sums_to_cov(f.ids_dev, 1, f.pooled, np, f.mu_raw, p, 0.0, consistency_factor(o.quantile, p), f.mu_rew,
+                       f.sig_rew, st);
+    if (out) out->n_weighted = (int64_t)llround(kw);
+  }
+  // de-standardise raw and reweighted fits (H13)
+  launch_destandardize(f.uni, f.mu_raw, f.sig_raw, p, f.muX, f.sigX, st);
+  launch_destandardize(f.uni, f.mu_rew, f.sig_rew, p, f.muX + RTD_MAXP, f.sigX + M2, st);
+  // H12: flag all n rows under the reweighted fit in X units
+  {
+    int stv = 0;
+    RTD_CU(cudaMemsetAsync(f.st1, 0, sizeof(int), st));
+    launch_prepare(f.ids_dev, 1, f.muX + RTD_MAXP, f.sigX + M2, p, 1e300, f.cb.cstage, cstride, nullptr, nullptr,
+                   f.st1, nullptr, 0, 0, st);
+    d2h(st, &stv, f.st1, sizeof(int));
+    if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "reweighted scatter is not positive definite"};
+    upload_const(f.cb.cstage, cstride, st);
+    if (want_flags) launch_flag(p, Xdev, n, d.log, c2, f.flags_d, f.rd2_d, st);
+  }
+  // per-row weights and h-subset membership in original row order
+  if (out && (out->weights || out->hsubset)) {
+    if (d.perm || q * m < n) {
+      RTD_CU(cudaMemsetAsync(f.weights_d, 0, n, st));
+      RTD_CU(cudaMemsetAsync(f.hsub_d, 0, n, st));
+    }
+    launch_weights_from_d2(f.cb.d2, (long long)q * m, c2, f.rowmap, f.weights_d, st);
+    launch_hsub_from_mem(f.cb.memA, f.chosen_dev, q, m, f.rowmap, f.hsub_d, st);
+  }
+  RTD_CU(cudaStreamSynchronize(st));
+
+  // outputs
+  if (out) {
+    std::vector<double> mx(4 * RTD_MAXP), sx(4 * M2);
+    d2h(st, mx.data(), f.muX, 2 * RTD_MAXP * sizeof(double));
+    d2h(st, sx.data(), f.sigX, 2 * M2 * sizeof(double));
+    for (int j = 0; j < p; j++) {
+      if (out->loc) out->loc[j] = uni[j].loc;
+      if (out->scale) out->scale[j] = uni[j].scale;
+      if (out->mu_raw) out->mu_raw[j] = mx[j];
+      if (out->mu_rew) out->mu_rew[j] = mx[RTD_MAXP + j];
+    }
+    for (int e = 0; e < p * p; e++) {
+      if (out->sigma_raw) out->sigma_raw[e] = sx[e];
+      if (out->sigma_rew) out->sigma_rew[e] = sx[M2 + e];
+    }
+    out->logdet_raw = (q == 1 && chosen[0] >= 0) ? logdet[chosen_inst[0]] : NAN;
+    out->cutoff2 = c2;
+    out->h = d.h;
+    out->h_block = d.hb;
+    out->m = m;
+    out->q_used = q;
+    out->warnings = warnings;
+    out->n_valid_blocks = (int)valid_ids.size();
+    out->n_kept_blocks = n_kept;
+    if (out->block_chosen)
+      for (int b = 0; b < q; b++) out->block_chosen[b] = chosen[b];
+    if (out->start_steps)
+      for (int i = 0; i < ninst; i++) out->start_steps[i] = steps[i];
+    if (out->start_status)
+      for (int i = 0; i < ninst; i++) out->start_status[i] = status[i];
+    if (out->start_logdet)
+      for (int i = 0; i < ninst; i++) out->start_logdet[i] = logdet[i];
+    output_copy(st, out->flags, f.flags_d, n);
+    output_copy(st, out->rd2, f.rd2_d, n * sizeof(double));
+    output_copy(st, out->weights, f.weights_d, n);
+    output_copy(st, out->hsubset, f.hsub_d, n);
+    RTD_CU(cudaStreamSynchronize(st));
+  }
+}
+
+template <class F>
+rtdetmcd_status guarded(rtdetmcd_ctx* c, F&& fn) {
+  if (!c) return RTD_E_INVALID_ARG;
+  c->err.clear();
+  try {
+    RTD_CU(cudaSetDevice(c->device));
+    fn();
+    return RTD_OK;
+  } catch (const Fail& f) {
+    c->err = f.msg;
+    return f.code;
+  } catch (const CudaError& e) {
+    c->err = std::string("CUDA error ") + cudaGetErrorString(e.code) + " in " + e.where;
+    return RTD_E_CUDA;
+  } catch (const std::string& s) {
+    c->err = s;
+    return RTD_E_INTERNAL;
+  } catch (...) {
+    c->err = "unknown internal error";
+    return RTD_E_INTERNAL;
+  }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+void rtdetmcd_opts_default(rtdetmcd_opts* o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->h = 0;
+  o->alpha = 0.5;
+  o->shards = 1;
+  o->shard_cap = 64;
+  o->omega = 4096;
+  o->kappa_max = 1000.0;
+  o->quantile = 0.975;
+  o->max_csteps = 100;
+  o->refresh_every = 32;
+  o->seed = 0;
+  o->partition = RTD_PART_PERMUTE;
+  o->log_transform = 0;
+}
+
+rtdetmcd_status rtdetmcd_create(rtdetmcd_ctx** ctx, int device, void* cuda_stream) {
+  if (!ctx) return RTD_E_INVALID_ARG;
+  *ctx = nullptr;
+  rtdetmcd_ctx* c = new (std::nothrow) rtdetmcd_ctx();
+  if (!c) return RTD_E_OOM;
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return RTD_E_CUDA;
+  }
+  if (cuda_stream) {
+    c->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaGetLastError();
+      delete c;
+      return RTD_E_CUDA;
+    }
+    c->own_stream = true;
+  }
+  *ctx = c;
+  return RTD_OK;
+}
+
+void rtdetmcd_destroy(rtdetmcd_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->ws && !c->ws_user) cudaFree(c->ws);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* rtdetmcd_last_error(const rtdetmcd_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+rtdetmcd_status rtdetmcd_set_workspace(rtdetmcd_ctx* c, void* dev_ptr, size_t bytes) {
+  return guarded(c, [&] {
+    if (c->ws && !c->ws_user) cudaFree(c->ws);
+    c->ws = (char*)dev_ptr;
+    c->ws_cap = dev_ptr ? bytes : 0;
+    c->ws_user = dev_ptr != nullptr;
+  });
+}
+
+size_t rtdetmcd_fit_workspace_size(int64_t n, int32_t p, const rtdetmcd_opts* opts) {
+  try {
+    rtdetmcd_opts o;
+    if (opts) o = *opts; else rtdetmcd_opts_default(&o);
+    Dims d = make_dims(n, p, o, true);
+    Arena dry;
+    FitBufs f;
+    carve_fit(dry, f, d, o, true, true, true, true);
+    return dry.off + 4096;
+  } catch (...) {
+    return 0;
+  }
+}
+
+rtdetmcd_status rtdetmcd_fit(rtdetmcd_ctx* c, const double* X, int64_t n, int32_t p, const rtdetmcd_opts* opts,
+                             rtdetmcd_result* out) {
+  return guarded(c, [&] {
+    if (!X) throw Fail{RTD_E_INVALID_ARG, "X is NULL"};
+    rtdetmcd_opts o;
+    if (opts) o = *opts; else rtdetmcd_opts_default(&o);
+    fit_impl(c, X, n, p, o, out);
+  });
+}
+
+rtdetmcd_status rtdetmcd_flag(rtdetmcd_ctx* c, const double* X, int64_t n, int32_t p, const double* mu,
+                              const double* sigma, double quantile, int32_t log_transform, uint8_t* flags,
+                              double* rd2) {
+  return guarded(c, [&] {
+    if (!X || !mu || !sigma) throw Fail{RTD_E_INVALID_ARG, "NULL input"};
+    if (p < 1 || p > RTD_MAXP || n < 1) throw Fail{RTD_E_INVALID_ARG, "bad n or p"};
+    if (!(quantile > 0.0 && quantile < 1.0)) throw Fail{RTD_E_INVALID_ARG, "quantile must be in (0,1)"};
+    cudaStream_t st = c->stream;
+    const bool xh = !is_device_ptr(X);
+    const bool fh = flags && !is_device_ptr(flags);
+    const bool rh = rd2 && !is_device_ptr(rd2);
+    Arena dry;
+    auto carve = [&](Arena& A, double*& xd, double*& musig, double*& cs, int*& inst, int*& stt, uint8_t*& fd,
+                     double*& rdd) {
+      xd = xh ? A.take<double>((size_t)n * p) : nullptr;
+      musig = A.take<double>(RTD_MAXP + M2);
+      cs = A.take<double>(RTD_CONST_DOUBLES);
+      inst = A.take<int>(8);
+      stt = A.take<int>(8);
+      fd = fh ? A.take<uint8_t>(n) : nullptr;
+      rdd = rh ? A.take<double>(n) : nullptr;
+    };
+    double *xd, *musig, *cs, *rdd;
+    int *inst, *stt;
+    uint8_t* fd;
+    carve(dry, xd, musig, cs, inst, stt, fd, rdd);
+    ensure_ws(c, dry.off + 4096);
+    Arena A;
+    A.base = c->ws;
+    A.cap = c->ws_cap;
+    carve(A, xd, musig, cs, inst, stt, fd, rdd);
+    const double* Xd = X;
+    if (xh) {
+      h2d(st, xd, X, (size_t)n * p * sizeof(double));
+      Xd = xd;
+    }
+    std::vector<double> ms(RTD_MAXP + M2, 0.0);
+    for (int j = 0; j < p; j++) ms[j] = mu[j];
+    for (int e = 0; e < p * p; e++) ms[RTD_MAXP + e] = sigma[e];
+    h2d(st, musig, ms.data(), ms.size() * sizeof(double));
+    int zero[2] = {0, 0};
+    h2d(st, inst, zero, sizeof(int));
+    h2d(st, stt, zero, sizeof(int));
+    const int cstride = p + p * (p + 1) / 2;
+    launch_prepare(inst, 1, musig, musig + RTD_MAXP, p, 1e300, cs, cstride, nullptr, nullptr, stt, nullptr, 0, 0, st);
+    int stv = 0;
+    d2h(st, &stv, stt, sizeof(int));
+    if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "sigma is not positive definite"};
+    upload_const(cs, cstride, st);
+    launch_flag(p, Xd, n, log_transform ? 1 : 0, chi2_quantile(quantile, p), fh ? fd : flags, rh ? rdd : rd2, st);
+    if (fh) RTD_CU(cudaMemcpyAsync(flags, fd, n, cudaMemcpyDeviceToHost, st));
+    if (rh) RTD_CU(cudaMemcpyAsync(rd2, rdd, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RTD_CU(cudaStreamSynchronize(st));
+  });
+}
+
+rtdetmcd_status rtdetmcd_unimcd(rtdetmcd_ctx* c, const double* cols, int64_t len, int32_t ncols, double* loc,
+                                double* scale, double* raw_loc, double* raw_var, int64_t* start) {
+  return guarded(c, [&] {
+    if (!cols || len < 2 || ncols < 1) throw Fail{RTD_E_INVALID_ARG, "bad arguments"};
+    cudaStream_t st = c->stream;
+    size_t ub = uni_bytes(len, ncols);
+    Arena dry;
+    dry.take<UniOut>(ncols);
+    dry.take<char>(ub);
+    ensure_ws(c, dry.off + 4096);
+    Arena A;
+    A.base = c->ws;
+    A.cap = c->ws_cap;
+    UniOut* u = A.take<UniOut>(ncols);
+    char* scr = A.take<char>(ub);
+    run_unimcd(st, scr, ub, cols, len, ncols, u);
+    std::vector<UniOut> h(ncols);
+    d2h(st, h.data(), u, ncols * sizeof(UniOut));
+    for (int j = 0; j < ncols; j++) {
+      if (loc) loc[j] = h[j].loc;
+      if (scale) scale[j] = h[j].scale;
+      if (raw_loc) raw_loc[j] = h[j].raw_loc;
+      if (raw_var) raw_var[j] = h[j].raw_var;
+      if (start) start[j] = h[j].start;
+    }
+    for (int j = 0; j < ncols; j++)
+      if (h[j].status) throw Fail{RTD_E_DEGENERATE_COLUMN, "column " + std::to_string(j)};
+  });
+}
+
+rtdetmcd_status rtdetmcd_initial(rtdetmcd_ctx* c, const double* Z, int64_t m, int32_t p, double* S1, double* S2,
+                                 int32_t* s2_ok) {
+  return guarded(c, [&] {
+    if (!Z || p < 1 || p > RTD_MAXP || m < 4) throw Fail{RTD_E_INVALID_ARG, "bad arguments"};
+    cudaStream_t st = c->stream;
+    Arena dry;
+    InitBufs ib;
+    carve_init(dry, ib, 1, m, p);
+    ensure_ws(c, dry.off + 4096);
+    Arena A;
+    A.base = c->ws;
+    A.cap = c->ws_cap;
+    carve_init(A, ib, 1, m, p);
+    run_initial(st, ib, Z, m, p, 1, (long long)p * m);
+    std::vector<double> s1(M2), s2(M2);
+    int ok = 0;
+    d2h(st, s1.data(), ib.S1, M2 * sizeof(double));
+    d2h(st, s2.data(), ib.S2, M2 * sizeof(double));
+    d2h(st, &ok, ib.abok, sizeof(int));
+    for (int e = 0; e < p * p; e++) {
+      if (S1) S1[e] = s1[e];
+      if (S2) S2[e] = s2[e];
+    }
+    if (s2_ok) *s2_ok = ok;
+  });
+}
+
+rtdetmcd_status rtdetmcd_refine(rtdetmcd_ctx* c, const double* Z, int64_t m, int32_t p, const double* S,
+                                double kappa_max, double* mu, double* sigma, double* lam, int32_t* ok) {
+  return guarded(c, [&] {
+    if (!Z || !S || p < 1 || p > RTD_MAXP || m < 4) throw Fail{RTD_E_INVALID_ARG, "bad arguments"};
+    cudaStream_t st = c->stream;
+    auto carve = [&](Arena& A, RefineBufs& rb, double*& Sd, double*& V, double*& L, int*& jok, double*& muo,
+                     double*& sgo) {
+      carve_refine(A, rb, m, p);
+      Sd = A.take<double>(M2);
+      V = A.take<double>(M2);
+      L = A.take<double>(RTD_MAXP);
+      jok = A.take<int>(4);
+      muo = A.take<double>(RTD_MAXP);
+      sgo = A.take<double>(M2);
+    };
+    RefineBufs rb;
+    double *Sd, *V, *L, *muo, *sgo;
+    int* jok;
+    Arena dry;
+    carve(dry, rb, Sd, V, L, jok, muo, sgo);
+    ensure_ws(c, dry.off + 4096);
+    Arena A;
+    A.base = c->ws;
+    A.cap = c->ws_cap;
+    carve(A, rb, Sd, V, L, jok, muo, sgo);
+    std::vector<double> sh(M2, 0.0);
+    for (int e = 0; e < p * p; e++) sh[e] = S[e];
+    h2d(st, Sd, sh.data(), M2 * sizeof(double));
+    launch_jacobi(Sd, 1, p, kappa_max, V, L, jok, st);
+    int okv = 0;
+    d2h(st, &okv, jok, sizeof(int));
+    std::vector<double> lh(RTD_MAXP);
+    d2h(st, lh.data(), L, RTD_MAXP * sizeof(double));
+    if (lam)
+      for (int j = 0; j < p; j++) lam[j] = lh[j];
+    if (okv) okv = refine_from_V(st, rb, Z, m, p, V, muo, sgo) ? 1 : 0;
+    if (okv) {
+      std::vector<double> mh(RTD_MAXP), sgh(M2);
+      d2h(st, mh.data(), muo, RTD_MAXP * sizeof(double));
+      d2h(st, sgh.data(), sgo, M2 * sizeof(double));
+      for (int j = 0; j < p; j++)
+        if (mu) mu[j] = mh[j];
+      for (int e = 0; e < p * p; e++)
+        if (sigma) sigma[e] = sgh[e];
+    }
+    if (ok) *ok = okv;
+  });
+}
+
+rtdetmcd_status rtdetmcd_csteps(rtdetmcd_ctx* c, const double* Z, int64_t m, int32_t p, int64_t h,
+                                const double* mu0, const double* sigma0, double kappa_max, int32_t max_steps,
+                                int32_t refresh_every, double* mu, double* sigma, double* logdet, int32_t* steps,
+                                int32_t* status, uint8_t* hsubset, double* logdet_traj) {
+  return guarded(c, [&] {
+    if (!Z || !mu0 || !sigma0 || p < 1 || p > RTD_MAXP || !(h > p && h <= m) || max_steps < 1)
+      throw Fail{RTD_E_INVALID_ARG, "bad arguments"};
+    cudaStream_t st = c->stream;
+    CStepBufs cb;
+    Arena dry;
+    carve_cstep(dry, cb, 1, m, p, max_steps);
+    ensure_ws(c, dry.off + 4096);
+    Arena A;
+    A.base = c->ws;
+    A.cap = c->ws_cap;
+    carve_cstep(A, cb, 1, m, p, max_steps);
+    std::vector<double> mh(RTD_MAXP, 0.0), sh(M2, 0.0);
+    for (int j = 0; j < p; j++) mh[j] = mu0[j];
+    for (int e = 0; e < p * p; e++) sh[e] = sigma0[e];
+    h2d(st, cb.mu, mh.data(), RTD_MAXP * sizeof(double));
+    h2d(st, cb.sigma, sh.data(), M2 * sizeof(double));
+    std::vector<int> stv(1, ST_ACTIVE), stp(1, 0);
+    run_csteps(st, cb, Z, (long long)p * m, 1, 1, h, kappa_max, max_steps, refresh_every, stv, stp);
+    d2h(st, mh.data(), cb.mu, RTD_MAXP * sizeof(double));
+    d2h(st, sh.data(), cb.sigma, M2 * sizeof(double));
+    double ld = 0.0;
+    d2h(st, &ld, cb.logdet, sizeof(double));
+    for (int j = 0; j < p; j++)
+      if (mu) mu[j] = mh[j];
+    for (int e = 0; e < p * p; e++)
+      if (sigma) sigma[e] = sh[e];
+    if (logdet) *logdet = ld;
+    if (steps) *steps = stp[0];
+    if (status) *status = stv[0];
+    if (logdet_traj) {
+      std::vector<double> tr(cb.traj_stride);
+      d2h(st, tr.data(), cb.traj, cb.traj_stride * sizeof(double));
+      for (int s = 0; s <= max_steps; s++) logdet_traj[s] = s <= stp[0] ? tr[s] : NAN;
+    }
+    if (hsubset) output_copy(st, hsubset, cb.memA, m);
+    RTD_CU(cudaStreamSynchronize(st));
+  });
+}
+
+double rtdetmcd_chi2_quantile(double prob, int32_t dof) { return chi2_quantile(prob, dof); }
+double rtdetmcd_consistency_factor(double alpha, int32_t p) { return consistency_factor(alpha, p); }
+
+int32_t rtdetmcd_choose_q(int64_t n, int32_t p, int64_t omega, int32_t cap) {
+  if (p < 1 || omega < 1) return 1;
+  long long q = n / ((long long)p * omega);
+  if (q < 1) q = 1;
+  if (cap > 0 && q > cap) q = cap;
+  return (int32_t)q;
+}
+
+rtdetmcd_status rtdetmcd_partition_perm(rtdetmcd_ctx* c, int64_t n, uint64_t seed, int64_t* out) {
+  return guarded(c, [&] {
+    if (n < 1 || !out) throw Fail{RTD_E_INVALID_ARG, "bad arguments"};
+    Arena dry;
+    dry.take<long long>(n);
+    ensure_ws(c, dry.off + 4096);
+    Arena A;
+    A.base = c->ws;
+    A.cap = c->ws_cap;
+    long long* d = A.take<long long>(n);
+    launch_feistel_fwd(n, seed, d, c->stream);
+    d2h(c->stream, out, d, n * sizeof(long long));
+  });
+}
+
+}  // extern "C"

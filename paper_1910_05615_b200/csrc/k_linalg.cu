@@ -1,0 +1,569 @@
+// K4 / K11: single-CTA dense linear algebra for p <= 40, one CTA per instance.
+//   k_prepare   Cholesky Sigma = L L^T, log det = 2 sum log L_jj
+//               (PAPER.md:637-641), exact inverse -> ||Sigma||_1 ||Sigma^-1||_1 >= kappa_max
+//               test, and the distance operator [mu | L^-1] staged
+//               for the constant bank.
+//   k_jacobi    cyclic Jacobi eigen-decomposition with round-robin parallel
+//               pairs, eigenvalues descending and the
+//               kappa_max check of refinement step 2.
+//   k_refine    Sigma_k = V D~ V^T, Sigma_k^{+-1/2}.
+//   k_sums_to_cov  mean / covariance from shifted sums (eqs. cstep4a/b).
+//   k_aggregate entrywise median, KL ranking, ceil(q/2) kept, pooling.
+#include "rtd_internal.h"
+#include "rtd_linalg.h"
+#include <cstdio>
+#include <cstdlib>
+
+namespace rtd {
+
+static constexpr int LT = 256;
+static constexpr int LD = RTD_MAXP + 1;
+
+// The helpers take flat shared arrays (row stride LD) and contain no early
+// return inside loops: nvcc 12.9 for sm_100a emitted a use-before-def register
+// (stores landing one element off) for a 2-D-array-parameter version with an
+// in-loop return (tools/t_min3.cu reproduces it; tools/t_min4.cu is this form).
+
+// Cholesky of the p x p matrix in A into L; returns false if not PD.
+__device__ __noinline__ bool block_cholesky(const double* A, double* L, int p, int* s_fail) {
+  const int t = threadIdx.x;
+  if (t == 0) *s_fail = 0;
+  for (int e = t; e < RTD_MAXP * LD; e += blockDim.x) L[e] = 0.0;
+  __syncthreads();
+  bool ok = true;
+  for (int j = 0; j < p; j++) {
+    if (t == 0) {
+      double s = A[j * LD + j];
+      for (int k = 0; k < j; k++) s -= L[j * LD + k] * L[j * LD + k];
+      if (!(s > 0.0) || !isfinite(s)) *s_fail = 1;
+      L[j * LD + j] = s > 0.0 ? sqrt(s) : 1.0;
+    }
+    __syncthreads();
+    if (*s_fail) {
+      ok = false;
+      break;
+    }
+    for (int i = j + 1 + t; i < p; i += blockDim.x) {
+      double s = A[i * LD + j];
+      for (int k = 0; k < j; k++) s -= L[i * LD + k] * L[j * LD + k];
+      L[i * LD + j] = s / L[j * LD + j];
+    }
+    __syncthreads();
+  }
+  return ok;
+}
+
+// Li = L^-1 (lower triangular), column-parallel forward substitution.
+__device__ __noinline__ void block_tri_inverse(const double* L, double* Li, int p) {
+  const int t = threadIdx.x;
+  for (int e = t; e < RTD_MAXP * LD; e += blockDim.x) Li[e] = 0.0;
+  __syncthreads();
+  if (t < p) {
+    const int c = t;
+    for (int i = c; i < p; i++) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; k++) s -= L[i * LD + k] * Li[k * LD + c];
+      Li[i * LD + c] = s / L[i * LD + i];
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __noinline__ double block_max_colsum_abs(const double* A, int p, double* red) {
+  const int t = threadIdx.x;
+  if (t < p) {
+    double s = 0.0;
+    for (int i = 0; i < p; i++) s += fabs(A[i * LD + t]);
+    red[t] = s;
+  }
+  __syncthreads();
+  double mx = 0.0;
+  for (int j = 0; j < p; j++) mx = fmax(mx, red[j]);
+  __syncthreads();
+  return mx;
+}
+
+// Sigma^-1 = Li^T Li into B
+__device__ __noinline__ void block_inv_from_li(const double* Li, double* B, int p) {
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    int i = e / p, j = e - i * p;
+    int k0 = i > j ? i : j;
+    double s = 0.0;
+    for (int k = k0; k < p; k++) s += Li[k * LD + i] * Li[k * LD + j];
+    B[i * LD + j] = s;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(LT) k_prepare(const int* __restrict__ inst, const double* __restrict__ mu_all,
+                                                const double* __restrict__ sigma_all, int p, double kappa_max,
+                                                double* __restrict__ cstage, int cstride, double* __restrict__ logdet_out,
+                                                double* __restrict__ cond_out, int* __restrict__ status_out,
+                                                double* __restrict__ traj, int traj_stride, int step) {
+  __shared__ double A[RTD_MAXP * LD], L[RTD_MAXP * LD], Li[RTD_MAXP * LD];
+  __shared__ double red[RTD_MAXP];
+  __shared__ int s_fail;
+  const int slot = blockIdx.x;
+  const int id = inst[slot];
+  const int t = threadIdx.x;
+  if (status_out && status_out[id] != 0) return;  // instance no longer active
+  const double* sg = sigma_all + (long long)id * RTD_MAXP * RTD_MAXP;
+  for (int e = t; e < p * p; e += blockDim.x) A[(e / p) * LD + e % p] = sg[e];
+  __syncthreads();
+  const bool ok = block_cholesky(A, L, p, &s_fail);
+  if (!ok) {
+    if (t == 0 && status_out) status_out[id] = ST_NOT_PD;
+    return;
+  }
+  block_tri_inverse(L, Li, p);
+  const double n1 = block_max_colsum_abs(A, p, red);
+  block_inv_from_li(Li, A, p);  // A <- Sigma^-1
+  const double n1i = block_max_colsum_abs(A, p, red);
+  const double kappa = n1 * n1i;
+  if (t == 0) {
+    double ld = 0.0;
+    for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
+    ld *= 2.0;
+    if (logdet_out) logdet_out[id] = ld;
+    if (cond_out) cond_out[id] = kappa;
+    if (traj) traj[(long long)id * traj_stride + step] = ld;
+    if (status_out && !(kappa < kappa_max)) status_out[id] = ST_COND;
+  }
+  if (cstage) {
+    double* cs = cstage + (long long)slot * cstride;
+    const double* mu = mu_all + (long long)id * RTD_MAXP;
+    for (int k = t; k < p; k += blockDim.x) cs[k] = mu[k];
+    for (int e = t; e < p * (p + 1) / 2; e += blockDim.x) {
+      int j = 0;
+      while ((j + 1) * (j + 2) / 2 <= e) j++;
+      int k = e - j * (j + 1) / 2;
+      cs[p + e] = Li[j * LD + k];
+    }
+  }
+}
+
+void launch_prepare(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p, double kappa_max,
+                    double* cstage, int cstride, double* logdet_out, double* cond_out, int* status_out, double* traj,
+                    int traj_stride, int step, cudaStream_t st) {
+  k_prepare<<<ninst, LT, 0, st>>>(inst, mu_all, sigma_all, p, kappa_max, cstage, cstride, logdet_out, cond_out,
+                                  status_out, traj, traj_stride, step);
+  RTD_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ sums -> (mu, Sigma)
+// sums: [S1 (p)] [S2 packed lower (p(p+1)/2)] [count] about shift c.
+// mode 0: mu = c + S1/n, Sigma = (S2 - S1 S1^T / n) / (n - 1) * factor   (n = count or given)
+__global__ void k_sums_to_cov(const int* __restrict__ inst, const double* __restrict__ sums_all, int np,
+                              const double* __restrict__ shift_all, int p, double n_given, double factor,
+                              double* __restrict__ mu_all, double* __restrict__ sigma_all) {
+  const int id = inst ? inst[blockIdx.x] : blockIdx.x;
+  const double* S = sums_all + (long long)id * np;
+  const double n = n_given > 0 ? n_given : S[np - 1];
+  const double* c = shift_all ? shift_all + (long long)id * RTD_MAXP : nullptr;
+  double* mu = mu_all + (long long)id * RTD_MAXP;
+  double* sg = sigma_all + (long long)id * RTD_MAXP * RTD_MAXP;
+  for (int k = threadIdx.x; k < p; k += blockDim.x) mu[k] = (c ? c[k] : 0.0) + S[k] / n;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    int j = e / p, k = e - j * p;
+    int a = j > k ? j : k, b = j > k ? k : j;
+    double s2 = S[p + a * (a + 1) / 2 + b];
+    sg[e] = factor * ((s2 - S[j] * S[k] / n) / (n - 1.0));
+  }
+}
+
+void launch_sums_to_cov(const int* inst, int ninst, const double* sums_all, int np, const double* shift_all, int p,
+                        double n_given, double factor, double* mu_all, double* sigma_all, cudaStream_t st) {
+  k_sums_to_cov<<<ninst, 256, 0, st>>>(inst, sums_all, np, shift_all, p, n_given, factor, mu_all, sigma_all);
+  RTD_LAUNCHED();
+}
+
+// S~2 = S2 / n (uncentred second moment)
+__global__ void k_sums_to_second(const double* __restrict__ sums_all, int np, int p, double n,
+                                 double* __restrict__ out_all) {
+  const int b = blockIdx.x;
+  const double* S = sums_all + (long long)b * np;
+  double* o = out_all + (long long)b * RTD_MAXP * RTD_MAXP;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    int j = e / p, k = e - j * p;
+    int a = j > k ? j : k, bb = j > k ? k : j;
+    o[e] = S[p + a * (a + 1) / 2 + bb] / n;
+  }
+}
+
+void launch_sums_to_second(const double* sums_all, int nb, int np, int p, double n, double* out_all, cudaStream_t st) {
+  k_sums_to_second<<<nb, 256, 0, st>>>(sums_all, np, p, n, out_all);
+  RTD_LAUNCHED();
+}
+
+__global__ void k_copy_vec(const int* __restrict__ inst, const double* __restrict__ src, double* __restrict__ dst,
+                           int p) {
+  const int id = inst[blockIdx.x];
+  for (int k = threadIdx.x; k < p; k += blockDim.x) dst[(long long)id * RTD_MAXP + k] = src[(long long)id * RTD_MAXP + k];
+}
+
+void launch_copy_vec(const int* inst, int ninst, const double* src, double* dst, int p, cudaStream_t st) {
+  k_copy_vec<<<ninst, 64, 0, st>>>(inst, src, dst, p);
+  RTD_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ Jacobi eigen-decomposition
+__global__ void __launch_bounds__(LT) k_jacobi(const double* __restrict__ A_all, int p, double kappa_max,
+                                               double* __restrict__ V_all, double* __restrict__ lam_all,
+                                               int* __restrict__ ok_all) {
+  __shared__ double A[RTD_MAXP][LD], V[RTD_MAXP][LD];
+  __shared__ double cs[RTD_MAXP / 2 + 1], sn[RTD_MAXP / 2 + 1];
+  __shared__ int pa[RTD_MAXP / 2 + 1], qa[RTD_MAXP / 2 + 1];
+  __shared__ int order[RTD_MAXP + 2];
+  __shared__ double red[LT];
+  __shared__ int s_stop;
+  const int b = blockIdx.x, t = threadIdx.x;
+  const double* Ain = A_all + (long long)b * RTD_MAXP * RTD_MAXP;
+  for (int e = t; e < p * p; e += blockDim.x) {
+    int i = e / p, j = e - i * p;
+    A[i][j] = 0.5 * (Ain[i * p + j] + Ain[j * p + i]);
+    V[i][j] = (i == j) ? 1.0 : 0.0;
+  }
+  const int n2 = p + (p & 1);
+  if (t < n2) order[t] = t;
+  __syncthreads();
+  for (int sweep = 0; sweep < 60; sweep++) {
+    // convergence: off-diagonal mass relative to the total
+    double off = 0.0, tot = 0.0;
+    for (int e = t; e < p * p; e += blockDim.x) {
+      int i = e / p, j = e - i * p;
+      double v = A[i][j] * A[i][j];
+      tot += v;
+      if (i != j) off += v;
+    }
+    red[t] = off;
+    __syncthreads();
+    if (t == 0) {
+      double so = 0.0;
+      for (int k = 0; k < blockDim.x; k++) so += red[k];
+      red[0] = so;
+    }
+    __syncthreads();
+    double so = red[0];
+    __syncthreads();
+    red[t] = tot;
+    __syncthreads();
+    if (t == 0) {
+      double st = 0.0;
+      for (int k = 0; k < blockDim.x; k++) st += red[k];
+      s_stop = (so <= 1e-32 * st) || so == 0.0;
+    }
+    __syncthreads();
+    if (s_stop) break;
+    for (int round = 0; round < n2 - 1; round++) {
+      if (t < n2 / 2) {
+        int P = order[t], Q = order[n2 - 1 - t];
+        if (P > Q) { int tmp = P; P = Q; Q = tmp; }
+        double c = 1.0, s = 0.0;
+        if (Q < p && A[P][Q] != 0.0) {
+          double apq = A[P][Q];
+          double tau = (A[Q][Q] - A[P][P]) / (2.0 * apq);
+          double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + tt * tt);
+          s = tt * c;
+        }
+        pa[t] = P;
+        qa[t] = Q;
+        cs[t] = c;
+        sn[t] = s;
+      }
+      __syncthreads();
+      // rows: A <- P^T A
+      for (int e = t; e < (n2 / 2) * p; e += blockDim.x) {
+        int k = e / p, j = e - k * p;
+        int P = pa[k], Q = qa[k];
+        if (Q >= p || sn[k] == 0.0) continue;
+        double c = cs[k], s = sn[k];
+        double ap = A[P][j], aq = A[Q][j];
+        A[P][j] = c * ap - s * aq;
+        A[Q][j] = s * ap + c * aq;
+      }
+      __syncthreads();
+      // columns: A <- A P, V <- V P
+      for (int e = t; e < (n2 / 2) * p; e += blockDim.x) {
+        int k = e / p, i = e - k * p;
+        int P = pa[k], Q = qa[k];
+        if (Q >= p || sn[k] == 0.0) continue;
+        double c = cs[k], s = sn[k];
+        double ap = A[i][P], aq = A[i][Q];
+        A[i][P] = c * ap - s * aq;
+        A[i][Q] = s * ap + c * aq;
+        double vp = V[i][P], vq = V[i][Q];
+        V[i][P] = c * vp - s * vq;
+        V[i][Q] = s * vp + c * vq;
+      }
+      __syncthreads();
+      if (t < n2 / 2) {
+        int P = pa[t], Q = qa[t];
+        if (Q < p && sn[t] != 0.0) {
+          A[P][Q] = 0.0;
+          A[Q][P] = 0.0;
+        }
+      }
+      // rotate the round-robin order (position 0 fixed)
+      if (t == 0) {
+        int last = order[n2 - 1];
+        for (int k = n2 - 1; k > 1; k--) order[k] = order[k - 1];
+        order[1] = last;
+      }
+      __syncthreads();
+    }
+  }
+  // sort eigenvalues descending (stable), normalise signs
+  if (t == 0) {
+    int idx[RTD_MAXP];
+    for (int k = 0; k < p; k++) idx[k] = k;
+    for (int i = 1; i < p; i++) {  // insertion sort, stable
+      int v = idx[i];
+      int j = i - 1;
+      while (j >= 0 && A[idx[j]][idx[j]] < A[v][v]) {
+        idx[j + 1] = idx[j];
+        j--;
+      }
+      idx[j + 1] = v;
+    }
+    for (int k = 0; k < p; k++) order[k] = idx[k];
+    double lmax = A[idx[0]][idx[0]], lmin = A[idx[p - 1]][idx[p - 1]];
+    ok_all[b] = (lmin > 0.0 && lmax / lmin <= kappa_max) ? 1 : 0;
+  }
+  __syncthreads();
+  double* Vo = V_all + (long long)b * RTD_MAXP * RTD_MAXP;
+  double* lo = lam_all + (long long)b * RTD_MAXP;
+  if (t < p) {
+    const int src = order[t];
+    lo[t] = A[src][src];
+    int km = 0;
+    double vm = fabs(V[0][src]);
+    for (int i = 1; i < p; i++)
+      if (fabs(V[i][src]) > vm) { vm = fabs(V[i][src]); km = i; }
+    const double sg = V[km][src] < 0 ? -1.0 : 1.0;
+    for (int i = 0; i < p; i++) Vo[i * p + t] = sg * V[i][src];
+  }
+}
+
+void launch_jacobi(const double* A_all, int nb, int p, double kappa_max, double* V_all, double* lam_all, int* ok_all,
+                   cudaStream_t st) {
+  k_jacobi<<<nb, LT, 0, st>>>(A_all, p, kappa_max, V_all, lam_all, ok_all);
+  RTD_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ refinement matrices
+// which: 0 -> Sigma = V diag(d) V^T ; 1 -> V diag(d^-1/2) V^T ; 2 -> V diag(d^1/2) V^T
+__global__ void k_vdv(const double* __restrict__ V_all, const double* __restrict__ d_all, int p, int which,
+                      double* __restrict__ out_all) {
+  const int b = blockIdx.x;
+  const double* V = V_all + (long long)b * RTD_MAXP * RTD_MAXP;
+  const double* d = d_all + (long long)b * RTD_MAXP;
+  double* o = out_all + (long long)b * RTD_MAXP * RTD_MAXP;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    int i = e / p, j = e - i * p;
+    double s = 0.0;
+    for (int k = 0; k < p; k++) {
+      double dk = which == 0 ? d[k] : (which == 1 ? 1.0 / sqrt(d[k]) : sqrt(d[k]));
+      s += V[i * p + k] * dk * V[j * p + k];
+    }
+    o[e] = s;
+  }
+}
+
+void launch_vdv(const double* V_all, const double* d_all, int nb, int p, int which, double* out_all, cudaStream_t st) {
+  k_vdv<<<nb, 256, 0, st>>>(V_all, d_all, p, which, out_all);
+  RTD_LAUNCHED();
+}
+
+// y = A x for nb instances (A p x p row-major, stride MAXP^2; x, y stride MAXP)
+__global__ void k_matvec(const double* __restrict__ A_all, const double* __restrict__ x_all, int p,
+                         double* __restrict__ y_all) {
+  const int b = blockIdx.x;
+  const double* A = A_all + (long long)b * RTD_MAXP * RTD_MAXP;
+  const double* x = x_all + (long long)b * RTD_MAXP;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < p; k++) s += A[i * p + k] * x[k];
+    y_all[(long long)b * RTD_MAXP + i] = s;
+  }
+}
+
+void launch_matvec(const double* A_all, const double* x_all, int nb, int p, double* y_all, cudaStream_t st) {
+  k_matvec<<<nb, 64, 0, st>>>(A_all, x_all, p, y_all);
+  RTD_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ type-7 quantile cutoffs of sorted norms
+__global__ void k_lr_cutoffs(const double* __restrict__ rs_all, long long m, double* __restrict__ AB, int* __restrict__ ok) {
+  const int b = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const double* y = rs_all + (long long)b * m;
+  auto q7 = [&](double prob) {
+    double hpos = (double)(m - 1) * prob;
+    long long j = (long long)floor(hpos);
+    double g = hpos - (double)j;
+    if (j + 1 >= m) return y[m - 1];
+    return y[j] + g * (y[j + 1] - y[j]);
+  };
+  double A = q7(0.5);
+  double iqr = q7(0.75) - q7(0.25);
+  AB[2 * b] = A;
+  AB[2 * b + 1] = A + 1.5 * iqr;
+  ok[b] = iqr > 0.0 ? 1 : 0;
+}
+
+void launch_lr_cutoffs(const double* rs_all, int nb, long long m, double* AB, int* ok, cudaStream_t st) {
+  k_lr_cutoffs<<<nb, 32, 0, st>>>(rs_all, m, AB, ok);
+  RTD_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ aggregation of q block fits (K11)
+// in: mu[b][MAXP], sig[b][MAXP^2] for nv valid blocks (ids ascending), m rows per block.
+// out: mu_raw, sigma_raw; kept[b] flags; keys[b]
+__global__ void __launch_bounds__(LT) k_aggregate(const double* __restrict__ mu_base, const double* __restrict__ sig_base,
+                                                  const int* __restrict__ ids, int nv, int p, double m, double* __restrict__ mu_out,
+                                                  double* __restrict__ sig_out, int* __restrict__ kept,
+                                                  double* __restrict__ keys, double* __restrict__ scratch) {
+  __shared__ double A[RTD_MAXP * LD], L[RTD_MAXP * LD], Li[RTD_MAXP * LD];
+  __shared__ double mmed[RTD_MAXP], red[RTD_MAXP];
+  __shared__ int s_fail;
+  __shared__ int s_order[256];
+  const int t = threadIdx.x;
+#define mu_all_l(l) (mu_base + (long long)ids[l] * RTD_MAXP)
+#define sig_all_l(l) (sig_base + (long long)ids[l] * RTD_MAXP * RTD_MAXP)
+  // entrywise median (even count -> mean of the two middle values); scratch holds Sigma_med
+  double* smed = scratch;
+  for (int e = t; e < p + p * p; e += blockDim.x) {
+    double v[256];
+    int cnt = 0;
+    for (int l = 0; l < nv; l++) {
+      double x = e < p ? mu_all_l(l)[e] : sig_all_l(l)[e - p];
+      int j = cnt - 1;
+      while (j >= 0 && v[j] > x) { v[j + 1] = v[j]; j--; }
+      v[j + 1] = x;
+      cnt++;
+    }
+    double med = (nv & 1) ? v[nv / 2] : 0.5 * (v[nv / 2 - 1] + v[nv / 2]);
+    if (e < p) mmed[e] = med; else smed[e - p] = med;
+  }
+  __syncthreads();
+  // KL' key per block: tr(S_med S_l^-1) + log det S_l + (mu_med - mu_l)^T S_l^-1 (mu_med - mu_l)
+  for (int l = 0; l < nv; l++) {
+    const double* S = sig_all_l(l);
+    for (int e = t; e < p * p; e += blockDim.x) A[(e / p) * LD + e % p] = S[e];
+    __syncthreads();
+    bool ok = block_cholesky(A, L, p, &s_fail);
+    if (!ok) {
+      if (t == 0) keys[l] = INFINITY;
+      __syncthreads();
+      continue;
+    }
+    block_tri_inverse(L, Li, p);
+    block_inv_from_li(Li, A, p);  // A = S_l^-1
+    if (t == 0) {
+      double tr = 0.0;
+      for (int i = 0; i < p; i++)
+        for (int k = 0; k < p; k++) tr += smed[i * p + k] * A[k * LD + i];
+      double ld = 0.0;
+      for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
+      ld *= 2.0;
+      const double* mu = mu_all_l(l);
+      double quad = 0.0;
+      for (int i = 0; i < p; i++) {
+        double s = 0.0;
+        for (int k = 0; k < p; k++) s += A[i * LD + k] * (mmed[k] - mu[k]);
+        quad += (mmed[i] - mu[i]) * s;
+      }
+      keys[l] = tr + ld + quad;
+    }
+    __syncthreads();
+  }
+  // keep ceil(nv/2) smallest keys (ties -> lower block position), pool in block order
+  if (t == 0) {
+    for (int l = 0; l < nv; l++) s_order[l] = l;
+    for (int i = 1; i < nv; i++) {
+      int v = s_order[i], j = i - 1;
+      while (j >= 0 && (keys[s_order[j]] > keys[v])) { s_order[j + 1] = s_order[j]; j--; }
+      s_order[j + 1] = v;
+    }
+    const int keep = (nv + 1) / 2;
+    for (int l = 0; l < nv; l++) kept[l] = 0;
+    for (int i = 0; i < keep; i++) kept[s_order[i]] = 1;
+  }
+  __syncthreads();
+  // single-pass pooling (eqs. covpool) in block order
+  double* Lam = scratch + RTD_MAXP * RTD_MAXP;
+  __shared__ double mup[RTD_MAXP], dmu[RTD_MAXP];
+  __shared__ double np_s;
+  int first = 1;
+  for (int l = 0; l < nv; l++) {
+    if (!kept[l]) continue;
+    const double* S = sig_all_l(l);
+    const double* mu = mu_all_l(l);
+    if (first) {
+      for (int e = t; e < p * p; e += blockDim.x) Lam[e] = (m - 1.0) * S[e];
+      for (int k = t; k < p; k += blockDim.x) mup[k] = mu[k];
+      if (t == 0) np_s = m;
+      first = 0;
+      __syncthreads();
+      continue;
+    }
+    for (int k = t; k < p; k += blockDim.x) dmu[k] = mu[k] - mup[k];
+    __syncthreads();
+    const double npool = np_s;
+    const double w = npool * m / (npool + m);
+    for (int e = t; e < p * p; e += blockDim.x) {
+      int i = e / p, j = e - i * p;
+      Lam[e] = Lam[e] + (m - 1.0) * S[e] + dmu[i] * dmu[j] * w;
+    }
+    for (int k = t; k < p; k += blockDim.x) mup[k] = (npool * mup[k] + m * mu[k]) / (npool + m);
+    __syncthreads();
+    if (t == 0) np_s = npool + m;
+    __syncthreads();
+  }
+  for (int k = t; k < p; k += blockDim.x) mu_out[k] = mup[k];
+  for (int e = t; e < p * p; e += blockDim.x) sig_out[e] = Lam[e] / (np_s - 1.0);
+  (void)red;
+#undef mu_all_l
+#undef sig_all_l
+}
+
+void launch_aggregate(const double* mu_base, const double* sig_base, const int* ids, int nv, int p, double m,
+                      double* mu_out, double* sig_out, int* kept, double* keys, double* scratch, cudaStream_t st) {
+  k_aggregate<<<1, LT, 0, st>>>(mu_base, sig_base, ids, nv, p, m, mu_out, sig_out, kept, keys, scratch);
+  RTD_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ pool reweight partial sums over blocks
+// sums[b][np] about the common shift c; out mu, Sigma = factor * (S2 - S1 S1^T/k)/(k-1)
+__global__ void k_pool_sums(const double* __restrict__ sums_all, int nb, int np, double* __restrict__ out) {
+  for (int e = threadIdx.x; e < np; e += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; b++) s += sums_all[(long long)b * np + e];
+    out[e] = s;
+  }
+}
+
+void launch_pool_sums(const double* sums_all, int nb, int np, double* out, cudaStream_t st) {
+  k_pool_sums<<<1, 256, 0, st>>>(sums_all, nb, np, out);
+  RTD_LAUNCHED();
+}
+
+// mu_X = loc + scale mu_Z ; Sigma_X = diag(scale) Sigma_Z diag(scale)
+__global__ void k_destandardize(const UniOut* __restrict__ uni, const double* __restrict__ mu_z,
+                                const double* __restrict__ sig_z, int p, double* __restrict__ mu_x,
+                                double* __restrict__ sig_x) {
+  for (int k = threadIdx.x; k < p; k += blockDim.x) mu_x[k] = uni[k].loc + uni[k].scale * mu_z[k];
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    int i = e / p, j = e - i * p;
+    sig_x[e] = sig_z[e] * (uni[i].scale * uni[j].scale);
+  }
+}
+
+void launch_destandardize(const UniOut* uni, const double* mu_z, const double* sig_z, int p, double* mu_x,
+                          double* sig_x, cudaStream_t st) {
+  k_destandardize<<<1, 256, 0, st>>>(uni, mu_z, sig_z, p, mu_x, sig_x);
+  RTD_LAUNCHED();
+}
+
+}  // namespace rtd

@@ -1,0 +1,96 @@
+// Small helper kernels: Feistel forward map, extraction of univariate results,
+// per-row outputs in original row order, scaled matrix copies.
+#include "rtd_internal.h"
+
+namespace rtd {
+
+__device__ __forceinline__ unsigned long long splitmix64_f(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ unsigned long long feistel_enc(unsigned long long x, unsigned long long seed, int half) {
+  const unsigned long long mask = (1ull << half) - 1ull;
+  unsigned long long L = x >> half, R = x & mask;
+  for (int r = 0; r < 6; r++) {
+    unsigned long long F = splitmix64_f(seed ^ ((unsigned long long)r * 0x9E3779B97F4A7C15ull) ^ R) & mask;
+    unsigned long long nl = R;
+    R = L ^ F;
+    L = nl;
+  }
+  return (L << half) | R;
+}
+
+__global__ void k_feistel_fwd(long long n, unsigned long long seed, int half, long long* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long x = feistel_enc((unsigned long long)i, seed, half);
+    while (x >= (unsigned long long)n) x = feistel_enc(x, seed, half);
+    out[i] = (long long)x;
+  }
+}
+
+void launch_feistel_fwd(long long n, unsigned long long seed, long long* out, cudaStream_t st) {
+  int bits = 0;
+  while ((1ll << bits) < n) bits++;
+  if (bits < 2) bits = 2;
+  bits += bits & 1;
+  unsigned gx = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
+  k_feistel_fwd<<<gx, 256, 0, st>>>(n, seed, bits / 2, out);
+  RTD_LAUNCHED();
+}
+
+// which 0: out[j] = scale_j^2 (refinement step 3); 1: out[j] = loc_j (step 4)
+__global__ void k_uni_extract(const UniOut* __restrict__ uni, int p, int which, double* __restrict__ out) {
+  for (int j = threadIdx.x; j < p; j += blockDim.x) out[j] = which == 0 ? uni[j].scale * uni[j].scale : uni[j].loc;
+}
+
+void launch_uni_extract(const UniOut* uni, int p, int which, double* out, cudaStream_t st) {
+  k_uni_extract<<<1, 64, 0, st>>>(uni, p, which, out);
+  RTD_LAUNCHED();
+}
+
+__global__ void k_weights_from_d2(const double* __restrict__ d2, long long total, double c2,
+                                  const long long* __restrict__ rowmap, uint8_t* __restrict__ dst) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    long long row = rowmap ? rowmap[t] : t;
+    dst[row] = d2[t] <= c2 ? 1 : 0;
+  }
+}
+
+void launch_weights_from_d2(const double* d2, long long total, double c2, const long long* rowmap, uint8_t* dst,
+                            cudaStream_t st) {
+  unsigned gx = (unsigned)std::min<long long>((total + 255) / 256, 148 * 16);
+  k_weights_from_d2<<<gx, 256, 0, st>>>(d2, total, c2, rowmap, dst);
+  RTD_LAUNCHED();
+}
+
+__global__ void k_hsub_from_mem(const uint8_t* __restrict__ mem_all, const int* __restrict__ chosen_inst, long long m,
+                                const long long* __restrict__ rowmap, uint8_t* __restrict__ dst) {
+  const int b = blockIdx.y;
+  const int id = chosen_inst[b];
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < m; s += (long long)gridDim.x * blockDim.x) {
+    long long t = (long long)b * m + s;
+    long long row = rowmap ? rowmap[t] : t;
+    dst[row] = id >= 0 ? mem_all[(long long)id * m + s] : 0;
+  }
+}
+
+void launch_hsub_from_mem(const uint8_t* mem_all, const int* chosen_inst, int q, long long m, const long long* rowmap,
+                          uint8_t* dst, cudaStream_t st) {
+  unsigned gx = (unsigned)std::min<long long>((m + 255) / 256, 148 * 8);
+  k_hsub_from_mem<<<dim3(gx, q), 256, 0, st>>>(mem_all, chosen_inst, m, rowmap, dst);
+  RTD_LAUNCHED();
+}
+
+__global__ void k_scale_copy(const double* __restrict__ src, double* __restrict__ dst, int p, double factor) {
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) dst[e] = factor * src[e];
+}
+
+void launch_scale_copy(const double* src, double* dst, int p, double factor, cudaStream_t st) {
+  k_scale_copy<<<1, 256, 0, st>>>(src, dst, p, factor);
+  RTD_LAUNCHED();
+}
+
+}  // namespace rtd

@@ -1,0 +1,315 @@
+// K1: batched univariate reweighted MCD (§3.1).
+//
+// For every column: sort (CUB radix sort of fp64 keys), then evaluate the
+// window objective h*SQ(s) = h*S2(s) - S1(s)^2 for every start s from
+// double-double prefix sums, take the argmin (ties -> lowest s, reading R2),
+// and finish the raw and reweighted estimates (readings R3, R4):
+//   loc0 = S1(s*)/h, var0 = c(h/n,1) SQ(s*)/(h-1),
+//   kept = {(y-loc0)^2 <= chi2_{1,.975} var0} (a contiguous range of the sorted column),
+//   loc = round(sum kept)/k, scale^2 = c(.975,1) sum_kept (y-loc)^2/(k-1).
+// Prefix sums are never materialised: each window CTA rebuilds the two
+// prefix streams it needs (P(s) and P(s+h)) from per-chunk totals.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "rtd_internal.h"
+
+namespace rtd {
+
+static constexpr int UCH = 1024;   // elements per chunk
+static constexpr int UTH = 256;    // threads per CTA (4 elements each)
+static constexpr int UPT = UCH / UTH;
+
+__global__ void __launch_bounds__(UTH) k_uni_chunksum(const double* __restrict__ sorted, long long len, int nchunks,
+                                                      dd2* __restrict__ csum) {
+  __shared__ dd2 sm[33];
+  const int col = blockIdx.y;
+  const long long s0 = (long long)blockIdx.x * UCH;
+  const double* y = sorted + (long long)col * len;
+  dd2 acc = dd2_zero();
+#pragma unroll
+  for (int e = 0; e < UPT; e++) {
+    long long i = s0 + threadIdx.x * UPT + e;
+    if (i < len) acc = dd2_add(acc, dd2_of(y[i]));
+  }
+  dd2 tot = block_sum_dd2(acc, sm);
+  if (threadIdx.x == 0) csum[(long long)col * nchunks + blockIdx.x] = tot;
+}
+
+// exclusive prefix of chunk totals; coff[col][c] for c in [0, nchunks]
+__global__ void __launch_bounds__(1024) k_uni_chunkscan(const dd2* __restrict__ csum, int nchunks,
+                                                        dd2* __restrict__ coff) {
+  __shared__ dd2 sm[33];
+  const int col = blockIdx.y;
+  const dd2* cs = csum + (long long)col * nchunks;
+  dd2* co = coff + (long long)col * (nchunks + 1);
+  const int per = (nchunks + blockDim.x - 1) / blockDim.x;
+  const int c0 = threadIdx.x * per;
+  dd2 loc = dd2_zero();
+  for (int c = c0; c < min(c0 + per, nchunks); c++) loc = dd2_add(loc, cs[c]);
+  dd2 tot;
+  dd2 ex = block_exscan_dd2(loc, &tot, sm);
+  for (int c = c0; c < min(c0 + per, nchunks); c++) {
+    co[c] = ex;
+    ex = dd2_add(ex, cs[c]);
+  }
+  if (threadIdx.x == 0) co[nchunks] = tot;
+}
+
+// P(t) = sum_{i<t} (y_i, y_i^2), block-cooperative; all threads get the value.
+__device__ dd2 block_prefix_at(const double* __restrict__ y, const dd2* __restrict__ co, long long t, dd2* sm) {
+  const long long c = t / UCH;
+  const long long s0 = c * UCH;
+  dd2 acc = dd2_zero();
+#pragma unroll
+  for (int e = 0; e < UPT; e++) {
+    long long i = s0 + threadIdx.x * UPT + e;
+    if (i < t) acc = dd2_add(acc, dd2_of(y[i]));
+  }
+  dd2 tot = block_sum_dd2(acc, sm);
+  return dd2_add(co[c], tot);
+}
+
+struct WinPartial {
+  double vhi, vlo;
+  long long s;
+};
+
+__device__ __forceinline__ bool win_better(double ahi, double alo, long long as, double bhi, double blo, long long bs) {
+  if (ahi != bhi) return ahi < bhi;
+  if (alo != blo) return alo < blo;
+  return as < bs;
+}
+
+// window objective for starts s in [blockIdx.x*UCH, +UCH) ∩ [0, nwin)
+__global__ void __launch_bounds__(UTH) k_uni_window(const double* __restrict__ sorted, long long len, long long h,
+                                                    int nchunks, const dd2* __restrict__ coff, int nwchunks,
+                                                    WinPartial* __restrict__ part) {
+  __shared__ dd2 sm[33];
+  __shared__ WinPartial wsm[UTH / 32];
+  const int col = blockIdx.y;
+  const double* y = sorted + (long long)col * len;
+  const dd2* co = coff + (long long)col * (nchunks + 1);
+  const long long nwin = len - h + 1;
+  const long long s0 = (long long)blockIdx.x * UCH;
+  // left stream P(s), s = s0 + 4t + e ; s0 is a chunk boundary
+  double yl[UPT], yr[UPT];
+#pragma unroll
+  for (int e = 0; e < UPT; e++) {
+    long long i = s0 + threadIdx.x * UPT + e;
+    yl[e] = i < len ? y[i] : 0.0;
+  }
+  dd2 tl = dd2_zero();
+#pragma unroll
+  for (int e = 0; e < UPT; e++) tl = dd2_add(tl, dd2_of(yl[e]));
+  dd2 totl;
+  dd2 exl = block_exscan_dd2(tl, &totl, sm);
+  exl = dd2_add(co[blockIdx.x], exl);
+  // right stream P(s + h)
+  const long long a = s0 + h;
+  dd2 Pa = block_prefix_at(y, co, a, sm);
+#pragma unroll
+  for (int e = 0; e < UPT; e++) {
+    long long i = a + threadIdx.x * UPT + e;
+    yr[e] = i < len ? y[i] : 0.0;
+  }
+  dd2 tr = dd2_zero();
+#pragma unroll
+  for (int e = 0; e < UPT; e++) tr = dd2_add(tr, dd2_of(yr[e]));
+  dd2 totr;
+  dd2 exr = block_exscan_dd2(tr, &totr, sm);
+  exr = dd2_add(Pa, exr);
+  double bhi = __longlong_as_double(0x7ff0000000000000LL), blo = 0.0;
+  long long bs = 0x7fffffffffffffffLL;
+  const double hd = (double)h;
+#pragma unroll
+  for (int e = 0; e < UPT; e++) {
+    long long s = s0 + threadIdx.x * UPT + e;
+    if (s < nwin) {
+      dd S1 = dd_sub(exr.s1, exl.s1);
+      dd S2 = dd_sub(exr.s2, exl.s2);
+      dd v = dd_sub(dd_mul_d(S2, hd), dd_mul(S1, S1));
+      if (win_better(v.hi, v.lo, s, bhi, blo, bs)) {
+        bhi = v.hi;
+        blo = v.lo;
+        bs = s;
+      }
+    }
+    exl = dd2_add(exl, dd2_of(yl[e]));
+    exr = dd2_add(exr, dd2_of(yr[e]));
+  }
+  // block argmin
+  for (int d = 16; d > 0; d >>= 1) {
+    double ohi = __shfl_down_sync(0xffffffffu, bhi, d);
+    double olo = __shfl_down_sync(0xffffffffu, blo, d);
+    long long os = __shfl_down_sync(0xffffffffu, bs, d);
+    if (win_better(ohi, olo, os, bhi, blo, bs)) {
+      bhi = ohi;
+      blo = olo;
+      bs = os;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) wsm[threadIdx.x >> 5] = {bhi, blo, bs};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    WinPartial b = wsm[0];
+    for (int w = 1; w < UTH / 32; w++)
+      if (win_better(wsm[w].vhi, wsm[w].vlo, wsm[w].s, b.vhi, b.vlo, b.s)) b = wsm[w];
+    part[(long long)col * nwchunks + blockIdx.x] = b;
+  }
+}
+
+__device__ __forceinline__ bool uni_keep(double y, double loc0, double thresh) {
+  double d = __dsub_rn(y, loc0);
+  return __dmul_rn(d, d) <= thresh;
+}
+
+__global__ void __launch_bounds__(UTH) k_uni_final(const double* __restrict__ sorted, long long len, long long h,
+                                                   int nchunks, const dd2* __restrict__ coff, int nwchunks,
+                                                   const WinPartial* __restrict__ part, UniConst uc,
+                                                   UniOut* __restrict__ out) {
+  __shared__ dd2 sm[33];
+  __shared__ WinPartial wsm[UTH / 32];
+  __shared__ long long s_lohi[2];
+  const int col = blockIdx.x;
+  const double* y = sorted + (long long)col * len;
+  const dd2* co = coff + (long long)col * (nchunks + 1);
+  const WinPartial* pp = part + (long long)col * nwchunks;
+  double bhi = __longlong_as_double(0x7ff0000000000000LL), blo = 0.0;
+  long long bs = 0x7fffffffffffffffLL;
+  for (int c = threadIdx.x; c < nwchunks; c += blockDim.x) {
+    WinPartial w = pp[c];
+    if (win_better(w.vhi, w.vlo, w.s, bhi, blo, bs)) {
+      bhi = w.vhi;
+      blo = w.vlo;
+      bs = w.s;
+    }
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    double ohi = __shfl_down_sync(0xffffffffu, bhi, d);
+    double olo = __shfl_down_sync(0xffffffffu, blo, d);
+    long long os = __shfl_down_sync(0xffffffffu, bs, d);
+    if (win_better(ohi, olo, os, bhi, blo, bs)) {
+      bhi = ohi;
+      blo = olo;
+      bs = os;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) wsm[threadIdx.x >> 5] = {bhi, blo, bs};
+  __syncthreads();
+  WinPartial best = wsm[0];
+  for (int w = 1; w < UTH / 32; w++)
+    if (win_better(wsm[w].vhi, wsm[w].vlo, wsm[w].s, best.vhi, best.vlo, best.s)) best = wsm[w];
+  __syncthreads();
+  const long long s = best.s;
+  dd2 P0 = block_prefix_at(y, co, s, sm);
+  dd2 P1 = block_prefix_at(y, co, s + h, sm);
+  dd S1 = dd_sub(P1.s1, P0.s1);
+  const double hd = (double)h;
+  const double loc0 = dd_to_d(dd_div_d(S1, hd));
+  dd v = {best.vhi, best.vlo};
+  const double var_raw = h > 1 ? dd_to_d(dd_div_d(dd_div_d(v, hd), (double)(h - 1))) : 0.0;
+  const double var0 = uc.c_raw * var_raw;
+  const double thresh = uc.q1 * var0;
+  if (threadIdx.x == 0) {
+    // i0 = first index with y >= loc0
+    long long lo = 0, hi = len;
+    while (lo < hi) {
+      long long mid = (lo + hi) >> 1;
+      if (y[mid] < loc0) lo = mid + 1; else hi = mid;
+    }
+    const long long i0 = lo;
+    // first kept index in [0, i0] (keep is false then true on [0, i0))
+    lo = 0; hi = i0;
+    while (lo < hi) {
+      long long mid = (lo + hi) >> 1;
+      if (uni_keep(y[mid], loc0, thresh)) hi = mid; else lo = mid + 1;
+    }
+    const long long klo = lo;
+    // first non-kept index in [i0, len) (keep is true then false)
+    lo = i0; hi = len;
+    while (lo < hi) {
+      long long mid = (lo + hi) >> 1;
+      if (uni_keep(y[mid], loc0, thresh)) lo = mid + 1; else hi = mid;
+    }
+    s_lohi[0] = klo;
+    s_lohi[1] = lo;
+  }
+  __syncthreads();
+  const long long klo = s_lohi[0], khi = s_lohi[1];
+  const long long k = khi - klo;
+  dd2 Q0 = block_prefix_at(y, co, klo, sm);
+  dd2 Q1 = block_prefix_at(y, co, khi, sm);
+  if (threadIdx.x == 0) {
+    UniOut o;
+    o.raw_loc = loc0;
+    o.raw_var = var_raw;
+    o.var0 = var0;
+    o.start = s;
+    o.kept = k;
+    o.pad = 0;
+    o.status = 0;
+    o.loc = 0.0;
+    o.scale = 0.0;
+    if (!(var0 > 0.0) || k < 2) {
+      o.status = 1;
+    } else {
+      dd2 K = dd2_sub(Q1, Q0);
+      const double Sd = dd_to_d(K.s1);
+      const double loc = Sd / (double)k;
+      // sum (y - loc)^2 = S2 - 2 loc S1 + k loc^2, in dd
+      dd q = dd_sub(K.s2, dd_mul_d(K.s1, 2.0 * loc));
+      q = dd_add(q, dd_mul_d(two_prod(loc, loc), (double)k));
+      const double var = uc.c_rew * (dd_to_d(q) / (double)(k - 1));
+      o.loc = loc;
+      o.scale = sqrt(var);
+      if (!(var > 0.0)) o.status = 1;
+    }
+    out[col] = o;
+  }
+}
+
+struct UniScratch {
+  double* sorted;
+  dd2* csum;
+  dd2* coff;
+  WinPartial* part;
+  void* cub_tmp;
+  size_t cub_bytes;
+};
+
+static size_t cub_sort_bytes(long long len) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const double*)nullptr, (double*)nullptr, (int)len);
+  return bytes;
+}
+
+void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, int ncols, UniConst uc,
+                  UniOut* out_dev) {
+  const long long h = len / 2 + 1;
+  const int nchunks = (int)((len + UCH - 1) / UCH);
+  const long long nwin = len - h + 1;
+  const int nwchunks = (int)((nwin + UCH - 1) / UCH);
+  UniScratch s;
+  s.sorted = A.take<double>((size_t)ncols * len);
+  s.csum = A.take<dd2>((size_t)ncols * nchunks);
+  s.coff = A.take<dd2>((size_t)ncols * (nchunks + 1));
+  s.part = A.take<WinPartial>((size_t)ncols * nwchunks);
+  s.cub_bytes = cub_sort_bytes(len);
+  s.cub_tmp = A.take<char>(s.cub_bytes);
+  if (A.base == nullptr) return;  // dry run
+  for (int j = 0; j < ncols; j++) {
+    size_t bytes = s.cub_bytes;
+    RTD_CU(cub::DeviceRadixSort::SortKeys(s.cub_tmp, bytes, cols + (long long)j * len, s.sorted + (long long)j * len,
+                                          (int)len, 0, 64, st));
+  }
+  k_uni_chunksum<<<dim3(nchunks, ncols), UTH, 0, st>>>(s.sorted, len, nchunks, s.csum);
+  RTD_LAUNCHED();
+  k_uni_chunkscan<<<dim3(1, ncols), 1024, 0, st>>>(s.csum, nchunks, s.coff);
+  RTD_LAUNCHED();
+  k_uni_window<<<dim3(nwchunks, ncols), UTH, 0, st>>>(s.sorted, len, h, nchunks, s.coff, nwchunks, s.part);
+  RTD_LAUNCHED();
+  k_uni_final<<<ncols, UTH, 0, st>>>(s.sorted, len, h, nchunks, s.coff, nwchunks, s.part, uc, out_dev);
+  RTD_LAUNCHED();
+}
+
+}  // namespace rtd

