@@ -1,0 +1,301 @@
+#!/usr/bin/env python
+"""bench.py — RT-DetMCD fit + flag throughput on B200 (BASELINE.json `metric`).
+
+One step = one whole pass of the hot path over
+one batch of synthetic input: standardise, starts, refinement, C-steps,
+raw fit (+ aggregation for q > 1), reweighting and the flag pass over all n
+rows.  Default workload: BASELINE config 4 (n = 8,000,000, p = 40, h = 0.75 n,
+q = 8 blocks, seeded Feistel partition) on one GPU; inputs (2.56 GB) are larger
+than L2 (126 MB), so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+Prints ONE JSON line (rank 0).  `value` = observations/s over all ranks with X
+resident in HBM; `e2e` = the same through the C ABI with pinned HOST buffers
+(H2D of X and D2H of the flags inside the timed region); `roofline` = the
+C-step distance pass (the north-star kernel) measured live with CUDA events
+on the library stream; `cpu_baseline` = the CPU oracle on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_NAMES = {1: "cfg1_n1000_p5", 2: "cfg2_n100k_p10", 3: "cfg3_n1M_p20", 4: "cfg4_n8M_p40_q8", 5: "cfg5_n20k_p8"}
+METRIC = "observations/sec fitted+flagged (RT-DetMCD, fp64)"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(cfg: int, n: int | None = None):
+    from paper_1910_05615_b200 import datagen
+    d = datagen.make_config(cfg, n=n)
+    return d
+
+
+def cpu_baseline(cfg: int, sample_n: int | None = None):
+    """The oracle, as it stands, on a bounded sample of the same workload (rank 0, N = 1 only)."""
+    from threadpoolctl import threadpool_info
+
+    from oracle import fit as ofit
+    from paper_1910_05615_b200 import datagen
+    if sample_n is None:
+        sample_n = {1: 1000, 2: 100_000, 3: 200_000, 4: 200_000, 5: 20_000}[cfg]
+    d = datagen.make_config(cfg, n=sample_n)
+    q = d.q if cfg == 4 else 1
+    h = int(math.floor(0.75 * sample_n)) if cfg == 4 else d.h
+    t0 = time.perf_counter()
+    ofit.fit(d.X, h=h, q=q, seed=191005615, log_transform=d.log_transform)
+    dt = time.perf_counter() - t0
+    threads = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+    return {"value": sample_n / dt, "unit": "obs/s", "cores": int(threads), "kind": "oracle",
+            "sample": f"config {cfg} recipe at n={sample_n} (q={q}), one fit+flag, {dt:.1f} s wall"}
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the CPU oracle is this tier's reference arm (rank 0 only)."""
+    if rank != 0:
+        return
+    cfg = args.config
+    times = []
+    sample_n = args.ref_sample or {1: 1000, 2: 50_000, 3: 50_000, 4: 50_000, 5: 20_000}[cfg]
+    for s in range(args.warmup + args.steps):
+        cb = cpu_baseline(cfg, sample_n)
+        if s >= args.warmup:
+            times.append(sample_n / cb["value"])
+    ms = 1e3 * float(np.mean(times))
+    value = sample_n / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": CONFIG_NAMES[cfg], "sample_rows": sample_n},
+            "cpu_baseline": {"value": value, "unit": "obs/s", "cores": cb["cores"], "kind": "oracle",
+                             "sample": cb["sample"]},
+            "e2e": {"value": value, "unit": "obs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--n", type=int, default=0, help="override rows (debug only; not a bench line)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_1910_05615_b200 import api
+
+    cfg = args.config
+    d = make_workload(cfg, n=args.n or None)
+    n, p = d.X.shape
+    q = d.q
+    h = d.h
+    if world > 1:
+        from paper_1910_05615_b200 import distributed as rtd_dist
+        runner = rtd_dist.ShardedFit(d.X, h=h, q=q, seed=191005615, log_transform=d.log_transform, rank=rank,
+                                     world=world, device=local)
+        step = runner.step
+        n_rows_total = n
+    else:
+        Xd = torch.from_numpy(d.X).to(f"cuda:{local}")
+
+        def step():
+            return api.fit(Xd, h=h, q=q, seed=191005615, log_transform=d.log_transform,
+                           outputs=("flags",))
+        n_rows_total = n
+    del_host = None
+
+    # warm-up (also sizes the workspace)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    api.set_profiling(True, device=local)
+    k0, s0 = api.counters()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    stream = torch.cuda.current_stream()
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    k1, s1 = api.counters()
+    prof = api.profile(device=local)
+    api.set_profiling(False, device=local)
+    ms_local = ev0.elapsed_time(ev1)
+    ms = ms_local
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms_local], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = n_rows_total * args.steps / (ms / 1e3)
+
+    # e2e: the same step through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        Xh = torch.from_numpy(d.X).pin_memory()
+        fl = torch.empty(n, dtype=torch.uint8).pin_memory()
+        api.fit(Xh, h=h, q=q, seed=191005615, log_transform=d.log_transform, outputs=(), out_buffers={"flags": fl})
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            api.fit(Xh, h=h, q=q, seed=191005615, log_transform=d.log_transform, outputs=(),
+                    out_buffers={"flags": fl})
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ems = max(e0.elapsed_time(e1), wall * 1e3)
+        e2e = {"value": n * args.steps / (ems / 1e3), "unit": "obs/s", "h2d_bytes_per_step": int(n * p * 8),
+               "d2h_bytes_per_step": int(n)}
+
+    peaks = _peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm_peak else "fallback (B200_PROFILING.md 6650 GB/s)"
+    hbm_peak = hbm_peak or 6650.0
+    roof = None
+    if "dist" in prof and prof["dist"]["ms"] > 0:
+        dstat = prof["dist"]
+        achieved = dstat["bytes"] / (dstat["ms"] / 1e3) / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "dist_traffic.json")
+        if os.path.exists(tf):
+            try:
+                tj = json.load(open(tf))
+                if tj.get("config") == CONFIG_NAMES[cfg]:
+                    traffic = tj.get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic, "kernel": "k_dist (C-step distance pass)", "peak_source": peak_src,
+                "launches": dstat["launches"], "avg_launch_ms": dstat["ms"] / dstat["launches"],
+                "bytes_per_launch": dstat["bytes"] / dstat["launches"],
+                "ms_share_of_step": dstat["ms"] / ms_local}
+    breakdown = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                     "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] > 0 else None}
+                 for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(cfg)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": CONFIG_NAMES[cfg], "n": int(n), "p": int(p), "h": int(h), "q": int(q),
+                           "partition": "feistel", "l2": "inputs larger than L2 (no flush)",
+                           "parallelism": f"rows over {world} GPU(s)"},
+                "e2e": e2e, "roofline": roof, "cpu_baseline": cb,
+                "gpu_launches": int((k1 - k0)), "cub_sorts": int(s1 - s0),
+                "clocks": clk.summary(), "breakdown": breakdown,
+                "fit": {"block_chosen": [int(x) for x in res.block_chosen] if hasattr(res, "block_chosen") else None,
+                        "start_steps": [int(x) for x in res.start_steps] if hasattr(res, "start_steps") else None}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

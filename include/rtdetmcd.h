@@ -181,6 +181,22 @@ rtdetmcd_status rtdetmcd_csteps(rtdetmcd_ctx* ctx, const double* Z, int64_t m, i
                                 int32_t refresh_every, double* mu, double* sigma, double* logdet, int32_t* steps,
                                 int32_t* status, uint8_t* hsubset, double* logdet_traj);
 
+/* Per-kernel-class timing (for bench.py's roofline).  on != 0 enables it and
+ * clears the counters: every later call records a CUDA event pair on the
+ * context stream around each timed kernel class ("dist" = the C-step /
+ * reweight distance pass, "select", "moments_dense", "moments_delta",
+ * "unimcd", "matmul", "initial", "flag", ...).  Entries accumulate the
+ * device time (ms), the launch count and the ALGORITHMIC bytes of those
+ * launches (e.g. dist: rows * (8p + 8)).  name [host] receives up to
+ * name_len-1 characters. */
+rtdetmcd_status rtdetmcd_set_profiling(rtdetmcd_ctx* ctx, int32_t on);
+/* Process-wide counters: hand-written kernel launches and CUB radix-sort
+ * invocations issued by this library so far (host pointers, nullable). */
+void rtdetmcd_counters(int64_t* kernels, int64_t* sorts);
+int32_t rtdetmcd_prof_count(const rtdetmcd_ctx* ctx);
+rtdetmcd_status rtdetmcd_prof_entry(const rtdetmcd_ctx* ctx, int32_t i, char* name, size_t name_len, double* ms_total,
+                                    int64_t* launches, double* bytes_total);
+
 /* Host numerics used by the fit, exported for checking. */
 double rtdetmcd_chi2_quantile(double prob, int32_t dof);
 double rtdetmcd_consistency_factor(double alpha, int32_t p);

@@ -23,6 +23,7 @@ EXPORTS = [
     "rtdetmcd_set_workspace", "rtdetmcd_fit_workspace_size", "rtdetmcd_fit", "rtdetmcd_flag",
     "rtdetmcd_unimcd", "rtdetmcd_initial", "rtdetmcd_refine", "rtdetmcd_csteps",
     "rtdetmcd_chi2_quantile", "rtdetmcd_consistency_factor", "rtdetmcd_choose_q", "rtdetmcd_partition_perm",
+    "rtdetmcd_set_profiling", "rtdetmcd_prof_count", "rtdetmcd_prof_entry", "rtdetmcd_counters",
 ]
 
 
@@ -81,6 +82,12 @@ def lib() -> C.CDLL:
     L.rtdetmcd_choose_q.argtypes = [i64, i32, i64, i32]
     L.rtdetmcd_choose_q.restype = i32
     L.rtdetmcd_partition_perm.argtypes = [vp, i64, u64, vp]
+    L.rtdetmcd_set_profiling.argtypes = [vp, i32]
+    L.rtdetmcd_counters.argtypes = [vp, vp]
+    L.rtdetmcd_counters.restype = None
+    L.rtdetmcd_prof_count.argtypes = [vp]
+    L.rtdetmcd_prof_count.restype = i32
+    L.rtdetmcd_prof_entry.argtypes = [vp, i32, C.c_char_p, C.c_size_t, vp, vp, vp]
     for name in EXPORTS:  # every declared symbol must resolve
         getattr(L, name)
     _LIB = L

@@ -122,7 +122,7 @@ def workspace_size(n: int, p: int, **opts) -> int:
 def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, kappa_max: float = 1000.0,
         quantile: float = 0.975, max_csteps: int = 100, refresh_every: int = 32, partition: int = 0,
         log_transform: bool = False, outputs=("flags", "rd2", "weights", "hsubset"), device: int | None = None,
-        torch_workspace: bool = True) -> Fit:
+        torch_workspace: bool = True, out_buffers: dict | None = None) -> Fit:
     """rtdetmcd_fit on an n x p row-major float64 matrix (numpy or torch, host or device)."""
     ptr, keep, is_cuda, dev = _as_f64(X)
     n, p = int(keep.shape[0]), int(keep.shape[1])
@@ -152,7 +152,11 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
         setattr(r, k, a.ctypes.data)
     rows = {}
     for k, dt in (("flags", np.uint8), ("rd2", np.float64), ("weights", np.uint8), ("hsubset", np.uint8)):
-        if k in outputs:
+        if out_buffers and k in out_buffers:          # caller-provided buffer (e.g. pinned host tensor)
+            buf = out_buffers[k]
+            rows[k] = buf
+            setattr(r, k, buf.data_ptr() if hasattr(buf, "data_ptr") else buf.ctypes.data)
+        elif k in outputs:
             buf, bp = _out_buffer(n, dt, is_cuda, dev)
             rows[k] = buf
             setattr(r, k, bp)
@@ -266,3 +270,28 @@ def partition_perm(n: int, seed: int, device: int = 0) -> np.ndarray:
     out = np.zeros(n, np.int64)
     _check(lib().rtdetmcd_partition_perm(ctx["h"], int(n), C.c_uint64(seed & (2 ** 64 - 1)), out.ctypes.data), ctx)
     return out
+
+
+def set_profiling(on: bool = True, device: int = 0) -> None:
+    ctx = _ctx(device)
+    _check(lib().rtdetmcd_set_profiling(ctx["h"], int(bool(on))), ctx)
+
+
+def profile(device: int = 0) -> dict:
+    """{kernel class: {"ms": total device ms, "launches": n, "bytes": algorithmic bytes}} since set_profiling."""
+    ctx = _ctx(device)
+    L = lib()
+    out = {}
+    for i in range(L.rtdetmcd_prof_count(ctx["h"])):
+        name = C.create_string_buffer(64)
+        ms, n, by = C.c_double(), C.c_int64(), C.c_double()
+        _check(L.rtdetmcd_prof_entry(ctx["h"], i, name, 64, C.byref(ms), C.byref(n), C.byref(by)), ctx)
+        out[name.value.decode()] = {"ms": ms.value, "launches": n.value, "bytes": by.value}
+    return out
+
+
+def counters() -> tuple:
+    """(hand-written kernel launches, CUB sort invocations) issued by the library so far."""
+    k, s = C.c_int64(), C.c_int64()
+    lib().rtdetmcd_counters(C.byref(k), C.byref(s))
+    return k.value, s.value

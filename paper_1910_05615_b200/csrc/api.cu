@@ -15,6 +15,8 @@
 #include "rtd_linalg.h"
 
 namespace rtd {
+long long launch_count();
+long long sort_count();
 void launch_feistel_fwd(long long n, unsigned long long seed, long long* out, cudaStream_t st);
 void launch_uni_extract(const UniOut* uni, int p, int which, double* out, cudaStream_t st);
 void launch_scatter_u8(const uint8_t* src, const long long* rowmap, long long total, uint8_t* dst, cudaStream_t st);
@@ -27,6 +29,74 @@ void launch_hsub_from_mem(const uint8_t* mem_all, const int* chosen_inst, int q,
 
 using namespace rtd;
 
+// ------------------------------------------------------------------ optional per-kernel-class timing
+// When profiling is on, each timed region records a CUDA event pair on the
+// context stream; elapsed times are folded in after the call synchronised.
+struct ProfStat {
+  double ms = 0.0, bytes = 0.0;
+  long long launches = 0;
+};
+struct Prof {
+  bool on = false;
+  std::vector<std::pair<std::string, ProfStat>> stats;
+  struct Pending {
+    int idx;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  int index(const char* name) {
+    for (size_t i = 0; i < stats.size(); i++)
+      if (stats[i].first == name) return (int)i;
+    stats.push_back({name, ProfStat{}});
+    return (int)stats.size() - 1;
+  }
+  void fold() {
+    for (auto& pd : pending) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pd.a, pd.b);
+      auto& s = stats[pd.idx].second;
+      s.ms += ms;
+      s.bytes += pd.bytes;
+      s.launches += 1;
+      pool.push_back(pd.a);
+      pool.push_back(pd.b);
+    }
+    pending.clear();
+  }
+};
+static thread_local Prof* g_prof = nullptr;
+static thread_local cudaStream_t g_prof_stream = nullptr;
+
+struct ProfScope {
+  int idx = -1;
+  cudaEvent_t a{}, b{};
+  double bytes;
+  ProfScope(const char* name, double algorithmic_bytes) : bytes(algorithmic_bytes) {
+    if (!g_prof || !g_prof->on) return;
+    idx = g_prof->index(name);
+    a = g_prof->ev();
+    b = g_prof->ev();
+    cudaEventRecord(a, g_prof_stream);
+  }
+  ~ProfScope() {
+    if (idx < 0) return;
+    cudaEventRecord(b, g_prof_stream);
+    g_prof->pending.push_back({idx, a, b, bytes});
+  }
+};
+
 struct rtdetmcd_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -35,6 +105,7 @@ struct rtdetmcd_ctx {
   char* ws = nullptr;
   size_t ws_cap = 0;
   bool ws_user = false;
+  Prof prof;
 };
 
 namespace {
@@ -104,6 +175,7 @@ UniConst uni_const(long long len) {
 
 void run_unimcd(cudaStream_t st, char* scratch, size_t scratch_bytes, const double* cols, long long len, int ncols,
                 UniOut* out) {
+  ProfScope ps("unimcd", (double)ncols * len * 8.0);
   Arena a;
   a.base = scratch;
   a.cap = scratch_bytes;
@@ -176,6 +248,7 @@ void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long
   for (int g0 = 0; g0 < nact; g0 += cap) {
     const int cnt = std::min(cap, nact - g0);
     upload_const(b.cstage + (size_t)g0 * cstride, (size_t)cnt * cstride, st);
+    ProfScope ps("dist", (double)cnt * b.m * (8.0 * b.p + 8.0));
     launch_dist(b.p, Z, b.m, blk_stride, b.inst_dev + g0, nstart, cnt, cstride, b.d2, st);
   }
 }
@@ -205,11 +278,17 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     if (act.empty()) break;
     const int na = (int)act.size();
     h2d(st, b.inst_dev, act.data(), na * sizeof(int));
-    launch_prepare(b.inst_dev, na, b.mu, b.sigma, p, kappa_max, b.cstage, cstride, b.logdet, b.cond, b.status, b.traj,
-                   b.traj_stride, step, st);
+    {
+      ProfScope ps("prepare", 0.0);
+      launch_prepare(b.inst_dev, na, b.mu, b.sigma, p, kappa_max, b.cstage, cstride, b.logdet, b.cond, b.status,
+                     b.traj, b.traj_stride, step, st);
+    }
     dist_groups(st, b, Z, blk_stride, nstart, na, cstride);
     RTD_CU(cudaMemsetAsync(b.changed, 0, ninst * sizeof(int), st));
-    launch_select(b.d2, m, h, b.inst_dev, na, b.sel, b.hist, memB, memA, b.changed, st);
+    {
+      ProfScope ps("select", (double)na * m * 9.0);
+      launch_select(b.d2, m, h, b.inst_dev, na, b.sel, b.hist, memB, memA, b.changed, st);
+    }
     std::swap(memA, memB);  // memA = membership of this step, memB = previous
     d2h(st, status_h.data(), b.status, ninst * sizeof(int));
     d2h(st, changed.data(), b.changed, ninst * sizeof(int));
@@ -229,12 +308,14 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     if (!dense.empty()) {
       h2d(st, b.inst_dev, dense.data(), dense.size() * sizeof(int));
       launch_copy_vec(b.inst_dev, (int)dense.size(), b.mu, b.shift, p, st);
+      ProfScope ps("moments_dense", (double)dense.size() * m * (8.0 * p + 1.0));
       launch_moments(MOM_MEMBER, ma, (int)dense.size(), st);
       launch_mom_reduce(b.partial, (int)dense.size(), b.inst_dev, b.ctas, np, b.sums, 0, st);
       launch_sums_to_cov(b.inst_dev, (int)dense.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
     }
     if (!upd.empty()) {
       h2d(st, b.inst_dev, upd.data(), upd.size() * sizeof(int));
+      ProfScope ps("moments_delta", (double)upd.size() * m * 2.0);
       launch_moments(MOM_DELTA, ma, (int)upd.size(), st);
       launch_mom_reduce(b.partial, (int)upd.size(), b.inst_dev, b.ctas, np, b.sums, 1, st);
       launch_sums_to_cov(b.inst_dev, (int)upd.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
@@ -254,6 +335,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     h2d(st, b.inst_dev, fin.data(), fin.size() * sizeof(int));
     ma.mem_new = b.memA;
     launch_copy_vec(b.inst_dev, (int)fin.size(), b.mu, b.shift, p, st);
+    ProfScope ps("moments_dense", (double)fin.size() * m * (8.0 * p + 1.0));
     launch_moments(MOM_MEMBER, ma, (int)fin.size(), st);
     launch_mom_reduce(b.partial, (int)fin.size(), b.inst_dev, b.ctas, np, b.sums, 0, st);
     launch_sums_to_cov(b.inst_dev, (int)fin.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
@@ -294,7 +376,10 @@ bool refine_from_V(cudaStream_t st, RefineBufs& r, const double* Zb, long long m
                    double* mu_out, double* sig_out) {
   // T = Z V -> D~ = diag(sigma_uni^2(T_j))
   upload_const(Vdev, (size_t)p * p, st);
-  launch_matmul(p, Zb, m, r.T, st);
+  {
+    ProfScope ps("matmul", (double)m * p * 16.0);
+    launch_matmul(p, Zb, m, r.T, st);
+  }
   run_unimcd(st, r.uscratch, r.uscratch_bytes, r.T, m, p, r.uni);
   std::vector<UniOut> u(p);
   d2h(st, u.data(), r.uni, p * sizeof(UniOut));
@@ -306,7 +391,10 @@ bool refine_from_V(cudaStream_t st, RefineBufs& r, const double* Zb, long long m
   launch_vdv(Vdev, r.d, 1, p, 2, r.Sh, st);
   // Z~ = Z Sigma^-1/2 -> mu~ = mu_uni(Z~_j) -> mu0 = Sigma^1/2 mu~
   upload_const(r.Smh, (size_t)p * p, st);
-  launch_matmul(p, Zb, m, r.T, st);
+  {
+    ProfScope ps("matmul", (double)m * p * 16.0);
+    launch_matmul(p, Zb, m, r.T, st);
+  }
   run_unimcd(st, r.uscratch, r.uscratch_bytes, r.T, m, p, r.uni);
   d2h(st, u.data(), r.uni, p * sizeof(UniOut));
   for (int j = 0; j < p; j++)
@@ -358,6 +446,7 @@ void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int
   a.partial = b.partial;
   a.ctas = b.ctas;
   // S~1: covariance of the wrapped data (centred at the wrapped mean, n - 1)
+  ProfScope ps("initial", (double)q * m * p * 16.0);
   launch_moments(MOM_WRAP, a, q, st);
   launch_mom_reduce(b.partial, q, b.inst_dev, b.ctas, np, b.sums, 0, st);
   launch_sums_to_cov(b.inst_dev, q, b.sums, np, nullptr, p, (double)m, 1.0, b.mudummy, b.S1, st);
@@ -365,6 +454,7 @@ void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int
   launch_norms(Z, m, p, q, blk_stride, b.r, st);
   for (int l = 0; l < q; l++) {
     size_t bytes = b.sort_bytes;
+    count_sort();
     RTD_CU(cub::DeviceRadixSort::SortKeys(b.sort_tmp, bytes, b.r + (size_t)l * m, b.rs + (size_t)l * m, (int)m, 0, 64,
                                           st));
   }
@@ -497,7 +587,10 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     Xdev = f.Xd;
   }
   RTD_CU(cudaMemsetAsync(f.bad, 0xff, sizeof(unsigned long long), st));
-  launch_transpose(Xdev, n, p, d.log, f.Xc, f.bad, st);
+  {
+    ProfScope ps("transpose", (double)n * p * 16.0);
+    launch_transpose(Xdev, n, p, d.log, f.Xc, f.bad, st);
+  }
   unsigned long long bad = 0;
   d2h(st, &bad, f.bad, sizeof(bad));
   if (bad != ~0ull) throw Fail{RTD_E_NONFINITE, "row " + std::to_string(bad) + (d.log ? " is not finite and > 0" : " is not finite")};
@@ -510,7 +603,10 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     if (uni[j].status) throw Fail{RTD_E_DEGENERATE_COLUMN, "column " + std::to_string(j)};
 
   // partition + Z = (X - loc)/scale per block, column-major
-  launch_build_Z(f.Xc, Xdev, n, p, q, m, d.perm, o.seed, d.log, f.uni, f.Z, f.rowmap, st);
+  {
+    ProfScope ps("build_Z", (double)q * m * p * 16.0);
+    launch_build_Z(f.Xc, Xdev, n, p, q, m, d.perm, o.seed, d.log, f.uni, f.Z, f.rowmap, st);
+  }
 
   // H2, H3: S~1, S~2 per block
   run_initial(st, f.ib, f.Z, m, p, q, blk_stride);
@@ -612,7 +708,10 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     for (int b = 0; b < q; b++) blocks[b] = b;
     h2d(st, f.cb.inst_dev, blocks.data(), q * sizeof(int));
     upload_const(f.cb.cstage, cstride, st);
-    launch_dist(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, 0, f.cb.d2, st);
+    {
+      ProfScope ps("dist", (double)q * m * (8.0 * p + 8.0));
+      launch_dist(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, 0, f.cb.d2, st);
+    }
     // shift = mu_raw for every block
     for (int b = 0; b < q; b++)
       RTD_CU(cudaMemcpyAsync(f.cb.shift + (size_t)b * RTD_MAXP, f.mu_raw, RTD_MAXP * sizeof(double),
@@ -620,7 +719,10 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     MomArgs a = mom_args(f.cb, f.Z, blk_stride, 1);
     a.c2 = c2;
     const int np = mom_np(p);
-    launch_moments(MOM_REWEIGHT, a, q, st);
+    {
+      ProfScope ps("reweight", (double)q * m * (8.0 * p + 8.0));
+      launch_moments(MOM_REWEIGHT, a, q, st);
+    }
     launch_mom_reduce(f.cb.partial, q, f.cb.inst_dev, f.cb.ctas, np, f.sums_rw, 0, st);
     launch_pool_sums(f.sums_rw, q, np, f.pooled, st);
     std::vector<double> pooled(np);
@@ -645,7 +747,10 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     d2h(st, &stv, f.st1, sizeof(int));
     if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "reweighted scatter is not positive definite"};
     upload_const(f.cb.cstage, cstride, st);
-    if (want_flags) launch_flag(p, Xdev, n, d.log, c2, f.flags_d, f.rd2_d, st);
+    if (want_flags) {
+      ProfScope ps("flag", (double)n * (8.0 * p + 9.0));
+      launch_flag(p, Xdev, n, d.log, c2, f.flags_d, f.rd2_d, st);
+    }
   }
   // per-row weights and h-subset membership in original row order
   if (out && (out->weights || out->hsubset)) {
@@ -702,9 +807,15 @@ template <class F>
 rtdetmcd_status guarded(rtdetmcd_ctx* c, F&& fn) {
   if (!c) return RTD_E_INVALID_ARG;
   c->err.clear();
+  g_prof = &c->prof;
+  g_prof_stream = c->stream;
   try {
     RTD_CU(cudaSetDevice(c->device));
     fn();
+    if (c->prof.on) {
+      RTD_CU(cudaStreamSynchronize(c->stream));
+      c->prof.fold();
+    }
     return RTD_OK;
   } catch (const Fail& f) {
     c->err = f.msg;
@@ -860,7 +971,10 @@ rtdetmcd_status rtdetmcd_flag(rtdetmcd_ctx* c, const double* X, int64_t n, int32
     d2h(st, &stv, stt, sizeof(int));
     if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "sigma is not positive definite"};
     upload_const(cs, cstride, st);
-    launch_flag(p, Xd, n, log_transform ? 1 : 0, chi2_quantile(quantile, p), fh ? fd : flags, rh ? rdd : rd2, st);
+    {
+      ProfScope ps("flag", (double)n * (8.0 * p + 9.0));
+      launch_flag(p, Xd, n, log_transform ? 1 : 0, chi2_quantile(quantile, p), fh ? fd : flags, rh ? rdd : rd2, st);
+    }
     if (fh) RTD_CU(cudaMemcpyAsync(flags, fd, n, cudaMemcpyDeviceToHost, st));
     if (rh) RTD_CU(cudaMemcpyAsync(rd2, rdd, n * sizeof(double), cudaMemcpyDeviceToHost, st));
     RTD_CU(cudaStreamSynchronize(st));
@@ -1015,6 +1129,35 @@ rtdetmcd_status rtdetmcd_csteps(rtdetmcd_ctx* c, const double* Z, int64_t m, int
     if (hsubset) output_copy(st, hsubset, cb.memA, m);
     RTD_CU(cudaStreamSynchronize(st));
   });
+}
+
+rtdetmcd_status rtdetmcd_set_profiling(rtdetmcd_ctx* c, int32_t on) {
+  if (!c) return RTD_E_INVALID_ARG;
+  c->prof.on = on != 0;
+  c->prof.stats.clear();
+  c->prof.pending.clear();
+  return RTD_OK;
+}
+
+void rtdetmcd_counters(int64_t* kernels, int64_t* sorts) {
+  if (kernels) *kernels = launch_count();
+  if (sorts) *sorts = sort_count();
+}
+
+int32_t rtdetmcd_prof_count(const rtdetmcd_ctx* c) { return c ? (int32_t)c->prof.stats.size() : 0; }
+
+rtdetmcd_status rtdetmcd_prof_entry(const rtdetmcd_ctx* c, int32_t i, char* name, size_t name_len, double* ms_total,
+                                    int64_t* launches, double* bytes_total) {
+  if (!c || i < 0 || i >= (int32_t)c->prof.stats.size()) return RTD_E_INVALID_ARG;
+  const auto& e = c->prof.stats[i];
+  if (name && name_len) {
+    strncpy(name, e.first.c_str(), name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (ms_total) *ms_total = e.second.ms;
+  if (launches) *launches = e.second.launches;
+  if (bytes_total) *bytes_total = e.second.bytes;
+  return RTD_OK;
 }
 
 double rtdetmcd_chi2_quantile(double prob, int32_t dof) { return chi2_quantile(prob, dof); }

@@ -7,9 +7,16 @@
 // Lentz continued fraction above); the quantile is found by bisection to the
 // last representable double.
 #include <cmath>
+#include <atomic>
 #include <cstdlib>
 
 namespace rtd {
+
+static std::atomic<long long> g_launches{0}, g_sorts{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_sort() { g_sorts.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
+long long sort_count() { return g_sorts.load(); }
 
 bool debug_sync() {
   static int v = -1;

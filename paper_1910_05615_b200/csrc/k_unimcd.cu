@@ -270,6 +270,8 @@ __global__ void __launch_bounds__(UTH) k_uni_final(const double* __restrict__ so
 
 struct UniScratch {
   double* sorted;
+  double* tmpk;
+  uint8_t *ids, *tmpid, *idout;
   dd2* csum;
   dd2* coff;
   WinPartial* part;
@@ -277,30 +279,67 @@ struct UniScratch {
   size_t cub_bytes;
 };
 
-static size_t cub_sort_bytes(long long len) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const double*)nullptr, (double*)nullptr, (int)len);
-  return bytes;
+__global__ void k_fill_colid(uint8_t* __restrict__ ids, long long len, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x)
+    ids[i] = (uint8_t)(i / len);
+}
+
+static int id_bits(int ncols) {
+  int b = 1;
+  while ((1 << b) < ncols) b++;
+  return b;
+}
+
+// All ncols columns are sorted with two device-wide radix sorts instead of
+// ncols small ones: (value -> column id) by the fp64 key, then a stable sort
+// by column id, which leaves every column sorted and contiguous.
+static size_t cub_sort_bytes(long long len, int ncols) {
+  const long long N = len * ncols;
+  size_t b1 = 0, b2 = 0;
+  if (ncols == 1) {
+    cub::DeviceRadixSort::SortKeys(nullptr, b1, (const double*)nullptr, (double*)nullptr, (int)N);
+    return b1;
+  }
+  cub::DeviceRadixSort::SortPairs(nullptr, b1, (const double*)nullptr, (double*)nullptr, (const uint8_t*)nullptr,
+                                  (uint8_t*)nullptr, (int)N);
+  cub::DeviceRadixSort::SortPairs(nullptr, b2, (const uint8_t*)nullptr, (uint8_t*)nullptr, (const double*)nullptr,
+                                  (double*)nullptr, (int)N, 0, id_bits(ncols));
+  return std::max(b1, b2);
 }
 
 void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, int ncols, UniConst uc,
                   UniOut* out_dev) {
+  if (ncols > 256) throw std::string("unimcd_batch: at most 256 columns per call");
   const long long h = len / 2 + 1;
   const int nchunks = (int)((len + UCH - 1) / UCH);
   const long long nwin = len - h + 1;
   const int nwchunks = (int)((nwin + UCH - 1) / UCH);
+  const long long N = len * ncols;
   UniScratch s;
-  s.sorted = A.take<double>((size_t)ncols * len);
+  s.sorted = A.take<double>((size_t)N);
+  s.tmpk = ncols > 1 ? A.take<double>((size_t)N) : nullptr;
+  s.ids = ncols > 1 ? A.take<uint8_t>((size_t)N) : nullptr;
+  s.tmpid = ncols > 1 ? A.take<uint8_t>((size_t)N) : nullptr;
+  s.idout = ncols > 1 ? A.take<uint8_t>((size_t)N) : nullptr;
   s.csum = A.take<dd2>((size_t)ncols * nchunks);
   s.coff = A.take<dd2>((size_t)ncols * (nchunks + 1));
   s.part = A.take<WinPartial>((size_t)ncols * nwchunks);
-  s.cub_bytes = cub_sort_bytes(len);
+  s.cub_bytes = cub_sort_bytes(len, ncols);
   s.cub_tmp = A.take<char>(s.cub_bytes);
   if (A.base == nullptr) return;  // dry run
-  for (int j = 0; j < ncols; j++) {
-    size_t bytes = s.cub_bytes;
-    RTD_CU(cub::DeviceRadixSort::SortKeys(s.cub_tmp, bytes, cols + (long long)j * len, s.sorted + (long long)j * len,
-                                          (int)len, 0, 64, st));
+  size_t bytes = s.cub_bytes;
+  if (ncols == 1) {
+    count_sort();
+    RTD_CU(cub::DeviceRadixSort::SortKeys(s.cub_tmp, bytes, cols, s.sorted, (int)N, 0, 64, st));
+  } else {
+    k_fill_colid<<<(unsigned)std::min<long long>((N + 255) / 256, 148 * 16), 256, 0, st>>>(s.ids, len, N);
+    RTD_LAUNCHED();
+    count_sort();
+    RTD_CU(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, cols, s.tmpk, s.ids, s.tmpid, (int)N, 0, 64, st));
+    bytes = s.cub_bytes;
+    count_sort();
+    RTD_CU(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.tmpid, s.idout, s.tmpk, s.sorted, (int)N, 0,
+                                           id_bits(ncols), st));
   }
   k_uni_chunksum<<<dim3(nchunks, ncols), UTH, 0, st>>>(s.sorted, len, nchunks, s.csum);
   RTD_LAUNCHED();

@@ -21,8 +21,11 @@ struct CudaError {
     if (e__ != cudaSuccess) throw ::rtd::CudaError{e__, #x};              \
   } while (0)
 bool debug_sync();  // RTD_DEBUG_SYNC=1: synchronise and check after every launch
+void count_launch();  // kernels launched by this library (hand-written kernels)
+void count_sort();    // CUB radix-sort invocations
 #define RTD_LAUNCHED()                                                      \
   do {                                                                      \
+    ::rtd::count_launch();                                                  \
     RTD_CU(cudaGetLastError());                                             \
     if (::rtd::debug_sync()) {                                              \
       cudaError_t e2__ = cudaDeviceSynchronize();                           \
