@@ -15,6 +15,9 @@
 #include "rtd_linalg.h"
 
 namespace rtd {
+bool dist_mma_supported(int p);
+void launch_dist_mma(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
+                     int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st);
 long long launch_count();
 long long sort_count();
 void launch_feistel_fwd(long long n, unsigned long long seed, long long* out, cudaStream_t st);
@@ -244,6 +247,11 @@ MomArgs mom_args(const CStepBufs& b, const double* Z, long long blk_stride, int 
 // upload distance operators of instances act[g0, g0+cnt) (staged in cstage slots) and run the distance pass
 void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long blk_stride, int nstart, int nact,
                  int cstride) {
+  if (dist_mma_supported(b.p)) {  // FP64 tensor-pipe kernel: operator read from cstage, all instances at once
+    ProfScope ps("dist", (double)nact * b.m * (8.0 * b.p + 8.0));
+    launch_dist_mma(b.p, Z, b.m, blk_stride, b.inst_dev, nstart, nact, b.cstage, cstride, b.d2, st);
+    return;
+  }
   const int cap = std::max(1, RTD_CONST_DOUBLES / std::max(1, cstride));
   for (int g0 = 0; g0 < nact; g0 += cap) {
     const int cnt = std::min(cap, nact - g0);
@@ -707,10 +715,14 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     std::vector<int> blocks(q);
     for (int b = 0; b < q; b++) blocks[b] = b;
     h2d(st, f.cb.inst_dev, blocks.data(), q * sizeof(int));
-    upload_const(f.cb.cstage, cstride, st);
     {
       ProfScope ps("dist", (double)q * m * (8.0 * p + 8.0));
-      launch_dist(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, 0, f.cb.d2, st);
+      if (dist_mma_supported(p)) {
+        launch_dist_mma(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, f.cb.cstage, 0, f.cb.d2, st);
+      } else {
+        upload_const(f.cb.cstage, cstride, st);
+        launch_dist(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, 0, f.cb.d2, st);
+      }
     }
     // shift = mu_raw for every block
     for (int b = 0; b < q; b++)

@@ -1,0 +1,130 @@
+// H6 on the FP64 tensor pipe: the C-step distance pass as a small dense
+// contraction Y = (Z - mu) M^T with DMMA (mma.sync m8n8k4 f64), then
+// d_i^2 = ||Y_i||^2 (§3.4).
+//
+// Measured on this B200 (tools/fp64_peak.cu): DMMA 37.0 TF/s vs DFMA 33.6 TF/s,
+// and the two share one FP64 pipe.  At p = 40 the pass needs 5.4 flop per byte
+// of X, at the FP64 ridge, so instruction issue decides: one DMMA does 256 FMA
+// where a DFMA does 32, and the operator M = L^-1 (lower triangular) lives in
+// registers as B fragments for the whole kernel.  Blocks of M^T that are
+// entirely above the diagonal are skipped (30 of 50 8x4 blocks at p = 40).
+//
+// Fragment layout of m8n8k4 f64 (g = lane >> 2, t = lane & 3):
+//   A (8 x 4, rows x k):  A[g][t]          -> (Z - mu)[row0 + g][4 kb + t]
+//   B (4 x 8, k x n):     B[t][g]          -> M[8 nb + g][4 kb + t]
+//   C (8 x 8):            C[g][2t], C[g][2t+1]
+#include "rtd_internal.h"
+
+namespace rtd {
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int P, int MB>
+__global__ void __launch_bounds__(256) k_dist_mma(const double* __restrict__ Zall, long long m, long long blk_stride,
+                                                  const int* __restrict__ inst, int nstart,
+                                                  const double* __restrict__ cstage, int cstride,
+                                                  double* __restrict__ d2_all) {
+  constexpr int KB = (P + 3) / 4;
+  constexpr int NB = (P + 7) / 8;
+  const int slot = blockIdx.y;
+  const int id = inst[slot];
+  const double* __restrict__ Z = Zall + (long long)(id / nstart) * blk_stride;
+  double* __restrict__ d2 = d2_all + (long long)id * m;
+  const double* __restrict__ cs = cstage + (long long)slot * cstride;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  // operator fragments, resident for the whole kernel
+  double bf[KB][NB];
+  double mu[KB];
+#pragma unroll
+  for (int kb = 0; kb < KB; kb++) {
+    const int k = 4 * kb + t;
+    mu[kb] = k < P ? cs[k] : 0.0;
+#pragma unroll
+    for (int nb = 0; nb < NB; nb++) {
+      const int j = 8 * nb + g;
+      bf[kb][nb] = (j < P && k <= j) ? cs[P + j * (j + 1) / 2 + k] : 0.0;
+    }
+  }
+  const long long rows_per_tile = 8 * MB;
+  const long long ntiles = (m + rows_per_tile - 1) / rows_per_tile;
+  const long long warp0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long tile = warp0; tile < ntiles; tile += nwarps) {
+    const long long r0 = tile * rows_per_tile;
+    double acc[MB][NB][2];
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < KB; kb++) {
+      const int k = 4 * kb + t;
+      double a[MB];
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++) {
+        const long long row = r0 + mb * 8 + g;
+        a[mb] = (k < P && row < m) ? __dsub_rn(Z[(long long)k * m + row], mu[kb]) : 0.0;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        if (8 * nb + 7 < 4 * kb) continue;  // block entirely above the diagonal of M
+#pragma unroll
+        for (int mb = 0; mb < MB; mb++) dmma_8x8x4(acc[mb][nb][0], acc[mb][nb][1], a[mb], bf[kb][nb]);
+      }
+    }
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++) {
+      double s = 0.0;
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        s = fma(acc[mb][nb][0], acc[mb][nb][0], s);
+        s = fma(acc[mb][nb][1], acc[mb][nb][1], s);
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      const long long row = r0 + mb * 8 + g;
+      if (t == 0 && row < m) d2[row] = s;
+    }
+  }
+}
+
+template <int P>
+static void dist_mma_launch(const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
+                            int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st) {
+  constexpr int MB = P <= 24 ? 4 : 2;
+  const long long tiles = (m + 8 * MB - 1) / (8 * MB);
+  const long long need = (tiles + 7) / 8;  // 8 warps per CTA
+  const long long cap = std::max<long long>(1, 148LL * 4 / std::max(1, ninst));
+  k_dist_mma<P, MB><<<dim3((unsigned)std::min(need, cap), ninst), 256, 0, st>>>(Zall, m, blk_stride, inst, nstart,
+                                                                                 cstage, cstride, d2_all);
+}
+
+#define RTD_DISPATCH_P8(p, F, ...)                                                                          \
+  switch (p) {                                                                                           \
+    case 8: F<8>(__VA_ARGS__); break; case 9: F<9>(__VA_ARGS__); break; case 10: F<10>(__VA_ARGS__); break; \
+    case 11: F<11>(__VA_ARGS__); break; case 12: F<12>(__VA_ARGS__); break; case 13: F<13>(__VA_ARGS__); break; \
+    case 14: F<14>(__VA_ARGS__); break; case 15: F<15>(__VA_ARGS__); break; case 16: F<16>(__VA_ARGS__); break; \
+    case 17: F<17>(__VA_ARGS__); break; case 18: F<18>(__VA_ARGS__); break; case 19: F<19>(__VA_ARGS__); break; \
+    case 20: F<20>(__VA_ARGS__); break; case 21: F<21>(__VA_ARGS__); break; case 22: F<22>(__VA_ARGS__); break; \
+    case 23: F<23>(__VA_ARGS__); break; case 24: F<24>(__VA_ARGS__); break; case 25: F<25>(__VA_ARGS__); break; \
+    case 26: F<26>(__VA_ARGS__); break; case 27: F<27>(__VA_ARGS__); break; case 28: F<28>(__VA_ARGS__); break; \
+    case 29: F<29>(__VA_ARGS__); break; case 30: F<30>(__VA_ARGS__); break; case 31: F<31>(__VA_ARGS__); break; \
+    case 32: F<32>(__VA_ARGS__); break; case 33: F<33>(__VA_ARGS__); break; case 34: F<34>(__VA_ARGS__); break; \
+    case 35: F<35>(__VA_ARGS__); break; case 36: F<36>(__VA_ARGS__); break; case 37: F<37>(__VA_ARGS__); break; \
+    case 38: F<38>(__VA_ARGS__); break; case 39: F<39>(__VA_ARGS__); break; case 40: F<40>(__VA_ARGS__); break; \
+    default: throw std::string("dist_mma: p out of range");                                               \
+  }
+
+bool dist_mma_supported(int p) { return p >= 8 && p <= RTD_MAXP; }
+
+void launch_dist_mma(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
+                     int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st) {
+  RTD_DISPATCH_P8(p, dist_mma_launch, Zall, m, blk_stride, inst, nstart, ninst, cstage, cstride, d2_all, st);
+  RTD_LAUNCHED();
+}
+
+}  // namespace rtd
