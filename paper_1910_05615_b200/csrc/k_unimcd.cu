@@ -11,9 +11,14 @@
 // prefix streams it needs (P(s) and P(s+h)) from per-chunk totals.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <cstdlib>
+
 #include "rtd_internal.h"
 
 namespace rtd {
+
+bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len, int ncols, UniConst uc,
+                   UniOut* out_dev);
 
 static constexpr int UCH = 1024;   // elements per chunk
 static constexpr int UTH = 256;    // threads per CTA (4 elements each)
@@ -326,6 +331,14 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
   s.part = A.take<WinPartial>((size_t)ncols * nwchunks);
   s.cub_bytes = cub_sort_bytes(len, ncols);
   s.cub_tmp = A.take<char>(s.cub_bytes);
+  // Large columns: exact window by bucketing + bounds (k_unimcd_pruned.cu); the
+  // sort path below is the fallback and the small-n path.
+  static const bool force_sort = getenv("RTD_UNI_FULLSORT") != nullptr;
+  if (len >= (1LL << 16) && !force_sort) {
+    const bool done = unimcd_pruned(A, st, cols, len, ncols, uc, out_dev);
+    if (A.base == nullptr) return;  // dry run (both paths measured)
+    if (done) return;
+  }
   if (A.base == nullptr) return;  // dry run
   size_t bytes = s.cub_bytes;
   if (ncols == 1) {

@@ -62,6 +62,32 @@ def test_unimcd_exact_ties_and_symmetry():
         assert g["scale"][0] == pytest.approx(o.scale, rel=1e-13)
 
 
+def _uni_columns(n, seed):
+    rng = np.random.default_rng(seed)
+    cols = [rng.standard_normal(n),                                     # clean
+            np.concatenate([rng.standard_normal(n - n // 5), 8 + 0.01 * rng.standard_normal(n // 5)]),
+            rng.exponential(size=n) * 3 - 1,                            # skewed
+            rng.standard_t(2, size=n),                                  # heavy tails
+            np.concatenate([0.001 * rng.standard_normal(int(0.45 * n)), rng.standard_normal(n - int(0.45 * n))]),
+            rng.integers(0, 50, size=n).astype(np.float64),             # heavy ties (fallback path)
+            1e6 + rng.standard_normal(n)]                               # large offset
+    return np.stack([rng.permutation(c) for c in cols])
+
+
+@pytest.mark.parametrize("n", [65_536, 200_001, 1_000_000])
+def test_unimcd_large_columns(n):
+    """Sizes that take the bucket-and-bound path (n >= 2^16) and its fallback."""
+    cols = _uni_columns(n, n)
+    g = api.unimcd(_cuda(cols))
+    for j in range(cols.shape[0]):
+        o = unimcd_reweighted(cols[j])
+        assert g["start"][j] == o.raw.start, j
+        assert g["raw_loc"][j] == pytest.approx(o.raw.loc, rel=1e-15, abs=1e-300), j
+        assert g["raw_var"][j] == pytest.approx(o.raw.var_raw, rel=1e-13), j
+        assert g["loc"][j] == pytest.approx(o.loc, rel=1e-14, abs=1e-14), j
+        assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13), j
+
+
 def test_unimcd_degenerate_column_errors():
     x = np.ones((1, 100))
     with pytest.raises(api.RTDError) as e:
