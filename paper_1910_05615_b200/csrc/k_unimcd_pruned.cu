@@ -327,14 +327,58 @@ __device__ __forceinline__ int rank_bucket(const long long* C, long long r) {  /
   return lo;
 }
 
-// 3b. bounds for every start s; pass 0: per-CTA min of the upper bounds, pass 1: per-CTA candidate range
+// partial-bucket sums of one window start s (start bucket b, end bucket be), see window_bounds
+struct PartBounds {
+  double t1lo, t1hi, t2lo, t2hi;
+};
+__device__ __forceinline__ PartBounds part_bounds(long long s, long long h, int b, int be, const PrunedCol& c,
+                                                  const long long* C, const int* cn, const double* sb) {
+  const double L1 = bucket_lo(b, c), U1 = bucket_hi(b, c), L2 = bucket_lo(be, c), U2 = bucket_hi(be, c);
+  const double n1 = (double)cn[b], n2 = (double)cn[be];
+  const double Sb = sb[b], Se = sb[be];
+  const double r1 = (double)(C[b + 1] - s), r2 = (double)(s + h - C[be]);
+  const double a = fmax(r1 * L1, r1 * Sb / n1), bb = fmin(r1 * U1, Sb - (n1 - r1) * L1);
+  const double d = fmax(r2 * L2, Se - (n2 - r2) * U2), e = fmin(r2 * U2, r2 * Se / n2);
+  return {fmin(a, bb), fmax(a, bb), fmin(d, e), fmax(d, e)};
+}
+
+// Lower bound of h*SQ(s) valid for every s in [sa, sb] (same b, be, b != be): the partial
+// sums are monotone in s (t1 decreases, t2 increases), so the extremes come from the endpoints.
+__device__ __forceinline__ double chunk_lower(long long sa, long long sb, long long h, int b, int be,
+                                              const PrunedCol& c, const long long* C, const double* A1,
+                                              const double* Q2lo, const int* cn, const double* sbk, BucketScan m) {
+  const double hd = (double)h;
+  const PartBounds pa = part_bounds(sa, h, b, be, c, C, cn, sbk), pb = part_bounds(sb, h, b, be, c, C, cn, sbk);
+  const double F1 = A1[be] - A1[b + 1];
+  const double lo1 = F1 + fmin(pa.t1lo, pb.t1lo) + fmin(pa.t2lo, pb.t2lo) - m.E1;
+  const double hi1 = F1 + fmax(pa.t1hi, pb.t1hi) + fmax(pa.t2hi, pb.t2hi) + m.E1;
+  const double L1 = bucket_lo(b, c), U1 = bucket_hi(b, c), L2 = bucket_lo(be, c), U2 = bucket_hi(be, c);
+  const double mn1 = (L1 <= 0 && U1 >= 0) ? 0.0 : fmin(L1 * L1, U1 * U1);
+  const double mn2 = (L2 <= 0 && U2 >= 0) ? 0.0 : fmin(L2 * L2, U2 * U2);
+  double lo2 = INFINITY;
+  for (int k = 0; k < 2; k++) {
+    const long long s = k ? sb : sa;
+    lo2 = fmin(lo2, (Q2lo[be] - Q2lo[b + 1]) + (double)(C[b + 1] - s) * mn1 + (double)(s + h - C[be]) * mn2);
+  }
+  lo2 -= m.E2;
+  const double sq_hi_1 = fmax(lo1 * lo1, hi1 * hi1);
+  const double slack = 1e-9 * (hd * fabs(lo2) + sq_hi_1) + 1e-300;
+  return hd * lo2 - sq_hi_1 - slack;
+}
+
+static constexpr int CHUNK = 32;  // starts per chunk in the coarse lower-bound pass
+
+// 3b. mode 0: upper bounds on a stride-CHUNK subset of starts (any subset gives a valid bound on the
+//             minimum) -> per-CTA minimum;
+//     mode 1: chunk lower bounds over all starts -> per-CTA range of candidate chunks;
+//     mode 2: per-start lower bounds inside the candidate chunk range -> per-CTA candidate range.
 __global__ void __launch_bounds__(PT) k_pr_bound(long long len, long long h, const PrunedCol* __restrict__ pc,
                                                  const int* __restrict__ cnt, const double* __restrict__ s1,
                                                  const long long* __restrict__ Cg, const double* __restrict__ A1g,
                                                  const double* __restrict__ Q2log, const double* __restrict__ Q2hig,
-                                                 const BucketScan* __restrict__ bsc, int pass,
-                                                 const double* __restrict__ best_ub, double* __restrict__ ub_part,
-                                                 long long* __restrict__ range_part) {
+                                                 const BucketScan* __restrict__ bsc, int mode,
+                                                 const double* __restrict__ best_ub, const long long* __restrict__ crange,
+                                                 double* __restrict__ ub_part, long long* __restrict__ range_part) {
   __shared__ double rd[PT / 32];
   __shared__ long long ra[PT / 32], rb[PT / 32];
   const int col = blockIdx.y;
@@ -345,31 +389,56 @@ __global__ void __launch_bounds__(PT) k_pr_bound(long long len, long long h, con
   const double* Q2lo = Q2log + (long long)col * (NBK + 1);
   const double* Q2hi = Q2hig + (long long)col * (NBK + 1);
   const int* cn = cnt + (long long)col * NBK;
-  const double* sb = s1 + (long long)col * NBK;
+  const double* sbk = s1 + (long long)col * NBK;
   const BucketScan m = bsc[col];
   const long long nwin = len - h + 1;
+  const long long gtid = (long long)blockIdx.x * PT + threadIdx.x;
   const long long nthreads = (long long)gridDim.x * PT;
-  const long long per = (nwin + nthreads - 1) / nthreads;
-  const long long s0 = ((long long)blockIdx.x * PT + threadIdx.x) * per, s1e = min(nwin, s0 + per);
-  const double bub = pass ? best_ub[col] : 0.0;
+  const double bub = mode ? best_ub[col] : 0.0;
   double ub = INFINITY;
   long long cmin = 0x7fffffffffffffffLL, cmax = -1;
-  if (s0 < s1e) {
-    int b = rank_bucket(C, s0), be = rank_bucket(C, s0 + h - 1);
-    for (long long s = s0; s < s1e; s++) {
-      while (C[b + 1] <= s) b++;
-      while (C[be + 1] <= s + h - 1) be++;
-      const VBound v = window_bounds(s, h, b, be, c, C, A1, Q2lo, Q2hi, cn, sb, m);
-      if (pass == 0) {
-        ub = fmin(ub, v.hi);
-      } else if (v.lo <= bub) {
-        cmin = min(cmin, s);
-        cmax = max(cmax, s);
+  if (mode == 0) {
+    for (long long s = gtid * CHUNK; s < nwin; s += nthreads * CHUNK) {
+      const int b = rank_bucket(C, s), be = rank_bucket(C, s + h - 1);
+      ub = fmin(ub, window_bounds(s, h, b, be, c, C, A1, Q2lo, Q2hi, cn, sbk, m).hi);
+    }
+  } else if (mode == 1) {
+    const long long nchunks = (nwin + CHUNK - 1) / CHUNK;
+    for (long long ch = gtid; ch < nchunks; ch += nthreads) {
+      const long long s0 = ch * CHUNK, s1e = min(nwin, s0 + CHUNK);
+      long long sa = s0;
+      while (sa < s1e) {
+        const int b = rank_bucket(C, sa), be = rank_bucket(C, sa + h - 1);
+        const long long sb = min(min(s1e, C[b + 1]), C[be + 1] - h + 1) - 1;  // same (b, be) on [sa, sb]
+        const double lo = (b == be) ? -INFINITY : chunk_lower(sa, sb, h, b, be, c, C, A1, Q2lo, cn, sbk, m);
+        if (lo <= bub) {
+          cmin = min(cmin, sa);
+          cmax = max(cmax, sb);
+        }
+        sa = sb + 1;
+      }
+    }
+  } else {
+    const long long lo_s = crange[2 * col], hi_s = crange[2 * col + 1];
+    if (lo_s <= hi_s) {
+      const long long cnt_s = hi_s - lo_s + 1;
+      const long long per = (cnt_s + nthreads - 1) / nthreads;
+      const long long s0 = lo_s + gtid * per, s1e = min(hi_s + 1, s0 + per);
+      if (s0 < s1e) {
+        int b = rank_bucket(C, s0), be = rank_bucket(C, s0 + h - 1);
+        for (long long s = s0; s < s1e; s++) {
+          while (C[b + 1] <= s) b++;
+          while (C[be + 1] <= s + h - 1) be++;
+          if (window_bounds(s, h, b, be, c, C, A1, Q2lo, Q2hi, cn, sbk, m).lo <= bub) {
+            cmin = min(cmin, s);
+            cmax = max(cmax, s);
+          }
+        }
       }
     }
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (pass == 0) {
+  if (mode == 0) {
     for (int d = 16; d > 0; d >>= 1) ub = fmin(ub, __shfl_down_sync(0xffffffffu, ub, d));
     if (lane == 0) rd[w] = ub;
     __syncthreads();
@@ -407,18 +476,27 @@ __global__ void k_pr_ubmin(const PrunedCol* __restrict__ pc, const double* __res
   best_ub[col] = ub;
 }
 
-// 3c. candidate range -> gathered bucket ranges
-__global__ void k_pr_cand(long long len, long long h, PrunedCol* __restrict__ pc, const long long* __restrict__ Cg,
-                          const long long* __restrict__ range_part, int nb) {
+__global__ void k_pr_range(const PrunedCol* __restrict__ pc, const long long* __restrict__ range_part, int nb,
+                           long long* __restrict__ crange) {
   const int col = blockIdx.x;
-  PrunedCol c = pc[col];
-  if (c.status || threadIdx.x != 0) return;
-  const long long* C = Cg + (long long)col * (NBK + 1);
+  if (pc[col].status || threadIdx.x != 0) return;
   long long smin = 0x7fffffffffffffffLL, smax = -1;
   for (int k = 0; k < nb; k++) {
     smin = min(smin, range_part[((long long)col * nb + k) * 2]);
     smax = max(smax, range_part[((long long)col * nb + k) * 2 + 1]);
   }
+  crange[2 * col] = smin;
+  crange[2 * col + 1] = smax;
+}
+
+// 3c. candidate range -> gathered bucket ranges
+__global__ void k_pr_cand(long long len, long long h, PrunedCol* __restrict__ pc, const long long* __restrict__ Cg,
+                          const long long* __restrict__ crange) {
+  const int col = blockIdx.x;
+  PrunedCol c = pc[col];
+  if (c.status || threadIdx.x != 0) return;
+  const long long* C = Cg + (long long)col * (NBK + 1);
+  const long long smin = crange[2 * col], smax = crange[2 * col + 1];
   c.smin = smin;
   c.smax = smax;
   if (smax < smin) {
@@ -674,6 +752,7 @@ struct PrScratch {
   double *A1, *Q2lo, *Q2hi, *ub_part, *best_ub;
   BucketScan* bsc;
   long long* range_part;
+  long long* crange;
   int nbound;
 };
 
@@ -711,6 +790,7 @@ static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.ub_part = A.take<double>((size_t)ncols * s.nbound);
   s.best_ub = A.take<double>(ncols);
   s.range_part = A.take<long long>((size_t)ncols * s.nbound * 2);
+  s.crange = A.take<long long>((size_t)ncols * 2);
 }
 
 // Returns true when every column was resolved by the pruned path (out_dev filled);
@@ -731,15 +811,15 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   RTD_LAUNCHED();
   k_pr_scan<<<ncols, 1024, 0, st>>>(s.pc, s.cnt, s.s1, s.mm, s.C, s.A1, s.Q2lo, s.Q2hi, s.bsc);
   RTD_LAUNCHED();
-  k_pr_bound<<<dim3(s.nbound, ncols), PT, 0, st>>>(len, h, s.pc, s.cnt, s.s1, s.C, s.A1, s.Q2lo, s.Q2hi, s.bsc, 0,
-                                                    s.best_ub, s.ub_part, s.range_part);
-  RTD_LAUNCHED();
-  k_pr_ubmin<<<ncols, 32, 0, st>>>(s.pc, s.ub_part, s.nbound, s.best_ub);
-  RTD_LAUNCHED();
-  k_pr_bound<<<dim3(s.nbound, ncols), PT, 0, st>>>(len, h, s.pc, s.cnt, s.s1, s.C, s.A1, s.Q2lo, s.Q2hi, s.bsc, 1,
-                                                    s.best_ub, s.ub_part, s.range_part);
-  RTD_LAUNCHED();
-  k_pr_cand<<<ncols, 32, 0, st>>>(len, h, s.pc, s.C, s.range_part, s.nbound);
+  for (int mode = 0; mode < 3; mode++) {
+    k_pr_bound<<<dim3(s.nbound, ncols), PT, 0, st>>>(len, h, s.pc, s.cnt, s.s1, s.C, s.A1, s.Q2lo, s.Q2hi, s.bsc,
+                                                      mode, s.best_ub, s.crange, s.ub_part, s.range_part);
+    RTD_LAUNCHED();
+    if (mode == 0) k_pr_ubmin<<<ncols, 32, 0, st>>>(s.pc, s.ub_part, s.nbound, s.best_ub);
+    else k_pr_range<<<ncols, 32, 0, st>>>(s.pc, s.range_part, s.nbound, s.crange);
+    RTD_LAUNCHED();
+  }
+  k_pr_cand<<<ncols, 32, 0, st>>>(len, h, s.pc, s.C, s.crange);
   RTD_LAUNCHED();
   k_pr_gather<<<dim3(PCTA, ncols), PT, 0, st>>>(cols, len, s.pc, s.g, s.gcount, s.below);
   RTD_LAUNCHED();
