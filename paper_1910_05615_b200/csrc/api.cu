@@ -20,6 +20,8 @@ void launch_dist_mma(int p, const double* Zall, long long m, long long blk_strid
                      int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st);
 long long launch_count();
 long long sort_count();
+void launch_moments_mma(int mode, const MomArgs& a, int ninst, cudaStream_t st);
+void launch_matmul_mma(int p, const double* Z, long long m, const double* W, double* out, cudaStream_t st);
 void launch_feistel_fwd(long long n, unsigned long long seed, long long* out, cudaStream_t st);
 void launch_uni_extract(const UniOut* uni, int p, int which, double* out, cudaStream_t st);
 void launch_scatter_u8(const uint8_t* src, const long long* rowmap, long long total, uint8_t* dst, cudaStream_t st);
@@ -31,6 +33,16 @@ void launch_hsub_from_mem(const uint8_t* mem_all, const int* chosen_inst, int q,
 }  // namespace rtd
 
 using namespace rtd;
+
+// FP64 tensor-pipe kernels unless RTD_SIMT=1 (the DFMA kernels stay for comparison)
+static bool use_mma() {
+  static const bool v = getenv("RTD_SIMT") == nullptr;
+  return v;
+}
+static void moments(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
+  if (use_mma()) launch_moments_mma(mode, a, ninst, st);
+  else launch_moments(mode, a, ninst, st);
+}
 
 // ------------------------------------------------------------------ optional per-kernel-class timing
 // When profiling is on, each timed region records a CUDA event pair on the
@@ -317,14 +329,14 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
       h2d(st, b.inst_dev, dense.data(), dense.size() * sizeof(int));
       launch_copy_vec(b.inst_dev, (int)dense.size(), b.mu, b.shift, p, st);
       ProfScope ps("moments_dense", (double)dense.size() * m * (8.0 * p + 1.0));
-      launch_moments(MOM_MEMBER, ma, (int)dense.size(), st);
+      moments(MOM_MEMBER, ma, (int)dense.size(), st);
       launch_mom_reduce(b.partial, (int)dense.size(), b.inst_dev, b.ctas, np, b.sums, 0, st);
       launch_sums_to_cov(b.inst_dev, (int)dense.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
     }
     if (!upd.empty()) {
       h2d(st, b.inst_dev, upd.data(), upd.size() * sizeof(int));
       ProfScope ps("moments_delta", (double)upd.size() * m * 2.0);
-      launch_moments(MOM_DELTA, ma, (int)upd.size(), st);
+      moments(MOM_DELTA, ma, (int)upd.size(), st);
       launch_mom_reduce(b.partial, (int)upd.size(), b.inst_dev, b.ctas, np, b.sums, 1, st);
       launch_sums_to_cov(b.inst_dev, (int)upd.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
     }
@@ -344,7 +356,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     ma.mem_new = b.memA;
     launch_copy_vec(b.inst_dev, (int)fin.size(), b.mu, b.shift, p, st);
     ProfScope ps("moments_dense", (double)fin.size() * m * (8.0 * p + 1.0));
-    launch_moments(MOM_MEMBER, ma, (int)fin.size(), st);
+    moments(MOM_MEMBER, ma, (int)fin.size(), st);
     launch_mom_reduce(b.partial, (int)fin.size(), b.inst_dev, b.ctas, np, b.sums, 0, st);
     launch_sums_to_cov(b.inst_dev, (int)fin.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
     launch_prepare(b.inst_dev, (int)fin.size(), b.mu, b.sigma, p, kappa_max, nullptr, 0, b.logdet, b.cond, nullptr,
@@ -383,10 +395,11 @@ void carve_refine(Arena& A, RefineBufs& r, long long m, int p) {
 bool refine_from_V(cudaStream_t st, RefineBufs& r, const double* Zb, long long m, int p, const double* Vdev,
                    double* mu_out, double* sig_out) {
   // T = Z V -> D~ = diag(sigma_uni^2(T_j))
-  upload_const(Vdev, (size_t)p * p, st);
+  if (!use_mma()) upload_const(Vdev, (size_t)p * p, st);
   {
     ProfScope ps("matmul", (double)m * p * 16.0);
-    launch_matmul(p, Zb, m, r.T, st);
+    if (use_mma()) launch_matmul_mma(p, Zb, m, Vdev, r.T, st);
+    else launch_matmul(p, Zb, m, r.T, st);
   }
   run_unimcd(st, r.uscratch, r.uscratch_bytes, r.T, m, p, r.uni);
   std::vector<UniOut> u(p);
@@ -398,10 +411,11 @@ bool refine_from_V(cudaStream_t st, RefineBufs& r, const double* Zb, long long m
   launch_vdv(Vdev, r.d, 1, p, 1, r.Smh, st);
   launch_vdv(Vdev, r.d, 1, p, 2, r.Sh, st);
   // Z~ = Z Sigma^-1/2 -> mu~ = mu_uni(Z~_j) -> mu0 = Sigma^1/2 mu~
-  upload_const(r.Smh, (size_t)p * p, st);
+  if (!use_mma()) upload_const(r.Smh, (size_t)p * p, st);
   {
     ProfScope ps("matmul", (double)m * p * 16.0);
-    launch_matmul(p, Zb, m, r.T, st);
+    if (use_mma()) launch_matmul_mma(p, Zb, m, r.Smh, r.T, st);
+    else launch_matmul(p, Zb, m, r.T, st);
   }
   run_unimcd(st, r.uscratch, r.uscratch_bytes, r.T, m, p, r.uni);
   d2h(st, u.data(), r.uni, p * sizeof(UniOut));
@@ -455,7 +469,7 @@ void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int
   a.ctas = b.ctas;
   // S~1: covariance of the wrapped data (centred at the wrapped mean, n - 1)
   ProfScope ps("initial", (double)q * m * p * 16.0);
-  launch_moments(MOM_WRAP, a, q, st);
+  moments(MOM_WRAP, a, q, st);
   launch_mom_reduce(b.partial, q, b.inst_dev, b.ctas, np, b.sums, 0, st);
   launch_sums_to_cov(b.inst_dev, q, b.sums, np, nullptr, p, (double)m, 1.0, b.mudummy, b.S1, st);
   // S~2: norms, type-7 cutoffs, xi^2-weighted second moment / n
@@ -469,7 +483,7 @@ void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int
   launch_lr_cutoffs(b.rs, q, m, b.AB, b.abok, st);
   a.r = b.r;
   a.AB = b.AB;
-  launch_moments(MOM_XI, a, q, st);
+  moments(MOM_XI, a, q, st);
   launch_mom_reduce(b.partial, q, b.inst_dev, b.ctas, np, b.sums, 0, st);
   launch_sums_to_second(b.sums, q, np, p, (double)m, b.S2, st);
 }
@@ -733,7 +747,7 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     const int np = mom_np(p);
     {
       ProfScope ps("reweight", (double)q * m * (8.0 * p + 8.0));
-      launch_moments(MOM_REWEIGHT, a, q, st);
+      moments(MOM_REWEIGHT, a, q, st);
     }
     launch_mom_reduce(f.cb.partial, q, f.cb.inst_dev, f.cb.ctas, np, f.sums_rw, 0, st);
     launch_pool_sums(f.sums_rw, q, np, f.pooled, st);

@@ -1,0 +1,263 @@
+// Moments and the refinement GEMMs on the FP64 tensor pipe (DMMA m8n8k4).
+//
+// k_moments_mma: S2 = sum_r w_r u_r u_r^T (lower 8x8 blocks), S1 = sum_r w_r u_r,
+//   count = sum_r w_r over the rows of a block, for every MomMode of
+//   k_moments.cu (wrapping S~1, LR-GSSCM S~2, C-step dense / delta moments,
+//   reweighting).  Each warp takes 4 rows per step: lane (g, t) loads
+//   u[r0 + t][8b + g] for every 8-column group b and feeds it as the A operand
+//   (scaled by w) of block row b and as the B operand of block column b, so
+//   one load serves (NB+1)/2 DMMAs.  Groups of 4 rows whose weights are all
+//   zero (most rows of the update-based C-step) are skipped
+//   without reading Z.  Partials are reduced in a fixed order (deterministic).
+// k_matmul_mma: out = Z W (W full p x p, e.g. the eigenvectors V or
+//   Sigma^-1/2 of the refinement), column-major out.
+#include "rtd_internal.h"
+
+namespace rtd {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double wrap_g2(double z) {
+  const double b = 1.5, c = 4.0, q1 = 1.541, q2 = 0.862;
+  double az = fabs(z);
+  if (az <= b) return z;
+  if (az <= c) {
+    double t = __dmul_rn(q1, tanh(__dmul_rn(q2, __dsub_rn(c, az))));
+    return z > 0 ? t : (z < 0 ? -t : 0.0);
+  }
+  return 0.0;
+}
+
+static constexpr int MW = 8;  // warps per CTA
+
+template <int NB, int MODE>
+__global__ void __launch_bounds__(MW * 32) k_moments_mma(MomArgs a) {
+  constexpr int NBLK = NB * (NB + 1) / 2;
+  extern __shared__ double red[];  // [MW][NP]
+  const int slot = blockIdx.y;
+  const int id = a.inst[slot];
+  const int blk = id / a.nstart;
+  const int p = a.p;
+  const long long m = a.m;
+  const double* __restrict__ Z = a.Z + (long long)blk * a.blk_stride;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
+  const int NP = p + p * (p + 1) / 2 + 1;
+  const double* shift = (MODE >= MOM_MEMBER) ? a.shift + (long long)id * RTD_MAXP : nullptr;
+  double sh[NB];
+#pragma unroll
+  for (int b = 0; b < NB; b++) sh[b] = (shift && 8 * b + g < p) ? shift[8 * b + g] : 0.0;
+  double A = 0.0, B = 0.0;
+  if (MODE == MOM_XI) {
+    A = a.AB[2 * blk];
+    B = a.AB[2 * blk + 1];
+  }
+  double acc[NBLK][2];
+#pragma unroll
+  for (int k = 0; k < NBLK; k++) acc[k][0] = acc[k][1] = 0.0;
+  double s1[NB];
+#pragma unroll
+  for (int b = 0; b < NB; b++) s1[b] = 0.0;
+  double cnt = 0.0;
+  // rows of this CTA: contiguous range, 4-row groups interleaved over warps
+  long long per = (m + a.ctas - 1) / a.ctas;
+  per = (per + 3) / 4 * 4;
+  const long long r_begin = (long long)blockIdx.x * per, r_end = min(m, r_begin + per);
+  for (long long r0 = r_begin + 4LL * warp; r0 < r_end; r0 += 4LL * MW) {
+    const long long row = r0 + t;
+    double w = 0.0;
+    if (row < r_end) {
+      if (MODE == MOM_WRAP) {
+        w = 1.0;
+      } else if (MODE == MOM_XI) {
+        const double r = a.r[(long long)blk * m + row];
+        const double xi = r <= A ? 1.0 : (r <= B ? __ddiv_rn(__dsub_rn(B, r), __dsub_rn(B, A)) : 0.0);
+        w = __dmul_rn(xi, xi);
+      } else if (MODE == MOM_MEMBER) {
+        w = (double)a.mem_new[(long long)id * m + row];
+      } else if (MODE == MOM_DELTA) {
+        w = (double)((int)a.mem_new[(long long)id * m + row] - (int)a.mem_old[(long long)id * m + row]);
+      } else {
+        w = a.d2[(long long)id * m + row] <= a.c2 ? 1.0 : 0.0;
+      }
+    }
+    if (!__any_sync(0xffffffffu, w != 0.0)) continue;
+    double u[NB];
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+      const int col = 8 * b + g;
+      double v = 0.0;
+      if (w != 0.0 && col < p) {
+        v = Z[(long long)col * m + row];
+        if (MODE == MOM_WRAP) v = wrap_g2(v);
+        else if (MODE >= MOM_MEMBER) v = __dsub_rn(v, sh[b]);
+      }
+      u[b] = v;
+    }
+    double wu[NB];
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+      wu[b] = w * u[b];
+      s1[b] += wu[b];
+    }
+    if (g == 0) cnt += w;
+    int k = 0;
+#pragma unroll
+    for (int jb = 0; jb < NB; jb++)
+#pragma unroll
+      for (int kb = 0; kb <= jb; kb++) {
+        dmma(acc[k][0], acc[k][1], wu[jb], u[kb]);  // A[j][r] = w_r u_r[8jb+j], B[r][k] = u_r[8kb+k]
+        k++;
+      }
+  }
+  // reduce: S1 over the 4 t-lanes, count over the t-lanes of g == 0
+#pragma unroll
+  for (int b = 0; b < NB; b++) {
+    s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 1);
+    s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 2);
+  }
+  cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+  cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+  double* rw = red + warp * NP;
+  for (int e = lane; e < NP; e += 32) rw[e] = 0.0;
+  __syncwarp();
+  if (t == 0) {
+#pragma unroll
+    for (int b = 0; b < NB; b++)
+      if (8 * b + g < p) rw[8 * b + g] = s1[b];
+  }
+  if (lane == 0) rw[NP - 1] = cnt;
+  {
+    int k = 0;
+#pragma unroll
+    for (int jb = 0; jb < NB; jb++)
+#pragma unroll
+      for (int kb = 0; kb <= jb; kb++) {
+        const int j = 8 * jb + g;
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int kk = 8 * kb + 2 * t + e;
+          if (j < p && kk < p && kk <= j) rw[p + j * (j + 1) / 2 + kk] = acc[k][e];
+        }
+        k++;
+      }
+  }
+  __syncthreads();
+  double* out = a.partial + ((long long)slot * a.ctas + blockIdx.x) * NP;
+  for (int e = threadIdx.x; e < NP; e += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < MW; q++) s += red[q * NP + e];
+    out[e] = s;
+  }
+}
+
+template <int NB>
+static void moments_mma_nb(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
+  const int NP = mom_np(a.p);
+  const size_t smem = (size_t)MW * NP * sizeof(double);
+  dim3 grid(a.ctas, ninst);
+#define RTD_MM_CASE(M)                                                                                   \
+  case M:                                                                                                \
+    RTD_CU(cudaFuncSetAttribute(k_moments_mma<NB, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                (int)smem));                                                             \
+    k_moments_mma<NB, M><<<grid, MW * 32, smem, st>>>(a);                                                \
+    break;
+  switch (mode) {
+    RTD_MM_CASE(MOM_WRAP)
+    RTD_MM_CASE(MOM_XI)
+    RTD_MM_CASE(MOM_MEMBER)
+    RTD_MM_CASE(MOM_DELTA)
+    RTD_MM_CASE(MOM_REWEIGHT)
+  }
+#undef RTD_MM_CASE
+}
+
+void launch_moments_mma(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
+  switch ((a.p + 7) / 8) {
+    case 1: moments_mma_nb<1>(mode, a, ninst, st); break;
+    case 2: moments_mma_nb<2>(mode, a, ninst, st); break;
+    case 3: moments_mma_nb<3>(mode, a, ninst, st); break;
+    case 4: moments_mma_nb<4>(mode, a, ninst, st); break;
+    case 5: moments_mma_nb<5>(mode, a, ninst, st); break;
+    default: throw std::string("moments_mma: p out of range");
+  }
+  RTD_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ out = Z W on DMMA
+template <int NB, int MB>
+__global__ void __launch_bounds__(256) k_matmul_mma(const double* __restrict__ Z, long long m, int p,
+                                                    const double* __restrict__ W, double* __restrict__ out) {
+  constexpr int KB = 2 * NB;  // k-blocks of 4 (k padded to 8 NB)
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double bf[KB][NB];
+#pragma unroll
+  for (int kb = 0; kb < KB; kb++)
+#pragma unroll
+    for (int nb = 0; nb < NB; nb++) {
+      const int k = 4 * kb + t, j = 8 * nb + g;
+      bf[kb][nb] = (k < p && j < p) ? W[k * p + j] : 0.0;
+    }
+  const long long rows_per_tile = 8 * MB;
+  const long long ntiles = (m + rows_per_tile - 1) / rows_per_tile;
+  const long long warp0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long tile = warp0; tile < ntiles; tile += nwarps) {
+    const long long r0 = tile * rows_per_tile;
+    double acc[MB][NB][2];
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < KB; kb++) {
+      const int k = 4 * kb + t;
+      double av[MB];
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++) {
+        const long long row = r0 + mb * 8 + g;
+        av[mb] = (k < p && row < m) ? Z[(long long)k * m + row] : 0.0;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++)
+#pragma unroll
+        for (int mb = 0; mb < MB; mb++) dmma(acc[mb][nb][0], acc[mb][nb][1], av[mb], bf[kb][nb]);
+    }
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++) {
+      const long long row = r0 + mb * 8 + g;
+      if (row >= m) continue;
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        const int j = 8 * nb + 2 * t;
+        if (j < p) out[(long long)j * m + row] = acc[mb][nb][0];
+        if (j + 1 < p) out[(long long)(j + 1) * m + row] = acc[mb][nb][1];
+      }
+    }
+  }
+}
+
+template <int NB>
+static void matmul_mma_nb(const double* Z, long long m, int p, const double* W, double* out, cudaStream_t st) {
+  constexpr int MB = NB <= 3 ? 4 : 2;
+  const long long tiles = (m + 8 * MB - 1) / (8 * MB);
+  const unsigned grid = (unsigned)std::min<long long>((tiles + 7) / 8, 148LL * 4);
+  k_matmul_mma<NB, MB><<<grid, 256, 0, st>>>(Z, m, p, W, out);
+}
+
+void launch_matmul_mma(int p, const double* Z, long long m, const double* W, double* out, cudaStream_t st) {
+  switch ((p + 7) / 8) {
+    case 1: matmul_mma_nb<1>(Z, m, p, W, out, st); break;
+    case 2: matmul_mma_nb<2>(Z, m, p, W, out, st); break;
+    case 3: matmul_mma_nb<3>(Z, m, p, W, out, st); break;
+    case 4: matmul_mma_nb<4>(Z, m, p, W, out, st); break;
+    case 5: matmul_mma_nb<5>(Z, m, p, W, out, st); break;
+    default: throw std::string("matmul_mma: p out of range");
+  }
+  RTD_LAUNCHED();
+}
+
+}  // namespace rtd
