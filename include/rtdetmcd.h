@@ -197,6 +197,49 @@ int32_t rtdetmcd_prof_count(const rtdetmcd_ctx* ctx);
 rtdetmcd_status rtdetmcd_prof_entry(const rtdetmcd_ctx* ctx, int32_t i, char* name, size_t name_len, double* ms_total,
                                     int64_t* launches, double* bytes_total);
 
+/* ---- distributed stages (one process per GPU; the caller moves data between
+ * ranks, e.g. with torch.distributed over NCCL).  Blocks are contiguous row
+ * ranges; rank r holds blocks [r q/G, (r+1) q/G).  Sequence per rank:
+ *   rtdetmcd_columns -> (exchange columns) -> rtdetmcd_unimcd on owned columns
+ *   -> (all-gather loc/scale) -> rtdetmcd_blocks_fit -> (all-gather records)
+ *   -> rtdetmcd_aggregate -> rtdetmcd_blocks_reweight -> (all-gather sums)
+ *   -> rtdetmcd_pool_reweight -> rtdetmcd_flag on the local rows.
+ * The results equal rtdetmcd_fit with shards = q and RTD_PART_CONTIGUOUS on
+ * the concatenated rows (§4 steps 1-10).
+ * rtdetmcd_blocks_fit opens a session held by the context; aggregate,
+ * blocks_reweight and pool_reweight use it; any other call closes it. */
+
+/* record layout written by rtdetmcd_blocks_fit, per block, in doubles:
+ * [valid, chosen start, log det (unscaled), C-steps, mu (p), c(alpha)-scaled Sigma (p*p)] (standardised units) */
+#define RTDETMCD_RECORD_DOUBLES(p) (4 + (p) + (p) * (p))
+/* doubles per block of reweighting sums: p (S1) + p(p+1)/2 (S2, packed lower) + 1 (count) */
+int32_t rtdetmcd_moment_doubles(int32_t p);
+
+/* H0 alone: X [dev|host] n x p row-major -> Xc [dev] p x n column-major
+ * (validated; ln applied when log_transform).  RTD_E_NONFINITE names the row. */
+rtdetmcd_status rtdetmcd_columns(rtdetmcd_ctx* ctx, const double* X, int64_t n, int32_t p, int32_t log_transform,
+                                 double* Xc);
+/* Fit q_local contiguous blocks of m = n_local / q_local rows of X_local
+ * [dev|host] with the GLOBAL standardisation loc/scale [host p] and block
+ * coverage h_block (= floor(h m / n)).  records [host] q_local records.
+ * q_global sizes the aggregation buffers of the session. */
+rtdetmcd_status rtdetmcd_blocks_fit(rtdetmcd_ctx* ctx, const double* X_local, int64_t n_local, int32_t p,
+                                    const double* loc, const double* scale, int32_t q_local, int32_t q_global,
+                                    int64_t h_block, const rtdetmcd_opts* opts, double* records);
+/* Entrywise median, KL ranking, ceil(q_valid/2) kept, pooling of the q_global
+ * records [host] of all ranks (block order) -> raw fit [host] in standardised
+ * units; identical on every rank. */
+rtdetmcd_status rtdetmcd_aggregate(rtdetmcd_ctx* ctx, int32_t q, int32_t p, int64_t m, const double* records,
+                                   double* mu_raw, double* sigma_raw, int32_t* n_kept);
+/* Reweighting sums of the session's blocks about mu_raw -> sums [host]
+ * q_local * rtdetmcd_moment_doubles(p); weights [dev|host] n_local, nullable. */
+rtdetmcd_status rtdetmcd_blocks_reweight(rtdetmcd_ctx* ctx, double quantile, double* sums, uint8_t* weights);
+/* Pool the q_global blocks' sums [host] (block order) -> raw and reweighted
+ * fits in ORIGINAL units [host]; n_weighted [host] nullable. */
+rtdetmcd_status rtdetmcd_pool_reweight(rtdetmcd_ctx* ctx, int32_t q, const double* sums, double quantile,
+                                       double* mu_raw, double* sigma_raw, double* mu_rew, double* sigma_rew,
+                                       int64_t* n_weighted);
+
 /* Host numerics used by the fit, exported for checking. */
 double rtdetmcd_chi2_quantile(double prob, int32_t dof);
 double rtdetmcd_consistency_factor(double alpha, int32_t p);

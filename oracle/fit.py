@@ -142,7 +142,7 @@ def fit_block(Zb: np.ndarray, hb: int, kappa_max: float = 1000.0, max_csteps: in
 
 def fit(X: np.ndarray, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0,
         kappa_max: float = 1000.0, quantile: float = 0.975, max_csteps: int = 100,
-        log_transform: bool = False) -> FitResult:
+        log_transform: bool = False, partition_mode: str = "permute") -> FitResult:
     X = np.asarray(X, dtype=np.float64)
     n, p = X.shape
     if not np.all(np.isfinite(X)):
@@ -160,7 +160,7 @@ def fit(X: np.ndarray, h: int | None = None, alpha: float = 0.5, q: int = 1, see
         warnings.append("H_BELOW_BOUND")
     loc, scale = standardize(X)
     Z = (X - loc[None, :]) / scale[None, :]
-    block, pos, m = partition(n, q, seed)
+    block, pos, m = partition(n, q, seed, partition_mode)
     hb = (h * m) // n
     if not hb > p:
         raise FitError("INVALID_ARG", "block h_l <= p")

@@ -92,11 +92,21 @@ def feistel_perm_array(n: int, seed: int) -> np.ndarray:
     return x.astype(np.int64)
 
 
-def partition(n: int, q: int, seed: int):
-    """(block[i], pos[i], m) for every row; block = -1 for the discarded remainder."""
+def partition(n: int, q: int, seed: int, mode: str = "permute"):
+    """(block[i], pos[i], m) for every row; block = -1 for the discarded remainder.
+
+    mode "permute": the keyed random permutation (reading R13, PAPER.md:752-755);
+    mode "contiguous": block l = rows [l m, (l+1) m) (BASELINE.json configs[3]:
+    rows sharded over GPUs with per-shard DetMCD).
+    """
     m = n // q
     block = np.full(n, -1, dtype=np.int64)
     pos = np.full(n, -1, dtype=np.int64)
+    if mode == "contiguous":
+        idx = np.arange(q * m)
+        block[: q * m] = idx // m
+        pos[: q * m] = idx % m
+        return block, pos, m
     if q == 1:
         block[:] = 0
         pos[:] = np.arange(n)

@@ -24,6 +24,8 @@ EXPORTS = [
     "rtdetmcd_unimcd", "rtdetmcd_initial", "rtdetmcd_refine", "rtdetmcd_csteps",
     "rtdetmcd_chi2_quantile", "rtdetmcd_consistency_factor", "rtdetmcd_choose_q", "rtdetmcd_partition_perm",
     "rtdetmcd_set_profiling", "rtdetmcd_prof_count", "rtdetmcd_prof_entry", "rtdetmcd_counters",
+    "rtdetmcd_moment_doubles", "rtdetmcd_columns", "rtdetmcd_blocks_fit", "rtdetmcd_aggregate",
+    "rtdetmcd_blocks_reweight", "rtdetmcd_pool_reweight",
 ]
 
 
@@ -83,6 +85,13 @@ def lib() -> C.CDLL:
     L.rtdetmcd_choose_q.restype = i32
     L.rtdetmcd_partition_perm.argtypes = [vp, i64, u64, vp]
     L.rtdetmcd_set_profiling.argtypes = [vp, i32]
+    L.rtdetmcd_moment_doubles.argtypes = [i32]
+    L.rtdetmcd_moment_doubles.restype = i32
+    L.rtdetmcd_columns.argtypes = [vp, vp, i64, i32, i32, vp]
+    L.rtdetmcd_blocks_fit.argtypes = [vp, vp, i64, i32, vp, vp, i32, i32, i64, C.POINTER(Opts), vp]
+    L.rtdetmcd_aggregate.argtypes = [vp, i32, i32, i64, vp, vp, vp, vp]
+    L.rtdetmcd_blocks_reweight.argtypes = [vp, f64, vp, vp]
+    L.rtdetmcd_pool_reweight.argtypes = [vp, i32, vp, f64, vp, vp, vp, vp, vp]
     L.rtdetmcd_counters.argtypes = [vp, vp]
     L.rtdetmcd_counters.restype = None
     L.rtdetmcd_prof_count.argtypes = [vp]

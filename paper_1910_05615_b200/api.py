@@ -46,6 +46,22 @@ def _ctx(device: int = 0):
     return _CTX[key]
 
 
+def _sync_torch(device: int) -> None:
+    """Make work queued by torch on `device` visible to the library's stream."""
+    torch = _torch()
+    if torch.cuda.is_available():
+        torch.cuda.current_stream(device).synchronize()
+
+
+def new_context(device: int = 0) -> dict:
+    """A private context (own stream, own workspace), e.g. one per rank thread."""
+    h = C.c_void_p()
+    rc = lib().rtdetmcd_create(C.byref(h), device, None)
+    if rc != 0:
+        raise RTDError(rc, "rtdetmcd_create failed")
+    return {"h": h, "ws": None}
+
+
 def _check(rc: int, ctx) -> None:
     if rc != 0:
         raise RTDError(rc, lib().rtdetmcd_last_error(ctx["h"]).decode())
@@ -122,12 +138,14 @@ def workspace_size(n: int, p: int, **opts) -> int:
 def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, kappa_max: float = 1000.0,
         quantile: float = 0.975, max_csteps: int = 100, refresh_every: int = 32, partition: int = 0,
         log_transform: bool = False, outputs=("flags", "rd2", "weights", "hsubset"), device: int | None = None,
-        torch_workspace: bool = True, out_buffers: dict | None = None) -> Fit:
+        torch_workspace: bool = True, out_buffers: dict | None = None, ctx: dict | None = None) -> Fit:
     """rtdetmcd_fit on an n x p row-major float64 matrix (numpy or torch, host or device)."""
     ptr, keep, is_cuda, dev = _as_f64(X)
     n, p = int(keep.shape[0]), int(keep.shape[1])
     dev = dev if device is None else device
-    ctx = _ctx(dev)
+    ctx = ctx or _ctx(dev)
+    if is_cuda:
+        _sync_torch(dev)
     o = default_opts(h=int(h or 0), alpha=float(alpha), shards=int(q), seed=int(seed), kappa_max=float(kappa_max),
                      quantile=float(quantile), max_csteps=int(max_csteps), refresh_every=int(refresh_every),
                      partition=int(partition), log_transform=int(bool(log_transform)))
@@ -174,11 +192,14 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
                **rows)
 
 
-def flag(X, mu, sigma, quantile: float = 0.975, log_transform: bool = False, want_rd2: bool = True):
+def flag(X, mu, sigma, quantile: float = 0.975, log_transform: bool = False, want_rd2: bool = True,
+         ctx: dict | None = None):
     """rtdetmcd_flag: (flags, rd2) of rows of X under (mu, sigma)."""
     ptr, keep, is_cuda, dev = _as_f64(X)
     n, p = int(keep.shape[0]), int(keep.shape[1])
-    ctx = _ctx(dev)
+    ctx = ctx or _ctx(dev)
+    if is_cuda:
+        _sync_torch(dev)
     mu = np.ascontiguousarray(mu, dtype=np.float64)
     sg = np.ascontiguousarray(sigma, dtype=np.float64)
     fl, fp = _out_buffer(n, np.uint8, is_cuda, dev)
@@ -188,13 +209,14 @@ def flag(X, mu, sigma, quantile: float = 0.975, log_transform: bool = False, wan
     return fl, rd
 
 
-def unimcd(cols, device: int = 0):
+def unimcd(cols, device: int = 0, ctx: dict | None = None):
     """Univariate reweighted MCD of each column of a (ncols, len) device tensor."""
     ptr, keep, is_cuda, dev = _as_f64(cols)
     if not is_cuda:
         raise ValueError("unimcd stage call takes a CUDA tensor (ncols, len)")
     ncols, ln = int(keep.shape[0]), int(keep.shape[1])
-    ctx = _ctx(dev)
+    ctx = ctx or _ctx(dev)
+    _sync_torch(dev)
     out = {k: np.zeros(ncols) for k in ("loc", "scale", "raw_loc", "raw_var")}
     start = np.zeros(ncols, np.int64)
     _check(lib().rtdetmcd_unimcd(ctx["h"], C.c_void_p(ptr), ln, ncols, out["loc"].ctypes.data,
@@ -210,6 +232,7 @@ def _zcols(Z):
     if not (isinstance(Z, torch.Tensor) and Z.is_cuda):
         raise ValueError("stage calls take a CUDA tensor")
     Zc = Z.detach().to(torch.float64).t().contiguous()
+    _sync_torch(Z.device.index or 0)
     return Zc, int(Z.shape[0]), int(Z.shape[1]), Z.device.index or 0
 
 

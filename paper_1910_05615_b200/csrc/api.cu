@@ -121,6 +121,7 @@ struct rtdetmcd_ctx {
   size_t ws_cap = 0;
   bool ws_user = false;
   Prof prof;
+  void* session = nullptr;  // distributed stages (DistSession), see rtdetmcd_blocks_fit
 };
 
 namespace {
@@ -154,7 +155,11 @@ void h2d(cudaStream_t st, void* dev, const void* host, size_t bytes) {
   RTD_CU(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st));
 }
 
+void drop_session(rtdetmcd_ctx* c);
+
+// Every call that carves the workspace invalidates a distributed-stage session.
 void ensure_ws(rtdetmcd_ctx* c, size_t bytes) {
+  drop_session(c);
   if (bytes <= c->ws_cap) return;
   if (c->ws_user) throw Fail{RTD_E_OOM, "workspace too small: need " + std::to_string(bytes) + " bytes"};
   if (c->ws) cudaFree(c->ws);
@@ -516,7 +521,7 @@ struct FitBufs {
 };
 
 void carve_fit(Arena& A, FitBufs& f, const Dims& d, const rtdetmcd_opts& o, bool need_flags, bool need_rd2,
-               bool need_w, bool need_h) {
+               bool need_w, bool need_h, int q_agg = 0) {
   const long long n = d.n, m = d.m;
   const int p = d.p, q = d.q;
   f.Xd = d.x_host ? A.take<double>((size_t)n * p) : nullptr;
@@ -533,21 +538,21 @@ void carve_fit(Arena& A, FitBufs& f, const Dims& d, const rtdetmcd_opts& o, bool
   f.V2 = A.take<double>((size_t)2 * q * M2);
   f.lam2 = A.take<double>((size_t)2 * q * RTD_MAXP);
   f.jok = A.take<int>(2 * q);
-  f.sigraw_blk = A.take<double>((size_t)q * M2);
+  f.sigraw_blk = A.take<double>((size_t)std::max(q, q_agg) * M2);
   f.mu_raw = A.take<double>(RTD_MAXP);
   f.sig_raw = A.take<double>(M2);
-  f.keys = A.take<double>(q);
+  f.keys = A.take<double>(std::max(q, q_agg));
   f.agg_scratch = A.take<double>(2 * M2);
   f.mu_rew = A.take<double>(RTD_MAXP);
   f.sig_rew = A.take<double>(M2);
-  f.sums_rw = A.take<double>((size_t)q * NPMAX);
+  f.sums_rw = A.take<double>((size_t)std::max(q, q_agg) * NPMAX);
   f.pooled = A.take<double>(NPMAX);
   f.muX = A.take<double>(4 * RTD_MAXP);
   f.sigX = A.take<double>(4 * M2);
-  f.kept = A.take<int>(q);
-  f.ids_dev = A.take<int>(q + 8);
+  f.kept = A.take<int>(std::max(q, q_agg));
+  f.ids_dev = A.take<int>(std::max(q, q_agg) + 8);
   f.st1 = A.take<int>(8);
-  f.mu_blk = A.take<double>((size_t)q * RTD_MAXP);
+  f.mu_blk = A.take<double>((size_t)std::max(q, q_agg) * RTD_MAXP);
   f.chosen_dev = A.take<int>(q + 8);
   f.flags_d = need_flags ? A.take<uint8_t>(n) : nullptr;
   f.rd2_d = need_rd2 ? A.take<double>(n) : nullptr;
@@ -583,6 +588,160 @@ void output_copy(cudaStream_t st, void* user, const void* dev, size_t bytes) {
   else RTD_CU(cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDeviceToHost, st));
 }
 
+// ------------------------------------------------------------------ phases of the fit (shared by
+// rtdetmcd_fit and the distributed stage entry points)
+struct BlockResult {
+  std::vector<int> status, steps, chosen, chosen_inst, valid_ids;
+  std::vector<double> logdet;
+  int warnings = 0;
+};
+
+// H0: X (device) -> validated, optionally ln, column-major Xc; throws RTD_E_NONFINITE
+void phase_columns(cudaStream_t st, const double* Xdev, long long n, int p, int log, double* Xc,
+                   unsigned long long* bad) {
+  RTD_CU(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  {
+    ProfScope ps("transpose", (double)n * p * 16.0);
+    launch_transpose(Xdev, n, p, log, Xc, bad, st);
+  }
+  unsigned long long b = 0;
+  d2h(st, &b, bad, sizeof(b));
+  if (b != ~0ull) throw Fail{RTD_E_NONFINITE, "row " + std::to_string(b) + (log ? " is not finite and > 0" : " is not finite")};
+}
+
+// H2-H9 for the q blocks already in f.Z: starts, refinement, C-steps, start choice, c(alpha) scaling.
+// Leaves mu_blk[b] / sigraw_blk[b] (standardised units) for the valid blocks and f.chosen_dev.
+BlockResult phase_blocks(cudaStream_t st, FitBufs& f, const Dims& d, const rtdetmcd_opts& o) {
+  const int p = d.p, q = d.q;
+  const long long m = d.m, blk_stride = (long long)p * m;
+  BlockResult r;
+  run_initial(st, f.ib, f.Z, m, p, q, blk_stride);
+  launch_jacobi(f.ib.S1, q, p, o.kappa_max, f.V2, f.lam2, f.jok, st);
+  launch_jacobi(f.ib.S2, q, p, o.kappa_max, f.V2 + (size_t)q * M2, f.lam2 + (size_t)q * RTD_MAXP, f.jok + q, st);
+  std::vector<int> jok(2 * q), abok(q);
+  d2h(st, jok.data(), f.jok, 2 * q * sizeof(int));
+  d2h(st, abok.data(), f.ib.abok, q * sizeof(int));
+  const int ninst = 2 * q;
+  r.status.assign(ninst, ST_ACTIVE);
+  for (int b = 0; b < q; b++) {
+    for (int k = 0; k < 2; k++) {
+      const int id = 2 * b + k;
+      const bool eig_ok = jok[k * q + b] != 0 && (k == 0 || abok[b] != 0);
+      if (!eig_ok) {
+        r.status[id] = ST_REFINE;
+        continue;
+      }
+      const double* V = f.V2 + ((size_t)k * q + b) * M2;
+      bool ok = refine_from_V(st, f.rb, f.Z + (size_t)b * blk_stride, m, p, V, f.cb.mu + (size_t)id * RTD_MAXP,
+                              f.cb.sigma + (size_t)id * M2);
+      if (!ok) r.status[id] = ST_REFINE;
+    }
+  }
+  run_csteps(st, f.cb, f.Z, blk_stride, 2, ninst, d.hb, o.kappa_max, o.max_csteps, o.refresh_every, r.status,
+             r.steps);
+  r.logdet.resize(ninst);
+  d2h(st, r.logdet.data(), f.cb.logdet, ninst * sizeof(double));
+  const double calpha = consistency_factor((double)d.hb / (double)m, p);
+  r.chosen.assign(q, -1);
+  r.chosen_inst.assign(q, -1);
+  for (int b = 0; b < q; b++) {
+    bool u0 = r.status[2 * b] == ST_CONVERGED || r.status[2 * b] == ST_MAXSTEPS;
+    bool u1 = r.status[2 * b + 1] == ST_CONVERGED || r.status[2 * b + 1] == ST_MAXSTEPS;
+    if (!u0 || !u1) r.warnings |= RTD_W_START_FAILED;
+    int ch = -1;
+    if (u0) ch = 0;
+    if (u1 && (!u0 || r.logdet[2 * b + 1] < r.logdet[2 * b])) ch = 1;
+    r.chosen[b] = ch;
+    if (ch >= 0) {
+      r.valid_ids.push_back(b);
+      r.chosen_inst[b] = 2 * b + ch;
+      if (r.status[2 * b + ch] == ST_MAXSTEPS) r.warnings |= RTD_W_MAX_CSTEPS;
+    } else {
+      r.warnings |= RTD_W_BLOCK_FAILED;
+    }
+  }
+  h2d(st, f.chosen_dev, r.chosen_inst.data(), q * sizeof(int));
+  for (int b : r.valid_ids) {
+    launch_scale_copy(f.cb.sigma + (size_t)r.chosen_inst[b] * M2, f.sigraw_blk + (size_t)b * M2, p, calpha, st);
+    RTD_CU(cudaMemcpyAsync(f.mu_blk + (size_t)b * RTD_MAXP, f.cb.mu + (size_t)r.chosen_inst[b] * RTD_MAXP,
+                           RTD_MAXP * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  return r;
+}
+
+// H9/H10: raw fit from the valid block fits in mu_blk / sigraw_blk (q == 1: the block fit itself)
+int phase_raw(cudaStream_t st, FitBufs& f, int p, int q, long long m, const std::vector<int>& valid_ids) {
+  if (q == 1) {
+    if (valid_ids.empty()) throw Fail{RTD_E_BOTH_STARTS_FAILED, "both starts were dropped"};
+    RTD_CU(cudaMemcpyAsync(f.mu_raw, f.mu_blk, RTD_MAXP * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    RTD_CU(cudaMemcpyAsync(f.sig_raw, f.sigraw_blk, M2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return 1;
+  }
+  if ((int)valid_ids.size() < q - q / 2)
+    throw Fail{RTD_E_TOO_FEW_VALID_BLOCKS, std::to_string(valid_ids.size()) + " of " + std::to_string(q) + " blocks valid"};
+  h2d(st, f.ids_dev, valid_ids.data(), valid_ids.size() * sizeof(int));
+  launch_aggregate(f.mu_blk, f.sigraw_blk, f.ids_dev, (int)valid_ids.size(), p, (double)m, f.mu_raw, f.sig_raw,
+                   f.kept, f.keys, f.agg_scratch, st);
+  std::vector<int> kept(valid_ids.size());
+  d2h(st, kept.data(), f.kept, kept.size() * sizeof(int));
+  int n_kept = 0;
+  for (int v : kept) n_kept += v;
+  return n_kept;
+}
+
+// H11 per block: d^2 under (mu_raw, Sigma_raw) for the q blocks in f.Z and the weighted sums about mu_raw
+// -> f.sums_rw [q][np]; f.cb.d2 keeps the distances (weights)
+void phase_reweight_blocks(cudaStream_t st, FitBufs& f, int p, int q, long long m, double c2) {
+  const long long blk_stride = (long long)p * m;
+  const int cstride = p + p * (p + 1) / 2;
+  int zero2[2] = {0, 0};
+  h2d(st, f.ids_dev, zero2, sizeof(int));
+  h2d(st, f.st1, zero2, sizeof(int));
+  launch_prepare(f.ids_dev, 1, f.mu_raw, f.sig_raw, p, 1e300, f.cb.cstage, cstride, nullptr, nullptr, f.st1, nullptr,
+                 0, 0, st);
+  int stv = 0;
+  d2h(st, &stv, f.st1, sizeof(int));
+  if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "raw scatter is not positive definite"};
+  std::vector<int> blocks(q);
+  for (int b = 0; b < q; b++) blocks[b] = b;
+  h2d(st, f.cb.inst_dev, blocks.data(), q * sizeof(int));
+  {
+    ProfScope ps("dist", (double)q * m * (8.0 * p + 8.0));
+    if (dist_mma_supported(p)) {
+      launch_dist_mma(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, f.cb.cstage, 0, f.cb.d2, st);
+    } else {
+      upload_const(f.cb.cstage, cstride, st);
+      launch_dist(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, 0, f.cb.d2, st);
+    }
+  }
+  for (int b = 0; b < q; b++)
+    RTD_CU(cudaMemcpyAsync(f.cb.shift + (size_t)b * RTD_MAXP, f.mu_raw, RTD_MAXP * sizeof(double),
+                           cudaMemcpyDeviceToDevice, st));
+  MomArgs a = mom_args(f.cb, f.Z, blk_stride, 1);
+  a.c2 = c2;
+  const int np = mom_np(p);
+  {
+    ProfScope ps("reweight", (double)q * m * (8.0 * p + 8.0));
+    moments(MOM_REWEIGHT, a, q, st);
+  }
+  launch_mom_reduce(f.cb.partial, q, f.cb.inst_dev, f.cb.ctas, np, f.sums_rw, 0, st);
+}
+
+// H11 pooled: sum of the q block sums (block order) -> (mu_rew, Sigma_rew) scaled by c(quantile, p); returns k
+double phase_pool(cudaStream_t st, FitBufs& f, int p, int q, double quantile, const double* sums_dev) {
+  const int np = mom_np(p);
+  launch_pool_sums(sums_dev, q, np, f.pooled, st);
+  std::vector<double> pooled(np);
+  d2h(st, pooled.data(), f.pooled, np * sizeof(double));
+  const double kw = pooled[np - 1];
+  if (!(kw > p)) throw Fail{RTD_E_NOT_PD, "too few reweighted inliers"};
+  int zero = 0;
+  h2d(st, f.ids_dev, &zero, sizeof(int));
+  launch_sums_to_cov(f.ids_dev, 1, f.pooled, np, f.mu_raw, p, 0.0, consistency_factor(quantile, p), f.mu_rew,
+                     f.sig_rew, st);
+  return kw;
+}
+
 void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetmcd_opts& o, rtdetmcd_result* out) {
   cudaStream_t st = c->stream;
   const bool x_host = !is_device_ptr(X);
@@ -598,7 +757,6 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
   A.base = c->ws;
   A.cap = c->ws_cap;
   carve_fit(A, f, d, o, true, true, true, true);
-  const long long blk_stride = (long long)p * m;
   int warnings = 0;
   if (d.h < (n + p + 1) / 2) warnings |= RTD_W_H_BELOW_BOUND;
 
@@ -608,14 +766,7 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     h2d(st, f.Xd, X, (size_t)n * p * sizeof(double));
     Xdev = f.Xd;
   }
-  RTD_CU(cudaMemsetAsync(f.bad, 0xff, sizeof(unsigned long long), st));
-  {
-    ProfScope ps("transpose", (double)n * p * 16.0);
-    launch_transpose(Xdev, n, p, d.log, f.Xc, f.bad, st);
-  }
-  unsigned long long bad = 0;
-  d2h(st, &bad, f.bad, sizeof(bad));
-  if (bad != ~0ull) throw Fail{RTD_E_NONFINITE, "row " + std::to_string(bad) + (d.log ? " is not finite and > 0" : " is not finite")};
+  phase_columns(st, Xdev, n, p, d.log, f.Xc, f.bad);
 
   // H1: global column standardisation
   run_unimcd(st, f.uscratch, f.uscratch_bytes, f.Xc, n, p, f.uni);
@@ -630,137 +781,17 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     launch_build_Z(f.Xc, Xdev, n, p, q, m, d.perm, o.seed, d.log, f.uni, f.Z, f.rowmap, st);
   }
 
-  // H2, H3: S~1, S~2 per block
-  run_initial(st, f.ib, f.Z, m, p, q, blk_stride);
-  std::vector<int> abok(q);
-  // H4 step 1-2: eigen-decomposition + condition check of both starts
-  launch_jacobi(f.ib.S1, q, p, o.kappa_max, f.V2, f.lam2, f.jok, st);
-  launch_jacobi(f.ib.S2, q, p, o.kappa_max, f.V2 + (size_t)q * M2, f.lam2 + (size_t)q * RTD_MAXP, f.jok + q, st);
-  std::vector<int> jok(2 * q);
-  d2h(st, jok.data(), f.jok, 2 * q * sizeof(int));
-  d2h(st, abok.data(), f.ib.abok, q * sizeof(int));
-
-  // H4 steps 3-4: refinement per (block, start); instance id = 2 b + k
-  const int ninst = 2 * q;
-  std::vector<int> status(ninst, ST_ACTIVE), steps(ninst, 0);
-  for (int b = 0; b < q; b++) {
-    for (int k = 0; k < 2; k++) {
-      const int id = 2 * b + k;
-      const bool eig_ok = jok[k * q + b] != 0 && (k == 0 || abok[b] != 0);
-      if (!eig_ok) {
-        status[id] = ST_REFINE;
-        continue;
-      }
-      const double* V = f.V2 + ((size_t)k * q + b) * M2;
-      bool ok = refine_from_V(st, f.rb, f.Z + (size_t)b * blk_stride, m, p, V, f.cb.mu + (size_t)id * RTD_MAXP,
-                              f.cb.sigma + (size_t)id * M2);
-      if (!ok) status[id] = ST_REFINE;
-    }
-  }
-
-  // H5-H9: C-steps for all (block, start) instances in lock step
-  run_csteps(st, f.cb, f.Z, blk_stride, 2, ninst, d.hb, o.kappa_max, o.max_csteps, o.refresh_every, status, steps);
-  std::vector<double> logdet(ninst);
-  d2h(st, logdet.data(), f.cb.logdet, ninst * sizeof(double));
-  const double calpha = consistency_factor((double)d.hb / (double)m, p);
-  std::vector<int> chosen(q, -1), valid_ids;
-  for (int b = 0; b < q; b++) {
-    bool u0 = status[2 * b] == ST_CONVERGED || status[2 * b] == ST_MAXSTEPS;
-    bool u1 = status[2 * b + 1] == ST_CONVERGED || status[2 * b + 1] == ST_MAXSTEPS;
-    if (!u0 || !u1) warnings |= RTD_W_START_FAILED;
-    int ch = -1;
-    if (u0) ch = 0;
-    if (u1 && (!u0 || logdet[2 * b + 1] < logdet[2 * b])) ch = 1;
-    chosen[b] = ch;
-    if (ch >= 0) {
-      valid_ids.push_back(b);
-      if (status[2 * b + ch] == ST_MAXSTEPS) warnings |= RTD_W_MAX_CSTEPS;
-    } else {
-      warnings |= RTD_W_BLOCK_FAILED;
-    }
-  }
-  // per-block raw fits: c(alpha_l) * Sigma
-  std::vector<int> chosen_inst(q, -1);
-  for (int b = 0; b < q; b++) chosen_inst[b] = chosen[b] >= 0 ? 2 * b + chosen[b] : -1;
-  h2d(st, f.chosen_dev, chosen_inst.data(), q * sizeof(int));
-  for (int b : valid_ids)
-    launch_scale_copy(f.cb.sigma + (size_t)chosen_inst[b] * M2, f.sigraw_blk + (size_t)b * M2, p, calpha, st);
-  if (q == 1) {
-    if (valid_ids.empty()) throw Fail{RTD_E_BOTH_STARTS_FAILED, "both starts were dropped"};
-  } else {
-    if ((int)valid_ids.size() < q - q / 2)
-      throw Fail{RTD_E_TOO_FEW_VALID_BLOCKS,
-                 std::to_string(valid_ids.size()) + " of " + std::to_string(q) + " blocks valid"};
-  }
-  int n_kept = 1;
-  if (q == 1) {
-    RTD_CU(cudaMemcpyAsync(f.mu_raw, f.cb.mu + (size_t)chosen_inst[0] * RTD_MAXP, RTD_MAXP * sizeof(double),
-                           cudaMemcpyDeviceToDevice, st));
-    RTD_CU(cudaMemcpyAsync(f.sig_raw, f.sigraw_blk, M2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  } else {
-    // chosen centres of the valid blocks -> mu_blk[b]; median / KL / pooling on the device (K11)
-    for (int b : valid_ids)
-      RTD_CU(cudaMemcpyAsync(f.mu_blk + (size_t)b * RTD_MAXP, f.cb.mu + (size_t)chosen_inst[b] * RTD_MAXP,
-                             RTD_MAXP * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    h2d(st, f.ids_dev, valid_ids.data(), valid_ids.size() * sizeof(int));
-    launch_aggregate(f.mu_blk, f.sigraw_blk, f.ids_dev, (int)valid_ids.size(), p, (double)m, f.mu_raw, f.sig_raw,
-                     f.kept, f.keys, f.agg_scratch, st);
-    std::vector<int> kept(valid_ids.size());
-    d2h(st, kept.data(), f.kept, kept.size() * sizeof(int));
-    n_kept = 0;
-    for (int v : kept) n_kept += v;
-  }
+  // H2-H9 per block, H10 raw fit
+  BlockResult br = phase_blocks(st, f, d, o);
+  warnings |= br.warnings;
+  const int n_kept = phase_raw(st, f, p, q, m, br.valid_ids);
 
   // H11: reweighting over the fitted rows, per block then pooled
   const double c2 = chi2_quantile(o.quantile, p);
   const int cstride = p + p * (p + 1) / 2;
-  {
-    // distance operator of the raw fit; also its positive-definiteness check
-    int zero2[2] = {0, 0};
-    h2d(st, f.ids_dev, zero2, sizeof(int));
-    h2d(st, f.st1, zero2, sizeof(int));
-    launch_prepare(f.ids_dev, 1, f.mu_raw, f.sig_raw, p, 1e300, f.cb.cstage, cstride, nullptr, nullptr, f.st1,
-                   nullptr, 0, 0, st);
-    int stv = 0;
-    d2h(st, &stv, f.st1, sizeof(int));
-    if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "raw scatter is not positive definite"};
-  }
-  {
-    std::vector<int> blocks(q);
-    for (int b = 0; b < q; b++) blocks[b] = b;
-    h2d(st, f.cb.inst_dev, blocks.data(), q * sizeof(int));
-    {
-      ProfScope ps("dist", (double)q * m * (8.0 * p + 8.0));
-      if (dist_mma_supported(p)) {
-        launch_dist_mma(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, f.cb.cstage, 0, f.cb.d2, st);
-      } else {
-        upload_const(f.cb.cstage, cstride, st);
-        launch_dist(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, 0, f.cb.d2, st);
-      }
-    }
-    // shift = mu_raw for every block
-    for (int b = 0; b < q; b++)
-      RTD_CU(cudaMemcpyAsync(f.cb.shift + (size_t)b * RTD_MAXP, f.mu_raw, RTD_MAXP * sizeof(double),
-                             cudaMemcpyDeviceToDevice, st));
-    MomArgs a = mom_args(f.cb, f.Z, blk_stride, 1);
-    a.c2 = c2;
-    const int np = mom_np(p);
-    {
-      ProfScope ps("reweight", (double)q * m * (8.0 * p + 8.0));
-      moments(MOM_REWEIGHT, a, q, st);
-    }
-    launch_mom_reduce(f.cb.partial, q, f.cb.inst_dev, f.cb.ctas, np, f.sums_rw, 0, st);
-    launch_pool_sums(f.sums_rw, q, np, f.pooled, st);
-    std::vector<double> pooled(np);
-    d2h(st, pooled.data(), f.pooled, np * sizeof(double));
-    const double kw = pooled[np - 1];
-    if (!(kw > p)) throw Fail{RTD_E_NOT_PD, "too few reweighted inliers"};
-    std::vector<int> zero(1, 0);
-    h2d(st, f.ids_dev, zero.data(), sizeof(int));
-    launch_sums_to_cov(f.ids_dev, 1, f.pooled, np, f.mu_raw, p, 0.0, consistency_factor(o.quantile, p), f.mu_rew,
-                       f.sig_rew, st);
-    if (out) out->n_weighted = (int64_t)llround(kw);
-  }
+  phase_reweight_blocks(st, f, p, q, m, c2);
+  const double kw = phase_pool(st, f, p, q, o.quantile, f.sums_rw);
+  if (out) out->n_weighted = (int64_t)llround(kw);
   // de-standardise raw and reweighted fits (H13)
   launch_destandardize(f.uni, f.mu_raw, f.sig_raw, p, f.muX, f.sigX, st);
   launch_destandardize(f.uni, f.mu_rew, f.sig_rew, p, f.muX + RTD_MAXP, f.sigX + M2, st);
@@ -804,29 +835,49 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
       if (out->sigma_raw) out->sigma_raw[e] = sx[e];
       if (out->sigma_rew) out->sigma_rew[e] = sx[M2 + e];
     }
-    out->logdet_raw = (q == 1 && chosen[0] >= 0) ? logdet[chosen_inst[0]] : NAN;
+    const int ninst = 2 * q;
+    out->logdet_raw = (q == 1 && br.chosen[0] >= 0) ? br.logdet[br.chosen_inst[0]] : NAN;
     out->cutoff2 = c2;
     out->h = d.h;
     out->h_block = d.hb;
     out->m = m;
     out->q_used = q;
     out->warnings = warnings;
-    out->n_valid_blocks = (int)valid_ids.size();
+    out->n_valid_blocks = (int)br.valid_ids.size();
     out->n_kept_blocks = n_kept;
     if (out->block_chosen)
-      for (int b = 0; b < q; b++) out->block_chosen[b] = chosen[b];
+      for (int b = 0; b < q; b++) out->block_chosen[b] = br.chosen[b];
     if (out->start_steps)
-      for (int i = 0; i < ninst; i++) out->start_steps[i] = steps[i];
+      for (int i = 0; i < ninst; i++) out->start_steps[i] = br.steps[i];
     if (out->start_status)
-      for (int i = 0; i < ninst; i++) out->start_status[i] = status[i];
+      for (int i = 0; i < ninst; i++) out->start_status[i] = br.status[i];
     if (out->start_logdet)
-      for (int i = 0; i < ninst; i++) out->start_logdet[i] = logdet[i];
+      for (int i = 0; i < ninst; i++) out->start_logdet[i] = br.logdet[i];
     output_copy(st, out->flags, f.flags_d, n);
     output_copy(st, out->rd2, f.rd2_d, n * sizeof(double));
     output_copy(st, out->weights, f.weights_d, n);
     output_copy(st, out->hsubset, f.hsub_d, n);
     RTD_CU(cudaStreamSynchronize(st));
   }
+}
+
+struct DistSession {
+  Dims d;
+  FitBufs f;
+  rtdetmcd_opts o;
+  int q_global = 1;
+  BlockResult br;
+  bool have_raw = false;
+};
+
+void drop_session(rtdetmcd_ctx* c) {
+  delete static_cast<DistSession*>(c->session);
+  c->session = nullptr;
+}
+
+DistSession* session_of(rtdetmcd_ctx* c) {
+  if (!c->session) throw Fail{RTD_E_INVALID_ARG, "no block session: call rtdetmcd_blocks_fit first"};
+  return static_cast<DistSession*>(c->session);
 }
 
 template <class F>
@@ -907,6 +958,7 @@ rtdetmcd_status rtdetmcd_create(rtdetmcd_ctx** ctx, int device, void* cuda_strea
 
 void rtdetmcd_destroy(rtdetmcd_ctx* c) {
   if (!c) return;
+  drop_session(c);
   cudaSetDevice(c->device);
   if (c->ws && !c->ws_user) cudaFree(c->ws);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -944,6 +996,7 @@ rtdetmcd_status rtdetmcd_fit(rtdetmcd_ctx* c, const double* X, int64_t n, int32_
     if (!X) throw Fail{RTD_E_INVALID_ARG, "X is NULL"};
     rtdetmcd_opts o;
     if (opts) o = *opts; else rtdetmcd_opts_default(&o);
+    drop_session(c);
     fit_impl(c, X, n, p, o, out);
   });
 }
@@ -1184,6 +1237,188 @@ rtdetmcd_status rtdetmcd_prof_entry(const rtdetmcd_ctx* c, int32_t i, char* name
   if (launches) *launches = e.second.launches;
   if (bytes_total) *bytes_total = e.second.bytes;
   return RTD_OK;
+}
+
+int32_t rtdetmcd_moment_doubles(int32_t p) { return mom_np(p); }
+
+rtdetmcd_status rtdetmcd_columns(rtdetmcd_ctx* c, const double* X, int64_t n, int32_t p, int32_t log_transform,
+                                 double* Xc) {
+  return guarded(c, [&] {
+    if (!X || !Xc || n < 1 || p < 1 || p > RTD_MAXP) throw Fail{RTD_E_INVALID_ARG, "bad arguments"};
+    cudaStream_t st = c->stream;
+    const bool xh = !is_device_ptr(X);
+    Arena dry;
+    dry.take<double>(xh ? (size_t)n * p : 1);
+    dry.take<unsigned long long>(1);
+    ensure_ws(c, dry.off + 4096);
+    drop_session(c);
+    Arena A;
+    A.base = c->ws;
+    A.cap = c->ws_cap;
+    double* xd = A.take<double>(xh ? (size_t)n * p : 1);
+    unsigned long long* bad = A.take<unsigned long long>(1);
+    const double* Xdev = X;
+    if (xh) {
+      h2d(st, xd, X, (size_t)n * p * sizeof(double));
+      Xdev = xd;
+    }
+    phase_columns(st, Xdev, n, p, log_transform ? 1 : 0, Xc, bad);
+    RTD_CU(cudaStreamSynchronize(st));
+  });
+}
+
+rtdetmcd_status rtdetmcd_blocks_fit(rtdetmcd_ctx* c, const double* X_local, int64_t n_local, int32_t p,
+                                    const double* loc, const double* scale, int32_t q_local, int32_t q_global,
+                                    int64_t h_block, const rtdetmcd_opts* opts, double* records) {
+  return guarded(c, [&] {
+    if (!X_local || !loc || !scale || !records || p < 1 || p > RTD_MAXP || q_local < 1 || q_global < q_local)
+      throw Fail{RTD_E_INVALID_ARG, "bad arguments"};
+    rtdetmcd_opts o;
+    if (opts) o = *opts; else rtdetmcd_opts_default(&o);
+    cudaStream_t st = c->stream;
+    DistSession* S = new DistSession();
+    Dims& d = S->d;
+    d.n = n_local;
+    d.p = p;
+    d.q = q_local;
+    d.m = n_local / q_local;
+    d.hb = h_block;
+    d.h = h_block;
+    d.perm = 0;
+    d.log = o.log_transform ? 1 : 0;
+    d.x_host = !is_device_ptr(X_local);
+    if (!(d.hb > p && d.hb <= d.m)) throw Fail{RTD_E_INVALID_ARG, "need p < h_block <= m"};
+    S->o = o;
+    S->q_global = q_global;
+    Arena dry;
+    carve_fit(dry, S->f, d, o, false, false, true, false, q_global);
+    try {
+      ensure_ws(c, dry.off + 4096);  // drops any previous session
+    } catch (...) {
+      delete S;
+      throw;
+    }
+    c->session = S;
+    Arena A;
+    A.base = c->ws;
+    A.cap = c->ws_cap;
+    carve_fit(A, S->f, d, o, false, false, true, false, q_global);
+    FitBufs& f = S->f;
+    const double* Xdev = X_local;
+    if (d.x_host) {
+      h2d(st, f.Xd, X_local, (size_t)n_local * p * sizeof(double));
+      Xdev = f.Xd;
+    }
+    phase_columns(st, Xdev, n_local, p, d.log, f.Xc, f.bad);
+    std::vector<UniOut> u(RTD_MAXP);
+    memset(u.data(), 0, u.size() * sizeof(UniOut));
+    for (int j = 0; j < p; j++) {
+      if (!(scale[j] > 0.0)) throw Fail{RTD_E_DEGENERATE_COLUMN, "column " + std::to_string(j)};
+      u[j].loc = loc[j];
+      u[j].scale = scale[j];
+    }
+    h2d(st, f.uni, u.data(), RTD_MAXP * sizeof(UniOut));
+    launch_build_Z(f.Xc, Xdev, n_local, p, q_local, d.m, 0, 0, d.log, f.uni, f.Z, nullptr, st);
+    S->br = phase_blocks(st, f, d, o);
+    const int R = 4 + p + p * p;
+    std::vector<double> mu(RTD_MAXP), sg(M2);
+    for (int b = 0; b < q_local; b++) {
+      double* rec = records + (size_t)b * R;
+      memset(rec, 0, R * sizeof(double));
+      const int ch = S->br.chosen[b];
+      rec[0] = ch >= 0 ? 1.0 : 0.0;
+      rec[1] = ch;
+      rec[2] = ch >= 0 ? S->br.logdet[2 * b + ch] : NAN;
+      rec[3] = ch >= 0 ? S->br.steps[2 * b + ch] : 0;
+      if (ch < 0) continue;
+      d2h(st, mu.data(), f.mu_blk + (size_t)b * RTD_MAXP, RTD_MAXP * sizeof(double));
+      d2h(st, sg.data(), f.sigraw_blk + (size_t)b * M2, M2 * sizeof(double));
+      for (int j = 0; j < p; j++) rec[4 + j] = mu[j];
+      for (int e = 0; e < p * p; e++) rec[4 + p + e] = sg[e];
+    }
+  });
+}
+
+rtdetmcd_status rtdetmcd_aggregate(rtdetmcd_ctx* c, int32_t q, int32_t p, int64_t m, const double* records,
+                                   double* mu_raw, double* sigma_raw, int32_t* n_kept) {
+  return guarded(c, [&] {
+    DistSession* S = session_of(c);
+    if (!records || p != S->d.p || q != S->q_global) throw Fail{RTD_E_INVALID_ARG, "bad arguments"};
+    cudaStream_t st = c->stream;
+    FitBufs& f = S->f;
+    const int R = 4 + p + p * p;
+    std::vector<int> valid;
+    std::vector<double> mu(RTD_MAXP, 0.0), sg(M2, 0.0);
+    for (int b = 0; b < q; b++) {
+      const double* rec = records + (size_t)b * R;
+      if (rec[0] == 0.0) continue;
+      valid.push_back(b);
+      for (int j = 0; j < p; j++) mu[j] = rec[4 + j];
+      for (int e = 0; e < p * p; e++) sg[e] = rec[4 + p + e];
+      h2d(st, f.mu_blk + (size_t)b * RTD_MAXP, mu.data(), RTD_MAXP * sizeof(double));
+      h2d(st, f.sigraw_blk + (size_t)b * M2, sg.data(), M2 * sizeof(double));
+    }
+    const int nk = phase_raw(st, f, p, q, m, valid);
+    if (n_kept) *n_kept = nk;
+    d2h(st, mu.data(), f.mu_raw, RTD_MAXP * sizeof(double));
+    d2h(st, sg.data(), f.sig_raw, M2 * sizeof(double));
+    for (int j = 0; j < p; j++)
+      if (mu_raw) mu_raw[j] = mu[j];
+    for (int e = 0; e < p * p; e++)
+      if (sigma_raw) sigma_raw[e] = sg[e];
+    S->have_raw = true;
+  });
+}
+
+rtdetmcd_status rtdetmcd_blocks_reweight(rtdetmcd_ctx* c, double quantile, double* sums, uint8_t* weights) {
+  return guarded(c, [&] {
+    DistSession* S = session_of(c);
+    if (!S->have_raw || !sums) throw Fail{RTD_E_INVALID_ARG, "call rtdetmcd_aggregate first"};
+    cudaStream_t st = c->stream;
+    FitBufs& f = S->f;
+    const int p = S->d.p, q = S->d.q;
+    const long long m = S->d.m, n = S->d.n;
+    const double c2 = chi2_quantile(quantile, p);
+    phase_reweight_blocks(st, f, p, q, m, c2);
+    const int np = mom_np(p);
+    std::vector<double> h((size_t)q * np);
+    d2h(st, h.data(), f.sums_rw, h.size() * sizeof(double));
+    for (size_t e = 0; e < h.size(); e++) sums[e] = h[e];
+    if (weights) {
+      if (q * m < n) RTD_CU(cudaMemsetAsync(f.weights_d, 0, n, st));
+      launch_weights_from_d2(f.cb.d2, (long long)q * m, c2, nullptr, f.weights_d, st);
+      output_copy(st, weights, f.weights_d, n);
+      RTD_CU(cudaStreamSynchronize(st));
+    }
+  });
+}
+
+rtdetmcd_status rtdetmcd_pool_reweight(rtdetmcd_ctx* c, int32_t q, const double* sums, double quantile,
+                                       double* mu_raw_x, double* sigma_raw_x, double* mu_rew_x, double* sigma_rew_x,
+                                       int64_t* n_weighted) {
+  return guarded(c, [&] {
+    DistSession* S = session_of(c);
+    if (!S->have_raw || !sums || q != S->q_global) throw Fail{RTD_E_INVALID_ARG, "bad arguments"};
+    cudaStream_t st = c->stream;
+    FitBufs& f = S->f;
+    const int p = S->d.p, np = mom_np(p);
+    h2d(st, f.sums_rw, sums, (size_t)q * np * sizeof(double));
+    const double kw = phase_pool(st, f, p, q, quantile, f.sums_rw);
+    if (n_weighted) *n_weighted = (int64_t)llround(kw);
+    launch_destandardize(f.uni, f.mu_raw, f.sig_raw, p, f.muX, f.sigX, st);
+    launch_destandardize(f.uni, f.mu_rew, f.sig_rew, p, f.muX + RTD_MAXP, f.sigX + M2, st);
+    std::vector<double> mx(2 * RTD_MAXP), sx(2 * M2);
+    d2h(st, mx.data(), f.muX, 2 * RTD_MAXP * sizeof(double));
+    d2h(st, sx.data(), f.sigX, 2 * M2 * sizeof(double));
+    for (int j = 0; j < p; j++) {
+      if (mu_raw_x) mu_raw_x[j] = mx[j];
+      if (mu_rew_x) mu_rew_x[j] = mx[RTD_MAXP + j];
+    }
+    for (int e = 0; e < p * p; e++) {
+      if (sigma_raw_x) sigma_raw_x[e] = sx[e];
+      if (sigma_rew_x) sigma_rew_x[e] = sx[M2 + e];
+    }
+  });
 }
 
 double rtdetmcd_chi2_quantile(double prob, int32_t dof) { return chi2_quantile(prob, dof); }

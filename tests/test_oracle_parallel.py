@@ -121,3 +121,8 @@ def test_single_block_is_identity():
     mu = rng.standard_normal(3)
     mu_p, S_p, kept, _ = select_and_pool([mu], [S], [77])
     assert np.array_equal(mu_p, mu) and np.allclose(S_p, S, rtol=1e-15)
+
+
+def test_contiguous_partition():
+    block, pos, m = partition(10, 3, seed=1, mode="contiguous")
+    assert m == 3 and list(block) == [0, 0, 0, 1, 1, 1, 2, 2, 2, -1] and list(pos[:9]) == [0, 1, 2] * 3
