@@ -5,7 +5,7 @@ One step = one whole pass of the hot path over
 one batch of synthetic input: standardise, starts, refinement, C-steps,
 raw fit (+ aggregation for q > 1), reweighting and the flag pass over all n
 rows.  Default workload: BASELINE config 4 (n = 8,000,000, p = 40, h = 0.75 n,
-q = 8 blocks, seeded Feistel partition) on one GPU; inputs (2.56 GB) are larger
+q = 8 contiguous per-shard blocks) on one GPU; inputs (2.56 GB) are larger
 than L2 (126 MB), so no flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
@@ -115,7 +115,8 @@ def cpu_baseline(cfg: int, sample_n: int | None = None):
     q = d.q if cfg == 4 else 1
     h = int(math.floor(0.75 * sample_n)) if cfg == 4 else d.h
     t0 = time.perf_counter()
-    ofit.fit(d.X, h=h, q=q, seed=191005615, log_transform=d.log_transform)
+    ofit.fit(d.X, h=h, q=q, seed=191005615, log_transform=d.log_transform,
+             partition_mode="contiguous" if cfg == 4 else "permute")
     dt = time.perf_counter() - t0
     threads = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
     return {"value": sample_n / dt, "unit": "obs/s", "cores": int(threads), "kind": "oracle",
@@ -199,7 +200,8 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    api.set_profiling(True, device=local)
+    prof_ctx = runner.engine.ctx if world > 1 else None
+    api.set_profiling(True, device=local, ctx=prof_ctx)
     k0, s0 = api.counters()
 
     def barrier():
@@ -219,8 +221,8 @@ def main():
         torch.cuda.synchronize()
         barrier()
     k1, s1 = api.counters()
-    prof = api.profile(device=local)
-    api.set_profiling(False, device=local)
+    prof = api.profile(device=local, ctx=prof_ctx)
+    api.set_profiling(False, device=local, ctx=prof_ctx)
     ms_local = ev0.elapsed_time(ev1)
     ms = ms_local
     if world > 1:

@@ -295,14 +295,14 @@ def partition_perm(n: int, seed: int, device: int = 0) -> np.ndarray:
     return out
 
 
-def set_profiling(on: bool = True, device: int = 0) -> None:
-    ctx = _ctx(device)
+def set_profiling(on: bool = True, device: int = 0, ctx: dict | None = None) -> None:
+    ctx = ctx or _ctx(device)
     _check(lib().rtdetmcd_set_profiling(ctx["h"], int(bool(on))), ctx)
 
 
-def profile(device: int = 0) -> dict:
+def profile(device: int = 0, ctx: dict | None = None) -> dict:
     """{kernel class: {"ms": total device ms, "launches": n, "bytes": algorithmic bytes}} since set_profiling."""
-    ctx = _ctx(device)
+    ctx = ctx or _ctx(device)
     L = lib()
     out = {}
     for i in range(L.rtdetmcd_prof_count(ctx["h"])):

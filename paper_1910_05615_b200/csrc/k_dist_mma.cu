@@ -24,31 +24,28 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 }
 
 template <int P, int MB>
-__global__ void __launch_bounds__(256) k_dist_mma(const double* __restrict__ Zall, long long m, long long blk_stride,
-                                                  const int* __restrict__ inst, int nstart,
-                                                  const double* __restrict__ cstage, int cstride,
-                                                  double* __restrict__ d2_all) {
+__global__ void __launch_bounds__(256, 2) k_dist_mma(const double* __restrict__ Zall, long long m, long long blk_stride,
+                                                     const int* __restrict__ inst, int nstart,
+                                                     const double* __restrict__ cstage, int cstride,
+                                                     double* __restrict__ d2_all) {
   constexpr int KB = (P + 3) / 4;
   constexpr int NB = (P + 7) / 8;
+  // operator fragments in shared memory: lane-major, conflict-free; each is reused by MB m-blocks
+  __shared__ double bsm[KB * NB * 32];
+  __shared__ double musm[KB * 4];
   const int slot = blockIdx.y;
   const int id = inst[slot];
   const double* __restrict__ Z = Zall + (long long)(id / nstart) * blk_stride;
   double* __restrict__ d2 = d2_all + (long long)id * m;
   const double* __restrict__ cs = cstage + (long long)slot * cstride;
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  // operator fragments, resident for the whole kernel
-  double bf[KB][NB];
-  double mu[KB];
-#pragma unroll
-  for (int kb = 0; kb < KB; kb++) {
-    const int k = 4 * kb + t;
-    mu[kb] = k < P ? cs[k] : 0.0;
-#pragma unroll
-    for (int nb = 0; nb < NB; nb++) {
-      const int j = 8 * nb + g;
-      bf[kb][nb] = (j < P && k <= j) ? cs[P + j * (j + 1) / 2 + k] : 0.0;
-    }
+  for (int e = threadIdx.x; e < KB * NB * 32; e += blockDim.x) {
+    const int ln = e & 31, blk = e >> 5, kb = blk / NB, nb = blk - kb * NB;
+    const int k = 4 * kb + (ln & 3), j = 8 * nb + (ln >> 2);
+    bsm[e] = (j < P && k <= j) ? cs[P + j * (j + 1) / 2 + k] : 0.0;
   }
+  for (int e = threadIdx.x; e < KB * 4; e += blockDim.x) musm[e] = e < P ? cs[e] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const long long rows_per_tile = 8 * MB;
   const long long ntiles = (m + rows_per_tile - 1) / rows_per_tile;
   const long long warp0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -63,17 +60,19 @@ __global__ void __launch_bounds__(256) k_dist_mma(const double* __restrict__ Zal
 #pragma unroll
     for (int kb = 0; kb < KB; kb++) {
       const int k = 4 * kb + t;
+      const double muk = musm[4 * kb + t];
       double a[MB];
 #pragma unroll
       for (int mb = 0; mb < MB; mb++) {
         const long long row = r0 + mb * 8 + g;
-        a[mb] = (k < P && row < m) ? __dsub_rn(Z[(long long)k * m + row], mu[kb]) : 0.0;
+        a[mb] = (k < P && row < m) ? __dsub_rn(Z[(long long)k * m + row], muk) : 0.0;
       }
 #pragma unroll
       for (int nb = 0; nb < NB; nb++) {
         if (8 * nb + 7 < 4 * kb) continue;  // block entirely above the diagonal of M
+        const double bv = bsm[(kb * NB + nb) * 32 + lane];
 #pragma unroll
-        for (int mb = 0; mb < MB; mb++) dmma_8x8x4(acc[mb][nb][0], acc[mb][nb][1], a[mb], bf[kb][nb]);
+        for (int mb = 0; mb < MB; mb++) dmma_8x8x4(acc[mb][nb][0], acc[mb][nb][1], a[mb], bv);
       }
     }
 #pragma unroll
@@ -95,10 +94,10 @@ __global__ void __launch_bounds__(256) k_dist_mma(const double* __restrict__ Zal
 template <int P>
 static void dist_mma_launch(const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
                             int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st) {
-  constexpr int MB = P <= 24 ? 4 : 2;
+  constexpr int MB = P <= 24 ? 4 : 3;
   const long long tiles = (m + 8 * MB - 1) / (8 * MB);
   const long long need = (tiles + 7) / 8;  // 8 warps per CTA
-  const long long cap = std::max<long long>(1, 148LL * 4 / std::max(1, ninst));
+  const long long cap = std::max<long long>(1, 148LL * 2 * 2 / std::max(1, ninst));
   k_dist_mma<P, MB><<<dim3((unsigned)std::min(need, cap), ninst), 256, 0, st>>>(Zall, m, blk_stride, inst, nstart,
                                                                                  cstage, cstride, d2_all);
 }
