@@ -146,10 +146,122 @@ def run_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def run_stream(args, local: int):
+    """Config 5: the real-time stream (BASELINE.json configs[4]) -- B consecutive batches of
+    20,000 x 8 (ln of lognormal), each one fit + flag; per-batch latency p50 / p99.
+
+    X of every batch is resident in HBM before the timed region; each batch is timed with
+    CUDA events on the launching stream (device) and with the host clock around the
+    synchronous call (wall).  `e2e` repeats the stream from pinned host batches (H2D of X
+    and D2H of the flags inside each call)."""
+    import torch
+
+    from paper_1910_05615_b200 import api, datagen
+    nb = args.steps
+    t0 = time.perf_counter()
+    batches = [datagen.make_config(5, batch=b) for b in range(nb)]
+    gen_s = time.perf_counter() - t0
+    n, p = batches[0].X.shape
+    h = batches[0].h
+    Xd = [torch.from_numpy(b.X).to(f"cuda:{local}") for b in batches]
+    stream = torch.cuda.current_stream()
+
+    def one(X, **kw):
+        return api.fit(X, h=h, q=1, log_transform=True, outputs=("flags",), **kw)
+
+    for b in range(args.warmup):
+        one(Xd[b % nb])
+    torch.cuda.synchronize()
+    k0, s0 = api.counters()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nb)]
+    wall = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for b in range(nb):
+            w0 = time.perf_counter()
+            evs[b][0].record(stream)
+            res = one(Xd[b])
+            evs[b][1].record(stream)
+            wall.append(1e3 * (time.perf_counter() - w0))
+        g1.record(stream)
+        torch.cuda.synchronize()
+    k1, s1 = api.counters()
+    # kernel breakdown / roofline from a separate profiled pass (per-kernel events stay out of the latencies)
+    nprof = min(nb, 100)
+    api.set_profiling(True, device=local)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    for b in range(nprof):
+        one(Xd[b])
+    pe1.record(stream)
+    torch.cuda.synchronize()
+    prof = api.profile(device=local)
+    api.set_profiling(False, device=local)
+    prof_ms = pe0.elapsed_time(pe1)
+    dev_ms = np.array([a.elapsed_time(b) for a, b in evs])
+    total_ms = g0.elapsed_time(g1)
+    value = n * nb / (total_ms / 1e3)
+    # e2e: pinned host batch in, host flags out, through the same public call
+    e2e = None
+    if not args.no_e2e:
+        Xh = [torch.from_numpy(b.X).pin_memory() for b in batches]
+        fl = torch.empty(n, dtype=torch.uint8).pin_memory()
+        one(Xh[0], out_buffers={"flags": fl})
+        torch.cuda.synchronize()
+        e_wall = []
+        w_start = time.perf_counter()
+        for b in range(nb):
+            w0 = time.perf_counter()
+            one(Xh[b], out_buffers={"flags": fl})
+            e_wall.append(1e3 * (time.perf_counter() - w0))
+        e_tot = time.perf_counter() - w_start
+        e2e = {"value": n * nb / e_tot, "unit": "obs/s", "h2d_bytes_per_step": int(n * p * 8),
+               "d2h_bytes_per_step": int(n),
+               "latency_ms": {"p50": float(np.percentile(e_wall, 50)), "p99": float(np.percentile(e_wall, 99))}}
+    roof = _roofline(prof, prof_ms)
+    cb = None if args.no_cpu_baseline else cpu_baseline(5)
+    line = {"metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": 1, "steps": nb, "warmup": args.warmup,
+            "ms_per_step": total_ms / nb, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[5], "n": int(n), "p": int(p), "h": int(h), "q": 1, "batches": nb,
+                       "log_transform": True, "l2": "batch (1.28 MB) is L2-resident: latency-bound by design",
+                       "batch_gen_s": gen_s, "parallelism": "replicas only (batches are independent)"},
+            "latency_ms": {"p50": float(np.percentile(dev_ms, 50)), "p99": float(np.percentile(dev_ms, 99)),
+                           "wall_p50": float(np.percentile(wall, 50)), "wall_p99": float(np.percentile(wall, 99)),
+                           "max": float(dev_ms.max())},
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cb, "gpu_launches": int(k1 - k0), "cub_sorts": int(s1 - s0),
+            "clocks": clk.summary(), "breakdown": _breakdown(prof, nprof),
+            "fit": {"start_steps": [int(x) for x in res.start_steps]}}
+    print(json.dumps(line), flush=True)
+
+
+def _roofline(prof: dict, ms_local: float):
+    peaks = _peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm_peak else "fallback (B200_PROFILING.md 6650 GB/s)"
+    hbm_peak = hbm_peak or 6650.0
+    if "dist" not in prof or prof["dist"]["ms"] <= 0:
+        return None
+    dstat = prof["dist"]
+    achieved = dstat["bytes"] / (dstat["ms"] / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "traffic": None, "kernel": "k_dist (C-step distance pass)", "peak_source": peak_src,
+            "launches": dstat["launches"], "avg_launch_ms": dstat["ms"] / dstat["launches"],
+            "bytes_per_launch": dstat["bytes"] / dstat["launches"], "ms_share_of_step": dstat["ms"] / ms_local}
+
+
+def _breakdown(prof: dict, steps: int):
+    return {k: {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] / steps,
+                "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] > 0 else None}
+            for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default 5; config 5: 1000 batches)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -159,6 +271,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override rows (debug only; not a bench line)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps is None:
+        args.steps = 1000 if args.config == 5 else 5
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -175,6 +289,14 @@ def main():
     from paper_1910_05615_b200 import api
 
     cfg = args.config
+    if cfg == 5:
+        if rank == 0:
+            run_stream(args, local)    # replicas only: other ranks have no shared work to do
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     d = make_workload(cfg, n=args.n or None)
     n, p = d.X.shape
     q = d.q
@@ -254,31 +376,17 @@ def main():
         e2e = {"value": n * args.steps / (ems / 1e3), "unit": "obs/s", "h2d_bytes_per_step": int(n * p * 8),
                "d2h_bytes_per_step": int(n)}
 
-    peaks = _peaks()
-    hbm_peak = peaks.get("hbm_gbs")
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm_peak else "fallback (B200_PROFILING.md 6650 GB/s)"
-    hbm_peak = hbm_peak or 6650.0
-    roof = None
-    if "dist" in prof and prof["dist"]["ms"] > 0:
-        dstat = prof["dist"]
-        achieved = dstat["bytes"] / (dstat["ms"] / 1e3) / 1e9
-        traffic = None
+    roof = _roofline(prof, ms_local)
+    if roof is not None:
         tf = os.path.join(ROOT, "profiles", "dist_traffic.json")
         if os.path.exists(tf):
             try:
                 tj = json.load(open(tf))
                 if tj.get("config") == CONFIG_NAMES[cfg]:
-                    traffic = tj.get("dram_bytes_per_launch")
+                    roof["traffic"] = tj.get("dram_bytes_per_launch")
             except Exception:
-                traffic = None
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                "traffic": traffic, "kernel": "k_dist (C-step distance pass)", "peak_source": peak_src,
-                "launches": dstat["launches"], "avg_launch_ms": dstat["ms"] / dstat["launches"],
-                "bytes_per_launch": dstat["bytes"] / dstat["launches"],
-                "ms_share_of_step": dstat["ms"] / ms_local}
-    breakdown = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
-                     "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] > 0 else None}
-                 for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+                pass
+    breakdown = _breakdown(prof, args.steps)
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -71,6 +71,33 @@ __device__ __forceinline__ double ord_val(unsigned long long k) {
   return __longlong_as_double((long long)u);
 }
 
+// Running (sum y, sum y^2) of one thread in double-double, adding one double at a time:
+// error-free two-sum / two-product with a single renormalisation (about 23 fp64 ops per
+// element instead of 42 for a full dd2_add); thread partials are then folded with dd2_add.
+struct ddacc {
+  double h1, l1, h2, l2;
+};
+__device__ __forceinline__ ddacc ddacc_zero() { return {0.0, 0.0, 0.0, 0.0}; }
+__device__ __forceinline__ void ddacc_add(ddacc& a, double v) {
+  double s = __dadd_rn(a.h1, v);
+  double bb = __dsub_rn(s, a.h1);
+  double e = __dadd_rn(__dsub_rn(a.h1, __dsub_rn(s, bb)), __dsub_rn(v, bb));
+  double lo = __dadd_rn(a.l1, e);
+  a.h1 = __dadd_rn(s, lo);
+  a.l1 = __dsub_rn(lo, __dsub_rn(a.h1, s));
+  const double p = __dmul_rn(v, v);
+  const double pe = __fma_rn(v, v, -p);
+  s = __dadd_rn(a.h2, p);
+  bb = __dsub_rn(s, a.h2);
+  e = __dadd_rn(__dsub_rn(a.h2, __dsub_rn(s, bb)), __dsub_rn(p, bb));
+  lo = __dadd_rn(a.l2, __dadd_rn(e, pe));
+  a.h2 = __dadd_rn(s, lo);
+  a.l2 = __dsub_rn(lo, __dsub_rn(a.h2, s));
+}
+__device__ __forceinline__ dd2 ddacc_dd2(const ddacc& a) { return {{a.h1, a.l1}, {a.h2, a.l2}}; }
+
+static constexpr int ILP = 8;  // elements loaded per thread before they are consumed (latency hiding)
+
 __device__ void smem_bitonic(double* a, int npow2) {
   for (int k = 2; k <= npow2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
@@ -133,14 +160,24 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
   unsigned long long kmin = ~0ull, kmax = 0ull;
   const long long per = (len + gridDim.x - 1) / gridDim.x;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
-  for (long long i = i0 + threadIdx.x; i < i1; i += PT) {
-    const double v = y[i];
-    const int b = bucket_of(v, c);
-    atomicAdd(&hc[b], 1);
-    atomicAdd(&hs[b], v);
-    const unsigned long long k = ord_key(v);
-    kmin = min(kmin, k);
-    kmax = max(kmax, k);
+  for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
+    double v[ILP];
+#pragma unroll
+    for (int k = 0; k < ILP; k++) {
+      const long long i = base + (long long)k * PT;
+      v[k] = i < i1 ? __ldg(y + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < ILP; k++) {
+      if (base + (long long)k * PT < i1) {
+        const int b = bucket_of(v[k], c);
+        atomicAdd(&hc[b], 1);
+        atomicAdd(&hs[b], v[k]);
+        const unsigned long long kk = ord_key(v[k]);
+        kmin = min(kmin, kk);
+        kmax = max(kmax, kk);
+      }
+    }
   }
   for (int d = 16; d > 0; d >>= 1) {
     kmin = min(kmin, __shfl_down_sync(0xffffffffu, kmin, d));
@@ -397,25 +434,38 @@ __global__ void __launch_bounds__(PT) k_pr_bound(long long len, long long h, con
   const double bub = mode ? best_ub[col] : 0.0;
   double ub = INFINITY;
   long long cmin = 0x7fffffffffffffffLL, cmax = -1;
+  // modes 0 and 1: every thread takes a contiguous range of sampled starts / chunks, finds the
+  // start and end buckets once by binary search and then only walks them forward
+  const long long nchunks = (nwin + CHUNK - 1) / CHUNK;
+  const long long cper = (nchunks + nthreads - 1) / nthreads;
+  const long long ch0 = gtid * cper, ch1 = min(nchunks, ch0 + cper);
   if (mode == 0) {
-    for (long long s = gtid * CHUNK; s < nwin; s += nthreads * CHUNK) {
-      const int b = rank_bucket(C, s), be = rank_bucket(C, s + h - 1);
-      ub = fmin(ub, window_bounds(s, h, b, be, c, C, A1, Q2lo, Q2hi, cn, sbk, m).hi);
+    if (ch0 < ch1) {
+      int b = rank_bucket(C, ch0 * CHUNK), be = rank_bucket(C, ch0 * CHUNK + h - 1);
+      for (long long ch = ch0; ch < ch1; ch++) {
+        const long long s = ch * CHUNK;
+        while (C[b + 1] <= s) b++;
+        while (C[be + 1] <= s + h - 1) be++;
+        ub = fmin(ub, window_bounds(s, h, b, be, c, C, A1, Q2lo, Q2hi, cn, sbk, m).hi);
+      }
     }
   } else if (mode == 1) {
-    const long long nchunks = (nwin + CHUNK - 1) / CHUNK;
-    for (long long ch = gtid; ch < nchunks; ch += nthreads) {
-      const long long s0 = ch * CHUNK, s1e = min(nwin, s0 + CHUNK);
-      long long sa = s0;
-      while (sa < s1e) {
-        const int b = rank_bucket(C, sa), be = rank_bucket(C, sa + h - 1);
-        const long long sb = min(min(s1e, C[b + 1]), C[be + 1] - h + 1) - 1;  // same (b, be) on [sa, sb]
-        const double lo = (b == be) ? -INFINITY : chunk_lower(sa, sb, h, b, be, c, C, A1, Q2lo, cn, sbk, m);
-        if (lo <= bub) {
-          cmin = min(cmin, sa);
-          cmax = max(cmax, sb);
+    if (ch0 < ch1) {
+      int b = rank_bucket(C, ch0 * CHUNK), be = rank_bucket(C, ch0 * CHUNK + h - 1);
+      for (long long ch = ch0; ch < ch1; ch++) {
+        const long long s0 = ch * CHUNK, s1e = min(nwin, s0 + CHUNK);
+        long long sa = s0;
+        while (sa < s1e) {
+          while (C[b + 1] <= sa) b++;
+          while (C[be + 1] <= sa + h - 1) be++;
+          const long long sb = min(min(s1e, C[b + 1]), C[be + 1] - h + 1) - 1;  // same (b, be) on [sa, sb]
+          const double lo = (b == be) ? -INFINITY : chunk_lower(sa, sb, h, b, be, c, C, A1, Q2lo, cn, sbk, m);
+          if (lo <= bub) {
+            cmin = min(cmin, sa);
+            cmax = max(cmax, sb);
+          }
+          sa = sb + 1;
         }
-        sa = sb + 1;
       }
     }
   } else {
@@ -514,7 +564,10 @@ __global__ void k_pr_cand(long long len, long long h, PrunedCol* __restrict__ pc
   pc[col] = c;
 }
 
-// 4. gather candidate-end elements; sum everything below them (fixed-order per-CTA partials)
+// 4. gather candidate-end elements and sum, in double-double, the elements strictly between the
+//    two gathered bucket ranges' lower ends: K = sum over buckets [bs_lo, be_lo).  The window sum of
+//    start s is then K + (first s + h - ce_lo sorted E elements) - (first s - cs_lo sorted S elements):
+//    every window sum shares the same K, so elements below bs_lo never need to be summed.
 __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ cols, long long len,
                                                   const PrunedCol* __restrict__ pc, double* __restrict__ g,
                                                   int* __restrict__ gcount, dd2* __restrict__ below) {
@@ -525,27 +578,34 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
   const double* y = cols + (long long)col * len;
   double* S = g + (long long)(2 * col) * CAP;
   double* E = g + (long long)(2 * col + 1) * CAP;
-  dd2 bs = dd2_zero(), be = dd2_zero();
+  ddacc acc = ddacc_zero();
   const long long per = (len + PCTA - 1) / PCTA;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
-  for (long long i = i0 + threadIdx.x; i < i1; i += PT) {
-    const double v = y[i];
-    const int b = bucket_of(v, c);
-    if (b < c.bs_lo) bs = dd2_add(bs, dd2_of(v));
-    if (b < c.be_lo) be = dd2_add(be, dd2_of(v));
-    if (b >= c.bs_lo && b <= c.bs_hi) {
-      const int pos = atomicAdd(&gcount[2 * col], 1);
-      if (pos < CAP) S[pos] = v;
+  for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
+    double v[ILP];
+#pragma unroll
+    for (int k = 0; k < ILP; k++) {
+      const long long i = base + (long long)k * PT;
+      v[k] = i < i1 ? __ldg(y + i) : 0.0;
     }
-    if (b >= c.be_lo && b <= c.be_hi) {
-      const int pos = atomicAdd(&gcount[2 * col + 1], 1);
-      if (pos < CAP) E[pos] = v;
+#pragma unroll
+    for (int k = 0; k < ILP; k++) {
+      if (base + (long long)k * PT >= i1) continue;
+      const int b = bucket_of(v[k], c);
+      if (b >= c.bs_lo && b < c.be_lo) ddacc_add(acc, v[k]);
+      if (b >= c.bs_lo && b <= c.bs_hi) {
+        const int pos = atomicAdd(&gcount[2 * col], 1);
+        if (pos < CAP) S[pos] = v[k];
+      }
+      if (b >= c.be_lo && b <= c.be_hi) {
+        const int pos = atomicAdd(&gcount[2 * col + 1], 1);
+        if (pos < CAP) E[pos] = v[k];
+      }
     }
   }
-  dd2 ts = block_sum_dd2(bs, sm);
-  dd2 te = block_sum_dd2(be, sm);
+  dd2 te = block_sum_dd2(ddacc_dd2(acc), sm);
   if (threadIdx.x == 0) {
-    below[((long long)col * PCTA + blockIdx.x) * 2] = ts;
+    below[((long long)col * PCTA + blockIdx.x) * 2] = dd2_zero();
     below[((long long)col * PCTA + blockIdx.x) * 2 + 1] = te;
   }
 }
@@ -683,17 +743,26 @@ __global__ void __launch_bounds__(PT) k_pr_keep(const double* __restrict__ cols,
   const double loc0 = o.raw_loc, thresh = uc.q1 * o.var0;
   const long long per = (len + PCTA - 1) / PCTA;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
-  dd2 acc = dd2_zero();
+  ddacc acc = ddacc_zero();
   long long k = 0;
-  for (long long i = i0 + threadIdx.x; i < i1; i += PT) {
-    const double v = y[i];
-    const double d = __dsub_rn(v, loc0);
-    if (__dmul_rn(d, d) <= thresh) {
-      acc = dd2_add(acc, dd2_of(v));
-      k++;
+  for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
+    double v[ILP];
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      const long long i = base + (long long)u * PT;
+      v[u] = i < i1 ? __ldg(y + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      if (base + (long long)u * PT >= i1) continue;
+      const double d = __dsub_rn(v[u], loc0);
+      if (__dmul_rn(d, d) <= thresh) {
+        ddacc_add(acc, v[u]);
+        k++;
+      }
     }
   }
-  dd2 tot = block_sum_dd2(acc, sm);
+  dd2 tot = block_sum_dd2(ddacc_dd2(acc), sm);
   for (int d = 16; d > 0; d >>= 1) k += __shfl_down_sync(0xffffffffu, k, d);
   if ((threadIdx.x & 31) == 0) kc[threadIdx.x >> 5] = k;
   __syncthreads();

@@ -159,6 +159,7 @@ def make_config(cfg: int, n: int | None = None, batch: int | None = None) -> Dat
         m = 8.0 * _mahal_unit(rng, Sigma, 1)[0]
         X[cl_idx] = m + 0.05 * (rng.standard_normal((len(cl_idx), p)) @ L.T)
         out_idx = perm
+        kinds = {"shift_rows": np.sort(sh_idx), "cluster_rows": np.sort(cl_idx)}
         h = int(math.floor(0.75 * n)); q = 8; log = False
     elif cfg == 5:
         N, p = 20_000, 8
@@ -177,8 +178,11 @@ def make_config(cfg: int, n: int | None = None, batch: int | None = None) -> Dat
         raise ValueError(f"unknown config {cfg}")
     mask = np.zeros(n, dtype=bool)
     mask[out_idx] = True
+    meta = {"n": n, "p": X.shape[1]}
+    if cfg == 4:
+        meta.update(kinds)
     return Dataset(X=np.ascontiguousarray(X), h=h, q=q, log_transform=log, sigma=Sigma,
-                   outliers=mask, name=f"cfg{cfg}", meta={"n": n, "p": X.shape[1]})
+                   outliers=mask, name=f"cfg{cfg}", meta=meta)
 
 
 def gaussian(n: int, p: int, seed: int, sigma: np.ndarray | None = None) -> np.ndarray:
