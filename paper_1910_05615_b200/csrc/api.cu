@@ -21,7 +21,11 @@ void launch_dist_mma(int p, const double* Zall, long long m, long long blk_strid
 long long launch_count();
 long long sort_count();
 void launch_moments_mma(int mode, const MomArgs& a, int ninst, cudaStream_t st);
-void launch_matmul_mma(int p, const double* Z, long long m, const double* W, double* out, cudaStream_t st);
+void launch_matmul_mma_batch(int p, const double* Zall, long long m, long long blk_stride, const int* slot_of,
+                             const int* blk_of_slot, int nitems, const double* W_all, double* out_all,
+                             cudaStream_t st);
+void launch_uni_extract_batch(const UniOut* uni, const int* slot_of, int nitems, int p, int which, double* out_all,
+                              cudaStream_t st);
 void launch_feistel_fwd(long long n, unsigned long long seed, long long* out, cudaStream_t st);
 void launch_uni_extract(const UniOut* uni, int p, int which, double* out, cudaStream_t st);
 void launch_scatter_u8(const uint8_t* src, const long long* rowmap, long long total, uint8_t* dst, cudaStream_t st);
@@ -214,6 +218,10 @@ struct CStepBufs {
   uint8_t *memA, *memB;
   SelState* sel;
   unsigned int* hist;
+  unsigned int* selcnt;
+  int* list;      // [inst][m] ordered changed rows per segment (update-based C-step)
+  int* seg_cnt;   // [inst][ctas]
+  long long seg_len;
   int traj_stride;
   int ctas;
 };
@@ -241,6 +249,10 @@ void carve_cstep(Arena& A, CStepBufs& b, int ninst, long long m, int p, int max_
   b.memB = A.take<uint8_t>((size_t)ninst * m);
   b.sel = A.take<SelState>(ninst);
   b.hist = A.take<unsigned int>((size_t)ninst * 4096);
+  b.selcnt = A.take<unsigned int>(ninst);
+  b.list = A.take<int>((size_t)ninst * m);
+  b.seg_cnt = A.take<int>((size_t)ninst * b.ctas);
+  b.seg_len = ((m + b.ctas - 1) / b.ctas + 255) / 256 * 256;
 }
 
 MomArgs mom_args(const CStepBufs& b, const double* Z, long long blk_stride, int nstart) {
@@ -258,6 +270,9 @@ MomArgs mom_args(const CStepBufs& b, const double* Z, long long blk_stride, int 
   a.d2 = b.d2;
   a.partial = b.partial;
   a.ctas = b.ctas;
+  a.list = b.list;
+  a.seg_cnt = b.seg_cnt;
+  a.seg_len = b.seg_len;
   return a;
 }
 
@@ -290,6 +305,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
   RTD_CU(cudaMemsetAsync(b.memA, 0, (size_t)ninst * m, st));
   RTD_CU(cudaMemsetAsync(b.memB, 0, (size_t)ninst * m, st));
   RTD_CU(cudaMemsetAsync(b.hist, 0, (size_t)ninst * 4096 * sizeof(unsigned int), st));
+  RTD_CU(cudaMemsetAsync(b.sel, 0, (size_t)ninst * sizeof(SelState), st));
   h2d(st, b.status, status_h.data(), ninst * sizeof(int));
   steps_h.assign(ninst, 0);
   std::vector<int> act, changed(ninst);
@@ -312,11 +328,24 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     RTD_CU(cudaMemsetAsync(b.changed, 0, ninst * sizeof(int), st));
     {
       ProfScope ps("select", (double)na * m * 9.0);
-      launch_select(b.d2, m, h, b.inst_dev, na, b.sel, b.hist, memB, memA, b.changed, st);
+      launch_select(b.d2, m, h, b.inst_dev, na, b.sel, b.hist, b.selcnt, memB, memA, b.changed, b.list, b.seg_cnt,
+                    b.ctas, b.seg_len, st);
+      d2h(st, changed.data(), b.changed, ninst * sizeof(int));
+      std::vector<int> more;
+      for (int i : act)
+        if (changed[i] < 0) more.push_back(i);
+      if (!more.empty()) {  // rare: ties or a jump of the h-th distance needed more radix levels
+        h2d(st, b.inst_dev, more.data(), more.size() * sizeof(int));
+        RTD_CU(cudaMemsetAsync(b.changed, 0, ninst * sizeof(int), st));
+        launch_select_finish(b.d2, m, b.inst_dev, (int)more.size(), b.sel, b.hist, b.selcnt, memB, memA, b.changed,
+                             b.list, b.seg_cnt, b.ctas, b.seg_len, st);
+        std::vector<int> ch2(ninst);
+        d2h(st, ch2.data(), b.changed, ninst * sizeof(int));
+        for (int i : more) changed[i] = ch2[i];
+      }
     }
     std::swap(memA, memB);  // memA = membership of this step, memB = previous
     d2h(st, status_h.data(), b.status, ninst * sizeof(int));
-    d2h(st, changed.data(), b.changed, ninst * sizeof(int));
     std::vector<int> upd, dense;
     for (int i : act) {
       steps_h[i] = step;
@@ -325,7 +354,10 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
         status_h[i] = ST_CONVERGED;
         continue;
       }
-      if (step == 1 || (refresh > 0 && (step - 1) % refresh == 0)) dense.push_back(i); else upd.push_back(i);
+      // update-based sums while few rows change; a full recompute when many do
+      // (the gather of changed rows then costs as much as the dense pass) or every `refresh` steps
+      const bool many = (long long)changed[i] * 8 > m;
+      if (step == 1 || many || (refresh > 0 && (step - 1) % refresh == 0)) dense.push_back(i); else upd.push_back(i);
     }
     // moments for the new subsets: dense recompute about shift = mu_old, or the delta update
     ma.mem_new = memA;
@@ -340,7 +372,9 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     }
     if (!upd.empty()) {
       h2d(st, b.inst_dev, upd.data(), upd.size() * sizeof(int));
-      ProfScope ps("moments_delta", (double)upd.size() * m * 2.0);
+      double nch = 0.0;
+      for (int i : upd) nch += changed[i];
+      ProfScope ps("moments_delta", nch * (8.0 * p + 4.0));
       moments(MOM_DELTA, ma, (int)upd.size(), st);
       launch_mom_reduce(b.partial, (int)upd.size(), b.inst_dev, b.ctas, np, b.sums, 1, st);
       launch_sums_to_cov(b.inst_dev, (int)upd.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
@@ -370,65 +404,103 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
   RTD_CU(cudaStreamSynchronize(st));
 }
 
-// ------------------------------------------------------------------ refinement of one start
+// ------------------------------------------------------------------ refinement, batched
+// All starts of all blocks are refined together: one GEMM launch per refinement step and the
+// univariate MCDs of every start's p columns in as few batched calls as the scratch allows.
 struct RefineBufs {
-  double *T, *V, *lam, *d, *mut, *Sig, *Smh, *Sh, *mu0;
-  int* ok;
-  UniOut* uni;
+  int cap;                                   // slots (instances)
+  int ucols;                                 // columns per univariate-MCD call
+  double* T;                                 // [cap][p][m] column-major scores / sphered data
+  double *V, *d, *mut, *Smh, *Sh;            // per slot (stride M2 / RTD_MAXP)
+  int *slot_of, *blk_of_slot;                // [cap]
+  UniOut* uni;                               // [cap * p]
   char* uscratch;
   size_t uscratch_bytes;
 };
 
-void carve_refine(Arena& A, RefineBufs& r, long long m, int p) {
-  r.T = A.take<double>((size_t)p * m);
-  r.V = A.take<double>(M2);
-  r.lam = A.take<double>(RTD_MAXP);
-  r.d = A.take<double>(RTD_MAXP);
-  r.mut = A.take<double>(RTD_MAXP);
-  r.Sig = A.take<double>(M2);
-  r.Smh = A.take<double>(M2);
-  r.Sh = A.take<double>(M2);
-  r.mu0 = A.take<double>(RTD_MAXP);
-  r.ok = A.take<int>(4);
-  r.uni = A.take<UniOut>(RTD_MAXP);
-  r.uscratch_bytes = uni_bytes(m, p);
+void carve_refine(Arena& A, RefineBufs& r, long long m, int p, int cap) {
+  r.cap = cap;
+  const int tot = cap * p;
+  const int calls = (tot + 255) / 256;
+  r.ucols = (tot + calls - 1) / calls;
+  r.T = A.take<double>((size_t)cap * p * m);
+  r.V = A.take<double>((size_t)cap * M2);
+  r.d = A.take<double>((size_t)cap * RTD_MAXP);
+  r.mut = A.take<double>((size_t)cap * RTD_MAXP);
+  r.Smh = A.take<double>((size_t)cap * M2);
+  r.Sh = A.take<double>((size_t)cap * M2);
+  r.slot_of = A.take<int>(cap + 8);
+  r.blk_of_slot = A.take<int>(cap + 8);
+  r.uni = A.take<UniOut>((size_t)tot);
+  r.uscratch_bytes = uni_bytes(m, r.ucols);
   r.uscratch = A.take<char>(r.uscratch_bytes);
 }
 
-// Given V (eigenvectors of the start, already checked), produce (mu0, Sigma0) into mu_out / sig_out.
-// Returns false when a univariate scale is degenerate.
-bool refine_from_V(cudaStream_t st, RefineBufs& r, const double* Zb, long long m, int p, const double* Vdev,
-                   double* mu_out, double* sig_out) {
-  // T = Z V -> D~ = diag(sigma_uni^2(T_j))
-  if (!use_mma()) upload_const(Vdev, (size_t)p * p, st);
-  {
-    ProfScope ps("matmul", (double)m * p * 16.0);
-    if (use_mma()) launch_matmul_mma(p, Zb, m, Vdev, r.T, st);
-    else launch_matmul(p, Zb, m, r.T, st);
+// items: slots taking part; T[i] = Z_{blk(slot_i)} W_slot_i for every item i
+static void refine_matmul(cudaStream_t st, RefineBufs& r, const double* Zall, long long blk_stride, long long m,
+                          int p, int nitems, const double* W_all, const std::vector<int>& items,
+                          const std::vector<int>& blk) {
+  ProfScope ps("matmul", (double)nitems * m * p * 16.0);
+  if (use_mma()) {
+    launch_matmul_mma_batch(p, Zall, m, blk_stride, r.slot_of, r.blk_of_slot, nitems, W_all, r.T, st);
+    return;
   }
-  run_unimcd(st, r.uscratch, r.uscratch_bytes, r.T, m, p, r.uni);
-  std::vector<UniOut> u(p);
-  d2h(st, u.data(), r.uni, p * sizeof(UniOut));
-  for (int j = 0; j < p; j++)
-    if (u[j].status) return false;
-  launch_uni_extract(r.uni, p, 0, r.d, st);
-  launch_vdv(Vdev, r.d, 1, p, 0, sig_out, st);
-  launch_vdv(Vdev, r.d, 1, p, 1, r.Smh, st);
-  launch_vdv(Vdev, r.d, 1, p, 2, r.Sh, st);
-  // Z~ = Z Sigma^-1/2 -> mu~ = mu_uni(Z~_j) -> mu0 = Sigma^1/2 mu~
-  if (!use_mma()) upload_const(r.Smh, (size_t)p * p, st);
-  {
-    ProfScope ps("matmul", (double)m * p * 16.0);
-    if (use_mma()) launch_matmul_mma(p, Zb, m, r.Smh, r.T, st);
-    else launch_matmul(p, Zb, m, r.T, st);
+  for (int i = 0; i < nitems; i++) {
+    upload_const(W_all + (size_t)items[i] * M2, (size_t)p * p, st);
+    launch_matmul(p, Zall + (size_t)blk[items[i]] * blk_stride, m, r.T + (size_t)i * p * m, st);
   }
-  run_unimcd(st, r.uscratch, r.uscratch_bytes, r.T, m, p, r.uni);
-  d2h(st, u.data(), r.uni, p * sizeof(UniOut));
-  for (int j = 0; j < p; j++)
-    if (u[j].status) return false;
-  launch_uni_extract(r.uni, p, 1, r.mut, st);
-  launch_matvec(r.Sh, r.mut, 1, p, mu_out, st);
-  return true;
+}
+
+// univariate MCD of the p columns of every item; returns per-item ok
+static std::vector<int> refine_unimcd(cudaStream_t st, RefineBufs& r, long long m, int p, int nitems) {
+  const int tot = nitems * p;
+  for (int c0 = 0; c0 < tot; c0 += r.ucols) {
+    const int nc = std::min(r.ucols, tot - c0);
+    run_unimcd(st, r.uscratch, r.uscratch_bytes, r.T + (size_t)c0 * m, m, nc, r.uni + c0);
+  }
+  std::vector<UniOut> u(tot);
+  d2h(st, u.data(), r.uni, tot * sizeof(UniOut));
+  std::vector<int> ok(nitems, 1);
+  for (int i = 0; i < nitems; i++)
+    for (int j = 0; j < p; j++)
+      if (u[(size_t)i * p + j].status) ok[i] = 0;
+  return ok;
+}
+
+// Refinement of the starts of slots with active[slot] (eigenvectors V_src(slot), already checked):
+//   T = Z V -> D~ = diag(sigma_uni^2(T_j)) -> Sigma_k = V D~ V^T (into sig_out[slot]);
+//   Z~ = Z Sigma_k^-1/2 -> mu~ = mu_uni(Z~_j) -> mu_k = Sigma_k^1/2 mu~ (into mu_out[slot]).
+// Returns ok per slot (false: inactive or a degenerate univariate scale).
+std::vector<int> refine_batch(cudaStream_t st, RefineBufs& r, const double* Zall, long long blk_stride, long long m,
+                              int p, int nslot, const std::vector<int>& blk, const std::vector<int>& active,
+                              const std::vector<const double*>& V_src, double* mu_out, double* sig_out) {
+  std::vector<int> ok(nslot, 0);
+  std::vector<int> items;
+  for (int sl = 0; sl < nslot; sl++)
+    if (active[sl]) {
+      items.push_back(sl);
+      RTD_CU(cudaMemcpyAsync(r.V + (size_t)sl * M2, V_src[sl], M2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+  if (items.empty()) return ok;
+  h2d(st, r.blk_of_slot, blk.data(), nslot * sizeof(int));
+  h2d(st, r.slot_of, items.data(), items.size() * sizeof(int));
+  refine_matmul(st, r, Zall, blk_stride, m, p, (int)items.size(), r.V, items, blk);
+  std::vector<int> ok1 = refine_unimcd(st, r, m, p, (int)items.size());
+  std::vector<int> items2;
+  for (size_t i = 0; i < items.size(); i++)
+    if (ok1[i]) items2.push_back(items[i]);
+  launch_uni_extract_batch(r.uni, r.slot_of, (int)items.size(), p, 0, r.d, st);
+  launch_vdv(r.V, r.d, nslot, p, 0, sig_out, st);
+  launch_vdv(r.V, r.d, nslot, p, 1, r.Smh, st);
+  launch_vdv(r.V, r.d, nslot, p, 2, r.Sh, st);
+  if (items2.empty()) return ok;
+  h2d(st, r.slot_of, items2.data(), items2.size() * sizeof(int));
+  refine_matmul(st, r, Zall, blk_stride, m, p, (int)items2.size(), r.Smh, items2, blk);
+  std::vector<int> ok2 = refine_unimcd(st, r, m, p, (int)items2.size());
+  launch_uni_extract_batch(r.uni, r.slot_of, (int)items2.size(), p, 1, r.mut, st);
+  launch_matvec(r.Sh, r.mut, nslot, p, mu_out, st);
+  for (size_t i = 0; i < items2.size(); i++) ok[items2[i]] = ok2[i];
+  return ok;
 }
 
 // ------------------------------------------------------------------ initial estimators of q blocks
@@ -533,7 +605,7 @@ void carve_fit(Arena& A, FitBufs& f, const Dims& d, const rtdetmcd_opts& o, bool
   f.Z = A.take<double>((size_t)q * m * p);
   f.rowmap = d.perm ? A.take<long long>((size_t)q * m) : nullptr;
   carve_init(A, f.ib, q, m, p);
-  carve_refine(A, f.rb, m, p);
+  carve_refine(A, f.rb, m, p, 2 * q);
   carve_cstep(A, f.cb, 2 * q, m, p, o.max_csteps);
   f.V2 = A.take<double>((size_t)2 * q * M2);
   f.lam2 = A.take<double>((size_t)2 * q * RTD_MAXP);
@@ -623,20 +695,18 @@ BlockResult phase_blocks(cudaStream_t st, FitBufs& f, const Dims& d, const rtdet
   d2h(st, abok.data(), f.ib.abok, q * sizeof(int));
   const int ninst = 2 * q;
   r.status.assign(ninst, ST_ACTIVE);
-  for (int b = 0; b < q; b++) {
+  std::vector<int> blk(ninst), active(ninst);
+  std::vector<const double*> Vsrc(ninst);
+  for (int b = 0; b < q; b++)
     for (int k = 0; k < 2; k++) {
       const int id = 2 * b + k;
-      const bool eig_ok = jok[k * q + b] != 0 && (k == 0 || abok[b] != 0);
-      if (!eig_ok) {
-        r.status[id] = ST_REFINE;
-        continue;
-      }
-      const double* V = f.V2 + ((size_t)k * q + b) * M2;
-      bool ok = refine_from_V(st, f.rb, f.Z + (size_t)b * blk_stride, m, p, V, f.cb.mu + (size_t)id * RTD_MAXP,
-                              f.cb.sigma + (size_t)id * M2);
-      if (!ok) r.status[id] = ST_REFINE;
+      blk[id] = b;
+      active[id] = jok[k * q + b] != 0 && (k == 0 || abok[b] != 0);
+      Vsrc[id] = f.V2 + ((size_t)k * q + b) * M2;
     }
-  }
+  std::vector<int> rok = refine_batch(st, f.rb, f.Z, blk_stride, m, p, ninst, blk, active, Vsrc, f.cb.mu, f.cb.sigma);
+  for (int id = 0; id < ninst; id++)
+    if (!rok[id]) r.status[id] = ST_REFINE;
   run_csteps(st, f.cb, f.Z, blk_stride, 2, ninst, d.hb, o.kappa_max, o.max_csteps, o.refresh_every, r.status,
              r.steps);
   r.logdet.resize(ninst);
@@ -1124,7 +1194,7 @@ rtdetmcd_status rtdetmcd_refine(rtdetmcd_ctx* c, const double* Z, int64_t m, int
     cudaStream_t st = c->stream;
     auto carve = [&](Arena& A, RefineBufs& rb, double*& Sd, double*& V, double*& L, int*& jok, double*& muo,
                      double*& sgo) {
-      carve_refine(A, rb, m, p);
+      carve_refine(A, rb, m, p, 1);
       Sd = A.take<double>(M2);
       V = A.take<double>(M2);
       L = A.take<double>(RTD_MAXP);
@@ -1152,7 +1222,7 @@ rtdetmcd_status rtdetmcd_refine(rtdetmcd_ctx* c, const double* Z, int64_t m, int
     d2h(st, lh.data(), L, RTD_MAXP * sizeof(double));
     if (lam)
       for (int j = 0; j < p; j++) lam[j] = lh[j];
-    if (okv) okv = refine_from_V(st, rb, Z, m, p, V, muo, sgo) ? 1 : 0;
+    if (okv) okv = refine_batch(st, rb, Z, 0, m, p, 1, {0}, {1}, {V}, muo, sgo)[0];
     if (okv) {
       std::vector<double> mh(RTD_MAXP), sgh(M2);
       d2h(st, mh.data(), muo, RTD_MAXP * sizeof(double));

@@ -51,6 +51,23 @@ void launch_uni_extract(const UniOut* uni, int p, int which, double* out, cudaSt
   RTD_LAUNCHED();
 }
 
+// batched: item i (uni columns [i p, (i+1) p)) -> out_all[slot_of[i]][j]
+__global__ void k_uni_extract_batch(const UniOut* __restrict__ uni, const int* __restrict__ slot_of, int p, int which,
+                                    double* __restrict__ out_all) {
+  const int i = blockIdx.x;
+  double* out = out_all + (long long)slot_of[i] * RTD_MAXP;
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    const UniOut& u = uni[(long long)i * p + j];
+    out[j] = which == 0 ? u.scale * u.scale : u.loc;
+  }
+}
+
+void launch_uni_extract_batch(const UniOut* uni, const int* slot_of, int nitems, int p, int which, double* out_all,
+                              cudaStream_t st) {
+  k_uni_extract_batch<<<nitems, 64, 0, st>>>(uni, slot_of, p, which, out_all);
+  RTD_LAUNCHED();
+}
+
 __global__ void k_weights_from_d2(const double* __restrict__ d2, long long total, double c2,
                                   const long long* __restrict__ rowmap, uint8_t* __restrict__ dst) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {

@@ -8,7 +8,10 @@
 //   (scaled by w) of block row b and as the B operand of block column b, so
 //   one load serves (NB+1)/2 DMMAs.  Groups of 4 rows whose weights are all
 //   zero (most rows of the update-based C-step) are skipped
-//   without reading Z.  Partials are reduced in a fixed order (deterministic).
+//   without reading Z; the update-based C-step (MOM_DELTA) reads only the
+//   ordered changed-row list written by the select (k_sel_member), a gather of
+//   the entering / leaving rows.  Partials are reduced in a fixed order
+//   (deterministic).
 // k_matmul_mma: out = Z W (W full p x p, e.g. the eigenvectors V or
 //   Sigma^-1/2 of the refinement), column-major out.
 #include "rtd_internal.h"
@@ -33,9 +36,10 @@ __device__ __forceinline__ double wrap_g2(double z) {
 }
 
 static constexpr int MW = 8;  // warps per CTA
+static constexpr int RG = 4;  // 4-row groups per warp iteration (loads in flight)
 
 template <int NB, int MODE>
-__global__ void __launch_bounds__(MW * 32) k_moments_mma(MomArgs a) {
+__global__ void __launch_bounds__(MW * 32, 2) k_moments_mma(MomArgs a) {
   constexpr int NBLK = NB * (NB + 1) / 2;
   extern __shared__ double red[];  // [MW][NP]
   const int slot = blockIdx.y;
@@ -62,56 +66,79 @@ __global__ void __launch_bounds__(MW * 32) k_moments_mma(MomArgs a) {
 #pragma unroll
   for (int b = 0; b < NB; b++) s1[b] = 0.0;
   double cnt = 0.0;
-  // rows of this CTA: contiguous range, 4-row groups interleaved over warps
+  // rows of this CTA: contiguous range, 4-row groups interleaved over warps; the update-based
+  // C-step (MOM_DELTA) walks instead the ordered list of changed rows of segment blockIdx.x
   long long per = (m + a.ctas - 1) / a.ctas;
   per = (per + 3) / 4 * 4;
-  const long long r_begin = (long long)blockIdx.x * per, r_end = min(m, r_begin + per);
-  for (long long r0 = r_begin + 4LL * warp; r0 < r_end; r0 += 4LL * MW) {
-    const long long row = r0 + t;
-    double w = 0.0;
-    if (row < r_end) {
-      if (MODE == MOM_WRAP) {
-        w = 1.0;
-      } else if (MODE == MOM_XI) {
-        const double r = a.r[(long long)blk * m + row];
-        const double xi = r <= A ? 1.0 : (r <= B ? __ddiv_rn(__dsub_rn(B, r), __dsub_rn(B, A)) : 0.0);
-        w = __dmul_rn(xi, xi);
-      } else if (MODE == MOM_MEMBER) {
-        w = (double)a.mem_new[(long long)id * m + row];
-      } else if (MODE == MOM_DELTA) {
-        w = (double)((int)a.mem_new[(long long)id * m + row] - (int)a.mem_old[(long long)id * m + row]);
-      } else {
-        w = a.d2[(long long)id * m + row] <= a.c2 ? 1.0 : 0.0;
+  long long r_begin = (long long)blockIdx.x * per, r_end = min(m, r_begin + per);
+  const int* lst = nullptr;
+  if (MODE == MOM_DELTA) {
+    lst = a.list + (long long)id * m + (long long)blockIdx.x * a.seg_len;
+    r_begin = 0;
+    r_end = a.seg_cnt[(long long)id * a.ctas + blockIdx.x];
+  }
+  // RG groups of 4 rows per warp iteration: all of their loads are issued before the first DMMA
+  for (long long rb = r_begin + 4LL * RG * warp; rb < r_end; rb += 4LL * RG * MW) {
+    long long row[RG];
+    double w[RG];
+    bool anyw = false;
+#pragma unroll
+    for (int q = 0; q < RG; q++) {
+      row[q] = rb + 4 * q + t;
+      w[q] = 0.0;
+      if (MODE == MOM_DELTA) {
+        if (row[q] < r_end) {
+          const int e = lst[row[q]];
+          w[q] = e > 0 ? 1.0 : -1.0;
+          row[q] = (e > 0 ? e : -e) - 1;
+        }
+      } else if (row[q] < r_end) {
+        if (MODE == MOM_WRAP) {
+          w[q] = 1.0;
+        } else if (MODE == MOM_XI) {
+          const double r = a.r[(long long)blk * m + row[q]];
+          const double xi = r <= A ? 1.0 : (r <= B ? __ddiv_rn(__dsub_rn(B, r), __dsub_rn(B, A)) : 0.0);
+          w[q] = __dmul_rn(xi, xi);
+        } else if (MODE == MOM_MEMBER) {
+          w[q] = (double)a.mem_new[(long long)id * m + row[q]];
+        } else {
+          w[q] = a.d2[(long long)id * m + row[q]] <= a.c2 ? 1.0 : 0.0;
+        }
       }
+      anyw |= w[q] != 0.0;
     }
-    if (!__any_sync(0xffffffffu, w != 0.0)) continue;
-    double u[NB];
+    if (!__any_sync(0xffffffffu, anyw)) continue;
+    double u[RG][NB];
 #pragma unroll
-    for (int b = 0; b < NB; b++) {
-      const int col = 8 * b + g;
-      double v = 0.0;
-      if (w != 0.0 && col < p) {
-        v = Z[(long long)col * m + row];
-        if (MODE == MOM_WRAP) v = wrap_g2(v);
-        else if (MODE >= MOM_MEMBER) v = __dsub_rn(v, sh[b]);
+    for (int q = 0; q < RG; q++)
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        const int col = 8 * b + g;
+        u[q][b] = (w[q] != 0.0 && col < p) ? Z[(long long)col * m + row[q]] : 0.0;
       }
-      u[b] = v;
-    }
-    double wu[NB];
 #pragma unroll
-    for (int b = 0; b < NB; b++) {
-      wu[b] = w * u[b];
-      s1[b] += wu[b];
-    }
-    if (g == 0) cnt += w;
-    int k = 0;
+    for (int q = 0; q < RG; q++) {
 #pragma unroll
-    for (int jb = 0; jb < NB; jb++)
-#pragma unroll
-      for (int kb = 0; kb <= jb; kb++) {
-        dmma(acc[k][0], acc[k][1], wu[jb], u[kb]);  // A[j][r] = w_r u_r[8jb+j], B[r][k] = u_r[8kb+k]
-        k++;
+      for (int b = 0; b < NB; b++) {
+        if (MODE == MOM_WRAP) u[q][b] = wrap_g2(u[q][b]);
+        else if (MODE >= MOM_MEMBER) u[q][b] = (w[q] != 0.0 && 8 * b + g < p) ? __dsub_rn(u[q][b], sh[b]) : 0.0;
       }
+      double wu[NB];
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        wu[b] = w[q] * u[q][b];
+        s1[b] += wu[b];
+      }
+      if (g == 0) cnt += w[q];
+      int k = 0;
+#pragma unroll
+      for (int jb = 0; jb < NB; jb++)
+#pragma unroll
+        for (int kb = 0; kb <= jb; kb++) {
+          dmma(acc[k][0], acc[k][1], wu[jb], u[q][kb]);  // A[j][r] = w_r u_r[8jb+j], B[r][k] = u_r[8kb+k]
+          k++;
+        }
+    }
   }
   // reduce: S1 over the 4 t-lanes, count over the t-lanes of g == 0
 #pragma unroll
@@ -188,11 +215,19 @@ void launch_moments_mma(int mode, const MomArgs& a, int ninst, cudaStream_t st) 
 }
 
 // ------------------------------------------------------------------ out = Z W on DMMA
+// Batched over work items (blockIdx.y = i): slot = slot_of[i] (or i), Z = Zall + blk_of_slot[slot] *
+// blk_stride (or Zall), W = W_all + slot * RTD_MAXP^2, out = out_all + i * p * m.
 template <int NB, int MB>
-__global__ void __launch_bounds__(256) k_matmul_mma(const double* __restrict__ Z, long long m, int p,
-                                                    const double* __restrict__ W, double* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_matmul_mma(const double* __restrict__ Zall, long long m, int p,
+                                                    long long blk_stride, const int* __restrict__ slot_of,
+                                                    const int* __restrict__ blk_of_slot,
+                                                    const double* __restrict__ W_all, double* __restrict__ out_all) {
   constexpr int KB = 2 * NB;  // k-blocks of 4 (k padded to 8 NB)
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int slot = slot_of ? slot_of[blockIdx.y] : (int)blockIdx.y;
+  const double* __restrict__ Z = Zall + (blk_of_slot ? (long long)blk_of_slot[slot] * blk_stride : 0LL);
+  const double* __restrict__ W = W_all + (long long)slot * RTD_MAXP * RTD_MAXP;
+  double* __restrict__ out = out_all + (long long)blockIdx.y * p * m;
   double bf[KB][NB];
 #pragma unroll
   for (int kb = 0; kb < KB; kb++)
@@ -241,20 +276,23 @@ __global__ void __launch_bounds__(256) k_matmul_mma(const double* __restrict__ Z
 }
 
 template <int NB>
-static void matmul_mma_nb(const double* Z, long long m, int p, const double* W, double* out, cudaStream_t st) {
+static void matmul_mma_nb(const double* Z, long long m, int p, long long blk_stride, const int* slot_of,
+                          const int* blk_of_slot, int nitems, const double* W, double* out, cudaStream_t st) {
   constexpr int MB = NB <= 3 ? 4 : 2;
   const long long tiles = (m + 8 * MB - 1) / (8 * MB);
-  const unsigned grid = (unsigned)std::min<long long>((tiles + 7) / 8, 148LL * 4);
-  k_matmul_mma<NB, MB><<<grid, 256, 0, st>>>(Z, m, p, W, out);
+  const unsigned grid = (unsigned)std::min<long long>((tiles + 7) / 8, std::max(1, 148 * 4 / std::max(1, nitems)));
+  k_matmul_mma<NB, MB><<<dim3(grid, nitems), 256, 0, st>>>(Z, m, p, blk_stride, slot_of, blk_of_slot, W, out);
 }
 
-void launch_matmul_mma(int p, const double* Z, long long m, const double* W, double* out, cudaStream_t st) {
+void launch_matmul_mma_batch(int p, const double* Zall, long long m, long long blk_stride, const int* slot_of,
+                             const int* blk_of_slot, int nitems, const double* W_all, double* out_all,
+                             cudaStream_t st) {
   switch ((p + 7) / 8) {
-    case 1: matmul_mma_nb<1>(Z, m, p, W, out, st); break;
-    case 2: matmul_mma_nb<2>(Z, m, p, W, out, st); break;
-    case 3: matmul_mma_nb<3>(Z, m, p, W, out, st); break;
-    case 4: matmul_mma_nb<4>(Z, m, p, W, out, st); break;
-    case 5: matmul_mma_nb<5>(Z, m, p, W, out, st); break;
+    case 1: matmul_mma_nb<1>(Zall, m, p, blk_stride, slot_of, blk_of_slot, nitems, W_all, out_all, st); break;
+    case 2: matmul_mma_nb<2>(Zall, m, p, blk_stride, slot_of, blk_of_slot, nitems, W_all, out_all, st); break;
+    case 3: matmul_mma_nb<3>(Zall, m, p, blk_stride, slot_of, blk_of_slot, nitems, W_all, out_all, st); break;
+    case 4: matmul_mma_nb<4>(Zall, m, p, blk_stride, slot_of, blk_of_slot, nitems, W_all, out_all, st); break;
+    case 5: matmul_mma_nb<5>(Zall, m, p, blk_stride, slot_of, blk_of_slot, nitems, W_all, out_all, st); break;
     default: throw std::string("matmul_mma: p out of range");
   }
   RTD_LAUNCHED();
