@@ -2,20 +2,29 @@
 //
 // H_new = the h rows with the smallest (d_i^2, i) — ties at the h-th distance
 // broken by row position (reading R11).  Instead of sorting, an exact radix
-// select walks the 95-bit composite key C_i = (bits(d_i^2) << 32) | i, which
+// select walks the 96-bit composite key C_i = (bits(d_i^2) << 32) | i, which
 // is unique per row and ordered like (d^2, i) because d^2 >= 0 so its IEEE
-// bits are order-preserving.  Each level resolves 12 bits with a shared-memory
-// histogram; selection stops as soon as the bin holding the h-th key is fully
-// inside the subset.  Membership is then one comparison per row, and the
-// number of rows whose membership changed (|delta|) is
-// counted for the convergence test.
+// bits are order-preserving.  Each level resolves a digit of the key with a
+// shared-memory histogram; selection stops as soon as the bin holding the h-th
+// key is fully inside the subset.  Membership is then one comparison per row,
+// and the rows whose membership changed (delta) are listed.
+//
+// First level: from the second C-step on, the h-th distance moves little, so
+// the first digit is the top 24 bits of the key (sign, exponent, 12 mantissa
+// bits) measured from the previous step's h-th key minus 2048: 4094 bins of
+// relative width 2^-12 around it, everything below / above counted in the two
+// end bins (warp-aggregated, no atomic contention).  If the h-th key falls in
+// an end bin the level is discarded and the plain 12-bit levels run.  Each
+// level is one launch: the last CTA of an instance to finish its histogram
+// (threadfence + counter) scans it and advances the state.
 #include "rtd_internal.h"
 
 namespace rtd {
 
 static constexpr int SEL_BITS = 12;
 static constexpr int SEL_BINS = 1 << SEL_BITS;
-static constexpr int SEL_LEVELS = 8;  // 96 bits >= 95
+static constexpr int SEL_MAXLEV = 10;  // 1 centred level that may fail + 8 plain levels (96 bits) + slack
+static constexpr int SEL_FAST = 3;     // levels launched before the host checks completion
 static constexpr int SEL_T = 256;
 
 typedef unsigned __int128 u128;
@@ -25,61 +34,92 @@ __device__ __forceinline__ u128 composite(double d2, long long i) {
   return ((u128)key << 32) | (u128)(unsigned int)i;
 }
 
-__global__ void k_sel_init(const int* __restrict__ inst, SelState* __restrict__ st_all, long long h) {
+__global__ void k_sel_init(const int* __restrict__ inst, SelState* __restrict__ st_all, unsigned int* __restrict__ cnt_all,
+                           long long h) {
   const int id = inst[blockIdx.x];
   if (threadIdx.x == 0) {
+    const SelState old = st_all[id];
     SelState s;
     s.prefix_hi = 0;
     s.prefix_lo = 0;
     s.rank = h;
-    s.level = 0;
+    s.plen = 0;
     s.done = 0;
     s.count_in = 0;
+    s.centred = 0;
+    s.base = 0;
+    if (old.valid && old.plen >= 24) {
+      const u128 pre = ((u128)old.prefix_hi << 64) | (u128)old.prefix_lo;
+      const unsigned long long top24 = (unsigned long long)(pre >> (old.plen - 24));
+      s.centred = 1;
+      s.base = top24 > 2048 ? top24 - 2048 : 0;
+    }
+    s.valid = 0;
     st_all[id] = s;
+    cnt_all[id] = 0;
   }
 }
 
-__global__ void __launch_bounds__(SEL_T) k_sel_hist(const double* __restrict__ d2_all, long long m,
-                                                    const int* __restrict__ inst, const SelState* __restrict__ st_all,
-                                                    unsigned int* __restrict__ hist_all, int level) {
+// one level: histogram of the current digit (CTAs of blockIdx.y's instance), then the last CTA scans it
+__global__ void __launch_bounds__(SEL_T) k_sel_level(const double* __restrict__ d2_all, long long m,
+                                                     const int* __restrict__ inst, SelState* __restrict__ st_all,
+                                                     unsigned int* __restrict__ hist_all,
+                                                     unsigned int* __restrict__ cnt_all) {
   __shared__ unsigned int sh[SEL_BINS];
+  __shared__ long long wsum[SEL_T / 32];
+  __shared__ int found_bin;
+  __shared__ long long found_before, found_cnt;
+  __shared__ bool last;
   const int id = inst[blockIdx.y];
-  const SelState s = st_all[id];
-  if (s.done || s.level != level) return;
+  SelState s = st_all[id];
+  if (s.done) return;
   for (int b = threadIdx.x; b < SEL_BINS; b += SEL_T) sh[b] = 0;
   __syncthreads();
   const double* d2 = d2_all + (long long)id * m;
   const u128 prefix = ((u128)s.prefix_hi << 64) | (u128)s.prefix_lo;
-  const int shift_pref = 96 - SEL_BITS * level;        // bits above this level
-  const int shift_dig = 96 - SEL_BITS * (level + 1);
+  const bool centred = s.centred && s.plen == 0;
+  const int lane = threadIdx.x & 31;
+  unsigned int below = 0, above = 0;
   for (long long i = blockIdx.x * (long long)SEL_T + threadIdx.x; i < m; i += (long long)gridDim.x * SEL_T) {
-    u128 C = composite(d2[i], i);
-    if (level == 0 || (C >> shift_pref) == prefix) {
-      unsigned int dig = (unsigned int)(C >> shift_dig) & (SEL_BINS - 1);
-      atomicAdd(&sh[dig], 1u);
+    const double v = d2[i];
+    if (centred) {
+      const unsigned long long top24 = (unsigned long long)__double_as_longlong(v) >> 40;
+      if (top24 < s.base) below++;
+      else if (top24 >= s.base + (SEL_BINS - 2)) above++;
+      else atomicAdd(&sh[top24 - s.base + 1], 1u);
+    } else {
+      const u128 C = composite(v, i);
+      if (s.plen == 0 || (C >> (96 - s.plen)) == prefix)
+        atomicAdd(&sh[(unsigned int)(C >> (96 - s.plen - SEL_BITS)) & (SEL_BINS - 1)], 1u);
+    }
+  }
+  if (centred) {
+    for (int d = 16; d > 0; d >>= 1) {
+      below += __shfl_down_sync(0xffffffffu, below, d);
+      above += __shfl_down_sync(0xffffffffu, above, d);
+    }
+    if (lane == 0) {
+      if (below) atomicAdd(&sh[0], below);
+      if (above) atomicAdd(&sh[SEL_BINS - 1], above);
     }
   }
   __syncthreads();
   unsigned int* hg = hist_all + (long long)id * SEL_BINS;
   for (int b = threadIdx.x; b < SEL_BINS; b += SEL_T)
     if (sh[b]) atomicAdd(&hg[b], sh[b]);
-}
-
-__global__ void __launch_bounds__(1024) k_sel_scan(const int* __restrict__ inst, SelState* __restrict__ st_all,
-                                                   unsigned int* __restrict__ hist_all, int level) {
-  __shared__ long long wsum[32];
-  __shared__ int found_bin;
-  __shared__ long long found_before, found_cnt;
-  const int id = inst[blockIdx.x];
-  SelState s = st_all[id];
-  if (s.done || s.level != level) return;
-  unsigned int* hg = hist_all + (long long)id * SEL_BINS;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  // 4 bins per thread, contiguous
-  long long c[4], loc = 0;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&cnt_all[id], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  // ---- scan (last CTA of the instance): 16 contiguous bins per thread
+  __threadfence();
+  constexpr int PER = SEL_BINS / SEL_T;
+  const int t = threadIdx.x, w = t >> 5;
+  long long c[PER], loc = 0;
 #pragma unroll
-  for (int e = 0; e < 4; e++) {
-    c[e] = hg[t * 4 + e];
+  for (int e = 0; e < PER; e++) {
+    c[e] = atomicAdd(&hg[t * PER + e], 0u);  // coherent read of the global histogram
     loc += c[e];
   }
   long long inc = loc;
@@ -89,87 +129,148 @@ __global__ void __launch_bounds__(1024) k_sel_scan(const int* __restrict__ inst,
   }
   if (lane == 31) wsum[w] = inc;
   __syncthreads();
-  if (w == 0) {
-    long long v = wsum[lane], vi = v;
-    for (int d = 1; d < 32; d <<= 1) {
-      long long u = __shfl_up_sync(0xffffffffu, vi, d);
-      if (lane >= d) vi += u;
+  if (t == 0) {
+    long long acc = 0;
+    for (int k = 0; k < SEL_T / 32; k++) {
+      long long v = wsum[k];
+      wsum[k] = acc;
+      acc += v;
     }
-    wsum[lane] = vi - v;
   }
   __syncthreads();
   long long before = wsum[w] + inc - loc;
 #pragma unroll
-  for (int e = 0; e < 4; e++) {
+  for (int e = 0; e < PER; e++) {
     if (c[e] > 0 && before < s.rank && s.rank <= before + c[e]) {
-      found_bin = t * 4 + e;
+      found_bin = t * PER + e;
       found_before = before;
       found_cnt = c[e];
     }
     before += c[e];
   }
   __syncthreads();
-  // clear this instance's histogram for the next level
 #pragma unroll
-  for (int e = 0; e < 4; e++) hg[t * 4 + e] = 0;
+  for (int e = 0; e < PER; e++) hg[t * PER + e] = 0;  // clean for the next level
   if (t == 0) {
-    u128 prefix = ((u128)s.prefix_hi << 64) | (u128)s.prefix_lo;
-    prefix = (prefix << SEL_BITS) | (u128)found_bin;
-    s.prefix_hi = (unsigned long long)(prefix >> 64);
-    s.prefix_lo = (unsigned long long)prefix;
-    s.count_in += found_before;
-    s.rank -= found_before;
-    s.level = level + 1;
-    if (found_cnt == s.rank || s.level == SEL_LEVELS) s.done = 1;
+    cnt_all[id] = 0;
+    if (centred && (found_bin == 0 || found_bin == SEL_BINS - 1)) {
+      s.centred = 0;  // the h-th key left the window: plain levels from the top
+    } else {
+      u128 pre = prefix;
+      if (centred) {
+        pre = (u128)(s.base + (unsigned long long)found_bin - 1ull);
+        s.plen = 24;
+        s.centred = 0;
+      } else {
+        pre = (pre << SEL_BITS) | (u128)found_bin;
+        s.plen += SEL_BITS;
+      }
+      s.prefix_hi = (unsigned long long)(pre >> 64);
+      s.prefix_lo = (unsigned long long)pre;
+      s.count_in += found_before;
+      s.rank -= found_before;
+      if (found_cnt == s.rank || s.plen >= 96) {
+        s.done = 1;
+        s.valid = 1;
+      }
+    }
     st_all[id] = s;
   }
 }
 
+// Membership of every row, the count of rows whose membership changed, and the
+// ordered list of those rows (row + 1 entering, -(row + 1) leaving):
+// CTA x owns rows [x seg_len, (x+1) seg_len) and writes its changed rows, in row
+// order, to list[x seg_len ...] with the count in seg_cnt[x].  The update-based
+// moments then gather only those rows, in a fixed order (deterministic sums).
 __global__ void __launch_bounds__(SEL_T) k_sel_member(const double* __restrict__ d2_all, long long m,
                                                       const int* __restrict__ inst,
                                                       const SelState* __restrict__ st_all,
                                                       uint8_t* __restrict__ mem_new_all,
                                                       const uint8_t* __restrict__ mem_old_all,
-                                                      int* __restrict__ changed) {
+                                                      int* __restrict__ changed, int* __restrict__ list_all,
+                                                      int* __restrict__ seg_cnt_all, long long seg_len) {
   __shared__ int wc[SEL_T / 32];
+  __shared__ int woff[SEL_T / 32 + 1];
   const int id = inst[blockIdx.y];
   const SelState s = st_all[id];
+  if (!s.done) {  // more levels needed: the host relaunches the selection (launch_select_finish)
+    if (blockIdx.x == 0 && threadIdx.x == 0) changed[id] = -1;
+    return;
+  }
   const u128 prefix = ((u128)s.prefix_hi << 64) | (u128)s.prefix_lo;
-  const int sh = 96 - SEL_BITS * s.level;
+  const int sh = 96 - s.plen;
   const double* d2 = d2_all + (long long)id * m;
   uint8_t* mn = mem_new_all + (long long)id * m;
   const uint8_t* mo = mem_old_all + (long long)id * m;
-  int cnt = 0;
-  for (long long i = blockIdx.x * (long long)SEL_T + threadIdx.x; i < m; i += (long long)gridDim.x * SEL_T) {
-    u128 C = composite(d2[i], i);
-    uint8_t in = (C >> sh) <= prefix ? 1 : 0;
-    mn[i] = in;
-    cnt += (in != mo[i]);
+  const long long r_begin = (long long)blockIdx.x * seg_len, r_end = min(m, r_begin + seg_len);
+  int* list = list_all + (long long)id * m + r_begin;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int base = 0;  // entries written by this CTA so far (uniform)
+  for (long long c0 = r_begin; c0 < r_end; c0 += SEL_T) {
+    const long long i = c0 + threadIdx.x;
+    bool ch = false;
+    int entry = 0;
+    if (i < r_end) {
+      u128 C = composite(d2[i], i);
+      const uint8_t in = (C >> sh) <= prefix ? 1 : 0;
+      mn[i] = in;
+      ch = in != mo[i];
+      entry = in ? (int)(i + 1) : -(int)(i + 1);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, ch);
+    if (lane == 0) wc[w] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int k = 0; k < SEL_T / 32; k++) {
+        woff[k] = acc;
+        acc += wc[k];
+      }
+      woff[SEL_T / 32] = acc;
+    }
+    __syncthreads();
+    if (ch) list[base + woff[w] + __popc(bal & ((1u << lane) - 1u))] = entry;
+    base += woff[SEL_T / 32];
+    __syncthreads();
   }
-  for (int d = 16; d > 0; d >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, d);
-  if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = cnt;
-  __syncthreads();
   if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int k = 0; k < SEL_T / 32; k++) tot += wc[k];
-    if (tot) atomicAdd(&changed[id], tot);
+    seg_cnt_all[(long long)id * gridDim.x + blockIdx.x] = base;
+    if (base) atomicAdd(&changed[id], base);  // changed[id] was zeroed by the host before the select
   }
 }
 
+static unsigned sel_grid(long long m, int ninst) {
+  return (unsigned)std::min<long long>((m + SEL_T - 1) / SEL_T, std::max(1, 148 * 4 / std::max(1, ninst)));
+}
+
 void launch_select(const double* d2_all, long long m, long long h, const int* inst, int ninst, SelState* st_all,
-                   unsigned int* hist_all, uint8_t* mem_new_all, const uint8_t* mem_old_all, int* changed,
-                   cudaStream_t st) {
-  k_sel_init<<<ninst, 32, 0, st>>>(inst, st_all, h);
+                   unsigned int* hist_all, unsigned int* cnt_all, uint8_t* mem_new_all, const uint8_t* mem_old_all,
+                   int* changed, int* list_all, int* seg_cnt_all, int nseg, long long seg_len, cudaStream_t st) {
+  k_sel_init<<<ninst, 32, 0, st>>>(inst, st_all, cnt_all, h);
   RTD_LAUNCHED();
-  unsigned gx = (unsigned)std::min<long long>((m + SEL_T - 1) / SEL_T, std::max(1, 148 * 4 / std::max(1, ninst)));
-  for (int L = 0; L < SEL_LEVELS; L++) {
-    k_sel_hist<<<dim3(gx, ninst), SEL_T, 0, st>>>(d2_all, m, inst, st_all, hist_all, L);
-    RTD_LAUNCHED();
-    k_sel_scan<<<ninst, 1024, 0, st>>>(inst, st_all, hist_all, L);
+  const unsigned gx = sel_grid(m, ninst);
+  for (int L = 0; L < SEL_FAST; L++) {
+    k_sel_level<<<dim3(gx, ninst), SEL_T, 0, st>>>(d2_all, m, inst, st_all, hist_all, cnt_all);
     RTD_LAUNCHED();
   }
-  unsigned gm = (unsigned)std::min<long long>((m + SEL_T - 1) / SEL_T, std::max(1, 148 * 8 / std::max(1, ninst)));
-  k_sel_member<<<dim3(gm, ninst), SEL_T, 0, st>>>(d2_all, m, inst, st_all, mem_new_all, mem_old_all, changed);
+  k_sel_member<<<dim3(nseg, ninst), SEL_T, 0, st>>>(d2_all, m, inst, st_all, mem_new_all, mem_old_all, changed,
+                                                     list_all, seg_cnt_all, seg_len);
+  RTD_LAUNCHED();
+}
+
+// the rare case: some instance needed more than SEL_FAST levels (changed[id] == -1 after launch_select)
+void launch_select_finish(const double* d2_all, long long m, const int* inst, int ninst, SelState* st_all,
+                          unsigned int* hist_all, unsigned int* cnt_all, uint8_t* mem_new_all,
+                          const uint8_t* mem_old_all, int* changed, int* list_all, int* seg_cnt_all, int nseg,
+                          long long seg_len, cudaStream_t st) {
+  const unsigned gx = sel_grid(m, ninst);
+  for (int L = SEL_FAST; L < SEL_MAXLEV; L++) {
+    k_sel_level<<<dim3(gx, ninst), SEL_T, 0, st>>>(d2_all, m, inst, st_all, hist_all, cnt_all);
+    RTD_LAUNCHED();
+  }
+  k_sel_member<<<dim3(nseg, ninst), SEL_T, 0, st>>>(d2_all, m, inst, st_all, mem_new_all, mem_old_all, changed,
+                                                     list_all, seg_cnt_all, seg_len);
   RTD_LAUNCHED();
 }
 

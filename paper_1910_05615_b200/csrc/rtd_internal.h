@@ -118,6 +118,9 @@ struct MomArgs {
   const double* AB;         // [block][2] cutoffs (xi mode)
   double* partial;          // [slot][cta][NP]
   int ctas;                 // CTAs per instance
+  const int* list;          // [inst][m] changed rows per segment (+-(row+1)), MOM_DELTA on the tensor pipe
+  const int* seg_cnt;       // [inst][ctas] entries per segment
+  long long seg_len;        // rows per segment (segment x = CTA x)
 };
 int mom_np(int p);  // p + p(p+1)/2 + 1
 void launch_moments(int mode, const MomArgs& a, int ninst, cudaStream_t st);
@@ -127,15 +130,26 @@ void launch_mom_reduce(const double* partial, int ninst, const int* inst, int ct
 
 // ---------------------------------------------------------------- select (k_select.cu)
 struct SelState {
-  unsigned long long prefix_hi;  // composite prefix (up to 96 bits) hi part
+  unsigned long long prefix_hi;  // composite-key prefix of the bin holding the h-th key (plen bits)
   unsigned long long prefix_lo;
   long long rank;                // rank still needed inside the current prefix
-  int level;                     // digits resolved
+  unsigned long long base;       // centred first level: top-24-bit key of bin 1
+  long long count_in;            // keys below the current prefix (diagnostic)
+  int plen;                      // prefix length in bits (0..96)
   int done;
-  long long count_in;            // elements with prefix < current (diagnostic)
+  int valid;                     // done and prefix usable to centre the next step's first level
+  int centred;                   // the next level is the centred 24-bit level
 };
+// Selection of the h smallest (d^2, row) per instance + membership + ordered changed-row lists:
+// list_all[id][seg x at x seg_len] (+-(row+1)), seg_cnt_all[id][nseg]; changed[id] must be zero on
+// entry; changed[id] == -1 on exit means the selection needs launch_select_finish.
+// st_all must be zeroed before the first step of a trajectory (no centring then).
 void launch_select(const double* d2_all, long long m, long long h, const int* inst, int ninst, SelState* st_all,
-                   unsigned int* hist_all, uint8_t* mem_new_all, const uint8_t* mem_old_all, int* changed,
-                   cudaStream_t st);
+                   unsigned int* hist_all, unsigned int* cnt_all, uint8_t* mem_new_all, const uint8_t* mem_old_all,
+                   int* changed, int* list_all, int* seg_cnt_all, int nseg, long long seg_len, cudaStream_t st);
+void launch_select_finish(const double* d2_all, long long m, const int* inst, int ninst, SelState* st_all,
+                          unsigned int* hist_all, unsigned int* cnt_all, uint8_t* mem_new_all,
+                          const uint8_t* mem_old_all, int* changed, int* list_all, int* seg_cnt_all, int nseg,
+                          long long seg_len, cudaStream_t st);
 
 }  // namespace rtd
