@@ -103,7 +103,8 @@ typedef struct {
   /* [host] nullable per-block diagnostics, sized q (block_chosen) or 2q (per (block, start)) */
   int32_t* block_chosen;  /* 0 = wrapping start, 1 = GSSCM start, -1 = block failed */
   int32_t* start_steps;   /* C-steps run (distance passes) per (block, start) */
-  int32_t* start_status;  /* 1 converged, 2 not PD, 3 condition >= kappa_max, 4 max steps, 5 refinement dropped */
+  int32_t* start_status;  /* 1 converged, 2 not PD, 3 condition >= kappa_max, 4 max steps, 5 refinement dropped,
+                             6 skipped (warm start) */
   double* start_logdet;   /* log det of the converged unscaled scatter per (block, start) */
   /* [dev|host] nullable, sized n, in ORIGINAL row order */
   uint8_t* flags;    /* 1 iff RD^2 > cutoff2 under (mu_rew, sigma_rew) */
@@ -135,6 +136,17 @@ size_t rtdetmcd_fit_workspace_size(int64_t n, int32_t p, const rtdetmcd_opts* op
  * X [dev|host]: n x p row-major.  out: any nullable field may be NULL. */
 rtdetmcd_status rtdetmcd_fit(rtdetmcd_ctx* ctx, const double* X, int64_t n, int32_t p, const rtdetmcd_opts* opts,
                              rtdetmcd_result* out);
+
+/* Warm start (the closing note of §4): the same fit, but every block's
+ * C-steps (step 3 of §4) start from (mu0, sigma0) -- typically the previous run's reweighted
+ * estimate (mu_rew, sigma_rew) -- instead of from the two refined initial estimators (steps 1-2,
+ * which are skipped).  mu0 [host] p, sigma0 [host] p*p row-major, in the units the fit reports
+ * (ORIGINAL units of X, after ln when opts->log_transform); they are re-expressed in this run's
+ * standardisation.  A warm start the C-step cannot take (not positive definite, or 1-norm
+ * condition >= kappa_max) drops the block (q = 1: RTD_E_BOTH_STARTS_FAILED).  In the result,
+ * block_chosen = 0 and the (block, 1) entries are unused (start_status 6 = skipped). */
+rtdetmcd_status rtdetmcd_fit_warm(rtdetmcd_ctx* ctx, const double* X, int64_t n, int32_t p, const rtdetmcd_opts* opts,
+                                  const double* mu0, const double* sigma0, rtdetmcd_result* out);
 
 /* Step 10 on its own (the paper's 8.4 ms "flagging" figure,
  * PAPER.md:1624-1627): rd2_i = (x_i - mu)^T sigma^-1 (x_i - mu) by a Cholesky

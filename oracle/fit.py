@@ -140,9 +140,27 @@ def fit_block(Zb: np.ndarray, hb: int, kappa_max: float = 1000.0, max_csteps: in
     return starts, chosen
 
 
+def warm_block(Zb: np.ndarray, mu0: np.ndarray, Sigma0: np.ndarray, hb: int, kappa_max: float = 1000.0,
+               max_csteps: int = 100):
+    """Warm start (§4 closing note): the previous run's reweighted estimate,
+    expressed in this run's standardised units, is the input of step 3 -- the C-steps of
+    PAPER.md:822-827 -- of every block; steps 1-2 (initial estimators, refinement) are skipped.
+    Reading W1: a warm start the C-step cannot take (not PD, condition >= kappa_max) fails the
+    block like a dropped start (reading R10).  Returns (starts, chosen) like fit_block."""
+    try:
+        c = concentrate(Zb, mu0, Sigma0, hb, kappa_max, max_csteps)
+    except (SingularCandidate, NotPositiveDefinite) as e:
+        return [StartResult(ok=False, reason=f"warm: {e}", mu0=mu0, Sigma0=Sigma0)], -1
+    st = StartResult(ok=True, mu0=mu0, Sigma0=Sigma0, H=c.H, mu=c.mu, Sigma=c.Sigma, logdet=c.logdet,
+                     steps=c.steps, converged=c.converged, logdets=c.logdets)
+    return [st], 0
+
+
 def fit(X: np.ndarray, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0,
         kappa_max: float = 1000.0, quantile: float = 0.975, max_csteps: int = 100,
-        log_transform: bool = False, partition_mode: str = "permute") -> FitResult:
+        log_transform: bool = False, partition_mode: str = "permute", warm_start=None) -> FitResult:
+    """warm_start: optional (mu, Sigma) of a previous fit in the units this fit reports (after ln
+    when log_transform) -- the single C-step start of every block (warm_block)."""
     X = np.asarray(X, dtype=np.float64)
     n, p = X.shape
     if not np.all(np.isfinite(X)):
@@ -168,7 +186,12 @@ def fit(X: np.ndarray, h: int | None = None, alpha: float = 0.5, q: int = 1, see
     for l in range(q):
         rows = block_rows(block, pos, l, m)
         Zb = Z[rows]
-        starts, chosen = fit_block(Zb, hb, kappa_max, max_csteps)
+        if warm_start is None:
+            starts, chosen = fit_block(Zb, hb, kappa_max, max_csteps)
+        else:
+            mu_w = (np.asarray(warm_start[0], float) - loc) / scale
+            S_w = np.asarray(warm_start[1], float) / np.outer(scale, scale)
+            starts, chosen = warm_block(Zb, mu_w, S_w, hb, kappa_max, max_csteps)
         bf = BlockFit(block=l, rows=rows, m=m, h=hb, starts=starts, chosen=chosen)
         if chosen >= 0:
             st = starts[chosen]

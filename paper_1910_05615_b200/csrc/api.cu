@@ -26,6 +26,8 @@ void launch_matmul_mma_batch(int p, const double* Zall, long long m, long long b
                              cudaStream_t st);
 void launch_uni_extract_batch(const UniOut* uni, const int* slot_of, int nitems, int p, int which, double* out_all,
                               cudaStream_t st);
+void launch_warm_start(const UniOut* uni, const double* mu_x, const double* sig_x, int p, int q, double* mu_all,
+                       double* sig_all, cudaStream_t st);
 void launch_feistel_fwd(long long n, unsigned long long seed, long long* out, cudaStream_t st);
 void launch_uni_extract(const UniOut* uni, int p, int which, double* out, cudaStream_t st);
 void launch_scatter_u8(const uint8_t* src, const long long* rowmap, long long total, uint8_t* dst, cudaStream_t st);
@@ -510,12 +512,14 @@ struct InitBufs {
   int* inst_dev;
   char* sort_tmp;
   size_t sort_bytes;
+  char* qscratch;
+  double* qv;
   int ctas;
 };
 
 void carve_init(Arena& A, InitBufs& b, int q, long long m, int p) {
-  b.S1 = A.take<double>((size_t)q * M2);
-  b.S2 = A.take<double>((size_t)q * M2);
+  b.S1 = A.take<double>((size_t)2 * q * M2);  // S~1 of all blocks, then S~2 of all blocks (one Jacobi launch)
+  b.S2 = b.S1 ? b.S1 + (size_t)q * M2 : nullptr;
   b.r = A.take<double>((size_t)q * m);
   b.rs = A.take<double>((size_t)q * m);
   b.AB = A.take<double>(2 * (size_t)q);
@@ -527,6 +531,8 @@ void carve_init(Arena& A, InitBufs& b, int q, long long m, int p) {
   b.inst_dev = A.take<int>(q + 8);
   b.sort_bytes = sort_bytes(m);
   b.sort_tmp = A.take<char>(b.sort_bytes);
+  b.qscratch = A.take<char>(quantile_scratch_bytes(q));
+  b.qv = A.take<double>((size_t)q * 6);
 }
 
 void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int p, int q, long long blk_stride) {
@@ -551,13 +557,17 @@ void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int
   launch_sums_to_cov(b.inst_dev, q, b.sums, np, nullptr, p, (double)m, 1.0, b.mudummy, b.S1, st);
   // S~2: norms, type-7 cutoffs, xi^2-weighted second moment / n
   launch_norms(Z, m, p, q, blk_stride, b.r, st);
-  for (int l = 0; l < q; l++) {
+  // exact order statistics of the norms by bucketing (k_quantile.cu); blocks with massive ties are sorted
+  std::vector<int> fb;
+  launch_quantiles(b.r, m, q, b.qscratch, b.qv, st, fb);
+  for (int l : fb) {
     size_t bytes = b.sort_bytes;
     count_sort();
     RTD_CU(cub::DeviceRadixSort::SortKeys(b.sort_tmp, bytes, b.r + (size_t)l * m, b.rs + (size_t)l * m, (int)m, 0, 64,
                                           st));
+    launch_q_from_sorted(b.rs + (size_t)l * m, m, l, b.qv, st);
   }
-  launch_lr_cutoffs(b.rs, q, m, b.AB, b.abok, st);
+  launch_q_cutoffs(b.qv, m, q, b.AB, b.abok, st);
   a.r = b.r;
   a.AB = b.AB;
   moments(MOM_XI, a, q, st);
@@ -590,6 +600,7 @@ struct FitBufs {
   uint8_t *flags_d, *weights_d, *hsub_d;
   double* rd2_d;
   int* chosen_dev;
+  double *warm_mu, *warm_sig;  // warm start (X units), device copies
 };
 
 void carve_fit(Arena& A, FitBufs& f, const Dims& d, const rtdetmcd_opts& o, bool need_flags, bool need_rd2,
@@ -614,7 +625,7 @@ void carve_fit(Arena& A, FitBufs& f, const Dims& d, const rtdetmcd_opts& o, bool
   f.mu_raw = A.take<double>(RTD_MAXP);
   f.sig_raw = A.take<double>(M2);
   f.keys = A.take<double>(std::max(q, q_agg));
-  f.agg_scratch = A.take<double>(2 * M2);
+  f.agg_scratch = A.take<double>(3 * M2);  // pooling Lambda + entrywise median [p + p*p]
   f.mu_rew = A.take<double>(RTD_MAXP);
   f.sig_rew = A.take<double>(M2);
   f.sums_rw = A.take<double>((size_t)std::max(q, q_agg) * NPMAX);
@@ -626,6 +637,8 @@ void carve_fit(Arena& A, FitBufs& f, const Dims& d, const rtdetmcd_opts& o, bool
   f.st1 = A.take<int>(8);
   f.mu_blk = A.take<double>((size_t)std::max(q, q_agg) * RTD_MAXP);
   f.chosen_dev = A.take<int>(q + 8);
+  f.warm_mu = A.take<double>(RTD_MAXP);
+  f.warm_sig = A.take<double>(M2);
   f.flags_d = need_flags ? A.take<uint8_t>(n) : nullptr;
   f.rd2_d = need_rd2 ? A.take<double>(n) : nullptr;
   f.weights_d = need_w ? A.take<uint8_t>(n) : nullptr;
@@ -683,13 +696,13 @@ void phase_columns(cudaStream_t st, const double* Xdev, long long n, int p, int 
 
 // H2-H9 for the q blocks already in f.Z: starts, refinement, C-steps, start choice, c(alpha) scaling.
 // Leaves mu_blk[b] / sigraw_blk[b] (standardised units) for the valid blocks and f.chosen_dev.
-BlockResult phase_blocks(cudaStream_t st, FitBufs& f, const Dims& d, const rtdetmcd_opts& o) {
+// H2-H4: S~1, S~2, their eigenvectors and the refinement of every start -> cb.mu / cb.sigma; status per start
+std::vector<int> phase_starts(cudaStream_t st, FitBufs& f, const Dims& d, const rtdetmcd_opts& o) {
   const int p = d.p, q = d.q;
   const long long m = d.m, blk_stride = (long long)p * m;
   BlockResult r;
   run_initial(st, f.ib, f.Z, m, p, q, blk_stride);
-  launch_jacobi(f.ib.S1, q, p, o.kappa_max, f.V2, f.lam2, f.jok, st);
-  launch_jacobi(f.ib.S2, q, p, o.kappa_max, f.V2 + (size_t)q * M2, f.lam2 + (size_t)q * RTD_MAXP, f.jok + q, st);
+  launch_jacobi(f.ib.S1, 2 * q, p, o.kappa_max, f.V2, f.lam2, f.jok, st);  // [k q + b]: S~1 blocks, then S~2
   std::vector<int> jok(2 * q), abok(q);
   d2h(st, jok.data(), f.jok, 2 * q * sizeof(int));
   d2h(st, abok.data(), f.ib.abok, q * sizeof(int));
@@ -707,6 +720,14 @@ BlockResult phase_blocks(cudaStream_t st, FitBufs& f, const Dims& d, const rtdet
   std::vector<int> rok = refine_batch(st, f.rb, f.Z, blk_stride, m, p, ninst, blk, active, Vsrc, f.cb.mu, f.cb.sigma);
   for (int id = 0; id < ninst; id++)
     if (!rok[id]) r.status[id] = ST_REFINE;
+  return r.status;
+}
+
+// H5-H9: C-steps of the active starts, start choice, c(alpha) scaling -> mu_blk / sigraw_blk, chosen_dev
+BlockResult phase_csteps_choose(cudaStream_t st, FitBufs& f, const Dims& d, const rtdetmcd_opts& o, BlockResult r) {
+  const int p = d.p, q = d.q;
+  const long long m = d.m, blk_stride = (long long)p * m;
+  const int ninst = 2 * q;
   run_csteps(st, f.cb, f.Z, blk_stride, 2, ninst, d.hb, o.kappa_max, o.max_csteps, o.refresh_every, r.status,
              r.steps);
   r.logdet.resize(ninst);
@@ -717,7 +738,8 @@ BlockResult phase_blocks(cudaStream_t st, FitBufs& f, const Dims& d, const rtdet
   for (int b = 0; b < q; b++) {
     bool u0 = r.status[2 * b] == ST_CONVERGED || r.status[2 * b] == ST_MAXSTEPS;
     bool u1 = r.status[2 * b + 1] == ST_CONVERGED || r.status[2 * b + 1] == ST_MAXSTEPS;
-    if (!u0 || !u1) r.warnings |= RTD_W_START_FAILED;
+    if ((!u0 && r.status[2 * b] != ST_SKIPPED) || (!u1 && r.status[2 * b + 1] != ST_SKIPPED))
+      r.warnings |= RTD_W_START_FAILED;
     int ch = -1;
     if (u0) ch = 0;
     if (u1 && (!u0 || r.logdet[2 * b + 1] < r.logdet[2 * b])) ch = 1;
@@ -737,6 +759,23 @@ BlockResult phase_blocks(cudaStream_t st, FitBufs& f, const Dims& d, const rtdet
                            RTD_MAXP * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
   return r;
+}
+
+// warm (reading W1): the previous fit (f.warm_mu / f.warm_sig, X units, already on
+// the device) is the single C-step start of every block; the initial estimators and the refinement are
+// skipped and start 1 of each block is marked ST_SKIPPED.
+BlockResult phase_blocks(cudaStream_t st, FitBufs& f, const Dims& d, const rtdetmcd_opts& o, bool warm = false) {
+  const int p = d.p, q = d.q;
+  const long long m = d.m, blk_stride = (long long)p * m;
+  BlockResult r;
+  if (warm) {
+    launch_warm_start(f.uni, f.warm_mu, f.warm_sig, p, q, f.cb.mu, f.cb.sigma, st);
+    r.status.assign(2 * q, ST_ACTIVE);
+    for (int b = 0; b < q; b++) r.status[2 * b + 1] = ST_SKIPPED;
+  } else {
+    r.status = phase_starts(st, f, d, o);
+  }
+  return phase_csteps_choose(st, f, d, o, r);
 }
 
 // H9/H10: raw fit from the valid block fits in mu_blk / sigraw_blk (q == 1: the block fit itself)
@@ -812,7 +851,8 @@ double phase_pool(cudaStream_t st, FitBufs& f, int p, int q, double quantile, co
   return kw;
 }
 
-void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetmcd_opts& o, rtdetmcd_result* out) {
+void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetmcd_opts& o, rtdetmcd_result* out,
+              const double* warm_mu = nullptr, const double* warm_sigma = nullptr) {
   cudaStream_t st = c->stream;
   const bool x_host = !is_device_ptr(X);
   Dims d = make_dims(n, p, o, x_host);
@@ -852,7 +892,15 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
   }
 
   // H2-H9 per block, H10 raw fit
-  BlockResult br = phase_blocks(st, f, d, o);
+  const bool warm = warm_mu != nullptr;
+  if (warm) {
+    std::vector<double> wm(RTD_MAXP, 0.0), ws(M2, 0.0);
+    for (int j = 0; j < p; j++) wm[j] = warm_mu[j];
+    for (int e = 0; e < p * p; e++) ws[e] = warm_sigma[e];
+    h2d(st, f.warm_mu, wm.data(), RTD_MAXP * sizeof(double));
+    h2d(st, f.warm_sig, ws.data(), M2 * sizeof(double));
+  }
+  BlockResult br = phase_blocks(st, f, d, o, warm);
   warnings |= br.warnings;
   const int n_kept = phase_raw(st, f, p, q, m, br.valid_ids);
 
@@ -1068,6 +1116,20 @@ rtdetmcd_status rtdetmcd_fit(rtdetmcd_ctx* c, const double* X, int64_t n, int32_
     if (opts) o = *opts; else rtdetmcd_opts_default(&o);
     drop_session(c);
     fit_impl(c, X, n, p, o, out);
+  });
+}
+
+rtdetmcd_status rtdetmcd_fit_warm(rtdetmcd_ctx* c, const double* X, int64_t n, int32_t p, const rtdetmcd_opts* opts,
+                                  const double* mu0, const double* sigma0, rtdetmcd_result* out) {
+  return guarded(c, [&] {
+    if (!X || !mu0 || !sigma0) throw Fail{RTD_E_INVALID_ARG, "X, mu0 and sigma0 are required"};
+    if (is_device_ptr(mu0) || is_device_ptr(sigma0)) throw Fail{RTD_E_INVALID_ARG, "mu0 / sigma0 must be host memory"};
+    for (int e = 0; e < (p >= 1 && p <= RTD_MAXP ? p * p : 0); e++)
+      if (!std::isfinite(sigma0[e])) throw Fail{RTD_E_INVALID_ARG, "sigma0 is not finite"};
+    rtdetmcd_opts o;
+    if (opts) o = *opts; else rtdetmcd_opts_default(&o);
+    drop_session(c);
+    fit_impl(c, X, n, p, o, out, mu0, sigma0);
   });
 }
 

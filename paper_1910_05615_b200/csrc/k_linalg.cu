@@ -235,21 +235,21 @@ __global__ void __launch_bounds__(LT) k_jacobi(const double* __restrict__ A_all,
       tot += v;
       if (i != j) off += v;
     }
-    red[t] = off;
-    __syncthreads();
-    if (t == 0) {
-      double so = 0.0;
-      for (int k = 0; k < blockDim.x; k++) so += red[k];
-      red[0] = so;
+    for (int d = 16; d > 0; d >>= 1) {
+      off += __shfl_down_sync(0xffffffffu, off, d);
+      tot += __shfl_down_sync(0xffffffffu, tot, d);
+    }
+    if ((t & 31) == 0) {
+      red[t >> 5] = off;
+      red[32 + (t >> 5)] = tot;
     }
     __syncthreads();
-    double so = red[0];
-    __syncthreads();
-    red[t] = tot;
-    __syncthreads();
     if (t == 0) {
-      double st = 0.0;
-      for (int k = 0; k < blockDim.x; k++) st += red[k];
+      double so = 0.0, st = 0.0;
+      for (int k = 0; k < LT / 32; k++) {
+        so += red[k];
+        st += red[32 + k];
+      }
       s_stop = (so <= 1e-32 * st) || so == 0.0;
     }
     __syncthreads();
@@ -420,65 +420,82 @@ void launch_lr_cutoffs(const double* rs_all, int nb, long long m, double* AB, in
 // ------------------------------------------------------------------ aggregation of q block fits (K11)
 // in: mu[b][MAXP], sig[b][MAXP^2] for nv valid blocks (ids ascending), m rows per block.
 // out: mu_raw, sigma_raw; kept[b] flags; keys[b]
-__global__ void __launch_bounds__(LT) k_aggregate(const double* __restrict__ mu_base, const double* __restrict__ sig_base,
-                                                  const int* __restrict__ ids, int nv, int p, double m, double* __restrict__ mu_out,
-                                                  double* __restrict__ sig_out, int* __restrict__ kept,
-                                                  double* __restrict__ keys, double* __restrict__ scratch) {
-  __shared__ double A[RTD_MAXP * LD], L[RTD_MAXP * LD], Li[RTD_MAXP * LD];
-  __shared__ double mmed[RTD_MAXP], red[RTD_MAXP];
-  __shared__ int s_fail;
-  __shared__ int s_order[256];
-  const int t = threadIdx.x;
-#define mu_all_l(l) (mu_base + (long long)ids[l] * RTD_MAXP)
-#define sig_all_l(l) (sig_base + (long long)ids[l] * RTD_MAXP * RTD_MAXP)
-  // entrywise median (even count -> mean of the two middle values); scratch holds Sigma_med
-  double* smed = scratch;
-  for (int e = t; e < p + p * p; e += blockDim.x) {
-    double v[256];
-    int cnt = 0;
+// (a) entrywise median over the nv valid fits (even count -> mean of the two middle values, R14):
+//     one thread per entry, order statistics by counting (no per-thread arrays, any nv)
+__global__ void __launch_bounds__(LT) k_agg_median(const double* __restrict__ mu_base, const double* __restrict__ sig_base,
+                                                   const int* __restrict__ ids, int nv, int p,
+                                                   double* __restrict__ med /* [p + p*p] */) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p + p * p) return;
+  auto val = [&](int l) {
+    return e < p ? mu_base[(long long)ids[l] * RTD_MAXP + e] : sig_base[(long long)ids[l] * RTD_MAXP * RTD_MAXP + e - p];
+  };
+  // k-th smallest (0-based) with ties: the value x_l with #{x < x_l} <= k < #{x <= x_l}
+  auto kth = [&](int k) {
+    double r = 0.0;
     for (int l = 0; l < nv; l++) {
-      double x = e < p ? mu_all_l(l)[e] : sig_all_l(l)[e - p];
-      int j = cnt - 1;
-      while (j >= 0 && v[j] > x) { v[j + 1] = v[j]; j--; }
-      v[j + 1] = x;
-      cnt++;
-    }
-    double med = (nv & 1) ? v[nv / 2] : 0.5 * (v[nv / 2 - 1] + v[nv / 2]);
-    if (e < p) mmed[e] = med; else smed[e - p] = med;
-  }
-  __syncthreads();
-  // KL' key per block: tr(S_med S_l^-1) + log det S_l + (mu_med - mu_l)^T S_l^-1 (mu_med - mu_l)
-  for (int l = 0; l < nv; l++) {
-    const double* S = sig_all_l(l);
-    for (int e = t; e < p * p; e += blockDim.x) A[(e / p) * LD + e % p] = S[e];
-    __syncthreads();
-    bool ok = block_cholesky(A, L, p, &s_fail);
-    if (!ok) {
-      if (t == 0) keys[l] = INFINITY;
-      __syncthreads();
-      continue;
-    }
-    block_tri_inverse(L, Li, p);
-    block_inv_from_li(Li, A, p);  // A = S_l^-1
-    if (t == 0) {
-      double tr = 0.0;
-      for (int i = 0; i < p; i++)
-        for (int k = 0; k < p; k++) tr += smed[i * p + k] * A[k * LD + i];
-      double ld = 0.0;
-      for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
-      ld *= 2.0;
-      const double* mu = mu_all_l(l);
-      double quad = 0.0;
-      for (int i = 0; i < p; i++) {
-        double s = 0.0;
-        for (int k = 0; k < p; k++) s += A[i * LD + k] * (mmed[k] - mu[k]);
-        quad += (mmed[i] - mu[i]) * s;
+      const double x = val(l);
+      int lt = 0, le = 0;
+      for (int u = 0; u < nv; u++) {
+        const double y = val(u);
+        lt += y < x;
+        le += y <= x;
       }
-      keys[l] = tr + ld + quad;
+      if (lt <= k && k < le) r = x;
     }
-    __syncthreads();
+    return r;
+  };
+  med[e] = (nv & 1) ? kth(nv / 2) : 0.5 * (kth(nv / 2 - 1) + kth(nv / 2));
+}
+
+// (b) KL' key of every fit, one CTA per fit: tr(S_med S_l^-1) + log det S_l + (mu_med - mu_l)^T S_l^-1 (...)
+//     (reading R15; INFINITY when S_l is not positive definite)
+__global__ void __launch_bounds__(LT) k_agg_keys(const double* __restrict__ mu_base, const double* __restrict__ sig_base,
+                                                 const int* __restrict__ ids, int p, const double* __restrict__ med,
+                                                 double* __restrict__ keys) {
+  __shared__ double A[RTD_MAXP * LD], L[RTD_MAXP * LD], Li[RTD_MAXP * LD];
+  __shared__ double dm[RTD_MAXP], red[LT / 32];
+  __shared__ int s_fail;
+  const int l = blockIdx.x, t = threadIdx.x;
+  const double* S = sig_base + (long long)ids[l] * RTD_MAXP * RTD_MAXP;
+  const double* mu = mu_base + (long long)ids[l] * RTD_MAXP;
+  for (int e = t; e < p * p; e += blockDim.x) A[(e / p) * LD + e % p] = S[e];
+  for (int k = t; k < p; k += blockDim.x) dm[k] = med[k] - mu[k];
+  __syncthreads();
+  if (!block_cholesky(A, L, p, &s_fail)) {
+    if (t == 0) keys[l] = INFINITY;
+    return;
   }
-  // keep ceil(nv/2) smallest keys (ties -> lower block position), pool in block order
+  block_tri_inverse(L, Li, p);
+  block_inv_from_li(Li, A, p);  // A = S_l^-1
+  const double* smed = med + p;
+  double part = 0.0;
+  for (int e = t; e < p * p; e += blockDim.x) {
+    const int i = e / p, k = e - i * p;
+    part += smed[i * p + k] * A[k * LD + i] + dm[i] * A[i * LD + k] * dm[k];
+  }
+  if (t < p) part += 2.0 * log(L[t * LD + t]);
+  for (int d = 16; d > 0; d >>= 1) part += __shfl_down_sync(0xffffffffu, part, d);
+  if ((t & 31) == 0) red[t >> 5] = part;
+  __syncthreads();
+  if (t == 0) {
+    double k = 0.0;
+    for (int w = 0; w < LT / 32; w++) k += red[w];
+    keys[l] = k;
+  }
+}
+
+// (c) keep ceil(nv/2) smallest keys (ties -> lower block position), single-pass pooling (eqs. covpool)
+//     in block order with weight m (reading R15)
+__global__ void __launch_bounds__(LT) k_agg_pool(const double* __restrict__ mu_base, const double* __restrict__ sig_base,
+                                                 const int* __restrict__ ids, int nv, int p, double m,
+                                                 const double* __restrict__ keys, double* __restrict__ mu_out,
+                                                 double* __restrict__ sig_out, int* __restrict__ kept,
+                                                 double* __restrict__ scratch) {
+  __shared__ int s_order[1024];
+  __shared__ double mup[RTD_MAXP], dmu[RTD_MAXP];
+  __shared__ double np_s;
+  const int t = threadIdx.x;
   if (t == 0) {
     for (int l = 0; l < nv; l++) s_order[l] = l;
     for (int i = 1; i < nv; i++) {
@@ -491,15 +508,12 @@ __global__ void __launch_bounds__(LT) k_aggregate(const double* __restrict__ mu_
     for (int i = 0; i < keep; i++) kept[s_order[i]] = 1;
   }
   __syncthreads();
-  // single-pass pooling (eqs. covpool) in block order
-  double* Lam = scratch + RTD_MAXP * RTD_MAXP;
-  __shared__ double mup[RTD_MAXP], dmu[RTD_MAXP];
-  __shared__ double np_s;
+  double* Lam = scratch;
   int first = 1;
   for (int l = 0; l < nv; l++) {
     if (!kept[l]) continue;
-    const double* S = sig_all_l(l);
-    const double* mu = mu_all_l(l);
+    const double* S = sig_base + (long long)ids[l] * RTD_MAXP * RTD_MAXP;
+    const double* mu = mu_base + (long long)ids[l] * RTD_MAXP;
     if (first) {
       for (int e = t; e < p * p; e += blockDim.x) Lam[e] = (m - 1.0) * S[e];
       for (int k = t; k < p; k += blockDim.x) mup[k] = mu[k];
@@ -523,14 +537,17 @@ __global__ void __launch_bounds__(LT) k_aggregate(const double* __restrict__ mu_
   }
   for (int k = t; k < p; k += blockDim.x) mu_out[k] = mup[k];
   for (int e = t; e < p * p; e += blockDim.x) sig_out[e] = Lam[e] / (np_s - 1.0);
-  (void)red;
-#undef mu_all_l
-#undef sig_all_l
 }
 
 void launch_aggregate(const double* mu_base, const double* sig_base, const int* ids, int nv, int p, double m,
                       double* mu_out, double* sig_out, int* kept, double* keys, double* scratch, cudaStream_t st) {
-  k_aggregate<<<1, LT, 0, st>>>(mu_base, sig_base, ids, nv, p, m, mu_out, sig_out, kept, keys, scratch);
+  if (nv > 1024) throw std::string("aggregate: at most 1024 blocks");
+  double* med = scratch + RTD_MAXP * RTD_MAXP;  // [p + p*p] after the pooling scratch
+  k_agg_median<<<(p + p * p + LT - 1) / LT, LT, 0, st>>>(mu_base, sig_base, ids, nv, p, med);
+  RTD_LAUNCHED();
+  k_agg_keys<<<nv, LT, 0, st>>>(mu_base, sig_base, ids, p, med, keys);
+  RTD_LAUNCHED();
+  k_agg_pool<<<1, LT, 0, st>>>(mu_base, sig_base, ids, nv, p, m, keys, mu_out, sig_out, kept, scratch);
   RTD_LAUNCHED();
 }
 

@@ -51,6 +51,27 @@ void launch_uni_extract(const UniOut* uni, int p, int which, double* out, cudaSt
   RTD_LAUNCHED();
 }
 
+// warm start: the previous fit (mu, Sigma) in X units -> this run's standardised
+// units, written as start 0 of every block: mu_z = (mu - loc) / scale, Sigma_z = Sigma / (scale scale^T)
+__global__ void k_warm_start(const UniOut* __restrict__ uni, const double* __restrict__ mu_x,
+                             const double* __restrict__ sig_x, int p, double* __restrict__ mu_all,
+                             double* __restrict__ sig_all) {
+  const int b = blockIdx.x;
+  double* mu = mu_all + (long long)(2 * b) * RTD_MAXP;
+  double* sg = sig_all + (long long)(2 * b) * RTD_MAXP * RTD_MAXP;
+  for (int k = threadIdx.x; k < p; k += blockDim.x) mu[k] = __ddiv_rn(__dsub_rn(mu_x[k], uni[k].loc), uni[k].scale);
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int i = e / p, j = e - i * p;
+    sg[e] = __ddiv_rn(sig_x[e], __dmul_rn(uni[i].scale, uni[j].scale));
+  }
+}
+
+void launch_warm_start(const UniOut* uni, const double* mu_x, const double* sig_x, int p, int q, double* mu_all,
+                       double* sig_all, cudaStream_t st) {
+  k_warm_start<<<q, 256, 0, st>>>(uni, mu_x, sig_x, p, mu_all, sig_all);
+  RTD_LAUNCHED();
+}
+
 // batched: item i (uni columns [i p, (i+1) p)) -> out_all[slot_of[i]][j]
 __global__ void k_uni_extract_batch(const UniOut* __restrict__ uni, const int* __restrict__ slot_of, int p, int which,
                                     double* __restrict__ out_all) {

@@ -169,21 +169,35 @@ void launch_moments(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
   RTD_LAUNCHED();
 }
 
-__global__ void k_mom_reduce(const double* __restrict__ partial, const int* __restrict__ inst, int ctas, int np,
-                             double* __restrict__ out, int accumulate) {
-  const int slot = blockIdx.x;
+// Fixed-order (deterministic) sum of the per-CTA partials: CTA (x, slot) owns 32 consecutive
+// entries; warp w sums the partials of CTAs w, w+8, w+16, ... and the 8 warp sums are added in
+// warp order.
+__global__ void __launch_bounds__(256) k_mom_reduce(const double* __restrict__ partial, const int* __restrict__ inst,
+                                                    int ctas, int np, double* __restrict__ out, int accumulate) {
+  __shared__ double ws[8][32];
+  const int slot = blockIdx.y;
   const int id = inst[slot];
-  for (int e = threadIdx.x; e < np; e += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < ctas; c++) s += partial[((long long)slot * ctas + c) * np + e];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (e < np) {
+    const double* src = partial + (long long)slot * ctas * np + e;
+#pragma unroll 4
+    for (int c = w; c < ctas; c += 8) s += src[(long long)c * np];
+  }
+  ws[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && e < np) {
+    double t = ws[0][lane];
+    for (int k = 1; k < 8; k++) t += ws[k][lane];
     double* o = out + (long long)id * np + e;
-    *o = accumulate ? *o + s : s;
+    *o = accumulate ? *o + t : t;
   }
 }
 
 void launch_mom_reduce(const double* partial, int ninst, const int* inst, int ctas, int np, double* out,
                        int accumulate, cudaStream_t st) {
-  k_mom_reduce<<<ninst, 256, 0, st>>>(partial, inst, ctas, np, out, accumulate);
+  k_mom_reduce<<<dim3((np + 31) / 32, ninst), 256, 0, st>>>(partial, inst, ctas, np, out, accumulate);
   RTD_LAUNCHED();
 }
 

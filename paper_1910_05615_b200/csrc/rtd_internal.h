@@ -100,6 +100,15 @@ void launch_flag(int p, const double* X, long long n, int log_transform, double 
                  cudaStream_t st);
 void launch_norms(const double* Z, long long m, int p, int nblk, long long blk_stride, double* r, cudaStream_t st);
 
+// ---------------------------------------------------------------- norm quantiles (k_quantile.cu)
+size_t quantile_scratch_bytes(int nb);
+// qv[nb][6] = order statistics j, j+1 of the type-7 positions (m-1){.25,.5,.75} of r_all[b][0..m);
+// fallback = blocks whose target bucket overflowed (the caller sorts them, launch_q_from_sorted)
+void launch_quantiles(const double* r_all, long long m, int nb, char* scratch, double* qv, cudaStream_t st,
+                      std::vector<int>& fallback);
+void launch_q_from_sorted(const double* sorted, long long m, int b, double* qv, cudaStream_t st);
+void launch_q_cutoffs(const double* qv, long long m, int nb, double* AB, int* ok, cudaStream_t st);
+
 // ---------------------------------------------------------------- moments (k_moments.cu)
 enum MomMode { MOM_WRAP = 0, MOM_XI = 1, MOM_MEMBER = 2, MOM_DELTA = 3, MOM_REWEIGHT = 4 };
 struct MomArgs {

@@ -6,7 +6,7 @@
 
 namespace rtd {
 
-enum InstStatus { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_NOT_PD = 2, ST_COND = 3, ST_MAXSTEPS = 4, ST_REFINE = 5 };
+enum InstStatus { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_NOT_PD = 2, ST_COND = 3, ST_MAXSTEPS = 4, ST_REFINE = 5, ST_SKIPPED = 6 };
 
 void launch_prepare(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p, double kappa_max,
                     double* cstage, int cstride, double* logdet_out, double* cond_out, int* status_out, double* traj,

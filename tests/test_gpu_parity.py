@@ -112,6 +112,20 @@ def test_initial_estimators(cfg, n):
     assert rel_sigma(S2, gsscm_lr(Z)) < 1e-12
 
 
+def test_initial_estimators_tied_norms_and_large_block():
+    """Norm quantiles (S~2 cut-offs): heavy ties force the sorting fall-back of the bucket
+    order statistics; a 1M-row block exercises the bucket path at bench size."""
+    rng = np.random.default_rng(11)
+    Zt = rng.integers(-2, 3, size=(30_000, 5)).astype(np.float64)
+    Zt[:, 4] += 0.5
+    Zl = rng.standard_normal((1_000_000, 7))
+    for Z in (Zt, Zl):
+        S1, S2, ok = api.initial(_cuda(Z))
+        assert ok
+        assert rel_sigma(S1, wrapped_covariance(Z)) < 1e-12
+        assert rel_sigma(S2, gsscm_lr(Z)) < 1e-12
+
+
 @pytest.mark.parametrize("cfg,n", [(1, 1000), (2, 20_000), (3, 30_001), (4, 12_345), (5, 20_000)])
 def test_refinement(cfg, n):
     d, Z = _zblock(cfg, n)

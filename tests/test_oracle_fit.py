@@ -152,3 +152,32 @@ def test_config4_recipe_cluster_absorbed():
     assert not np.isin(b.rows[clean.H], cl).any()
     assert np.isin(b.rows[st.H], cl).mean() > 0.05
     assert st.logdet < clean.logdet - 1.0
+
+
+def test_warm_start_from_cold_raw_fit_reproduces_it():
+    """A warm start at the cold fit's own raw estimate: its h-subset is a C-step fixed point
+     and a positive multiple of Sigma ranks distances identically, so the
+    first C-step returns the same subset and the warm fit equals the cold fit exactly."""
+    d = datagen.make_config(1)
+    cold = F.fit(d.X, h=d.h)
+    warm = F.fit(d.X, h=d.h, warm_start=(cold.mu_raw, cold.Sigma_raw))
+    st_c = cold.blocks[0].starts[cold.blocks[0].chosen]
+    st_w = warm.blocks[0].starts[0]
+    assert np.array_equal(st_c.H, st_w.H) and st_w.steps == 2  # one C-step + the pass confirming H_new == H_old
+    assert np.allclose(warm.Sigma_rew, cold.Sigma_rew, rtol=1e-13, atol=1e-15)
+    assert np.array_equal(warm.flags, cold.flags)
+
+
+def test_warm_start_stream_and_failure():
+    """Config 5 stream: batch 1 warm-started from batch 0's reweighted fit flags the 2% shifted rows
+    like the cold fit; a singular warm start fails the block (reading W1)."""
+    b0, b1 = datagen.make_config(5, batch=0), datagen.make_config(5, batch=1)
+    f0 = F.fit(b0.X, h=b0.h, log_transform=True)
+    cold = F.fit(b1.X, h=b1.h, log_transform=True)
+    warm = F.fit(b1.X, h=b1.h, log_transform=True, warm_start=(f0.mu_rew, f0.Sigma_rew))
+    assert warm.flags[b1.outliers].mean() > 0.97
+    assert (warm.flags == cold.flags).mean() > 0.995
+    p = b1.X.shape[1]
+    with pytest.raises(F.FitError) as e:
+        F.fit(b1.X, h=b1.h, log_transform=True, warm_start=(f0.mu_rew, np.zeros((p, p))))
+    assert e.value.code == "BOTH_STARTS_FAILED"
