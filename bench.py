@@ -188,6 +188,19 @@ def run_stream(args, local: int):
         g1.record(stream)
         torch.cuda.synchronize()
     k1, s1 = api.counters()
+    # warm-started stream: batch b's C-steps start from batch b-1's reweighted fit
+    # (the previous batch's own result from the chain; batch 0's cold fit seeds it)
+    wdev = []
+    prev = (res0 := one(Xd[0])).mu_rew, res0.sigma_rew
+    torch.cuda.synchronize()
+    for b in range(1, nb):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rw = one(Xd[b], warm_start=prev)
+        e1.record(stream)
+        e1.synchronize()
+        wdev.append(e0.elapsed_time(e1))
+        prev = (rw.mu_rew, rw.sigma_rew)
     # kernel breakdown / roofline from a separate profiled pass (per-kernel events stay out of the latencies)
     nprof = min(nb, 100)
     api.set_profiling(True, device=local)
@@ -231,6 +244,11 @@ def run_stream(args, local: int):
             "latency_ms": {"p50": float(np.percentile(dev_ms, 50)), "p99": float(np.percentile(dev_ms, 99)),
                            "wall_p50": float(np.percentile(wall, 50)), "wall_p99": float(np.percentile(wall, 99)),
                            "max": float(dev_ms.max())},
+            "warm_start": {"latency_ms": {"p50": float(np.percentile(wdev, 50)), "p99": float(np.percentile(wdev, 99))},
+                           "value": n * len(wdev) / (sum(wdev) / 1e3), "unit": "obs/s",
+                           "note": "each batch's C-steps start from the previous batch's reweighted fit "
+                                   "(PAPER.md:1038-1043); initial estimators and refinement skipped"}
+            if wdev else None,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cb, "gpu_launches": int(k1 - k0), "cub_sorts": int(s1 - s0),
             "clocks": clk.summary(), "breakdown": _breakdown(prof, nprof),
             "fit": {"start_steps": [int(x) for x in res.start_steps]}}

@@ -138,8 +138,13 @@ def workspace_size(n: int, p: int, **opts) -> int:
 def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, kappa_max: float = 1000.0,
         quantile: float = 0.975, max_csteps: int = 100, refresh_every: int = 32, partition: int = 0,
         log_transform: bool = False, outputs=("flags", "rd2", "weights", "hsubset"), device: int | None = None,
-        torch_workspace: bool = True, out_buffers: dict | None = None, ctx: dict | None = None) -> Fit:
-    """rtdetmcd_fit on an n x p row-major float64 matrix (numpy or torch, host or device)."""
+        torch_workspace: bool = True, out_buffers: dict | None = None, ctx: dict | None = None,
+        warm_start=None) -> Fit:
+    """rtdetmcd_fit on an n x p row-major float64 matrix (numpy or torch, host or device).
+
+    warm_start=(mu, sigma): rtdetmcd_fit_warm -- the C-steps of every block start from this
+    previous fit (X units, after ln when log_transform) instead of the refined initial estimators.
+    """
     ptr, keep, is_cuda, dev = _as_f64(X)
     n, p = int(keep.shape[0]), int(keep.shape[1])
     dev = dev if device is None else device
@@ -178,7 +183,13 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
             buf, bp = _out_buffer(n, dt, is_cuda, dev)
             rows[k] = buf
             setattr(r, k, bp)
-    rc = L.rtdetmcd_fit(ctx["h"], C.c_void_p(ptr), n, p, C.byref(o), C.byref(r))
+    if warm_start is None:
+        rc = L.rtdetmcd_fit(ctx["h"], C.c_void_p(ptr), n, p, C.byref(o), C.byref(r))
+    else:
+        wm = np.ascontiguousarray(warm_start[0], dtype=np.float64).reshape(p)
+        wS = np.ascontiguousarray(warm_start[1], dtype=np.float64).reshape(p, p)
+        rc = L.rtdetmcd_fit_warm(ctx["h"], C.c_void_p(ptr), n, p, C.byref(o), C.c_void_p(wm.ctypes.data),
+                                 C.c_void_p(wS.ctypes.data), C.byref(r))
     if torch_workspace:
         L.rtdetmcd_set_workspace(ctx["h"], None, 0)
     _check(rc, ctx)

@@ -300,3 +300,39 @@ def test_fit_deterministic():
     g2 = api.fit(_cuda(d.X), alpha=0.75)
     assert np.array_equal(g1.sigma_rew, g2.sigma_rew) and np.array_equal(g1.mu_raw, g2.mu_raw)
     assert torch.equal(g1.flags, g2.flags) and torch.equal(g1.rd2, g2.rd2)
+
+
+# ------------------------------------------------------------------ warm start
+def test_fit_warm_stream_matches_oracle():
+    b0, b1 = datagen.make_config(5, batch=0), datagen.make_config(5, batch=1)
+    f0 = ofit.fit(b0.X, h=b0.h, log_transform=True)
+    ws = (f0.mu_rew, f0.Sigma_rew)
+    o = ofit.fit(b1.X, h=b1.h, log_transform=True, warm_start=ws)
+    g = api.fit(_cuda(b1.X), h=b1.h, log_transform=True, warm_start=ws)
+    _compare_fit(g, o, np.log(b1.X))
+    assert g.block_chosen[0] == 0 and g.start_status[1] == 6
+    assert g.start_steps[0] == o.blocks[0].starts[0].steps
+
+
+def test_fit_warm_blocked_matches_oracle():
+    d = datagen.make_config(4, n=40_003)
+    h = int(0.75 * d.X.shape[0])
+    cold = ofit.fit(d.X, h=h, q=8, seed=5)
+    ws = (cold.mu_rew, cold.Sigma_rew)
+    o = ofit.fit(d.X, h=h, q=8, seed=5, warm_start=ws)
+    g = api.fit(_cuda(d.X), h=h, q=8, seed=5, warm_start=ws)
+    _compare_fit(g, o, d.X)
+    assert list(g.block_chosen) == [0] * 8
+    assert list(g.start_steps[0::2]) == [b.starts[0].steps for b in o.blocks]
+
+
+def test_fit_warm_from_cold_raw_reproduces_cold_and_errors():
+    d = datagen.make_config(2, n=20_000)
+    cold = ofit.fit(d.X, h=d.h)
+    g = api.fit(_cuda(d.X), h=d.h, warm_start=(cold.mu_raw, cold.Sigma_raw))
+    _compare_fit(g, cold, d.X)
+    assert g.start_steps[0] == 2  # one C-step + the pass confirming H_new == H_old
+    p = d.X.shape[1]
+    with pytest.raises(api.RTDError) as e:
+        api.fit(_cuda(d.X), h=d.h, warm_start=(cold.mu_raw, np.zeros((p, p))))
+    assert e.value.name == "RTD_E_BOTH_STARTS_FAILED"
