@@ -197,3 +197,34 @@ def a09(p: int) -> np.ndarray:
     """A09 scatter Sigma_jk = (-0.9)^|j-k|."""
     j = np.arange(p)
     return (-0.9) ** np.abs(j[:, None] - j[None, :])
+
+
+def paper_simulation(p: int, eps: float, kind: str, rep: int, n: int = 65536, gamma: float = 50.0) -> Dataset:
+    """The paper's simulation design (Table 2): n cases from N(0, Sigma) with the
+    A09 Sigma, floor(eps n) random cases replaced by outliers around mu_C = gamma v, v the last
+    eigenvector of Sigma rescaled to v^T Sigma^-1 v = p:
+      point   -- every outlier at mu_C;
+      shift   -- N(mu_C, Sigma);
+      cluster -- N(mu_C, 0.05^2 I).
+    Seeded by default_rng([191005615, 2000, p, round(1000 eps), kind index, rep])."""
+    kinds = ("point", "shift", "cluster")
+    rng = np.random.default_rng([SEED_BASE, 2000, p, int(round(1000 * eps)), kinds.index(kind), rep])
+    Sigma = a09(p)
+    L = np.linalg.cholesky(Sigma)
+    X = rng.standard_normal((n, p)) @ L.T
+    w, V = np.linalg.eigh(Sigma)
+    v = V[:, 0]                                   # eigenvector of the smallest eigenvalue
+    v = v * math.sqrt(p / (v @ np.linalg.solve(Sigma, v)))
+    mu_c = gamma * v
+    k = int(math.floor(eps * n))
+    idx = rng.choice(n, size=k, replace=False)
+    if kind == "point":
+        X[idx] = mu_c
+    elif kind == "shift":
+        X[idx] = mu_c + rng.standard_normal((k, p)) @ L.T
+    else:
+        X[idx] = mu_c + 0.05 * rng.standard_normal((k, p))
+    mask = np.zeros(n, dtype=bool)
+    mask[idx] = True
+    return Dataset(X=np.ascontiguousarray(X), h=n // 2, q=1, log_transform=False, sigma=Sigma, outliers=mask,
+                   name=f"sim_a09_p{p}_{kind}_{eps}", meta={"n": n, "p": p, "gamma": gamma, "rep": rep})

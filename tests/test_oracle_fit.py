@@ -181,3 +181,35 @@ def test_warm_start_stream_and_failure():
     with pytest.raises(F.FitError) as e:
         F.fit(b1.X, h=b1.h, log_transform=True, warm_start=(f0.mu_rew, np.zeros((p, p))))
     assert e.value.code == "BOTH_STARTS_FAILED"
+
+
+def test_table2_kl_pins_the_median_consistency_rule():
+    """Table 2 (tests/golden/table2_kl_a09.json): A09, gamma = 50, n = 65536,
+    alpha = 0.5, shift contamination, p = 4.  The KL deviation of the raw scatter the paper reports is
+    reproduced when the h-subset covariance is rescaled so that the median squared robust distance of
+    all n rows is chi2_{p,0.5} (the DetMCD implementations' rule), not with the c(alpha) factor of the
+    text (our reading R1), which the oracle follows: under contamination the two
+    differ (the h-subset is a central (h/n)/(1-eps) part of the inliers).  Finding F1 in DESIGN.md."""
+    import json
+    import os
+    from oracle.chi2 import chi2_quantile
+    from oracle.numerics import mahalanobis_sq
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table2_kl_a09.json")))
+
+    def kl(A, B):
+        M = A @ np.linalg.inv(B)
+        return float(np.trace(M) - A.shape[0] - np.linalg.slogdet(M)[1])
+
+    for eps in (0.1, 0.3):
+        r1, med = [], []
+        for rep in range(3):
+            d = datagen.paper_simulation(4, eps, "shift", rep)
+            n = d.X.shape[0]
+            o = F.fit(d.X, alpha=0.5)
+            S_h = o.Sigma_raw / consistency_factor((n // 2) / n, 4)
+            d2 = mahalanobis_sq(d.X, o.mu_raw, S_h)
+            r1.append(kl(o.Sigma_raw, d.sigma))
+            med.append(kl(S_h * np.median(d2) / chi2_quantile(0.5, 4), d.sigma))
+        paper = gold["IDC"][str(eps)]["shift"][0]
+        assert abs(np.mean(med) / paper - 1.0) < 0.2, (eps, np.mean(med), paper)
+        assert np.mean(r1) / paper < 0.8, (eps, np.mean(r1), paper)
