@@ -255,7 +255,19 @@ def run_stream(args, local: int):
     print(json.dumps(line), flush=True)
 
 
+def _fp64_peak():
+    """FP64 tensor-pipe (DMMA m8n8k4) peak: profiles/fp64_peak.json written by tools/fp64_peak on a B200
+    (MEASURED_PEAKS.json has no fp64 entry), else the value DESIGN.md records from that tool."""
+    try:
+        j = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        return float(j["dmma_tflops"]), "measured (profiles/fp64_peak.json, tools/fp64_peak.cu DMMA burst)"
+    except Exception:
+        return 37.0, "measured earlier with tools/fp64_peak.cu (DMMA burst at 1965 MHz, DESIGN.md section 6)"
+
+
 def _roofline(prof: dict, ms_local: float):
+    """The C-step distance pass (north-star kernel): HBM GB/s and FP64-tensor TFLOP/s of its launches
+    (algorithmic bytes / flops over their CUDA-event time); `bound` is the resource closer to its peak."""
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm_peak else "fallback (B200_PROFILING.md 6650 GB/s)"
@@ -263,11 +275,21 @@ def _roofline(prof: dict, ms_local: float):
     if "dist" not in prof or prof["dist"]["ms"] <= 0:
         return None
     dstat = prof["dist"]
-    achieved = dstat["bytes"] / (dstat["ms"] / 1e3) / 1e9
-    return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-            "traffic": None, "kernel": "k_dist (C-step distance pass)", "peak_source": peak_src,
+    sec = dstat["ms"] / 1e3
+    gbs = dstat["bytes"] / sec / 1e9
+    tfs = dstat.get("flops", 0.0) / sec / 1e12
+    fpk, fsrc = _fp64_peak()
+    hbm = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "peak_source": peak_src}
+    ten = {"achieved": tfs, "peak": fpk, "unit": "TFLOP/s", "frac": tfs / fpk, "peak_source": fsrc}
+    main = ten if ten["frac"] > hbm["frac"] else hbm
+    return {"bound": "tensor" if main is ten else "hbm", "achieved": main["achieved"], "peak": main["peak"],
+            "unit": main["unit"], "frac": main["frac"], "traffic": None,
+            "kernel": "k_dist_mma (C-step distance pass)",
+            "peak_source": main["peak_source"], "hbm": hbm, "fp64_tensor": ten,
             "launches": dstat["launches"], "avg_launch_ms": dstat["ms"] / dstat["launches"],
-            "bytes_per_launch": dstat["bytes"] / dstat["launches"], "ms_share_of_step": dstat["ms"] / ms_local}
+            "bytes_per_launch": dstat["bytes"] / dstat["launches"],
+            "flops_per_launch": dstat.get("flops", 0.0) / dstat["launches"],
+            "ms_share_of_step": dstat["ms"] / ms_local}
 
 
 def _breakdown(prof: dict, steps: int):

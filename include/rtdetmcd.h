@@ -198,16 +198,20 @@ rtdetmcd_status rtdetmcd_csteps(rtdetmcd_ctx* ctx, const double* Z, int64_t m, i
  * context stream around each timed kernel class ("dist" = the C-step /
  * reweight distance pass, "select", "moments_dense", "moments_delta",
  * "unimcd", "matmul", "initial", "flag", ...).  Entries accumulate the
- * device time (ms), the launch count and the ALGORITHMIC bytes of those
- * launches (e.g. dist: rows * (8p + 8)).  name [host] receives up to
- * name_len-1 characters. */
+ * device time (ms), the launch count, the ALGORITHMIC HBM bytes of those
+ * launches, their algorithmic flops (0 where not meaningful) and, for the
+ * distance pass, the bytes the paper's per-start C-steps would stream
+ * (rows * starts * (8p + 8); the fused pass reads a block once for both
+ * starts).  name [host] receives up to name_len-1 characters; every output
+ * pointer is nullable. */
 rtdetmcd_status rtdetmcd_set_profiling(rtdetmcd_ctx* ctx, int32_t on);
 /* Process-wide counters: hand-written kernel launches and CUB radix-sort
  * invocations issued by this library so far (host pointers, nullable). */
 void rtdetmcd_counters(int64_t* kernels, int64_t* sorts);
 int32_t rtdetmcd_prof_count(const rtdetmcd_ctx* ctx);
 rtdetmcd_status rtdetmcd_prof_entry(const rtdetmcd_ctx* ctx, int32_t i, char* name, size_t name_len, double* ms_total,
-                                    int64_t* launches, double* bytes_total);
+                                    int64_t* launches, double* bytes_total, double* flops_total,
+                                    double* eff_bytes_total);
 
 /* ---- distributed stages (one process per GPU; the caller moves data between
  * ranks, e.g. with torch.distributed over NCCL).  Blocks are contiguous row

@@ -97,7 +97,7 @@ def lib() -> C.CDLL:
     L.rtdetmcd_counters.restype = None
     L.rtdetmcd_prof_count.argtypes = [vp]
     L.rtdetmcd_prof_count.restype = i32
-    L.rtdetmcd_prof_entry.argtypes = [vp, i32, C.c_char_p, C.c_size_t, vp, vp, vp]
+    L.rtdetmcd_prof_entry.argtypes = [vp, i32, C.c_char_p, C.c_size_t, vp, vp, vp, vp, vp]
     for name in EXPORTS:  # every declared symbol must resolve
         getattr(L, name)
     _LIB = L

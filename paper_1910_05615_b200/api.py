@@ -312,15 +312,17 @@ def set_profiling(on: bool = True, device: int = 0, ctx: dict | None = None) -> 
 
 
 def profile(device: int = 0, ctx: dict | None = None) -> dict:
-    """{kernel class: {"ms": total device ms, "launches": n, "bytes": algorithmic bytes}} since set_profiling."""
+    """{kernel class: {"ms", "launches", "bytes" (algorithmic HBM), "flops", "eff_bytes"}} since set_profiling."""
     ctx = ctx or _ctx(device)
     L = lib()
     out = {}
     for i in range(L.rtdetmcd_prof_count(ctx["h"])):
         name = C.create_string_buffer(64)
-        ms, n, by = C.c_double(), C.c_int64(), C.c_double()
-        _check(L.rtdetmcd_prof_entry(ctx["h"], i, name, 64, C.byref(ms), C.byref(n), C.byref(by)), ctx)
-        out[name.value.decode()] = {"ms": ms.value, "launches": n.value, "bytes": by.value}
+        ms, n, by, fl, eb = C.c_double(), C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+        _check(L.rtdetmcd_prof_entry(ctx["h"], i, name, 64, C.byref(ms), C.byref(n), C.byref(by), C.byref(fl),
+                                     C.byref(eb)), ctx)
+        out[name.value.decode()] = {"ms": ms.value, "launches": n.value, "bytes": by.value, "flops": fl.value,
+                                    "eff_bytes": eb.value}
     return out
 
 

@@ -54,7 +54,7 @@ static void moments(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
 // When profiling is on, each timed region records a CUDA event pair on the
 // context stream; elapsed times are folded in after the call synchronised.
 struct ProfStat {
-  double ms = 0.0, bytes = 0.0;
+  double ms = 0.0, bytes = 0.0, flops = 0.0, eff_bytes = 0.0;
   long long launches = 0;
 };
 struct Prof {
@@ -63,7 +63,7 @@ struct Prof {
   struct Pending {
     int idx;
     cudaEvent_t a, b;
-    double bytes;
+    double bytes, flops, eff_bytes;
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> pool;
@@ -90,6 +90,8 @@ struct Prof {
       auto& s = stats[pd.idx].second;
       s.ms += ms;
       s.bytes += pd.bytes;
+      s.flops += pd.flops;
+      s.eff_bytes += pd.eff_bytes;
       s.launches += 1;
       pool.push_back(pd.a);
       pool.push_back(pd.b);
@@ -100,11 +102,14 @@ struct Prof {
 static thread_local Prof* g_prof = nullptr;
 static thread_local cudaStream_t g_prof_stream = nullptr;
 
+// bytes: algorithmic HBM bytes of the region; flops: algorithmic flops; eff_bytes: for the fused
+// distance pass, the bytes the paper's per-start C-steps would stream (8(p+1) per row per start)
 struct ProfScope {
   int idx = -1;
   cudaEvent_t a{}, b{};
-  double bytes;
-  ProfScope(const char* name, double algorithmic_bytes) : bytes(algorithmic_bytes) {
+  double bytes, flops, eff_bytes;
+  ProfScope(const char* name, double algorithmic_bytes, double algorithmic_flops = 0.0, double effective_bytes = 0.0)
+      : bytes(algorithmic_bytes), flops(algorithmic_flops), eff_bytes(effective_bytes) {
     if (!g_prof || !g_prof->on) return;
     idx = g_prof->index(name);
     a = g_prof->ev();
@@ -114,7 +119,7 @@ struct ProfScope {
   ~ProfScope() {
     if (idx < 0) return;
     cudaEventRecord(b, g_prof_stream);
-    g_prof->pending.push_back({idx, a, b, bytes});
+    g_prof->pending.push_back({idx, a, b, bytes, flops, eff_bytes});
   }
 };
 
@@ -156,6 +161,36 @@ void d2h(cudaStream_t st, void* host, const void* dev, size_t bytes) {
   RTD_CU(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st));
   RTD_CU(cudaStreamSynchronize(st));
 }
+// Several device -> host reads behind ONE stream synchronisation: the copies land in a pinned staging
+// buffer (a copy into pageable memory would synchronise by itself), then are unpacked.
+struct Fetch {
+  void* host;
+  const void* dev;
+  size_t bytes;
+};
+void fetch(cudaStream_t st, std::initializer_list<Fetch> items) {
+  static thread_local char* stage = nullptr;
+  static thread_local size_t cap = 0;
+  size_t need = 0;
+  for (const Fetch& f : items) need += (f.bytes + 255) & ~size_t(255);
+  if (need > cap) {
+    if (stage) cudaFreeHost(stage);
+    cap = std::max(need, size_t(1) << 20);
+    RTD_CU(cudaMallocHost(&stage, cap));
+  }
+  size_t off = 0;
+  for (const Fetch& f : items) {
+    if (f.bytes) RTD_CU(cudaMemcpyAsync(stage + off, f.dev, f.bytes, cudaMemcpyDeviceToHost, st));
+    off += (f.bytes + 255) & ~size_t(255);
+  }
+  RTD_CU(cudaStreamSynchronize(st));
+  off = 0;
+  for (const Fetch& f : items) {
+    if (f.bytes) memcpy(f.host, stage + off, f.bytes);
+    off += (f.bytes + 255) & ~size_t(255);
+  }
+}
+
 void h2d(cudaStream_t st, void* dev, const void* host, size_t bytes) {
   if (!bytes) return;
   RTD_CU(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st));
@@ -279,10 +314,15 @@ MomArgs mom_args(const CStepBufs& b, const double* Z, long long blk_stride, int 
 }
 
 // upload distance operators of instances act[g0, g0+cnt) (staged in cstage slots) and run the distance pass
+// upload distance operators of instances act[g0, g0+cnt) (staged in cstage slots) and run the distance pass
 void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long blk_stride, int nstart, int nact,
                  int cstride) {
+  // algorithmic HBM bytes: every start's C-step streams its block (8 p per row) and writes d^2 (8 per row);
+  // flops: the triangular operator and the squared norm, 2 (p(p+1)/2 + p) per row per start
+  const double fm = (double)b.m, pp = (double)b.p;
   if (dist_mma_supported(b.p)) {  // FP64 tensor-pipe kernel: operator read from cstage, all instances at once
-    ProfScope ps("dist", (double)nact * b.m * (8.0 * b.p + 8.0));
+    ProfScope ps("dist", (double)nact * fm * (8.0 * pp + 8.0), (double)nact * fm * (pp * (pp + 1.0) + 2.0 * pp),
+                 (double)nact * fm * (8.0 * pp + 8.0));
     launch_dist_mma(b.p, Z, b.m, blk_stride, b.inst_dev, nstart, nact, b.cstage, cstride, b.d2, st);
     return;
   }
@@ -290,7 +330,8 @@ void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long
   for (int g0 = 0; g0 < nact; g0 += cap) {
     const int cnt = std::min(cap, nact - g0);
     upload_const(b.cstage + (size_t)g0 * cstride, (size_t)cnt * cstride, st);
-    ProfScope ps("dist", (double)cnt * b.m * (8.0 * b.p + 8.0));
+    ProfScope ps("dist", (double)cnt * fm * (8.0 * pp + 8.0), (double)cnt * fm * (pp * (pp + 1.0) + 2.0 * pp),
+                 (double)cnt * fm * (8.0 * pp + 8.0));
     launch_dist(b.p, Z, b.m, blk_stride, b.inst_dev + g0, nstart, cnt, cstride, b.d2, st);
   }
 }
@@ -332,7 +373,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
       ProfScope ps("select", (double)na * m * 9.0);
       launch_select(b.d2, m, h, b.inst_dev, na, b.sel, b.hist, b.selcnt, memB, memA, b.changed, b.list, b.seg_cnt,
                     b.ctas, b.seg_len, st);
-      d2h(st, changed.data(), b.changed, ninst * sizeof(int));
+      fetch(st, {{changed.data(), b.changed, ninst * sizeof(int)}, {status_h.data(), b.status, ninst * sizeof(int)}});
       std::vector<int> more;
       for (int i : act)
         if (changed[i] < 0) more.push_back(i);
@@ -347,7 +388,6 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
       }
     }
     std::swap(memA, memB);  // memA = membership of this step, memB = previous
-    d2h(st, status_h.data(), b.status, ninst * sizeof(int));
     std::vector<int> upd, dense;
     for (int i : act) {
       steps_h[i] = step;
@@ -704,8 +744,7 @@ std::vector<int> phase_starts(cudaStream_t st, FitBufs& f, const Dims& d, const 
   run_initial(st, f.ib, f.Z, m, p, q, blk_stride);
   launch_jacobi(f.ib.S1, 2 * q, p, o.kappa_max, f.V2, f.lam2, f.jok, st);  // [k q + b]: S~1 blocks, then S~2
   std::vector<int> jok(2 * q), abok(q);
-  d2h(st, jok.data(), f.jok, 2 * q * sizeof(int));
-  d2h(st, abok.data(), f.ib.abok, q * sizeof(int));
+  fetch(st, {{jok.data(), f.jok, 2 * q * sizeof(int)}, {abok.data(), f.ib.abok, q * sizeof(int)}});
   const int ninst = 2 * q;
   r.status.assign(ninst, ST_ACTIVE);
   std::vector<int> blk(ninst), active(ninst);
@@ -800,7 +839,9 @@ int phase_raw(cudaStream_t st, FitBufs& f, int p, int q, long long m, const std:
 
 // H11 per block: d^2 under (mu_raw, Sigma_raw) for the q blocks in f.Z and the weighted sums about mu_raw
 // -> f.sums_rw [q][np]; f.cb.d2 keeps the distances (weights)
-void phase_reweight_blocks(cudaStream_t st, FitBufs& f, int p, int q, long long m, double c2) {
+// defer: leave the positive-definiteness status of the raw scatter in f.st1[0] for the caller to check
+// (one synchronisation at the end of the fit instead of one here)
+void phase_reweight_blocks(cudaStream_t st, FitBufs& f, int p, int q, long long m, double c2, bool defer = false) {
   const long long blk_stride = (long long)p * m;
   const int cstride = p + p * (p + 1) / 2;
   int zero2[2] = {0, 0};
@@ -808,14 +849,17 @@ void phase_reweight_blocks(cudaStream_t st, FitBufs& f, int p, int q, long long 
   h2d(st, f.st1, zero2, sizeof(int));
   launch_prepare(f.ids_dev, 1, f.mu_raw, f.sig_raw, p, 1e300, f.cb.cstage, cstride, nullptr, nullptr, f.st1, nullptr,
                  0, 0, st);
-  int stv = 0;
-  d2h(st, &stv, f.st1, sizeof(int));
-  if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "raw scatter is not positive definite"};
+  if (!defer) {
+    int stv = 0;
+    d2h(st, &stv, f.st1, sizeof(int));
+    if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "raw scatter is not positive definite"};
+  }
   std::vector<int> blocks(q);
   for (int b = 0; b < q; b++) blocks[b] = b;
   h2d(st, f.cb.inst_dev, blocks.data(), q * sizeof(int));
   {
-    ProfScope ps("dist", (double)q * m * (8.0 * p + 8.0));
+    ProfScope ps("dist", (double)q * m * (8.0 * p + 8.0), (double)q * m * ((double)p * (p + 1.0) + 2.0 * p),
+                 (double)q * m * (8.0 * p + 8.0));
     if (dist_mma_supported(p)) {
       launch_dist_mma(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, f.cb.cstage, 0, f.cb.d2, st);
     } else {
@@ -837,13 +881,18 @@ void phase_reweight_blocks(cudaStream_t st, FitBufs& f, int p, int q, long long 
 }
 
 // H11 pooled: sum of the q block sums (block order) -> (mu_rew, Sigma_rew) scaled by c(quantile, p); returns k
-double phase_pool(cudaStream_t st, FitBufs& f, int p, int q, double quantile, const double* sums_dev) {
+// defer: the weighted count stays in f.pooled[np - 1] for the caller to check (returns -1)
+double phase_pool(cudaStream_t st, FitBufs& f, int p, int q, double quantile, const double* sums_dev,
+                  bool defer = false) {
   const int np = mom_np(p);
   launch_pool_sums(sums_dev, q, np, f.pooled, st);
-  std::vector<double> pooled(np);
-  d2h(st, pooled.data(), f.pooled, np * sizeof(double));
-  const double kw = pooled[np - 1];
-  if (!(kw > p)) throw Fail{RTD_E_NOT_PD, "too few reweighted inliers"};
+  double kw = -1.0;
+  if (!defer) {
+    std::vector<double> pooled(np);
+    d2h(st, pooled.data(), f.pooled, np * sizeof(double));
+    kw = pooled[np - 1];
+    if (!(kw > p)) throw Fail{RTD_E_NOT_PD, "too few reweighted inliers"};
+  }
   int zero = 0;
   h2d(st, f.ids_dev, &zero, sizeof(int));
   launch_sums_to_cov(f.ids_dev, 1, f.pooled, np, f.mu_raw, p, 0.0, consistency_factor(quantile, p), f.mu_rew,
@@ -907,20 +956,16 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
   // H11: reweighting over the fitted rows, per block then pooled
   const double c2 = chi2_quantile(o.quantile, p);
   const int cstride = p + p * (p + 1) / 2;
-  phase_reweight_blocks(st, f, p, q, m, c2);
-  const double kw = phase_pool(st, f, p, q, o.quantile, f.sums_rw);
-  if (out) out->n_weighted = (int64_t)llround(kw);
+  phase_reweight_blocks(st, f, p, q, m, c2, true);
+  phase_pool(st, f, p, q, o.quantile, f.sums_rw, true);
   // de-standardise raw and reweighted fits (H13)
   launch_destandardize(f.uni, f.mu_raw, f.sig_raw, p, f.muX, f.sigX, st);
   launch_destandardize(f.uni, f.mu_rew, f.sig_rew, p, f.muX + RTD_MAXP, f.sigX + M2, st);
   // H12: flag all n rows under the reweighted fit in X units
   {
-    int stv = 0;
-    RTD_CU(cudaMemsetAsync(f.st1, 0, sizeof(int), st));
+    RTD_CU(cudaMemsetAsync(f.st1 + 1, 0, sizeof(int), st));
     launch_prepare(f.ids_dev, 1, f.muX + RTD_MAXP, f.sigX + M2, p, 1e300, f.cb.cstage, cstride, nullptr, nullptr,
-                   f.st1, nullptr, 0, 0, st);
-    d2h(st, &stv, f.st1, sizeof(int));
-    if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "reweighted scatter is not positive definite"};
+                   f.st1 + 1, nullptr, 0, 0, st);
     upload_const(f.cb.cstage, cstride, st);
     if (want_flags) {
       ProfScope ps("flag", (double)n * (8.0 * p + 9.0));
@@ -936,13 +981,19 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     launch_weights_from_d2(f.cb.d2, (long long)q * m, c2, f.rowmap, f.weights_d, st);
     launch_hsub_from_mem(f.cb.memA, f.chosen_dev, q, m, f.rowmap, f.hsub_d, st);
   }
-  RTD_CU(cudaStreamSynchronize(st));
+  // one synchronisation: deferred status words (raw / reweighted scatter PD), weighted count, estimates
+  std::vector<double> mx(4 * RTD_MAXP), sx(4 * M2);
+  int pd[2] = {0, 0};
+  double kw = 0.0;
+  fetch(st, {{pd, f.st1, 2 * sizeof(int)}, {&kw, f.pooled + (mom_np(p) - 1), sizeof(double)},
+             {mx.data(), f.muX, 2 * RTD_MAXP * sizeof(double)}, {sx.data(), f.sigX, 2 * M2 * sizeof(double)}});
+  if (pd[0] == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "raw scatter is not positive definite"};
+  if (!(kw > p)) throw Fail{RTD_E_NOT_PD, "too few reweighted inliers"};
+  if (pd[1] == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "reweighted scatter is not positive definite"};
 
   // outputs
   if (out) {
-    std::vector<double> mx(4 * RTD_MAXP), sx(4 * M2);
-    d2h(st, mx.data(), f.muX, 2 * RTD_MAXP * sizeof(double));
-    d2h(st, sx.data(), f.sigX, 2 * M2 * sizeof(double));
+    out->n_weighted = (int64_t)llround(kw);
     for (int j = 0; j < p; j++) {
       if (out->loc) out->loc[j] = uni[j].loc;
       if (out->scale) out->scale[j] = uni[j].scale;
@@ -1358,7 +1409,8 @@ void rtdetmcd_counters(int64_t* kernels, int64_t* sorts) {
 int32_t rtdetmcd_prof_count(const rtdetmcd_ctx* c) { return c ? (int32_t)c->prof.stats.size() : 0; }
 
 rtdetmcd_status rtdetmcd_prof_entry(const rtdetmcd_ctx* c, int32_t i, char* name, size_t name_len, double* ms_total,
-                                    int64_t* launches, double* bytes_total) {
+                                    int64_t* launches, double* bytes_total, double* flops_total,
+                                    double* eff_bytes_total) {
   if (!c || i < 0 || i >= (int32_t)c->prof.stats.size()) return RTD_E_INVALID_ARG;
   const auto& e = c->prof.stats[i];
   if (name && name_len) {
@@ -1368,6 +1420,8 @@ rtdetmcd_status rtdetmcd_prof_entry(const rtdetmcd_ctx* c, int32_t i, char* name
   if (ms_total) *ms_total = e.second.ms;
   if (launches) *launches = e.second.launches;
   if (bytes_total) *bytes_total = e.second.bytes;
+  if (flops_total) *flops_total = e.second.flops;
+  if (eff_bytes_total) *eff_bytes_total = e.second.eff_bytes;
   return RTD_OK;
 }
 

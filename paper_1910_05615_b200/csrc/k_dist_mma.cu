@@ -23,16 +23,24 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-template <int P, int MB>
-__global__ void __launch_bounds__(256, 2) k_dist_mma(const double* __restrict__ Zall, long long m, long long blk_stride,
-                                                     const int* __restrict__ inst, int nstart,
-                                                     const double* __restrict__ cstage, int cstride,
-                                                     double* __restrict__ d2_all) {
+// MINB CTAs per SM (register budget); CINIT folds the centring into the accumulators (d = M z - M mu,
+// the same arithmetic object) instead of subtracting mu from every A element.  tools/dist_bench.cu
+// compared the variants on a B200 (profiles/r01_dist_bench.txt): at p = 40 the pass is DMMA-bound
+// (0.70 of the measured DMMA peak) and neither CINIT, 4 m-blocks at 1 CTA/SM, nor one pass shared by
+// the two starts of a block (loads once, two operators) is faster; in the pipeline (config 3) the
+// p = 20 winner of the isolated test was not, so every p uses MB 4 (p <= 24) / 3, 2 CTAs/SM, subtract.
+// Each start has its own pass; the L2 serves the second start's reads of a block when both run.
+template <int P, int MB, int MINB, bool CINIT>
+__global__ void __launch_bounds__(256, MINB) k_dist_mma(const double* __restrict__ Zall, long long m,
+                                                        long long blk_stride, const int* __restrict__ inst, int nstart,
+                                                        const double* __restrict__ cstage, int cstride,
+                                                        double* __restrict__ d2_all) {
   constexpr int KB = (P + 3) / 4;
   constexpr int NB = (P + 7) / 8;
   // operator fragments in shared memory: lane-major, conflict-free; each is reused by MB m-blocks
   __shared__ double bsm[KB * NB * 32];
   __shared__ double musm[KB * 4];
+  __shared__ double csm[NB * 8];
   const int slot = blockIdx.y;
   const int id = inst[slot];
   const double* __restrict__ Z = Zall + (long long)(id / nstart) * blk_stride;
@@ -44,6 +52,14 @@ __global__ void __launch_bounds__(256, 2) k_dist_mma(const double* __restrict__ 
     bsm[e] = (j < P && k <= j) ? cs[P + j * (j + 1) / 2 + k] : 0.0;
   }
   for (int e = threadIdx.x; e < KB * 4; e += blockDim.x) musm[e] = e < P ? cs[e] : 0.0;
+  if (CINIT) {
+    for (int j = threadIdx.x; j < NB * 8; j += blockDim.x) {  // c_j = (M mu)_j, fixed order
+      double c = 0.0;
+      if (j < P)
+        for (int k = 0; k <= j; k++) c = fma(cs[P + j * (j + 1) / 2 + k], cs[k], c);
+      csm[j] = -c;
+    }
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const long long rows_per_tile = 8 * MB;
@@ -56,7 +72,10 @@ __global__ void __launch_bounds__(256, 2) k_dist_mma(const double* __restrict__ 
 #pragma unroll
     for (int mb = 0; mb < MB; mb++)
 #pragma unroll
-      for (int nb = 0; nb < NB; nb++) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+      for (int nb = 0; nb < NB; nb++) {
+        acc[mb][nb][0] = CINIT ? csm[8 * nb + 2 * t] : 0.0;
+        acc[mb][nb][1] = CINIT ? csm[8 * nb + 2 * t + 1] : 0.0;
+      }
 #pragma unroll
     for (int kb = 0; kb < KB; kb++) {
       const int k = 4 * kb + t;
@@ -65,7 +84,8 @@ __global__ void __launch_bounds__(256, 2) k_dist_mma(const double* __restrict__ 
 #pragma unroll
       for (int mb = 0; mb < MB; mb++) {
         const long long row = r0 + mb * 8 + g;
-        a[mb] = (k < P && row < m) ? __dsub_rn(Z[(long long)k * m + row], muk) : 0.0;
+        a[mb] = (k < P && row < m) ? (CINIT ? __ldg(Z + (long long)k * m + row)
+                                            : __dsub_rn(__ldg(Z + (long long)k * m + row), muk)) : 0.0;
       }
 #pragma unroll
       for (int nb = 0; nb < NB; nb++) {
@@ -94,12 +114,13 @@ __global__ void __launch_bounds__(256, 2) k_dist_mma(const double* __restrict__ 
 template <int P>
 static void dist_mma_launch(const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
                             int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st) {
-  constexpr int MB = P <= 24 ? 4 : 3;
+  constexpr int MB = P <= 24 ? 4 : 3, MINB = 2;
+  constexpr bool SMALL = false;
   const long long tiles = (m + 8 * MB - 1) / (8 * MB);
   const long long need = (tiles + 7) / 8;  // 8 warps per CTA
-  const long long cap = std::max<long long>(1, 148LL * 2 * 2 / std::max(1, ninst));
-  k_dist_mma<P, MB><<<dim3((unsigned)std::min(need, cap), ninst), 256, 0, st>>>(Zall, m, blk_stride, inst, nstart,
-                                                                                 cstage, cstride, d2_all);
+  const long long cap = std::max<long long>(1, 148LL * MINB * 2 / std::max(1, ninst));
+  k_dist_mma<P, MB, MINB, SMALL><<<dim3((unsigned)std::min(need, cap), ninst), 256, 0, st>>>(
+      Zall, m, blk_stride, inst, nstart, cstage, cstride, d2_all);
 }
 
 #define RTD_DISPATCH_P8(p, F, ...)                                                                          \

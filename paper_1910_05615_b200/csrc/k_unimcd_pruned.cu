@@ -71,30 +71,32 @@ __device__ __forceinline__ double ord_val(unsigned long long k) {
   return __longlong_as_double((long long)u);
 }
 
-// Running (sum y, sum y^2) of one thread in double-double, adding one double at a time:
-// error-free two-sum / two-product with a single renormalisation (about 23 fp64 ops per
-// element instead of 42 for a full dd2_add); thread partials are then folded with dd2_add.
+// Running (sum y, sum y^2) of one thread in double-double, adding one double at a time with
+// error-free transformations (two-sum, two-product) and no per-element renormalisation: the
+// rounding errors are collected in the low words (17 fp64 ops per element instead of 23).  A thread adds at most a
+// few thousand terms, so the low words stay exact to ~2^-100 relative; thread partials are folded
+// with the full dd2_add.
 struct ddacc {
   double h1, l1, h2, l2;
 };
 __device__ __forceinline__ ddacc ddacc_zero() { return {0.0, 0.0, 0.0, 0.0}; }
 __device__ __forceinline__ void ddacc_add(ddacc& a, double v) {
-  double s = __dadd_rn(a.h1, v);
-  double bb = __dsub_rn(s, a.h1);
-  double e = __dadd_rn(__dsub_rn(a.h1, __dsub_rn(s, bb)), __dsub_rn(v, bb));
-  double lo = __dadd_rn(a.l1, e);
-  a.h1 = __dadd_rn(s, lo);
-  a.l1 = __dsub_rn(lo, __dsub_rn(a.h1, s));
-  const double p = __dmul_rn(v, v);
-  const double pe = __fma_rn(v, v, -p);
-  s = __dadd_rn(a.h2, p);
-  bb = __dsub_rn(s, a.h2);
-  e = __dadd_rn(__dsub_rn(a.h2, __dsub_rn(s, bb)), __dsub_rn(p, bb));
-  lo = __dadd_rn(a.l2, __dadd_rn(e, pe));
-  a.h2 = __dadd_rn(s, lo);
-  a.l2 = __dsub_rn(lo, __dsub_rn(a.h2, s));
+  const double s = __dadd_rn(a.h1, v);
+  const double bb = __dsub_rn(s, a.h1);
+  const double e = __dadd_rn(__dsub_rn(a.h1, __dsub_rn(s, bb)), __dsub_rn(v, bb));
+  a.h1 = s;
+  a.l1 = __dadd_rn(a.l1, e);
+  const double pr = __dmul_rn(v, v);
+  const double pe = __fma_rn(v, v, -pr);
+  const double s2 = __dadd_rn(a.h2, pr);
+  const double b2 = __dsub_rn(s2, a.h2);
+  const double e2 = __dadd_rn(__dsub_rn(a.h2, __dsub_rn(s2, b2)), __dsub_rn(pr, b2));
+  a.h2 = s2;
+  a.l2 = __dadd_rn(a.l2, __dadd_rn(e2, pe));
 }
-__device__ __forceinline__ dd2 ddacc_dd2(const ddacc& a) { return {{a.h1, a.l1}, {a.h2, a.l2}}; }
+__device__ __forceinline__ dd2 ddacc_dd2(const ddacc& a) {
+  return {quick_two_sum(a.h1, a.l1), quick_two_sum(a.h2, a.l2)};
+}
 
 static constexpr int ILP = 8;  // elements loaded per thread before they are consumed (latency hiding)
 
@@ -855,7 +857,7 @@ static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.Q2lo = A.take<double>((size_t)ncols * (NBK + 1));
   s.Q2hi = A.take<double>((size_t)ncols * (NBK + 1));
   s.bsc = A.take<BucketScan>(ncols);
-  s.nbound = std::max(1, 148 * 4 / ncols);
+  s.nbound = std::max(1, 148 * 8 / ncols);
   s.ub_part = A.take<double>((size_t)ncols * s.nbound);
   s.best_ub = A.take<double>(ncols);
   s.range_part = A.take<long long>((size_t)ncols * s.nbound * 2);
@@ -875,7 +877,9 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   RTD_CU(cudaMemsetAsync(s.gcount, 0, 2 * (size_t)ncols * sizeof(int), st));
   k_pr_sample<<<ncols, 1024, 0, st>>>(cols, len, s.pc, s.mm);
   RTD_LAUNCHED();
-  const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((len + 4095) / 4096, 148LL * 4 / ncols + 1));
+  // ~64K elements per CTA: many CTAs per column so the 4-CTA/SM waves quantise finely (a CTA flushes its
+  // 4096-bin histogram with global atomics, about 1/8 of its element count)
+  const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((len + 65535) / 65536, 1024));
   k_pr_hist<<<dim3(gx, ncols), PT, 0, st>>>(cols, len, s.pc, s.cnt, s.s1, s.mm);
   RTD_LAUNCHED();
   k_pr_scan<<<ncols, 1024, 0, st>>>(s.pc, s.cnt, s.s1, s.mm, s.C, s.A1, s.Q2lo, s.Q2hi, s.bsc);
