@@ -161,36 +161,6 @@ void d2h(cudaStream_t st, void* host, const void* dev, size_t bytes) {
   RTD_CU(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st));
   RTD_CU(cudaStreamSynchronize(st));
 }
-// Several device -> host reads behind ONE stream synchronisation: the copies land in a pinned staging
-// buffer (a copy into pageable memory would synchronise by itself), then are unpacked.
-struct Fetch {
-  void* host;
-  const void* dev;
-  size_t bytes;
-};
-void fetch(cudaStream_t st, std::initializer_list<Fetch> items) {
-  static thread_local char* stage = nullptr;
-  static thread_local size_t cap = 0;
-  size_t need = 0;
-  for (const Fetch& f : items) need += (f.bytes + 255) & ~size_t(255);
-  if (need > cap) {
-    if (stage) cudaFreeHost(stage);
-    cap = std::max(need, size_t(1) << 20);
-    RTD_CU(cudaMallocHost(&stage, cap));
-  }
-  size_t off = 0;
-  for (const Fetch& f : items) {
-    if (f.bytes) RTD_CU(cudaMemcpyAsync(stage + off, f.dev, f.bytes, cudaMemcpyDeviceToHost, st));
-    off += (f.bytes + 255) & ~size_t(255);
-  }
-  RTD_CU(cudaStreamSynchronize(st));
-  off = 0;
-  for (const Fetch& f : items) {
-    if (f.bytes) memcpy(f.host, stage + off, f.bytes);
-    off += (f.bytes + 255) & ~size_t(255);
-  }
-}
-
 void h2d(cudaStream_t st, void* dev, const void* host, size_t bytes) {
   if (!bytes) return;
   RTD_CU(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st));

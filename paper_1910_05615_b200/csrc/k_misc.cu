@@ -1,8 +1,38 @@
 // Small helper kernels: Feistel forward map, extraction of univariate results,
-// per-row outputs in original row order, scaled matrix copies.
+// per-row outputs in original row order, scaled matrix copies; the batched
+// device -> host read helper.
+#include <algorithm>
+#include <cstring>
+
 #include "rtd_internal.h"
 
 namespace rtd {
+
+// Several device -> host reads behind ONE stream synchronisation: the copies land in a pinned staging
+// buffer (a copy into pageable memory would synchronise by itself), then are unpacked.
+void fetch(cudaStream_t st, std::initializer_list<Fetch> items) {
+  static thread_local char* stage = nullptr;
+  static thread_local size_t cap = 0;
+  size_t need = 0;
+  for (const Fetch& f : items) need += (f.bytes + 255) & ~size_t(255);
+  if (need > cap) {
+    if (stage) cudaFreeHost(stage);
+    cap = std::max(need, size_t(1) << 20);
+    RTD_CU(cudaMallocHost(&stage, cap));
+  }
+  size_t off = 0;
+  for (const Fetch& f : items) {
+    if (f.bytes) RTD_CU(cudaMemcpyAsync(stage + off, f.dev, f.bytes, cudaMemcpyDeviceToHost, st));
+    off += (f.bytes + 255) & ~size_t(255);
+  }
+  RTD_CU(cudaStreamSynchronize(st));
+  off = 0;
+  for (const Fetch& f : items) {
+    if (f.bytes) memcpy(f.host, stage + off, f.bytes);
+    off += (f.bytes + 255) & ~size_t(255);
+  }
+}
+
 
 __device__ __forceinline__ unsigned long long splitmix64_f(unsigned long long z) {
   z += 0x9E3779B97F4A7C15ull;

@@ -620,17 +620,11 @@ __global__ void k_pr_segs(const int* __restrict__ gcount, int nseg, int* __restr
 }
 
 // 5a. double-double prefix sums of each sorted gathered segment (one CTA per segment)
-__global__ void __launch_bounds__(1024) k_pr_prefix(const PrunedCol* __restrict__ pc, const double* __restrict__ gsorted,
-                                                    const int* __restrict__ gcount, const dd2* __restrict__ below,
-                                                    dd2* __restrict__ pref) {
+__device__ void prefix_body(const double* v, int cn, int col, int side, const dd2* __restrict__ below,
+                            dd2* __restrict__ P) {
   __shared__ dd2 sm[33];
-  const int seg = blockIdx.x, col = seg >> 1, side = seg & 1;
-  if (pc[col].status) return;
-  const int t = threadIdx.x;
-  const int cn = min(gcount[seg], CAP);
-  const double* v = gsorted + (long long)seg * CAP;
-  dd2* P = pref + (long long)seg * (CAP + 1);
   __shared__ dd2 base;
+  const int t = threadIdx.x;
   if (t == 0) {
     dd2 B = dd2_zero();
     for (int k = 0; k < PCTA; k++) B = dd2_add(B, below[((long long)col * PCTA + k) * 2 + side]);
@@ -649,6 +643,35 @@ __global__ void __launch_bounds__(1024) k_pr_prefix(const PrunedCol* __restrict_
     ex = dd2_add(ex, dd2_of(v[i]));
   }
   if (t == 0) P[cn] = dd2_add(base, tot);
+}
+
+__global__ void __launch_bounds__(1024) k_pr_prefix(const PrunedCol* __restrict__ pc, const double* __restrict__ gsorted,
+                                                    const int* __restrict__ gcount, const dd2* __restrict__ below,
+                                                    dd2* __restrict__ pref) {
+  const int seg = blockIdx.x, col = seg >> 1, side = seg & 1;
+  if (pc[col].status) return;
+  const int cn = min(gcount[seg], CAP);
+  prefix_body(gsorted + (long long)seg * CAP, cn, col, side, below, pref + (long long)seg * (CAP + 1));
+}
+
+// 5a'. the common case, every gathered segment holding at most SMAX elements: sort the segment in
+//      shared memory (bitonic) and take its prefix sums in the same CTA (replaces the segmented radix
+//      sort's passes and the separate prefix launch)
+static constexpr int SMAX = 8192;
+__global__ void __launch_bounds__(1024) k_pr_sortprefix(const PrunedCol* __restrict__ pc, const double* __restrict__ g,
+                                                        const int* __restrict__ gcount, const dd2* __restrict__ below,
+                                                        dd2* __restrict__ pref) {
+  extern __shared__ double sv[];
+  const int seg = blockIdx.x, col = seg >> 1, side = seg & 1;
+  if (pc[col].status) return;
+  const int cn = min(gcount[seg], CAP);
+  int np2 = 1;
+  while (np2 < cn) np2 <<= 1;
+  const double* src = g + (long long)seg * CAP;
+  for (int i = threadIdx.x; i < np2; i += blockDim.x) sv[i] = i < cn ? src[i] : INFINITY;
+  __syncthreads();
+  smem_bitonic(sv, np2);
+  prefix_body(sv, cn, col, side, below, pref + (long long)seg * (CAP + 1));
 }
 
 __device__ __forceinline__ bool win_better2(double ahi, double alo, long long as, double bhi, double blo, long long bs) {
@@ -897,8 +920,8 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   k_pr_gather<<<dim3(PCTA, ncols), PT, 0, st>>>(cols, len, s.pc, s.g, s.gcount, s.below);
   RTD_LAUNCHED();
   std::vector<PrunedCol> hc(ncols);
-  RTD_CU(cudaMemcpyAsync(hc.data(), s.pc, ncols * sizeof(PrunedCol), cudaMemcpyDeviceToHost, st));
-  RTD_CU(cudaStreamSynchronize(st));
+  std::vector<int> gc(2 * ncols);
+  fetch(st, {{hc.data(), s.pc, ncols * sizeof(PrunedCol)}, {gc.data(), s.gcount, 2 * ncols * sizeof(int)}});
   static const bool dbg = getenv("RTD_DEBUG_PRUNED") != nullptr;
   if (dbg) {
     for (int j = 0; j < ncols; j++)
@@ -908,14 +931,28 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   }
   for (int j = 0; j < ncols; j++)
     if (hc[j].status) return false;
-  k_pr_segs<<<1, 256, 0, st>>>(s.gcount, 2 * ncols, s.sbeg, s.send);
-  RTD_LAUNCHED();
-  size_t bytes = s.cub_bytes;
-  count_sort();
-  RTD_CU(cub::DeviceSegmentedRadixSort::SortKeys(s.cub_tmp, bytes, s.g, s.gsorted, 2 * ncols * CAP, 2 * ncols,
-                                                 s.sbeg, s.send, 0, 64, st));
-  k_pr_prefix<<<2 * ncols, 1024, 0, st>>>(s.pc, s.gsorted, s.gcount, s.below, s.pref);
-  RTD_LAUNCHED();
+  int gmax = 0;
+  for (int v : gc) gmax = std::max(gmax, v);
+  if (gmax <= SMAX) {
+    static const int smem = [] {
+      cudaFuncSetAttribute(k_pr_sortprefix, cudaFuncAttributeMaxDynamicSharedMemorySize, SMAX * (int)sizeof(double));
+      return SMAX * (int)sizeof(double);
+    }();
+    int np2 = 1;
+    while (np2 < gmax) np2 <<= 1;
+    k_pr_sortprefix<<<2 * ncols, 1024, std::min(smem, np2 * (int)sizeof(double)), st>>>(s.pc, s.g, s.gcount, s.below,
+                                                                                         s.pref);
+    RTD_LAUNCHED();
+  } else {
+    k_pr_segs<<<1, 256, 0, st>>>(s.gcount, 2 * ncols, s.sbeg, s.send);
+    RTD_LAUNCHED();
+    size_t bytes = s.cub_bytes;
+    count_sort();
+    RTD_CU(cub::DeviceSegmentedRadixSort::SortKeys(s.cub_tmp, bytes, s.g, s.gsorted, 2 * ncols * CAP, 2 * ncols,
+                                                   s.sbeg, s.send, 0, 64, st));
+    k_pr_prefix<<<2 * ncols, 1024, 0, st>>>(s.pc, s.gsorted, s.gcount, s.below, s.pref);
+    RTD_LAUNCHED();
+  }
   k_pr_eval<<<dim3(s.nch, ncols), PT, 0, st>>>(h, s.pc, s.pref, s.part, s.nch);
   RTD_LAUNCHED();
   k_pr_raw<<<ncols, 32, 0, st>>>(h, s.pc, s.pref, s.part, s.nch, uc, out_dev);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <initializer_list>
 #include <string>
 #include <vector>
 #include <cuda_runtime.h>
@@ -33,6 +34,15 @@ void count_sort();    // CUB radix-sort invocations
         throw ::rtd::CudaError{e2__, std::string("kernel before ") + __FILE__ + ":" + std::to_string(__LINE__)}; \
     }                                                                       \
   } while (0)
+
+// ---------------------------------------------------------------- device -> host reads
+// Several device -> host copies behind one stream synchronisation (pinned staging; api.cu).
+struct Fetch {
+  void* host;
+  const void* dev;
+  size_t bytes;
+};
+void fetch(cudaStream_t st, std::initializer_list<Fetch> items);
 
 // ---------------------------------------------------------------- arena
 // Bump allocator over one device buffer.  A dry run (base == nullptr)

@@ -56,3 +56,15 @@ def test_host_numerics_match_oracle(so):
             assert api.consistency_factor(a, p) == pytest.approx(o_cf(a, p), rel=1e-12)
     for n, p, w in ((2 ** 16, 4, 4096), (2 ** 19, 8, 8192), (8_000_000, 40, 4096), (1000, 5, 4096)):
         assert api.choose_q(n, p, w) == o_choose_q(n, p, w)
+
+
+def test_library_has_no_undefined_internal_symbols(so):
+    """Every rtd:: symbol the library references is defined in it (a shared object links with
+    undefined symbols and would only fail at load / first call)."""
+    import shutil
+    import subprocess
+    if not shutil.which("nm"):
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-D", "--undefined-only", LIB], capture_output=True, text=True).stdout
+    bad = [ln for ln in out.splitlines() if "rtd" in ln or "rtdetmcd" in ln]
+    assert not bad, bad
