@@ -14,6 +14,9 @@
 //   (deterministic).
 // k_matmul_mma: out = Z W (W full p x p, e.g. the eigenvectors V or
 //   Sigma^-1/2 of the refinement), column-major out.
+#include <algorithm>
+#include <cstdlib>
+
 #include "rtd_internal.h"
 
 namespace rtd {
@@ -37,6 +40,185 @@ __device__ __forceinline__ double wrap_g2(double z) {
 
 static constexpr int MW = 8;  // warps per CTA
 static constexpr int RG = 4;  // 4-row groups per warp iteration (loads in flight)
+
+// per-warp results -> shared memory -> fixed-order sum over the warps -> this CTA's partial row
+template <int NB>
+__device__ __forceinline__ void mom_epilogue(double (&acc)[NB * (NB + 1) / 2][2], double (&s1)[NB], double cnt,
+                                             double* red, const MomArgs& a, int slot, int p, int NP) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
+  // reduce: S1 over the 4 t-lanes, count over the t-lanes of g == 0
+#pragma unroll
+  for (int b = 0; b < NB; b++) {
+    s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 1);
+    s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 2);
+  }
+  cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+  cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+  double* rw = red + warp * NP;
+  for (int e = lane; e < NP; e += 32) rw[e] = 0.0;
+  __syncwarp();
+  if (t == 0) {
+#pragma unroll
+    for (int b = 0; b < NB; b++)
+      if (8 * b + g < p) rw[8 * b + g] = s1[b];
+  }
+  if (lane == 0) rw[NP - 1] = cnt;
+  {
+    int k = 0;
+#pragma unroll
+    for (int jb = 0; jb < NB; jb++)
+#pragma unroll
+      for (int kb = 0; kb <= jb; kb++) {
+        const int j = 8 * jb + g;
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int kk = 8 * kb + 2 * t + e;
+          if (j < p && kk < p && kk <= j) rw[p + j * (j + 1) / 2 + kk] = acc[k][e];
+        }
+        k++;
+      }
+  }
+  __syncthreads();
+  double* out = a.partial + ((long long)slot * a.ctas + blockIdx.x) * NP;
+  for (int e = threadIdx.x; e < NP; e += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < MW; q++) s += red[q * NP + e];
+    out[e] = s;
+  }
+}
+
+// ---------------------------------------------------------------- staged dense moments
+// Same sums as k_moments_mma for the dense modes (WRAP, XI, MEMBER, REWEIGHT), with the rows of Z
+// streamed through shared memory by cp.async in SR-row tiles, NST stages deep: the loads of the next
+// tiles are in flight while the DMMAs of the current one run (ncu put the register-fed kernel at
+// 16 long-scoreboard stalls per issue and 35 % DMMA activity).  The per-row weight source (membership
+// byte, norm, d^2) is loaded into a register one issue ahead and stored, as the weight, at the next
+// issue.  Warp w takes 4-row groups 2w, 2w+1 of each 64-row tile.
+static constexpr int SR = 64;        // rows per tile
+static constexpr int SLD = SR + 4;   // padded column stride in shared memory (doubles)
+static constexpr int NST = 3;        // pipeline stages
+
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int NB, int MODE>
+__global__ void __launch_bounds__(MW * 32, 2) k_moments_st(MomArgs a) {
+  constexpr int NBLK = NB * (NB + 1) / 2;
+  extern __shared__ double smem[];  // [NST][p][SLD] tiles, [NST][SR] weights; reused by the epilogue
+  const int slot = blockIdx.y;
+  const int id = a.inst[slot];
+  const int blk = id / a.nstart;
+  const int p = a.p;
+  const long long m = a.m;
+  const double* __restrict__ Z = a.Z + (long long)blk * a.blk_stride;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+  const int NP = p + p * (p + 1) / 2 + 1;
+  double* tiles = smem;
+  double* wts = smem + (size_t)NST * p * SLD;
+  double sh[NB];
+#pragma unroll
+  for (int b = 0; b < NB; b++)
+    sh[b] = (MODE >= MOM_MEMBER && 8 * b + g < p) ? a.shift[(long long)id * RTD_MAXP + 8 * b + g] : 0.0;
+  double A = 0.0, B = 0.0;
+  if (MODE == MOM_XI) {
+    A = a.AB[2 * blk];
+    B = a.AB[2 * blk + 1];
+  }
+  double acc[NBLK][2];
+#pragma unroll
+  for (int k = 0; k < NBLK; k++) acc[k][0] = acc[k][1] = 0.0;
+  double s1[NB];
+#pragma unroll
+  for (int b = 0; b < NB; b++) s1[b] = 0.0;
+  double cnt = 0.0;
+  long long per = (m + a.ctas - 1) / a.ctas;
+  per = (per + 3) / 4 * 4;
+  const long long r_begin = (long long)blockIdx.x * per, r_end = min(m, r_begin + per);
+  const int ntile = r_end > r_begin ? (int)((r_end - r_begin + SR - 1) / SR) : 0;
+  // weight of row r (0 beyond the range)
+  auto wsrc = [&](long long r) -> double {
+    if (r >= r_end) return 0.0;
+    if (MODE == MOM_WRAP) return 1.0;
+    if (MODE == MOM_MEMBER) return (double)a.mem_new[(long long)id * m + r];
+    if (MODE == MOM_XI) {
+      const double rr = a.r[(long long)blk * m + r];
+      const double xi = rr <= A ? 1.0 : (rr <= B ? __ddiv_rn(__dsub_rn(B, rr), __dsub_rn(B, A)) : 0.0);
+      return __dmul_rn(xi, xi);
+    }
+    return a.d2[(long long)id * m + r] <= a.c2 ? 1.0 : 0.0;
+  };
+  double wpend = 0.0;
+  int wpend_stage = -1;
+  auto issue = [&](int tile) {
+    if (wpend_stage >= 0 && tid < SR) wts[wpend_stage * SR + tid] = wpend;  // weight loaded one issue ago
+    wpend_stage = -1;
+    if (tile < ntile) {
+      const int stg = tile % NST;
+      const long long row0 = r_begin + (long long)tile * SR;
+      const int rows = (int)min((long long)SR, r_end - row0);
+      double* T = tiles + (size_t)stg * p * SLD;
+      for (int e = tid; e < p * SR; e += MW * 32) {
+        const int k = e / SR, r = e - k * SR;
+        if (r < rows) cp_async8(T + k * SLD + r, Z + (long long)k * m + row0 + r);
+      }
+      if (tid < SR) {
+        wpend = wsrc(row0 + tid);
+        wpend_stage = stg;
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+  for (int tile = 0; tile < ntile; tile++) {
+    issue(tile + 2);  // stores tile+1's weights, fetches tile+2 into the stage tile-1 used
+    cp_async_wait<2>();
+    __syncthreads();
+    const int stg = tile % NST;
+    const double* T = tiles + (size_t)stg * p * SLD;
+    const double* W = wts + stg * SR;
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      const int r = (2 * warp + q) * 4 + t;  // row of this lane in the tile
+      const double w = W[r];
+      if (!__any_sync(0xffffffffu, w != 0.0)) continue;
+      double u[NB];
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        const int col = 8 * b + g;
+        double v = (w != 0.0 && col < p) ? T[col * SLD + r] : 0.0;
+        if (MODE == MOM_WRAP) v = wrap_g2(v);
+        else if (MODE >= MOM_MEMBER) v = (w != 0.0 && col < p) ? __dsub_rn(v, sh[b]) : 0.0;
+        u[b] = v;
+      }
+      double wu[NB];
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        wu[b] = w * u[b];
+        s1[b] += wu[b];
+      }
+      if (g == 0) cnt += w;
+      int k = 0;
+#pragma unroll
+      for (int jb = 0; jb < NB; jb++)
+#pragma unroll
+        for (int kb = 0; kb <= jb; kb++) {
+          dmma(acc[k][0], acc[k][1], wu[jb], u[kb]);
+          k++;
+        }
+    }
+    __syncthreads();  // the stage of this tile is refilled two issues later
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  mom_epilogue<NB>(acc, s1, cnt, smem, a, slot, p, NP);
+}
 
 template <int NB, int MODE>
 __global__ void __launch_bounds__(MW * 32, 2) k_moments_mma(MomArgs a) {
@@ -140,52 +322,33 @@ __global__ void __launch_bounds__(MW * 32, 2) k_moments_mma(MomArgs a) {
         }
     }
   }
-  // reduce: S1 over the 4 t-lanes, count over the t-lanes of g == 0
-#pragma unroll
-  for (int b = 0; b < NB; b++) {
-    s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 1);
-    s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 2);
-  }
-  cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-  cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
-  double* rw = red + warp * NP;
-  for (int e = lane; e < NP; e += 32) rw[e] = 0.0;
-  __syncwarp();
-  if (t == 0) {
-#pragma unroll
-    for (int b = 0; b < NB; b++)
-      if (8 * b + g < p) rw[8 * b + g] = s1[b];
-  }
-  if (lane == 0) rw[NP - 1] = cnt;
-  {
-    int k = 0;
-#pragma unroll
-    for (int jb = 0; jb < NB; jb++)
-#pragma unroll
-      for (int kb = 0; kb <= jb; kb++) {
-        const int j = 8 * jb + g;
-#pragma unroll
-        for (int e = 0; e < 2; e++) {
-          const int kk = 8 * kb + 2 * t + e;
-          if (j < p && kk < p && kk <= j) rw[p + j * (j + 1) / 2 + kk] = acc[k][e];
-        }
-        k++;
-      }
-  }
-  __syncthreads();
-  double* out = a.partial + ((long long)slot * a.ctas + blockIdx.x) * NP;
-  for (int e = threadIdx.x; e < NP; e += blockDim.x) {
-    double s = 0.0;
-    for (int q = 0; q < MW; q++) s += red[q * NP + e];
-    out[e] = s;
-  }
+  mom_epilogue<NB>(acc, s1, cnt, red, a, slot, p, NP);
 }
 
 template <int NB>
 static void moments_mma_nb(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
   const int NP = mom_np(a.p);
-  const size_t smem = (size_t)MW * NP * sizeof(double);
   dim3 grid(a.ctas, ninst);
+  // staged only where it measured faster on the B200 (config 4, p = 40: dense moments 4.9 -> 3.8 ms per
+  // fit); at p <= 24 or short blocks (configs 1-3, 5) the register-fed kernel is faster
+  static const bool unstaged = getenv("RTD_MOM_UNSTAGED") != nullptr;
+  if (mode != MOM_DELTA && NB >= 4 && a.m >= 65536 && !unstaged) {
+    const size_t smem = std::max((size_t)MW * NP, (size_t)NST * a.p * SLD + (size_t)NST * SR) * sizeof(double);
+#define RTD_ST_CASE(M)                                                                                   \
+  case M:                                                                                                \
+    RTD_CU(cudaFuncSetAttribute(k_moments_st<NB, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_moments_st<NB, M><<<grid, MW * 32, smem, st>>>(a);                                                 \
+    break;
+    switch (mode) {
+      RTD_ST_CASE(MOM_WRAP)
+      RTD_ST_CASE(MOM_XI)
+      RTD_ST_CASE(MOM_MEMBER)
+      RTD_ST_CASE(MOM_REWEIGHT)
+    }
+#undef RTD_ST_CASE
+    return;
+  }
+  const size_t smem = (size_t)MW * NP * sizeof(double);
 #define RTD_MM_CASE(M)                                                                                   \
   case M:                                                                                                \
     RTD_CU(cudaFuncSetAttribute(k_moments_mma<NB, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
