@@ -33,7 +33,7 @@ namespace rtd {
 static constexpr int NBK = 4096;         // buckets per column (incl. underflow 0 and overflow NBK-1)
 static constexpr int SAMPLE = 4096;      // strided sample for the bucket map
 static constexpr int CAP = 65536;        // max gathered elements per side per column
-static constexpr int PCTA = 128;         // CTAs per column in the streaming passes (fixed -> deterministic)
+static constexpr int PCTA = 32;          // CTAs per column in the streaming passes (fixed -> deterministic)
 static constexpr int PT = 256;
 
 struct PrunedCol {
@@ -144,22 +144,29 @@ __global__ void __launch_bounds__(1024) k_pr_sample(const double* __restrict__ c
   }
 }
 
-// 2. histogram (count, sum) per bucket: shared-memory privatised, folded with global atomics
+// 2. histogram per bucket: the count and, for interior buckets, the sum of the 16-bit fixed-point
+//    offsets q = floor(2^16 (y - L_b) / w) of its elements (native 32-bit shared atomics; a CTA takes at
+//    most 65536 elements so a bucket's sum fits 32 bits).  An element with offset q lies in
+//    [L_b + w (q - 1) 2^-16, L_b + w (q + 2) 2^-16] (the margin covers the rounding of the offset), so
+//    the bucket sum is known to an interval (k_pr_scan).  The under- and overflow buckets' sums are
+//    accumulated in registers (fp64) and added once per warp.
 __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols, long long len,
                                                 const PrunedCol* __restrict__ pc, int* __restrict__ cnt,
-                                                double* __restrict__ s1, unsigned long long* __restrict__ mm) {
-  __shared__ int hc[NBK];
-  __shared__ double hs[NBK];
+                                                unsigned long long* __restrict__ tq, double* __restrict__ esum,
+                                                unsigned long long* __restrict__ mm) {
+  __shared__ unsigned int hc[NBK];
+  __shared__ unsigned int hq[NBK];
   const int col = blockIdx.y;
   const PrunedCol c = pc[col];
   if (c.status) return;
   for (int b = threadIdx.x; b < NBK; b += PT) {
-    hc[b] = 0;
-    hs[b] = 0.0;
+    hc[b] = 0u;
+    hq[b] = 0u;
   }
   __syncthreads();
   const double* y = cols + (long long)col * len;
   unsigned long long kmin = ~0ull, kmax = 0ull;
+  double e0 = 0.0, e1 = 0.0;
   const long long per = (len + gridDim.x - 1) / gridDim.x;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
   for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
@@ -173,8 +180,16 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
     for (int k = 0; k < ILP; k++) {
       if (base + (long long)k * PT < i1) {
         const int b = bucket_of(v[k], c);
-        atomicAdd(&hc[b], 1);
-        atomicAdd(&hs[b], v[k]);
+        atomicAdd(&hc[b], 1u);
+        if (b == 0) {
+          e0 += v[k];
+        } else if (b == NBK - 1) {
+          e1 += v[k];
+        } else {
+          const double tt = __dsub_rn(__dmul_rn(__dsub_rn(v[k], c.lo), c.inv_w), (double)(b - 1));
+          const int q = (int)fmin(fmax(__dmul_rn(tt, 65536.0), 0.0), 65535.0);
+          atomicAdd(&hq[b], (unsigned int)q);
+        }
         const unsigned long long kk = ord_key(v[k]);
         kmin = min(kmin, kk);
         kmax = max(kmax, kk);
@@ -184,72 +199,113 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
   for (int d = 16; d > 0; d >>= 1) {
     kmin = min(kmin, __shfl_down_sync(0xffffffffu, kmin, d));
     kmax = max(kmax, __shfl_down_sync(0xffffffffu, kmax, d));
+    e0 += __shfl_down_sync(0xffffffffu, e0, d);
+    e1 += __shfl_down_sync(0xffffffffu, e1, d);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicMin(&mm[2 * col], kmin);
     atomicMax(&mm[2 * col + 1], kmax);
+    if (e0 != 0.0) atomicAdd(&esum[2 * col], e0);
+    if (e1 != 0.0) atomicAdd(&esum[2 * col + 1], e1);
   }
   __syncthreads();
   int* cn = cnt + (long long)col * NBK;
-  double* a1 = s1 + (long long)col * NBK;
+  unsigned long long* tqc = tq + (long long)col * NBK;
   for (int b = threadIdx.x; b < NBK; b += PT)
     if (hc[b]) {
-      atomicAdd(&cn[b], hc[b]);
-      atomicAdd(&a1[b], hs[b]);
+      atomicAdd(&cn[b], (int)hc[b]);
+      if (hq[b]) atomicAdd(&tqc[b], (unsigned long long)hq[b]);
     }
 }
 
-// 3a. prefix arrays over buckets (one CTA per column): rank offsets C, sums A1,
-//     and bounds on the sums of squares Q2lo / Q2hi; margins E1, E2
+// 3a. prefix arrays over buckets (one CTA per column): rank offsets C, the interval [Slo, Shi] of
+//     every bucket's sum (fixed-point offsets, k_pr_hist; the end buckets' fp64 sums widened by 1e-12
+//     relative) and its prefix sums A1lo / A1hi, bounds on the sums of squares Q2lo / Q2hi; margins E1,
+//     E2 for the rounding of these fp64 evaluations
 struct BucketScan {
   double E1, E2;
 };
 
+__device__ __forceinline__ void bucket_sum_interval(int b, int r, unsigned long long T, const double* es,
+                                                    const PrunedCol& c, double& Slo, double& Shi) {
+  if (r == 0) {
+    Slo = Shi = 0.0;
+  } else if (b == 0 || b == NBK - 1) {
+    const double S = es[b == 0 ? 0 : 1];
+    Slo = S - 1e-12 * fabs(S);
+    Shi = S + 1e-12 * fabs(S);
+  } else {
+    const double rd = (double)r, Lb = c.lo + (double)(b - 1) * c.w, u = c.w * (1.0 / 65536.0);
+    Slo = fmax(rd * bucket_lo(b, c), rd * Lb + u * ((double)T - rd));
+    Shi = fmin(rd * bucket_hi(b, c), rd * Lb + u * ((double)T + 2.0 * rd));
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_pr_scan(PrunedCol* __restrict__ pc, const int* __restrict__ cnt,
-                                                  const double* __restrict__ s1,
+                                                  const unsigned long long* __restrict__ tq,
+                                                  const double* __restrict__ esum,
                                                   const unsigned long long* __restrict__ mm, long long* __restrict__ Cg,
                                                   double* __restrict__ A1g, double* __restrict__ Q2log,
-                                                  double* __restrict__ Q2hig, BucketScan* __restrict__ bsc) {
+                                                  double* __restrict__ Q2hig, double* __restrict__ sbg,
+                                                  BucketScan* __restrict__ bsc) {
   __shared__ double red_d[32];
   __shared__ long long wc[32];
-  __shared__ double w1[32], wlo[32], whi[32];
+  __shared__ double w1[32], wh[32], wlo[32], whi[32];
   const int col = blockIdx.x;
   PrunedCol c = pc[col];
   if (c.status) return;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int* cn = cnt + (long long)col * NBK;
-  const double* sb = s1 + (long long)col * NBK;
+  const unsigned long long* tqc = tq + (long long)col * NBK;
+  const double* es = esum + 2 * col;
+  double* sblo = sbg + (long long)col * 2 * NBK;
+  double* sbhi = sblo + NBK;
   c.cmin = ord_val(mm[2 * col]);
   c.cmax = ord_val(mm[2 * col + 1]);
   long long* C = Cg + (long long)col * (NBK + 1);
-  double* A1 = A1g + (long long)col * (NBK + 1);
+  double* A1lo = A1g + (long long)col * 2 * (NBK + 1);
+  double* A1hi = A1lo + (NBK + 1);
   double* Q2lo = Q2log + (long long)col * (NBK + 1);
   double* Q2hi = Q2hig + (long long)col * (NBK + 1);
-  const int per = NBK / 1024;
+  constexpr int per = NBK / 1024;
+  double slo[per], shi[per], qlo[per], qhi[per];
   long long lc = 0;
-  double l1 = 0.0, llo = 0.0, lhi = 0.0, abs1 = 0.0;
-  for (int b = t * per; b < (t + 1) * per; b++) {
+  double l1 = 0.0, lh = 0.0, llo = 0.0, lhi = 0.0, abs1 = 0.0;
+#pragma unroll
+  for (int e = 0; e < per; e++) {
+    const int b = t * per + e;
     const int r = cn[b];
-    const double S = sb[b];
-    const double L = bucket_lo(b, c), U = bucket_hi(b, c);
-    lc += r;
-    l1 += S;
-    abs1 += fabs(S);
+    bucket_sum_interval(b, r, tqc[b], es, c, slo[e], shi[e]);
+    sblo[b] = slo[e];
+    sbhi[b] = shi[e];
+    const double L = bucket_lo(b, c), U = bucket_hi(b, c), rd = (double)r;
+    qlo[e] = 0.0;
+    qhi[e] = 0.0;
     if (r > 0) {
-      llo += S * S / r;
-      lhi += fmax(S * (L + U) - r * L * U, S * S / r);
+      const double mn2 = (slo[e] <= 0.0 && shi[e] >= 0.0) ? 0.0 : fmin(slo[e] * slo[e], shi[e] * shi[e]);
+      const double mx2 = fmax(slo[e] * slo[e], shi[e] * shi[e]);
+      qlo[e] = mn2 / rd;
+      qhi[e] = fmax(fmax(slo[e] * (L + U), shi[e] * (L + U)) - rd * L * U, mx2 / rd);
     }
+    lc += r;
+    l1 += slo[e];
+    lh += shi[e];
+    llo += qlo[e];
+    lhi += qhi[e];
+    abs1 += fmax(fabs(slo[e]), fabs(shi[e]));
   }
   long long ic = lc;
-  double i1 = l1, ilo = llo, ihi = lhi;
+  double i1 = l1, ih = lh, ilo = llo, ihi = lhi;
   for (int d = 1; d < 32; d <<= 1) {
     long long vc = __shfl_up_sync(0xffffffffu, ic, d);
     double v1 = __shfl_up_sync(0xffffffffu, i1, d);
+    double vh = __shfl_up_sync(0xffffffffu, ih, d);
     double vlo = __shfl_up_sync(0xffffffffu, ilo, d);
     double vhi = __shfl_up_sync(0xffffffffu, ihi, d);
     if (lane >= d) {
       ic += vc;
       i1 += v1;
+      ih += vh;
       ilo += vlo;
       ihi += vhi;
     }
@@ -257,53 +313,57 @@ __global__ void __launch_bounds__(1024) k_pr_scan(PrunedCol* __restrict__ pc, co
   if (lane == 31) {
     wc[w] = ic;
     w1[w] = i1;
+    wh[w] = ih;
     wlo[w] = ilo;
     whi[w] = ihi;
   }
   __syncthreads();
   if (w == 0) {
     long long vc = wc[lane];
-    double v1 = w1[lane], vlo = wlo[lane], vhi = whi[lane];
+    double v1 = w1[lane], vh = wh[lane], vlo = wlo[lane], vhi = whi[lane];
     long long xc = vc;
-    double x1 = v1, xlo = vlo, xhi = vhi;
+    double x1 = v1, xh = vh, xlo = vlo, xhi = vhi;
     for (int d = 1; d < 32; d <<= 1) {
       long long yc = __shfl_up_sync(0xffffffffu, xc, d);
       double y1 = __shfl_up_sync(0xffffffffu, x1, d);
+      double yh = __shfl_up_sync(0xffffffffu, xh, d);
       double ylo = __shfl_up_sync(0xffffffffu, xlo, d);
       double yhi = __shfl_up_sync(0xffffffffu, xhi, d);
       if (lane >= d) {
         xc += yc;
         x1 += y1;
+        xh += yh;
         xlo += ylo;
         xhi += yhi;
       }
     }
     wc[lane] = xc - vc;
     w1[lane] = x1 - v1;
+    wh[lane] = xh - vh;
     wlo[lane] = xlo - vlo;
     whi[lane] = xhi - vhi;
   }
   __syncthreads();
   long long ec = wc[w] + ic - lc;
-  double e1 = w1[w] + i1 - l1, elo = wlo[w] + ilo - llo, ehi = whi[w] + ihi - lhi;
-  for (int b = t * per; b < (t + 1) * per; b++) {
-    const int r = cn[b];
-    const double S = sb[b];
+  double e1 = w1[w] + i1 - l1, eh = wh[w] + ih - lh, elo = wlo[w] + ilo - llo, ehi = whi[w] + ihi - lhi;
+#pragma unroll
+  for (int e = 0; e < per; e++) {
+    const int b = t * per + e;
     C[b] = ec;
-    A1[b] = e1;
+    A1lo[b] = e1;
+    A1hi[b] = eh;
     Q2lo[b] = elo;
     Q2hi[b] = ehi;
-    ec += r;
-    e1 += S;
-    if (r > 0) {
-      const double L = bucket_lo(b, c), U = bucket_hi(b, c);
-      elo += S * S / r;
-      ehi += fmax(S * (L + U) - r * L * U, S * S / r);
-    }
+    ec += cn[b];
+    e1 += slo[e];
+    eh += shi[e];
+    elo += qlo[e];
+    ehi += qhi[e];
   }
   if (t == 1023) {
     C[NBK] = ec;
-    A1[NBK] = e1;
+    A1lo[NBK] = e1;
+    A1hi[NBK] = eh;
     Q2lo[NBK] = elo;
     Q2hi[NBK] = ehi;
   }
@@ -339,15 +399,16 @@ __device__ __forceinline__ VBound window_bounds(long long s, long long h, int b,
     hi2 = hd * mx1;
   } else {
     const double n1 = (double)cn[b], n2 = (double)cn[be];
-    const double Sb = sb[b], Se = sb[be];
+    // bucket sums are intervals: sb[0..NBK) lower ends, sb[NBK..2NBK) upper ends; A1 likewise
+    const double Sblo = sb[b], Sbhi = sb[NBK + b], Selo = sb[be], Sehi = sb[NBK + be];
     const double r1 = (double)(C[b + 1] - s), r2 = (double)(s + h - C[be]);
     // top r1 elements of bucket b: mean >= bucket mean; the other n1 - r1 are >= L1
-    const double t1lo = fmax(r1 * L1, r1 * Sb / n1), t1hi = fmin(r1 * U1, Sb - (n1 - r1) * L1);
+    const double t1lo = fmax(r1 * L1, r1 * Sblo / n1), t1hi = fmin(r1 * U1, Sbhi - (n1 - r1) * L1);
     // bottom r2 elements of bucket be: mean <= bucket mean; the other n2 - r2 are <= U2
-    const double t2lo = fmax(r2 * L2, Se - (n2 - r2) * U2), t2hi = fmin(r2 * U2, r2 * Se / n2);
-    const double F1 = A1[be] - A1[b + 1];
-    lo1 = F1 + fmin(t1lo, t1hi) + fmin(t2lo, t2hi) - m.E1;
-    hi1 = F1 + fmax(t1lo, t1hi) + fmax(t2lo, t2hi) + m.E1;
+    const double t2lo = fmax(r2 * L2, Selo - (n2 - r2) * U2), t2hi = fmin(r2 * U2, r2 * Sehi / n2);
+    const double F1lo = A1[be] - A1[b + 1], F1hi = A1[NBK + 1 + be] - A1[NBK + 1 + b + 1];
+    lo1 = F1lo + fmin(t1lo, t1hi) + fmin(t2lo, t2hi) - m.E1;
+    hi1 = F1hi + fmax(t1lo, t1hi) + fmax(t2lo, t2hi) + m.E1;
     lo2 = (Q2lo[be] - Q2lo[b + 1]) + r1 * mn1 + r2 * mn2 - m.E2;
     hi2 = (Q2hi[be] - Q2hi[b + 1]) + r1 * mx1 + r2 * mx2 + m.E2;
   }
@@ -374,10 +435,10 @@ __device__ __forceinline__ PartBounds part_bounds(long long s, long long h, int 
                                                   const long long* C, const int* cn, const double* sb) {
   const double L1 = bucket_lo(b, c), U1 = bucket_hi(b, c), L2 = bucket_lo(be, c), U2 = bucket_hi(be, c);
   const double n1 = (double)cn[b], n2 = (double)cn[be];
-  const double Sb = sb[b], Se = sb[be];
+  const double Sblo = sb[b], Sbhi = sb[NBK + b], Selo = sb[be], Sehi = sb[NBK + be];
   const double r1 = (double)(C[b + 1] - s), r2 = (double)(s + h - C[be]);
-  const double a = fmax(r1 * L1, r1 * Sb / n1), bb = fmin(r1 * U1, Sb - (n1 - r1) * L1);
-  const double d = fmax(r2 * L2, Se - (n2 - r2) * U2), e = fmin(r2 * U2, r2 * Se / n2);
+  const double a = fmax(r1 * L1, r1 * Sblo / n1), bb = fmin(r1 * U1, Sbhi - (n1 - r1) * L1);
+  const double d = fmax(r2 * L2, Selo - (n2 - r2) * U2), e = fmin(r2 * U2, r2 * Sehi / n2);
   return {fmin(a, bb), fmax(a, bb), fmin(d, e), fmax(d, e)};
 }
 
@@ -388,9 +449,9 @@ __device__ __forceinline__ double chunk_lower(long long sa, long long sb, long l
                                               const double* Q2lo, const int* cn, const double* sbk, BucketScan m) {
   const double hd = (double)h;
   const PartBounds pa = part_bounds(sa, h, b, be, c, C, cn, sbk), pb = part_bounds(sb, h, b, be, c, C, cn, sbk);
-  const double F1 = A1[be] - A1[b + 1];
-  const double lo1 = F1 + fmin(pa.t1lo, pb.t1lo) + fmin(pa.t2lo, pb.t2lo) - m.E1;
-  const double hi1 = F1 + fmax(pa.t1hi, pb.t1hi) + fmax(pa.t2hi, pb.t2hi) + m.E1;
+  const double F1lo = A1[be] - A1[b + 1], F1hi = A1[NBK + 1 + be] - A1[NBK + 1 + b + 1];
+  const double lo1 = F1lo + fmin(pa.t1lo, pb.t1lo) + fmin(pa.t2lo, pb.t2lo) - m.E1;
+  const double hi1 = F1hi + fmax(pa.t1hi, pb.t1hi) + fmax(pa.t2hi, pb.t2hi) + m.E1;
   const double L1 = bucket_lo(b, c), U1 = bucket_hi(b, c), L2 = bucket_lo(be, c), U2 = bucket_hi(be, c);
   const double mn1 = (L1 <= 0 && U1 >= 0) ? 0.0 : fmin(L1 * L1, U1 * U1);
   const double mn2 = (L2 <= 0 && U2 >= 0) ? 0.0 : fmin(L2 * L2, U2 * U2);
@@ -412,7 +473,7 @@ static constexpr int CHUNK = 32;  // starts per chunk in the coarse lower-bound 
 //     mode 1: chunk lower bounds over all starts -> per-CTA range of candidate chunks;
 //     mode 2: per-start lower bounds inside the candidate chunk range -> per-CTA candidate range.
 __global__ void __launch_bounds__(PT) k_pr_bound(long long len, long long h, const PrunedCol* __restrict__ pc,
-                                                 const int* __restrict__ cnt, const double* __restrict__ s1,
+                                                 const int* __restrict__ cnt, const double* __restrict__ sbg,
                                                  const long long* __restrict__ Cg, const double* __restrict__ A1g,
                                                  const double* __restrict__ Q2log, const double* __restrict__ Q2hig,
                                                  const BucketScan* __restrict__ bsc, int mode,
@@ -424,11 +485,11 @@ __global__ void __launch_bounds__(PT) k_pr_bound(long long len, long long h, con
   const PrunedCol c = pc[col];
   if (c.status) return;
   const long long* C = Cg + (long long)col * (NBK + 1);
-  const double* A1 = A1g + (long long)col * (NBK + 1);
+  const double* A1 = A1g + (long long)col * 2 * (NBK + 1);  // [lo | hi] prefix sums of bucket sums
   const double* Q2lo = Q2log + (long long)col * (NBK + 1);
   const double* Q2hi = Q2hig + (long long)col * (NBK + 1);
   const int* cn = cnt + (long long)col * NBK;
-  const double* sbk = s1 + (long long)col * NBK;
+  const double* sbk = sbg + (long long)col * 2 * NBK;       // [lo | hi] bucket sums
   const BucketScan m = bsc[col];
   const long long nwin = len - h + 1;
   const long long gtid = (long long)blockIdx.x * PT + threadIdx.x;
@@ -657,7 +718,7 @@ __global__ void __launch_bounds__(1024) k_pr_prefix(const PrunedCol* __restrict_
 // 5a'. the common case, every gathered segment holding at most SMAX elements: sort the segment in
 //      shared memory (bitonic) and take its prefix sums in the same CTA (replaces the segmented radix
 //      sort's passes and the separate prefix launch)
-static constexpr int SMAX = 8192;
+static constexpr int SMAX = 16384;
 __global__ void __launch_bounds__(1024) k_pr_sortprefix(const PrunedCol* __restrict__ pc, const double* __restrict__ g,
                                                         const int* __restrict__ gcount, const dd2* __restrict__ below,
                                                         dd2* __restrict__ pref) {
@@ -829,7 +890,9 @@ __global__ void k_pr_final(UniConst uc, const dd2* __restrict__ part, const long
 struct PrScratch {
   PrunedCol* pc;
   int* cnt;
-  double* s1;
+  unsigned long long* tq;  // fixed-point offset sums per bucket
+  double* esum;            // under- / overflow bucket sums
+  double* sbb;             // [col][lo | hi] bucket sum intervals
   unsigned long long* mm;
   double *g, *gsorted;
   int* gcount;
@@ -860,7 +923,9 @@ static size_t seg_sort_bytes(int nseg) {
 static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.pc = A.take<PrunedCol>(ncols);
   s.cnt = A.take<int>((size_t)ncols * NBK);
-  s.s1 = A.take<double>((size_t)ncols * NBK);
+  s.tq = A.take<unsigned long long>((size_t)ncols * NBK);
+  s.esum = A.take<double>((size_t)ncols * 2);
+  s.sbb = A.take<double>((size_t)ncols * 2 * NBK);
   s.mm = A.take<unsigned long long>(2 * (size_t)ncols);
   s.g = A.take<double>((size_t)2 * ncols * CAP);
   s.gsorted = A.take<double>((size_t)2 * ncols * CAP);
@@ -876,7 +941,7 @@ static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.cub_bytes = seg_sort_bytes(2 * ncols);
   s.cub_tmp = A.take<char>(s.cub_bytes);
   s.C = A.take<long long>((size_t)ncols * (NBK + 1));
-  s.A1 = A.take<double>((size_t)ncols * (NBK + 1));
+  s.A1 = A.take<double>((size_t)ncols * 2 * (NBK + 1));
   s.Q2lo = A.take<double>((size_t)ncols * (NBK + 1));
   s.Q2hi = A.take<double>((size_t)ncols * (NBK + 1));
   s.bsc = A.take<BucketScan>(ncols);
@@ -896,19 +961,20 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   if (A.base == nullptr) return true;  // dry run
   const long long h = len / 2 + 1;
   RTD_CU(cudaMemsetAsync(s.cnt, 0, (size_t)ncols * NBK * sizeof(int), st));
-  RTD_CU(cudaMemsetAsync(s.s1, 0, (size_t)ncols * NBK * sizeof(double), st));
+  RTD_CU(cudaMemsetAsync(s.tq, 0, (size_t)ncols * NBK * sizeof(unsigned long long), st));
+  RTD_CU(cudaMemsetAsync(s.esum, 0, (size_t)ncols * 2 * sizeof(double), st));
   RTD_CU(cudaMemsetAsync(s.gcount, 0, 2 * (size_t)ncols * sizeof(int), st));
   k_pr_sample<<<ncols, 1024, 0, st>>>(cols, len, s.pc, s.mm);
   RTD_LAUNCHED();
   // ~64K elements per CTA: many CTAs per column so the 4-CTA/SM waves quantise finely (a CTA flushes its
   // 4096-bin histogram with global atomics, about 1/8 of its element count)
-  const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((len + 65535) / 65536, 1024));
-  k_pr_hist<<<dim3(gx, ncols), PT, 0, st>>>(cols, len, s.pc, s.cnt, s.s1, s.mm);
+  const unsigned gx = (unsigned)std::max<long long>(1, (len + 65535) / 65536);  // <= 65536 elements per CTA
+  k_pr_hist<<<dim3(gx, ncols), PT, 0, st>>>(cols, len, s.pc, s.cnt, s.tq, s.esum, s.mm);
   RTD_LAUNCHED();
-  k_pr_scan<<<ncols, 1024, 0, st>>>(s.pc, s.cnt, s.s1, s.mm, s.C, s.A1, s.Q2lo, s.Q2hi, s.bsc);
+  k_pr_scan<<<ncols, 1024, 0, st>>>(s.pc, s.cnt, s.tq, s.esum, s.mm, s.C, s.A1, s.Q2lo, s.Q2hi, s.sbb, s.bsc);
   RTD_LAUNCHED();
   for (int mode = 0; mode < 3; mode++) {
-    k_pr_bound<<<dim3(s.nbound, ncols), PT, 0, st>>>(len, h, s.pc, s.cnt, s.s1, s.C, s.A1, s.Q2lo, s.Q2hi, s.bsc,
+    k_pr_bound<<<dim3(s.nbound, ncols), PT, 0, st>>>(len, h, s.pc, s.cnt, s.sbb, s.C, s.A1, s.Q2lo, s.Q2hi, s.bsc,
                                                       mode, s.best_ub, s.crange, s.ub_part, s.range_part);
     RTD_LAUNCHED();
     if (mode == 0) k_pr_ubmin<<<ncols, 32, 0, st>>>(s.pc, s.ub_part, s.nbound, s.best_ub);
