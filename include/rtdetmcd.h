@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define RTDETMCD_ABI_VERSION 1
+#define RTDETMCD_ABI_VERSION 2
 
 typedef struct rtdetmcd_ctx rtdetmcd_ctx;
 
@@ -53,6 +53,14 @@ typedef enum {
 } rtdetmcd_status;
 
 enum { RTD_PART_PERMUTE = 0, RTD_PART_CONTIGUOUS = 1 };
+/* C-step distances (the "D" of the paper's Table 1): by the Cholesky factor
+ * (§3.4, default) or by the explicit inverse (variant I; needs p >= 8) */
+enum { RTD_DIST_CHOLESKY = 0, RTD_DIST_INVERSE = 1 };
+/* consistency factor of the raw scatter: c(alpha) of Croux-Haesbroeck as the text defines it
+ * (default) or the median rule -- the h-subset covariance times
+ * median_i d_i^2 / chi2_{p,0.5} over the rows of the block -- with which the paper's Table 2 KL
+ * values are reproduced (DESIGN.md finding F1) */
+enum { RTD_CONS_ALPHA = 0, RTD_CONS_MEDIAN = 1 };
 
 /* warning bits of rtdetmcd_result.warnings (non-fatal) */
 enum {
@@ -72,10 +80,13 @@ typedef struct {
   double kappa_max;      /* condition threshold; default 1000 */
   double quantile;       /* cut-off quantile; default 0.975 */
   int32_t max_csteps;    /* C-step cap per start; default 100 */
-  int32_t refresh_every; /* update-based C-steps: full recompute of the sums every this many steps; default 32 */
+  int32_t refresh_every; /* update-based C-steps: full recompute of the sums every this many steps; default 32;
+                            1 = plain recompute every step (variants I / ID of Table 1) */
   uint64_t seed;         /* key of the random partition */
   int32_t partition;     /* RTD_PART_PERMUTE (keyed Feistel permutation, default) | RTD_PART_CONTIGUOUS */
   int32_t log_transform; /* 1: fit ln(x) (x must be > 0), as in BASELINE config 5 */
+  int32_t distance;      /* RTD_DIST_CHOLESKY (default) | RTD_DIST_INVERSE (ablation variant I) */
+  int32_t consistency;   /* RTD_CONS_ALPHA (default) | RTD_CONS_MEDIAN */
 } rtdetmcd_opts;
 
 /* Fills *o with the defaults above. */

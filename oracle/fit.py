@@ -158,9 +158,16 @@ def warm_block(Zb: np.ndarray, mu0: np.ndarray, Sigma0: np.ndarray, hb: int, kap
 
 def fit(X: np.ndarray, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0,
         kappa_max: float = 1000.0, quantile: float = 0.975, max_csteps: int = 100,
-        log_transform: bool = False, partition_mode: str = "permute", warm_start=None) -> FitResult:
+        log_transform: bool = False, partition_mode: str = "permute", warm_start=None,
+        consistency: str = "alpha") -> FitResult:
     """warm_start: optional (mu, Sigma) of a previous fit in the units this fit reports (after ln
-    when log_transform) -- the single C-step start of every block (warm_block)."""
+    when log_transform) -- the single C-step start of every block (warm_block).
+
+    consistency: "alpha" -- Sigma_raw = c(alpha) Sigma_H, the factor the text defines (PAPER.md:158-175,
+    reading R1); "median" -- Sigma_raw = median_i d^2(z_i; mu_H, Sigma_H) / chi2_{p,0.5} Sigma_H over the
+    rows of the block, the rule that reproduces the paper's Table 2 (DESIGN.md finding F1)."""
+    if consistency not in ("alpha", "median"):
+        raise FitError("INVALID_ARG", f"consistency {consistency}")
     X = np.asarray(X, dtype=np.float64)
     n, p = X.shape
     if not np.all(np.isfinite(X)):
@@ -196,7 +203,11 @@ def fit(X: np.ndarray, h: int | None = None, alpha: float = 0.5, q: int = 1, see
         if chosen >= 0:
             st = starts[chosen]
             bf.mu = st.mu
-            bf.Sigma_raw = consistency_factor(hb / m, p) * st.Sigma
+            if consistency == "median":
+                factor = float(np.median(mahalanobis_sq(Zb, st.mu, st.Sigma))) / chi2_quantile(0.5, p)
+            else:
+                factor = consistency_factor(hb / m, p)
+            bf.Sigma_raw = factor * st.Sigma
             bf.logdet = st.logdet
             if not st.converged:
                 warnings.append(f"MAX_CSTEPS_BLOCK{l}")

@@ -34,6 +34,7 @@ class Opts(C.Structure):
         ("h", C.c_int64), ("alpha", C.c_double), ("shards", C.c_int32), ("shard_cap", C.c_int32),
         ("omega", C.c_int64), ("kappa_max", C.c_double), ("quantile", C.c_double), ("max_csteps", C.c_int32),
         ("refresh_every", C.c_int32), ("seed", C.c_uint64), ("partition", C.c_int32), ("log_transform", C.c_int32),
+        ("distance", C.c_int32), ("consistency", C.c_int32),
     ]
 
 

@@ -139,11 +139,13 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
         quantile: float = 0.975, max_csteps: int = 100, refresh_every: int = 32, partition: int = 0,
         log_transform: bool = False, outputs=("flags", "rd2", "weights", "hsubset"), device: int | None = None,
         torch_workspace: bool = True, out_buffers: dict | None = None, ctx: dict | None = None,
-        warm_start=None) -> Fit:
+        warm_start=None, distance: int = 0, consistency: int = 0) -> Fit:
     """rtdetmcd_fit on an n x p row-major float64 matrix (numpy or torch, host or device).
 
     warm_start=(mu, sigma): rtdetmcd_fit_warm -- the C-steps of every block start from this
     previous fit (X units, after ln when log_transform) instead of the refined initial estimators.
+    distance: RTD_DIST_CHOLESKY (0) | RTD_DIST_INVERSE (1, Table 1 variant I); refresh_every=1 gives the
+    plain-recompute C-steps of variants I / ID.  consistency: RTD_CONS_ALPHA (0) | RTD_CONS_MEDIAN (1).
     """
     ptr, keep, is_cuda, dev = _as_f64(X)
     n, p = int(keep.shape[0]), int(keep.shape[1])
@@ -153,7 +155,8 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
         _sync_torch(dev)
     o = default_opts(h=int(h or 0), alpha=float(alpha), shards=int(q), seed=int(seed), kappa_max=float(kappa_max),
                      quantile=float(quantile), max_csteps=int(max_csteps), refresh_every=int(refresh_every),
-                     partition=int(partition), log_transform=int(bool(log_transform)))
+                     partition=int(partition), log_transform=int(bool(log_transform)), distance=int(distance),
+                     consistency=int(consistency))
     L = lib()
     if torch_workspace:
         torch = _torch()

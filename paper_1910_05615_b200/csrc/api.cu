@@ -16,6 +16,10 @@
 
 namespace rtd {
 bool dist_mma_supported(int p);
+void launch_dist_inv(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
+                     int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st);
+void launch_scale_median(const double* sig_all, const int* chosen_inst, const double* qv, int q, long long m, int p,
+                         double chi2half, double* out_all, cudaStream_t st);
 void launch_dist_mma(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
                      int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st);
 long long launch_count();
@@ -245,7 +249,7 @@ void carve_cstep(Arena& A, CStepBufs& b, int ninst, long long m, int p, int max_
   b.cond = A.take<double>(ninst);
   b.traj_stride = max_steps + 2;
   b.traj = A.take<double>((size_t)ninst * b.traj_stride);
-  b.cstage = A.take<double>(RTD_CONST_DOUBLES + (size_t)ninst * (RTD_MAXP + RTD_MAXP * (RTD_MAXP + 1) / 2));
+  b.cstage = A.take<double>(RTD_CONST_DOUBLES + (size_t)ninst * (RTD_MAXP + RTD_MAXP * RTD_MAXP));  // full inverse fits
   b.ctas = (int)std::max<long long>(1, std::min<long long>(256, (m + 4095) / 4096));
   b.partial = A.take<double>((size_t)ninst * b.ctas * NPMAX);
   b.d2 = A.take<double>((size_t)ninst * m);
@@ -286,10 +290,16 @@ MomArgs mom_args(const CStepBufs& b, const double* Z, long long blk_stride, int 
 // upload distance operators of instances act[g0, g0+cnt) (staged in cstage slots) and run the distance pass
 // upload distance operators of instances act[g0, g0+cnt) (staged in cstage slots) and run the distance pass
 void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long blk_stride, int nstart, int nact,
-                 int cstride) {
+                 int cstride, int dist_mode = RTD_DIST_CHOLESKY) {
   // algorithmic HBM bytes: every start's C-step streams its block (8 p per row) and writes d^2 (8 per row);
   // flops: the triangular operator and the squared norm, 2 (p(p+1)/2 + p) per row per start
   const double fm = (double)b.m, pp = (double)b.p;
+  if (dist_mode == RTD_DIST_INVERSE) {  // ablation variant I: full quadratic form, 2 p^2 + 2 p flops per row
+    ProfScope ps("dist", (double)nact * fm * (8.0 * pp + 8.0), (double)nact * fm * (2.0 * pp * pp + 2.0 * pp),
+                 (double)nact * fm * (8.0 * pp + 8.0));
+    launch_dist_inv(b.p, Z, b.m, blk_stride, b.inst_dev, nstart, nact, b.cstage, cstride, b.d2, st);
+    return;
+  }
   if (dist_mma_supported(b.p)) {  // FP64 tensor-pipe kernel: operator read from cstage, all instances at once
     ProfScope ps("dist", (double)nact * fm * (8.0 * pp + 8.0), (double)nact * fm * (pp * (pp + 1.0) + 2.0 * pp),
                  (double)nact * fm * (8.0 * pp + 8.0));
@@ -310,10 +320,11 @@ void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long
 // On exit: status ST_CONVERGED / ST_MAXSTEPS (usable) or a failure code;
 // mu/sigma = exact mean / covariance of the final h-subset (in memA), logdet.
 void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_stride, int nstart, int ninst, long long h,
-                double kappa_max, int max_steps, int refresh, std::vector<int>& status_h, std::vector<int>& steps_h) {
+                double kappa_max, int max_steps, int refresh, std::vector<int>& status_h, std::vector<int>& steps_h,
+                int dist_mode = RTD_DIST_CHOLESKY) {
   const int p = b.p;
   const long long m = b.m;
-  const int cstride = p + p * (p + 1) / 2;
+  const int cstride = p + (dist_mode == RTD_DIST_INVERSE ? p * p : p * (p + 1) / 2);
   const int np = mom_np(p);
   RTD_CU(cudaMemsetAsync(b.memA, 0, (size_t)ninst * m, st));
   RTD_CU(cudaMemsetAsync(b.memB, 0, (size_t)ninst * m, st));
@@ -335,9 +346,9 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     {
       ProfScope ps("prepare", 0.0);
       launch_prepare(b.inst_dev, na, b.mu, b.sigma, p, kappa_max, b.cstage, cstride, b.logdet, b.cond, b.status,
-                     b.traj, b.traj_stride, step, st);
+                     b.traj, b.traj_stride, step, st, dist_mode == RTD_DIST_INVERSE);
     }
-    dist_groups(st, b, Z, blk_stride, nstart, na, cstride);
+    dist_groups(st, b, Z, blk_stride, nstart, na, cstride, dist_mode);
     RTD_CU(cudaMemsetAsync(b.changed, 0, ninst * sizeof(int), st));
     {
       ProfScope ps("select", (double)na * m * 9.0);
@@ -674,6 +685,13 @@ Dims make_dims(long long n, int p, const rtdetmcd_opts& o, bool x_host) {
   d.x_host = x_host;
   if (o.max_csteps < 1 || o.max_csteps > 10000) throw Fail{RTD_E_INVALID_ARG, "max_csteps out of range"};
   if (!(o.quantile > 0.0 && o.quantile < 1.0)) throw Fail{RTD_E_INVALID_ARG, "quantile must be in (0,1)"};
+  if (o.distance != RTD_DIST_CHOLESKY && o.distance != RTD_DIST_INVERSE)
+    throw Fail{RTD_E_INVALID_ARG, "distance must be RTD_DIST_CHOLESKY or RTD_DIST_INVERSE"};
+  if (o.distance == RTD_DIST_INVERSE && !dist_mma_supported(p))
+    throw Fail{RTD_E_INVALID_ARG, "distance = RTD_DIST_INVERSE needs 8 <= p <= 40"};
+  if (o.consistency != RTD_CONS_ALPHA && o.consistency != RTD_CONS_MEDIAN)
+    throw Fail{RTD_E_INVALID_ARG, "consistency must be RTD_CONS_ALPHA or RTD_CONS_MEDIAN"};
+  if (o.refresh_every < 0) throw Fail{RTD_E_INVALID_ARG, "refresh_every must be >= 0"};
   return d;
 }
 
@@ -738,7 +756,7 @@ BlockResult phase_csteps_choose(cudaStream_t st, FitBufs& f, const Dims& d, cons
   const long long m = d.m, blk_stride = (long long)p * m;
   const int ninst = 2 * q;
   run_csteps(st, f.cb, f.Z, blk_stride, 2, ninst, d.hb, o.kappa_max, o.max_csteps, o.refresh_every, r.status,
-             r.steps);
+             r.steps, o.distance);
   r.logdet.resize(ninst);
   d2h(st, r.logdet.data(), f.cb.logdet, ninst * sizeof(double));
   const double calpha = consistency_factor((double)d.hb / (double)m, p);
@@ -762,8 +780,34 @@ BlockResult phase_csteps_choose(cudaStream_t st, FitBufs& f, const Dims& d, cons
     }
   }
   h2d(st, f.chosen_dev, r.chosen_inst.data(), q * sizeof(int));
+  if (o.consistency == RTD_CONS_MEDIAN && !r.valid_ids.empty()) {
+    // median rule (F1): d^2 of the block's rows under the chosen start's final (mu, Sigma_H),
+    // gathered per block into the (no longer needed) norm buffer, exact medians by bucketed order
+    // statistics, Sigma_raw = median / chi2_{p,0.5} * Sigma_H
+    const int cstride = p + p * (p + 1) / 2;
+    std::vector<int> ch;
+    for (int b : r.valid_ids) ch.push_back(r.chosen_inst[b]);
+    h2d(st, f.cb.inst_dev, ch.data(), ch.size() * sizeof(int));
+    launch_prepare(f.cb.inst_dev, (int)ch.size(), f.cb.mu, f.cb.sigma, p, 1e300, f.cb.cstage, cstride, nullptr,
+                   nullptr, nullptr, nullptr, 0, 0, st);
+    dist_groups(st, f.cb, f.Z, blk_stride, 2, (int)ch.size(), cstride);
+    for (int b : r.valid_ids)
+      RTD_CU(cudaMemcpyAsync(f.ib.r + (size_t)b * m, f.cb.d2 + (size_t)r.chosen_inst[b] * m, m * sizeof(double),
+                             cudaMemcpyDeviceToDevice, st));
+    std::vector<int> fb;
+    launch_quantiles(f.ib.r, m, q, f.ib.qscratch, f.ib.qv, st, fb);
+    for (int l : fb) {
+      size_t bytes = f.ib.sort_bytes;
+      count_sort();
+      RTD_CU(cub::DeviceRadixSort::SortKeys(f.ib.sort_tmp, bytes, f.ib.r + (size_t)l * m, f.ib.rs + (size_t)l * m,
+                                            (int)m, 0, 64, st));
+      launch_q_from_sorted(f.ib.rs + (size_t)l * m, m, l, f.ib.qv, st);
+    }
+    launch_scale_median(f.cb.sigma, f.chosen_dev, f.ib.qv, q, m, p, chi2_quantile(0.5, p), f.sigraw_blk, st);
+  }
   for (int b : r.valid_ids) {
-    launch_scale_copy(f.cb.sigma + (size_t)r.chosen_inst[b] * M2, f.sigraw_blk + (size_t)b * M2, p, calpha, st);
+    if (o.consistency != RTD_CONS_MEDIAN)
+      launch_scale_copy(f.cb.sigma + (size_t)r.chosen_inst[b] * M2, f.sigraw_blk + (size_t)b * M2, p, calpha, st);
     RTD_CU(cudaMemcpyAsync(f.mu_blk + (size_t)b * RTD_MAXP, f.cb.mu + (size_t)r.chosen_inst[b] * RTD_MAXP,
                            RTD_MAXP * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
@@ -1068,6 +1112,8 @@ void rtdetmcd_opts_default(rtdetmcd_opts* o) {
   o->seed = 0;
   o->partition = RTD_PART_PERMUTE;
   o->log_transform = 0;
+  o->distance = RTD_DIST_CHOLESKY;
+  o->consistency = RTD_CONS_ALPHA;
 }
 
 rtdetmcd_status rtdetmcd_create(rtdetmcd_ctx** ctx, int device, void* cuda_stream) {

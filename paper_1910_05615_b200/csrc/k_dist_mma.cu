@@ -111,6 +111,89 @@ __global__ void __launch_bounds__(256, MINB) k_dist_mma(const double* __restrict
   }
 }
 
+// Variant I of the paper's Table 1 ("D" switched off): the distance by the
+// explicit inverse, d_i^2 = u_i^T Sigma^-1 u_i with u_i = z_i - mu, as y = Sigma^-1 u on DMMA (the full
+// p x p operator: no block is skipped) followed by the dot product u . y (u re-read, L1-resident).
+// The operator of slot s is [mu (P) | Sigma^-1 row-major (P*P)] at cstage + s * cstride.
+template <int P, int MB>
+__global__ void __launch_bounds__(256, 2) k_dist_inv(const double* __restrict__ Zall, long long m, long long blk_stride,
+                                                     const int* __restrict__ inst, int nstart,
+                                                     const double* __restrict__ cstage, int cstride,
+                                                     double* __restrict__ d2_all) {
+  constexpr int KB = (P + 3) / 4;
+  constexpr int NB = (P + 7) / 8;
+  __shared__ double bsm[KB * NB * 32];
+  __shared__ double musm[NB * 8];
+  const int slot = blockIdx.y;
+  const int id = inst[slot];
+  const double* __restrict__ Z = Zall + (long long)(id / nstart) * blk_stride;
+  double* __restrict__ d2 = d2_all + (long long)id * m;
+  const double* __restrict__ cs = cstage + (long long)slot * cstride;
+  for (int e = threadIdx.x; e < KB * NB * 32; e += blockDim.x) {
+    const int ln = e & 31, blk = e >> 5, kb = blk / NB, nb = blk - kb * NB;
+    const int k = 4 * kb + (ln & 3), j = 8 * nb + (ln >> 2);
+    bsm[e] = (j < P && k < P) ? cs[P + j * P + k] : 0.0;  // B[k][j] = Sigma^-1[j][k] (symmetric)
+  }
+  for (int e = threadIdx.x; e < NB * 8; e += blockDim.x) musm[e] = e < P ? cs[e] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const long long rows_per_tile = 8 * MB;
+  const long long ntiles = (m + rows_per_tile - 1) / rows_per_tile;
+  const long long warp0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long tile = warp0; tile < ntiles; tile += nwarps) {
+    const long long r0 = tile * rows_per_tile;
+    double acc[MB][NB][2];
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < KB; kb++) {
+      const int k = 4 * kb + t;
+      double a[MB];
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++) {
+        const long long row = r0 + mb * 8 + g;
+        a[mb] = (k < P && row < m) ? __dsub_rn(__ldg(Z + (long long)k * m + row), musm[k]) : 0.0;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        const double bv = bsm[(kb * NB + nb) * 32 + lane];
+#pragma unroll
+        for (int mb = 0; mb < MB; mb++) dmma_8x8x4(acc[mb][nb][0], acc[mb][nb][1], a[mb], bv);
+      }
+    }
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++) {
+      const long long row = r0 + mb * 8 + g;
+      double s = 0.0;
+      if (row < m) {
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) {
+          const int j = 8 * nb + 2 * t;
+          if (j < P) s = fma(__dsub_rn(__ldg(Z + (long long)j * m + row), musm[j]), acc[mb][nb][0], s);
+          if (j + 1 < P) s = fma(__dsub_rn(__ldg(Z + (long long)(j + 1) * m + row), musm[j + 1]), acc[mb][nb][1], s);
+        }
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (t == 0 && row < m) d2[row] = s;
+    }
+  }
+}
+
+template <int P>
+static void dist_inv_launch(const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
+                            int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st) {
+  constexpr int MB = P <= 24 ? 4 : 2;
+  const long long tiles = (m + 8 * MB - 1) / (8 * MB);
+  const long long need = (tiles + 7) / 8;
+  const long long cap = std::max<long long>(1, 148LL * 2 * 2 / std::max(1, ninst));
+  k_dist_inv<P, MB><<<dim3((unsigned)std::min(need, cap), ninst), 256, 0, st>>>(Zall, m, blk_stride, inst, nstart,
+                                                                                 cstage, cstride, d2_all);
+}
+
 template <int P>
 static void dist_mma_launch(const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
                             int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st) {
@@ -140,6 +223,12 @@ static void dist_mma_launch(const double* Zall, long long m, long long blk_strid
   }
 
 bool dist_mma_supported(int p) { return p >= 8 && p <= RTD_MAXP; }
+
+void launch_dist_inv(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
+                     int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st) {
+  RTD_DISPATCH_P8(p, dist_inv_launch, Zall, m, blk_stride, inst, nstart, ninst, cstage, cstride, d2_all, st);
+  RTD_LAUNCHED();
+}
 
 void launch_dist_mma(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
                      int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st) {

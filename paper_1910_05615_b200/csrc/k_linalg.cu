@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(LT) k_prepare(const int* __restrict__ inst, co
                                                 const double* __restrict__ sigma_all, int p, double kappa_max,
                                                 double* __restrict__ cstage, int cstride, double* __restrict__ logdet_out,
                                                 double* __restrict__ cond_out, int* __restrict__ status_out,
-                                                double* __restrict__ traj, int traj_stride, int step) {
+                                                double* __restrict__ traj, int traj_stride, int step,
+                                                int full_inverse) {
   __shared__ double A[RTD_MAXP * LD], L[RTD_MAXP * LD], Li[RTD_MAXP * LD];
   __shared__ double red[RTD_MAXP];
   __shared__ int s_fail;
@@ -133,20 +134,24 @@ __global__ void __launch_bounds__(LT) k_prepare(const int* __restrict__ inst, co
     double* cs = cstage + (long long)slot * cstride;
     const double* mu = mu_all + (long long)id * RTD_MAXP;
     for (int k = t; k < p; k += blockDim.x) cs[k] = mu[k];
-    for (int e = t; e < p * (p + 1) / 2; e += blockDim.x) {
-      int j = 0;
-      while ((j + 1) * (j + 2) / 2 <= e) j++;
-      int k = e - j * (j + 1) / 2;
-      cs[p + e] = Li[j * LD + k];
+    if (full_inverse) {  // [mu | Sigma^-1 row-major]: variant I of Table 1 (distances by the inverse)
+      for (int e = t; e < p * p; e += blockDim.x) cs[p + e] = A[(e / p) * LD + e % p];
+    } else {             // [mu | L^-1 packed lower]: §3.4 (distances by the Cholesky factor)
+      for (int e = t; e < p * (p + 1) / 2; e += blockDim.x) {
+        int j = 0;
+        while ((j + 1) * (j + 2) / 2 <= e) j++;
+        int k = e - j * (j + 1) / 2;
+        cs[p + e] = Li[j * LD + k];
+      }
     }
   }
 }
 
 void launch_prepare(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p, double kappa_max,
                     double* cstage, int cstride, double* logdet_out, double* cond_out, int* status_out, double* traj,
-                    int traj_stride, int step, cudaStream_t st) {
+                    int traj_stride, int step, cudaStream_t st, int full_inverse) {
   k_prepare<<<ninst, LT, 0, st>>>(inst, mu_all, sigma_all, p, kappa_max, cstage, cstride, logdet_out, cond_out,
-                                  status_out, traj, traj_stride, step);
+                                  status_out, traj, traj_stride, step, full_inverse);
   RTD_LAUNCHED();
 }
 

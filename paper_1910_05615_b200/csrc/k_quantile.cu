@@ -223,6 +223,30 @@ __global__ void k_q_cutoffs(const double* __restrict__ qv, long long m, int nb, 
   ok[b] = iqr > 0.0 ? 1 : 0;
 }
 
+// median rule of the raw scatter: out[b] = (median of block b's d^2 / chi2_{p,0.5}) * Sigma_H of the chosen
+// start; the median is the type-7 interpolation at 0.5 (numpy's median) of the targets j, j+1
+__global__ void k_scale_median(const double* __restrict__ sig_all, const int* __restrict__ chosen_inst,
+                               const double* __restrict__ qv, long long m, int p, double chi2half,
+                               double* __restrict__ out_all) {
+  const int b = blockIdx.x;
+  const int ci = chosen_inst[b];
+  if (ci < 0) return;
+  const double hpos = (double)(m - 1) * 0.5;
+  const double g = hpos - floor(hpos);
+  const double y0 = qv[b * QTARGETS + 2], y1 = qv[b * QTARGETS + 3];
+  const double med = ((long long)floor(hpos) + 1 >= m) ? y0 : y0 + g * (y1 - y0);
+  const double f = med / chi2half;
+  const double* S = sig_all + (long long)ci * RTD_MAXP * RTD_MAXP;
+  double* O = out_all + (long long)b * RTD_MAXP * RTD_MAXP;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) O[e] = f * S[e];
+}
+
+void launch_scale_median(const double* sig_all, const int* chosen_inst, const double* qv, int q, long long m, int p,
+                         double chi2half, double* out_all, cudaStream_t st) {
+  k_scale_median<<<q, 256, 0, st>>>(sig_all, chosen_inst, qv, m, p, chi2half, out_all);
+  RTD_LAUNCHED();
+}
+
 size_t quantile_scratch_bytes(int nb) {
   return (size_t)nb * (sizeof(QMap) + QNB * sizeof(unsigned int) + QTARGETS * (sizeof(int) + QCAP * sizeof(double) +
                                                                                sizeof(double))) + 4096;

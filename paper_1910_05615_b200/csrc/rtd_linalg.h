@@ -10,7 +10,7 @@ enum InstStatus { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_NOT_PD = 2, ST_COND = 3, S
 
 void launch_prepare(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p, double kappa_max,
                     double* cstage, int cstride, double* logdet_out, double* cond_out, int* status_out, double* traj,
-                    int traj_stride, int step, cudaStream_t st);
+                    int traj_stride, int step, cudaStream_t st, int full_inverse = 0);
 void launch_sums_to_cov(const int* inst, int ninst, const double* sums_all, int np, const double* shift_all, int p,
                         double n_given, double factor, double* mu_all, double* sigma_all, cudaStream_t st);
 void launch_sums_to_second(const double* sums_all, int nb, int np, int p, double n, double* out_all, cudaStream_t st);

@@ -336,3 +336,35 @@ def test_fit_warm_from_cold_raw_reproduces_cold_and_errors():
     with pytest.raises(api.RTDError) as e:
         api.fit(_cuda(d.X), h=d.h, warm_start=(cold.mu_raw, np.zeros((p, p))))
     assert e.value.name == "RTD_E_BOTH_STARTS_FAILED"
+
+
+# ------------------------------------------------------------------ ablation variants / consistency rule
+@pytest.mark.parametrize("cfg,n,q", [(2, 20_000, 1), (4, 40_003, 8)])
+def test_fit_variants_I_ID_match_oracle(cfg, n, q):
+    """Table 1 variants: I = distances by the explicit inverse + plain recompute,
+    ID = Cholesky distances + plain recompute.  Same estimator, so the same oracle."""
+    d = datagen.make_config(cfg, n=n)
+    h = int(0.75 * n)
+    o = ofit.fit(d.X, h=h, q=q, seed=3)
+    for distance, refresh in ((1, 1), (0, 1)):
+        g = api.fit(_cuda(d.X), h=h, q=q, seed=3, distance=distance, refresh_every=refresh)
+        _compare_fit(g, o, d.X)
+
+
+@pytest.mark.parametrize("cfg,n,q", [(1, None, 1), (2, 20_000, 1), (4, 40_003, 8), (5, None, 1)])
+def test_fit_median_consistency_matches_oracle(cfg, n, q):
+    d = datagen.make_config(cfg, n=n)
+    h = d.h if q == 1 else int(0.75 * d.X.shape[0])
+    o = ofit.fit(d.X, h=h, q=q, seed=3, log_transform=d.log_transform, consistency="median")
+    g = api.fit(_cuda(d.X), h=h, q=q, seed=3, log_transform=d.log_transform, consistency=1)
+    X = np.log(d.X) if d.log_transform else d.X
+    _compare_fit(g, o, X)
+
+
+def test_fit_variant_errors():
+    X = datagen.gaussian(500, 5, seed=4)
+    with pytest.raises(api.RTDError) as e:
+        api.fit(_cuda(X), h=300, distance=1)   # the inverse variant runs on the tensor-pipe kernel: p >= 8
+    assert e.value.name == "RTD_E_INVALID_ARG"
+    with pytest.raises(api.RTDError):
+        api.fit(_cuda(X), h=300, consistency=7)

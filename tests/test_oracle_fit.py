@@ -213,3 +213,23 @@ def test_table2_kl_pins_the_median_consistency_rule():
         paper = gold["IDC"][str(eps)]["shift"][0]
         assert abs(np.mean(med) / paper - 1.0) < 0.2, (eps, np.mean(med), paper)
         assert np.mean(r1) / paper < 0.8, (eps, np.mean(r1), paper)
+
+
+def test_median_consistency_rule_invariant():
+    """consistency="median": the raw scatter is rescaled so that the median squared robust distance of
+    the block's rows under (mu_raw, Sigma_raw) is exactly chi2_{p,0.5} (F1); the h-subsets
+    and the raw centre are those of the default rule."""
+    from oracle.chi2 import chi2_quantile
+    from oracle.numerics import mahalanobis_sq
+    d = datagen.make_config(2, n=20_000)
+    a = F.fit(d.X, h=d.h)
+    m = F.fit(d.X, h=d.h, consistency="median")
+    Z = (d.X - m.loc) / m.scale
+    med = np.median(mahalanobis_sq(Z, m.mu_raw_z, m.Sigma_raw_z))
+    assert med == pytest.approx(chi2_quantile(0.5, d.X.shape[1]), rel=1e-12)
+    assert np.array_equal(a.blocks[0].starts[a.blocks[0].chosen].H, m.blocks[0].starts[m.blocks[0].chosen].H)
+    assert np.allclose(a.mu_raw, m.mu_raw, rtol=0, atol=0)
+    r = m.Sigma_raw / a.Sigma_raw
+    assert np.allclose(r, r[0, 0], rtol=1e-12)  # a scalar multiple
+    with pytest.raises(F.FitError):
+        F.fit(d.X, h=d.h, consistency="other")

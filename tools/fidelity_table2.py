@@ -5,9 +5,9 @@ KL deviation KL(A, B) = tr(A B^-1) - p - log det(A B^-1) of the estimated scatte
 CUDA path through the public API.
 
 Reported per cell: KL of the raw scatter (c(alpha)-scaled, reading R1 -- the text's definition,
-PAPER.md:158-175), KL of the reweighted scatter, and KL of the raw h-subset covariance rescaled so
-that the median squared robust distance of all n rows equals chi2_{p,0.5} (the consistency rule of
-the DetMCD implementations; a diagnostic computed here in numpy from the GPU's raw fit).  The paper's
+PAPER.md:158-175), KL of the reweighted scatter, and KL of the raw scatter of the fit with
+consistency = RTD_CONS_MEDIAN (the h-subset covariance rescaled so that the median squared robust
+distance of the block's rows equals chi2_{p,0.5}, the rule of the DetMCD implementations; F1).  The paper's
 IDC / IDCP_4 values (tests/golden/table2_kl_a09.json) are printed beside them.
 
   python tools/fidelity_table2.py [--reps 50] [--out profiles/r01_fidelity_table2.json]
@@ -55,12 +55,8 @@ def main():
                         g = api.fit(Xd, alpha=0.5, q=q, seed=1000 + rep, outputs=())
                         acc[var]["raw"].append(kl(g.sigma_raw, d.sigma))
                         acc[var]["rew"].append(kl(g.sigma_rew, d.sigma))
-                        c = api.consistency_factor(g.h_block / g.m, p)
-                        S_h = g.sigma_raw / c
-                        D = d.X - g.mu_raw
-                        d2 = np.einsum("ij,ij->i", D, np.linalg.solve(S_h, D.T).T)
-                        S_med = S_h * (np.median(d2) / api.chi2_quantile(0.5, p))
-                        acc[var]["med"].append(kl(S_med, d.sigma))
+                        gm = api.fit(Xd, alpha=0.5, q=q, seed=1000 + rep, outputs=(), consistency=1)
+                        acc[var]["med"].append(kl(gm.sigma_raw, d.sigma))
                 for var in ("IDC", "IDCP4"):
                     paper = gold[var][str(eps)][kind][pi]
                     r = {k: float(np.mean(v)) for k, v in acc[var].items()}
