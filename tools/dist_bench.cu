@@ -95,6 +95,121 @@ __global__ void __launch_bounds__(256, MINB) kvar(const double* __restrict__ Zal
   }
 }
 
+// staged variant: persistent grid (one CTA per SM), flattened (instance, tile) space, tiles of
+// 8 * MB * 8 rows streamed through shared memory by cp.async NST deep, operator (B fragments) in
+// registers, reloaded when the CTA's range crosses into the next instance
+__device__ __forceinline__ void cpa8(double* d, const double* s) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(d)), "l"(s));
+}
+template <int P, int MB, int NST>
+__global__ void __launch_bounds__(256, 1) kstaged(const double* __restrict__ Zall, long long m, long long blk_stride,
+                                                  const double* __restrict__ ops, double* __restrict__ d2_all,
+                                                  int ninst) {
+  constexpr int KB = (P + 3) / 4, NB = (P + 7) / 8, CS = P + P * (P + 1) / 2;
+  constexpr int TR = 8 * 8 * MB;   // rows per tile
+  constexpr int LD = TR + 4;
+  extern __shared__ double sm[];   // [NST][P][LD]
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  const long long tpi = (m + TR - 1) / TR, total = tpi * ninst;
+  const long long t0 = total * blockIdx.x / gridDim.x, t1 = total * (blockIdx.x + 1) / gridDim.x;
+  const int ntile = (int)(t1 - t0);
+  auto issue = [&](int i) {
+    if (i < ntile) {
+      const long long tt = t0 + i;
+      const int id = (int)(tt / tpi);
+      const double* Z = Zall + (long long)(id / 2) * blk_stride;
+      const long long row0 = (tt - (long long)id * tpi) * TR;
+      const int rows = (int)min((long long)TR, m - row0);
+      double* T = sm + (size_t)(i % NST) * P * LD;
+      for (int e = tid; e < P * TR; e += 256) {
+        const int k = e / TR, r = e - k * TR;
+        if (r < rows) cpa8(T + k * LD + r, Z + (long long)k * m + row0 + r);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double bf[KB][NB], mu[KB];
+  int cur = -1;
+  for (int f = 0; f < NST - 1; f++) issue(f);
+  for (int i = 0; i < ntile; i++) {
+    issue(i + NST - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NST - 1));
+    __syncthreads();
+    const long long tt = t0 + i;
+    const int id = (int)(tt / tpi);
+    if (id != cur) {
+      const double* cs = ops + (long long)id * CS;
+#pragma unroll
+      for (int kb = 0; kb < KB; kb++) {
+        const int k = 4 * kb + t;
+        mu[kb] = k < P ? cs[k] : 0.0;
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) {
+          const int j = 8 * nb + g;
+          bf[kb][nb] = (j < P && k <= j) ? cs[P + j * (j + 1) / 2 + k] : 0.0;
+        }
+      }
+      cur = id;
+    }
+    const long long row0 = (tt - (long long)id * tpi) * TR;
+    const double* T = sm + (size_t)(i % NST) * P * LD;
+    double acc[MB][NB][2];
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < KB; kb++) {
+      const int k = 4 * kb + t;
+      double a[MB];
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++) a[mb] = k < P ? T[k * LD + (warp * MB + mb) * 8 + g] - mu[kb] : 0.0;
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        if (8 * nb + 7 < 4 * kb) continue;
+#pragma unroll
+        for (int mb = 0; mb < MB; mb++) dmma(acc[mb][nb][0], acc[mb][nb][1], a[mb], bf[kb][nb]);
+      }
+    }
+    double* d2 = d2_all + (long long)id * m;
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++) {
+      double s = 0.0;
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) s = fma(acc[mb][nb][0], acc[mb][nb][0], fma(acc[mb][nb][1], acc[mb][nb][1], s));
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      const long long row = row0 + (warp * MB + mb) * 8 + g;
+      if (t == 0 && row < m) d2[row] = s;
+    }
+    __syncthreads();
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+template <int P, int MB, int NST>
+float run_staged(const double* Z, long long m, long long bs, const double* ops, double* d2, int nblk, double bytes,
+                 double flops) {
+  constexpr int TR = 8 * 8 * MB, LD = TR + 4;
+  const int smem = NST * P * LD * 8;
+  cudaFuncSetAttribute(kstaged<P, MB, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int w = 0; w < 3; w++) kstaged<P, MB, NST><<<148, 256, smem>>>(Z, m, bs, ops, d2, 2 * nblk);
+  cudaEventRecord(e0);
+  const int R = 10;
+  for (int r = 0; r < R; r++) kstaged<P, MB, NST><<<148, 256, smem>>>(Z, m, bs, ops, d2, 2 * nblk);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= R;
+  printf("%-34s P=%2d MB=%d NST=%d smem=%d: %.3f ms  eff %.0f GB/s  %.1f TF/s  %s\n", "staged persistent", P, MB, NST,
+         smem, ms, bytes / ms / 1e6, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+  return ms;
+}
+
 template <int P, int MB, int NS, int MINB, bool CINIT>
 float run(const char* name, const double* Z, long long m, long long bs, const double* ops, double* d2, int nblk,
           double bytes, double flops) {
@@ -146,6 +261,10 @@ void suite(long long m, int nblk) {
   run<P, 2, 2, 1, true>("c-init, 2 starts MB2 minb1", Z, m, bs, ops, d2, nblk, eff_bytes, flops);
   run<P, 3, 2, 1, true>("c-init, 2 starts MB3 minb1", Z, m, bs, ops, d2, nblk, eff_bytes, flops);
   run<P, 1, 2, 2, true>("c-init, 2 starts MB1 minb2", Z, m, bs, ops, d2, nblk, eff_bytes, flops);
+  run_staged<P, 2, 3>(Z, m, bs, ops, d2, nblk, eff_bytes, flops);
+  run_staged<P, 2, 4>(Z, m, bs, ops, d2, nblk, eff_bytes, flops);
+  run_staged<P, 3, 3>(Z, m, bs, ops, d2, nblk, eff_bytes, flops);
+  run_staged<P, 1, 4>(Z, m, bs, ops, d2, nblk, eff_bytes, flops);
   cudaFree(Z);
   cudaFree(ops);
   cudaFree(d2);
