@@ -273,6 +273,166 @@ __global__ void __launch_bounds__(UTH) k_uni_final(const double* __restrict__ so
   }
 }
 
+// ---------------------------------------------------------------- short columns in one kernel
+// len <= USMALL: one CTA of 1024 threads per column does the whole estimator in shared memory --
+// a bitonic sort (flip form: the virtual +inf padding up to the next power of two is never touched),
+// per-thread chunk totals and their block scan in double-double, the window objective of every start
+// (ties -> lowest s), the raw estimate and the reweighting -- so a short column costs one launch
+// instead of two radix sorts and four passes (the stream of BASELINE config 5, 20,000 rows).
+static constexpr int USMALL = 20480;  // shared-memory capacity bound
+static constexpr int USMALL_USE = 4096;  // measured: faster than the radix-sort path up to here (config 1:
+                                         // 3 calls 1.06 -> 0.21 ms), slower at 20,000 rows (config 5)
+static constexpr int UST = 1024;
+
+__device__ __forceinline__ void u_cmpswap(double* v, int i, int j) {
+  const double a = v[i], b = v[j];
+  if (a > b) {
+    v[i] = b;
+    v[j] = a;
+  }
+}
+
+// P(t) = sum_{i<t} (y_i, y_i^2) from the chunk prefixes cpre (chunk c = [c per, (c+1) per))
+__device__ __forceinline__ dd2 u_prefix(const double* v, const dd2* cpre, int per, int t) {
+  const int c = t / per;
+  dd2 acc = cpre[c];
+  for (int i = c * per; i < t; i++) acc = dd2_add(acc, dd2_of(v[i]));
+  return acc;
+}
+
+__global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ cols, int len, int h, UniConst uc,
+                                                   UniOut* __restrict__ out) {
+  extern __shared__ double usm[];
+  double* v = usm;                                   // [len]
+  dd2* cpre = reinterpret_cast<dd2*>(usm + ((len + 3) & ~3));  // [UST + 1]
+  __shared__ dd2 sm[33];
+  __shared__ WinPartial wsm[UST / 32];
+  __shared__ long long s_lohi[2];
+  const int col = blockIdx.x, t = threadIdx.x;
+  const double* y = cols + (long long)col * len;
+  for (int i = t; i < len; i += UST) v[i] = y[i];
+  int N = 1;
+  while (N < len) N <<= 1;
+  __syncthreads();
+  for (int lk = 1; (1 << lk) <= N; lk++) {
+    const int k = 1 << lk;
+    for (int q = t; q < N / 2; q += UST) {  // flip step: i in the lower half of its k-block
+      const int i = ((q >> (lk - 1)) << lk) | (q & (k / 2 - 1)), j = i ^ (k - 1);
+      if (j < len) u_cmpswap(v, i, j);
+    }
+    __syncthreads();
+    for (int ld = lk - 2; ld >= 0; ld--) {
+      const int d = 1 << ld;
+      for (int q = t; q < N / 2; q += UST) {
+        const int i = ((q >> ld) << (ld + 1)) | (q & (d - 1)), j = i + d;
+        if (j < len) u_cmpswap(v, i, j);
+      }
+      __syncthreads();
+    }
+  }
+  // chunk totals and their exclusive scan
+  const int per = (len + UST - 1) / UST;
+  const int c0 = t * per, c1 = min(len, c0 + per);
+  dd2 loc = dd2_zero();
+  for (int i = c0; i < c1; i++) loc = dd2_add(loc, dd2_of(v[i]));
+  dd2 tot;
+  const dd2 ex = block_exscan_dd2(loc, &tot, sm);
+  cpre[t] = ex;
+  if (t == 0) cpre[UST] = tot;
+  __syncthreads();
+  // window objective h S2 - S1^2 for starts s in [c0, c1) with s < nwin
+  const int nwin = len - h + 1;
+  double bhi = __longlong_as_double(0x7ff0000000000000LL), blo = 0.0;
+  long long bs = 0x7fffffffffffffffLL;
+  const double hd = (double)h;
+  if (c0 < nwin) {
+    dd2 Pl = ex;
+    dd2 Pr = u_prefix(v, cpre, per, c0 + h);
+    const int e1 = min(c1, nwin);
+    for (int s = c0; s < e1; s++) {
+      const dd S1 = dd_sub(Pr.s1, Pl.s1);
+      const dd S2 = dd_sub(Pr.s2, Pl.s2);
+      const dd w = dd_sub(dd_mul_d(S2, hd), dd_mul(S1, S1));
+      if (win_better(w.hi, w.lo, s, bhi, blo, bs)) {
+        bhi = w.hi;
+        blo = w.lo;
+        bs = s;
+      }
+      Pl = dd2_add(Pl, dd2_of(v[s]));
+      if (s + h < len) Pr = dd2_add(Pr, dd2_of(v[s + h]));
+    }
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    const double ohi = __shfl_down_sync(0xffffffffu, bhi, d);
+    const double olo = __shfl_down_sync(0xffffffffu, blo, d);
+    const long long os = __shfl_down_sync(0xffffffffu, bs, d);
+    if (win_better(ohi, olo, os, bhi, blo, bs)) {
+      bhi = ohi;
+      blo = olo;
+      bs = os;
+    }
+  }
+  if ((t & 31) == 0) wsm[t >> 5] = {bhi, blo, bs};
+  __syncthreads();
+  if (t != 0) return;
+  WinPartial best = wsm[0];
+  for (int w = 1; w < UST / 32; w++)
+    if (win_better(wsm[w].vhi, wsm[w].vlo, wsm[w].s, best.vhi, best.vlo, best.s)) best = wsm[w];
+  const int s = (int)best.s;
+  const dd S1 = dd_sub(u_prefix(v, cpre, per, s + h).s1, u_prefix(v, cpre, per, s).s1);
+  const double loc0 = dd_to_d(dd_div_d(S1, hd));
+  const dd wv = {best.vhi, best.vlo};
+  const double var_raw = h > 1 ? dd_to_d(dd_div_d(dd_div_d(wv, hd), (double)(h - 1))) : 0.0;
+  const double var0 = uc.c_raw * var_raw;
+  const double thresh = uc.q1 * var0;
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (v[mid] < loc0) lo = mid + 1; else hi = mid;
+  }
+  const int i0 = lo;
+  lo = 0;
+  hi = i0;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (uni_keep(v[mid], loc0, thresh)) hi = mid; else lo = mid + 1;
+  }
+  const int klo = lo;
+  lo = i0;
+  hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (uni_keep(v[mid], loc0, thresh)) lo = mid + 1; else hi = mid;
+  }
+  const int khi = lo;
+  (void)s_lohi;
+  UniOut o;
+  o.raw_loc = loc0;
+  o.raw_var = var_raw;
+  o.var0 = var0;
+  o.start = s;
+  o.kept = khi - klo;
+  o.pad = 0;
+  o.status = 0;
+  o.loc = 0.0;
+  o.scale = 0.0;
+  const long long k = khi - klo;
+  if (!(var0 > 0.0) || k < 2) {
+    o.status = 1;
+  } else {
+    const dd2 K = dd2_sub(u_prefix(v, cpre, per, khi), u_prefix(v, cpre, per, klo));
+    const double Sd = dd_to_d(K.s1);
+    const double lc = Sd / (double)k;
+    dd q = dd_sub(K.s2, dd_mul_d(K.s1, 2.0 * lc));
+    q = dd_add(q, dd_mul_d(two_prod(lc, lc), (double)k));
+    const double var = uc.c_rew * (dd_to_d(q) / (double)(k - 1));
+    o.loc = lc;
+    o.scale = sqrt(var);
+    if (!(var > 0.0)) o.status = 1;
+  }
+  out[col] = o;
+}
+
 struct UniScratch {
   double* sorted;
   double* tmpk;
@@ -314,6 +474,20 @@ static size_t cub_sort_bytes(long long len, int ncols) {
 
 void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, int ncols, UniConst uc,
                   UniOut* out_dev) {
+  static const bool no_small = getenv("RTD_UNI_NOSMALL") != nullptr;
+  if (len <= USMALL_USE && len >= 2 && !no_small) {
+    if (A.base == nullptr) return;  // no scratch
+    const int smem = (int)((((len + 3) & ~3LL) * sizeof(double)) + (UST + 1) * sizeof(dd2));
+    static const bool attr = [] {
+      cudaFuncSetAttribute(k_uni_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(USMALL * sizeof(double) + (UST + 1) * sizeof(dd2)));
+      return true;
+    }();
+    (void)attr;
+    k_uni_small<<<ncols, UST, smem, st>>>(cols, (int)len, (int)(len / 2 + 1), uc, out_dev);
+    RTD_LAUNCHED();
+    return;
+  }
   if (ncols > 256) throw std::string("unimcd_batch: at most 256 columns per call");
   const long long h = len / 2 + 1;
   const int nchunks = (int)((len + UCH - 1) / UCH);
