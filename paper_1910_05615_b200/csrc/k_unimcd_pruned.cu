@@ -403,9 +403,9 @@ __device__ __forceinline__ VBound window_bounds(long long s, long long h, int b,
     const double Sblo = sb[b], Sbhi = sb[NBK + b], Selo = sb[be], Sehi = sb[NBK + be];
     const double r1 = (double)(C[b + 1] - s), r2 = (double)(s + h - C[be]);
     // top r1 elements of bucket b: mean >= bucket mean; the other n1 - r1 are >= L1
-    const double t1lo = fmax(r1 * L1, r1 * Sblo / n1), t1hi = fmin(r1 * U1, Sbhi - (n1 - r1) * L1);
+    const double t1lo = fmax(r1 * L1, r1 * Sblo * __drcp_rn(n1)), t1hi = fmin(r1 * U1, Sbhi - (n1 - r1) * L1);
     // bottom r2 elements of bucket be: mean <= bucket mean; the other n2 - r2 are <= U2
-    const double t2lo = fmax(r2 * L2, Selo - (n2 - r2) * U2), t2hi = fmin(r2 * U2, r2 * Sehi / n2);
+    const double t2lo = fmax(r2 * L2, Selo - (n2 - r2) * U2), t2hi = fmin(r2 * U2, r2 * Sehi * __drcp_rn(n2));
     const double F1lo = A1[be] - A1[b + 1], F1hi = A1[NBK + 1 + be] - A1[NBK + 1 + b + 1];
     lo1 = F1lo + fmin(t1lo, t1hi) + fmin(t2lo, t2hi) - m.E1;
     hi1 = F1hi + fmax(t1lo, t1hi) + fmax(t2lo, t2hi) + m.E1;
@@ -437,8 +437,8 @@ __device__ __forceinline__ PartBounds part_bounds(long long s, long long h, int 
   const double n1 = (double)cn[b], n2 = (double)cn[be];
   const double Sblo = sb[b], Sbhi = sb[NBK + b], Selo = sb[be], Sehi = sb[NBK + be];
   const double r1 = (double)(C[b + 1] - s), r2 = (double)(s + h - C[be]);
-  const double a = fmax(r1 * L1, r1 * Sblo / n1), bb = fmin(r1 * U1, Sbhi - (n1 - r1) * L1);
-  const double d = fmax(r2 * L2, Selo - (n2 - r2) * U2), e = fmin(r2 * U2, r2 * Sehi / n2);
+  const double a = fmax(r1 * L1, r1 * Sblo * __drcp_rn(n1)), bb = fmin(r1 * U1, Sbhi - (n1 - r1) * L1);
+  const double d = fmax(r2 * L2, Selo - (n2 - r2) * U2), e = fmin(r2 * U2, r2 * Sehi * __drcp_rn(n2));
   return {fmin(a, bb), fmax(a, bb), fmin(d, e), fmax(d, e)};
 }
 
@@ -513,22 +513,22 @@ __global__ void __launch_bounds__(PT) k_pr_bound(long long len, long long h, con
       }
     }
   } else if (mode == 1) {
+    // the thread's contiguous range of starts, cut only where the start bucket or the end bucket
+    // changes: one lower bound per maximal (b, be) segment (about 2 NBK segments per column)
     if (ch0 < ch1) {
-      int b = rank_bucket(C, ch0 * CHUNK), be = rank_bucket(C, ch0 * CHUNK + h - 1);
-      for (long long ch = ch0; ch < ch1; ch++) {
-        const long long s0 = ch * CHUNK, s1e = min(nwin, s0 + CHUNK);
-        long long sa = s0;
-        while (sa < s1e) {
-          while (C[b + 1] <= sa) b++;
-          while (C[be + 1] <= sa + h - 1) be++;
-          const long long sb = min(min(s1e, C[b + 1]), C[be + 1] - h + 1) - 1;  // same (b, be) on [sa, sb]
-          const double lo = (b == be) ? -INFINITY : chunk_lower(sa, sb, h, b, be, c, C, A1, Q2lo, cn, sbk, m);
-          if (lo <= bub) {
-            cmin = min(cmin, sa);
-            cmax = max(cmax, sb);
-          }
-          sa = sb + 1;
+      const long long s1e = min(nwin, ch1 * CHUNK);
+      long long sa = ch0 * CHUNK;
+      int b = rank_bucket(C, sa), be = rank_bucket(C, sa + h - 1);
+      while (sa < s1e) {
+        while (C[b + 1] <= sa) b++;
+        while (C[be + 1] <= sa + h - 1) be++;
+        const long long sb = min(min(s1e, C[b + 1]), C[be + 1] - h + 1) - 1;  // same (b, be) on [sa, sb]
+        const double lo = (b == be) ? -INFINITY : chunk_lower(sa, sb, h, b, be, c, C, A1, Q2lo, cn, sbk, m);
+        if (lo <= bub) {
+          cmin = min(cmin, sa);
+          cmax = max(cmax, sb);
         }
+        sa = sb + 1;
       }
     }
   } else {
