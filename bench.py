@@ -423,7 +423,10 @@ def main():
             try:
                 tj = json.load(open(tf))
                 if tj.get("config") == CONFIG_NAMES[cfg]:
-                    roof["traffic"] = tj.get("dram_bytes_per_launch")
+                    # ncu DRAM bytes per algorithmic byte of the same kernel (one --set full capture),
+                    # scaled to this run's average launch
+                    roof["traffic"] = tj["dram_per_algorithmic_byte"] * roof["bytes_per_launch"]
+                    roof["traffic_source"] = tj.get("source")
             except Exception:
                 pass
     breakdown = _breakdown(prof, args.steps)

@@ -545,7 +545,8 @@ void carve_init(Arena& A, InitBufs& b, int q, long long m, int p) {
   b.rs = A.take<double>((size_t)q * m);
   b.AB = A.take<double>(2 * (size_t)q);
   b.abok = A.take<int>(q);
-  b.ctas = (int)std::max<long long>(1, std::min<long long>(128, (m + 4095) / 4096));
+  // CTAs per block: 4 full waves of 2 CTAs on each of the 148 SMs over the q blocks, >= 4096 rows each
+  b.ctas = (int)std::max<long long>(1, std::min<long long>((m + 4095) / 4096, (296LL * 4 + q - 1) / q));
   b.sums = A.take<double>((size_t)q * NPMAX);
   b.partial = A.take<double>((size_t)q * b.ctas * NPMAX);
   b.mudummy = A.take<double>((size_t)q * RTD_MAXP);
