@@ -333,6 +333,24 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
   h2d(st, b.status, status_h.data(), ninst * sizeof(int));
   steps_h.assign(ninst, 0);
   std::vector<int> act, changed(ninst);
+  static const bool no_small = getenv("RTD_NO_SMALL_CSTEPS") != nullptr;
+  if (dist_mode == RTD_DIST_CHOLESKY && csteps_small_supported(m, p) && !no_small) {
+    // short blocks: the whole loop of every active instance in one launch (k_csteps_small), dense
+    // moments every step (exact for the final subset), no host round trip per step
+    for (int i = 0; i < ninst; i++)
+      if (status_h[i] == ST_ACTIVE) act.push_back(i);
+    if (act.empty()) return;
+    h2d(st, b.inst_dev, act.data(), act.size() * sizeof(int));
+    {
+      ProfScope ps("csteps_small", (double)act.size() * m * (8.0 * p + 8.0));
+      launch_csteps_small(Z, m, p, blk_stride, nstart, b.inst_dev, (int)act.size(), h, kappa_max, max_steps, b.mu,
+                          b.sigma, b.status, b.changed, b.logdet, b.traj, b.traj_stride, b.memA, st);
+    }
+    std::vector<int> steps_all(ninst);
+    fetch(st, {{status_h.data(), b.status, ninst * sizeof(int)}, {steps_all.data(), b.changed, ninst * sizeof(int)}});
+    for (int i : act) steps_h[i] = steps_all[i];
+    return;
+  }
   MomArgs ma = mom_args(b, Z, blk_stride, nstart);
   uint8_t* memA = b.memA;  // latest membership
   uint8_t* memB = b.memB;

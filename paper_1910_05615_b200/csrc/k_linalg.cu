@@ -9,6 +9,8 @@
 //   k_refine    Sigma_k = V D~ V^T, Sigma_k^{+-1/2}.
 //   k_sums_to_cov  mean / covariance from shifted sums (eqs. cstep4a/b).
 //   k_aggregate entrywise median, KL ranking, ceil(q/2) kept, pooling.
+#include <algorithm>
+
 #include "rtd_internal.h"
 #include "rtd_linalg.h"
 #include <cstdio>
@@ -145,6 +147,359 @@ __global__ void __launch_bounds__(LT) k_prepare(const int* __restrict__ inst, co
       }
     }
   }
+}
+
+// ------------------------------------------------------------------ the whole C-step loop of a short block
+// For short blocks (p <= 16, see csteps_small_supported) the per-step work is tiny and the loop of run_csteps (about ten
+// launches and a host synchronisation per step) is latency-bound, so one CTA of 1024 threads runs the
+// loop of one instance to the end: Cholesky, 1-norm condition and log det
+// (the block_* helpers above), the distances d_i^2 = ||L^-1 (z_i - mu)||^2 into shared memory, the
+// exact selection of the h smallest (d^2, row) composite keys by a 12-bit radix select (warp-aggregated
+// shared atomics), the membership as bits and its change count (stop when H_new == H_old), and the
+// mean / covariance of H_new by DMMA about the current centre (dense every step: the moments are the
+// exact ones of the final subset, reading R12).  Same statuses, step counts and trajectory as run_csteps.
+static constexpr int CS_SMALL_M = 20480;
+static constexpr int CS_T = 512;
+static constexpr int CS_W = CS_T / 32;
+
+__device__ __forceinline__ void cs_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NB>
+__global__ void __launch_bounds__(CS_T, 1) k_csteps_small(const double* __restrict__ Zall, int m, int p,
+                                                          long long blk_stride, int nstart, const int* __restrict__ inst,
+                                                          int h, double kappa_max, int max_steps,
+                                                          double* __restrict__ mu_all, double* __restrict__ sigma_all,
+                                                          int* __restrict__ status_all, int* __restrict__ steps_all,
+                                                          double* __restrict__ logdet_all, double* __restrict__ traj,
+                                                          int traj_stride, uint8_t* __restrict__ mem_all) {
+  constexpr int NBLK = NB * (NB + 1) / 2;
+  constexpr int NRED = NBLK * 64 + 8 * NB + 1;  // per-warp partial: 8x8 blocks, S1, count
+  extern __shared__ double dsm[];               // A, L, Li (block_* layout) then d^2 [m] / moment partials
+  double* A = dsm;
+  double* L = dsm + RTD_MAXP * LD;
+  double* Li = dsm + 2 * RTD_MAXP * LD;
+  double* dyn = dsm + 3 * RTD_MAXP * LD;
+  __shared__ double red[RTD_MAXP];
+  __shared__ double mu_s[16], sg_s[16 * 16];
+  __shared__ unsigned int hist[4096];
+  __shared__ unsigned int cur[CS_SMALL_M / 32], prv[CS_SMALL_M / 32];
+  __shared__ long long wsum[CS_W];
+  __shared__ int s_fail, s_stat, s_found, s_done, s_changed;
+  __shared__ long long s_before, s_cnt;
+  __shared__ unsigned long long s_pre_hi, s_pre_lo;
+  __shared__ double s_logdet;
+  const int id = inst[blockIdx.x];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, g = lane >> 2, tq = lane & 3;
+  const double* __restrict__ Z = Zall + (long long)(id / nstart) * blk_stride;
+  const int nwords = (m + 31) / 32;
+  for (int e = t; e < p; e += CS_T) mu_s[e] = mu_all[(long long)id * RTD_MAXP + e];
+  for (int e = t; e < p * p; e += CS_T) sg_s[e] = sigma_all[(long long)id * RTD_MAXP * RTD_MAXP + e];
+  for (int w = t; w < nwords; w += CS_T) prv[w] = 0u;
+  if (t == 0) s_stat = ST_ACTIVE;
+  __syncthreads();
+  int step = 1;
+  for (; step <= max_steps; step++) {
+    // ---- factor: Cholesky, condition monitor, log det (k_prepare)
+    for (int e = t; e < p * p; e += CS_T) A[(e / p) * LD + e % p] = sg_s[e];
+    __syncthreads();
+    if (!block_cholesky(A, L, p, &s_fail)) {
+      if (t == 0) s_stat = ST_NOT_PD;
+      break;
+    }
+    block_tri_inverse(L, Li, p);
+    const double n1 = block_max_colsum_abs(A, p, red);
+    block_inv_from_li(Li, A, p);
+    const double kappa = n1 * block_max_colsum_abs(A, p, red);
+    if (t == 0) {
+      double ld = 0.0;
+      for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
+      ld *= 2.0;
+      s_logdet = ld;
+      if (traj) traj[(long long)id * traj_stride + step] = ld;
+      if (!(kappa < kappa_max)) s_stat = ST_COND;
+    }
+    __syncthreads();
+    if (s_stat != ST_ACTIVE) break;
+    // ---- distances (CS_R rows per thread in flight: the rows of Z come from L2 / HBM)
+    constexpr int CS_R = 4;
+    for (int i0 = t; i0 < m; i0 += CS_T * CS_R) {
+      double u[CS_R][8 * NB];
+#pragma unroll
+      for (int r = 0; r < CS_R; r++) {
+        const int i = i0 + r * CS_T;
+#pragma unroll
+        for (int k = 0; k < 8 * NB; k++) u[r][k] = (k < p && i < m) ? __ldg(Z + (long long)k * m + i) : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < CS_R; r++) {
+        const int i = i0 + r * CS_T;
+        if (i >= m) continue;
+        double d = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8 * NB; j++) {
+          if (j < p) {
+            double y = 0.0;
+#pragma unroll
+            for (int k = 0; k <= j; k++) y = fma(Li[j * LD + k], __dsub_rn(u[r][k], mu_s[k]), y);
+            d = fma(y, y, d);
+          }
+        }
+        dyn[i] = d;
+      }
+    }
+    __syncthreads();
+    // ---- exact selection of the h smallest composite keys (bits(d^2) << 32 | row)
+    if (t == 0) {
+      s_pre_hi = 0ull;
+      s_pre_lo = 0ull;
+      s_done = 0;
+      s_before = h;  // rank still needed
+    }
+    int plen = 0;
+    __syncthreads();
+    while (true) {
+      for (int b = t; b < 4096; b += CS_T) hist[b] = 0u;
+      __syncthreads();
+      const unsigned __int128 pre = ((unsigned __int128)s_pre_hi << 64) | s_pre_lo;
+      for (int i0 = 0; i0 < m; i0 += CS_T) {
+        const int i = i0 + t;
+        bool take = false;
+        unsigned dig = 0;
+        if (i < m) {
+          const unsigned __int128 C = ((unsigned __int128)(unsigned long long)__double_as_longlong(dyn[i]) << 32) | (unsigned)i;
+          take = plen == 0 || (C >> (96 - plen)) == pre;
+          dig = (unsigned)(C >> (96 - plen - 12)) & 4095u;
+        }
+        const unsigned act = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const unsigned same = __match_any_sync(act, dig);
+          if ((__ffs(same) - 1) == lane) atomicAdd(&hist[dig], (unsigned)__popc(same));
+        }
+      }
+      __syncthreads();
+      // scan of 4096 bins: BPT per thread
+      constexpr int BPT = 4096 / CS_T;
+      long long c[BPT], loc = 0;
+#pragma unroll
+      for (int e = 0; e < BPT; e++) {
+        c[e] = hist[t * BPT + e];
+        loc += c[e];
+      }
+      long long inc = loc;
+      for (int d = 1; d < 32; d <<= 1) {
+        const long long v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      __syncthreads();
+      if (t == 0) {
+        long long acc = 0;
+        for (int w = 0; w < CS_W; w++) {
+          const long long v = wsum[w];
+          wsum[w] = acc;
+          acc += v;
+        }
+      }
+      __syncthreads();
+      const long long rank = s_before;
+      long long before = wsum[warp] + inc - loc;
+#pragma unroll
+      for (int e = 0; e < BPT; e++) {
+        if (c[e] > 0 && before < rank && rank <= before + c[e]) {
+          s_found = t * BPT + e;
+          s_cnt = c[e];
+          s_pre_lo = (unsigned long long)before;  // temporarily: keys before the bin
+        }
+        before += c[e];
+      }
+      __syncthreads();
+      if (t == 0) {
+        const long long bef = (long long)s_pre_lo;
+        const unsigned __int128 np = (pre << 12) | (unsigned __int128)s_found;
+        s_pre_hi = (unsigned long long)(np >> 64);
+        s_pre_lo = (unsigned long long)np;
+        s_before = rank - bef;
+        s_done = (s_cnt == s_before || plen + 12 >= 96) ? 1 : 0;
+      }
+      plen += 12;
+      __syncthreads();
+      if (s_done) break;
+    }
+    // ---- membership bits and the changed-row count
+    {
+      const unsigned __int128 pre = ((unsigned __int128)s_pre_hi << 64) | s_pre_lo;
+      if (t == 0) s_changed = 0;
+      __syncthreads();
+      int chg = 0;
+      for (int i0 = 0; i0 < m; i0 += CS_T) {
+        const int i = i0 + t;
+        bool in = false;
+        if (i < m) {
+          const unsigned __int128 C = ((unsigned __int128)(unsigned long long)__double_as_longlong(dyn[i]) << 32) | (unsigned)i;
+          in = (C >> (96 - plen)) <= pre;
+        }
+        const unsigned wb = __ballot_sync(0xffffffffu, in);
+        if (lane == 0 && i0 / 32 + warp < nwords) {
+          const int w = i0 / 32 + warp;
+          cur[w] = wb;
+          chg += __popc(wb ^ prv[w]);
+        }
+      }
+      if (lane == 0 && chg) atomicAdd(&s_changed, chg);
+      __syncthreads();
+    }
+    if (step > 1 && s_changed == 0) {
+      if (t == 0) s_stat = ST_CONVERGED;
+      __syncthreads();
+      break;
+    }
+    // ---- moments of H_new about the current centre (DMMA per warp on 4-row groups)
+    {
+      double acc[NBLK][2], s1[NB], cntw = 0.0;
+#pragma unroll
+      for (int k = 0; k < NBLK; k++) acc[k][0] = acc[k][1] = 0.0;
+#pragma unroll
+      for (int b = 0; b < NB; b++) s1[b] = 0.0;
+      constexpr int CS_G = 8;  // 4-row groups per warp iteration, loads issued first
+      for (int rb = warp * 4 * CS_G; rb < m; rb += CS_W * 4 * CS_G) {
+        double w[CS_G], u[CS_G][NB];
+#pragma unroll
+        for (int q = 0; q < CS_G; q++) {
+          const int row = rb + 4 * q + tq;
+          w[q] = (row < m && ((cur[row >> 5] >> (row & 31)) & 1u)) ? 1.0 : 0.0;
+#pragma unroll
+          for (int b = 0; b < NB; b++) {
+            const int col = 8 * b + g;
+            u[q][b] = (w[q] != 0.0 && col < p) ? __ldg(Z + (long long)col * m + row) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < CS_G; q++) {
+          if (!__any_sync(0xffffffffu, w[q] != 0.0)) continue;
+          double uu[NB], wu[NB];
+#pragma unroll
+          for (int b = 0; b < NB; b++) {
+            const int col = 8 * b + g;
+            uu[b] = (w[q] != 0.0 && col < p) ? __dsub_rn(u[q][b], mu_s[col]) : 0.0;
+            wu[b] = w[q] * uu[b];
+            s1[b] += wu[b];
+          }
+          if (g == 0) cntw += w[q];
+          int k = 0;
+#pragma unroll
+          for (int jb = 0; jb < NB; jb++)
+#pragma unroll
+            for (int kb = 0; kb <= jb; kb++) {
+              cs_dmma(acc[k][0], acc[k][1], wu[jb], uu[kb]);
+              k++;
+            }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 1);
+        s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 2);
+      }
+      double* rw = dyn + (size_t)warp * NRED;
+#pragma unroll
+      for (int k = 0; k < NBLK; k++) {
+        rw[k * 64 + g * 8 + 2 * tq] = acc[k][0];
+        rw[k * 64 + g * 8 + 2 * tq + 1] = acc[k][1];
+      }
+      if (tq == 0) {
+#pragma unroll
+        for (int b = 0; b < NB; b++) rw[NBLK * 64 + 8 * b + g] = s1[b];
+      }
+      (void)cntw;
+      __syncthreads();
+      // fixed-order sum over the warps -> (mu, Sigma) of H_new
+      const double hd = (double)h;
+      if (t < p * p) {
+        const int j = t / p, k = t - j * p;
+        const int a = j > k ? j : k, bq = j > k ? k : j;  // lower-triangle entry (a >= bq)
+        const int ja = a >> 3, kbq = bq >> 3;
+        const int blk = ja * (ja + 1) / 2 + kbq;
+        const int e = blk * 64 + (a & 7) * 8 + (bq & 7);
+        double s2 = 0.0, sa = 0.0, sb = 0.0;
+        for (int w = 0; w < CS_W; w++) {
+          const double* rr = dyn + (size_t)w * NRED;
+          s2 += rr[e];
+          sa += rr[NBLK * 64 + a];
+          sb += rr[NBLK * 64 + bq];
+        }
+        red[0] = 0.0;  // (keeps the shared array referenced; the values below are per thread)
+        sg_s[t] = (s2 - sa * sb / hd) / (hd - 1.0);
+        if (j == k) A[j] = sa;  // S1_j, parked until every thread read mu_s
+      }
+      __syncthreads();
+      if (t < p) mu_s[t] = mu_s[t] + A[t] / hd;
+      for (int w = t; w < nwords; w += CS_T) prv[w] = cur[w];
+      __syncthreads();
+    }
+  }
+  if (step > max_steps) {
+    step = max_steps;
+    if (t == 0) s_stat = ST_MAXSTEPS;
+  }
+  __syncthreads();
+  const int stat = s_stat;
+  if (stat == ST_MAXSTEPS) {  // log det of the final (mu, Sigma)
+    for (int e = t; e < p * p; e += CS_T) A[(e / p) * LD + e % p] = sg_s[e];
+    __syncthreads();
+    if (block_cholesky(A, L, p, &s_fail) && t == 0) {
+      double ld = 0.0;
+      for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
+      s_logdet = 2.0 * ld;
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < p; e += CS_T) mu_all[(long long)id * RTD_MAXP + e] = mu_s[e];
+  for (int e = t; e < p * p; e += CS_T) sigma_all[(long long)id * RTD_MAXP * RTD_MAXP + e] = sg_s[e];
+  for (int i = t; i < m; i += CS_T) mem_all[(long long)id * m + i] = (uint8_t)((cur[i >> 5] >> (i & 31)) & 1u);
+  if (t == 0) {
+    status_all[id] = stat;
+    steps_all[id] = step;
+    logdet_all[id] = s_logdet;
+  }
+}
+
+// used up to 4096 rows: measured faster than the multi-launch loop there (config 1, 1000 x 5: fit + flag
+// 1.69 -> 0.98 ms) but slower at 20,000 rows (config 5: one SM per instance is too little for the
+// per-step passes), where run_csteps' grid-wide kernels win despite their launches
+bool csteps_small_supported(long long m, int p) { return m <= 4096 && m >= 2 && p >= 1 && p <= 16; }
+
+void launch_csteps_small(const double* Zall, long long m, int p, long long blk_stride, int nstart, const int* inst,
+                         int ninst, long long h, double kappa_max, int max_steps, double* mu_all, double* sigma_all,
+                         int* status_all, int* steps_all, double* logdet_all, double* traj, int traj_stride,
+                         uint8_t* mem_all, cudaStream_t st) {
+  const int nb = (p + 7) / 8;
+  const int nred = (nb * (nb + 1) / 2) * 64 + 8 * nb + 1;
+  const size_t dyn = (3 * (size_t)RTD_MAXP * LD + std::max<size_t>((size_t)m, (size_t)CS_W * nred)) * sizeof(double);
+  const int dmax = (int)((3 * (size_t)RTD_MAXP * LD + CS_SMALL_M) * sizeof(double));
+  if (nb == 1) {
+    static const bool a1 = [dmax] {
+      cudaFuncSetAttribute(k_csteps_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, dmax);
+      return true;
+    }();
+    (void)a1;
+    k_csteps_small<1><<<ninst, CS_T, dyn, st>>>(Zall, (int)m, p, blk_stride, nstart, inst, (int)h, kappa_max,
+                                                max_steps, mu_all, sigma_all, status_all, steps_all, logdet_all, traj,
+                                                traj_stride, mem_all);
+  } else {
+    static const bool a2 = [dmax] {
+      cudaFuncSetAttribute(k_csteps_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, dmax);
+      return true;
+    }();
+    (void)a2;
+    k_csteps_small<2><<<ninst, CS_T, dyn, st>>>(Zall, (int)m, p, blk_stride, nstart, inst, (int)h, kappa_max,
+                                                max_steps, mu_all, sigma_all, status_all, steps_all, logdet_all, traj,
+                                                traj_stride, mem_all);
+  }
+  RTD_LAUNCHED();
 }
 
 void launch_prepare(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p, double kappa_max,

@@ -11,6 +11,12 @@ enum InstStatus { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_NOT_PD = 2, ST_COND = 3, S
 void launch_prepare(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p, double kappa_max,
                     double* cstage, int cstride, double* logdet_out, double* cond_out, int* status_out, double* traj,
                     int traj_stride, int step, cudaStream_t st, int full_inverse = 0);
+// the whole C-step loop of short blocks (m <= 20480, p <= 16) in one CTA per instance (k_linalg.cu)
+bool csteps_small_supported(long long m, int p);
+void launch_csteps_small(const double* Zall, long long m, int p, long long blk_stride, int nstart, const int* inst,
+                         int ninst, long long h, double kappa_max, int max_steps, double* mu_all, double* sigma_all,
+                         int* status_all, int* steps_all, double* logdet_all, double* traj, int traj_stride,
+                         uint8_t* mem_all, cudaStream_t st);
 void launch_sums_to_cov(const int* inst, int ninst, const double* sums_all, int np, const double* shift_all, int p,
                         double n_given, double factor, double* mu_all, double* sigma_all, cudaStream_t st);
 void launch_sums_to_second(const double* sums_all, int nb, int np, int p, double n, double* out_all, cudaStream_t st);
