@@ -84,6 +84,17 @@ __device__ __forceinline__ dd2 dd2_zero() { return {{0.0, 0.0}, {0.0, 0.0}}; }
 __device__ __forceinline__ dd2 dd2_add(dd2 a, dd2 b) { return {dd_add(a.s1, b.s1), dd_add(a.s2, b.s2)}; }
 __device__ __forceinline__ dd2 dd2_sub(dd2 a, dd2 b) { return {dd_sub(a.s1, b.s1), dd_sub(a.s2, b.s2)}; }
 __device__ __forceinline__ dd2 dd2_of(double y) { return {dd_make(y), two_prod(y, y)}; }
+// (y, d^2) with d = y - c rounded: the reweighting sums (sum y for the mean, sum (y - c)^2 for the
+// variance about the raw location c, free of the cancellation of sum y^2 - (sum y)^2 / k)
+__device__ __forceinline__ dd2 dd2_of_dev(double y, double d) { return {dd_make(y), two_prod(d, d)}; }
+
+// reweighted variance numerator sum (y - loc)^2 from K = (sum y, sum (y - c)^2) over k kept values,
+// loc = round(sum y) / k:  sum (d - D)^2 = K.s2 - 2 D sum(y - c) + k D^2,  D = loc - c (exact, dd)
+__device__ __forceinline__ dd kept_sq_about_loc(const dd2& K, double c, double loc, double k) {
+  const dd B = dd_sub(K.s1, two_prod(c, k));
+  const dd D = two_sum(loc, -c);
+  return dd_add(K.s2, dd_sub(dd_mul(dd_mul_d(D, k), D), dd_mul_d(dd_mul(D, B), 2.0)));
+}
 
 __device__ __forceinline__ dd2 shfl_dd2(dd2 v, int src) {
   dd2 r;

@@ -40,27 +40,47 @@ __global__ void __launch_bounds__(UTH) k_uni_chunksum(const double* __restrict__
   if (threadIdx.x == 0) csum[(long long)col * nchunks + blockIdx.x] = tot;
 }
 
-// exclusive prefix of chunk totals; coff[col][c] for c in [0, nchunks]
+// Prefix sums of chunk totals ANCHORED at the chunk boundary nearest the middle of the sorted column:
+// coff[col][c] = P(c UCH) - P(A UCH), i.e. the sum of chunks [A, c) for c >= A and minus the sum of
+// chunks [c, A) for c < A.  Every window sum is a difference of two such values, and no partial sum
+// reaches past the window ends into the tails (a sorted column with entries of magnitude 1e12 at both
+// ends would otherwise lose the window sums to cancellation in the prefix differences).
 __global__ void __launch_bounds__(1024) k_uni_chunkscan(const dd2* __restrict__ csum, int nchunks,
                                                         dd2* __restrict__ coff) {
   __shared__ dd2 sm[33];
   const int col = blockIdx.y;
   const dd2* cs = csum + (long long)col * nchunks;
   dd2* co = coff + (long long)col * (nchunks + 1);
-  const int per = (nchunks + blockDim.x - 1) / blockDim.x;
-  const int c0 = threadIdx.x * per;
-  dd2 loc = dd2_zero();
-  for (int c = c0; c < min(c0 + per, nchunks); c++) loc = dd2_add(loc, cs[c]);
-  dd2 tot;
-  dd2 ex = block_exscan_dd2(loc, &tot, sm);
-  for (int c = c0; c < min(c0 + per, nchunks); c++) {
-    co[c] = ex;
-    ex = dd2_add(ex, cs[c]);
+  const int A = nchunks / 2;
+  {  // forward: chunks [A, nchunks)
+    const int nf = nchunks - A;
+    const int per = (nf + blockDim.x - 1) / blockDim.x;
+    const int c0 = A + threadIdx.x * per, c1 = min(nchunks, c0 + per);
+    dd2 loc = dd2_zero();
+    for (int c = c0; c < c1; c++) loc = dd2_add(loc, cs[c]);
+    dd2 tot;
+    dd2 ex = block_exscan_dd2(loc, &tot, sm);
+    for (int c = c0; c < c1; c++) {
+      co[c] = ex;
+      ex = dd2_add(ex, cs[c]);
+    }
+    if (threadIdx.x == 0) co[nchunks] = tot;
   }
-  if (threadIdx.x == 0) co[nchunks] = tot;
+  {  // backward: chunks A-1, A-2, ..., 0
+    const int per = (A + blockDim.x - 1) / blockDim.x;
+    const int i0 = threadIdx.x * per, i1 = min(A, i0 + per);
+    dd2 loc = dd2_zero();
+    for (int i = i0; i < i1; i++) loc = dd2_add(loc, cs[A - 1 - i]);
+    dd2 tot;
+    dd2 ex = block_exscan_dd2(loc, &tot, sm);
+    for (int i = i0; i < i1; i++) {
+      ex = dd2_add(ex, cs[A - 1 - i]);
+      co[A - 1 - i] = {dd_neg(ex.s1), dd_neg(ex.s2)};
+    }
+  }
 }
 
-// P(t) = sum_{i<t} (y_i, y_i^2), block-cooperative; all threads get the value.
+// P(t) - P(anchor) of (y_i, y_i^2), block-cooperative; all threads get the value.
 __device__ dd2 block_prefix_at(const double* __restrict__ y, const dd2* __restrict__ co, long long t, dd2* sm) {
   const long long c = t / UCH;
   const long long s0 = c * UCH;
@@ -242,8 +262,11 @@ __global__ void __launch_bounds__(UTH) k_uni_final(const double* __restrict__ so
   __syncthreads();
   const long long klo = s_lohi[0], khi = s_lohi[1];
   const long long k = khi - klo;
-  dd2 Q0 = block_prefix_at(y, co, klo, sm);
-  dd2 Q1 = block_prefix_at(y, co, khi, sm);
+  // sums over the kept range accumulated directly (no prefix differences)
+  dd2 kacc = dd2_zero();
+  for (long long i = klo + threadIdx.x; i < khi; i += blockDim.x)
+    kacc = dd2_add(kacc, dd2_of_dev(y[i], __dsub_rn(y[i], loc0)));
+  const dd2 Kd = block_sum_dd2(kacc, sm);
   if (threadIdx.x == 0) {
     UniOut o;
     o.raw_loc = loc0;
@@ -258,12 +281,11 @@ __global__ void __launch_bounds__(UTH) k_uni_final(const double* __restrict__ so
     if (!(var0 > 0.0) || k < 2) {
       o.status = 1;
     } else {
-      dd2 K = dd2_sub(Q1, Q0);
+      const dd2 K = Kd;
       const double Sd = dd_to_d(K.s1);
       const double loc = Sd / (double)k;
-      // sum (y - loc)^2 = S2 - 2 loc S1 + k loc^2, in dd
-      dd q = dd_sub(K.s2, dd_mul_d(K.s1, 2.0 * loc));
-      q = dd_add(q, dd_mul_d(two_prod(loc, loc), (double)k));
+      // sum (y - loc)^2 from sum y and sum (y - loc0)^2 (no cancellation of sum y^2)
+      const dd q = kept_sq_about_loc(K, loc0, loc, (double)k);
       const double var = uc.c_rew * (dd_to_d(q) / (double)(k - 1));
       o.loc = loc;
       o.scale = sqrt(var);
@@ -279,7 +301,7 @@ __global__ void __launch_bounds__(UTH) k_uni_final(const double* __restrict__ so
 // per-thread chunk totals and their block scan in double-double, the window objective of every start
 // (ties -> lowest s), the raw estimate and the reweighting -- so a short column costs one launch
 // instead of two radix sorts and four passes (the stream of BASELINE config 5, 20,000 rows).
-static constexpr int USMALL = 20480;  // shared-memory capacity bound
+static constexpr int USMALL = 16384;  // shared-memory capacity bound
 static constexpr int USMALL_USE = 4096;  // measured: faster than the radix-sort path up to here (config 1:
                                          // 3 calls 1.06 -> 0.21 ms), slower at 20,000 rows (config 5)
 static constexpr int UST = 1024;
@@ -307,7 +329,6 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
   dd2* cpre = reinterpret_cast<dd2*>(usm + ((len + 3) & ~3));  // [UST + 1]
   __shared__ dd2 sm[33];
   __shared__ WinPartial wsm[UST / 32];
-  __shared__ long long s_lohi[2];
   const int col = blockIdx.x, t = threadIdx.x;
   const double* y = cols + (long long)col * len;
   for (int i = t; i < len; i += UST) v[i] = y[i];
@@ -335,11 +356,24 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
   const int c0 = t * per, c1 = min(len, c0 + per);
   dd2 loc = dd2_zero();
   for (int i = c0; i < c1; i++) loc = dd2_add(loc, dd2_of(v[i]));
+  // prefixes anchored at chunk UST/2 (see k_uni_chunkscan): cpre[c] = P(c per) - P(UST/2 per)
+  constexpr int AN = UST / 2;
   dd2 tot;
-  const dd2 ex = block_exscan_dd2(loc, &tot, sm);
-  cpre[t] = ex;
+  const dd2 fex = block_exscan_dd2(t >= AN ? loc : dd2_zero(), &tot, sm);  // chunks [AN, t)
+  cpre[t] = loc;  // chunk totals, read back reversed below
+  __syncthreads();
+  const dd2 rin = t < AN ? cpre[AN - 1 - t] : dd2_zero();
+  dd2 btot;
+  const dd2 bex = block_exscan_dd2(rin, &btot, sm);  // chunks AN-1, ..., AN-t
+  __syncthreads();
+  if (t >= AN) cpre[t] = fex;
+  else {
+    const dd2 b = dd2_add(bex, rin);  // chunks [AN-1-t, AN)
+    cpre[AN - 1 - t] = {dd_neg(b.s1), dd_neg(b.s2)};
+  }
   if (t == 0) cpre[UST] = tot;
   __syncthreads();
+  const dd2 ex = cpre[t];
   // window objective h S2 - S1^2 for starts s in [c0, c1) with s < nwin
   const int nwin = len - h + 1;
   double bhi = __longlong_as_double(0x7ff0000000000000LL), blo = 0.0;
@@ -374,7 +408,9 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
   }
   if ((t & 31) == 0) wsm[t >> 5] = {bhi, blo, bs};
   __syncthreads();
-  if (t != 0) return;
+  __shared__ int s_k[2];
+  __shared__ double s_f[4];
+  if (t == 0) {
   WinPartial best = wsm[0];
   for (int w = 1; w < UST / 32; w++)
     if (win_better(wsm[w].vhi, wsm[w].vlo, wsm[w].s, best.vhi, best.vlo, best.s)) best = wsm[w];
@@ -405,7 +441,23 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
     if (uni_keep(v[mid], loc0, thresh)) lo = mid + 1; else hi = mid;
   }
   const int khi = lo;
-  (void)s_lohi;
+  s_k[0] = klo;
+  s_k[1] = khi;
+  s_f[0] = loc0;
+  s_f[1] = var_raw;
+  s_f[2] = var0;
+  s_f[3] = (double)s;
+  }
+  __syncthreads();
+  // sums over the kept range accumulated directly (no prefix differences)
+  const int klo = s_k[0], khi = s_k[1];
+  dd2 kacc = dd2_zero();
+  const double c0v = s_f[0];
+  for (int i = klo + t; i < khi; i += UST) kacc = dd2_add(kacc, dd2_of_dev(v[i], __dsub_rn(v[i], c0v)));
+  const dd2 Kd = block_sum_dd2(kacc, sm);
+  if (t != 0) return;
+  const double loc0 = s_f[0], var_raw = s_f[1], var0 = s_f[2];
+  const int s = (int)s_f[3];
   UniOut o;
   o.raw_loc = loc0;
   o.raw_var = var_raw;
@@ -420,11 +472,10 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
   if (!(var0 > 0.0) || k < 2) {
     o.status = 1;
   } else {
-    const dd2 K = dd2_sub(u_prefix(v, cpre, per, khi), u_prefix(v, cpre, per, klo));
+    const dd2 K = Kd;
     const double Sd = dd_to_d(K.s1);
     const double lc = Sd / (double)k;
-    dd q = dd_sub(K.s2, dd_mul_d(K.s1, 2.0 * lc));
-    q = dd_add(q, dd_mul_d(two_prod(lc, lc), (double)k));
+    const dd q = kept_sq_about_loc(K, loc0, lc, (double)k);
     const double var = uc.c_rew * (dd_to_d(q) / (double)(k - 1));
     o.loc = lc;
     o.scale = sqrt(var);

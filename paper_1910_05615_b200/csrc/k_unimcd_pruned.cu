@@ -94,6 +94,21 @@ __device__ __forceinline__ void ddacc_add(ddacc& a, double v) {
   a.h2 = s2;
   a.l2 = __dadd_rn(a.l2, __dadd_rn(e2, pe));
 }
+// the reweighting form: sum y and sum d^2 (d = y - c already rounded)
+__device__ __forceinline__ void ddacc_add_dev(ddacc& a, double v, double dv) {
+  const double s = __dadd_rn(a.h1, v);
+  const double bb = __dsub_rn(s, a.h1);
+  const double e = __dadd_rn(__dsub_rn(a.h1, __dsub_rn(s, bb)), __dsub_rn(v, bb));
+  a.h1 = s;
+  a.l1 = __dadd_rn(a.l1, e);
+  const double pr = __dmul_rn(dv, dv);
+  const double pe = __fma_rn(dv, dv, -pr);
+  const double s2 = __dadd_rn(a.h2, pr);
+  const double b2 = __dsub_rn(s2, a.h2);
+  const double e2 = __dadd_rn(__dsub_rn(a.h2, __dsub_rn(s2, b2)), __dsub_rn(pr, b2));
+  a.h2 = s2;
+  a.l2 = __dadd_rn(a.l2, __dadd_rn(e2, pe));
+}
 __device__ __forceinline__ dd2 ddacc_dd2(const ddacc& a) {
   return {quick_two_sum(a.h1, a.l1), quick_two_sum(a.h2, a.l2)};
 }
@@ -166,7 +181,7 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
   __syncthreads();
   const double* y = cols + (long long)col * len;
   unsigned long long kmin = ~0ull, kmax = 0ull;
-  double e0 = 0.0, e1 = 0.0;
+  double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;  // end-bucket sums and sums of magnitudes
   const long long per = (len + gridDim.x - 1) / gridDim.x;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
   for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
@@ -183,8 +198,10 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
         atomicAdd(&hc[b], 1u);
         if (b == 0) {
           e0 += v[k];
+          a0 += fabs(v[k]);
         } else if (b == NBK - 1) {
           e1 += v[k];
+          a1 += fabs(v[k]);
         } else {
           const double tt = __dsub_rn(__dmul_rn(__dsub_rn(v[k], c.lo), c.inv_w), (double)(b - 1));
           const int q = (int)fmin(fmax(__dmul_rn(tt, 65536.0), 0.0), 65535.0);
@@ -201,12 +218,20 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
     kmax = max(kmax, __shfl_down_sync(0xffffffffu, kmax, d));
     e0 += __shfl_down_sync(0xffffffffu, e0, d);
     e1 += __shfl_down_sync(0xffffffffu, e1, d);
+    a0 += __shfl_down_sync(0xffffffffu, a0, d);
+    a1 += __shfl_down_sync(0xffffffffu, a1, d);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicMin(&mm[2 * col], kmin);
     atomicMax(&mm[2 * col + 1], kmax);
-    if (e0 != 0.0) atomicAdd(&esum[2 * col], e0);
-    if (e1 != 0.0) atomicAdd(&esum[2 * col + 1], e1);
+    if (a0 != 0.0) {
+      atomicAdd(&esum[4 * col], e0);
+      atomicAdd(&esum[4 * col + 2], a0);
+    }
+    if (a1 != 0.0) {
+      atomicAdd(&esum[4 * col + 1], e1);
+      atomicAdd(&esum[4 * col + 3], a1);
+    }
   }
   __syncthreads();
   int* cn = cnt + (long long)col * NBK;
@@ -231,9 +256,12 @@ __device__ __forceinline__ void bucket_sum_interval(int b, int r, unsigned long 
   if (r == 0) {
     Slo = Shi = 0.0;
   } else if (b == 0 || b == NBK - 1) {
-    const double S = es[b == 0 ? 0 : 1];
-    Slo = S - 1e-12 * fabs(S);
-    Shi = S + 1e-12 * fabs(S);
+    // an fp64 sum of r terms in any order is within (r + 2) u sum|y| of the exact sum (u = 2^-53;
+    // the sum of magnitudes itself carries a relative error below (r + 2) u, hence the factor 2)
+    const double S = es[b == 0 ? 0 : 1], Sa = es[b == 0 ? 2 : 3];
+    const double err = 2.0 * ((double)r + 2.0) * 0x1p-53 * Sa + 1e-300;
+    Slo = S - err;
+    Shi = S + err;
   } else {
     const double rd = (double)r, Lb = c.lo + (double)(b - 1) * c.w, u = c.w * (1.0 / 65536.0);
     Slo = fmax(rd * bucket_lo(b, c), rd * Lb + u * ((double)T - rd));
@@ -257,7 +285,7 @@ __global__ void __launch_bounds__(1024) k_pr_scan(PrunedCol* __restrict__ pc, co
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int* cn = cnt + (long long)col * NBK;
   const unsigned long long* tqc = tq + (long long)col * NBK;
-  const double* es = esum + 2 * col;
+  const double* es = esum + 4 * col;
   double* sblo = sbg + (long long)col * 2 * NBK;
   double* sbhi = sblo + NBK;
   c.cmin = ord_val(mm[2 * col]);
@@ -843,7 +871,7 @@ __global__ void __launch_bounds__(PT) k_pr_keep(const double* __restrict__ cols,
       if (base + (long long)u * PT >= i1) continue;
       const double d = __dsub_rn(v[u], loc0);
       if (__dmul_rn(d, d) <= thresh) {
-        ddacc_add(acc, v[u]);
+        ddacc_add_dev(acc, v[u], d);
         k++;
       }
     }
@@ -877,8 +905,7 @@ __global__ void k_pr_final(UniConst uc, const dd2* __restrict__ part, const long
   } else {
     const double Sd = dd_to_d(K.s1);
     const double loc = Sd / (double)k;
-    dd q = dd_sub(K.s2, dd_mul_d(K.s1, 2.0 * loc));
-    q = dd_add(q, dd_mul_d(two_prod(loc, loc), (double)k));
+    const dd q = kept_sq_about_loc(K, o.raw_loc, loc, (double)k);
     const double var = uc.c_rew * (dd_to_d(q) / (double)(k - 1));
     o.loc = loc;
     o.scale = sqrt(var);
@@ -891,7 +918,7 @@ struct PrScratch {
   PrunedCol* pc;
   int* cnt;
   unsigned long long* tq;  // fixed-point offset sums per bucket
-  double* esum;            // under- / overflow bucket sums
+  double* esum;            // under- / overflow bucket sums and sums of magnitudes [col][4]
   double* sbb;             // [col][lo | hi] bucket sum intervals
   unsigned long long* mm;
   double *g, *gsorted;
@@ -924,7 +951,7 @@ static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.pc = A.take<PrunedCol>(ncols);
   s.cnt = A.take<int>((size_t)ncols * NBK);
   s.tq = A.take<unsigned long long>((size_t)ncols * NBK);
-  s.esum = A.take<double>((size_t)ncols * 2);
+  s.esum = A.take<double>((size_t)ncols * 4);
   s.sbb = A.take<double>((size_t)ncols * 2 * NBK);
   s.mm = A.take<unsigned long long>(2 * (size_t)ncols);
   s.g = A.take<double>((size_t)2 * ncols * CAP);
@@ -962,7 +989,7 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   const long long h = len / 2 + 1;
   RTD_CU(cudaMemsetAsync(s.cnt, 0, (size_t)ncols * NBK * sizeof(int), st));
   RTD_CU(cudaMemsetAsync(s.tq, 0, (size_t)ncols * NBK * sizeof(unsigned long long), st));
-  RTD_CU(cudaMemsetAsync(s.esum, 0, (size_t)ncols * 2 * sizeof(double), st));
+  RTD_CU(cudaMemsetAsync(s.esum, 0, (size_t)ncols * 4 * sizeof(double), st));
   RTD_CU(cudaMemsetAsync(s.gcount, 0, 2 * (size_t)ncols * sizeof(int), st));
   k_pr_sample<<<ncols, 1024, 0, st>>>(cols, len, s.pc, s.mm);
   RTD_LAUNCHED();

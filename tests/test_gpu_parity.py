@@ -88,6 +88,31 @@ def test_unimcd_large_columns(n):
         assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13), j
 
 
+def test_unimcd_heavy_mixed_sign_tails():
+    """Bucketed path (n >= 65536) with under- / overflow buckets holding huge values of both signs
+    (their fp64 sums enter the window bounds with a rigorous rounding margin)."""
+    rng = np.random.default_rng(77)
+    n = 200_000
+    cols = []
+    x = 1.0 + rng.random(n)
+    k = int(0.008 * n)
+    x[:k] = rng.choice([-1.0, 1.0], size=k) * 10.0 ** rng.uniform(0, 12, size=k)
+    cols.append(rng.permutation(x))
+    y = rng.standard_cauchy(n)
+    cols.append(y)
+    z = np.concatenate([rng.standard_normal(n // 2) * 1e-8 + 1e8, rng.standard_normal(n - n // 2)])
+    cols.append(rng.permutation(z))
+    cols = np.stack(cols)
+    g = api.unimcd(_cuda(cols))
+    for j in range(cols.shape[0]):
+        o = unimcd_reweighted(cols[j])
+        r = unimcd_raw(cols[j], n // 2 + 1)
+        assert g["start"][j] == r.start
+        assert g["raw_var"][j] == pytest.approx(r.var_raw, rel=1e-14)
+        assert g["loc"][j] == pytest.approx(o.loc, rel=1e-14, abs=1e-14)
+        assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13)
+
+
 def test_unimcd_degenerate_column_errors():
     x = np.ones((1, 100))
     with pytest.raises(api.RTDError) as e:
