@@ -380,8 +380,10 @@ void launch_moments_mma(int mode, const MomArgs& a, int ninst, cudaStream_t st) 
 // ------------------------------------------------------------------ out = Z W on DMMA
 // Batched over work items (blockIdx.y = i): slot = slot_of[i] (or i), Z = Zall + blk_of_slot[slot] *
 // blk_stride (or Zall), W = W_all + slot * RTD_MAXP^2, out = out_all + i * p * m.
-template <int NB, int MB>
-__global__ void __launch_bounds__(256) k_matmul_mma(const double* __restrict__ Zall, long long m, int p,
+// BSM: B fragments of W in shared memory (lane-major, conflict-free) instead of registers, so that
+// two CTAs fit on an SM at p = 40 (the register-held form runs one CTA of 8 warps at 180 registers)
+template <int NB, int MB, bool BSM>
+__global__ void __launch_bounds__(256, BSM ? 2 : 1) k_matmul_mma(const double* __restrict__ Zall, long long m, int p,
                                                     long long blk_stride, const int* __restrict__ slot_of,
                                                     const int* __restrict__ blk_of_slot,
                                                     const double* __restrict__ W_all, double* __restrict__ out_all) {
@@ -391,14 +393,24 @@ __global__ void __launch_bounds__(256) k_matmul_mma(const double* __restrict__ Z
   const double* __restrict__ Z = Zall + (blk_of_slot ? (long long)blk_of_slot[slot] * blk_stride : 0LL);
   const double* __restrict__ W = W_all + (long long)slot * RTD_MAXP * RTD_MAXP;
   double* __restrict__ out = out_all + (long long)blockIdx.y * p * m;
-  double bf[KB][NB];
-#pragma unroll
-  for (int kb = 0; kb < KB; kb++)
-#pragma unroll
-    for (int nb = 0; nb < NB; nb++) {
-      const int k = 4 * kb + t, j = 8 * nb + g;
-      bf[kb][nb] = (k < p && j < p) ? W[k * p + j] : 0.0;
+  __shared__ double bsm[BSM ? KB * NB * 32 : 1];
+  double bf[BSM ? 1 : KB][BSM ? 1 : NB];
+  if (BSM) {
+    for (int e = threadIdx.x; e < KB * NB * 32; e += blockDim.x) {
+      const int ln = e & 31, b = e >> 5, kb = b / NB, nb = b - kb * NB;
+      const int k = 4 * kb + (ln & 3), j = 8 * nb + (ln >> 2);
+      bsm[e] = (k < p && j < p) ? W[k * p + j] : 0.0;
     }
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int kb = 0; kb < KB; kb++)
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        const int k = 4 * kb + t, j = 8 * nb + g;
+        if (!BSM) bf[kb][nb] = (k < p && j < p) ? W[k * p + j] : 0.0;
+      }
+  }
   const long long rows_per_tile = 8 * MB;
   const long long ntiles = (m + rows_per_tile - 1) / rows_per_tile;
   const long long warp0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -420,9 +432,11 @@ __global__ void __launch_bounds__(256) k_matmul_mma(const double* __restrict__ Z
         av[mb] = (k < p && row < m) ? Z[(long long)k * m + row] : 0.0;
       }
 #pragma unroll
-      for (int nb = 0; nb < NB; nb++)
+      for (int nb = 0; nb < NB; nb++) {
+        const double bv = BSM ? bsm[(kb * NB + nb) * 32 + lane] : bf[BSM ? 0 : kb][BSM ? 0 : nb];
 #pragma unroll
-        for (int mb = 0; mb < MB; mb++) dmma(acc[mb][nb][0], acc[mb][nb][1], av[mb], bf[kb][nb]);
+        for (int mb = 0; mb < MB; mb++) dmma(acc[mb][nb][0], acc[mb][nb][1], av[mb], bv);
+      }
     }
 #pragma unroll
     for (int mb = 0; mb < MB; mb++) {
@@ -441,10 +455,20 @@ __global__ void __launch_bounds__(256) k_matmul_mma(const double* __restrict__ Z
 template <int NB>
 static void matmul_mma_nb(const double* Z, long long m, int p, long long blk_stride, const int* slot_of,
                           const int* blk_of_slot, int nitems, const double* W, double* out, cudaStream_t st) {
+  // p > 24: B in shared memory, 2 CTAs/SM, 3 m-blocks per warp (measured on config 4: the two refinement
+  // GEMMs 6.46 -> 5.13 ms per fit; RTD_MATMUL_VARIANT=0 selects the register-held form)
+  static const int variant = getenv("RTD_MATMUL_VARIANT") ? atoi(getenv("RTD_MATMUL_VARIANT")) : 1;
+  if (NB >= 4 && variant == 1) {
+    constexpr int MB = 3;
+    const long long tiles = (m + 8 * MB - 1) / (8 * MB);
+    const unsigned grid = (unsigned)std::min<long long>((tiles + 7) / 8, std::max(1, 148 * 4 / std::max(1, nitems)));
+    k_matmul_mma<NB, MB, true><<<dim3(grid, nitems), 256, 0, st>>>(Z, m, p, blk_stride, slot_of, blk_of_slot, W, out);
+    return;
+  }
   constexpr int MB = NB <= 3 ? 4 : 2;
   const long long tiles = (m + 8 * MB - 1) / (8 * MB);
   const unsigned grid = (unsigned)std::min<long long>((tiles + 7) / 8, std::max(1, 148 * 4 / std::max(1, nitems)));
-  k_matmul_mma<NB, MB><<<dim3(grid, nitems), 256, 0, st>>>(Z, m, p, blk_stride, slot_of, blk_of_slot, W, out);
+  k_matmul_mma<NB, MB, false><<<dim3(grid, nitems), 256, 0, st>>>(Z, m, p, blk_stride, slot_of, blk_of_slot, W, out);
 }
 
 void launch_matmul_mma_batch(int p, const double* Zall, long long m, long long blk_stride, const int* slot_of,
