@@ -393,3 +393,31 @@ def test_fit_variant_errors():
     assert e.value.name == "RTD_E_INVALID_ARG"
     with pytest.raises(api.RTDError):
         api.fit(_cuda(X), h=300, consistency=7)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 7, 8, 9, 16, 17, 24, 25, 33, 40])
+def test_fit_every_width_class(p):
+    """Every kernel-template class of p (SIMT distances below 8, DMMA 8..40; 1..5 column blocks of 8;
+    register vs shared-memory GEMM operand) against the oracle on a contaminated Gaussian sample
+    with a ragged row count."""
+    n = 3001 if p <= 24 else 9001
+    rng = np.random.default_rng([4242, p])
+    Q, _ = np.linalg.qr(rng.standard_normal((p, p)))
+    A = Q * np.linspace(1.0, 2.0, p)
+    X = rng.standard_normal((n, p)) @ A.T
+    u = rng.standard_normal(p)
+    X[: n // 10] += 8.0 * u / np.linalg.norm(u)
+    h = int(0.75 * n)
+    o = ofit.fit(X, h=h)
+    g = api.fit(_cuda(X), h=h)
+    _compare_fit(g, o, X)
+
+
+def test_fit_blocked_long_blocks_p40():
+    """q = 2 blocks of 70,000 rows at p = 40: the bucketed univariate MCD (>= 65,536 rows), the staged
+    dense moments and the shared-memory GEMM operand on the blocked path."""
+    d = datagen.make_config(4, n=140_001)
+    h = int(0.75 * 140_001)
+    o = ofit.fit(d.X, h=h, q=2, seed=11)
+    g = api.fit(_cuda(d.X), h=h, q=2, seed=11)
+    _compare_fit(g, o, d.X)
