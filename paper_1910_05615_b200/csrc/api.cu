@@ -250,7 +250,7 @@ void carve_cstep(Arena& A, CStepBufs& b, int ninst, long long m, int p, int max_
   b.traj_stride = max_steps + 2;
   b.traj = A.take<double>((size_t)ninst * b.traj_stride);
   b.cstage = A.take<double>(RTD_CONST_DOUBLES + (size_t)ninst * (RTD_MAXP + RTD_MAXP * RTD_MAXP));  // full inverse fits
-  b.ctas = (int)std::max<long long>(1, std::min<long long>(256, (m + 4095) / 4096));
+  b.ctas = (int)std::max<long long>(1, std::min<long long>(256, (m + 511) / 512));
   b.partial = A.take<double>((size_t)ninst * b.ctas * NPMAX);
   b.d2 = A.take<double>((size_t)ninst * m);
   b.status = A.take<int>(ninst);
@@ -563,8 +563,8 @@ void carve_init(Arena& A, InitBufs& b, int q, long long m, int p) {
   b.rs = A.take<double>((size_t)q * m);
   b.AB = A.take<double>(2 * (size_t)q);
   b.abok = A.take<int>(q);
-  // CTAs per block: 4 full waves of 2 CTAs on each of the 148 SMs over the q blocks, >= 4096 rows each
-  b.ctas = (int)std::max<long long>(1, std::min<long long>((m + 4095) / 4096, (296LL * 4 + q - 1) / q));
+  // CTAs per block: 4 full waves of 2 CTAs on each of the 148 SMs over the q blocks, >= 512 rows each
+  b.ctas = (int)std::max<long long>(1, std::min<long long>((m + 511) / 512, (296LL * 4 + q - 1) / q));
   b.sums = A.take<double>((size_t)q * NPMAX);
   b.partial = A.take<double>((size_t)q * b.ctas * NPMAX);
   b.mudummy = A.take<double>((size_t)q * RTD_MAXP);

@@ -183,6 +183,26 @@ __global__ void __launch_bounds__(UTH) k_uni_window(const double* __restrict__ s
   }
 }
 
+// first index in [lo, hi) with pred true (pred monotone false -> true; hi if none), by one warp:
+// 32 probes per round, ballot, narrow to one of 32 sub-ranges
+template <class Pred>
+__device__ __forceinline__ long long warp_partition_point(long long lo, long long hi, Pred pred) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const long long step = (hi - lo + 31) / 32;
+    const long long pos = min(hi - 1, lo + (lane + 1) * step - 1);
+    const unsigned b = __ballot_sync(0xffffffffu, pred(pos));
+    if (b == 0u) return hi;  // the last probe is hi - 1: nothing in range is true
+    const int f = __ffs(b) - 1;  // first probe that holds: the point is in (pos_{f-1}, pos_f]
+    const long long nlo = f == 0 ? lo : lo + f * step;
+    hi = min(hi, lo + (f + 1) * step);
+    lo = nlo;
+  }
+  const long long pos = lo + lane;
+  const unsigned b = __ballot_sync(0xffffffffu, pos < hi && pred(pos));
+  return b ? lo + (__ffs(b) - 1) : hi;
+}
+
 __device__ __forceinline__ bool uni_keep(double y, double loc0, double thresh) {
   double d = __dsub_rn(y, loc0);
   return __dmul_rn(d, d) <= thresh;
@@ -235,29 +255,17 @@ __global__ void __launch_bounds__(UTH) k_uni_final(const double* __restrict__ so
   const double var_raw = h > 1 ? dd_to_d(dd_div_d(dd_div_d(v, hd), (double)(h - 1))) : 0.0;
   const double var0 = uc.c_raw * var_raw;
   const double thresh = uc.q1 * var0;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // three 32-ary searches by warp 0 (a serial binary search is 3 x 15 dependent loads)
     // i0 = first index with y >= loc0
-    long long lo = 0, hi = len;
-    while (lo < hi) {
-      long long mid = (lo + hi) >> 1;
-      if (y[mid] < loc0) lo = mid + 1; else hi = mid;
-    }
-    const long long i0 = lo;
+    const long long i0 = warp_partition_point(0, len, [&](long long i) { return y[i] >= loc0; });
     // first kept index in [0, i0] (keep is false then true on [0, i0))
-    lo = 0; hi = i0;
-    while (lo < hi) {
-      long long mid = (lo + hi) >> 1;
-      if (uni_keep(y[mid], loc0, thresh)) hi = mid; else lo = mid + 1;
-    }
-    const long long klo = lo;
+    const long long klo = warp_partition_point(0, i0, [&](long long i) { return uni_keep(y[i], loc0, thresh); });
     // first non-kept index in [i0, len) (keep is true then false)
-    lo = i0; hi = len;
-    while (lo < hi) {
-      long long mid = (lo + hi) >> 1;
-      if (uni_keep(y[mid], loc0, thresh)) lo = mid + 1; else hi = mid;
+    const long long khi = warp_partition_point(i0, len, [&](long long i) { return !uni_keep(y[i], loc0, thresh); });
+    if (threadIdx.x == 0) {
+      s_lohi[0] = klo;
+      s_lohi[1] = khi;
     }
-    s_lohi[0] = klo;
-    s_lohi[1] = lo;
   }
   __syncthreads();
   const long long klo = s_lohi[0], khi = s_lohi[1];

@@ -276,7 +276,7 @@ def test_fit_serial(cfg, n):
     assert g.start_steps[0] == o.blocks[0].starts[0].steps
 
 
-@pytest.mark.parametrize("q,n", [(8, 40_003), (3, 30_000), (2, 9_001)])
+@pytest.mark.parametrize("q,n", [(8, 40_003), (3, 30_000), (2, 9_001), (64, 64 * 700 + 13)])
 def test_fit_blocked(q, n):
     d = datagen.make_config(4, n=n)
     h = int(0.75 * n)
