@@ -3,6 +3,7 @@
 // device -> host read helper.
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "rtd_internal.h"
 
@@ -99,6 +100,26 @@ __global__ void k_warm_start(const UniOut* __restrict__ uni, const double* __res
 void launch_warm_start(const UniOut* uni, const double* mu_x, const double* sig_x, int p, int q, double* mu_all,
                        double* sig_all, cudaStream_t st) {
   k_warm_start<<<q, 256, 0, st>>>(uni, mu_x, sig_x, p, mu_all, sig_all);
+  RTD_LAUNCHED();
+}
+
+// eq[b] = 1 iff the membership bytes of instances 2b and 2b+1 agree on all m rows (the two starts of
+// block b reached the same h-subset)
+__global__ void k_mem_pairs_equal(const uint8_t* __restrict__ mem_all, long long m, int* __restrict__ eq) {
+  const int b = blockIdx.y;
+  const uint8_t* x = mem_all + (long long)(2 * b) * m;
+  const uint8_t* y = mem_all + (long long)(2 * b + 1) * m;
+  int diff = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+    diff |= x[i] != y[i];
+  if (__syncthreads_or(diff) && threadIdx.x == 0) eq[b] = 0;
+}
+
+void launch_mem_pairs_equal(const uint8_t* mem_all, long long m, int nblk, int* eq, cudaStream_t st) {
+  std::vector<int> ones(nblk, 1);
+  RTD_CU(cudaMemcpyAsync(eq, ones.data(), nblk * sizeof(int), cudaMemcpyHostToDevice, st));
+  const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((m + 255) / 256, 64));
+  k_mem_pairs_equal<<<dim3(gx, nblk), 256, 0, st>>>(mem_all, m, eq);
   RTD_LAUNCHED();
 }
 
