@@ -98,13 +98,6 @@ static constexpr int SR = 64;        // rows per tile
 static constexpr int SLD = SR + 4;   // padded column stride in shared memory (doubles)
 static constexpr int NST = 3;        // pipeline stages
 
-__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int NB, int MODE>
 __global__ void __launch_bounds__(MW * 32, 2) k_moments_st(MomArgs a) {

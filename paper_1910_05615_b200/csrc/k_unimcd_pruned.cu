@@ -35,11 +35,14 @@ static constexpr int SAMPLE = 4096;      // strided sample for the bucket map
 static constexpr int CAP = 65536;        // max gathered elements per side per column
 static constexpr int PCTA = 32;          // CTAs per column in the streaming passes (fixed -> deterministic)
 static constexpr int PT = 256;
+static constexpr int LT = 512;    // k_pr_locate threads (one CTA per column)
 
 struct PrunedCol {
   double lo, hi, w, inv_w;   // bucket map
   double cmin, cmax;         // column min / max
   long long smin, smax;      // candidate window starts
+  long long rmin, rmax;      // range of starts left by the chunk lower bounds (diagnostics)
+  double tS0, tS1, tE0, tE1; // value thresholds of the gathered bucket ranges (bucket_threshold)
   int bs_lo, bs_hi, be_lo, be_hi;  // gathered bucket ranges (start side / end side)
   long long cs_lo, ce_lo;    // C[bs_lo], C[be_lo]
   int status;                // 0 ok, 1 fall back
@@ -69,6 +72,20 @@ __device__ __forceinline__ unsigned long long ord_key(double x) {
 __device__ __forceinline__ double ord_val(unsigned long long k) {
   unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)u);
+}
+
+// Smallest double y with bucket_of(y) >= b (bucket_of is monotone in y), found by bisection over the
+// ordered bit patterns: y >= bucket_threshold(b) <=> bucket_of(y) >= b, so the streaming passes can
+// test bucket ranges with two compares
+__device__ double bucket_threshold(int b, const PrunedCol& c) {
+  if (b <= 0) return -INFINITY;
+  if (b >= NBK) return INFINITY;
+  unsigned long long lo = ord_key(-INFINITY), hi = ord_key(INFINITY);  // bucket_of(ord_val(hi)) = NBK - 1 >= b
+  while (lo < hi) {
+    const unsigned long long mid = lo + (hi - lo) / 2;
+    if (bucket_of(ord_val(mid), c) >= b) hi = mid; else lo = mid + 1;
+  }
+  return ord_val(lo);
 }
 
 // Running (sum y, sum y^2) of one thread in double-double, adding one double at a time with
@@ -269,33 +286,16 @@ __device__ __forceinline__ void bucket_sum_interval(int b, int r, unsigned long 
   }
 }
 
-__global__ void __launch_bounds__(1024) k_pr_scan(PrunedCol* __restrict__ pc, const int* __restrict__ cnt,
-                                                  const unsigned long long* __restrict__ tq,
-                                                  const double* __restrict__ esum,
-                                                  const unsigned long long* __restrict__ mm, long long* __restrict__ Cg,
-                                                  double* __restrict__ A1g, double* __restrict__ Q2log,
-                                                  double* __restrict__ Q2hig, double* __restrict__ sbg,
-                                                  BucketScan* __restrict__ bsc) {
+__device__ __forceinline__ void scan_column(PrunedCol& c, const int* __restrict__ cn, const unsigned long long* __restrict__ tqc,
+                                            const double* __restrict__ es, long long* C, double* sblo, double* A1lo,
+                                            double* Q2lo, double* Q2hi, BucketScan& bs) {
   __shared__ double red_d[32];
   __shared__ long long wc[32];
   __shared__ double w1[32], wh[32], wlo[32], whi[32];
-  const int col = blockIdx.x;
-  PrunedCol c = pc[col];
-  if (c.status) return;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int* cn = cnt + (long long)col * NBK;
-  const unsigned long long* tqc = tq + (long long)col * NBK;
-  const double* es = esum + 4 * col;
-  double* sblo = sbg + (long long)col * 2 * NBK;
   double* sbhi = sblo + NBK;
-  c.cmin = ord_val(mm[2 * col]);
-  c.cmax = ord_val(mm[2 * col + 1]);
-  long long* C = Cg + (long long)col * (NBK + 1);
-  double* A1lo = A1g + (long long)col * 2 * (NBK + 1);
   double* A1hi = A1lo + (NBK + 1);
-  double* Q2lo = Q2log + (long long)col * (NBK + 1);
-  double* Q2hi = Q2hig + (long long)col * (NBK + 1);
-  constexpr int per = NBK / 1024;
+  constexpr int per = NBK / LT, NW = LT / 32;
   double slo[per], shi[per], qlo[per], qhi[per];
   long long lc = 0;
   double l1 = 0.0, lh = 0.0, llo = 0.0, lhi = 0.0, abs1 = 0.0;
@@ -347,8 +347,9 @@ __global__ void __launch_bounds__(1024) k_pr_scan(PrunedCol* __restrict__ pc, co
   }
   __syncthreads();
   if (w == 0) {
-    long long vc = wc[lane];
-    double v1 = w1[lane], vh = wh[lane], vlo = wlo[lane], vhi = whi[lane];
+    const bool in = lane < NW;
+    long long vc = in ? wc[lane] : 0;
+    double v1 = in ? w1[lane] : 0.0, vh = in ? wh[lane] : 0.0, vlo = in ? wlo[lane] : 0.0, vhi = in ? whi[lane] : 0.0;
     long long xc = vc;
     double x1 = v1, xh = vh, xlo = vlo, xhi = vhi;
     for (int d = 1; d < 32; d <<= 1) {
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(1024) k_pr_scan(PrunedCol* __restrict__ pc, co
     elo += qlo[e];
     ehi += qhi[e];
   }
-  if (t == 1023) {
+  if (t == LT - 1) {
     C[NBK] = ec;
     A1lo[NBK] = e1;
     A1hi[NBK] = eh;
@@ -398,12 +399,12 @@ __global__ void __launch_bounds__(1024) k_pr_scan(PrunedCol* __restrict__ pc, co
   for (int d = 16; d > 0; d >>= 1) abs1 += __shfl_down_sync(0xffffffffu, abs1, d);
   if (lane == 0) red_d[w] = abs1;
   __syncthreads();
-  if (t == 1023) {
+  if (t == LT - 1) {
     double tot_abs1 = 0.0;
-    for (int k = 0; k < 32; k++) tot_abs1 += red_d[k];
-    bsc[col] = {1e-10 * (tot_abs1 + 1e-300), 1e-10 * (fabs(ehi) + 1e-300)};
-    pc[col] = c;  // with column min / max
+    for (int k = 0; k < NW; k++) tot_abs1 += red_d[k];
+    bs = {1e-10 * (tot_abs1 + 1e-300), 1e-10 * (fabs(ehi) + 1e-300)};
   }
+  __syncthreads();
 }
 
 // bounds on h*SQ(s) for one start s (start bucket b, end bucket be)
@@ -411,39 +412,74 @@ struct VBound {
   double lo, hi;
 };
 
-__device__ __forceinline__ VBound window_bounds(long long s, long long h, int b, int be, const PrunedCol& c,
-                                                const long long* C, const double* A1, const double* Q2lo,
-                                                const double* Q2hi, const int* cn, const double* sb,
-                                                BucketScan m) {
+// the per-run part of window_bounds: everything that depends on the start bucket b and the end
+// bucket be only (a run of consecutive starts shares it)
+struct RunConst {
+  double L1, U1, L2, U2, mn1, mx1, mn2, mx2;
+  double n1, n2, m1lo, Sbhi, Selo, m2hi;  // m1lo = Sblo / n1, m2hi = Sehi / n2
+  double F1lo, F1hi, Q2l, Q2h;
+  long long Cb1, Cbe;                     // C[b + 1], C[be]
+  bool same;
+};
+
+__device__ __forceinline__ RunConst run_const(int b, int be, const PrunedCol& c, const long long* C, const double* A1,
+                                              const double* Q2lo, const double* Q2hi, const double* sb) {
+  RunConst r;
+  r.L1 = bucket_lo(b, c);
+  r.U1 = bucket_hi(b, c);
+  r.L2 = bucket_lo(be, c);
+  r.U2 = bucket_hi(be, c);
+  r.mx1 = fmax(r.L1 * r.L1, r.U1 * r.U1);
+  r.mn1 = (r.L1 <= 0 && r.U1 >= 0) ? 0.0 : fmin(r.L1 * r.L1, r.U1 * r.U1);
+  r.mx2 = fmax(r.L2 * r.L2, r.U2 * r.U2);
+  r.mn2 = (r.L2 <= 0 && r.U2 >= 0) ? 0.0 : fmin(r.L2 * r.L2, r.U2 * r.U2);
+  r.same = be == b;
+  r.Cb1 = C[b + 1];
+  r.Cbe = C[be];
+  r.n1 = (double)(r.Cb1 - C[b]);
+  r.n2 = (double)(C[be + 1] - r.Cbe);
+  // bucket sums are intervals: sb[0..NBK) lower ends, sb[NBK..2NBK) upper ends; A1 likewise
+  r.m1lo = sb[b] * __drcp_rn(r.n1);
+  r.Sbhi = sb[NBK + b];
+  r.Selo = sb[be];
+  r.m2hi = sb[NBK + be] * __drcp_rn(r.n2);
+  r.F1lo = A1[be] - A1[b + 1];
+  r.F1hi = A1[NBK + 1 + be] - A1[NBK + 1 + b + 1];
+  r.Q2l = Q2lo[be] - Q2lo[b + 1];
+  r.Q2h = Q2hi[be] - Q2hi[b + 1];
+  return r;
+}
+
+// bounds on h*SQ(s) for one start s of the run
+__device__ __forceinline__ VBound start_bounds(const RunConst& r, long long s, long long h, BucketScan m) {
   const double hd = (double)h;
-  const double L1 = bucket_lo(b, c), U1 = bucket_hi(b, c), L2 = bucket_lo(be, c), U2 = bucket_hi(be, c);
-  const double mx1 = fmax(L1 * L1, U1 * U1), mn1 = (L1 <= 0 && U1 >= 0) ? 0.0 : fmin(L1 * L1, U1 * U1);
-  const double mx2 = fmax(L2 * L2, U2 * U2), mn2 = (L2 <= 0 && U2 >= 0) ? 0.0 : fmin(L2 * L2, U2 * U2);
   double lo1, hi1, lo2, hi2;
-  if (be == b) {
-    lo1 = hd * L1;
-    hi1 = hd * U1;
-    lo2 = hd * mn1;
-    hi2 = hd * mx1;
+  if (r.same) {
+    lo1 = hd * r.L1;
+    hi1 = hd * r.U1;
+    lo2 = hd * r.mn1;
+    hi2 = hd * r.mx1;
   } else {
-    const double n1 = (double)cn[b], n2 = (double)cn[be];
-    // bucket sums are intervals: sb[0..NBK) lower ends, sb[NBK..2NBK) upper ends; A1 likewise
-    const double Sblo = sb[b], Sbhi = sb[NBK + b], Selo = sb[be], Sehi = sb[NBK + be];
-    const double r1 = (double)(C[b + 1] - s), r2 = (double)(s + h - C[be]);
+    const double r1 = (double)(r.Cb1 - s), r2 = (double)(s + h - r.Cbe);
     // top r1 elements of bucket b: mean >= bucket mean; the other n1 - r1 are >= L1
-    const double t1lo = fmax(r1 * L1, r1 * Sblo * __drcp_rn(n1)), t1hi = fmin(r1 * U1, Sbhi - (n1 - r1) * L1);
+    const double t1lo = fmax(r1 * r.L1, r1 * r.m1lo), t1hi = fmin(r1 * r.U1, r.Sbhi - (r.n1 - r1) * r.L1);
     // bottom r2 elements of bucket be: mean <= bucket mean; the other n2 - r2 are <= U2
-    const double t2lo = fmax(r2 * L2, Selo - (n2 - r2) * U2), t2hi = fmin(r2 * U2, r2 * Sehi * __drcp_rn(n2));
-    const double F1lo = A1[be] - A1[b + 1], F1hi = A1[NBK + 1 + be] - A1[NBK + 1 + b + 1];
-    lo1 = F1lo + fmin(t1lo, t1hi) + fmin(t2lo, t2hi) - m.E1;
-    hi1 = F1hi + fmax(t1lo, t1hi) + fmax(t2lo, t2hi) + m.E1;
-    lo2 = (Q2lo[be] - Q2lo[b + 1]) + r1 * mn1 + r2 * mn2 - m.E2;
-    hi2 = (Q2hi[be] - Q2hi[b + 1]) + r1 * mx1 + r2 * mx2 + m.E2;
+    const double t2lo = fmax(r2 * r.L2, r.Selo - (r.n2 - r2) * r.U2), t2hi = fmin(r2 * r.U2, r2 * r.m2hi);
+    lo1 = r.F1lo + fmin(t1lo, t1hi) + fmin(t2lo, t2hi) - m.E1;
+    hi1 = r.F1hi + fmax(t1lo, t1hi) + fmax(t2lo, t2hi) + m.E1;
+    lo2 = r.Q2l + r1 * r.mn1 + r2 * r.mn2 - m.E2;
+    hi2 = r.Q2h + r1 * r.mx1 + r2 * r.mx2 + m.E2;
   }
   const double sq_hi_1 = fmax(lo1 * lo1, hi1 * hi1);
   const double sq_lo_1 = (lo1 <= 0 && hi1 >= 0) ? 0.0 : fmin(lo1 * lo1, hi1 * hi1);
   const double slack = 1e-9 * (hd * fabs(hi2) + sq_hi_1) + 1e-300;
   return {hd * lo2 - sq_hi_1 - slack, hd * hi2 - sq_lo_1 + slack};
+}
+
+__device__ __forceinline__ VBound window_bounds(long long s, long long h, int b, int be, const PrunedCol& c,
+                                                const long long* C, const double* A1, const double* Q2lo,
+                                                const double* Q2hi, const double* sb, BucketScan m) {
+  return start_bounds(run_const(b, be, c, C, A1, Q2lo, Q2hi, sb), s, h, m);
 }
 
 __device__ __forceinline__ int rank_bucket(const long long* C, long long r) {  // largest b with C[b] <= r
@@ -455,94 +491,142 @@ __device__ __forceinline__ int rank_bucket(const long long* C, long long r) {  /
   return lo;
 }
 
-// partial-bucket sums of one window start s (start bucket b, end bucket be), see window_bounds
-struct PartBounds {
-  double t1lo, t1hi, t2lo, t2hi;
-};
-__device__ __forceinline__ PartBounds part_bounds(long long s, long long h, int b, int be, const PrunedCol& c,
-                                                  const long long* C, const int* cn, const double* sb) {
-  const double L1 = bucket_lo(b, c), U1 = bucket_hi(b, c), L2 = bucket_lo(be, c), U2 = bucket_hi(be, c);
-  const double n1 = (double)cn[b], n2 = (double)cn[be];
-  const double Sblo = sb[b], Sbhi = sb[NBK + b], Selo = sb[be], Sehi = sb[NBK + be];
-  const double r1 = (double)(C[b + 1] - s), r2 = (double)(s + h - C[be]);
-  const double a = fmax(r1 * L1, r1 * Sblo * __drcp_rn(n1)), bb = fmin(r1 * U1, Sbhi - (n1 - r1) * L1);
-  const double d = fmax(r2 * L2, Selo - (n2 - r2) * U2), e = fmin(r2 * U2, r2 * Sehi * __drcp_rn(n2));
-  return {fmin(a, bb), fmax(a, bb), fmin(d, e), fmax(d, e)};
-}
-
-// Lower bound of h*SQ(s) valid for every s in [sa, sb] (same b, be, b != be): the partial
-// sums are monotone in s (t1 decreases, t2 increases), so the extremes come from the endpoints.
-__device__ __forceinline__ double chunk_lower(long long sa, long long sb, long long h, int b, int be,
-                                              const PrunedCol& c, const long long* C, const double* A1,
-                                              const double* Q2lo, const int* cn, const double* sbk, BucketScan m) {
+// Lower bound of h*SQ(s) valid for every s in [sa, sb] of one run (b != be): the partial sums of
+// start_bounds are monotone in s (t1 decreases, t2 increases), so their extremes over the run come
+// from its endpoints.
+__device__ __forceinline__ double chunk_lower(const RunConst& r, long long sa, long long sb, long long h,
+                                              BucketScan m) {
   const double hd = (double)h;
-  const PartBounds pa = part_bounds(sa, h, b, be, c, C, cn, sbk), pb = part_bounds(sb, h, b, be, c, C, cn, sbk);
-  const double F1lo = A1[be] - A1[b + 1], F1hi = A1[NBK + 1 + be] - A1[NBK + 1 + b + 1];
-  const double lo1 = F1lo + fmin(pa.t1lo, pb.t1lo) + fmin(pa.t2lo, pb.t2lo) - m.E1;
-  const double hi1 = F1hi + fmax(pa.t1hi, pb.t1hi) + fmax(pa.t2hi, pb.t2hi) + m.E1;
-  const double L1 = bucket_lo(b, c), U1 = bucket_hi(b, c), L2 = bucket_lo(be, c), U2 = bucket_hi(be, c);
-  const double mn1 = (L1 <= 0 && U1 >= 0) ? 0.0 : fmin(L1 * L1, U1 * U1);
-  const double mn2 = (L2 <= 0 && U2 >= 0) ? 0.0 : fmin(L2 * L2, U2 * U2);
-  double lo2 = INFINITY;
+  double t1lo = INFINITY, t1hi = -INFINITY, t2lo = INFINITY, t2hi = -INFINITY, lo2 = INFINITY;
+#pragma unroll
   for (int k = 0; k < 2; k++) {
     const long long s = k ? sb : sa;
-    lo2 = fmin(lo2, (Q2lo[be] - Q2lo[b + 1]) + (double)(C[b + 1] - s) * mn1 + (double)(s + h - C[be]) * mn2);
+    const double r1 = (double)(r.Cb1 - s), r2 = (double)(s + h - r.Cbe);
+    const double a = fmax(r1 * r.L1, r1 * r.m1lo), bb = fmin(r1 * r.U1, r.Sbhi - (r.n1 - r1) * r.L1);
+    const double d = fmax(r2 * r.L2, r.Selo - (r.n2 - r2) * r.U2), e = fmin(r2 * r.U2, r2 * r.m2hi);
+    t1lo = fmin(t1lo, fmin(a, bb));
+    t1hi = fmax(t1hi, fmax(a, bb));
+    t2lo = fmin(t2lo, fmin(d, e));
+    t2hi = fmax(t2hi, fmax(d, e));
+    lo2 = fmin(lo2, r.Q2l + r1 * r.mn1 + r2 * r.mn2);
   }
+  const double lo1 = r.F1lo + t1lo + t2lo - m.E1;
+  const double hi1 = r.F1hi + t1hi + t2hi + m.E1;
   lo2 -= m.E2;
   const double sq_hi_1 = fmax(lo1 * lo1, hi1 * hi1);
   const double slack = 1e-9 * (hd * fabs(lo2) + sq_hi_1) + 1e-300;
   return hd * lo2 - sq_hi_1 - slack;
 }
 
-static constexpr int CHUNK = 32;  // starts per chunk in the coarse lower-bound pass
+static constexpr int CHUNK = 64;      // starts per piece in the interval lower-bound pass
+static constexpr int UB1 = 4096;      // strided starts of the first upper-bound sample (the second is LT)
 
-// 3b. mode 0: upper bounds on a stride-CHUNK subset of starts (any subset gives a valid bound on the
-//             minimum) -> per-CTA minimum;
-//     mode 1: chunk lower bounds over all starts -> per-CTA range of candidate chunks;
-//     mode 2: per-start lower bounds inside the candidate chunk range -> per-CTA candidate range.
-__global__ void __launch_bounds__(PT) k_pr_bound(long long len, long long h, const PrunedCol* __restrict__ pc,
-                                                 const int* __restrict__ cnt, const double* __restrict__ sbg,
-                                                 const long long* __restrict__ Cg, const double* __restrict__ A1g,
-                                                 const double* __restrict__ Q2log, const double* __restrict__ Q2hig,
-                                                 const BucketScan* __restrict__ bsc, int mode,
-                                                 const double* __restrict__ best_ub, const long long* __restrict__ crange,
-                                                 double* __restrict__ ub_part, long long* __restrict__ range_part) {
-  __shared__ double rd[PT / 32];
-  __shared__ long long ra[PT / 32], rb[PT / 32];
-  const int col = blockIdx.y;
-  const PrunedCol c = pc[col];
+struct LocSmem {  // one column's bucket prefix arrays (the layout of window_bounds' arguments)
+  long long C[NBK + 1];
+  double sb[2 * NBK];          // [lo | hi] bucket sum intervals
+  double A1[2 * (NBK + 1)];    // [lo | hi] prefix sums of the bucket sums
+  double Q2lo[NBK + 1], Q2hi[NBK + 1];
+};
+static constexpr int LOC_SMEM = (int)sizeof(LocSmem);
+
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, Op op, T* red) {
+  for (int d = 16; d > 0; d >>= 1) v = op(v, __shfl_down_sync(0xffffffffu, v, d));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = red[0];
+  for (int k = 1; k < LT / 32; k++) v = op(v, red[k]);
+  return v;
+}
+
+// 3. one CTA per column, the column's prefix arrays in shared memory:
+//    a. prefix arrays over buckets (scan_column);
+//    b. the smallest upper bound of h*SQ(s) over a strided subset of starts (any subset bounds the minimum);
+//    c. chunk lower bounds over all starts, one per maximal run of starts with the same start and end
+//       buckets -> the range of starts whose chunk may hold the minimum;
+//    d. per-start lower bounds inside that range -> the candidate range [smin, smax];
+//    e. the gathered bucket ranges of the candidate window ends (k_pr_gather).
+__global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, PrunedCol* __restrict__ pc,
+                                                  const int* __restrict__ cnt, const unsigned long long* __restrict__ tq,
+                                                  const double* __restrict__ esum,
+                                                  const unsigned long long* __restrict__ mm) {
+  extern __shared__ __align__(16) unsigned char loc_raw[];
+  LocSmem& S = *reinterpret_cast<LocSmem*>(loc_raw);
+  __shared__ BucketScan bs;
+  __shared__ double redd[LT / 32];
+  __shared__ long long redl[LT / 32];
+  const int col = blockIdx.x;
+  PrunedCol c = pc[col];
   if (c.status) return;
-  const long long* C = Cg + (long long)col * (NBK + 1);
-  const double* A1 = A1g + (long long)col * 2 * (NBK + 1);  // [lo | hi] prefix sums of bucket sums
-  const double* Q2lo = Q2log + (long long)col * (NBK + 1);
-  const double* Q2hi = Q2hig + (long long)col * (NBK + 1);
-  const int* cn = cnt + (long long)col * NBK;
-  const double* sbk = sbg + (long long)col * 2 * NBK;       // [lo | hi] bucket sums
-  const BucketScan m = bsc[col];
+  c.cmin = ord_val(mm[2 * col]);
+  c.cmax = ord_val(mm[2 * col + 1]);
+  scan_column(c, cnt + (long long)col * NBK, tq + (long long)col * NBK, esum + 4 * col, S.C, S.sb, S.A1, S.Q2lo,
+              S.Q2hi, bs);
+  const long long* C = S.C;
+  const BucketScan m = bs;
   const long long nwin = len - h + 1;
-  const long long gtid = (long long)blockIdx.x * PT + threadIdx.x;
-  const long long nthreads = (long long)gridDim.x * PT;
-  const double bub = mode ? best_ub[col] : 0.0;
+  const int t = threadIdx.x;
+
+  // b. the smallest upper bound over two strided sets of starts: UB1 starts across all of [0, nwin),
+  //    then UB2 starts at 1/16 of that spacing around the best of them (any subset of starts gives a
+  //    valid upper bound on the minimum; the second set makes it as tight near the optimum as a
+  //    16x denser global sampling)
+  __shared__ double bestv[LT / 32];
+  __shared__ long long bests[LT / 32];
+  __shared__ long long s_centre;
+  const long long stride1 = std::max<long long>(1, (nwin + UB1 - 1) / UB1);
   double ub = INFINITY;
-  long long cmin = 0x7fffffffffffffffLL, cmax = -1;
-  // modes 0 and 1: every thread takes a contiguous range of sampled starts / chunks, finds the
-  // start and end buckets once by binary search and then only walks them forward
-  const long long nchunks = (nwin + CHUNK - 1) / CHUNK;
-  const long long cper = (nchunks + nthreads - 1) / nthreads;
-  const long long ch0 = gtid * cper, ch1 = min(nchunks, ch0 + cper);
-  if (mode == 0) {
-    if (ch0 < ch1) {
-      int b = rank_bucket(C, ch0 * CHUNK), be = rank_bucket(C, ch0 * CHUNK + h - 1);
-      for (long long ch = ch0; ch < ch1; ch++) {
-        const long long s = ch * CHUNK;
-        while (C[b + 1] <= s) b++;
-        while (C[be + 1] <= s + h - 1) be++;
-        ub = fmin(ub, window_bounds(s, h, b, be, c, C, A1, Q2lo, Q2hi, cn, sbk, m).hi);
-      }
+  long long ubs = 0;
+  for (long long k = t; k * stride1 < nwin; k += LT) {
+    const long long s = k * stride1;
+    const double v = window_bounds(s, h, rank_bucket(C, s), rank_bucket(C, s + h - 1), c, C, S.A1, S.Q2lo, S.Q2hi,
+                                   S.sb, m).hi;
+    if (v < ub) {
+      ub = v;
+      ubs = s;
     }
-  } else if (mode == 1) {
-    // the thread's contiguous range of starts, cut only where the start bucket or the end bucket
-    // changes: one lower bound per maximal (b, be) segment (about 2 NBK segments per column)
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    const double ov = __shfl_down_sync(0xffffffffu, ub, d);
+    const long long os = __shfl_down_sync(0xffffffffu, ubs, d);
+    if (ov < ub || (ov == ub && os < ubs)) {
+      ub = ov;
+      ubs = os;
+    }
+  }
+  if ((t & 31) == 0) {
+    bestv[t >> 5] = ub;
+    bests[t >> 5] = ubs;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double v = bestv[0];
+    long long sc = bests[0];
+    for (int k = 1; k < LT / 32; k++)
+      if (bestv[k] < v) {
+        v = bestv[k];
+        sc = bests[k];
+      }
+    s_centre = sc;
+  }
+  __syncthreads();
+  {
+    const long long stride2 = std::max<long long>(1, stride1 / 16);
+    const long long s = s_centre + ((long long)t - LT / 2) * stride2;
+    if (s >= 0 && s < nwin)
+      ub = fmin(ub, window_bounds(s, h, rank_bucket(C, s), rank_bucket(C, s + h - 1), c, C, S.A1, S.Q2lo, S.Q2hi,
+                                  S.sb, m).hi);
+  }
+  const double bub = block_reduce(ub, [](double x, double y) { return fmin(x, y); }, redd);
+
+  // c. interval lower bounds over all starts: the thread's contiguous range of starts, cut where the
+  //    start or end bucket changes and at multiples of CHUNK (the bound of a piece of a run is
+  //    tighter than that of the whole run); the run's constants are computed once per run
+  long long cmin = 0x7fffffffffffffffLL, cmax = -1;
+  {
+    const long long nchunks = (nwin + CHUNK - 1) / CHUNK;
+    const long long per = (nchunks + LT - 1) / LT, ch0 = t * per, ch1 = min(nchunks, ch0 + per);
     if (ch0 < ch1) {
       const long long s1e = min(nwin, ch1 * CHUNK);
       long long sa = ch0 * CHUNK;
@@ -550,151 +634,177 @@ __global__ void __launch_bounds__(PT) k_pr_bound(long long len, long long h, con
       while (sa < s1e) {
         while (C[b + 1] <= sa) b++;
         while (C[be + 1] <= sa + h - 1) be++;
-        const long long sb = min(min(s1e, C[b + 1]), C[be + 1] - h + 1) - 1;  // same (b, be) on [sa, sb]
-        const double lo = (b == be) ? -INFINITY : chunk_lower(sa, sb, h, b, be, c, C, A1, Q2lo, cn, sbk, m);
-        if (lo <= bub) {
+        const long long re = min(min(s1e, C[b + 1]), C[be + 1] - h + 1) - 1;  // same (b, be) on [sa, re]
+        if (b == be) {
           cmin = min(cmin, sa);
-          cmax = max(cmax, sb);
+          cmax = max(cmax, re);
+        } else {
+          const RunConst rc = run_const(b, be, c, C, S.A1, S.Q2lo, S.Q2hi, S.sb);
+          for (long long pa = sa; pa <= re;) {
+            const long long pb = min(re, (pa / CHUNK + 1) * CHUNK - 1);
+            if (chunk_lower(rc, pa, pb, h, m) <= bub) {
+              cmin = min(cmin, pa);
+              cmax = max(cmax, pb);
+            }
+            pa = pb + 1;
+          }
         }
-        sa = sb + 1;
+        sa = re + 1;
       }
     }
-  } else {
-    const long long lo_s = crange[2 * col], hi_s = crange[2 * col + 1];
-    if (lo_s <= hi_s) {
-      const long long cnt_s = hi_s - lo_s + 1;
-      const long long per = (cnt_s + nthreads - 1) / nthreads;
-      const long long s0 = lo_s + gtid * per, s1e = min(hi_s + 1, s0 + per);
-      if (s0 < s1e) {
-        int b = rank_bucket(C, s0), be = rank_bucket(C, s0 + h - 1);
-        for (long long s = s0; s < s1e; s++) {
-          while (C[b + 1] <= s) b++;
-          while (C[be + 1] <= s + h - 1) be++;
-          if (window_bounds(s, h, b, be, c, C, A1, Q2lo, Q2hi, cn, sbk, m).lo <= bub) {
+  }
+  const long long lo_s = block_reduce(cmin, [](long long x, long long y) { return min(x, y); }, redl);
+  const long long hi_s = block_reduce(cmax, [](long long x, long long y) { return max(x, y); }, redl);
+
+  // d. per-start lower bounds inside [lo_s, hi_s]: the thread's contiguous range, run by run
+  cmin = 0x7fffffffffffffffLL;
+  cmax = -1;
+  if (lo_s <= hi_s) {
+    const long long cnt_s = hi_s - lo_s + 1;
+    const long long per = (cnt_s + LT - 1) / LT;
+    long long sa = lo_s + t * per;
+    const long long s1e = min(hi_s + 1, sa + per);
+    if (sa < s1e) {
+      int b = rank_bucket(C, sa), be = rank_bucket(C, sa + h - 1);
+      while (sa < s1e) {
+        while (C[b + 1] <= sa) b++;
+        while (C[be + 1] <= sa + h - 1) be++;
+        const long long sb = min(min(s1e, C[b + 1]), C[be + 1] - h + 1) - 1;  // same (b, be) on [sa, sb]
+        const RunConst rc = run_const(b, be, c, C, S.A1, S.Q2lo, S.Q2hi, S.sb);
+        for (long long s = sa; s <= sb; s++)
+          if (start_bounds(rc, s, h, m).lo <= bub) {
             cmin = min(cmin, s);
             cmax = max(cmax, s);
           }
-        }
+        sa = sb + 1;
       }
     }
   }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (mode == 0) {
-    for (int d = 16; d > 0; d >>= 1) ub = fmin(ub, __shfl_down_sync(0xffffffffu, ub, d));
-    if (lane == 0) rd[w] = ub;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int k = 1; k < PT / 32; k++) ub = fmin(ub, rd[k]);
-      ub_part[(long long)col * gridDim.x + blockIdx.x] = ub;
-    }
-  } else {
-    for (int d = 16; d > 0; d >>= 1) {
-      cmin = min(cmin, __shfl_down_sync(0xffffffffu, cmin, d));
-      cmax = max(cmax, __shfl_down_sync(0xffffffffu, cmax, d));
-    }
-    if (lane == 0) {
-      ra[w] = cmin;
-      rb[w] = cmax;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int k = 1; k < PT / 32; k++) {
-        cmin = min(cmin, ra[k]);
-        cmax = max(cmax, rb[k]);
-      }
-      range_part[((long long)col * gridDim.x + blockIdx.x) * 2] = cmin;
-      range_part[((long long)col * gridDim.x + blockIdx.x) * 2 + 1] = cmax;
-    }
-  }
-}
+  const long long smin = block_reduce(cmin, [](long long x, long long y) { return min(x, y); }, redl);
+  const long long smax = block_reduce(cmax, [](long long x, long long y) { return max(x, y); }, redl);
 
-__global__ void k_pr_ubmin(const PrunedCol* __restrict__ pc, const double* __restrict__ ub_part, int nb,
-                           double* __restrict__ best_ub) {
-  const int col = blockIdx.x;
-  if (pc[col].status || threadIdx.x != 0) return;
-  double ub = INFINITY;
-  for (int k = 0; k < nb; k++) ub = fmin(ub, ub_part[(long long)col * nb + k]);
-  best_ub[col] = ub;
-}
-
-__global__ void k_pr_range(const PrunedCol* __restrict__ pc, const long long* __restrict__ range_part, int nb,
-                           long long* __restrict__ crange) {
-  const int col = blockIdx.x;
-  if (pc[col].status || threadIdx.x != 0) return;
-  long long smin = 0x7fffffffffffffffLL, smax = -1;
-  for (int k = 0; k < nb; k++) {
-    smin = min(smin, range_part[((long long)col * nb + k) * 2]);
-    smax = max(smax, range_part[((long long)col * nb + k) * 2 + 1]);
+  // e. gathered bucket ranges
+  if (t == 0) {
+    c.smin = smin;
+    c.smax = smax;
+    c.rmin = lo_s;
+    c.rmax = hi_s;
+    if (smax < smin) {
+      c.status = 1;
+    } else {
+      c.bs_lo = rank_bucket(C, smin);
+      c.bs_hi = rank_bucket(C, smax);
+      c.be_lo = rank_bucket(C, smin + h);
+      c.be_hi = rank_bucket(C, min(smax + h, len - 1));
+      c.cs_lo = C[c.bs_lo];
+      c.ce_lo = C[c.be_lo];
+      const long long ns = C[c.bs_hi + 1] - C[c.bs_lo], ne = C[c.be_hi + 1] - C[c.be_lo];
+      if (ns > CAP || ne > CAP) c.status = 1;
+      c.tS0 = bucket_threshold(c.bs_lo, c);
+      c.tS1 = bucket_threshold(c.bs_hi + 1, c);
+      c.tE0 = bucket_threshold(c.be_lo, c);
+      c.tE1 = bucket_threshold(c.be_hi + 1, c);
+    }
+    pc[col] = c;
   }
-  crange[2 * col] = smin;
-  crange[2 * col + 1] = smax;
-}
-
-// 3c. candidate range -> gathered bucket ranges
-__global__ void k_pr_cand(long long len, long long h, PrunedCol* __restrict__ pc, const long long* __restrict__ Cg,
-                          const long long* __restrict__ crange) {
-  const int col = blockIdx.x;
-  PrunedCol c = pc[col];
-  if (c.status || threadIdx.x != 0) return;
-  const long long* C = Cg + (long long)col * (NBK + 1);
-  const long long smin = crange[2 * col], smax = crange[2 * col + 1];
-  c.smin = smin;
-  c.smax = smax;
-  if (smax < smin) {
-    c.status = 1;
-  } else {
-    c.bs_lo = rank_bucket(C, smin);
-    c.bs_hi = rank_bucket(C, smax);
-    c.be_lo = rank_bucket(C, smin + h);
-    c.be_hi = rank_bucket(C, min(smax + h, len - 1));
-    c.cs_lo = C[c.bs_lo];
-    c.ce_lo = C[c.be_lo];
-    const long long ns = C[c.bs_hi + 1] - C[c.bs_lo], ne = C[c.be_hi + 1] - C[c.be_lo];
-    if (ns > CAP || ne > CAP) c.status = 1;
-  }
-  pc[col] = c;
 }
 
 // 4. gather candidate-end elements and sum, in double-double, the elements strictly between the
 //    two gathered bucket ranges' lower ends: K = sum over buckets [bs_lo, be_lo).  The window sum of
 //    start s is then K + (first s + h - ce_lo sorted E elements) - (first s - cs_lo sorted S elements):
 //    every window sum shares the same K, so elements below bs_lo never need to be summed.
+static constexpr int GST = 3;  // k_pr_gather: cp.async stages of ILP elements per thread in flight
+static constexpr int GBUF = 1024;  // k_pr_gather: per-CTA shared buffer of gathered elements per side
+
 __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ cols, long long len,
                                                   const PrunedCol* __restrict__ pc, double* __restrict__ g,
                                                   int* __restrict__ gcount, dd2* __restrict__ below) {
   __shared__ dd2 sm[33];
+  __shared__ double sbuf[2][GBUF];  // this CTA's gathered elements, flushed with one global atomic per side
+  __shared__ int scnt[2], sbase[2];
+  extern __shared__ double gbuf[];  // [GST][ILP][PT]: each thread reads back only what it copied
   const int col = blockIdx.y;
   const PrunedCol c = pc[col];
   if (c.status) return;
   const double* y = cols + (long long)col * len;
   double* S = g + (long long)(2 * col) * CAP;
   double* E = g + (long long)(2 * col + 1) * CAP;
-  ddacc acc = ddacc_zero();
+  constexpr int NACC = 4;  // independent accumulators: the two-sum chains of successive elements overlap
+  ddacc acc[NACC];
+#pragma unroll
+  for (int q = 0; q < NACC; q++) acc[q] = ddacc_zero();
   const long long per = (len + PCTA - 1) / PCTA;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
-  for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
-    double v[ILP];
+  const unsigned lane = threadIdx.x & 31, lt_mask = (1u << lane) - 1u;
+  if (threadIdx.x < 2) scnt[threadIdx.x] = 0;
+  __syncthreads();
+  const long long nb = (i1 - i0 + (long long)PT * ILP - 1) / ((long long)PT * ILP);  // warp-uniform trip count
+  auto issue = [&](long long it) {
+    if (it < nb) {
+      double* dst = gbuf + (it % GST) * ILP * PT + threadIdx.x;
+      const long long base = i0 + it * (long long)PT * ILP + threadIdx.x;
 #pragma unroll
-    for (int k = 0; k < ILP; k++) {
-      const long long i = base + (long long)k * PT;
-      v[k] = i < i1 ? __ldg(y + i) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < ILP; k++) {
-      if (base + (long long)k * PT >= i1) continue;
-      const int b = bucket_of(v[k], c);
-      if (b >= c.bs_lo && b < c.be_lo) ddacc_add(acc, v[k]);
-      if (b >= c.bs_lo && b <= c.bs_hi) {
-        const int pos = atomicAdd(&gcount[2 * col], 1);
-        if (pos < CAP) S[pos] = v[k];
+      for (int k = 0; k < ILP; k++) {
+        const long long i = base + (long long)k * PT;
+        if (i < i1) cp_async8(dst + k * PT, y + i);
       }
-      if (b >= c.be_lo && b <= c.be_hi) {
-        const int pos = atomicAdd(&gcount[2 * col + 1], 1);
-        if (pos < CAP) E[pos] = v[k];
+    }
+    cp_async_commit();  // (possibly empty) group: keeps the wait count uniform
+  };
+#pragma unroll
+  for (int st = 0; st < GST - 1; st++) issue(st);
+  for (long long it = 0; it < nb; it++) {
+    issue(it + GST - 1);
+    cp_async_wait<GST - 1>();
+    const double* src = gbuf + (it % GST) * ILP * PT + threadIdx.x;
+    const long long base = i0 + it * (long long)PT * ILP + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < ILP; k++) {
+      const bool ok = base + (long long)k * PT < i1;
+      // bucket ranges by value thresholds: bucket_of(y) in [b0, b1) <=> T(b0) <= y < T(b1)
+      const double x = ok ? src[k * PT] : 0.0;
+      const bool geS = x >= c.tS0, geE = x >= c.tE0;
+      ddacc_add(acc[k % NACC], (ok && geS && !geE) ? x : 0.0);  // [bs_lo, be_lo); branch-free: adding 0 is exact
+      const bool inS = ok && geS && x < c.tS1, inE = ok && geE && x < c.tE1;
+      const unsigned ms = __ballot_sync(0xffffffffu, inS), me = __ballot_sync(0xffffffffu, inE);
+#pragma unroll
+      for (int side = 0; side < 2; side++) {  // one shared atomic per warp and side
+        const unsigned mm = side ? me : ms;
+        if (mm) {
+          const bool mine = side ? inE : inS;
+          int pos = 0;
+          if (lane == (unsigned)(__ffs(mm) - 1)) pos = atomicAdd(&scnt[side], __popc(mm));
+          pos = __shfl_sync(0xffffffffu, pos, __ffs(mm) - 1) + __popc(mm & lt_mask);
+          if (mine) {
+            if (pos < GBUF) {
+              sbuf[side][pos] = x;
+            } else {  // CTA buffer full: straight to global memory
+              const int gp = atomicAdd(&gcount[2 * col + side], 1);
+              if (gp < CAP) (side ? E : S)[gp] = x;
+            }
+          }
+        }
       }
     }
   }
-  dd2 te = block_sum_dd2(ddacc_dd2(acc), sm);
+  cp_async_wait<0>();
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    const int n = min(scnt[threadIdx.x], GBUF);
+    sbase[threadIdx.x] = n ? atomicAdd(&gcount[2 * col + threadIdx.x], n) : 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    const int n = min(scnt[side], GBUF), b0 = sbase[side];
+    double* dst = side ? E : S;
+    for (int i = threadIdx.x; i < n; i += PT)
+      if (b0 + i < CAP) dst[b0 + i] = sbuf[side][i];
+  }
+  dd2 tacc = ddacc_dd2(acc[0]);
+#pragma unroll
+  for (int q = 1; q < NACC; q++) tacc = dd2_add(tacc, ddacc_dd2(acc[q]));
+  dd2 te = block_sum_dd2(tacc, sm);
   if (threadIdx.x == 0) {
     below[((long long)col * PCTA + blockIdx.x) * 2] = dd2_zero();
     below[((long long)col * PCTA + blockIdx.x) * 2 + 1] = te;
@@ -919,7 +1029,6 @@ struct PrScratch {
   int* cnt;
   unsigned long long* tq;  // fixed-point offset sums per bucket
   double* esum;            // under- / overflow bucket sums and sums of magnitudes [col][4]
-  double* sbb;             // [col][lo | hi] bucket sum intervals
   unsigned long long* mm;
   double *g, *gsorted;
   int* gcount;
@@ -932,12 +1041,6 @@ struct PrScratch {
   void* cub_tmp;
   size_t cub_bytes;
   int nch;
-  long long* C;
-  double *A1, *Q2lo, *Q2hi, *ub_part, *best_ub;
-  BucketScan* bsc;
-  long long* range_part;
-  long long* crange;
-  int nbound;
 };
 
 static size_t seg_sort_bytes(int nseg) {
@@ -952,7 +1055,6 @@ static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.cnt = A.take<int>((size_t)ncols * NBK);
   s.tq = A.take<unsigned long long>((size_t)ncols * NBK);
   s.esum = A.take<double>((size_t)ncols * 4);
-  s.sbb = A.take<double>((size_t)ncols * 2 * NBK);
   s.mm = A.take<unsigned long long>(2 * (size_t)ncols);
   s.g = A.take<double>((size_t)2 * ncols * CAP);
   s.gsorted = A.take<double>((size_t)2 * ncols * CAP);
@@ -967,16 +1069,6 @@ static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.kcnt = A.take<long long>((size_t)ncols * PCTA);
   s.cub_bytes = seg_sort_bytes(2 * ncols);
   s.cub_tmp = A.take<char>(s.cub_bytes);
-  s.C = A.take<long long>((size_t)ncols * (NBK + 1));
-  s.A1 = A.take<double>((size_t)ncols * 2 * (NBK + 1));
-  s.Q2lo = A.take<double>((size_t)ncols * (NBK + 1));
-  s.Q2hi = A.take<double>((size_t)ncols * (NBK + 1));
-  s.bsc = A.take<BucketScan>(ncols);
-  s.nbound = std::max(1, 148 * 8 / ncols);
-  s.ub_part = A.take<double>((size_t)ncols * s.nbound);
-  s.best_ub = A.take<double>(ncols);
-  s.range_part = A.take<long long>((size_t)ncols * s.nbound * 2);
-  s.crange = A.take<long long>((size_t)ncols * 2);
 }
 
 // Returns true when every column was resolved by the pruned path (out_dev filled);
@@ -998,19 +1090,19 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   const unsigned gx = (unsigned)std::max<long long>(1, (len + 65535) / 65536);  // <= 65536 elements per CTA
   k_pr_hist<<<dim3(gx, ncols), PT, 0, st>>>(cols, len, s.pc, s.cnt, s.tq, s.esum, s.mm);
   RTD_LAUNCHED();
-  k_pr_scan<<<ncols, 1024, 0, st>>>(s.pc, s.cnt, s.tq, s.esum, s.mm, s.C, s.A1, s.Q2lo, s.Q2hi, s.sbb, s.bsc);
+  static const bool loc_attr = [] {
+    RTD_CU(cudaFuncSetAttribute(k_pr_locate, cudaFuncAttributeMaxDynamicSharedMemorySize, LOC_SMEM));
+    return true;
+  }();
+  (void)loc_attr;
+  k_pr_locate<<<ncols, LT, LOC_SMEM, st>>>(len, h, s.pc, s.cnt, s.tq, s.esum, s.mm);
   RTD_LAUNCHED();
-  for (int mode = 0; mode < 3; mode++) {
-    k_pr_bound<<<dim3(s.nbound, ncols), PT, 0, st>>>(len, h, s.pc, s.cnt, s.sbb, s.C, s.A1, s.Q2lo, s.Q2hi, s.bsc,
-                                                      mode, s.best_ub, s.crange, s.ub_part, s.range_part);
-    RTD_LAUNCHED();
-    if (mode == 0) k_pr_ubmin<<<ncols, 32, 0, st>>>(s.pc, s.ub_part, s.nbound, s.best_ub);
-    else k_pr_range<<<ncols, 32, 0, st>>>(s.pc, s.range_part, s.nbound, s.crange);
-    RTD_LAUNCHED();
-  }
-  k_pr_cand<<<ncols, 32, 0, st>>>(len, h, s.pc, s.C, s.crange);
-  RTD_LAUNCHED();
-  k_pr_gather<<<dim3(PCTA, ncols), PT, 0, st>>>(cols, len, s.pc, s.g, s.gcount, s.below);
+  static const int gsmem = [] {
+    const int b = GST * ILP * PT * (int)sizeof(double);
+    RTD_CU(cudaFuncSetAttribute(k_pr_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    return b;
+  }();
+  k_pr_gather<<<dim3(PCTA, ncols), PT, gsmem, st>>>(cols, len, s.pc, s.g, s.gcount, s.below);
   RTD_LAUNCHED();
   std::vector<PrunedCol> hc(ncols);
   std::vector<int> gc(2 * ncols);
@@ -1018,9 +1110,9 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   static const bool dbg = getenv("RTD_DEBUG_PRUNED") != nullptr;
   if (dbg) {
     for (int j = 0; j < ncols; j++)
-      fprintf(stderr, "pruned len=%lld col=%d status=%d s=[%lld,%lld] bs=[%d,%d] be=[%d,%d] span=%g\n", len, j,
-              hc[j].status, hc[j].smin, hc[j].smax, hc[j].bs_lo, hc[j].bs_hi, hc[j].be_lo, hc[j].be_hi,
-              hc[j].hi - hc[j].lo);
+      fprintf(stderr, "pruned len=%lld col=%d status=%d r=[%lld,%lld] s=[%lld,%lld] bs=[%d,%d] be=[%d,%d] span=%g g=%d,%d\n",
+              len, j, hc[j].status, hc[j].rmin, hc[j].rmax, hc[j].smin, hc[j].smax, hc[j].bs_lo, hc[j].bs_hi,
+              hc[j].be_lo, hc[j].be_hi, hc[j].hi - hc[j].lo, gc[2 * j], gc[2 * j + 1]);
   }
   for (int j = 0; j < ncols; j++)
     if (hc[j].status) return false;
