@@ -519,7 +519,7 @@ struct RefineBufs {
 void carve_refine(Arena& A, RefineBufs& r, long long m, int p, int cap) {
   r.cap = cap;
   const int tot = cap * p;
-  const int calls = (tot + 255) / 256;
+  const int calls = (tot + 1023) / 1024;  // the pruned path takes any number of columns per call
   r.ucols = (tot + calls - 1) / calls;
   r.T = A.take<double>((size_t)cap * p * m);
   r.V = A.take<double>((size_t)cap * M2);

@@ -517,6 +517,8 @@ static int id_bits(int ncols) {
 // All ncols columns are sorted with two device-wide radix sorts instead of
 // ncols small ones: (value -> column id) by the fp64 key, then a stable sort
 // by column id, which leaves every column sorted and contiguous.
+static constexpr int USORT = 256;  // columns per pass of the sort path (8-bit segment ids)
+
 static size_t cub_sort_bytes(long long len, int ncols) {
   const long long N = len * ncols;
   size_t b1 = 0, b2 = 0;
@@ -547,25 +549,26 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
     RTD_LAUNCHED();
     return;
   }
-  if (ncols > 256) throw std::string("unimcd_batch: at most 256 columns per call");
   const long long h = len / 2 + 1;
   const int nchunks = (int)((len + UCH - 1) / UCH);
   const long long nwin = len - h + 1;
   const int nwchunks = (int)((nwin + UCH - 1) / UCH);
-  const long long N = len * ncols;
+  // the sort path takes at most USORT columns per pass (8-bit column ids in the segmented sort)
+  const int sc = std::min(ncols, USORT);
+  const long long N = len * sc;
   UniScratch s;
   s.sorted = A.take<double>((size_t)N);
-  s.tmpk = ncols > 1 ? A.take<double>((size_t)N) : nullptr;
-  s.ids = ncols > 1 ? A.take<uint8_t>((size_t)N) : nullptr;
-  s.tmpid = ncols > 1 ? A.take<uint8_t>((size_t)N) : nullptr;
-  s.idout = ncols > 1 ? A.take<uint8_t>((size_t)N) : nullptr;
-  s.csum = A.take<dd2>((size_t)ncols * nchunks);
-  s.coff = A.take<dd2>((size_t)ncols * (nchunks + 1));
-  s.part = A.take<WinPartial>((size_t)ncols * nwchunks);
-  s.cub_bytes = cub_sort_bytes(len, ncols);
+  s.tmpk = sc > 1 ? A.take<double>((size_t)N) : nullptr;
+  s.ids = sc > 1 ? A.take<uint8_t>((size_t)N) : nullptr;
+  s.tmpid = sc > 1 ? A.take<uint8_t>((size_t)N) : nullptr;
+  s.idout = sc > 1 ? A.take<uint8_t>((size_t)N) : nullptr;
+  s.csum = A.take<dd2>((size_t)sc * nchunks);
+  s.coff = A.take<dd2>((size_t)sc * (nchunks + 1));
+  s.part = A.take<WinPartial>((size_t)sc * nwchunks);
+  s.cub_bytes = cub_sort_bytes(len, sc);
   s.cub_tmp = A.take<char>(s.cub_bytes);
-  // Large columns: exact window by bucketing + bounds (k_unimcd_pruned.cu); the
-  // sort path below is the fallback and the small-n path.
+  // Large columns: exact window by bucketing + bounds (k_unimcd_pruned.cu), every column in one pass;
+  // the sort path below is the fallback and the small-n path.
   static const bool force_sort = getenv("RTD_UNI_FULLSORT") != nullptr;
   if (len >= (1LL << 16) && !force_sort) {  // below: the two radix sorts measured faster (config 5)
     const bool done = unimcd_pruned(A, st, cols, len, ncols, uc, out_dev);
@@ -573,28 +576,33 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
     if (done) return;
   }
   if (A.base == nullptr) return;  // dry run
-  size_t bytes = s.cub_bytes;
-  if (ncols == 1) {
-    count_sort();
-    RTD_CU(cub::DeviceRadixSort::SortKeys(s.cub_tmp, bytes, cols, s.sorted, (int)N, 0, 64, st));
-  } else {
-    k_fill_colid<<<(unsigned)std::min<long long>((N + 255) / 256, 148 * 16), 256, 0, st>>>(s.ids, len, N);
+  for (int c0 = 0; c0 < ncols; c0 += USORT) {
+    const int nc = std::min(USORT, ncols - c0);
+    const double* cc = cols + (long long)c0 * len;
+    const long long Nc = len * nc;
+    size_t bytes = s.cub_bytes;
+    if (nc == 1) {
+      count_sort();
+      RTD_CU(cub::DeviceRadixSort::SortKeys(s.cub_tmp, bytes, cc, s.sorted, (int)Nc, 0, 64, st));
+    } else {
+      k_fill_colid<<<(unsigned)std::min<long long>((Nc + 255) / 256, 148 * 16), 256, 0, st>>>(s.ids, len, Nc);
+      RTD_LAUNCHED();
+      count_sort();
+      RTD_CU(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, cc, s.tmpk, s.ids, s.tmpid, (int)Nc, 0, 64, st));
+      bytes = s.cub_bytes;
+      count_sort();
+      RTD_CU(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.tmpid, s.idout, s.tmpk, s.sorted, (int)Nc, 0,
+                                             id_bits(nc), st));
+    }
+    k_uni_chunksum<<<dim3(nchunks, nc), UTH, 0, st>>>(s.sorted, len, nchunks, s.csum);
     RTD_LAUNCHED();
-    count_sort();
-    RTD_CU(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, cols, s.tmpk, s.ids, s.tmpid, (int)N, 0, 64, st));
-    bytes = s.cub_bytes;
-    count_sort();
-    RTD_CU(cub::DeviceRadixSort::SortPairs(s.cub_tmp, bytes, s.tmpid, s.idout, s.tmpk, s.sorted, (int)N, 0,
-                                           id_bits(ncols), st));
+    k_uni_chunkscan<<<dim3(1, nc), 1024, 0, st>>>(s.csum, nchunks, s.coff);
+    RTD_LAUNCHED();
+    k_uni_window<<<dim3(nwchunks, nc), UTH, 0, st>>>(s.sorted, len, h, nchunks, s.coff, nwchunks, s.part);
+    RTD_LAUNCHED();
+    k_uni_final<<<nc, UTH, 0, st>>>(s.sorted, len, h, nchunks, s.coff, nwchunks, s.part, uc, out_dev + c0);
+    RTD_LAUNCHED();
   }
-  k_uni_chunksum<<<dim3(nchunks, ncols), UTH, 0, st>>>(s.sorted, len, nchunks, s.csum);
-  RTD_LAUNCHED();
-  k_uni_chunkscan<<<dim3(1, ncols), 1024, 0, st>>>(s.csum, nchunks, s.coff);
-  RTD_LAUNCHED();
-  k_uni_window<<<dim3(nwchunks, ncols), UTH, 0, st>>>(s.sorted, len, h, nchunks, s.coff, nwchunks, s.part);
-  RTD_LAUNCHED();
-  k_uni_final<<<ncols, UTH, 0, st>>>(s.sorted, len, h, nchunks, s.coff, nwchunks, s.part, uc, out_dev);
-  RTD_LAUNCHED();
 }
 
 }  // namespace rtd
