@@ -39,6 +39,7 @@ static constexpr int LT = 512;    // k_pr_locate threads (one CTA per column)
 
 struct PrunedCol {
   double lo, hi, w, inv_w;   // bucket map
+  double inv_w16;            // 2^16 inv_w (exact): fl(fl(y - lo) inv_w16) = 2^16 fl(fl(y - lo) inv_w)
   double cmin, cmax;         // column min / max
   long long smin, smax;      // candidate window starts
   long long rmin, rmax;      // range of starts left by the chunk lower bounds (diagnostics)
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(1024) k_pr_sample(const double* __restrict__ c
     c.hi = qh + 0.05 * span;
     c.w = (c.hi - c.lo) / (double)(NBK - 2);
     c.inv_w = 1.0 / c.w;
+    c.inv_w16 = c.inv_w * 65536.0;
     c.status = (span > 0.0 && isfinite(span) && c.w > 0.0) ? 0 : 1;
     pc[col] = c;
     mm[2 * col] = ~0ull;
@@ -211,22 +213,32 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
 #pragma unroll
     for (int k = 0; k < ILP; k++) {
       if (base + (long long)k * PT < i1) {
-        const int b = bucket_of(v[k], c);
-        atomicAdd(&hc[b], 1u);
-        if (b == 0) {
-          e0 += v[k];
-          a0 += fabs(v[k]);
-        } else if (b == NBK - 1) {
-          e1 += v[k];
-          a1 += fabs(v[k]);
+        // bucket_of and the offset in one product: T = floor(2^16 t), t = fl(fl(y - lo) inv_w), so
+        // b = 1 + floor(t) = 1 + (T >> 16) and q = floor(2^16 frac(t)) = T & 0xffff.  The column min /
+        // max only bound the end buckets' values (bucket_lo(0), bucket_hi(NBK - 1)): tracked there only
+        const double x = v[k];
+        int b;
+        if (x < c.lo) {
+          b = 0;
+          e0 += x;
+          a0 += fabs(x);
+          kmin = min(kmin, ord_key(x));
+        } else if (x >= c.hi) {
+          b = NBK - 1;
+          e1 += x;
+          a1 += fabs(x);
+          kmax = max(kmax, ord_key(x));
         } else {
-          const double tt = __dsub_rn(__dmul_rn(__dsub_rn(v[k], c.lo), c.inv_w), (double)(b - 1));
-          const int q = (int)fmin(fmax(__dmul_rn(tt, 65536.0), 0.0), 65535.0);
-          atomicAdd(&hq[b], (unsigned int)q);
+          const int T = (int)__dmul_rn(__dsub_rn(x, c.lo), c.inv_w16);
+          b = 1 + (T >> 16);
+          unsigned int q = (unsigned int)(T & 0xffff);
+          if (b > NBK - 2) {
+            b = NBK - 2;
+            q = 65535u;
+          }
+          atomicAdd(&hq[b], q);
         }
-        const unsigned long long kk = ord_key(v[k]);
-        kmin = min(kmin, kk);
-        kmax = max(kmax, kk);
+        atomicAdd(&hc[b], 1u);
       }
     }
   }
