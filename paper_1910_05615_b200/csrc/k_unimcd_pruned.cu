@@ -205,14 +205,12 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
   for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
     double v[ILP];
+    const int rem = (int)min(i1 - base, (long long)PT * ILP);  // elements k with k PT < rem are in range
+#pragma unroll
+    for (int k = 0; k < ILP; k++) v[k] = k * PT < rem ? __ldg(y + base + k * PT) : 0.0;
 #pragma unroll
     for (int k = 0; k < ILP; k++) {
-      const long long i = base + (long long)k * PT;
-      v[k] = i < i1 ? __ldg(y + i) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < ILP; k++) {
-      if (base + (long long)k * PT < i1) {
+      if (k * PT < rem) {
         // bucket_of and the offset in one product: T = floor(2^16 t), t = fl(fl(y - lo) inv_w), so
         // b = 1 + floor(t) = 1 + (T >> 16) and q = floor(2^16 frac(t)) = T & 0xffff.  The column min /
         // max only bound the end buckets' values (bucket_lo(0), bucket_hi(NBK - 1)): tracked there only
@@ -759,6 +757,7 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
       for (int k = 0; k < ILP; k++) {
         const long long i = base + (long long)k * PT;
         if (i < i1) cp_async8(dst + k * PT, y + i);
+        else dst[k * PT] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: fails every range test
       }
     }
     cp_async_commit();  // (possibly empty) group: keeps the wait count uniform
@@ -769,15 +768,14 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
     issue(it + GST - 1);
     cp_async_wait<GST - 1>();
     const double* src = gbuf + (it % GST) * ILP * PT + threadIdx.x;
-    const long long base = i0 + it * (long long)PT * ILP + threadIdx.x;
 #pragma unroll
     for (int k = 0; k < ILP; k++) {
-      const bool ok = base + (long long)k * PT < i1;
-      // bucket ranges by value thresholds: bucket_of(y) in [b0, b1) <=> T(b0) <= y < T(b1)
-      const double x = ok ? src[k * PT] : 0.0;
+      // bucket ranges by value thresholds: bucket_of(y) in [b0, b1) <=> T(b0) <= y < T(b1); the
+      // slots past the CTA's range hold NaN, which fails every test
+      const double x = src[k * PT];
       const bool geS = x >= c.tS0, geE = x >= c.tE0;
-      ddacc_add(acc[k % NACC], (ok && geS && !geE) ? x : 0.0);  // [bs_lo, be_lo); branch-free: adding 0 is exact
-      const bool inS = ok && geS && x < c.tS1, inE = ok && geE && x < c.tE1;
+      ddacc_add(acc[k % NACC], (geS && !geE) ? x : 0.0);  // [bs_lo, be_lo); branch-free: adding 0 is exact
+      const bool inS = geS && x < c.tS1, inE = geE && x < c.tE1;
       const unsigned ms = __ballot_sync(0xffffffffu, inS), me = __ballot_sync(0xffffffffu, inE);
 #pragma unroll
       for (int side = 0; side < 2; side++) {  // one shared atomic per warp and side
@@ -983,14 +981,12 @@ __global__ void __launch_bounds__(PT) k_pr_keep(const double* __restrict__ cols,
   long long k = 0;
   for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
     double v[ILP];
+    const int rem = (int)min(i1 - base, (long long)PT * ILP);
+#pragma unroll
+    for (int u = 0; u < ILP; u++) v[u] = u * PT < rem ? __ldg(y + base + u * PT) : 0.0;
 #pragma unroll
     for (int u = 0; u < ILP; u++) {
-      const long long i = base + (long long)u * PT;
-      v[u] = i < i1 ? __ldg(y + i) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < ILP; u++) {
-      if (base + (long long)u * PT >= i1) continue;
+      if (u * PT >= rem) continue;
       const double d = __dsub_rn(v[u], loc0);
       if (__dmul_rn(d, d) <= thresh) {
         ddacc_add_dev(acc, v[u], d);
