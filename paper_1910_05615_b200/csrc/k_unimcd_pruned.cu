@@ -528,6 +528,36 @@ __device__ __forceinline__ double chunk_lower(const RunConst& r, long long sa, l
   return hd * lo2 - sq_hi_1 - slack;
 }
 
+// Coarse lower bound of h*SQ(s) valid for every start s in [sa, sb], whose start buckets lie in
+// [ba, bb] and end buckets in [ea, eb] (bb < ea): the window holds every element of buckets
+// bb+1 .. ea-1, r1 = C[bb+1] - s elements with values in [L(ba), U(bb)] and r2 = h - r1 - n_mid
+// elements with values in [L(ea), U(eb)]; all terms are linear in r1, so the endpoints bound them.
+__device__ __forceinline__ double group_lower(long long sa, long long sb, long long h, int ba, int bb, int ea, int eb,
+                                              const PrunedCol& c, const long long* C, const double* A1,
+                                              const double* Q2lo, BucketScan m) {
+  const double hd = (double)h;
+  const double L1 = bucket_lo(ba, c), U1 = bucket_hi(bb, c), L2 = bucket_lo(ea, c), U2 = bucket_hi(eb, c);
+  const double mn1 = (L1 <= 0 && U1 >= 0) ? 0.0 : fmin(L1 * L1, U1 * U1);
+  const double mn2 = (L2 <= 0 && U2 >= 0) ? 0.0 : fmin(L2 * L2, U2 * U2);
+  const double nmid = (double)(C[ea] - C[bb + 1]);
+  const double F1lo = A1[ea] - A1[bb + 1], F1hi = A1[NBK + 1 + ea] - A1[NBK + 1 + bb + 1];
+  const double Q2l = Q2lo[ea] - Q2lo[bb + 1];
+  double lo1 = INFINITY, hi1 = -INFINITY, lo2 = INFINITY;
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    const double r1 = (double)(C[bb + 1] - (k ? sb : sa)), r2 = hd - r1 - nmid;
+    lo1 = fmin(lo1, F1lo + r1 * L1 + r2 * L2);
+    hi1 = fmax(hi1, F1hi + r1 * U1 + r2 * U2);
+    lo2 = fmin(lo2, Q2l + r1 * mn1 + r2 * mn2);
+  }
+  lo1 -= m.E1;
+  hi1 += m.E1;
+  lo2 -= m.E2;
+  const double sq_hi_1 = fmax(lo1 * lo1, hi1 * hi1);
+  const double slack = 1e-9 * (hd * fabs(lo2) + sq_hi_1) + 1e-300;
+  return hd * lo2 - sq_hi_1 - slack;
+}
+
 static constexpr int CHUNK = 64;      // starts per piece in the interval lower-bound pass
 static constexpr int UB1 = 4096;      // strided starts of the first upper-bound sample (the second is LT)
 
@@ -630,16 +660,38 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
   }
   const double bub = block_reduce(ub, [](double x, double y) { return fmin(x, y); }, redd);
 
-  // c. interval lower bounds over all starts: the thread's contiguous range of starts, cut where the
-  //    start or end bucket changes and at multiples of CHUNK (the bound of a piece of a run is
-  //    tighter than that of the whole run); the run's constants are computed once per run
-  long long cmin = 0x7fffffffffffffffLL, cmax = -1;
+  // c. interval lower bounds over all starts, in two levels: (c0) one coarse bound per group of
+  //    NBK / LT start buckets (thread t: group t); (c1) the groups it does not exclude go round-robin
+  //    to the warps, whose lanes split the group's starts and bound every piece of at most CHUNK
+  //    starts of every run (same start and end bucket) in them, the run's constants once per run
+  constexpr int GB = NBK / LT;
+  __shared__ unsigned smask[LT / 32];
   {
-    const long long nchunks = (nwin + CHUNK - 1) / CHUNK;
-    const long long per = (nchunks + LT - 1) / LT, ch0 = t * per, ch1 = min(nchunks, ch0 + per);
-    if (ch0 < ch1) {
-      const long long s1e = min(nwin, ch1 * CHUNK);
-      long long sa = ch0 * CHUNK;
+    bool surv = false;
+    const long long sa = min(C[t * GB], nwin), sb = min(C[(t + 1) * GB], nwin) - 1;
+    if (sa <= sb) {
+      const int ba = rank_bucket(C, sa), bb = rank_bucket(C, sb);
+      const int ea = rank_bucket(C, sa + h - 1), eb = rank_bucket(C, sb + h - 1);
+      surv = bb >= ea || group_lower(sa, sb, h, ba, bb, ea, eb, c, C, S.A1, S.Q2lo, m) <= bub;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, surv);
+    if ((t & 31) == 0) smask[t >> 5] = bal;
+    __syncthreads();
+  }
+  long long cmin = 0x7fffffffffffffffLL, cmax = -1;
+  int ord = 0;  // ordinal of the surviving group: warp (ord mod LT/32) takes it, its lanes split the starts
+  const int wid = t >> 5, ln = t & 31;
+  for (int w = 0; w < LT / 32; w++) {
+    unsigned mk = smask[w];
+    while (mk) {
+      const int gi = w * 32 + __ffs(mk) - 1;
+      mk &= mk - 1;
+      if ((ord++) % (LT / 32) != wid) continue;
+      const long long ga = min(C[gi * GB], nwin), gb = min(C[(gi + 1) * GB], nwin);  // starts [ga, gb)
+      const long long per = (gb - ga + 31) / 32;
+      long long sa = ga + ln * per;
+      const long long s1e = min(gb, sa + per);
+      if (sa >= s1e) continue;
       int b = rank_bucket(C, sa), be = rank_bucket(C, sa + h - 1);
       while (sa < s1e) {
         while (C[b + 1] <= sa) b++;
