@@ -54,8 +54,11 @@ typedef enum {
 
 enum { RTD_PART_PERMUTE = 0, RTD_PART_CONTIGUOUS = 1 };
 /* C-step distances (the "D" of the paper's Table 1): by the Cholesky factor
- * (§3.4, default) or by the explicit inverse (variant I; needs p >= 8) */
-enum { RTD_DIST_CHOLESKY = 0, RTD_DIST_INVERSE = 1 };
+ * (§3.4, default) or by the explicit inverse (variant I; needs p >= 8), or by the
+ * explicit inverse kept up to date by Sherman-Morrison-Woodbury on the C-steps that interchange
+ * exactly two cases (the inverse and the determinant updated directly; every other
+ * step recomputes them; needs p >= 8) */
+enum { RTD_DIST_CHOLESKY = 0, RTD_DIST_INVERSE = 1, RTD_DIST_SMW = 2 };
 /* consistency factor of the raw scatter: c(alpha) of Croux-Haesbroeck as the text defines it
  * (default) or the median rule -- the h-subset covariance times
  * median_i d_i^2 / chi2_{p,0.5} over the rows of the block -- with which the paper's Table 2 KL
@@ -85,7 +88,7 @@ typedef struct {
   uint64_t seed;         /* key of the random partition */
   int32_t partition;     /* RTD_PART_PERMUTE (keyed Feistel permutation, default) | RTD_PART_CONTIGUOUS */
   int32_t log_transform; /* 1: fit ln(x) (x must be > 0), as in BASELINE config 5 */
-  int32_t distance;      /* RTD_DIST_CHOLESKY (default) | RTD_DIST_INVERSE (ablation variant I) */
+  int32_t distance;      /* RTD_DIST_CHOLESKY (default) | RTD_DIST_INVERSE (ablation variant I) | RTD_DIST_SMW */
   int32_t consistency;   /* RTD_CONS_ALPHA (default) | RTD_CONS_MEDIAN */
 } rtdetmcd_opts;
 

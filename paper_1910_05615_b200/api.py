@@ -144,8 +144,9 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
 
     warm_start=(mu, sigma): rtdetmcd_fit_warm -- the C-steps of every block start from this
     previous fit (X units, after ln when log_transform) instead of the refined initial estimators.
-    distance: RTD_DIST_CHOLESKY (0) | RTD_DIST_INVERSE (1, Table 1 variant I); refresh_every=1 gives the
-    plain-recompute C-steps of variants I / ID.  consistency: RTD_CONS_ALPHA (0) | RTD_CONS_MEDIAN (1).
+    distance: RTD_DIST_CHOLESKY (0) | RTD_DIST_INVERSE (1, Table 1 variant I) | RTD_DIST_SMW (2: the
+    inverse updated by Sherman-Morrison-Woodbury on single-swap C-steps, PAPER.md:715-740);
+    refresh_every=1 gives the plain-recompute C-steps of variants I / ID.  consistency: RTD_CONS_ALPHA (0) | RTD_CONS_MEDIAN (1).
     """
     ptr, keep, is_cuda, dev = _as_f64(X)
     n, p = int(keep.shape[0]), int(keep.shape[1])

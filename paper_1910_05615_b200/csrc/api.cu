@@ -231,6 +231,8 @@ struct CStepBufs {
   SelState* sel;
   unsigned int* hist;
   unsigned int* selcnt;
+  double* sinv;   // [inst][M2] Sigma^-1 of the current operator (RTD_DIST_SMW)
+  int* smw_valid; // [inst] sinv updated by SMW for the next step (RTD_DIST_SMW)
   int* list;      // [inst][m] ordered changed rows per segment (update-based C-step)
   int* seg_cnt;   // [inst][ctas]
   long long seg_len;
@@ -256,6 +258,8 @@ void carve_cstep(Arena& A, CStepBufs& b, int ninst, long long m, int p, int max_
   b.d2 = A.take<double>((size_t)ninst * m);
   b.status = A.take<int>(ninst);
   b.changed = A.take<int>(ninst);
+  b.sinv = A.take<double>((size_t)ninst * M2);
+  b.smw_valid = A.take<int>(ninst);
   b.inst_dev = A.take<int>(ninst + 8);
   b.memA = A.take<uint8_t>((size_t)ninst * m);
   b.memB = A.take<uint8_t>((size_t)ninst * m);
@@ -325,7 +329,10 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
                 int dist_mode = RTD_DIST_CHOLESKY) {
   const int p = b.p;
   const long long m = b.m;
-  const int cstride = p + (dist_mode == RTD_DIST_INVERSE ? p * p : p * (p + 1) / 2);
+  const bool full_inv = dist_mode == RTD_DIST_INVERSE || dist_mode == RTD_DIST_SMW;
+  const bool smw = dist_mode == RTD_DIST_SMW;
+  const int cstride = p + (full_inv ? p * p : p * (p + 1) / 2);
+  if (smw) RTD_CU(cudaMemsetAsync(b.smw_valid, 0, ninst * sizeof(int), st));
   const int np = mom_np(p);
   RTD_CU(cudaMemsetAsync(b.memA, 0, (size_t)ninst * m, st));
   RTD_CU(cudaMemsetAsync(b.memB, 0, (size_t)ninst * m, st));
@@ -365,9 +372,12 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     {
       ProfScope ps("prepare", 0.0);
       launch_prepare(b.inst_dev, na, b.mu, b.sigma, p, kappa_max, b.cstage, cstride, b.logdet, b.cond, b.status,
-                     b.traj, b.traj_stride, step, st, dist_mode == RTD_DIST_INVERSE);
+                     b.traj, b.traj_stride, step, st, full_inv, smw ? b.smw_valid : nullptr);
+      if (smw)
+        launch_smw_stage(b.inst_dev, na, b.mu, b.sigma, p, kappa_max, b.cstage, cstride, b.sinv, b.smw_valid,
+                         b.cond, b.status, st);
     }
-    dist_groups(st, b, Z, blk_stride, nstart, na, cstride, dist_mode);
+    dist_groups(st, b, Z, blk_stride, nstart, na, cstride, full_inv ? RTD_DIST_INVERSE : RTD_DIST_CHOLESKY);
     RTD_CU(cudaMemsetAsync(b.changed, 0, ninst * sizeof(int), st));
     {
       ProfScope ps("select", (double)na * m * 9.0);
@@ -412,6 +422,17 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
       moments(MOM_MEMBER, ma, (int)dense.size(), st);
       launch_mom_reduce(b.partial, (int)dense.size(), b.inst_dev, b.ctas, np, b.sums, 0, st);
       launch_sums_to_cov(b.inst_dev, (int)dense.size(), b.sums, np, b.shift, p, (double)h, 1.0, b.mu, b.sigma, st);
+    }
+    if (smw) {  // single swaps: the inverse and log det by SMW before the moments move to the new subset
+      std::vector<int> sw;
+      for (int i : upd)
+        if (changed[i] == 2) sw.push_back(i);
+      if (!sw.empty()) {
+        h2d(st, b.inst_dev, sw.data(), sw.size() * sizeof(int));
+        ProfScope ps("smw", 0.0);
+        launch_smw_update(b.inst_dev, (int)sw.size(), Z, m, blk_stride, nstart, b.mu, memA, b.list, b.seg_cnt, b.ctas,
+                          b.seg_len, p, h, b.sinv, b.logdet, b.smw_valid, st);
+      }
     }
     if (!upd.empty()) {
       h2d(st, b.inst_dev, upd.data(), upd.size() * sizeof(int));
@@ -761,10 +782,10 @@ Dims make_dims(long long n, int p, const rtdetmcd_opts& o, bool x_host) {
   d.x_host = x_host;
   if (o.max_csteps < 1 || o.max_csteps > 10000) throw Fail{RTD_E_INVALID_ARG, "max_csteps out of range"};
   if (!(o.quantile > 0.0 && o.quantile < 1.0)) throw Fail{RTD_E_INVALID_ARG, "quantile must be in (0,1)"};
-  if (o.distance != RTD_DIST_CHOLESKY && o.distance != RTD_DIST_INVERSE)
-    throw Fail{RTD_E_INVALID_ARG, "distance must be RTD_DIST_CHOLESKY or RTD_DIST_INVERSE"};
-  if (o.distance == RTD_DIST_INVERSE && !dist_mma_supported(p))
-    throw Fail{RTD_E_INVALID_ARG, "distance = RTD_DIST_INVERSE needs 8 <= p <= 40"};
+  if (o.distance != RTD_DIST_CHOLESKY && o.distance != RTD_DIST_INVERSE && o.distance != RTD_DIST_SMW)
+    throw Fail{RTD_E_INVALID_ARG, "distance must be RTD_DIST_CHOLESKY, RTD_DIST_INVERSE or RTD_DIST_SMW"};
+  if (o.distance != RTD_DIST_CHOLESKY && !dist_mma_supported(p))
+    throw Fail{RTD_E_INVALID_ARG, "distance = RTD_DIST_INVERSE / RTD_DIST_SMW needs 8 <= p <= 40"};
   if (o.consistency != RTD_CONS_ALPHA && o.consistency != RTD_CONS_MEDIAN)
     throw Fail{RTD_E_INVALID_ARG, "consistency must be RTD_CONS_ALPHA or RTD_CONS_MEDIAN"};
   if (o.refresh_every < 0) throw Fail{RTD_E_INVALID_ARG, "refresh_every must be >= 0"};

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(LT) k_prepare(const int* __restrict__ inst, co
                                                 double* __restrict__ cstage, int cstride, double* __restrict__ logdet_out,
                                                 double* __restrict__ cond_out, int* __restrict__ status_out,
                                                 double* __restrict__ traj, int traj_stride, int step,
-                                                int full_inverse) {
+                                                int full_inverse, const int* __restrict__ skip) {
   __shared__ double A[RTD_MAXP * LD], L[RTD_MAXP * LD], Li[RTD_MAXP * LD];
   __shared__ double red[RTD_MAXP];
   __shared__ int s_fail;
@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(LT) k_prepare(const int* __restrict__ inst, co
   const int id = inst[slot];
   const int t = threadIdx.x;
   if (status_out && status_out[id] != 0) return;  // instance no longer active
+  if (skip && skip[id]) return;                    // operator already updated (SMW variant)
   const double* sg = sigma_all + (long long)id * RTD_MAXP * RTD_MAXP;
   for (int e = t; e < p * p; e += blockDim.x) A[(e / p) * LD + e % p] = sg[e];
   __syncthreads();
@@ -504,9 +505,160 @@ void launch_csteps_small(const double* Zall, long long m, int p, long long blk_s
 
 void launch_prepare(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p, double kappa_max,
                     double* cstage, int cstride, double* logdet_out, double* cond_out, int* status_out, double* traj,
-                    int traj_stride, int step, cudaStream_t st, int full_inverse) {
+                    int traj_stride, int step, cudaStream_t st, int full_inverse, const int* skip) {
   k_prepare<<<ninst, LT, 0, st>>>(inst, mu_all, sigma_all, p, kappa_max, cstage, cstride, logdet_out, cond_out,
-                                  status_out, traj, traj_stride, step, full_inverse);
+                                  status_out, traj, traj_stride, step, full_inverse, skip);
+  RTD_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ single-swap inverse update (SMW variant)
+// when a C-step interchanges exactly two cases (sum |delta_i| = 2), the inverse of the
+// sscp matrix is updated directly by Sherman-Morrison-Woodbury and the determinant by
+// det(Lambda + delta u v^T) = Delta det(Lambda), Delta = 1 + delta v^T Lambda^-1 u, the cases taken in
+// row order with u = z - mu (mean before the case), v = z - mu' (after), as in the update loop
+// (PAPER.md:685-709).  Sigma = Lambda / (h - 1) has the same h before and after a swap, so
+// Sigma^-1_new = (h - 1) Lambda^-1_new and log det Sigma changes by sum log Delta.
+// sinv_all[id]: Sigma^-1 (row-major p x p) of the operator used by this step's distances; mu_all: the
+// mean of the old subset (before this step's moment update).  On success smw_valid[id] = 1 (the next
+// step skips k_prepare for the instance); a non-positive Delta leaves it 0 (full recompute).
+__global__ void __launch_bounds__(64) k_smw_update(const int* __restrict__ inst, const double* __restrict__ Zall,
+                                                   long long m, long long blk_stride, int nstart,
+                                                   const double* __restrict__ mu_all,
+                                                   const uint8_t* __restrict__ mem_new_all,
+                                                   const int* __restrict__ list_all, const int* __restrict__ seg_cnt_all,
+                                                   int nseg, long long seg_len, int p, long long h,
+                                                   double* __restrict__ sinv_all, double* __restrict__ logdet,
+                                                   int* __restrict__ smw_valid) {
+  __shared__ double A[RTD_MAXP * LD];
+  __shared__ double mu[RTD_MAXP], z[RTD_MAXP], u[RTD_MAXP], v[RTD_MAXP], Au[RTD_MAXP], vA[RTD_MAXP];
+  __shared__ int rows[2];  // list entries: +(row + 1) entering, -(row + 1) leaving (k_sel_member)
+  __shared__ double s_delta;
+  __shared__ int s_ok;
+  const int id = inst[blockIdx.x], t = threadIdx.x;
+  double* S = sinv_all + (long long)id * RTD_MAXP * RTD_MAXP;
+  const double* Z = Zall + (long long)(id / nstart) * blk_stride;
+  if (t == 0) {  // the two changed rows, in row order (segments are ordered, each segment's list too)
+    int k = 0;
+    for (int sgi = 0; sgi < nseg && k < 2; sgi++) {
+      const int c = seg_cnt_all[(long long)id * nseg + sgi];
+      for (int j = 0; j < c && k < 2; j++) rows[k++] = list_all[(long long)id * m + (long long)sgi * seg_len + j];
+    }
+    s_ok = k == 2;
+  }
+  const double hm1 = (double)(h - 1);
+  for (int e = t; e < p * p; e += blockDim.x) A[(e / p) * LD + e % p] = S[e] / hm1;  // Lambda^-1
+  for (int k = t; k < p; k += blockDim.x) mu[k] = mu_all[(long long)id * RTD_MAXP + k];
+  __syncthreads();
+  if (!s_ok) return;
+  double n = (double)h, dld = 0.0;
+  for (int c = 0; c < 2; c++) {
+    const long long r = (long long)abs(rows[c]) - 1;
+    const double delta = rows[c] > 0 ? 1.0 : -1.0;  // entering / leaving
+    const double n1 = n + delta;
+    for (int k = t; k < p; k += blockDim.x) {
+      z[k] = Z[(long long)k * m + r];
+      const double mk = mu[k] + delta * (z[k] - mu[k]) / n1;
+      u[k] = z[k] - mu[k];
+      v[k] = z[k] - mk;
+    }
+    __syncthreads();
+    for (int k = t; k < p; k += blockDim.x) {
+      double a = 0.0, b = 0.0;
+      for (int j = 0; j < p; j++) {
+        a = fma(A[k * LD + j], u[j], a);  // (Lambda^-1 u)_k
+        b = fma(v[j], A[j * LD + k], b);  // (v^T Lambda^-1)_k
+      }
+      Au[k] = a;
+      vA[k] = b;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double d = 0.0;
+      for (int k = 0; k < p; k++) d = fma(v[k], Au[k], d);
+      s_delta = 1.0 + delta * d;
+    }
+    __syncthreads();
+    const double D = s_delta;
+    if (!(D > 0.0) || !isfinite(D)) return;  // not PD after the update: k_prepare recomputes
+    const double f = delta / D;
+    for (int e = t; e < p * p; e += blockDim.x) {
+      const int i = e / p, j = e - i * p;
+      A[i * LD + j] -= f * Au[i] * vA[j];
+    }
+    dld += log(D);
+    for (int k = t; k < p; k += blockDim.x) mu[k] += delta * (z[k] - mu[k]) / n1;
+    n = n1;
+    __syncthreads();
+  }
+  for (int e = t; e < p * p; e += blockDim.x) S[e] = A[(e / p) * LD + e % p] * hm1;
+  if (t == 0) {
+    logdet[id] += dld;
+    smw_valid[id] = 1;
+  }
+}
+
+void launch_smw_update(const int* inst, int ninst, const double* Zall, long long m, long long blk_stride, int nstart,
+                       const double* mu_all, const uint8_t* mem_new_all, const int* list_all, const int* seg_cnt_all,
+                       int nseg, long long seg_len, int p, long long h, double* sinv_all, double* logdet,
+                       int* smw_valid, cudaStream_t st) {
+  k_smw_update<<<ninst, 64, 0, st>>>(inst, Zall, m, blk_stride, nstart, mu_all, mem_new_all, list_all, seg_cnt_all,
+                                     nseg, seg_len, p, h, sinv_all, logdet, smw_valid);
+  RTD_LAUNCHED();
+}
+
+// Per slot of this step's instance list (SMW variant), after k_prepare: an instance whose inverse was
+// updated by k_smw_update gets the operator [mu | Sigma^-1 (symmetrised)] staged from it and the 1-norm
+// condition check of k_prepare (||Sigma||_1 ||Sigma^-1||_1 < kappa_max); any other
+// instance's exact inverse (staged by k_prepare) is kept as the base of the next update.
+__global__ void __launch_bounds__(64) k_smw_stage(const int* __restrict__ inst, const double* __restrict__ mu_all,
+                                                  const double* __restrict__ sigma_all, int p, double kappa_max,
+                                                  double* __restrict__ cstage, int cstride,
+                                                  double* __restrict__ sinv_all, int* __restrict__ smw_valid,
+                                                  double* __restrict__ cond_out, int* __restrict__ status) {
+  __shared__ double red[2][RTD_MAXP];
+  const int slot = blockIdx.x, id = inst[slot], t = threadIdx.x;
+  if (status[id] != 0) return;
+  double* cs = cstage + (long long)slot * cstride;
+  double* S = sinv_all + (long long)id * RTD_MAXP * RTD_MAXP;
+  if (!smw_valid[id]) {
+    for (int e = t; e < p * p; e += blockDim.x) S[e] = cs[p + e];
+    return;
+  }
+  const double* mu = mu_all + (long long)id * RTD_MAXP;
+  const double* sg = sigma_all + (long long)id * RTD_MAXP * RTD_MAXP;
+  for (int k = t; k < p; k += blockDim.x) cs[k] = mu[k];
+  for (int e = t; e < p * p; e += blockDim.x) {
+    const int i = e / p, j = e - i * p;
+    cs[p + e] = 0.5 * (S[e] + S[j * p + i]);
+  }
+  for (int j = t; j < p; j += blockDim.x) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < p; i++) {
+      a += fabs(sg[i * p + j]);
+      b += fabs(S[i * p + j]);
+    }
+    red[0][j] = a;
+    red[1][j] = b;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double n1 = 0.0, n1i = 0.0;
+    for (int j = 0; j < p; j++) {
+      n1 = fmax(n1, red[0][j]);
+      n1i = fmax(n1i, red[1][j]);
+    }
+    const double kappa = n1 * n1i;
+    cond_out[id] = kappa;
+    if (!(kappa < kappa_max)) status[id] = ST_COND;
+    smw_valid[id] = 0;
+  }
+}
+
+void launch_smw_stage(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p,
+                      double kappa_max, double* cstage, int cstride, double* sinv_all, int* smw_valid,
+                      double* cond_out, int* status, cudaStream_t st) {
+  k_smw_stage<<<ninst, 64, 0, st>>>(inst, mu_all, sigma_all, p, kappa_max, cstage, cstride, sinv_all, smw_valid,
+                                    cond_out, status);
   RTD_LAUNCHED();
 }
 

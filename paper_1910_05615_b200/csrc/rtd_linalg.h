@@ -10,7 +10,15 @@ enum InstStatus { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_NOT_PD = 2, ST_COND = 3, S
 
 void launch_prepare(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p, double kappa_max,
                     double* cstage, int cstride, double* logdet_out, double* cond_out, int* status_out, double* traj,
-                    int traj_stride, int step, cudaStream_t st, int full_inverse = 0);
+                    int traj_stride, int step, cudaStream_t st, int full_inverse = 0, const int* skip = nullptr);
+// SMW variant (single-swap inverse updates; k_linalg.cu)
+void launch_smw_update(const int* inst, int ninst, const double* Zall, long long m, long long blk_stride, int nstart,
+                       const double* mu_all, const uint8_t* mem_new_all, const int* list_all, const int* seg_cnt_all,
+                       int nseg, long long seg_len, int p, long long h, double* sinv_all, double* logdet,
+                       int* smw_valid, cudaStream_t st);
+void launch_smw_stage(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p,
+                      double kappa_max, double* cstage, int cstride, double* sinv_all, int* smw_valid,
+                      double* cond_out, int* status, cudaStream_t st);
 // the whole C-step loop of short blocks (m <= 20480, p <= 16) in one CTA per instance (k_linalg.cu)
 bool csteps_small_supported(long long m, int p);
 void launch_csteps_small(const double* Zall, long long m, int p, long long blk_stride, int nstart, const int* inst,

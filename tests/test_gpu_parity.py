@@ -376,6 +376,23 @@ def test_fit_variants_I_ID_match_oracle(cfg, n, q):
         _compare_fit(g, o, d.X)
 
 
+@pytest.mark.parametrize("cfg,n,q,swaps", [(2, 20_000, 1, True), (3, 100_000, 1, False), (4, 40_003, 8, True)])
+def test_fit_variant_smw_matches_oracle(cfg, n, q, swaps):
+    """Single-swap SMW updates of the inverse and the determinant: the same
+    estimator, so the same oracle; on configs 2 and 4 the variant takes SMW steps (config 3 at this
+    size converges without a single-swap step)."""
+    d = datagen.make_config(cfg, n=n)
+    h = d.h if cfg == 3 else int(0.75 * n)
+    o = ofit.fit(d.X, h=h, q=q, seed=3)
+    api.set_profiling(True)
+    g = api.fit(_cuda(d.X), h=h, q=q, seed=3, distance=2)
+    prof = api.profile()
+    api.set_profiling(False)
+    _compare_fit(g, o, d.X)
+    if swaps:
+        assert prof.get("smw", {}).get("launches", 0) > 0, sorted(prof)
+
+
 @pytest.mark.parametrize("cfg,n,q", [(1, None, 1), (2, 20_000, 1), (4, 40_003, 8), (5, None, 1)])
 def test_fit_median_consistency_matches_oracle(cfg, n, q):
     d = datagen.make_config(cfg, n=n)
@@ -391,6 +408,10 @@ def test_fit_variant_errors():
     with pytest.raises(api.RTDError) as e:
         api.fit(_cuda(X), h=300, distance=1)   # the inverse variant runs on the tensor-pipe kernel: p >= 8
     assert e.value.name == "RTD_E_INVALID_ARG"
+    with pytest.raises(api.RTDError):
+        api.fit(_cuda(X), h=300, distance=2)
+    with pytest.raises(api.RTDError):
+        api.fit(_cuda(datagen.gaussian(500, 9, seed=4)), h=300, distance=3)
     with pytest.raises(api.RTDError):
         api.fit(_cuda(X), h=300, consistency=7)
 

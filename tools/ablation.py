@@ -7,6 +7,8 @@ the Cholesky factor (D), update-based C-steps (C), Parallelisation into q blocks
   I       distance=RTD_DIST_INVERSE, refresh_every=1 (explicit inverse, plain recompute every C-step)
   ID      distance=RTD_DIST_CHOLESKY, refresh_every=1
   IDC     the default serial fit (Cholesky distances, update-based C-steps)
+  IDC+SMW distance=RTD_DIST_SMW: the inverse and log det updated by Sherman-Morrison-Woodbury on the
+          C-steps that interchange exactly two cases, distances by the inverse
   IDCP_q  IDC on q blocks (contiguous blocks, the bench partition)
 
 for a BASELINE config, timed with CUDA events per fit (warm-up first), with the per-kernel-class device
@@ -40,7 +42,7 @@ def main():
     n, p = d.X.shape
     Xd = torch.from_numpy(d.X).to("cuda:0")
     variants = [("I", dict(distance=1, refresh_every=1, q=1)), ("ID", dict(distance=0, refresh_every=1, q=1)),
-                ("IDC", dict(q=1)), (f"IDCP_{a.q}", dict(q=a.q, partition=1))]
+                ("IDC", dict(q=1)), ("IDC+SMW", dict(distance=2, q=1)), (f"IDCP_{a.q}", dict(q=a.q, partition=1))]
     out = {"config": a.config, "n": n, "p": p, "h": d.h, "reps": a.reps, "table": "PAPER.md:1076-1100 (Table 1)",
            "variants": {}}
     stream = torch.cuda.current_stream()
