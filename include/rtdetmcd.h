@@ -162,6 +162,16 @@ rtdetmcd_status rtdetmcd_fit(rtdetmcd_ctx* ctx, const double* X, int64_t n, int3
 rtdetmcd_status rtdetmcd_fit_warm(rtdetmcd_ctx* ctx, const double* X, int64_t n, int32_t p, const rtdetmcd_opts* opts,
                                   const double* mu0, const double* sigma0, rtdetmcd_result* out);
 
+/* nb independent fits of the same shape and options over a sequence of HOST batches (a stream of
+ * data sets, e.g. successive windows of a production line; PAPER.md:1038-1043 motivates the
+ * real-time setting).  X[b] [host, pinned for full overlap]: n x p row-major.  Each batch is the
+ * exact rtdetmcd_fit of X[b] (out[b] filled as there); the library copies batch b+1 to the device
+ * on its own non-blocking copy stream while batch b is fitted, into two ctx-owned device buffers
+ * (2 n p 8 bytes, grow-only), so the host->device transfer overlaps the compute.  Stops at the
+ * first failing batch (its status is returned; later out[] are untouched).  out may be NULL. */
+rtdetmcd_status rtdetmcd_fit_batches(rtdetmcd_ctx* ctx, const double* const* X, int32_t nb, int64_t n, int32_t p,
+                                     const rtdetmcd_opts* opts, rtdetmcd_result* out);
+
 /* Step 10 on its own (the paper's 8.4 ms "flagging" figure,
  * PAPER.md:1624-1627): rd2_i = (x_i - mu)^T sigma^-1 (x_i - mu) by a Cholesky
  * solve, flags_i = rd2_i > chi2_{p, quantile}.

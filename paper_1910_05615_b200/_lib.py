@@ -20,7 +20,7 @@ RTD_STATUS = {
 
 EXPORTS = [
     "rtdetmcd_opts_default", "rtdetmcd_create", "rtdetmcd_destroy", "rtdetmcd_last_error",
-    "rtdetmcd_set_workspace", "rtdetmcd_fit_workspace_size", "rtdetmcd_fit", "rtdetmcd_fit_warm", "rtdetmcd_flag",
+    "rtdetmcd_set_workspace", "rtdetmcd_fit_workspace_size", "rtdetmcd_fit", "rtdetmcd_fit_warm", "rtdetmcd_fit_batches", "rtdetmcd_flag",
     "rtdetmcd_unimcd", "rtdetmcd_initial", "rtdetmcd_refine", "rtdetmcd_csteps",
     "rtdetmcd_chi2_quantile", "rtdetmcd_consistency_factor", "rtdetmcd_choose_q", "rtdetmcd_partition_perm",
     "rtdetmcd_set_profiling", "rtdetmcd_prof_count", "rtdetmcd_prof_entry", "rtdetmcd_counters",
@@ -74,6 +74,7 @@ def lib() -> C.CDLL:
     L.rtdetmcd_fit_workspace_size.restype = C.c_size_t
     L.rtdetmcd_fit.argtypes = [vp, vp, i64, i32, C.POINTER(Opts), C.POINTER(Result)]
     L.rtdetmcd_fit_warm.argtypes = [vp, vp, i64, i32, C.POINTER(Opts), vp, vp, C.POINTER(Result)]
+    L.rtdetmcd_fit_batches.argtypes = [vp, C.POINTER(C.c_void_p), i32, i64, i32, C.POINTER(Opts), C.POINTER(Result)]
     L.rtdetmcd_flag.argtypes = [vp, vp, i64, i32, vp, vp, f64, i32, vp, vp]
     L.rtdetmcd_unimcd.argtypes = [vp, vp, i64, i32, vp, vp, vp, vp, vp]
     L.rtdetmcd_initial.argtypes = [vp, vp, i64, i32, vp, vp, vp]

@@ -135,6 +135,42 @@ def workspace_size(n: int, p: int, **opts) -> int:
     return int(lib().rtdetmcd_fit_workspace_size(n, p, C.byref(o)))
 
 
+def _result_buffers(n, p, q, outputs, out_buffers, is_cuda, dev):
+    """A Result struct with its host arrays and per-row output buffers (caller-provided or new)."""
+    r = Result()
+    host = {k: np.zeros(p) for k in ("loc", "scale", "mu_raw", "mu_rew")}
+    host.update({k: np.zeros((p, p)) for k in ("sigma_raw", "sigma_rew")})
+    qmax = int(q) if q and q > 0 else 1024
+    host["block_chosen"] = np.zeros(qmax, np.int32)
+    host["start_steps"] = np.zeros(2 * qmax, np.int32)
+    host["start_status"] = np.zeros(2 * qmax, np.int32)
+    host["start_logdet"] = np.zeros(2 * qmax, np.float64)
+    for k, a in host.items():
+        setattr(r, k, a.ctypes.data)
+    rows = {}
+    for k, dt in (("flags", np.uint8), ("rd2", np.float64), ("weights", np.uint8), ("hsubset", np.uint8)):
+        if out_buffers and k in out_buffers:          # caller-provided buffer (e.g. pinned host tensor)
+            buf = out_buffers[k]
+            rows[k] = buf
+            setattr(r, k, buf.data_ptr() if hasattr(buf, "data_ptr") else buf.ctypes.data)
+        elif k in outputs:
+            buf, bp = _out_buffer(n, dt, is_cuda, dev)
+            rows[k] = buf
+            setattr(r, k, bp)
+    return r, host, rows
+
+
+def _make_fit(r, host, rows) -> "Fit":
+    qu = r.q_used
+    return Fit(loc=host["loc"], scale=host["scale"], mu_raw=host["mu_raw"], sigma_raw=host["sigma_raw"],
+               mu_rew=host["mu_rew"], sigma_rew=host["sigma_rew"], logdet_raw=r.logdet_raw, cutoff2=r.cutoff2,
+               h=r.h, h_block=r.h_block, m=r.m, q=qu, warnings=r.warnings, n_valid_blocks=r.n_valid_blocks,
+               n_kept_blocks=r.n_kept_blocks, n_weighted=r.n_weighted,
+               block_chosen=host["block_chosen"][:qu].copy(), start_steps=host["start_steps"][:2 * qu].copy(),
+               start_status=host["start_status"][:2 * qu].copy(), start_logdet=host["start_logdet"][:2 * qu].copy(),
+               **rows)
+
+
 def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, kappa_max: float = 1000.0,
         quantile: float = 0.975, max_csteps: int = 100, refresh_every: int = 32, partition: int = 0,
         log_transform: bool = False, outputs=("flags", "rd2", "weights", "hsubset"), device: int | None = None,
@@ -167,26 +203,7 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
             ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{dev}")
             ctx["ws"] = ws
         _check(L.rtdetmcd_set_workspace(ctx["h"], C.c_void_p(ws.data_ptr()), ws.numel()), ctx)
-    r = Result()
-    host = {k: np.zeros(p) for k in ("loc", "scale", "mu_raw", "mu_rew")}
-    host.update({k: np.zeros((p, p)) for k in ("sigma_raw", "sigma_rew")})
-    qmax = int(q) if q and q > 0 else 1024
-    host["block_chosen"] = np.zeros(qmax, np.int32)
-    host["start_steps"] = np.zeros(2 * qmax, np.int32)
-    host["start_status"] = np.zeros(2 * qmax, np.int32)
-    host["start_logdet"] = np.zeros(2 * qmax, np.float64)
-    for k, a in host.items():
-        setattr(r, k, a.ctypes.data)
-    rows = {}
-    for k, dt in (("flags", np.uint8), ("rd2", np.float64), ("weights", np.uint8), ("hsubset", np.uint8)):
-        if out_buffers and k in out_buffers:          # caller-provided buffer (e.g. pinned host tensor)
-            buf = out_buffers[k]
-            rows[k] = buf
-            setattr(r, k, buf.data_ptr() if hasattr(buf, "data_ptr") else buf.ctypes.data)
-        elif k in outputs:
-            buf, bp = _out_buffer(n, dt, is_cuda, dev)
-            rows[k] = buf
-            setattr(r, k, bp)
+    r, host, rows = _result_buffers(n, p, q, outputs, out_buffers, is_cuda, dev)
     if warm_start is None:
         rc = L.rtdetmcd_fit(ctx["h"], C.c_void_p(ptr), n, p, C.byref(o), C.byref(r))
     else:
@@ -197,14 +214,51 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
     if torch_workspace:
         L.rtdetmcd_set_workspace(ctx["h"], None, 0)
     _check(rc, ctx)
-    qu = r.q_used
-    return Fit(loc=host["loc"], scale=host["scale"], mu_raw=host["mu_raw"], sigma_raw=host["sigma_raw"],
-               mu_rew=host["mu_rew"], sigma_rew=host["sigma_rew"], logdet_raw=r.logdet_raw, cutoff2=r.cutoff2,
-               h=r.h, h_block=r.h_block, m=r.m, q=qu, warnings=r.warnings, n_valid_blocks=r.n_valid_blocks,
-               n_kept_blocks=r.n_kept_blocks, n_weighted=r.n_weighted,
-               block_chosen=host["block_chosen"][:qu].copy(), start_steps=host["start_steps"][:2 * qu].copy(),
-               start_status=host["start_status"][:2 * qu].copy(), start_logdet=host["start_logdet"][:2 * qu].copy(),
-               **rows)
+    return _make_fit(r, host, rows)
+
+
+def fit_batches(batches, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0,
+                kappa_max: float = 1000.0, quantile: float = 0.975, max_csteps: int = 100, refresh_every: int = 32,
+                partition: int = 0, log_transform: bool = False, outputs=("flags",), out_buffers=None,
+                device: int = 0, torch_workspace: bool = True, ctx: dict | None = None, distance: int = 0,
+                consistency: int = 0) -> list:
+    """rtdetmcd_fit_batches: one fit per HOST batch (n x p row-major float64, pinned torch tensors for
+    full overlap), batch b+1's host->device copy overlapping batch b's fit.  out_buffers: None, one
+    dict for every batch, or a list of dicts (per batch)."""
+    arrs = [_as_f64(X) for X in batches]
+    if any(a[2] for a in arrs):
+        raise ValueError("fit_batches takes host batches")
+    n, p = int(arrs[0][1].shape[0]), int(arrs[0][1].shape[1])
+    if any(tuple(a[1].shape) != (n, p) for a in arrs):
+        raise ValueError("all batches must have the same shape")
+    ctx = ctx or _ctx(device)
+    o = default_opts(h=int(h or 0), alpha=float(alpha), shards=int(q), seed=int(seed), kappa_max=float(kappa_max),
+                     quantile=float(quantile), max_csteps=int(max_csteps), refresh_every=int(refresh_every),
+                     partition=int(partition), log_transform=int(bool(log_transform)), distance=int(distance),
+                     consistency=int(consistency))
+    L = lib()
+    if torch_workspace:
+        torch = _torch()
+        need = int(L.rtdetmcd_fit_workspace_size(n, p, C.byref(o)))
+        ws = ctx["ws"]
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{device}")
+            ctx["ws"] = ws
+        _check(L.rtdetmcd_set_workspace(ctx["h"], C.c_void_p(ws.data_ptr()), ws.numel()), ctx)
+    nb = len(arrs)
+    per = []
+    for b in range(nb):
+        ob = out_buffers[b] if isinstance(out_buffers, (list, tuple)) else out_buffers
+        per.append(_result_buffers(n, p, q, outputs, ob, False, device))
+    res = (Result * nb)()
+    for b in range(nb):
+        res[b] = per[b][0]
+    ptrs = (C.c_void_p * nb)(*[a[0] for a in arrs])
+    rc = L.rtdetmcd_fit_batches(ctx["h"], ptrs, nb, n, p, C.byref(o), res)
+    if torch_workspace:
+        L.rtdetmcd_set_workspace(ctx["h"], None, 0)
+    _check(rc, ctx)
+    return [_make_fit(res[b], per[b][1], per[b][2]) for b in range(nb)]
 
 
 def flag(X, mu, sigma, quantile: float = 0.975, log_transform: bool = False, want_rd2: bool = True,

@@ -138,6 +138,11 @@ struct rtdetmcd_ctx {
   bool ws_user = false;
   Prof prof;
   void* session = nullptr;  // distributed stages (DistSession), see rtdetmcd_blocks_fit
+  // rtdetmcd_fit_batches: double-buffered device copies of the batches and the copy stream
+  double* xbuf[2] = {nullptr, nullptr};
+  size_t xbuf_cap = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -1243,6 +1248,11 @@ void rtdetmcd_destroy(rtdetmcd_ctx* c) {
   drop_session(c);
   cudaSetDevice(c->device);
   if (c->ws && !c->ws_user) cudaFree(c->ws);
+  for (int k = 0; k < 2; k++) {
+    if (c->xbuf[k]) cudaFree(c->xbuf[k]);
+    if (c->ev_copied[k]) cudaEventDestroy(c->ev_copied[k]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1294,6 +1304,49 @@ rtdetmcd_status rtdetmcd_fit_warm(rtdetmcd_ctx* c, const double* X, int64_t n, i
     if (opts) o = *opts; else rtdetmcd_opts_default(&o);
     drop_session(c);
     fit_impl(c, X, n, p, o, out, mu0, sigma0);
+  });
+}
+
+rtdetmcd_status rtdetmcd_fit_batches(rtdetmcd_ctx* c, const double* const* X, int32_t nb, int64_t n, int32_t p,
+                                     const rtdetmcd_opts* opts, rtdetmcd_result* out) {
+  return guarded(c, [&] {
+    if (!X || nb <= 0) throw Fail{RTD_E_INVALID_ARG, "X is NULL or nb <= 0"};
+    if (n <= 0 || p <= 0 || p > RTD_MAXP) throw Fail{RTD_E_INVALID_ARG, "bad n or p"};
+    for (int b = 0; b < nb; b++)
+      if (!X[b] || is_device_ptr(X[b])) throw Fail{RTD_E_INVALID_ARG, "every batch must be a host buffer"};
+    rtdetmcd_opts o;
+    if (opts) o = *opts; else rtdetmcd_opts_default(&o);
+    drop_session(c);
+    const size_t bytes = (size_t)n * p * sizeof(double);
+    if (c->xbuf_cap < bytes) {
+      for (int k = 0; k < 2; k++) {
+        if (c->xbuf[k]) RTD_CU(cudaFree(c->xbuf[k]));
+        c->xbuf[k] = nullptr;
+      }
+      c->xbuf_cap = 0;
+      for (int k = 0; k < 2; k++)
+        if (cudaMalloc(&c->xbuf[k], bytes) != cudaSuccess) {
+          cudaGetLastError();
+          throw Fail{RTD_E_OOM, "cannot allocate the batch buffers"};
+        }
+      c->xbuf_cap = bytes;
+    }
+    if (!c->copy_stream) {
+      RTD_CU(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; k++) RTD_CU(cudaEventCreateWithFlags(&c->ev_copied[k], cudaEventDisableTiming));
+    }
+    auto copy = [&](int b) {
+      RTD_CU(cudaMemcpyAsync(c->xbuf[b & 1], X[b], bytes, cudaMemcpyHostToDevice, c->copy_stream));
+      RTD_CU(cudaEventRecord(c->ev_copied[b & 1], c->copy_stream));
+    };
+    copy(0);
+    for (int b = 0; b < nb; b++) {
+      // the buffer of batch b + 1 last held batch b - 1, whose fit has returned (fits are synchronous)
+      if (b + 1 < nb) copy(b + 1);
+      RTD_CU(cudaStreamWaitEvent(c->stream, c->ev_copied[b & 1], 0));
+      fit_impl(c, c->xbuf[b & 1], n, p, o, out ? &out[b] : nullptr);
+    }
+    RTD_CU(cudaStreamSynchronize(c->copy_stream));
   });
 }
 

@@ -15,7 +15,7 @@ namespace rtd {
 
 static constexpr int QNB = 4096;
 static constexpr int QSAMPLE = 4096;
-static constexpr int QCAP = 4096;
+static constexpr int QCAP = 16384;  // elements of a target bucket sorted in shared memory (128 KB)
 static constexpr int QT = 256;
 static constexpr int QTARGETS = 6;
 
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(QT) k_q_gather(const double* __restrict__ r_al
 // one CTA per (target, block): sort the target's bucket in shared memory, read the element at the offset
 __global__ void __launch_bounds__(1024) k_q_pick(const QMap* __restrict__ maps, const double* __restrict__ gbuf,
                                                  const int* __restrict__ gcount, double* __restrict__ qv) {
-  __shared__ double a[QCAP];
+  extern __shared__ double a[];  // QCAP doubles
   const int k = blockIdx.x, b = blockIdx.y;
   const QMap c = maps[b];
   if (c.status) return;
@@ -271,7 +271,12 @@ void launch_quantiles(const double* r_all, long long m, int nb, char* scratch, d
   RTD_LAUNCHED();
   k_q_gather<<<dim3(gx, nb), QT, 0, st>>>(r_all, m, maps, gbuf, gcount);
   RTD_LAUNCHED();
-  k_q_pick<<<dim3(QTARGETS, nb), 1024, 0, st>>>(maps, gbuf, gcount, qv);
+  static const bool attr = [] {
+    RTD_CU(cudaFuncSetAttribute(k_q_pick, cudaFuncAttributeMaxDynamicSharedMemorySize, QCAP * (int)sizeof(double)));
+    return true;
+  }();
+  (void)attr;
+  k_q_pick<<<dim3(QTARGETS, nb), 1024, QCAP * sizeof(double), st>>>(maps, gbuf, gcount, qv);
   RTD_LAUNCHED();
   std::vector<QMap> h(nb);
   RTD_CU(cudaMemcpyAsync(h.data(), maps, nb * sizeof(QMap), cudaMemcpyDeviceToHost, st));

@@ -442,3 +442,21 @@ def test_fit_blocked_long_blocks_p40():
     o = ofit.fit(d.X, h=h, q=2, seed=11)
     g = api.fit(_cuda(d.X), h=h, q=2, seed=11)
     _compare_fit(g, o, d.X)
+
+
+# ------------------------------------------------------------------ batched host fits
+def test_fit_batches_equal_single_fits():
+    """rtdetmcd_fit_batches: each batch's result is the plain rtdetmcd_fit of that batch (the copy of
+    batch b+1 overlaps batch b's fit on the library's copy stream)."""
+    torch = pytest.importorskip("torch")
+    Xs = [datagen.make_config(2, n=30_000 + 1000 * k).X[:30_000] for k in range(3)]
+    hosts = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in Xs]
+    fits = api.fit_batches(hosts, h=22_500, q=1, seed=5, outputs=("flags", "rd2"))
+    assert len(fits) == 3
+    for x, g in zip(Xs, fits):
+        s = api.fit(x, h=22_500, q=1, seed=5, outputs=("flags", "rd2"))
+        assert np.array_equal(g.mu_rew, s.mu_rew) and np.array_equal(g.sigma_rew, s.sigma_rew)
+        assert np.array_equal(np.asarray(g.flags), np.asarray(s.flags))
+        assert np.array_equal(np.asarray(g.rd2), np.asarray(s.rd2))
+    with pytest.raises(ValueError):
+        api.fit_batches([_cuda(Xs[0])])
