@@ -25,6 +25,9 @@ void launch_dist_mma(int p, const double* Zall, long long m, long long blk_strid
 long long launch_count();
 long long sort_count();
 void launch_moments_mma(int mode, const MomArgs& a, int ninst, cudaStream_t st);
+void launch_matmul_mma_pairs(int p, const double* Zall, long long m, long long blk_stride, const int* slot_of,
+                             const int* blk_of_slot, const int* pairs, int npairs, const double* W_all,
+                             double* out_all, cudaStream_t st);
 void launch_matmul_mma_batch(int p, const double* Zall, long long m, long long blk_stride, const int* slot_of,
                              const int* blk_of_slot, int nitems, const double* W_all, double* out_all,
                              cudaStream_t st);
@@ -537,6 +540,7 @@ struct RefineBufs {
   double* T;                                 // [cap][p][m] column-major scores / sphered data
   double *V, *d, *mut, *Smh, *Sh;            // per slot (stride M2 / RTD_MAXP)
   int *slot_of, *blk_of_slot;                // [cap]
+  int* pairs;                                // [cap][2] items of one block per GEMM CTA row
   UniOut* uni;                               // [cap * p]
   char* uscratch;
   size_t uscratch_bytes;
@@ -555,6 +559,7 @@ void carve_refine(Arena& A, RefineBufs& r, long long m, int p, int cap) {
   r.Sh = A.take<double>((size_t)cap * M2);
   r.slot_of = A.take<int>(cap + 8);
   r.blk_of_slot = A.take<int>(cap + 8);
+  r.pairs = A.take<int>(2 * cap + 8);
   r.uni = A.take<UniOut>((size_t)tot);
   r.uscratch_bytes = uni_bytes(m, r.ucols);
   r.uscratch = A.take<char>(r.uscratch_bytes);
@@ -565,6 +570,20 @@ static void refine_matmul(cudaStream_t st, RefineBufs& r, const double* Zall, lo
                           int p, int nitems, const double* W_all, const std::vector<int>& items,
                           const std::vector<int>& blk) {
   ProfScope ps("matmul", (double)nitems * m * p * 16.0);
+  static const bool no_pair = getenv("RTD_MATMUL_NOPAIR") != nullptr;
+  if (use_mma() && p > 24 && !no_pair) {  // consecutive items of one block share a CTA (Z read once)
+    std::vector<int> pr;
+    for (int i = 0; i < nitems;) {
+      const bool two = i + 1 < nitems && blk[items[i]] == blk[items[i + 1]];
+      pr.push_back(i);
+      pr.push_back(two ? i + 1 : -1);
+      i += two ? 2 : 1;
+    }
+    h2d(st, r.pairs, pr.data(), pr.size() * sizeof(int));
+    launch_matmul_mma_pairs(p, Zall, m, blk_stride, r.slot_of, r.blk_of_slot, r.pairs, (int)pr.size() / 2, W_all, r.T,
+                            st);
+    return;
+  }
   if (use_mma()) {
     launch_matmul_mma_batch(p, Zall, m, blk_stride, r.slot_of, r.blk_of_slot, nitems, W_all, r.T, st);
     return;

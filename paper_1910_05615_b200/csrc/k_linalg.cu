@@ -26,49 +26,65 @@ static constexpr int LD = RTD_MAXP + 1;
 // (stores landing one element off) for a 2-D-array-parameter version with an
 // in-loop return (tools/t_min3.cu reproduces it; tools/t_min4.cu is this form).
 
-// Cholesky of the p x p matrix in A into L; returns false if not PD.
+// Cholesky of the p x p matrix in A into L; returns false if not PD.  Right-looking: per column j
+// one pivot (every thread reads the same updated diagonal, so the decision is uniform), the column
+// scaled by 1 / L_jj and a rank-1 update of the trailing triangle in parallel -- two barriers per
+// column and no dependent chain longer than one FMA (the left-looking form had a length-j dot product
+// on one thread per column: ~64 us per launch at p = 40, dominated by barrier waits).
 __device__ __noinline__ bool block_cholesky(const double* A, double* L, int p, int* s_fail) {
   const int t = threadIdx.x;
   if (t == 0) *s_fail = 0;
-  for (int e = t; e < RTD_MAXP * LD; e += blockDim.x) L[e] = 0.0;
+  for (int e = t; e < RTD_MAXP * LD; e += blockDim.x) {
+    const int i = e / LD, k = e - i * LD;
+    L[e] = (i < p && k <= i) ? A[i * LD + k] : 0.0;
+  }
   __syncthreads();
   bool ok = true;
   for (int j = 0; j < p; j++) {
-    if (t == 0) {
-      double s = A[j * LD + j];
-      for (int k = 0; k < j; k++) s -= L[j * LD + k] * L[j * LD + k];
-      if (!(s > 0.0) || !isfinite(s)) *s_fail = 1;
-      L[j * LD + j] = s > 0.0 ? sqrt(s) : 1.0;
-    }
-    __syncthreads();
-    if (*s_fail) {
+    const double d = L[j * LD + j];
+    if (!(d > 0.0) || !isfinite(d)) {
       ok = false;
       break;
     }
-    for (int i = j + 1 + t; i < p; i += blockDim.x) {
-      double s = A[i * LD + j];
-      for (int k = 0; k < j; k++) s -= L[i * LD + k] * L[j * LD + k];
-      L[i * LD + j] = s / L[j * LD + j];
+    const double r = sqrt(d);
+    __syncthreads();  // every thread has read the pivot before it is overwritten
+    if (t == 0) L[j * LD + j] = r;
+    for (int i = j + 1 + t; i < p; i += blockDim.x) L[i * LD + j] /= r;
+    __syncthreads();
+    const int nr = p - j - 1;
+    for (int e = t; e < nr * nr; e += blockDim.x) {
+      const int ii = e / nr, kk = e - ii * nr;
+      if (kk <= ii) {
+        const int i = j + 1 + ii, k = j + 1 + kk;
+        L[i * LD + k] = fma(-L[i * LD + j], L[k * LD + j], L[i * LD + k]);
+      }
     }
     __syncthreads();
   }
+  if (!ok && t == 0) *s_fail = 1;
+  __syncthreads();
   return ok;
 }
 
-// Li = L^-1 (lower triangular), column-parallel forward substitution.
+// Li = L^-1 (lower triangular): row-wise forward substitution L X = I, right-looking -- row k of X
+// is final once divided by L_kk, then its contribution is removed from the rows below in parallel.
 __device__ __noinline__ void block_tri_inverse(const double* L, double* Li, int p) {
   const int t = threadIdx.x;
-  for (int e = t; e < RTD_MAXP * LD; e += blockDim.x) Li[e] = 0.0;
-  __syncthreads();
-  if (t < p) {
-    const int c = t;
-    for (int i = c; i < p; i++) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; k++) s -= L[i * LD + k] * Li[k * LD + c];
-      Li[i * LD + c] = s / L[i * LD + i];
-    }
+  for (int e = t; e < RTD_MAXP * LD; e += blockDim.x) {
+    const int i = e / LD, k = e - i * LD;
+    Li[e] = (i == k && i < p) ? 1.0 : 0.0;
   }
   __syncthreads();
+  for (int k = 0; k < p; k++) {
+    for (int c = t; c <= k; c += blockDim.x) Li[k * LD + c] /= L[k * LD + k];
+    __syncthreads();
+    const int nr = p - k - 1, nc = k + 1;
+    for (int e = t; e < nr * nc; e += blockDim.x) {
+      const int i = k + 1 + e / nc, c = e % nc;
+      Li[i * LD + c] = fma(-L[i * LD + k], Li[k * LD + c], Li[i * LD + c]);
+    }
+    __syncthreads();
+  }
 }
 
 __device__ __noinline__ double block_max_colsum_abs(const double* A, int p, double* red) {

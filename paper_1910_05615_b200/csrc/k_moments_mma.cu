@@ -445,6 +445,118 @@ __global__ void __launch_bounds__(256, BSM ? 2 : 1) k_matmul_mma(const double* _
   }
 }
 
+// Two work items of the same block in one CTA (the refinement's two starts share Z): each A fragment
+// of Z feeds the DMMAs of both W, so Z is read once per pair.  pairs[2y], pairs[2y+1]: the items of CTA
+// row y (the second -1 for a lone item).  B fragments of both W in shared memory (lane-major).
+template <int NB, int MB, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_matmul_pair(const double* __restrict__ Zall, long long m, int p,
+                                                        long long blk_stride, const int* __restrict__ slot_of,
+                                                        const int* __restrict__ blk_of_slot,
+                                                        const int* __restrict__ pairs,
+                                                        const double* __restrict__ W_all,
+                                                        double* __restrict__ out_all) {
+  constexpr int KB = 2 * NB;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int i0 = pairs[2 * blockIdx.y], i1 = pairs[2 * blockIdx.y + 1];
+  const bool two = i1 >= 0;
+  const int s0 = slot_of[i0], s1 = two ? slot_of[i1] : s0;
+  const double* __restrict__ Z = Zall + (long long)blk_of_slot[s0] * blk_stride;
+  double* __restrict__ out0 = out_all + (long long)i0 * p * m;
+  double* __restrict__ out1 = out_all + (long long)(two ? i1 : i0) * p * m;
+  __shared__ double bsm[2][KB * NB * 32];
+  for (int e = threadIdx.x; e < KB * NB * 32; e += blockDim.x) {
+    const int ln = e & 31, b = e >> 5, kb = b / NB, nb = b - kb * NB;
+    const int k = 4 * kb + (ln & 3), j = 8 * nb + (ln >> 2);
+    const bool in = k < p && j < p;
+    bsm[0][e] = in ? W_all[(long long)s0 * RTD_MAXP * RTD_MAXP + k * p + j] : 0.0;
+    bsm[1][e] = in ? W_all[(long long)s1 * RTD_MAXP * RTD_MAXP + k * p + j] : 0.0;
+  }
+  __syncthreads();
+  const long long rows_per_tile = 8 * MB;
+  const long long ntiles = (m + rows_per_tile - 1) / rows_per_tile;
+  const long long warp0 = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long tile = warp0; tile < ntiles; tile += nwarps) {
+    const long long r0 = tile * rows_per_tile;
+    double acc[2][MB][NB][2];
+#pragma unroll
+    for (int w = 0; w < 2; w++)
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) acc[w][mb][nb][0] = acc[w][mb][nb][1] = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < KB; kb++) {
+      const int k = 4 * kb + t;
+      double av[MB];
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++) {
+        const long long row = r0 + mb * 8 + g;
+        av[mb] = (k < p && row < m) ? Z[(long long)k * m + row] : 0.0;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        const double b0 = bsm[0][(kb * NB + nb) * 32 + lane];
+#pragma unroll
+        for (int mb = 0; mb < MB; mb++) dmma(acc[0][mb][nb][0], acc[0][mb][nb][1], av[mb], b0);
+        if (two) {
+          const double b1 = bsm[1][(kb * NB + nb) * 32 + lane];
+#pragma unroll
+          for (int mb = 0; mb < MB; mb++) dmma(acc[1][mb][nb][0], acc[1][mb][nb][1], av[mb], b1);
+        }
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+      if (w == 1 && !two) break;
+      double* __restrict__ out = w ? out1 : out0;
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++) {
+        const long long row = r0 + mb * 8 + g;
+        if (row >= m) continue;
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) {
+          const int j = 8 * nb + 2 * t;
+          if (j < p) out[(long long)j * m + row] = acc[w][mb][nb][0];
+          if (j + 1 < p) out[(long long)(j + 1) * m + row] = acc[w][mb][nb][1];
+        }
+      }
+    }
+  }
+}
+
+template <int NB>
+static void matmul_pair_nb(const double* Z, long long m, int p, long long blk_stride, const int* slot_of,
+                           const int* blk_of_slot, const int* pairs, int npairs, const double* W, double* out,
+                           cudaStream_t st) {
+  // variant 0: 2 m-blocks per warp at 1 CTA/SM (no spills); 1: 1 m-block at 2 CTAs/SM
+  static const int variant = getenv("RTD_MATMUL_PAIR_VARIANT") ? atoi(getenv("RTD_MATMUL_PAIR_VARIANT")) : 0;
+  if (variant == 1) {
+    constexpr int MB = 1;
+    const long long tiles = (m + 8 * MB - 1) / (8 * MB);
+    const unsigned grid = (unsigned)std::min<long long>((tiles + 7) / 8, std::max(1, 148 * 4 / std::max(1, npairs)));
+    k_matmul_pair<NB, MB, 2><<<dim3(grid, npairs), 256, 0, st>>>(Z, m, p, blk_stride, slot_of, blk_of_slot, pairs, W,
+                                                                 out);
+    return;
+  }
+  constexpr int MB = 2;
+  const long long tiles = (m + 8 * MB - 1) / (8 * MB);
+  const unsigned grid = (unsigned)std::min<long long>((tiles + 7) / 8, std::max(1, 148 * 2 / std::max(1, npairs)));
+  k_matmul_pair<NB, MB, 1><<<dim3(grid, npairs), 256, 0, st>>>(Z, m, p, blk_stride, slot_of, blk_of_slot, pairs, W,
+                                                               out);
+}
+
+void launch_matmul_mma_pairs(int p, const double* Zall, long long m, long long blk_stride, const int* slot_of,
+                             const int* blk_of_slot, const int* pairs, int npairs, const double* W_all,
+                             double* out_all, cudaStream_t st) {
+  switch ((p + 7) / 8) {
+    case 4: matmul_pair_nb<4>(Zall, m, p, blk_stride, slot_of, blk_of_slot, pairs, npairs, W_all, out_all, st); break;
+    case 5: matmul_pair_nb<5>(Zall, m, p, blk_stride, slot_of, blk_of_slot, pairs, npairs, W_all, out_all, st); break;
+    default: throw std::string("matmul_pair: p out of range");
+  }
+  RTD_LAUNCHED();
+}
+
 template <int NB>
 static void matmul_mma_nb(const double* Z, long long m, int p, long long blk_stride, const int* slot_of,
                           const int* blk_of_slot, int nitems, const double* W, double* out, cudaStream_t st) {

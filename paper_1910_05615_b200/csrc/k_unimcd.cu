@@ -570,7 +570,8 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
   // Large columns: exact window by bucketing + bounds (k_unimcd_pruned.cu), every column in one pass;
   // the sort path below is the fallback and the small-n path.
   static const bool force_sort = getenv("RTD_UNI_FULLSORT") != nullptr;
-  if (len >= (1LL << 16) && !force_sort) {  // below: the two radix sorts measured faster (config 5)
+  static const long long pruned_min = getenv("RTD_UNI_PRUNED_MIN") ? atoll(getenv("RTD_UNI_PRUNED_MIN")) : (1LL << 16);
+  if (len >= pruned_min && !force_sort) {  // below: the two radix sorts measured faster (config 5)
     const bool done = unimcd_pruned(A, st, cols, len, ncols, uc, out_dev);
     if (A.base == nullptr) return;  // dry run (both paths measured)
     if (done) return;
