@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(MW * 32, 2) k_moments_st(MomArgs a) {
   const int NP = p + p * (p + 1) / 2 + 1;
   double* tiles = smem;
   double* wts = smem + (size_t)NST * p * SLD;
+  __shared__ int s_wn;                                   // MOM_WRAP: tanh-branch entries of the tile
+  int* wl = reinterpret_cast<int*>(wts + NST * SR);      // MOM_WRAP: their positions (p * SR ints)
+  if (MODE == MOM_WRAP && threadIdx.x == 0) s_wn = 0;
   double sh[NB];
 #pragma unroll
   for (int b = 0; b < NB; b++)
@@ -176,6 +179,32 @@ __global__ void __launch_bounds__(MW * 32, 2) k_moments_st(MomArgs a) {
     const int stg = tile % NST;
     const double* T = tiles + (size_t)stg * p * SLD;
     const double* W = wts + stg * SR;
+    if (MODE == MOM_WRAP) {
+      // psi of the tile in place: identity and zero branches directly, the tanh
+      // branch (b < |z| <= c, a minority of the entries) compacted into a list and evaluated once per
+      // listed entry instead of by every warp whose lanes hold any such entry
+      double* Tw = tiles + (size_t)stg * p * SLD;
+      const int rows_t = (int)min((long long)SR, r_end - (r_begin + (long long)tile * SR));
+      for (int e0 = 0; e0 < p * SR; e0 += MW * 32) {
+        const int e = e0 + tid, k = e / SR, r = e - k * SR;
+        const bool in = e < p * SR && r < rows_t;
+        const double z = in ? Tw[k * SLD + r] : 0.0, az = fabs(z);
+        const bool need = in && az > 1.5 && az <= 4.0;
+        if (in && az > 4.0) Tw[k * SLD + r] = 0.0;
+        const unsigned bal = __ballot_sync(0xffffffffu, need);
+        if (bal) {
+          int pos = 0;
+          if (lane == (unsigned)(__ffs(bal) - 1)) pos = atomicAdd(&s_wn, __popc(bal));
+          pos = __shfl_sync(0xffffffffu, pos, __ffs(bal) - 1) + __popc(bal & ((1u << lane) - 1u));
+          if (need) wl[pos] = k * SLD + r;
+        }
+      }
+      __syncthreads();
+      const int nw = s_wn;
+      for (int i = tid; i < nw; i += MW * 32) Tw[wl[i]] = wrap_g2(Tw[wl[i]]);
+      __syncthreads();
+      if (tid == 0) s_wn = 0;  // every thread has read the count; the next use follows two barriers
+    }
 #pragma unroll
     for (int q = 0; q < 2; q++) {
       const int r = (2 * warp + q) * 4 + t;  // row of this lane in the tile
@@ -185,9 +214,8 @@ __global__ void __launch_bounds__(MW * 32, 2) k_moments_st(MomArgs a) {
 #pragma unroll
       for (int b = 0; b < NB; b++) {
         const int col = 8 * b + g;
-        double v = (w != 0.0 && col < p) ? T[col * SLD + r] : 0.0;
-        if (MODE == MOM_WRAP) v = wrap_g2(v);
-        else if (MODE >= MOM_MEMBER) v = (w != 0.0 && col < p) ? __dsub_rn(v, sh[b]) : 0.0;
+        double v = (w != 0.0 && col < p) ? T[col * SLD + r] : 0.0;  // MOM_WRAP: psi already applied
+        if (MODE >= MOM_MEMBER) v = (w != 0.0 && col < p) ? __dsub_rn(v, sh[b]) : 0.0;
         u[b] = v;
       }
       double wu[NB];
@@ -326,7 +354,9 @@ static void moments_mma_nb(int mode, const MomArgs& a, int ninst, cudaStream_t s
   // fit); at p <= 24 or short blocks (configs 1-3, 5) the register-fed kernel is faster
   static const bool unstaged = getenv("RTD_MOM_UNSTAGED") != nullptr;
   if (mode != MOM_DELTA && NB >= 4 && a.m >= 65536 && !unstaged) {
-    const size_t smem = std::max((size_t)MW * NP, (size_t)NST * a.p * SLD + (size_t)NST * SR) * sizeof(double);
+    const size_t smem = std::max((size_t)MW * NP * sizeof(double),
+                                 ((size_t)NST * a.p * SLD + (size_t)NST * SR) * sizeof(double) +
+                                 (size_t)a.p * SR * sizeof(int));
 #define RTD_ST_CASE(M)                                                                                   \
   case M:                                                                                                \
     RTD_CU(cudaFuncSetAttribute(k_moments_st<NB, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
