@@ -113,7 +113,7 @@ __device__ __noinline__ void block_inv_from_li(const double* Li, double* B, int 
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(LT) k_prepare(const int* __restrict__ inst, const double* __restrict__ mu_all,
+__global__ void __launch_bounds__(512) k_prepare(const int* __restrict__ inst, const double* __restrict__ mu_all,
                                                 const double* __restrict__ sigma_all, int p, double kappa_max,
                                                 double* __restrict__ cstage, int cstride, double* __restrict__ logdet_out,
                                                 double* __restrict__ cond_out, int* __restrict__ status_out,
@@ -522,7 +522,7 @@ void launch_csteps_small(const double* Zall, long long m, int p, long long blk_s
 void launch_prepare(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p, double kappa_max,
                     double* cstage, int cstride, double* logdet_out, double* cond_out, int* status_out, double* traj,
                     int traj_stride, int step, cudaStream_t st, int full_inverse, const int* skip) {
-  k_prepare<<<ninst, LT, 0, st>>>(inst, mu_all, sigma_all, p, kappa_max, cstage, cstride, logdet_out, cond_out,
+  k_prepare<<<ninst, 512, 0, st>>>(inst, mu_all, sigma_all, p, kappa_max, cstage, cstride, logdet_out, cond_out,
                                   status_out, traj, traj_stride, step, full_inverse, skip);
   RTD_LAUNCHED();
 }
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(LT) k_jacobi(const double* __restrict__ A_all,
     __syncthreads();
     if (t == 0) {
       double so = 0.0, st = 0.0;
-      for (int k = 0; k < LT / 32; k++) {
+      for (int k = 0; k < (int)(blockDim.x >> 5); k++) {
         so += red[k];
         st += red[32 + k];
       }
