@@ -15,7 +15,7 @@
 //      smallest upper bound;
 //   4. one pass gathers the elements of the buckets that hold candidate
 //      window ends and sums (double-double, fixed order) everything below them;
-//   5. the gathered sets are sorted (segmented radix sort), prefix-summed in
+//   5. the gathered sets are sorted (shared-memory bitonic chunks + merge path), prefix-summed in
 //      double-double, and h*SQ(s) is evaluated exactly for every candidate s:
 //      argmin, ties -> lowest s (reading R2);
 //   6. one pass sums the kept points of the reweighting step (reading R4).
@@ -24,7 +24,6 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include <cub/device/device_segmented_radix_sort.cuh>
 
 #include "rtd_internal.h"
 
@@ -873,12 +872,6 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
   }
 }
 
-__global__ void k_pr_segs(const int* __restrict__ gcount, int nseg, int* __restrict__ sbeg, int* __restrict__ send) {
-  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
-    sbeg[i] = i * CAP;
-    send[i] = i * CAP + min(gcount[i], CAP);
-  }
-}
 
 // 5a. double-double prefix sums of each sorted gathered segment (one CTA per segment)
 __device__ void prefix_body(const double* v, int cn, int col, int side, const dd2* __restrict__ below,
@@ -945,6 +938,53 @@ struct WinBest {
   double vhi, vlo;
   long long s;
 };
+
+// 5a''. a segment longer than SMAX: chunks of SMAX sorted in shared memory in place, then merge
+//       rounds (merge path, one CTA per pair of runs) ping-ponging between g and gsorted; the
+//       final buffer feeds k_pr_prefix.  Equal values may interleave in either order: the prefix sums
+//       at every rank are the same.
+__global__ void __launch_bounds__(1024) k_pr_chunksort(const PrunedCol* __restrict__ pc, double* __restrict__ g,
+                                                       const int* __restrict__ gcount) {
+  extern __shared__ double sv[];
+  const int seg = blockIdx.y, col = seg >> 1;
+  if (pc[col].status) return;
+  const int cn = min(gcount[seg], CAP), c0 = blockIdx.x * SMAX;
+  if (c0 >= cn) return;
+  const int n = min(SMAX, cn - c0);
+  int np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  double* src = g + (long long)seg * CAP + c0;
+  for (int i = threadIdx.x; i < np2; i += blockDim.x) sv[i] = i < n ? src[i] : INFINITY;
+  __syncthreads();
+  smem_bitonic(sv, np2);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) src[i] = sv[i];
+}
+
+__global__ void __launch_bounds__(1024) k_pr_merge(const PrunedCol* __restrict__ pc, const double* __restrict__ src,
+                                                   double* __restrict__ dst, const int* __restrict__ gcount, int w) {
+  const int seg = blockIdx.y, col = seg >> 1;
+  if (pc[col].status) return;
+  const int cn = min(gcount[seg], CAP), a0 = blockIdx.x * 2 * w;
+  if (a0 >= cn) return;
+  const double* A = src + (long long)seg * CAP + a0;
+  const double* B = A + w;
+  const int na = min(w, cn - a0), nb = max(0, min(w, cn - a0 - w)), tot = na + nb;
+  double* out = dst + (long long)seg * CAP + a0;
+  const int K = (tot + blockDim.x - 1) / blockDim.x;
+  const int d0 = min(tot, (int)threadIdx.x * K), d1 = min(tot, d0 + K);
+  if (d0 >= d1) return;
+  // i = elements of A among the first d0 outputs (A first on ties)
+  int lo = max(0, d0 - nb), hi = min(d0, na);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A[mid] <= B[d0 - mid - 1]) lo = mid + 1; else hi = mid;
+  }
+  int ia = lo, ib = d0 - lo;
+  for (int d = d0; d < d1; d++) {
+    if (ib >= nb || (ia < na && A[ia] <= B[ib])) out[d] = A[ia++];
+    else out[d] = B[ib++];
+  }
+}
 
 // 5b. exact objective of every candidate start; per-CTA best, grid (chunks, ncols)
 __global__ void __launch_bounds__(PT) k_pr_eval(long long h, const PrunedCol* __restrict__ pc,
@@ -1092,23 +1132,14 @@ struct PrScratch {
   unsigned long long* mm;
   double *g, *gsorted;
   int* gcount;
-  int *sbeg, *send;
   dd2* below;
   dd2* pref;
   WinBest* part;
   dd2* kpart;
   long long* kcnt;
-  void* cub_tmp;
-  size_t cub_bytes;
   int nch;
 };
 
-static size_t seg_sort_bytes(int nseg) {
-  size_t b = 0;
-  cub::DeviceSegmentedRadixSort::SortKeys(nullptr, b, (const double*)nullptr, (double*)nullptr, nseg * CAP, nseg,
-                                          (const int*)nullptr, (const int*)nullptr);
-  return b;
-}
 
 static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.pc = A.take<PrunedCol>(ncols);
@@ -1119,16 +1150,12 @@ static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.g = A.take<double>((size_t)2 * ncols * CAP);
   s.gsorted = A.take<double>((size_t)2 * ncols * CAP);
   s.gcount = A.take<int>(2 * (size_t)ncols);
-  s.sbeg = A.take<int>(2 * (size_t)ncols);
-  s.send = A.take<int>(2 * (size_t)ncols);
   s.below = A.take<dd2>((size_t)ncols * PCTA * 2);
   s.pref = A.take<dd2>((size_t)2 * ncols * (CAP + 1));
   s.nch = 16;
   s.part = A.take<WinBest>((size_t)ncols * s.nch);
   s.kpart = A.take<dd2>((size_t)ncols * PCTA);
   s.kcnt = A.take<long long>((size_t)ncols * PCTA);
-  s.cub_bytes = seg_sort_bytes(2 * ncols);
-  s.cub_tmp = A.take<char>(s.cub_bytes);
 }
 
 // Returns true when every column was resolved by the pruned path (out_dev filled);
@@ -1188,14 +1215,21 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
     k_pr_sortprefix<<<2 * ncols, 1024, std::min(smem, np2 * (int)sizeof(double)), st>>>(s.pc, s.g, s.gcount, s.below,
                                                                                          s.pref);
     RTD_LAUNCHED();
-  } else {
-    k_pr_segs<<<1, 256, 0, st>>>(s.gcount, 2 * ncols, s.sbeg, s.send);
+  } else {  // chunk sorts + merge rounds (no library sort on the fit path)
+    static const int csmem = [] {
+      cudaFuncSetAttribute(k_pr_chunksort, cudaFuncAttributeMaxDynamicSharedMemorySize, SMAX * (int)sizeof(double));
+      return SMAX * (int)sizeof(double);
+    }();
+    const int nchunk = (gmax + SMAX - 1) / SMAX;
+    k_pr_chunksort<<<dim3(nchunk, 2 * ncols), 1024, csmem, st>>>(s.pc, s.g, s.gcount);
     RTD_LAUNCHED();
-    size_t bytes = s.cub_bytes;
-    count_sort();
-    RTD_CU(cub::DeviceSegmentedRadixSort::SortKeys(s.cub_tmp, bytes, s.g, s.gsorted, 2 * ncols * CAP, 2 * ncols,
-                                                   s.sbeg, s.send, 0, 64, st));
-    k_pr_prefix<<<2 * ncols, 1024, 0, st>>>(s.pc, s.gsorted, s.gcount, s.below, s.pref);
+    double *src = s.g, *dst = s.gsorted;
+    for (int w = SMAX; w < gmax; w *= 2) {
+      k_pr_merge<<<dim3((gmax + 2 * w - 1) / (2 * w), 2 * ncols), 1024, 0, st>>>(s.pc, src, dst, s.gcount, w);
+      RTD_LAUNCHED();
+      std::swap(src, dst);
+    }
+    k_pr_prefix<<<2 * ncols, 1024, 0, st>>>(s.pc, src, s.gcount, s.below, s.pref);
     RTD_LAUNCHED();
   }
   k_pr_eval<<<dim3(s.nch, ncols), PT, 0, st>>>(h, s.pc, s.pref, s.part, s.nch);

@@ -88,6 +88,25 @@ def test_unimcd_large_columns(n):
         assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13), j
 
 
+def test_unimcd_8m_rows_merge_sorted_candidates():
+    """Columns as long as config 4's (8M rows): the gathered candidate sets exceed one shared-memory
+    sort (16K), so they go through the chunk sorts + merge path before the exact evaluation."""
+    rng = np.random.default_rng(8)
+    n = 8_000_000
+    a = rng.standard_normal(n)
+    b = rng.standard_normal(n)
+    b[: n // 20] += 8.0
+    cols = np.stack([a, rng.permutation(b)])
+    g = api.unimcd(_cuda(cols))
+    for j in range(2):
+        o = unimcd_reweighted(cols[j])
+        assert g["start"][j] == o.raw.start, j
+        assert g["raw_loc"][j] == pytest.approx(o.raw.loc, rel=1e-15, abs=1e-300), j
+        assert g["raw_var"][j] == pytest.approx(o.raw.var_raw, rel=1e-13), j
+        assert g["loc"][j] == pytest.approx(o.loc, rel=1e-14, abs=1e-14), j
+        assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13), j
+
+
 def test_unimcd_heavy_mixed_sign_tails():
     """Bucketed path (n >= 65536) with under- / overflow buckets holding huge values of both signs
     (their fp64 sums enter the window bounds with a rigorous rounding margin)."""
