@@ -111,13 +111,22 @@ static int feistel_half(long long n) {
 
 __global__ void k_build_Z_identity(const double* __restrict__ Xc, long long n, int p, long long m, int q,
                                    const UniOut* __restrict__ uni, double* __restrict__ Z) {
-  // contiguous blocks: Z[b][k][s] = (Xc[k][b*m+s] - loc_k)/scale_k
-  const long long total = (long long)q * m;
+  // contiguous blocks: Z[b][k][s] = (Xc[k][b*m+s] - loc_k)/scale_k, block by block (no per-element
+  // 64-bit division of the flat index), 4 loads in flight per thread
   const int k = blockIdx.y;
   const double loc = uni[k].loc, sc = uni[k].scale;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    long long b = t / m, s = t - b * m;
-    Z[(b * p + k) * m + s] = __ddiv_rn(__dsub_rn(Xc[(long long)k * n + t], loc), sc);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int b = 0; b < q; b++) {
+    const double* __restrict__ src = Xc + (long long)k * n + (long long)b * m;
+    double* __restrict__ dst = Z + ((long long)b * p + k) * m;
+    for (long long s0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; s0 < m; s0 += 4 * stride) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) v[u] = s0 + u * stride < m ? __ldg(src + s0 + u * stride) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (s0 + u * stride < m) dst[s0 + u * stride] = __ddiv_rn(__dsub_rn(v[u], loc), sc);
+    }
   }
 }
 
@@ -142,8 +151,7 @@ void launch_build_Z(const double* Xc, const double* X, long long n, int p, int q
                     unsigned long long seed, int log_transform, const UniOut* uni, double* Z, long long* rowmap,
                     cudaStream_t st) {
   if (!perm) {
-    long long total = (long long)q * m;
-    unsigned gx = (unsigned)std::min<long long>((total + 255) / 256, 148 * 16);
+    const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((m + 1023) / 1024, 148 * 8));
     k_build_Z_identity<<<dim3(gx, p), 256, 0, st>>>(Xc, n, p, m, q, uni, Z);
   } else {
     long long total = (long long)q * m;
