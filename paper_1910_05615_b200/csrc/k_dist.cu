@@ -39,38 +39,72 @@ void upload_const(const double* dev_src, size_t count, cudaStream_t st) {
 // ------------------------------------------------------------------ transpose + validate
 static constexpr int TT_ROWS = 64;
 
-__global__ void __launch_bounds__(256) k_transpose(const double* __restrict__ X, long long n, int p, int log_transform,
-                                                   double* __restrict__ Xc, unsigned long long* __restrict__ bad) {
-  extern __shared__ double tile[];  // [TT_ROWS][p+1]
-  const long long r0 = (long long)blockIdx.x * TT_ROWS;
-  const int rows = (int)min((long long)TT_ROWS, n - r0);
-  const int S = p + 1;
-  const int cnt = rows * p;
+// Row-major X (optionally ln) -> column-major Xc through a shared-memory tile of TT_ROWS rows, with the
+// finiteness check (first bad row into *bad); p a compile-time constant (no runtime divisions), each CTA
+// walking several tiles; the tile's loads are issued back to back (unrolled, TT_ROWS * P / 256 each).
+template <int P>
+__global__ void __launch_bounds__(256) k_transpose_t(const double* __restrict__ X, long long n, int log_transform,
+                                                     double* __restrict__ Xc, unsigned long long* __restrict__ bad) {
+  constexpr int S = P + 1, CNT = TT_ROWS * P, PER = (CNT + 255) / 256;
+  __shared__ double tile[TT_ROWS * S];
   unsigned long long mybad = ~0ull;
-  for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-    int r = e / p, k = e - r * p;
-    double v = X[r0 * p + e];
-    bool ok = isfinite(v);
-    if (log_transform) {
-      ok = ok && v > 0.0;
-      v = log(v);
+  const long long ntiles = (n + TT_ROWS - 1) / TT_ROWS;
+  for (long long tb = blockIdx.x; tb < ntiles; tb += gridDim.x) {
+    const long long r0 = tb * TT_ROWS;
+    const int rows = (int)min((long long)TT_ROWS, n - r0);
+    const int cnt = rows * P;
+    double v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+      const int e = threadIdx.x + u * 256;
+      v[u] = e < cnt ? __ldg(X + r0 * P + e) : 0.0;
     }
-    if (!ok) mybad = min(mybad, (unsigned long long)(r0 + r));
-    tile[r * S + k] = v;
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+      const int e = threadIdx.x + u * 256;
+      if (e < cnt) {
+        const int r = e / P, k = e - r * P;
+        double x = v[u];
+        bool ok = isfinite(x);
+        if (log_transform) {
+          ok = ok && x > 0.0;
+          x = log(x);
+        }
+        if (!ok) mybad = min(mybad, (unsigned long long)(r0 + r));
+        tile[r * S + k] = x;
+      }
+    }
+    __syncthreads();
+    if (rows == TT_ROWS) {
+#pragma unroll
+      for (int u = 0; u < PER; u++) {
+        const int e = threadIdx.x + u * 256;
+        if (e < CNT) {
+          const int k = e / TT_ROWS, r = e - k * TT_ROWS;
+          Xc[(long long)k * n + r0 + r] = tile[r * S + k];
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < cnt; e += 256) {
+        const int k = e / rows, r = e - k * rows;
+        Xc[(long long)k * n + r0 + r] = tile[r * S + k];
+      }
+    }
+    __syncthreads();
   }
   if (mybad != ~0ull) atomicMin(bad, mybad);
-  __syncthreads();
-  for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
-    int k = e / rows, r = e - k * rows;
-    Xc[(long long)k * n + r0 + r] = tile[r * S + k];
-  }
+}
+
+template <int P>
+static void transpose_t_launch(const double* X, long long n, int log_transform, double* Xc, unsigned long long* bad,
+                               cudaStream_t st) {
+  const long long ntiles = (n + TT_ROWS - 1) / TT_ROWS;
+  k_transpose_t<P><<<(unsigned)std::min<long long>(ntiles, 148 * 12), 256, 0, st>>>(X, n, log_transform, Xc, bad);
 }
 
 void launch_transpose(const double* X, long long n, int p, int log_transform, double* Xc, unsigned long long* bad,
                       cudaStream_t st) {
-  long long grid = (n + TT_ROWS - 1) / TT_ROWS;
-  size_t sm = (size_t)TT_ROWS * (p + 1) * sizeof(double);
-  k_transpose<<<(unsigned)grid, 256, sm, st>>>(X, n, p, log_transform, Xc, bad);
+  RTD_DISPATCH_P(p, transpose_t_launch, X, n, log_transform, Xc, bad, st);
   RTD_LAUNCHED();
 }
 
