@@ -226,6 +226,14 @@ void run_unimcd(cudaStream_t st, char* scratch, size_t scratch_bytes, const doub
   unimcd_batch(a, st, cols, len, ncols, uni_const(len), out);
 }
 
+// H12 flagging of n rows; cs: the staged operator [mu | L^-1 packed] (also in the constant bank for k_flag)
+static void flag_rows(int p, const double* X, long long n, int log_transform, const double* cs, double c2,
+                      uint8_t* flags, double* rd2, cudaStream_t st) {
+  static const bool fma_only = getenv("RTD_FLAG_FMA") != nullptr;
+  if (p > 24 && n >= 65536 && !fma_only) launch_flag_mma(p, X, n, log_transform, cs, c2, flags, rd2, st);
+  else launch_flag(p, X, n, log_transform, c2, flags, rd2, st);
+}
+
 // ------------------------------------------------------------------ C-step engine
 struct CStepBufs {
   int ninst_max;
@@ -1104,7 +1112,7 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     upload_const(f.cb.cstage, cstride, st);
     if (want_flags) {
       ProfScope ps("flag", (double)n * (8.0 * p + 9.0));
-      launch_flag(p, Xdev, n, d.log, c2, f.flags_d, f.rd2_d, st);
+      flag_rows(p, Xdev, n, d.log, f.cb.cstage, c2, f.flags_d, f.rd2_d, st);
     }
   }
   // per-row weights and h-subset membership in original row order
@@ -1420,7 +1428,7 @@ rtdetmcd_status rtdetmcd_flag(rtdetmcd_ctx* c, const double* X, int64_t n, int32
     upload_const(cs, cstride, st);
     {
       ProfScope ps("flag", (double)n * (8.0 * p + 9.0));
-      launch_flag(p, Xd, n, log_transform ? 1 : 0, chi2_quantile(quantile, p), fh ? fd : flags, rh ? rdd : rd2, st);
+      flag_rows(p, Xd, n, log_transform ? 1 : 0, cs, chi2_quantile(quantile, p), fh ? fd : flags, rh ? rdd : rd2, st);
     }
     if (fh) RTD_CU(cudaMemcpyAsync(flags, fd, n, cudaMemcpyDeviceToHost, st));
     if (rh) RTD_CU(cudaMemcpyAsync(rd2, rdd, n * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -206,6 +206,117 @@ static void dist_mma_launch(const double* Zall, long long m, long long blk_strid
       Zall, m, blk_stride, inst, nstart, cstage, cstride, d2_all);
 }
 
+// H12 flagging pass on DMMA for row-major X: d_i^2 = ||M (x_i - mu)||^2, flags_i = d_i^2 > c2.  Each warp
+// streams its own tiles of 8 MB consecutive rows (contiguous in row-major X) into shared memory by
+// cp.async, two tiles per warp in flight (the next one copies while the current one is contracted), row
+// stride P + 1 so the A-fragment reads (8 rows x 4 columns per lane group) are conflict-free.  The
+// operator [mu | M packed lower] is read from the staged buffer cs.
+template <int P, int MB>
+__global__ void __launch_bounds__(256, 2) k_flag_mma(const double* __restrict__ X, long long n, int log_transform,
+                                                     const double* __restrict__ cs, double c2,
+                                                     uint8_t* __restrict__ flags, double* __restrict__ rd2) {
+  constexpr int KB = (P + 3) / 4, NB = (P + 7) / 8, S = P + 1, TR = 8 * MB, TE = TR * P;
+  __shared__ double bsm[KB * NB * 32];
+  __shared__ double musm[KB * 4];
+  extern __shared__ double xt[];  // [warp][2][TR * S]
+  for (int e = threadIdx.x; e < KB * NB * 32; e += blockDim.x) {
+    const int ln = e & 31, blk = e >> 5, kb = blk / NB, nb = blk - kb * NB;
+    const int k = 4 * kb + (ln & 3), j = 8 * nb + (ln >> 2);
+    bsm[e] = (j < P && k <= j) ? cs[P + j * (j + 1) / 2 + k] : 0.0;
+  }
+  for (int e = threadIdx.x; e < KB * 4; e += blockDim.x) musm[e] = e < P ? cs[e] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, w = threadIdx.x >> 5;
+  double* wbuf = xt + (size_t)w * 2 * TR * S;
+  const long long ntiles = (n + TR - 1) / TR;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  auto issue = [&](long long tile, int buf) {
+    if (tile < ntiles) {
+      const long long r0 = tile * TR;
+      const int cnt = (int)min((long long)TR, n - r0) * P;
+      double* dst = wbuf + buf * TR * S;
+      const double* src = X + r0 * P;
+      for (int e = lane; e < cnt; e += 32) {
+        const int r = e / P, k = e - r * P;
+        cp_async8(dst + r * S + k, src + e);
+      }
+    }
+    cp_async_commit();
+  };
+  long long tile = (long long)blockIdx.x * (blockDim.x >> 5) + w;
+  issue(tile, 0);
+  for (int it = 0; tile < ntiles; tile += nw, it++) {
+    issue(tile + nw, (it + 1) & 1);
+    cp_async_wait<1>();
+    __syncwarp();
+    const double* T = wbuf + (it & 1) * TR * S;
+    const long long r0 = tile * TR;
+    const int rows = (int)min((long long)TR, n - r0);
+    double acc[MB][NB][2];
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < KB; kb++) {
+      const int k = 4 * kb + t;
+      const double muk = musm[4 * kb + t];
+      double a[MB];
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++) {
+        const int r = mb * 8 + g;
+        double v = 0.0;
+        if (k < P && r < rows) {
+          v = T[r * S + k];
+          if (log_transform) v = log(v);
+          v = __dsub_rn(v, muk);
+        }
+        a[mb] = v;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        if (8 * nb + 7 < 4 * kb) continue;  // block entirely above the diagonal of M
+        const double bv = bsm[(kb * NB + nb) * 32 + lane];
+#pragma unroll
+        for (int mb = 0; mb < MB; mb++) dmma_8x8x4(acc[mb][nb][0], acc[mb][nb][1], a[mb], bv);
+      }
+    }
+#pragma unroll
+    for (int mb = 0; mb < MB; mb++) {
+      double s = 0.0;
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        s = fma(acc[mb][nb][0], acc[mb][nb][0], s);
+        s = fma(acc[mb][nb][1], acc[mb][nb][1], s);
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      const int r = mb * 8 + g;
+      if (t == 0 && r < rows) {
+        if (flags) flags[r0 + r] = s > c2 ? 1 : 0;
+        if (rd2) rd2[r0 + r] = s;
+      }
+    }
+    __syncwarp();  // the buffer just read is refilled by the next issue
+  }
+  cp_async_wait<0>();
+}
+
+template <int P>
+static void flag_mma_launch(const double* X, long long n, int log_transform, const double* cs, double c2,
+                            uint8_t* flags, double* rd2, cudaStream_t st) {
+  constexpr int MB = 2, S = P + 1, TR = 8 * MB;
+  const int smem = 8 * 2 * TR * S * (int)sizeof(double);
+  static const bool attr = [&] {
+    RTD_CU(cudaFuncSetAttribute(k_flag_mma<P, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    return true;
+  }();
+  (void)attr;
+  const long long tiles = (n + TR - 1) / TR;
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((tiles + 7) / 8, 296));
+  k_flag_mma<P, MB><<<grid, 256, smem, st>>>(X, n, log_transform, cs, c2, flags, rd2);
+}
+
 #define RTD_DISPATCH_P8(p, F, ...)                                                                          \
   switch (p) {                                                                                           \
     case 8: F<8>(__VA_ARGS__); break; case 9: F<9>(__VA_ARGS__); break; case 10: F<10>(__VA_ARGS__); break; \
@@ -227,6 +338,12 @@ bool dist_mma_supported(int p) { return p >= 8 && p <= RTD_MAXP; }
 void launch_dist_inv(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
                      int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st) {
   RTD_DISPATCH_P8(p, dist_inv_launch, Zall, m, blk_stride, inst, nstart, ninst, cstage, cstride, d2_all, st);
+  RTD_LAUNCHED();
+}
+
+void launch_flag_mma(int p, const double* X, long long n, int log_transform, const double* cs, double c2,
+                     uint8_t* flags, double* rd2, cudaStream_t st) {
+  RTD_DISPATCH_P8(p, flag_mma_launch, X, n, log_transform, cs, c2, flags, rd2, st);
   RTD_LAUNCHED();
 }
 

@@ -106,6 +106,9 @@ void launch_dist(int p, const double* Zall, long long m, long long blk_stride, c
 // out[j][i] = sum_k Z[k][i] * W[k][j], W full p x p in c_mat[0..p*p) (row-major k, j)
 void launch_matmul(int p, const double* Z, long long m, double* out, cudaStream_t st);
 // row-major flag pass: d2 = ||M (x - mu)||^2 with [mu][M] in c_mat slot 0
+// p >= 8: the flagging pass on DMMA, rows staged per warp by cp.async; operator read from cs
+void launch_flag_mma(int p, const double* X, long long n, int log_transform, const double* cs, double c2,
+                     uint8_t* flags, double* rd2, cudaStream_t st);
 void launch_flag(int p, const double* X, long long n, int log_transform, double c2, uint8_t* flags, double* rd2,
                  cudaStream_t st);
 void launch_norms(const double* Z, long long m, int p, int nblk, long long blk_stride, double* r, cudaStream_t st);
