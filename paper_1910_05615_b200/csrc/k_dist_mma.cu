@@ -212,7 +212,7 @@ static void dist_mma_launch(const double* Zall, long long m, long long blk_strid
 // stride P + 1 so the A-fragment reads (8 rows x 4 columns per lane group) are conflict-free.  The
 // operator [mu | M packed lower] is read from the staged buffer cs.
 template <int P, int MB>
-__global__ void __launch_bounds__(256, 2) k_flag_mma(const double* __restrict__ X, long long n, int log_transform,
+__global__ void __launch_bounds__(256, 4) k_flag_mma(const double* __restrict__ X, long long n, int log_transform,
                                                      const double* __restrict__ cs, double c2,
                                                      uint8_t* __restrict__ flags, double* __restrict__ rd2) {
   constexpr int KB = (P + 3) / 4, NB = (P + 7) / 8, S = P + 1, TR = 8 * MB, TE = TR * P;
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(256, 2) k_flag_mma(const double* __restrict__ 
 template <int P>
 static void flag_mma_launch(const double* X, long long n, int log_transform, const double* cs, double c2,
                             uint8_t* flags, double* rd2, cudaStream_t st) {
-  constexpr int MB = 2, S = P + 1, TR = 8 * MB;
+  constexpr int MB = 1, S = P + 1, TR = 8 * MB;
   const int smem = 8 * 2 * TR * S * (int)sizeof(double);
   static const bool attr = [&] {
     RTD_CU(cudaFuncSetAttribute(k_flag_mma<P, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -313,7 +313,7 @@ static void flag_mma_launch(const double* X, long long n, int log_transform, con
   }();
   (void)attr;
   const long long tiles = (n + TR - 1) / TR;
-  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((tiles + 7) / 8, 296));
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((tiles + 7) / 8, 592));
   k_flag_mma<P, MB><<<grid, 256, smem, st>>>(X, n, log_transform, cs, c2, flags, rd2);
 }
 
