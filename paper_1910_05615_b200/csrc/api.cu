@@ -446,7 +446,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
       if (!sw.empty()) {
         h2d(st, b.inst_dev, sw.data(), sw.size() * sizeof(int));
         ProfScope ps("smw", 0.0);
-        launch_smw_update(b.inst_dev, (int)sw.size(), Z, m, blk_stride, nstart, b.mu, memA, b.list, b.seg_cnt, b.ctas,
+        launch_smw_update(b.inst_dev, (int)sw.size(), Z, m, blk_stride, nstart, b.mu, b.list, b.seg_cnt, b.ctas,
                           b.seg_len, p, h, b.sinv, b.logdet, b.smw_valid, st);
       }
     }

@@ -540,7 +540,6 @@ void launch_prepare(const int* inst, int ninst, const double* mu_all, const doub
 __global__ void __launch_bounds__(64) k_smw_update(const int* __restrict__ inst, const double* __restrict__ Zall,
                                                    long long m, long long blk_stride, int nstart,
                                                    const double* __restrict__ mu_all,
-                                                   const uint8_t* __restrict__ mem_new_all,
                                                    const int* __restrict__ list_all, const int* __restrict__ seg_cnt_all,
                                                    int nseg, long long seg_len, int p, long long h,
                                                    double* __restrict__ sinv_all, double* __restrict__ logdet,
@@ -614,10 +613,10 @@ __global__ void __launch_bounds__(64) k_smw_update(const int* __restrict__ inst,
 }
 
 void launch_smw_update(const int* inst, int ninst, const double* Zall, long long m, long long blk_stride, int nstart,
-                       const double* mu_all, const uint8_t* mem_new_all, const int* list_all, const int* seg_cnt_all,
+                       const double* mu_all, const int* list_all, const int* seg_cnt_all,
                        int nseg, long long seg_len, int p, long long h, double* sinv_all, double* logdet,
                        int* smw_valid, cudaStream_t st) {
-  k_smw_update<<<ninst, 64, 0, st>>>(inst, Zall, m, blk_stride, nstart, mu_all, mem_new_all, list_all, seg_cnt_all,
+  k_smw_update<<<ninst, 64, 0, st>>>(inst, Zall, m, blk_stride, nstart, mu_all, list_all, seg_cnt_all,
                                      nseg, seg_len, p, h, sinv_all, logdet, smw_valid);
   RTD_LAUNCHED();
 }

@@ -13,7 +13,7 @@ void launch_prepare(const int* inst, int ninst, const double* mu_all, const doub
                     int traj_stride, int step, cudaStream_t st, int full_inverse = 0, const int* skip = nullptr);
 // SMW variant (single-swap inverse updates; k_linalg.cu)
 void launch_smw_update(const int* inst, int ninst, const double* Zall, long long m, long long blk_stride, int nstart,
-                       const double* mu_all, const uint8_t* mem_new_all, const int* list_all, const int* seg_cnt_all,
+                       const double* mu_all, const int* list_all, const int* seg_cnt_all,
                        int nseg, long long seg_len, int p, long long h, double* sinv_all, double* logdet,
                        int* smw_valid, cudaStream_t st);
 void launch_smw_stage(const int* inst, int ninst, const double* mu_all, const double* sigma_all, int p,
