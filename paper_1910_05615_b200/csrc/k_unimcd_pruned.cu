@@ -827,6 +827,7 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
       const bool geS = x >= c.tS0, geE = x >= c.tE0;
       ddacc_add(acc[k % NACC], (geS && !geE) ? x : 0.0);  // [bs_lo, be_lo); branch-free: adding 0 is exact
       const bool inS = geS && x < c.tS1, inE = geE && x < c.tE1;
+      if (!__any_sync(0xffffffffu, inS || inE)) continue;  // the common case: one vote, no candidate
       const unsigned ms = __ballot_sync(0xffffffffu, inS), me = __ballot_sync(0xffffffffu, inE);
 #pragma unroll
       for (int side = 0; side < 2; side++) {  // one shared atomic per warp and side
