@@ -479,3 +479,19 @@ def test_fit_batches_equal_single_fits():
         assert np.array_equal(np.asarray(g.rd2), np.asarray(s.rd2))
     with pytest.raises(ValueError):
         api.fit_batches([_cuda(Xs[0])])
+
+
+def test_fit_batches_c_abi_rejects_device_and_empty_batches():
+    """The C entry point itself refuses device batch pointers and nb <= 0 (RTD_E_INVALID_ARG)."""
+    import ctypes as C
+    from paper_1910_05615_b200._lib import Opts, Result, lib
+    ctx = api._ctx(0)
+    X = _cuda(datagen.gaussian(1000, 5, seed=2))
+    o = api.default_opts()
+    r = Result()
+    ptrs = (C.c_void_p * 1)(X.data_ptr())
+    assert lib().rtdetmcd_fit_batches(ctx["h"], ptrs, 1, 1000, 5, C.byref(o), C.byref(r)) != 0
+    assert lib().rtdetmcd_fit_batches(ctx["h"], ptrs, 0, 1000, 5, C.byref(o), C.byref(r)) != 0
+    # the context stays usable
+    g = api.fit(X, h=600)
+    assert np.isfinite(g.sigma_rew).all()
