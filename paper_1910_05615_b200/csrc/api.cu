@@ -339,7 +339,7 @@ void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long
 
 // Runs lock-step C-steps for the instances whose status is ST_ACTIVE on entry.
 // On exit: status ST_CONVERGED / ST_MAXSTEPS (usable) or a failure code;
-// mu/sigma = exact mean / covariance of the final h-subset (in memA), logdet.
+// mu/sigma = mean / covariance of the final h-subset (in memA; update-based, reading R12), logdet.
 void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_stride, int nstart, int ninst, long long h,
                 double kappa_max, int max_steps, int refresh, std::vector<int>& status_h, std::vector<int>& steps_h,
                 int dist_mode = RTD_DIST_CHOLESKY) {
@@ -466,14 +466,19 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     if (status_h[i] == ST_ACTIVE) status_h[i] = ST_MAXSTEPS;
   // both buffers hold H for converged instances; make memA the final subset for every instance
   if (memA != b.memA) RTD_CU(cudaMemcpyAsync(b.memA, memA, (size_t)ninst * m, cudaMemcpyDeviceToDevice, st));
-  // exact recompute of mean / covariance over the final subsets (reading R12) -- for the start of each
+  // optional exact recompute of mean / covariance over the final subsets (RTD_FINAL_EXACT) -- for the start of each
   // block that wins the lower-determinant choice: the update-based log det of every finished start is
   // within ~1e-13 of the exact one (measured on configs 1-4, |ld| ~ 6..33), so it decides the choice
   // unless the two starts are within 1e-11 relative (then both are recomputed); two starts that reached
   // the same h-subset share one recompute; the losing start keeps its update-based estimate
+  // Default (reading R12): no recompute -- the converged (mu, Sigma) are the update-based ones, as in the
+  // paper's loop (the update loop replaces eqs. cstep4a/b and Lambda_new / (h - 1) is
+  // scaled after convergence); they sit within ~1e-14 of the plain recompute (refresh every 32 steps
+  // bounds the drift).  RTD_FINAL_EXACT=1 recomputes them exactly as described above.
   std::vector<int> fin, twins_out;
+  static const bool final_exact = getenv("RTD_FINAL_EXACT") != nullptr;
   for (int i = 0; i < ninst; i++)
-    if (status_h[i] == ST_CONVERGED || status_h[i] == ST_MAXSTEPS) fin.push_back(i);
+    if (final_exact && (status_h[i] == ST_CONVERGED || status_h[i] == ST_MAXSTEPS)) fin.push_back(i);
   if (!fin.empty() && nstart == 2) {
     h2d(st, b.inst_dev, fin.data(), fin.size() * sizeof(int));
     launch_prepare(b.inst_dev, (int)fin.size(), b.mu, b.sigma, p, kappa_max, nullptr, 0, b.logdet, b.cond, nullptr,
