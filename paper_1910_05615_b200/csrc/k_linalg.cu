@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(LT) k_jacobi(const double* __restrict__ A_all,
   __shared__ int pa[RTD_MAXP / 2 + 1], qa[RTD_MAXP / 2 + 1];
   __shared__ int order[RTD_MAXP + 2];
   __shared__ double red[LT];
-  __shared__ int s_stop;
+  __shared__ int s_stop, s_rot;
   const int b = blockIdx.x, t = threadIdx.x;
   const double* Ain = A_all + (long long)b * RTD_MAXP * RTD_MAXP;
   for (int e = t; e < p * p; e += blockDim.x) {
@@ -779,18 +779,32 @@ __global__ void __launch_bounds__(LT) k_jacobi(const double* __restrict__ A_all,
       }
       s_stop = (so <= 1e-32 * st) || so == 0.0;
     }
+    if (t == 0) s_rot = 0;
     __syncthreads();
     if (s_stop) break;
     for (int round = 0; round < n2 - 1; round++) {
       if (t < n2 / 2) {
-        int P = order[t], Q = order[n2 - 1 - t];
+        // round-robin positions: 0 fixed, 1..n2-1 rotated right by one per round (period n2 - 1, so every
+        // sweep starts from the identity); computed, not stored, so no thread shifts a shared array
+        auto ord = [&](int k) { return k == 0 ? 0 : 1 + ((k - 1 - round) % (n2 - 1) + (n2 - 1)) % (n2 - 1); };
+        int P = ord(t), Q = ord(n2 - 1 - t);
         if (P > Q) { int tmp = P; P = Q; Q = tmp; }
         double c = 1.0, s = 0.0;
-        if (Q < p && A[P][Q] != 0.0) {
-          double apq = A[P][Q];
-          double tau = (A[Q][Q] - A[P][P]) / (2.0 * apq);
-          double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + tt * tt);
+        if (Q < p && A[P][Q] != 0.0 && 1e18 * fabs(A[P][Q]) <= fmin(fabs(A[P][P]), fabs(A[Q][Q]))) {
+          // below the rounding of both diagonal entries (the classical threshold test): dropped, so a
+          // sweep can end without rotations and the loop terminates
+          A[P][Q] = 0.0;
+          A[Q][P] = 0.0;
+        } else if (Q < p && A[P][Q] != 0.0) {
+          s_rot = 1;
+          // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = h / a_pq, h = (a_qq - a_pp) / 2, written
+          // without the first division: t = sign(tau) |a_pq| / (|h| + sqrt(h^2 + a_pq^2)); c = rsqrt(1 + t^2)
+          // (a shorter chain of the slow fp64 operations on the critical path of every round)
+          const double apq = A[P][Q];
+          const double hh = 0.5 * (A[Q][Q] - A[P][P]);
+          const bool pos = hh == 0.0 || ((hh > 0.0) == (apq > 0.0));
+          const double tt = (pos ? fabs(apq) : -fabs(apq)) / (fabs(hh) + sqrt(fma(hh, hh, apq * apq)));
+          c = rsqrt(fma(tt, tt, 1.0));
           s = tt * c;
         }
         pa[t] = P;
@@ -799,29 +813,32 @@ __global__ void __launch_bounds__(LT) k_jacobi(const double* __restrict__ A_all,
         sn[t] = s;
       }
       __syncthreads();
-      // rows: A <- P^T A
-      for (int e = t; e < (n2 / 2) * p; e += blockDim.x) {
-        int k = e / p, j = e - k * p;
-        int P = pa[k], Q = qa[k];
+      // rows: A <- P^T A (pair k per warp, column j per lane: no integer division per element)
+      const int npr = n2 / 2, nwp = blockDim.x >> 5, wid = t >> 5, ln = t & 31;
+      for (int k = wid; k < npr; k += nwp) {
+        const int P = pa[k], Q = qa[k];
         if (Q >= p || sn[k] == 0.0) continue;
-        double c = cs[k], s = sn[k];
-        double ap = A[P][j], aq = A[Q][j];
-        A[P][j] = c * ap - s * aq;
-        A[Q][j] = s * ap + c * aq;
+        const double c = cs[k], s = sn[k];
+        for (int j = ln; j < p; j += 32) {
+          const double ap = A[P][j], aq = A[Q][j];
+          A[P][j] = c * ap - s * aq;
+          A[Q][j] = s * ap + c * aq;
+        }
       }
       __syncthreads();
-      // columns: A <- A P, V <- V P
-      for (int e = t; e < (n2 / 2) * p; e += blockDim.x) {
-        int k = e / p, i = e - k * p;
-        int P = pa[k], Q = qa[k];
+      // columns: A <- A P, V <- V P (pair k per warp, row i per lane)
+      for (int k = wid; k < npr; k += nwp) {
+        const int P = pa[k], Q = qa[k];
         if (Q >= p || sn[k] == 0.0) continue;
-        double c = cs[k], s = sn[k];
-        double ap = A[i][P], aq = A[i][Q];
-        A[i][P] = c * ap - s * aq;
-        A[i][Q] = s * ap + c * aq;
-        double vp = V[i][P], vq = V[i][Q];
-        V[i][P] = c * vp - s * vq;
-        V[i][Q] = s * vp + c * vq;
+        const double c = cs[k], s = sn[k];
+        for (int i = ln; i < p; i += 32) {
+          const double ap = A[i][P], aq = A[i][Q];
+          A[i][P] = c * ap - s * aq;
+          A[i][Q] = s * ap + c * aq;
+          const double vp = V[i][P], vq = V[i][Q];
+          V[i][P] = c * vp - s * vq;
+          V[i][Q] = s * vp + c * vq;
+        }
       }
       __syncthreads();
       if (t < n2 / 2) {
@@ -831,14 +848,9 @@ __global__ void __launch_bounds__(LT) k_jacobi(const double* __restrict__ A_all,
           A[Q][P] = 0.0;
         }
       }
-      // rotate the round-robin order (position 0 fixed)
-      if (t == 0) {
-        int last = order[n2 - 1];
-        for (int k = n2 - 1; k > 1; k--) order[k] = order[k - 1];
-        order[1] = last;
-      }
       __syncthreads();
     }
+    if (!s_rot) break;  // a sweep without a rotation: converged
   }
   // sort eigenvalues descending (stable), normalise signs
   if (t == 0) {
