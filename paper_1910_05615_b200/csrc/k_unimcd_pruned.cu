@@ -30,7 +30,7 @@
 namespace rtd {
 
 static constexpr int NBK = 4096;         // buckets per column (incl. underflow 0 and overflow NBK-1)
-static constexpr int SAMPLE = 4096;      // strided sample for the bucket map
+static constexpr int SAMPLE = 2048;      // strided sample for the bucket map
 static constexpr int CAP = 65536;        // max gathered elements per side per column
 static constexpr int PCTA = 32;          // CTAs per column in the streaming passes (fixed -> deterministic)
 static constexpr int PT = 256;
