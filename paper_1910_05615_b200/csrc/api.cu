@@ -25,6 +25,7 @@ void launch_dist_mma(int p, const double* Zall, long long m, long long blk_strid
 long long launch_count();
 long long sort_count();
 void launch_moments_mma(int mode, const MomArgs& a, int ninst, cudaStream_t st);
+bool moments_staged(int mode, const MomArgs& a);  // staged kernel (MOM_WRAP there also writes a.r_out)
 void launch_matmul_mma_pairs(int p, const double* Zall, long long m, long long blk_stride, const int* slot_of,
                              const int* blk_of_slot, const int* pairs, int npairs, const double* W_all,
                              double* out_all, cudaStream_t st);
@@ -707,11 +708,15 @@ void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int
   a.ctas = b.ctas;
   // S~1: covariance of the wrapped data (centred at the wrapped mean, n - 1)
   ProfScope ps("initial", (double)q * m * p * 16.0);
+  // the staged wrap pass also writes the row norms of S~2 (one read of Z less)
+  const bool fused_norms = use_mma() && moments_staged(MOM_WRAP, a);
+  if (fused_norms) a.r_out = b.r;
   moments(MOM_WRAP, a, q, st);
+  a.r_out = nullptr;
   launch_mom_reduce(b.partial, q, b.inst_dev, b.ctas, np, b.sums, 0, st);
   launch_sums_to_cov(b.inst_dev, q, b.sums, np, nullptr, p, (double)m, 1.0, b.mudummy, b.S1, st);
   // S~2: norms, type-7 cutoffs, xi^2-weighted second moment / n
-  launch_norms(Z, m, p, q, blk_stride, b.r, st);
+  if (!fused_norms) launch_norms(Z, m, p, q, blk_stride, b.r, st);
   // exact order statistics of the norms by bucketing (k_quantile.cu); blocks with massive ties are sorted
   std::vector<int> fb;
   launch_quantiles(b.r, m, q, b.qscratch, b.qv, st, fb);

@@ -179,6 +179,21 @@ __global__ void __launch_bounds__(MW * 32, 2) k_moments_st(MomArgs a) {
     const int stg = tile % NST;
     const double* T = tiles + (size_t)stg * p * SLD;
     const double* W = wts + stg * SR;
+    if (MODE == MOM_WRAP && a.r_out) {
+      // the norms ||z_i|| of the tile's rows for S~2 from the raw tile, before psi:
+      // 4 threads per row, fixed-order combination
+      const int row = tid >> 2, part = tid & 3;
+      const int rows_n = (int)min((long long)SR, r_end - (r_begin + (long long)tile * SR));
+      double sq = 0.0;
+      for (int k = part; k < p; k += 4) {
+        const double v = T[k * SLD + row];
+        sq = __dadd_rn(sq, __dmul_rn(v, v));
+      }
+      sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, 1));
+      sq = __dadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, 2));
+      if (part == 0 && row < rows_n) a.r_out[(long long)blk * m + r_begin + (long long)tile * SR + row] = __dsqrt_rn(sq);
+      __syncthreads();  // the raw tile is read before psi overwrites it
+    }
     if (MODE == MOM_WRAP) {
       // psi of the tile in place: identity and zero branches directly, the tanh
       // branch (b < |z| <= c, a minority of the entries) compacted into a list and evaluated once per
@@ -386,6 +401,11 @@ static void moments_mma_nb(int mode, const MomArgs& a, int ninst, cudaStream_t s
     RTD_MM_CASE(MOM_REWEIGHT)
   }
 #undef RTD_MM_CASE
+}
+
+bool moments_staged(int mode, const MomArgs& a) {
+  static const bool unstaged = getenv("RTD_MOM_UNSTAGED") != nullptr;
+  return mode != MOM_DELTA && (a.p + 7) / 8 >= 4 && a.m >= 65536 && !unstaged;
 }
 
 void launch_moments_mma(int mode, const MomArgs& a, int ninst, cudaStream_t st) {

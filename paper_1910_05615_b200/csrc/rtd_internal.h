@@ -137,6 +137,7 @@ struct MomArgs {
   const double* d2;         // [inst][m] (reweight)
   double c2;
   const double* r;          // [block][m] norms (xi mode)
+  double* r_out;            // [block][m] norms written by the staged wrap pass (nullable)
   const double* AB;         // [block][2] cutoffs (xi mode)
   double* partial;          // [slot][cta][NP]
   int ctas;                 // CTAs per instance
