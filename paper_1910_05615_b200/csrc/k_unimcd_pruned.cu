@@ -33,6 +33,7 @@ static constexpr int NBK = 4096;         // buckets per column (incl. underflow 
 static constexpr int SAMPLE = 2048;      // strided sample for the bucket map
 static constexpr int CAP = 65536;        // max gathered elements per side per column
 static constexpr int PCTA = 32;          // CTAs per column in the streaming passes (fixed -> deterministic)
+static constexpr long long PACK_LEN = 1LL << 24;  // below: hist flushes count + offset sum in one 64-bit atomic
 static constexpr int PT = 256;
 static constexpr int LT = 512;    // k_pr_locate threads (one CTA per column)
 
@@ -262,10 +263,15 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
   __syncthreads();
   int* cn = cnt + (long long)col * NBK;
   unsigned long long* tqc = tq + (long long)col * NBK;
+  const bool packed = len < PACK_LEN;  // count (bits 40..63) + offset sum (< len 2^16 <= 2^40) in one word
   for (int b = threadIdx.x; b < NBK; b += PT)
     if (hc[b]) {
-      atomicAdd(&cn[b], (int)hc[b]);
-      if (hq[b]) atomicAdd(&tqc[b], (unsigned long long)hq[b]);
+      if (packed) {
+        atomicAdd(&tqc[b], ((unsigned long long)hc[b] << 40) | (unsigned long long)hq[b]);
+      } else {
+        atomicAdd(&cn[b], (int)hc[b]);
+        if (hq[b]) atomicAdd(&tqc[b], (unsigned long long)hq[b]);
+      }
     }
 }
 
@@ -295,7 +301,8 @@ __device__ __forceinline__ void bucket_sum_interval(int b, int r, unsigned long 
   }
 }
 
-__device__ __forceinline__ void scan_column(PrunedCol& c, const int* __restrict__ cn, const unsigned long long* __restrict__ tqc,
+__device__ __forceinline__ void scan_column(PrunedCol& c, bool packed, const int* __restrict__ cn,
+                                            const unsigned long long* __restrict__ tqc,
                                             const double* __restrict__ es, long long* C, double* sblo, double* A1lo,
                                             double* Q2lo, double* Q2hi, BucketScan& bs) {
   __shared__ double red_d[32];
@@ -306,13 +313,16 @@ __device__ __forceinline__ void scan_column(PrunedCol& c, const int* __restrict_
   double* A1hi = A1lo + (NBK + 1);
   constexpr int per = NBK / LT, NW = LT / 32;
   double slo[per], shi[per], qlo[per], qhi[per];
+  int rr[per];
   long long lc = 0;
   double l1 = 0.0, lh = 0.0, llo = 0.0, lhi = 0.0, abs1 = 0.0;
 #pragma unroll
   for (int e = 0; e < per; e++) {
     const int b = t * per + e;
-    const int r = cn[b];
-    bucket_sum_interval(b, r, tqc[b], es, c, slo[e], shi[e]);
+    const unsigned long long tw = tqc[b];
+    const int r = packed ? (int)(tw >> 40) : cn[b];
+    rr[e] = r;
+    bucket_sum_interval(b, r, packed ? (tw & ((1ull << 40) - 1ull)) : tw, es, c, slo[e], shi[e]);
     sblo[b] = slo[e];
     sbhi[b] = shi[e];
     const double L = bucket_lo(b, c), U = bucket_hi(b, c), rd = (double)r;
@@ -392,7 +402,7 @@ __device__ __forceinline__ void scan_column(PrunedCol& c, const int* __restrict_
     A1hi[b] = eh;
     Q2lo[b] = elo;
     Q2hi[b] = ehi;
-    ec += cn[b];
+    ec += rr[e];
     e1 += slo[e];
     eh += shi[e];
     elo += qlo[e];
@@ -600,7 +610,7 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
   if (c.status) return;
   c.cmin = ord_val(mm[2 * col]);
   c.cmax = ord_val(mm[2 * col + 1]);
-  scan_column(c, cnt + (long long)col * NBK, tq + (long long)col * NBK, esum + 4 * col, S.C, S.sb, S.A1, S.Q2lo,
+  scan_column(c, len < PACK_LEN, cnt + (long long)col * NBK, tq + (long long)col * NBK, esum + 4 * col, S.C, S.sb, S.A1, S.Q2lo,
               S.Q2hi, bs);
   const long long* C = S.C;
   const BucketScan m = bs;
