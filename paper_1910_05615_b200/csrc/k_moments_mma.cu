@@ -591,7 +591,7 @@ static void matmul_pair_nb(const double* Z, long long m, int p, long long blk_st
   }
   constexpr int MB = 2;
   const long long tiles = (m + 8 * MB - 1) / (8 * MB);
-  const unsigned grid = (unsigned)std::min<long long>((tiles + 7) / 8, std::max(1, 148 * 2 / std::max(1, npairs)));
+  const unsigned grid = (unsigned)std::min<long long>((tiles + 7) / 8, std::max(1, 148 * 8 / std::max(1, npairs)));
   k_matmul_pair<NB, MB, 1><<<dim3(grid, npairs), 256, 0, st>>>(Z, m, p, blk_stride, slot_of, blk_of_slot, pairs, W,
                                                                out);
 }
