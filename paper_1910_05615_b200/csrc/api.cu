@@ -331,7 +331,7 @@ void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long
   const int cap = std::max(1, RTD_CONST_DOUBLES / std::max(1, cstride));
   for (int g0 = 0; g0 < nact; g0 += cap) {
     const int cnt = std::min(cap, nact - g0);
-    upload_const(b.cstage + (size_t)g0 * cstride, (size_t)cnt * cstride, st);
+    ConstLease lease(b.cstage + (size_t)g0 * cstride, (size_t)cnt * cstride, st);
     ProfScope ps("dist", (double)cnt * fm * (8.0 * pp + 8.0), (double)cnt * fm * (pp * (pp + 1.0) + 2.0 * pp),
                  (double)cnt * fm * (8.0 * pp + 8.0));
     launch_dist(b.p, Z, b.m, blk_stride, b.inst_dev + g0, nstart, cnt, cstride, b.d2, st);
@@ -603,7 +603,7 @@ static void refine_matmul(cudaStream_t st, RefineBufs& r, const double* Zall, lo
     return;
   }
   for (int i = 0; i < nitems; i++) {
-    upload_const(W_all + (size_t)items[i] * M2, (size_t)p * p, st);
+    ConstLease lease(W_all + (size_t)items[i] * M2, (size_t)p * p, st);
     launch_matmul(p, Zall + (size_t)blk[items[i]] * blk_stride, m, r.T + (size_t)i * p * m, st);
   }
 }
@@ -1016,7 +1016,7 @@ void phase_reweight_blocks(cudaStream_t st, FitBufs& f, int p, int q, long long 
     if (dist_mma_supported(p)) {
       launch_dist_mma(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, f.cb.cstage, 0, f.cb.d2, st);
     } else {
-      upload_const(f.cb.cstage, cstride, st);
+      ConstLease lease(f.cb.cstage, cstride, st);
       launch_dist(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, 0, f.cb.d2, st);
     }
   }
@@ -1119,8 +1119,8 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     RTD_CU(cudaMemsetAsync(f.st1 + 1, 0, sizeof(int), st));
     launch_prepare(f.ids_dev, 1, f.muX + RTD_MAXP, f.sigX + M2, p, 1e300, f.cb.cstage, cstride, nullptr, nullptr,
                    f.st1 + 1, nullptr, 0, 0, st);
-    upload_const(f.cb.cstage, cstride, st);
     if (want_flags) {
+      ConstLease lease(f.cb.cstage, cstride, st);
       ProfScope ps("flag", (double)n * (8.0 * p + 9.0));
       flag_rows(p, Xdev, n, d.log, f.cb.cstage, c2, f.flags_d, f.rd2_d, st);
     }
@@ -1376,6 +1376,12 @@ rtdetmcd_status rtdetmcd_fit_batches(rtdetmcd_ctx* c, const double* const* X, in
       RTD_CU(cudaMemcpyAsync(c->xbuf[b & 1], X[b], bytes, cudaMemcpyHostToDevice, c->copy_stream));
       RTD_CU(cudaEventRecord(c->ev_copied[b & 1], c->copy_stream));
     };
+    // on every exit (including a failing batch) wait for the copy stream, so no DMA still reads a
+    // caller's host buffer after the call returns
+    struct CopyDrain {
+      cudaStream_t s;
+      ~CopyDrain() { cudaStreamSynchronize(s); }
+    } drain{c->copy_stream};
     copy(0);
     for (int b = 0; b < nb; b++) {
       // the buffer of batch b + 1 last held batch b - 1, whose fit has returned (fits are synchronous)
@@ -1435,8 +1441,8 @@ rtdetmcd_status rtdetmcd_flag(rtdetmcd_ctx* c, const double* X, int64_t n, int32
     int stv = 0;
     d2h(st, &stv, stt, sizeof(int));
     if (stv == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "sigma is not positive definite"};
-    upload_const(cs, cstride, st);
     {
+      ConstLease lease(cs, cstride, st);
       ProfScope ps("flag", (double)n * (8.0 * p + 9.0));
       flag_rows(p, Xd, n, log_transform ? 1 : 0, cs, chi2_quantile(quantile, p), fh ? fd : flags, rh ? rdd : rd2, st);
     }

@@ -6,6 +6,7 @@
 // instance), compile-time P so the triangular mat-vec is fully unrolled:
 // P(P+1)/2 + P DFMA per row, X read once, coalesced (Z is column-major).
 #include <cmath>
+#include <mutex>
 
 #include "rtd_internal.h"
 
@@ -13,8 +14,32 @@ namespace rtd {
 
 __constant__ double c_mat[RTD_CONST_DOUBLES];
 
-void upload_const(const double* dev_src, size_t count, cudaStream_t st) {
-  RTD_CU(cudaMemcpyToSymbolAsync(c_mat, dev_src, count * sizeof(double), 0, cudaMemcpyDeviceToDevice, st));
+namespace {
+struct DevConst {
+  std::mutex mu;
+  cudaEvent_t done = nullptr;  // completion of the last lease's consumers (any stream)
+};
+DevConst g_const[128];
+}  // namespace
+
+ConstLease::ConstLease(const double* dev_src, size_t count, cudaStream_t st) : st_(st) {
+  RTD_CU(cudaGetDevice(&dev_));
+  DevConst& g = g_const[dev_ & 127];
+  g.mu.lock();
+  try {
+    if (!g.done) RTD_CU(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
+    else RTD_CU(cudaStreamWaitEvent(st, g.done, 0));
+    RTD_CU(cudaMemcpyToSymbolAsync(c_mat, dev_src, count * sizeof(double), 0, cudaMemcpyDeviceToDevice, st));
+  } catch (...) {
+    g.mu.unlock();
+    throw;
+  }
+}
+
+ConstLease::~ConstLease() {
+  DevConst& g = g_const[dev_ & 127];
+  cudaEventRecord(g.done, st_);
+  g.mu.unlock();
 }
 
 #define RTD_DISPATCH_P(p, F, ...)                                                                        \

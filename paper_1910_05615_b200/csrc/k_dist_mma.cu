@@ -7,7 +7,7 @@
 // of X, at the FP64 ridge, so instruction issue decides: one DMMA does 256 FMA
 // where a DFMA does 32, and the operator M = L^-1 (lower triangular) lives in
 // registers as B fragments for the whole kernel.  Blocks of M^T that are
-// entirely above the diagonal are skipped (30 of 50 8x4 blocks at p = 40).
+// entirely above the diagonal are skipped (20 of 50 8x4 blocks at p = 40; 30 are executed).
 //
 // Fragment layout of m8n8k4 f64 (g = lane >> 2, t = lane & 3):
 //   A (8 x 4, rows x k):  A[g][t]          -> (Z - mu)[row0 + g][4 kb + t]
@@ -178,7 +178,9 @@ __global__ void __launch_bounds__(256, 2) k_dist_inv(const double* __restrict__ 
       }
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
-      if (t == 0 && row < m) d2[row] = s;
+      // a full quadratic form can round (or, under a drifted SMW inverse, fall) below zero; the select's
+      // keys take the IEEE bits of d^2 >= 0, so clamp (this also maps -0.0 to +0.0)
+      if (t == 0 && row < m) d2[row] = fmax(s, 0.0);
     }
   }
 }

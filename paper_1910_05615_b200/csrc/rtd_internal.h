@@ -86,8 +86,22 @@ double chi2_quantile(double prob, int dof);
 double consistency_factor(double alpha, int p);
 
 // ---------------------------------------------------------------- constant bank
-// the constant bank c_mat lives in k_dist.cu (its only reader); filled by upload_const
-void upload_const(const double* dev_src, size_t count, cudaStream_t st);
+// the constant bank c_mat lives in k_dist.cu (its only reader).  It is one per device and process, so
+// several contexts (streams) must not overwrite it while another's kernel reads it: a ConstLease holds a
+// per-device lock from the upload until it goes out of scope (after the consuming launches are enqueued),
+// makes its stream wait for the previous lease's consumers, and records their completion on release.
+// Keep a lease alive exactly around the launches that read c_mat; never nest two.
+class ConstLease {
+ public:
+  ConstLease(const double* dev_src, size_t count, cudaStream_t st);
+  ~ConstLease();
+  ConstLease(const ConstLease&) = delete;
+  ConstLease& operator=(const ConstLease&) = delete;
+
+ private:
+  int dev_ = 0;
+  cudaStream_t st_;
+};
 
 // ---------------------------------------------------------------- streaming kernels (k_dist.cu)
 // X row-major n x p -> Xc column-major; nonfinite (or <= 0 when log) rows -> min index in *bad.

@@ -233,3 +233,17 @@ def test_median_consistency_rule_invariant():
     assert np.allclose(r, r[0, 0], rtol=1e-12)  # a scalar multiple
     with pytest.raises(F.FitError):
         F.fit(d.X, h=d.h, consistency="other")
+
+
+def test_reweighted_consistency_factor_p2():
+    # Reading R17: Sigma_rew = c(0.975, p) * classical covariance of the
+    # weighted rows.  On clean N(0, Sigma) data the reweighted RD^2 is then ~ chi2_p, so the flag rate
+    # is 1 - 0.975 = 0.025 (binomial sd 0.00035 at n = 200k); without the factor it would be
+    # P(chi2_2 > chi2_{2,.975} / c) = exp(-7.3778 / 2 / 1.1045) = 0.0354 at p = 2.  Also Sigma_rew
+    # itself must estimate the generating Sigma (it is 1/1.1045 of it without the factor).
+    S = np.array([[2.0, 0.6], [0.6, 0.5]])
+    X = datagen.gaussian(200_000, 2, seed=41, sigma=S)
+    r = F.fit(X, alpha=0.75)
+    assert abs(r.flags.mean() - 0.025) < 0.0025
+    ratio = np.trace(np.linalg.solve(S, r.Sigma_rew)) / 2
+    assert abs(ratio - 1.0) < 0.02

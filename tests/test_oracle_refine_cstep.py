@@ -113,3 +113,36 @@ def test_mahalanobis_invariant_under_affine():
     d1 = mahalanobis_sq(Z, mu, S)
     d2 = mahalanobis_sq(Z @ A.T + b, A @ mu + b, A @ S @ A.T)
     assert np.allclose(d1, d2, rtol=1e-10)
+
+
+def test_refine_translation_equivariance_nonidentity():
+    # PAPER.md:594-605 (§3.3 step 4): Z~ = Z Sigma_k^{-1/2} and mu_k = Sigma_k^{1/2} mu~.  The univariate
+    # MCD is translation equivariant and the scores' scales are not, so refine(S, Z + a) = (mu + a, Sigma).
+    # With a non-identity Sigma_k, the wrong back-transform (Sigma^{-1/2} instead of Sigma^{1/2}) gives
+    # mu + Sigma^{-1} a instead.
+    rng = np.random.default_rng(31)
+    Q, _ = np.linalg.qr(rng.standard_normal((4, 4)))
+    S = (Q * np.array([9.0, 4.0, 1.0, 0.25])) @ Q.T
+    Z = datagen.gaussian(20_000, 4, seed=32, sigma=S)
+    a = np.array([3.0, -2.0, 0.5, 7.0])
+    r0 = refine(S, Z)
+    r1 = refine(S, Z + a)
+    assert np.abs(np.diag(r0.Sigma) - 1.0).max() > 0.5          # far from the identity
+    assert np.allclose(r1.mu, r0.mu + a, rtol=0, atol=1e-9)
+    assert np.allclose(r1.Sigma, r0.Sigma, rtol=1e-9)
+    # scale equivariance: refine(S, c Z) = (c mu, c^2 Sigma) for c a power of two (exact)
+    r2 = refine(S, 4.0 * Z)
+    assert np.allclose(r2.mu, 4.0 * r0.mu, rtol=1e-12, atol=1e-13)
+    assert np.allclose(r2.Sigma, 16.0 * r0.Sigma, rtol=1e-12)
+
+
+def test_refine_p1_is_the_reweighted_univariate_mcd():
+    # p = 1: V = [1], T = Z, Sigma = sigma_uni^2(Z), mu = sigma * mu_uni(Z / sigma) = mu_uni(Z).  Reading R8
+    # ("univariate MCD" = the reweighted estimator of §3.1).  SPEC.md:164's worked
+    # example x = (0,1,2,3,4,1000): the reweighted MCD keeps {0..4}, so mu = 2 and
+    # Sigma = c(0.975,1) * 2.5 with c(0.975,1) = 1.174778641565 (pinned in
+    # tests/test_oracle_chi2.py).  The raw estimator would give mu = 1.5 (window {0,1,2,3}, lowest start).
+    Z = np.array([0.0, 1.0, 2.0, 3.0, 4.0, 1000.0])[:, None]
+    r = refine(np.eye(1), Z)
+    assert r.mu[0] == pytest.approx(2.0, rel=1e-14)
+    assert r.Sigma[0, 0] == pytest.approx(1.174778641565 * 2.5, rel=1e-11)

@@ -132,3 +132,53 @@ def test_breakdown():
     y[: 1001 - (1001 // 2 + 1)] = 1e9
     bad = unimcd_reweighted(y)
     assert abs(bad.loc - base.loc) < 5 * base.scale
+
+
+def _adversarial_column(seed, n=100_001, k=10, D=1.0):
+    """Mirror-symmetric middle block (k points at -D, a symmetric core, k points at +D) flanked by
+    asymmetric tails (L points near -1e12, R = L + 2*skew + 1 points near +1e3); the windows that avoid
+    the tails are the k + 1 middle ones, and by symmetry the two end windows tie exactly as the optimum
+    (SQ(j) = k D^2 - ((k - 2j) D)^2 / h + core terms).  One +D point nudged one ulp inward makes the
+    LAST middle window the unique exact optimum by ~4e-16 absolute on an SQ of ~10: below fp64
+    resolution, and the tails' rounding (~1e13 in the prefix sums of squares) swamps it.  A plain
+    fp64 prefix-sum argmin picks a window far off (checked: s = 50000); only a rigorous screening
+    margin plus exact evaluation of the shortlist (reading R2) finds it."""
+    rng = np.random.default_rng(seed)
+    h = n // 2 + 1
+    M = h + k
+    L = (n - M) // 2 - 3
+    R = n - M - L
+    c = np.sort(rng.uniform(-1e-3, 1e-3, (M - 2 * k) // 2))
+    core = np.concatenate([-c[::-1], [0.0] * ((M - 2 * k) % 2), c])
+    mid = np.concatenate([np.full(k, -D), core, np.full(k, D)])
+    mid[-1] = np.nextafter(D, 0.0)
+    x = np.concatenate([-1e12 * (1 + rng.uniform(0, 1, L)), mid, 1e3 * (1 + rng.uniform(0, 1, R))])
+    rng.shuffle(x)
+    return x, h, L + k
+
+
+def _exact_argmin_sliding(x, h):
+    """Exact rational SQ(s) of every window (sliding Fraction sums), ties -> lowest s."""
+    F = [Fraction(float(v)) for v in np.sort(x)]
+    s1 = sum(F[:h])
+    s2 = sum(v * v for v in F[:h])
+    best = (h * s2 - s1 * s1, 0)
+    for s in range(1, len(F) - h + 1):
+        o, nw = F[s - 1], F[s + h - 1]
+        s1 += nw - o
+        s2 += nw * nw - o * o
+        v = h * s2 - s1 * s1
+        if v < best[0]:
+            best = (v, s)
+    return best[1]
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_window_argmin_exact_on_adversarial_column(seed):
+    # n >= 1e5: the fp64 prefix-sum argmin cannot see a 1-ulp difference under 1e12 tails; the oracle's
+    # rigorous screening margin keeps every window it cannot exclude and the exact re-evaluation picks
+    # the true optimum, checked against exact enumeration of ALL n - h + 1 windows.
+    x, h, s_true = _adversarial_column(seed)
+    s_exact = _exact_argmin_sliding(x, h)
+    assert s_exact == s_true
+    assert unimcd_raw(x, h).start == s_true
