@@ -301,6 +301,24 @@ def _breakdown(prof: dict, steps: int):
             for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
 
 
+def _relaunch(n: int):
+    """`python bench.py --gpus N` without torchrun: start N ranks on this node (127.0.0.1 rendezvous)."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} needs {n} GPUs, this node has {have}"}), flush=True)
+        sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -319,6 +337,12 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        _relaunch(args.gpus)          # one process per GPU: re-exec under torchrun (never a silent 1-rank run)
+        return
+    if args.impl != "reference" and world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -348,9 +372,10 @@ def main():
     # contiguous blocks at every GPU count, so N = 1, 2, 4, 8 compute the same estimate
     part = 1 if cfg == 4 else 0
     if world > 1:
+        # rtdetmcd_fit_sharded over NCCL: the library exchanges columns, block records and reweighting sums
         from paper_1910_05615_b200 import distributed as rtd_dist
-        runner = rtd_dist.ShardedFit(d.X, h=h, q=q, seed=191005615, log_transform=d.log_transform, rank=rank,
-                                     world=world, device=local)
+        runner = rtd_dist.ShardedFit(d.X, h=h, q=q, log_transform=d.log_transform, rank=rank, world=world,
+                                     device=local)
         step = runner.step
         n_rows_total = n
     else:
@@ -367,7 +392,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    prof_ctx = runner.engine.ctx if world > 1 else None
+    prof_ctx = runner.ctx if world > 1 else None
     k0, s0 = api.counters()
 
     def barrier():
@@ -410,6 +435,32 @@ def main():
 
     # e2e: the same step through the C ABI with pinned host buffers
     e2e = None
+    if not args.no_e2e and world > 1:
+        # every rank: its pinned host rows in, its flags out, through rtdetmcd_fit_sharded (the library copies
+        # the rows to the device inside the call); time = max over ranks of the device-side span
+        import torch.distributed as dist
+        a, b, _, _ = rtd_dist.shard_rows(n, q, world, rank)
+        Xh = torch.from_numpy(np.ascontiguousarray(d.X[a:b])).pin_memory()
+        fl = torch.empty(b - a, dtype=torch.uint8).pin_memory()
+
+        def hstep():
+            return api.fit_sharded(Xh, n, runner.ctx, h=h, q=q, log_transform=d.log_transform, outputs=(),
+                                   out_buffers={"flags": fl})
+        hstep()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            hstep()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        t = torch.tensor([wall], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+        e2e = {"value": n * args.steps / wall, "unit": "obs/s", "h2d_bytes_per_step": int(n * p * 8),
+               "d2h_bytes_per_step": int(n),
+               "api": "rtdetmcd_fit_sharded per rank from pinned host rows (H2D + D2H of flags inside each call), "
+                      "max over ranks"}
     if not args.no_e2e and world == 1:
         # K host batches through rtdetmcd_fit_batches: every step copies its batch from pinned host memory
         # and reads its flags back; batch k+1's copy runs on the library's copy stream during batch k's fit
@@ -457,7 +508,8 @@ def main():
                 "config": {"workload": CONFIG_NAMES[cfg], "n": int(n), "p": int(p), "h": int(h), "q": int(q),
                            "partition": "contiguous per-shard blocks" if part else "feistel",
                            "l2": "inputs larger than L2 (no flush)",
-                           "parallelism": f"rows over {world} GPU(s)"},
+                           "parallelism": f"rows over {world} GPU(s)" + (
+                               " (rtdetmcd_fit_sharded, NCCL inside the library)" if world > 1 else "")},
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cb,
                 "gpu_launches": int((k1 - k0)), "cub_sorts": int(s1 - s0),
                 "clocks": clk.summary(), "breakdown": breakdown,

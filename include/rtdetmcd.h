@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define RTDETMCD_ABI_VERSION 2
+#define RTDETMCD_ABI_VERSION 3
 
 typedef struct rtdetmcd_ctx rtdetmcd_ctx;
 
@@ -49,7 +49,8 @@ typedef enum {
   RTD_E_NOT_PD = 6,               /* a scatter matrix that must be positive definite is not */
   RTD_E_CUDA = 7,
   RTD_E_OOM = 8,
-  RTD_E_INTERNAL = 9
+  RTD_E_INTERNAL = 9,
+  RTD_E_NCCL = 10                 /* an inter-rank exchange failed (NCCL error, or a transport callback returned != 0) */
 } rtdetmcd_status;
 
 enum { RTD_PART_PERMUTE = 0, RTD_PART_CONTIGUOUS = 1 };
@@ -182,6 +183,73 @@ rtdetmcd_status rtdetmcd_flag(rtdetmcd_ctx* ctx, const double* X, int64_t n, int
                               const double* sigma, double quantile, int32_t log_transform, uint8_t* flags,
                               double* rd2);
 
+/* ---- the sharded fit: one process (rank) per GPU, rows sharded over the ranks ----
+ *
+ * The paper's parallel scheme (§4 steps 1-10) with the blocks spread over ranks:
+ *   C2  the global standardisation needs every row of a column: columns are
+ *       exchanged all-to-all, the owner of column j runs its univariate MCD over all n_global rows,
+ *       the (loc, scale) records are all-gathered;
+ *   --  every rank fits its own blocks (steps 1-4);
+ *   C4  block records are all-gathered and every rank runs the same deterministic median / KL
+ *       ranking / pooling (steps 5-7; the paper's master thread);
+ *   C5  per-block reweighting sums are all-gathered and pooled in block order (steps 8-9,
+ *       PAPER.md:975-995, the union of the fitted rows);
+ *   --  every rank flags its own rows (step 10).
+ * Every fold is a fixed-order fold by block id (never a float all-reduce), so the result is
+ * bit-identical to rtdetmcd_fit with shards = q and RTD_PART_CONTIGUOUS on the concatenated rows,
+ * at every world size.
+ *
+ * Row layout (rtdetmcd_shard_layout): q blocks of m = floor(n_global / q) consecutive rows; rank r
+ * holds blocks [r q/world, (r+1) q/world) (q a multiple of world), i.e. global rows
+ * [row0, row0 + n_local); the last rank also holds the n_global - q m remainder rows, which are
+ * flagged but not fitted (reading R23).  The partition is the contiguous one: opts->partition must
+ * be RTD_PART_CONTIGUOUS when world > 1 (RTD_E_INVALID_ARG otherwise).
+ *
+ * Collective: every rank calls rtdetmcd_fit_sharded with the same n_global, p and options (checked:
+ * RTD_E_INVALID_ARG on every rank on a mismatch) and its own X_local.  An error detected on one rank
+ * (bad rows, a failed block) is agreed on by all ranks before they leave, so no rank is left waiting in
+ * a collective; RTD_E_NCCL on a failed exchange (the ranks' states are then undefined: destroy). */
+
+/* Transport callbacks on HOST buffers (an alternative to NCCL, e.g. gloo or MPI, or ranks as threads).
+ * Both are collective; return 0 on success. */
+typedef struct {
+  void* user;
+  /* every rank contributes `bytes` bytes at send; recv (world * bytes) receives them in rank order */
+  int32_t (*allgather)(void* user, const void* send, void* recv, size_t bytes);
+  /* send_bytes[s] bytes at send + send_offs[s] go to rank s; recv_bytes[s] bytes from rank s land at
+   * recv + recv_offs[s] (s = 0..world-1, including the rank itself) */
+  int32_t (*alltoallv)(void* user, const void* send, const size_t* send_bytes, const size_t* send_offs, void* recv,
+                       const size_t* recv_bytes, const size_t* recv_offs);
+} rtdetmcd_transport;
+
+/* 128-byte NCCL unique id (ncclGetUniqueId): created on one rank, shared by the caller (e.g. a
+ * torch.distributed broadcast), passed to rtdetmcd_create_dist on every rank.  libnccl.so.2 is
+ * loaded at run time (the copy already in the process, else the system one); RTD_E_NCCL if absent. */
+rtdetmcd_status rtdetmcd_nccl_unique_id(void* id_out);
+/* A context on `device` that is rank `rank` of `world` over NCCL (collective: all ranks call it).
+ * nccl_unique_id NULL requires world == 1 (no communicator).  The NCCL communicator is owned by the
+ * context and destroyed with it; collectives are enqueued on the context stream. */
+rtdetmcd_status rtdetmcd_create_dist(rtdetmcd_ctx** ctx, int device, void* cuda_stream, const void* nccl_unique_id,
+                                     int rank, int world);
+/* The same with caller callbacks (copied; `user` must outlive the context). */
+rtdetmcd_status rtdetmcd_create_transport(rtdetmcd_ctx** ctx, int device, void* cuda_stream,
+                                          const rtdetmcd_transport* transport, int rank, int world);
+/* Rows of rank `rank` (host-only arithmetic, no GPU): q blocks over world ranks as above.  Returns 0,
+ * or RTD_E_INVALID_ARG when q is not a positive multiple of world or n_global < q. */
+rtdetmcd_status rtdetmcd_shard_layout(int64_t n_global, int32_t q, int32_t world, int32_t rank, int64_t* row0,
+                                      int64_t* n_local, int32_t* block0, int32_t* q_local);
+/* The sharded fit + flag (collective).  X_local [dev|host]: this rank's n_local x p rows (row-major,
+ * global rows [row0, row0 + n_local)).  q = opts->shards (a multiple of world; 0: the rule of
+ * eq. partitionsize, rounded down to a multiple of world, at least world).  h = opts->h or
+ * floor(alpha n_global) over ALL rows; block coverage floor(h m / n_global).
+ * out: loc .. sigma_rew, scalars and the per-block arrays (sized q / 2q) are GLOBAL and identical on
+ * every rank; flags, rd2, weights, hsubset are this rank's n_local rows.  A context made by
+ * rtdetmcd_create (no communicator) runs it as world 1. */
+rtdetmcd_status rtdetmcd_fit_sharded(rtdetmcd_ctx* ctx, const double* X_local, int64_t n_local, int64_t n_global,
+                                     int32_t p, const rtdetmcd_opts* opts, rtdetmcd_result* out);
+/* rank / world / transport kind ("none", "nccl", "host") of a context */
+rtdetmcd_status rtdetmcd_ctx_comm(const rtdetmcd_ctx* ctx, int32_t* rank, int32_t* world, const char** kind);
+
 /* ---- stage entry points: the same kernels, exposed for intermediate parity
  * checks and as building blocks of the multi-process driver ---- */
 
@@ -237,8 +305,8 @@ rtdetmcd_status rtdetmcd_prof_entry(const rtdetmcd_ctx* ctx, int32_t i, char* na
                                     int64_t* launches, double* bytes_total, double* flops_total,
                                     double* eff_bytes_total);
 
-/* ---- distributed stages (one process per GPU; the caller moves data between
- * ranks, e.g. with torch.distributed over NCCL).  Blocks are contiguous row
+/* ---- distributed stages (the building blocks rtdetmcd_fit_sharded runs internally, exposed for
+ * callers that move the data between ranks themselves).  Blocks are contiguous row
  * ranges; rank r holds blocks [r q/G, (r+1) q/G).  Sequence per rank:
  *   rtdetmcd_columns -> (exchange columns) -> rtdetmcd_unimcd on owned columns
  *   -> (all-gather loc/scale) -> rtdetmcd_blocks_fit -> (all-gather records)

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libpaper_1910_05615_b200.so")
 RTD_STATUS = {
     0: "RTD_OK", 1: "RTD_E_INVALID_ARG", 2: "RTD_E_NONFINITE", 3: "RTD_E_DEGENERATE_COLUMN",
     4: "RTD_E_BOTH_STARTS_FAILED", 5: "RTD_E_TOO_FEW_VALID_BLOCKS", 6: "RTD_E_NOT_PD", 7: "RTD_E_CUDA",
-    8: "RTD_E_OOM", 9: "RTD_E_INTERNAL",
+    8: "RTD_E_OOM", 9: "RTD_E_INTERNAL", 10: "RTD_E_NCCL",
 }
 
 EXPORTS = [
@@ -26,7 +26,18 @@ EXPORTS = [
     "rtdetmcd_set_profiling", "rtdetmcd_prof_count", "rtdetmcd_prof_entry", "rtdetmcd_counters",
     "rtdetmcd_moment_doubles", "rtdetmcd_columns", "rtdetmcd_blocks_fit", "rtdetmcd_aggregate",
     "rtdetmcd_blocks_reweight", "rtdetmcd_pool_reweight",
+    "rtdetmcd_nccl_unique_id", "rtdetmcd_create_dist", "rtdetmcd_create_transport", "rtdetmcd_shard_layout",
+    "rtdetmcd_fit_sharded", "rtdetmcd_ctx_comm",
 ]
+
+# rtdetmcd_transport callbacks (host buffers)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
+                           C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t))
+
+
+class Transport(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", ALLGATHER_FN), ("alltoallv", ALLTOALLV_FN)]
 
 
 class Opts(C.Structure):
@@ -95,6 +106,12 @@ def lib() -> C.CDLL:
     L.rtdetmcd_aggregate.argtypes = [vp, i32, i32, i64, vp, vp, vp, vp]
     L.rtdetmcd_blocks_reweight.argtypes = [vp, f64, vp, vp]
     L.rtdetmcd_pool_reweight.argtypes = [vp, i32, vp, f64, vp, vp, vp, vp, vp]
+    L.rtdetmcd_nccl_unique_id.argtypes = [vp]
+    L.rtdetmcd_create_dist.argtypes = [C.POINTER(vp), C.c_int, vp, vp, C.c_int, C.c_int]
+    L.rtdetmcd_create_transport.argtypes = [C.POINTER(vp), C.c_int, vp, C.POINTER(Transport), C.c_int, C.c_int]
+    L.rtdetmcd_shard_layout.argtypes = [i64, i32, i32, i32, vp, vp, vp, vp]
+    L.rtdetmcd_fit_sharded.argtypes = [vp, vp, i64, i64, i32, C.POINTER(Opts), C.POINTER(Result)]
+    L.rtdetmcd_ctx_comm.argtypes = [vp, vp, vp, C.POINTER(C.c_char_p)]
     L.rtdetmcd_counters.argtypes = [vp, vp]
     L.rtdetmcd_counters.restype = None
     L.rtdetmcd_prof_count.argtypes = [vp]

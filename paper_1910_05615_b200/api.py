@@ -12,7 +12,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import RTD_STATUS, Opts, Result, lib
+from ._lib import RTD_STATUS, Opts, Result, Transport, lib
 
 
 class RTDError(RuntimeError):
@@ -60,6 +60,83 @@ def new_context(device: int = 0) -> dict:
     if rc != 0:
         raise RTDError(rc, "rtdetmcd_create failed")
     return {"h": h, "ws": None}
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for rtdetmcd_create_dist (create on one rank, share with the others)."""
+    buf = C.create_string_buffer(128)
+    rc = lib().rtdetmcd_nccl_unique_id(buf)
+    if rc != 0:
+        raise RTDError(rc, "rtdetmcd_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+    return buf.raw
+
+
+def dist_context(device: int, rank: int, world: int, unique_id: bytes | None) -> dict:
+    """rtdetmcd_create_dist: rank `rank` of `world` over NCCL (collective over the ranks)."""
+    h = C.c_void_p()
+    idb = C.create_string_buffer(unique_id, 128) if unique_id is not None else None
+    rc = lib().rtdetmcd_create_dist(C.byref(h), int(device), None, idb, int(rank), int(world))
+    if rc != 0:
+        raise RTDError(rc, "rtdetmcd_create_dist failed")
+    return {"h": h, "ws": None}
+
+
+def transport_context(device: int, rank: int, world: int, allgather, alltoallv) -> dict:
+    """rtdetmcd_create_transport with Python callbacks on host buffers:
+    allgather(send: memoryview, recv: memoryview) and
+    alltoallv(send: memoryview, send_bytes, send_offs, recv: memoryview, recv_bytes, recv_offs)."""
+    from ._lib import ALLGATHER_FN, ALLTOALLV_FN
+
+    def _ag(user, send, recv, nbytes):
+        try:
+            allgather((C.c_char * nbytes).from_address(send), (C.c_char * (nbytes * world)).from_address(recv))
+            return 0
+        except Exception as e:  # noqa: BLE001
+            print(f"rtdetmcd transport allgather failed on rank {rank}: {e!r}", flush=True)
+            return 1
+
+    def _a2a(user, send, sb, so, recv, rb, ro):
+        try:
+            sbl, sol = [sb[i] for i in range(world)], [so[i] for i in range(world)]
+            rbl, rol = [rb[i] for i in range(world)], [ro[i] for i in range(world)]
+            stot = max(a + b for a, b in zip(sol, sbl))
+            rtot = max(a + b for a, b in zip(rol, rbl))
+            sv = (C.c_char * max(stot, 1)).from_address(send) if send else None
+            rv = (C.c_char * max(rtot, 1)).from_address(recv) if recv else None
+            alltoallv(sv, sbl, sol, rv, rbl, rol)
+            return 0
+        except Exception as e:  # noqa: BLE001
+            print(f"rtdetmcd transport alltoallv failed on rank {rank}: {e!r}", flush=True)
+            return 1
+
+    t = Transport(None, ALLGATHER_FN(_ag), ALLTOALLV_FN(_a2a))
+    h = C.c_void_p()
+    rc = lib().rtdetmcd_create_transport(C.byref(h), int(device), None, C.byref(t), int(rank), int(world))
+    if rc != 0:
+        raise RTDError(rc, "rtdetmcd_create_transport failed")
+    return {"h": h, "ws": None, "keep": t}   # the callbacks must outlive the context
+
+
+def destroy_context(ctx: dict) -> None:
+    if ctx.get("h"):
+        lib().rtdetmcd_destroy(ctx["h"])
+        ctx["h"] = None
+
+
+def ctx_comm(ctx: dict) -> tuple:
+    r, w, k = C.c_int32(), C.c_int32(), C.c_char_p()
+    _check(lib().rtdetmcd_ctx_comm(ctx["h"], C.byref(r), C.byref(w), C.byref(k)), ctx)
+    return r.value, w.value, k.value.decode()
+
+
+def shard_layout(n_global: int, q: int, world: int, rank: int) -> tuple:
+    """(row0, n_local, block0, q_local) of `rank` (rtdetmcd_shard_layout; host arithmetic only)."""
+    r0, nl, b0, ql = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int32()
+    rc = lib().rtdetmcd_shard_layout(int(n_global), int(q), int(world), int(rank), C.byref(r0), C.byref(nl),
+                                     C.byref(b0), C.byref(ql))
+    if rc != 0:
+        raise RTDError(rc, f"no layout for n={n_global}, q={q}, world={world}, rank={rank}")
+    return r0.value, nl.value, b0.value, ql.value
 
 
 def _check(rc: int, ctx) -> None:
@@ -214,6 +291,25 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
     if torch_workspace:
         L.rtdetmcd_set_workspace(ctx["h"], None, 0)
     _check(rc, ctx)
+    return _make_fit(r, host, rows)
+
+
+def fit_sharded(X_local, n_global: int, ctx: dict, h: int | None = None, alpha: float = 0.5, q: int = 0,
+                seed: int = 0, kappa_max: float = 1000.0, quantile: float = 0.975, max_csteps: int = 100,
+                refresh_every: int = 32, log_transform: bool = False, outputs=("flags", "rd2", "weights", "hsubset"),
+                out_buffers: dict | None = None, distance: int = 0, consistency: int = 0) -> Fit:
+    """rtdetmcd_fit_sharded (collective): this rank's rows X_local (shard_layout) of an n_global-row data
+    set; global estimates, local per-row outputs.  Contiguous blocks (the sharded partition)."""
+    ptr, keep, is_cuda, dev = _as_f64(X_local)
+    n, p = int(keep.shape[0]), int(keep.shape[1])
+    if is_cuda:
+        _sync_torch(dev)
+    o = default_opts(h=int(h or 0), alpha=float(alpha), shards=int(q), seed=int(seed), kappa_max=float(kappa_max),
+                     quantile=float(quantile), max_csteps=int(max_csteps), refresh_every=int(refresh_every),
+                     partition=1, log_transform=int(bool(log_transform)), distance=int(distance),
+                     consistency=int(consistency))
+    r, host, rows = _result_buffers(n, p, q, outputs, out_buffers, is_cuda, dev)
+    _check(lib().rtdetmcd_fit_sharded(ctx["h"], C.c_void_p(ptr), n, int(n_global), p, C.byref(o), C.byref(r)), ctx)
     return _make_fit(r, host, rows)
 
 

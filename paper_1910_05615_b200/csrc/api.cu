@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -13,6 +14,7 @@
 #include "../../include/rtdetmcd.h"
 #include "rtd_internal.h"
 #include "rtd_linalg.h"
+#include "comm.h"
 
 namespace rtd {
 bool dist_mma_supported(int p);
@@ -147,6 +149,7 @@ struct rtdetmcd_ctx {
   size_t xbuf_cap = 0;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  rtd::Comm* comm = nullptr;  // rank / world of the sharded fit (rtdetmcd_create_dist / _create_transport)
 };
 
 namespace {
@@ -1183,6 +1186,306 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
   }
 }
 
+// ------------------------------------------------------------------ the sharded fit (rtdetmcd_fit_sharded)
+struct ShardLayout {
+  long long m = 0, row0 = 0, nloc = 0;
+  int q = 0, qloc = 0, b0 = 0;
+};
+
+bool shard_layout_calc(long long n, int q, int world, int rank, ShardLayout& L) {
+  if (q < 1 || world < 1 || q % world || rank < 0 || rank >= world || n < q) return false;
+  L.q = q;
+  L.m = n / q;
+  L.qloc = q / world;
+  L.b0 = rank * L.qloc;
+  L.row0 = (long long)L.b0 * L.m;
+  L.nloc = (long long)L.qloc * L.m + (rank == world - 1 ? n - (long long)q * L.m : 0);
+  return true;
+}
+
+// per-block record exchanged by C4: [valid, chosen, logdet(chosen), warnings, status0, status1, steps0, steps1,
+// logdet0, logdet1, mu (p), c(alpha)-scaled Sigma (p*p)] (standardised units)
+constexpr int REC_HEAD = 10;
+
+// An error detected on one rank must end the fit on every rank: each rank contributes its status
+// (code, detail) and all throw the lowest-rank failure, so no rank waits alone in a later collective.
+void agree(Comm* cm, cudaStream_t st, const Fail* mine) {
+  struct Word {
+    int64_t code, len;
+    char msg[240];
+  } w{};
+  if (mine) {
+    w.code = mine->code;
+    w.len = (int64_t)std::min<size_t>(mine->msg.size(), sizeof(w.msg) - 1);
+    memcpy(w.msg, mine->msg.data(), (size_t)w.len);
+  }
+  std::vector<Word> all(cm->world());
+  cm->allgather_host(&w, all.data(), sizeof(Word), st);
+  for (int r = 0; r < cm->world(); r++)
+    if (all[r].code)
+      throw Fail{(rtdetmcd_status)all[r].code,
+                 (r == cm->rank() ? std::string() : "rank " + std::to_string(r) + ": ") + std::string(all[r].msg)};
+}
+
+void fit_sharded_impl(rtdetmcd_ctx* c, const double* X, long long n_local, long long n_global, int p,
+                      const rtdetmcd_opts& o, rtdetmcd_result* out) {
+  Comm* cm = c->comm;
+  cudaStream_t st = c->stream;
+  const int world = cm->world(), rank = cm->rank();
+  // ---- agreement on the problem: every rank checks every rank's header (same verdict everywhere)
+  const double hdr_l[] = {(double)n_local, (double)n_global, (double)p, (double)o.h, o.alpha, (double)o.shards,
+                          (double)o.shard_cap, (double)o.omega, o.kappa_max, o.quantile, (double)o.max_csteps,
+                          (double)o.refresh_every, (double)(o.seed >> 32), (double)(o.seed & 0xffffffffu),
+                          (double)o.partition, (double)o.log_transform, (double)o.distance, (double)o.consistency};
+  constexpr int NH = sizeof(hdr_l) / sizeof(double);
+  std::vector<double> hdr((size_t)NH * world);
+  cm->allgather_host(hdr_l, hdr.data(), sizeof(hdr_l), st);
+  long long n_sum = 0;
+  std::vector<long long> nl(world);
+  for (int r = 0; r < world; r++) {
+    nl[r] = (long long)hdr[(size_t)r * NH];
+    n_sum += nl[r];
+    for (int k = 1; k < NH; k++)
+      if (memcmp(&hdr[(size_t)r * NH + k], &hdr[k], sizeof(double)) != 0)
+        throw Fail{RTD_E_INVALID_ARG, "rank " + std::to_string(r) + " passed different n_global / p / options"};
+  }
+  if (n_sum != n_global) throw Fail{RTD_E_INVALID_ARG, "the ranks' n_local do not add up to n_global"};
+  if (p < 1 || p > RTD_MAXP) throw Fail{RTD_E_INVALID_ARG, "p must be in [1, 40]"};
+  if (!(n_global > 2LL * p)) throw Fail{RTD_E_INVALID_ARG, "need n_global > 2p"};
+  int q = o.shards;
+  if (q <= 0) q = std::max(world, rtdetmcd_choose_q(n_global, p, o.omega, o.shard_cap) / world * world);
+  if (q > 1 && o.partition != RTD_PART_CONTIGUOUS)
+    throw Fail{RTD_E_INVALID_ARG, "the sharded fit partitions into contiguous shards: set partition = RTD_PART_CONTIGUOUS"};
+  std::vector<ShardLayout> lay(world);
+  for (int r = 0; r < world; r++) {
+    if (!shard_layout_calc(n_global, q, world, r, lay[r]))
+      throw Fail{RTD_E_INVALID_ARG, "q = " + std::to_string(q) + " must be a positive multiple of world = " +
+                                        std::to_string(world) + " with n_global >= q"};
+    if (lay[r].nloc != nl[r])
+      throw Fail{RTD_E_INVALID_ARG, "rank " + std::to_string(r) + " holds " + std::to_string(nl[r]) +
+                                        " rows; the layout of q = " + std::to_string(q) + " blocks needs " +
+                                        std::to_string(lay[r].nloc) + " (rtdetmcd_shard_layout)"};
+  }
+  const ShardLayout& L = lay[rank];
+  rtdetmcd_opts og = o;
+  og.shards = q;
+  Dims dg = make_dims(n_global, p, og, false);  // global h, block coverage
+  Dims d = dg;                                   // this rank's blocks
+  d.n = n_local;
+  d.q = L.qloc;
+  d.m = L.m;
+  d.perm = 0;
+  d.x_host = !is_device_ptr(X);
+  const long long m = L.m, n = n_local;
+  const int ql = L.qloc;
+  const int cpr = (p + world - 1) / world;                           // columns per owner (C2)
+  const int own0 = std::min(p, rank * cpr), nown = std::min(p, own0 + cpr) - own0;
+  const int np = mom_np(p);
+  const int R = REC_HEAD + p + p * p;
+  const bool want_flags = out && (out->flags || out->rd2);
+  auto carve = [&](Arena& A, FitBufs& f, double*& cols, double*& stage, UniOut*& uni_all, char*& ush,
+                   size_t& ush_bytes, double*& sums_all) {
+    carve_fit(A, f, d, o, true, true, true, true, q);
+    cols = A.take<double>((size_t)std::max(1, nown) * n_global);
+    stage = A.take<double>((size_t)std::max(1, nown) * n_global);
+    uni_all = A.take<UniOut>((size_t)world * cpr + RTD_MAXP);
+    ush_bytes = uni_bytes(n_global, std::max(1, nown));
+    ush = A.take<char>(ush_bytes);
+    sums_all = A.take<double>((size_t)q * np);
+  };
+  FitBufs f;
+  double *cols, *stage, *sums_all;
+  UniOut* uni_all;
+  char* ush;
+  size_t ush_bytes;
+  Arena dry;
+  carve(dry, f, cols, stage, uni_all, ush, ush_bytes, sums_all);
+  Fail werr{RTD_OK, ""};
+  try {
+    ensure_ws(c, dry.off + 4096);
+  } catch (const Fail& e) {
+    werr = e;
+  }
+  agree(cm, st, werr.code ? &werr : nullptr);
+  Arena A;
+  A.base = c->ws;
+  A.cap = c->ws_cap;
+  carve(A, f, cols, stage, uni_all, ush, ush_bytes, sums_all);
+  int warnings = 0;
+  if (dg.h < (n_global + p + 1) / 2) warnings |= RTD_W_H_BELOW_BOUND;
+
+  // H0 on the local rows; a bad row on any rank ends the fit on all (global row index in the message)
+  const double* Xdev = X;
+  if (d.x_host) {
+    h2d(st, f.Xd, X, (size_t)n * p * sizeof(double));
+    Xdev = f.Xd;
+  }
+  {
+    Fail e0{RTD_OK, ""};
+    RTD_CU(cudaMemsetAsync(f.bad, 0xff, sizeof(unsigned long long), st));
+    {
+      ProfScope ps("transpose", (double)n * p * 16.0);
+      launch_transpose(Xdev, n, p, d.log, f.Xc, f.bad, st);
+    }
+    unsigned long long b = 0;
+    d2h(st, &b, f.bad, sizeof(b));
+    if (b != ~0ull)
+      e0 = Fail{RTD_E_NONFINITE, "row " + std::to_string(L.row0 + (long long)b) +
+                                     (d.log ? " is not finite and > 0" : " is not finite")};
+    agree(cm, st, e0.code ? &e0 : nullptr);
+  }
+
+  // C2: column all-to-all -- the owner of column j receives every rank's slice of it, in rank (= global
+  // row) order, then runs the univariate MCD over all n_global rows
+  {
+    std::vector<size_t> sb(world), so(world), rb(world), ro(world);
+    size_t off = 0;
+    for (int s = 0; s < world; s++) {
+      const int a0 = std::min(p, s * cpr), cnt = std::min(p, a0 + cpr) - a0;
+      sb[s] = (size_t)cnt * n * sizeof(double);
+      so[s] = (size_t)a0 * n * sizeof(double);
+      rb[s] = (size_t)nown * lay[s].nloc * sizeof(double);
+      ro[s] = off;
+      off += rb[s];
+    }
+    {
+      ProfScope ps("exchange_columns", (double)(so[world - 1] + sb[world - 1]) + (double)off);
+      cm->alltoallv_dev(f.Xc, sb.data(), so.data(), stage, rb.data(), ro.data(), st);
+    }
+    for (int s = 0; s < world && nown > 0; s++)
+      RTD_CU(cudaMemcpy2DAsync(cols + lay[s].row0, (size_t)n_global * sizeof(double),
+                               (const char*)stage + ro[s], (size_t)lay[s].nloc * sizeof(double),
+                               (size_t)lay[s].nloc * sizeof(double), nown, cudaMemcpyDeviceToDevice, st));
+  }
+  UniOut* uni_own = uni_all + (size_t)world * cpr;  // scratch output of this rank's columns (cpr <= RTD_MAXP)
+  if (nown > 0) run_unimcd(st, ush, ush_bytes, cols, n_global, nown, uni_own);
+  cm->allgather_dev(uni_own, uni_all, (size_t)cpr * sizeof(UniOut), st);  // column j = s cpr + jj at index j
+  RTD_CU(cudaMemcpyAsync(f.uni, uni_all, (size_t)p * sizeof(UniOut), cudaMemcpyDeviceToDevice, st));
+  std::vector<UniOut> uni(p);
+  d2h(st, uni.data(), f.uni, p * sizeof(UniOut));
+  for (int j = 0; j < p; j++)
+    if (uni[j].status) throw Fail{RTD_E_DEGENERATE_COLUMN, "column " + std::to_string(j)};  // same on all ranks
+
+  // this rank's blocks: Z, steps 1-4
+  {
+    ProfScope ps("build_Z", (double)ql * m * p * 16.0);
+    launch_build_Z(f.Xc, Xdev, n, p, ql, m, 0, 0, d.log, f.uni, f.Z, nullptr, st);
+  }
+  BlockResult br = phase_blocks(st, f, d, o);
+
+  // C4: block records, all-gathered in block order; every rank folds them identically (steps 5-7)
+  std::vector<double> rec_l((size_t)ql * R, 0.0), rec((size_t)q * R);
+  {
+    std::vector<double> mu((size_t)ql * RTD_MAXP), sg((size_t)ql * M2);
+    fetch(st, {{mu.data(), f.mu_blk, mu.size() * sizeof(double)}, {sg.data(), f.sigraw_blk, sg.size() * sizeof(double)}});
+    for (int b = 0; b < ql; b++) {
+      double* r = rec_l.data() + (size_t)b * R;
+      const int ch = br.chosen[b];
+      r[0] = ch >= 0 ? 1.0 : 0.0;
+      r[1] = ch;
+      r[2] = ch >= 0 ? br.logdet[2 * b + ch] : NAN;
+      r[3] = br.warnings;
+      for (int k = 0; k < 2; k++) {
+        r[4 + k] = br.status[2 * b + k];
+        r[6 + k] = br.steps[2 * b + k];
+        r[8 + k] = br.logdet[2 * b + k];
+      }
+      if (ch < 0) continue;
+      for (int j = 0; j < p; j++) r[REC_HEAD + j] = mu[(size_t)b * RTD_MAXP + j];
+      for (int e = 0; e < p * p; e++) r[REC_HEAD + p + e] = sg[(size_t)b * M2 + e];
+    }
+  }
+  cm->allgather_host(rec_l.data(), rec.data(), rec_l.size() * sizeof(double), st);
+  std::vector<int> valid;
+  {
+    std::vector<double> mu(RTD_MAXP, 0.0), sg(M2, 0.0);
+    for (int b = 0; b < q; b++) {
+      const double* r = rec.data() + (size_t)b * R;
+      warnings |= (int)r[3];
+      if (r[0] == 0.0) continue;
+      valid.push_back(b);
+      for (int j = 0; j < p; j++) mu[j] = r[REC_HEAD + j];
+      for (int e = 0; e < p * p; e++) sg[e] = r[REC_HEAD + p + e];
+      h2d(st, f.mu_blk + (size_t)b * RTD_MAXP, mu.data(), RTD_MAXP * sizeof(double));
+      h2d(st, f.sigraw_blk + (size_t)b * M2, sg.data(), M2 * sizeof(double));
+    }
+  }
+  const int n_kept = phase_raw(st, f, p, q, m, valid);
+
+  // steps 8-9: per-block reweighting sums of this rank's blocks, C5 all-gather, pooled in block order
+  const double c2 = chi2_quantile(o.quantile, p);
+  const int cstride = p + p * (p + 1) / 2;
+  phase_reweight_blocks(st, f, p, ql, m, c2, true);
+  cm->allgather_dev(f.sums_rw, sums_all, (size_t)ql * np * sizeof(double), st);
+  phase_pool(st, f, p, q, o.quantile, sums_all, true);
+  launch_destandardize(f.uni, f.mu_raw, f.sig_raw, p, f.muX, f.sigX, st);
+  launch_destandardize(f.uni, f.mu_rew, f.sig_rew, p, f.muX + RTD_MAXP, f.sigX + M2, st);
+  // step 10 on the local rows
+  {
+    RTD_CU(cudaMemsetAsync(f.st1 + 1, 0, sizeof(int), st));
+    launch_prepare(f.ids_dev, 1, f.muX + RTD_MAXP, f.sigX + M2, p, 1e300, f.cb.cstage, cstride, nullptr, nullptr,
+                   f.st1 + 1, nullptr, 0, 0, st);
+    if (want_flags) {
+      ConstLease lease(f.cb.cstage, cstride, st);
+      ProfScope ps("flag", (double)n * (8.0 * p + 9.0));
+      flag_rows(p, Xdev, n, d.log, f.cb.cstage, c2, f.flags_d, f.rd2_d, st);
+    }
+  }
+  if (out && (out->weights || out->hsubset)) {
+    if ((long long)ql * m < n) {
+      RTD_CU(cudaMemsetAsync(f.weights_d, 0, n, st));
+      RTD_CU(cudaMemsetAsync(f.hsub_d, 0, n, st));
+    }
+    launch_weights_from_d2(f.cb.d2, (long long)ql * m, c2, nullptr, f.weights_d, st);
+    launch_hsub_from_mem(f.cb.memA, f.chosen_dev, ql, m, nullptr, f.hsub_d, st);
+  }
+  std::vector<double> mx(4 * RTD_MAXP), sx(4 * M2);
+  int pd[2] = {0, 0};
+  double kw = 0.0;
+  fetch(st, {{pd, f.st1, 2 * sizeof(int)}, {&kw, f.pooled + (np - 1), sizeof(double)},
+             {mx.data(), f.muX, 2 * RTD_MAXP * sizeof(double)}, {sx.data(), f.sigX, 2 * M2 * sizeof(double)}});
+  // raw fit, pooled sums and the reweighted fit are identical on every rank: so are these verdicts
+  if (pd[0] == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "raw scatter is not positive definite"};
+  if (!(kw > p)) throw Fail{RTD_E_NOT_PD, "too few reweighted inliers"};
+  if (pd[1] == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "reweighted scatter is not positive definite"};
+  if (out) {
+    out->n_weighted = (int64_t)llround(kw);
+    for (int j = 0; j < p; j++) {
+      if (out->loc) out->loc[j] = uni[j].loc;
+      if (out->scale) out->scale[j] = uni[j].scale;
+      if (out->mu_raw) out->mu_raw[j] = mx[j];
+      if (out->mu_rew) out->mu_rew[j] = mx[RTD_MAXP + j];
+    }
+    for (int e = 0; e < p * p; e++) {
+      if (out->sigma_raw) out->sigma_raw[e] = sx[e];
+      if (out->sigma_rew) out->sigma_rew[e] = sx[M2 + e];
+    }
+    out->logdet_raw = (q == 1 && rec[0] != 0.0) ? rec[2] : NAN;
+    out->cutoff2 = c2;
+    out->h = dg.h;
+    out->h_block = dg.hb;
+    out->m = m;
+    out->q_used = q;
+    out->warnings = warnings;
+    out->n_valid_blocks = (int)valid.size();
+    out->n_kept_blocks = n_kept;
+    for (int b = 0; b < q; b++) {
+      const double* r = rec.data() + (size_t)b * R;
+      if (out->block_chosen) out->block_chosen[b] = (int32_t)r[1];
+      for (int k = 0; k < 2; k++) {
+        if (out->start_status) out->start_status[2 * b + k] = (int32_t)r[4 + k];
+        if (out->start_steps) out->start_steps[2 * b + k] = (int32_t)r[6 + k];
+        if (out->start_logdet) out->start_logdet[2 * b + k] = r[8 + k];
+      }
+    }
+    output_copy(st, out->flags, f.flags_d, n);
+    output_copy(st, out->rd2, f.rd2_d, n * sizeof(double));
+    output_copy(st, out->weights, f.weights_d, n);
+    output_copy(st, out->hsubset, f.hsub_d, n);
+    RTD_CU(cudaStreamSynchronize(st));
+  }
+}
+
 struct DistSession {
   Dims d;
   FitBufs f;
@@ -1222,6 +1525,9 @@ rtdetmcd_status guarded(rtdetmcd_ctx* c, F&& fn) {
   } catch (const CudaError& e) {
     c->err = std::string("CUDA error ") + cudaGetErrorString(e.code) + " in " + e.where;
     return RTD_E_CUDA;
+  } catch (const CommError& e) {
+    c->err = e.msg;
+    return RTD_E_NCCL;
   } catch (const std::string& s) {
     c->err = s;
     return RTD_E_INTERNAL;
@@ -1283,6 +1589,8 @@ rtdetmcd_status rtdetmcd_create(rtdetmcd_ctx** ctx, int device, void* cuda_strea
 void rtdetmcd_destroy(rtdetmcd_ctx* c) {
   if (!c) return;
   drop_session(c);
+  delete c->comm;
+  c->comm = nullptr;
   cudaSetDevice(c->device);
   if (c->ws && !c->ws_user) cudaFree(c->ws);
   for (int k = 0; k < 2; k++) {
@@ -1814,6 +2122,83 @@ rtdetmcd_status rtdetmcd_pool_reweight(rtdetmcd_ctx* c, int32_t q, const double*
       if (sigma_rew_x) sigma_rew_x[e] = sx[M2 + e];
     }
   });
+}
+
+rtdetmcd_status rtdetmcd_nccl_unique_id(void* id_out) {
+  if (!id_out) return RTD_E_INVALID_ARG;
+  try {
+    nccl_unique_id(id_out);
+    return RTD_OK;
+  } catch (...) {
+    return RTD_E_NCCL;
+  }
+}
+
+static rtdetmcd_status create_with_comm(rtdetmcd_ctx** ctx, int device, void* cuda_stream, int rank, int world,
+                                        const std::function<Comm*()>& make) {
+  if (!ctx || world < 1 || rank < 0 || rank >= world) return RTD_E_INVALID_ARG;
+  rtdetmcd_status s = rtdetmcd_create(ctx, device, cuda_stream);
+  if (s != RTD_OK) return s;
+  try {
+    (*ctx)->comm = make();
+    return RTD_OK;
+  } catch (const CommError& e) {
+    fprintf(stderr, "rtdetmcd: %s\n", e.msg.c_str());
+  } catch (...) {
+  }
+  rtdetmcd_destroy(*ctx);
+  *ctx = nullptr;
+  return RTD_E_NCCL;
+}
+
+rtdetmcd_status rtdetmcd_create_dist(rtdetmcd_ctx** ctx, int device, void* cuda_stream, const void* nccl_unique_id,
+                                     int rank, int world) {
+  if (!nccl_unique_id) {
+    if (world != 1 || rank != 0) return RTD_E_INVALID_ARG;
+    return rtdetmcd_create(ctx, device, cuda_stream);
+  }
+  return create_with_comm(ctx, device, cuda_stream, rank, world, [&] { return make_nccl_comm(nccl_unique_id, rank, world); });
+}
+
+rtdetmcd_status rtdetmcd_create_transport(rtdetmcd_ctx** ctx, int device, void* cuda_stream,
+                                          const rtdetmcd_transport* t, int rank, int world) {
+  if (!t || !t->allgather || !t->alltoallv) return RTD_E_INVALID_ARG;
+  return create_with_comm(ctx, device, cuda_stream, rank, world, [&] { return make_host_comm(*t, rank, world); });
+}
+
+rtdetmcd_status rtdetmcd_shard_layout(int64_t n_global, int32_t q, int32_t world, int32_t rank, int64_t* row0,
+                                      int64_t* n_local, int32_t* block0, int32_t* q_local) {
+  ShardLayout L;
+  if (!shard_layout_calc(n_global, q, world, rank, L)) return RTD_E_INVALID_ARG;
+  if (row0) *row0 = L.row0;
+  if (n_local) *n_local = L.nloc;
+  if (block0) *block0 = L.b0;
+  if (q_local) *q_local = L.qloc;
+  return RTD_OK;
+}
+
+rtdetmcd_status rtdetmcd_fit_sharded(rtdetmcd_ctx* c, const double* X_local, int64_t n_local, int64_t n_global,
+                                     int32_t p, const rtdetmcd_opts* opts, rtdetmcd_result* out) {
+  return guarded(c, [&] {
+    if (!X_local || n_local < 1) throw Fail{RTD_E_INVALID_ARG, "X_local is NULL or n_local < 1"};
+    rtdetmcd_opts o;
+    if (opts) o = *opts; else rtdetmcd_opts_default(&o);
+    drop_session(c);
+    if (!c->comm || (c->comm->world() == 1 && o.partition != RTD_PART_CONTIGUOUS)) {  // world 1: the plain fit
+      if (n_local != n_global) throw Fail{RTD_E_INVALID_ARG, "world 1: n_local must equal n_global"};
+      fit_impl(c, X_local, n_local, p, o, out);
+      return;
+    }
+    fit_sharded_impl(c, X_local, n_local, n_global, p, o, out);
+  });
+}
+
+rtdetmcd_status rtdetmcd_ctx_comm(const rtdetmcd_ctx* c, int32_t* rank, int32_t* world, const char** kind) {
+  if (!c) return RTD_E_INVALID_ARG;
+  if (rank) *rank = c->comm ? c->comm->rank() : 0;
+  if (world) *world = c->comm ? c->comm->world() : 1;
+  if (kind) *kind = c->comm ? c->comm->kind() : "none";
+  return RTD_OK;
 }
 
 double rtdetmcd_chi2_quantile(double prob, int32_t dof) { return chi2_quantile(prob, dof); }

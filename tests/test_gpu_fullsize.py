@@ -19,6 +19,8 @@
   Everything is compared in original X units: the subset moments, the pooling
   and the Mahalanobis distances are affine equivariant (reading R22), so no
   GPU-computed standardisation enters the oracle side.
+* The whole oracle fit of config 4, precomputed by tools/golden_config4.py (oracle/ + the seeded
+  generator only) into tests/golden/config4_oracle.npz, compared element by element.
 * An opt-in (RTD_FULLSIZE_SLOW=1) case reruns the oracle's whole block fit of
   block 0 of config 4 (global standardisation over 8M rows, both starts,
   C-steps: several minutes of CPU) and compares its h-subset with the GPU's.
@@ -128,6 +130,50 @@ def test_config4_blocks_fixed_point_pool_reweight_flags(cfg4):
     fl = g.flags.cpu().numpy().astype(bool)
     assert fl[d.meta["shift_rows"]].mean() > 0.99
     assert fl[~d.outliers].mean() < 0.06
+
+
+def test_config4_matches_oracle_golden(cfg4):
+    """The WHOLE oracle fit of config 4 (tests/golden/config4_oracle.npz, written by
+    tools/golden_config4.py, which imports only oracle/ and the seeded generator; ~20 min of CPU)
+    against the CUDA fit of the bench workload, element by element: global standardisation
+    (PAPER.md:430-453, 756-766), every (block, start)'s converged log det and C-step count, the chosen
+    start and its h-subset per block, the pooled raw fit, the
+    reweighted fit and weights, the flags and sampled RD^2 of all n rows
+    (PAPER.md:217-220).  Tie bands of reading Q23 come from the oracle's own distances."""
+    import hashlib
+    d, g = cfg4
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "config4_oracle.npz"))
+    n, p, q = int(z["n"]), int(z["p"]), int(z["q"])
+    assert d.X.shape == (n, p) and d.h == int(z["h"]) and d.q == q
+    assert hashlib.sha256(d.X.tobytes()).digest() == z["x_digest"].tobytes(), "generator drift: regenerate the golden"
+    assert np.allclose(g.loc, z["loc"], rtol=1e-13, atol=1e-14)
+    assert np.allclose(g.scale, z["scale"], rtol=1e-12, atol=0)
+    # per (block, start): converged log det (update-based on the GPU, reading R12) and C-step count
+    sl = np.asarray(g.start_logdet).reshape(q, 2)
+    assert np.allclose(sl, z["start_logdet"], rtol=1e-12, atol=0)
+    assert np.array_equal(np.asarray(g.start_steps).reshape(q, 2), z["start_steps"])
+    assert [int(c) for c in g.block_chosen] == [int(c) for c in z["block_chosen"]]
+    # chosen h-subsets of all blocks, in original row order (exempt: rows in the oracle's tie band)
+    hs_o = np.unpackbits(z["hsubset_bits"])[:n].astype(bool)
+    hs_g = g.hsubset.cpu().numpy().astype(bool)
+    diff = np.nonzero(hs_o != hs_g)[0]
+    assert np.isin(diff, z["hsub_band_rows"]).all(), f"{diff.size} subset rows differ outside the tie band"
+    assert hs_g.sum() == hs_o.sum()
+    # pooled raw and reweighted fits (X units, north-star tolerance)
+    assert rel_sigma(g.sigma_raw, z["sigma_raw"]) < TOL
+    assert rel_mu(g.mu_raw, z["mu_raw"], z["sigma_raw"]) < TOL
+    assert rel_sigma(g.sigma_rew, z["sigma_rew"]) < TOL
+    assert rel_mu(g.mu_rew, z["mu_rew"], z["sigma_rew"]) < TOL
+    assert g.n_kept_blocks == len(z["kept_blocks"])
+    w_o = np.unpackbits(z["weights_bits"])[:n].astype(bool)
+    wd = np.nonzero(w_o != g.weights.cpu().numpy().astype(bool))[0]
+    assert np.isin(wd, z["weight_band_rows"]).all(), f"{wd.size} weights differ outside the tie band"
+    assert abs(g.n_weighted - int(z["n_weighted"])) <= len(z["weight_band_rows"])
+    f_o = np.unpackbits(z["flags_bits"])[:n].astype(bool)
+    fd = np.nonzero(f_o != g.flags.cpu().numpy().astype(bool))[0]
+    assert np.isin(fd, z["flag_band_rows"]).all(), f"{fd.size} flags differ outside the tie band"
+    idx = z["rd2_idx"]
+    assert np.allclose(g.rd2.cpu().numpy()[idx], z["rd2_val"], rtol=1e-9, atol=1e-9)
 
 
 @pytest.mark.slow
