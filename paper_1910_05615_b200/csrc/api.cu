@@ -22,6 +22,9 @@ void launch_dist_inv(int p, const double* Zall, long long m, long long blk_strid
                      int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st);
 void launch_scale_median(const double* sig_all, const int* chosen_inst, const double* qv, int q, long long m, int p,
                          double chi2half, double* out_all, cudaStream_t st);
+bool dist_tma_supported(int p, long long m);
+void launch_dist_tma(int p, const double* Zall, long long m, int nblk, const int* pairs, int npairs, const int* inst,
+                     int nstart, const double* cstage, int cstride, double* d2_all, cudaStream_t st);
 void launch_dist_mma(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
                      int ninst, const double* cstage, int cstride, double* d2_all, cudaStream_t st);
 long long launch_count();
@@ -253,6 +256,7 @@ struct CStepBufs {
   unsigned int* selcnt;
   double* sinv;   // [inst][M2] Sigma^-1 of the current operator (RTD_DIST_SMW)
   int* smw_valid; // [inst] sinv updated by SMW for the next step (RTD_DIST_SMW)
+  int* pairs;     // [inst][2] slots of the distance pass's CTA rows (two starts of a block share one)
   int* list;      // [inst][m] ordered changed rows per segment (update-based C-step)
   int* seg_cnt;   // [inst][ctas]
   long long seg_len;
@@ -281,6 +285,7 @@ void carve_cstep(Arena& A, CStepBufs& b, int ninst, long long m, int p, int max_
   b.sinv = A.take<double>((size_t)ninst * M2);
   b.smw_valid = A.take<int>(ninst);
   b.inst_dev = A.take<int>(ninst + 8);
+  b.pairs = A.take<int>(2 * (size_t)ninst + 8);
   b.memA = A.take<uint8_t>((size_t)ninst * m);
   b.memB = A.take<uint8_t>((size_t)ninst * m);
   b.sel = A.take<SelState>(ninst);
@@ -314,8 +319,29 @@ MomArgs mom_args(const CStepBufs& b, const double* Z, long long blk_stride, int 
 
 // upload distance operators of instances act[g0, g0+cnt) (staged in cstage slots) and run the distance pass
 // upload distance operators of instances act[g0, g0+cnt) (staged in cstage slots) and run the distance pass
-void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long blk_stride, int nstart, int nact,
-                 int cstride, int dist_mode = RTD_DIST_CHOLESKY) {
+// TMA-fed distance pass over the slots 0..nact-1 of inst_dev (instance ids `ids`, host copy): two starts
+// of the same block (ids 2b, 2b+1 with nstart = 2) in adjacent slots share one CTA row
+bool dist_tma(cudaStream_t st, const CStepBufs& b, const double* Z, long long blk_stride, int nstart,
+              const std::vector<int>& ids, int cstride) {
+  const int nact = (int)ids.size();
+  if (!dist_tma_supported(b.p, b.m) || blk_stride != (long long)b.p * b.m || nact == 0) return false;
+  std::vector<int> pr;
+  int nblk = 0;
+  for (int s = 0; s < nact; s++) {
+    nblk = std::max(nblk, ids[s] / nstart + 1);
+    const bool pair = nstart == 2 && s + 1 < nact && ids[s] % 2 == 0 && ids[s + 1] == ids[s] + 1;
+    pr.push_back(s);
+    pr.push_back(pair ? s + 1 : -1);
+    if (pair) s++;
+  }
+  h2d(st, b.pairs, pr.data(), pr.size() * sizeof(int));
+  launch_dist_tma(b.p, Z, b.m, nblk, b.pairs, (int)pr.size() / 2, b.inst_dev, nstart, b.cstage, cstride, b.d2, st);
+  return true;
+}
+
+void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long blk_stride, int nstart,
+                 const std::vector<int>& ids, int cstride, int dist_mode = RTD_DIST_CHOLESKY) {
+  const int nact = (int)ids.size();
   // algorithmic HBM bytes: every start's C-step streams its block (8 p per row) and writes d^2 (8 per row);
   // flops: the triangular operator and the squared norm, 2 (p(p+1)/2 + p) per row per start
   const double fm = (double)b.m, pp = (double)b.p;
@@ -328,6 +354,7 @@ void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long
   if (dist_mma_supported(b.p)) {  // FP64 tensor-pipe kernel: operator read from cstage, all instances at once
     ProfScope ps("dist", (double)nact * fm * (8.0 * pp + 8.0), (double)nact * fm * (pp * (pp + 1.0) + 2.0 * pp),
                  (double)nact * fm * (8.0 * pp + 8.0));
+    if (dist_tma(st, b, Z, blk_stride, nstart, ids, cstride)) return;
     launch_dist_mma(b.p, Z, b.m, blk_stride, b.inst_dev, nstart, nact, b.cstage, cstride, b.d2, st);
     return;
   }
@@ -397,7 +424,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
         launch_smw_stage(b.inst_dev, na, b.mu, b.sigma, p, kappa_max, b.cstage, cstride, b.sinv, b.smw_valid,
                          b.cond, b.status, st);
     }
-    dist_groups(st, b, Z, blk_stride, nstart, na, cstride, full_inv ? RTD_DIST_INVERSE : RTD_DIST_CHOLESKY);
+    dist_groups(st, b, Z, blk_stride, nstart, act, cstride, full_inv ? RTD_DIST_INVERSE : RTD_DIST_CHOLESKY);
     RTD_CU(cudaMemsetAsync(b.changed, 0, ninst * sizeof(int), st));
     {
       ProfScope ps("select", (double)na * m * 9.0);
@@ -932,7 +959,7 @@ BlockResult phase_csteps_choose(cudaStream_t st, FitBufs& f, const Dims& d, cons
     h2d(st, f.cb.inst_dev, ch.data(), ch.size() * sizeof(int));
     launch_prepare(f.cb.inst_dev, (int)ch.size(), f.cb.mu, f.cb.sigma, p, 1e300, f.cb.cstage, cstride, nullptr,
                    nullptr, nullptr, nullptr, 0, 0, st);
-    dist_groups(st, f.cb, f.Z, blk_stride, 2, (int)ch.size(), cstride);
+    dist_groups(st, f.cb, f.Z, blk_stride, 2, ch, cstride);
     for (int b : r.valid_ids)
       RTD_CU(cudaMemcpyAsync(f.ib.r + (size_t)b * m, f.cb.d2 + (size_t)r.chosen_inst[b] * m, m * sizeof(double),
                              cudaMemcpyDeviceToDevice, st));
@@ -1016,7 +1043,8 @@ void phase_reweight_blocks(cudaStream_t st, FitBufs& f, int p, int q, long long 
   {
     ProfScope ps("dist", (double)q * m * (8.0 * p + 8.0), (double)q * m * ((double)p * (p + 1.0) + 2.0 * p),
                  (double)q * m * (8.0 * p + 8.0));
-    if (dist_mma_supported(p)) {
+    if (dist_tma(st, f.cb, f.Z, blk_stride, 1, blocks, 0)) {
+    } else if (dist_mma_supported(p)) {
       launch_dist_mma(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, f.cb.cstage, 0, f.cb.d2, st);
     } else {
       ConstLease lease(f.cb.cstage, cstride, st);
