@@ -23,6 +23,8 @@ void launch_dist_inv(int p, const double* Zall, long long m, long long blk_strid
 void launch_scale_median(const double* sig_all, const int* chosen_inst, const double* qv, int q, long long m, int p,
                          double chi2half, double* out_all, cudaStream_t st);
 bool dist_tma_supported(int p, long long m);
+bool moments_tma_supported(int mode, const MomArgs& a);
+void launch_moments_tma(int mode, const MomArgs& a, int ninst, cudaStream_t st);
 void launch_dist_tma(int p, const double* Zall, long long m, int nblk, const int* pairs, int npairs, const int* inst,
                      int nstart, const double* cstage, int cstride, double* d2_all, cudaStream_t st);
 void launch_dist_mma(int p, const double* Zall, long long m, long long blk_stride, const int* inst, int nstart,
@@ -60,7 +62,8 @@ static bool use_mma() {
   return v;
 }
 static void moments(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
-  if (use_mma()) launch_moments_mma(mode, a, ninst, st);
+  if (use_mma() && moments_tma_supported(mode, a)) launch_moments_tma(mode, a, ninst, st);
+  else if (use_mma()) launch_moments_mma(mode, a, ninst, st);
   else launch_moments(mode, a, ninst, st);
 }
 
@@ -314,6 +317,8 @@ MomArgs mom_args(const CStepBufs& b, const double* Z, long long blk_stride, int 
   a.list = b.list;
   a.seg_cnt = b.seg_cnt;
   a.seg_len = b.seg_len;
+  a.nblk_hint = b.ninst_max / std::max(1, nstart);
+  a.ninst_hint = b.ninst_max;
   return a;
 }
 
@@ -736,10 +741,11 @@ void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int
   a.nstart = 1;
   a.partial = b.partial;
   a.ctas = b.ctas;
+  a.nblk_hint = q;
   // S~1: covariance of the wrapped data (centred at the wrapped mean, n - 1)
   ProfScope ps("initial", (double)q * m * p * 16.0);
   // the staged wrap pass also writes the row norms of S~2 (one read of Z less)
-  const bool fused_norms = use_mma() && moments_staged(MOM_WRAP, a);
+  const bool fused_norms = use_mma() && (moments_tma_supported(MOM_WRAP, a) || moments_staged(MOM_WRAP, a));
   if (fused_norms) a.r_out = b.r;
   moments(MOM_WRAP, a, q, st);
   a.r_out = nullptr;
@@ -1056,6 +1062,7 @@ void phase_reweight_blocks(cudaStream_t st, FitBufs& f, int p, int q, long long 
                            cudaMemcpyDeviceToDevice, st));
   MomArgs a = mom_args(f.cb, f.Z, blk_stride, 1);
   a.c2 = c2;
+  a.nblk_hint = q;
   const int np = mom_np(p);
   {
     ProfScope ps("reweight", (double)q * m * (8.0 * p + 8.0));

@@ -25,8 +25,11 @@
 #include <cstdlib>
 
 #include "rtd_internal.h"
+#include "tma.cuh"
 
 namespace rtd {
+
+using namespace tma;
 
 namespace {
 
@@ -34,43 +37,6 @@ __device__ __forceinline__ void dmma_t(double& c0, double& c1, double a, double 
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
 }
 
 // V = 0: tiles of G = 31 row groups (TR = 248 rows) for 8 consumer warps taking groups w, w+8, w+16, w+24
@@ -279,23 +245,6 @@ __global__ void __launch_bounds__((DistTmaCfg<P, V>::NCW + 1) * 32, DistTmaCfg<P
 
 namespace {
 
-using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiled encode_fn() {
-  static EncodeTiled fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    cudaGetLastError();
-    return reinterpret_cast<EncodeTiled>(p);
-  }();
-  return fn;
-}
-
 template <int P, int V>
 void dist_tma_launch_v(const CUtensorMap& map, long long m, const int* pairs, int npairs, const int* inst, int nstart,
                        const double* cstage, int cstride, double* d2_all, cudaStream_t st) {
@@ -317,14 +266,7 @@ void dist_tma_launch(const double* Zall, long long m, int nblk, const int* pairs
   static const int variant = getenv("RTD_DIST_TMA_VARIANT") ? atoi(getenv("RTD_DIST_TMA_VARIANT")) : 2;
   const int tr = variant == 1 ? DistTmaCfg<P, 1>::TR : (variant == 2 ? DistTmaCfg<P, 2>::TR : DistTmaCfg<P, 0>::TR);
   CUtensorMap map;
-  const cuuint64_t dims[3] = {(cuuint64_t)m, (cuuint64_t)P, (cuuint64_t)nblk};
-  const cuuint64_t strides[2] = {(cuuint64_t)m * 8, (cuuint64_t)m * P * 8};
-  const cuuint32_t box[3] = {(cuuint32_t)tr, (cuuint32_t)P, 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(Zall), dims, strides, box,
-                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw std::string("cuTensorMapEncodeTiled failed for the distance pass");
+  if (!encode_blocks(&map, Zall, m, P, nblk, tr)) throw std::string("cuTensorMapEncodeTiled failed for the distance pass");
   if (variant == 0) dist_tma_launch_v<P, 0>(map, m, pairs, npairs, inst, nstart, cstage, cstride, d2_all, st);
   else if (variant == 1) dist_tma_launch_v<P, 1>(map, m, pairs, npairs, inst, nstart, cstage, cstride, d2_all, st);
   else dist_tma_launch_v<P, 2>(map, m, pairs, npairs, inst, nstart, cstage, cstride, d2_all, st);

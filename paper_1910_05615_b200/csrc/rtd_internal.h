@@ -158,6 +158,8 @@ struct MomArgs {
   const int* list;          // [inst][m] changed rows per segment (+-(row+1)), MOM_DELTA on the tensor pipe
   const int* seg_cnt;       // [inst][ctas] entries per segment
   long long seg_len;        // rows per segment (segment x = CTA x)
+  int nblk_hint;            // blocks of m x p doubles at Z (the TMA-fed dense passes map them; 0: unknown)
+  int ninst_hint;           // instances the per-instance arrays (mem_new, d2) hold (0: unknown)
 };
 int mom_np(int p);  // p + p(p+1)/2 + 1
 void launch_moments(int mode, const MomArgs& a, int ninst, cudaStream_t st);
