@@ -103,24 +103,31 @@ def make_workload(cfg: int, n: int | None = None):
     return d
 
 
+SAMPLE_N = {1: 1000, 2: 100_000, 3: 100_000, 4: 100_000, 5: 20_000}  # one sample size for both CPU legs
+
+
 def cpu_baseline(cfg: int, sample_n: int | None = None):
-    """The oracle, as it stands, on a bounded sample of the same workload (rank 0, N = 1 only)."""
+    """The oracle, as it stands, on a bounded sample of the same workload (rank 0, N = 1 only).
+    `cores` = the cores the run actually kept busy (process CPU time / wall time: numpy's BLAS threads in
+    the matrix products, one core elsewhere); `blas_threads` = the BLAS pool size."""
     from threadpoolctl import threadpool_info
 
     from oracle import fit as ofit
     from paper_1910_05615_b200 import datagen
     if sample_n is None:
-        sample_n = {1: 1000, 2: 100_000, 3: 200_000, 4: 200_000, 5: 20_000}[cfg]
+        sample_n = SAMPLE_N[cfg]
     d = datagen.make_config(cfg, n=sample_n)
     q = d.q if cfg == 4 else 1
     h = int(math.floor(0.75 * sample_n)) if cfg == 4 else d.h
-    t0 = time.perf_counter()
+    c0, t0 = time.process_time(), time.perf_counter()
     ofit.fit(d.X, h=h, q=q, seed=191005615, log_transform=d.log_transform,
              partition_mode="contiguous" if cfg == 4 else "permute")
     dt = time.perf_counter() - t0
+    cpu = time.process_time() - c0
     threads = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
-    return {"value": sample_n / dt, "unit": "obs/s", "cores": int(threads), "kind": "oracle",
-            "sample": f"config {cfg} recipe at n={sample_n} (q={q}), one fit+flag, {dt:.1f} s wall"}
+    return {"value": sample_n / dt, "unit": "obs/s", "cores": round(cpu / dt, 2), "blas_threads": int(threads),
+            "kind": "oracle",
+            "sample": f"config {cfg} recipe at n={sample_n} (q={q}), one fit+flag, {dt:.1f} s wall, {cpu:.1f} s CPU"}
 
 
 def run_reference(args, rank: int, world: int):
@@ -129,7 +136,7 @@ def run_reference(args, rank: int, world: int):
         return
     cfg = args.config
     times = []
-    sample_n = args.ref_sample or {1: 1000, 2: 50_000, 3: 50_000, 4: 50_000, 5: 20_000}[cfg]
+    sample_n = args.ref_sample or SAMPLE_N[cfg]
     for s in range(args.warmup + args.steps):
         cb = cpu_baseline(cfg, sample_n)
         if s >= args.warmup:
@@ -140,8 +147,8 @@ def run_reference(args, rank: int, world: int):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": CONFIG_NAMES[cfg], "sample_rows": sample_n},
-            "cpu_baseline": {"value": value, "unit": "obs/s", "cores": cb["cores"], "kind": "oracle",
-                             "sample": cb["sample"]},
+            "cpu_baseline": {"value": value, "unit": "obs/s", "cores": cb["cores"], "blas_threads": cb["blas_threads"],
+                             "kind": "oracle", "sample": cb["sample"]},
             "e2e": {"value": value, "unit": "obs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -236,7 +243,7 @@ def run_stream(args, local: int):
         e2e = {"value": n * nb / e_tot, "unit": "obs/s", "h2d_bytes_per_step": int(n * p * 8),
                "d2h_bytes_per_step": int(n),
                "latency_ms": {"p50": float(np.percentile(e_wall, 50)), "p99": float(np.percentile(e_wall, 99))}}
-    roof = _roofline(prof, prof_ms)
+    roof = _roofline(prof, prof_ms, 5)
     cb = None if args.no_cpu_baseline else cpu_baseline(5)
     line = {"metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": 1, "steps": nb, "warmup": args.warmup,
             "ms_per_step": total_ms / nb, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -255,7 +262,47 @@ def run_stream(args, local: int):
             "e2e": e2e, "roofline": roof, "cpu_baseline": cb, "gpu_launches": int(k1 - k0), "cub_sorts": int(s1 - s0),
             "clocks": clk.summary(), "breakdown": _breakdown(prof, nprof),
             "fit": {"start_steps": [int(x) for x in res.start_steps]}}
-    print(json.dumps(line), flush=True)
+    return line
+
+
+def quick_fit(cfg: int, local: int, steps: int, warmup: int):
+    """A sub-record of the default bench line: config `cfg` fitted + flagged on this GPU (X resident),
+    CUDA events over `steps` fits after `warmup`, plus the distance-pass roofline from a profiled pass."""
+    import torch
+
+    from paper_1910_05615_b200 import api
+    d = make_workload(cfg)
+    n, p = d.X.shape
+    Xd = torch.from_numpy(d.X).to(f"cuda:{local}")
+    fl = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step():
+        return api.fit(Xd, h=d.h, q=d.q, log_transform=d.log_transform, outputs=(), out_buffers={"flags": fl})
+    for _ in range(warmup):
+        step()
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    api.set_profiling(True, device=local)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(steps):
+        step()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof = api.profile(device=local)
+    api.set_profiling(False, device=local)
+    del Xd
+    return {"workload": CONFIG_NAMES[cfg], "n": int(n), "p": int(p), "h": int(d.h), "q": int(d.q),
+            "value": n * steps / (ms / 1e3), "unit": "obs/s", "ms_per_step": ms / steps, "steps": steps,
+            "warmup": warmup, "roofline": _roofline(prof, p0.elapsed_time(p1), cfg),
+            "breakdown": {k: v for k, v in list(_breakdown(prof, steps).items())[:6]}}
 
 
 def _fp64_peak():
@@ -268,9 +315,23 @@ def _fp64_peak():
         return 37.0, "measured earlier with tools/fp64_peak.cu (DMMA burst at 1965 MHz, DESIGN.md section 6)"
 
 
-def _roofline(prof: dict, ms_local: float):
-    """The C-step distance pass (north-star kernel): HBM GB/s and FP64-tensor TFLOP/s of its launches
-    (algorithmic bytes / flops over their CUDA-event time); `bound` is the resource closer to its peak."""
+def _traffic(cfg: int):
+    """ncu DRAM bytes per algorithmic byte of the distance pass (profiles/r02_dist_traffic.json, from one
+    `ncu --set full` capture of the same kernel on the same workload)."""
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r02_dist_traffic.json")))
+        e = tj.get(CONFIG_NAMES[cfg])
+        return (e["dram_bytes"] / e["algorithmic_bytes"], tj.get("source")) if e else (None, None)
+    except Exception:
+        return None, None
+
+
+def _roofline(prof: dict, ms_local: float, cfg: int):
+    """The C-step distance pass (north-star kernel, k_dist_tma): per launch, its ALGORITHMIC bytes (every
+    block an item reads once -- the two starts of a block share the tile -- plus one d^2 per row and
+    start) and flops (p(p+1) + 2p per row and start) over the average launch time from CUDA events on the
+    library stream, against the measured HBM copy peak and the measured FP64 tensor (DMMA) peak.
+    `bound` is the resource at the higher fraction; both are reported."""
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm_peak else "fallback (B200_PROFILING.md 6650 GB/s)"
@@ -283,16 +344,26 @@ def _roofline(prof: dict, ms_local: float):
     tfs = dstat.get("flops", 0.0) / sec / 1e12
     fpk, fsrc = _fp64_peak()
     hbm = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "peak_source": peak_src}
-    ten = {"achieved": tfs, "peak": fpk, "unit": "TFLOP/s", "frac": tfs / fpk, "peak_source": fsrc}
+    ten = {"achieved": tfs, "peak": fpk, "unit": "TFLOP/s", "frac": tfs / fpk, "peak_source": fsrc,
+           "pipe": "FP64 tensor (DMMA m8n8k4)"}
     main = ten if ten["frac"] > hbm["frac"] else hbm
-    return {"bound": "tensor" if main is ten else "hbm", "achieved": main["achieved"], "peak": main["peak"],
-            "unit": main["unit"], "frac": main["frac"], "traffic": None,
-            "kernel": "k_dist_mma (C-step distance pass)",
-            "peak_source": main["peak_source"], "hbm": hbm, "fp64_tensor": ten,
-            "launches": dstat["launches"], "avg_launch_ms": dstat["ms"] / dstat["launches"],
-            "bytes_per_launch": dstat["bytes"] / dstat["launches"],
-            "flops_per_launch": dstat.get("flops", 0.0) / dstat["launches"],
-            "ms_share_of_step": dstat["ms"] / ms_local}
+    L = dstat["launches"]
+    out = {"bound": "tensor" if main is ten else "hbm", "achieved": main["achieved"], "peak": main["peak"],
+           "unit": main["unit"], "frac": main["frac"], "traffic": None,
+           "kernel": "k_dist_tma (C-step distance pass, TMA-fed, two starts per tile)",
+           "peak_source": main["peak_source"], "hbm": hbm, "fp64_tensor": ten,
+           "launches": L, "avg_launch_ms": dstat["ms"] / L, "bytes_per_launch": dstat["bytes"] / L,
+           "flops_per_launch": dstat.get("flops", 0.0) / L,
+           "per_start_definition": {"GBps": dstat.get("eff_bytes", 0.0) / sec / 1e9,
+                                    "frac": dstat.get("eff_bytes", 0.0) / sec / 1e9 / hbm_peak,
+                                    "note": "SURVEY 8(d): (8p + 8) bytes per row per start, as if every start "
+                                            "streamed its block alone"},
+           "ms_share_of_step": dstat["ms"] / ms_local}
+    ratio, src = _traffic(cfg)
+    if ratio is not None:
+        out["traffic"] = ratio * out["bytes_per_launch"]
+        out["traffic_source"] = src
+    return out
 
 
 def _breakdown(prof: dict, steps: int):
@@ -330,6 +401,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--n", type=int, default=0, help="override rows (debug only; not a bench line)")
+    ap.add_argument("--no-sub", action="store_true", help="skip the config-3 / config-5 sub-records")
+    ap.add_argument("--stream-batches", type=int, default=1000, help="batches of the config-5 sub-record")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
@@ -358,7 +431,7 @@ def main():
     cfg = args.config
     if cfg == 5:
         if rank == 0:
-            run_stream(args, local)    # replicas only: other ranks have no shared work to do
+            print(json.dumps(run_stream(args, local)), flush=True)  # replicas only (independent batches)
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
@@ -482,24 +555,25 @@ def main():
                "d2h_bytes_per_step": int(n),
                "api": "rtdetmcd_fit_batches over K pinned host batches (H2D of batch k+1 overlaps the fit of batch k)"}
 
-    roof = _roofline(prof, prof_ms)
-    if roof is not None:
-        tf = os.path.join(ROOT, "profiles", "dist_traffic.json")
-        if os.path.exists(tf):
-            try:
-                tj = json.load(open(tf))
-                if tj.get("config") == CONFIG_NAMES[cfg]:
-                    # ncu DRAM bytes per algorithmic byte of the same kernel (one --set full capture),
-                    # scaled to this run's average launch
-                    roof["traffic"] = tj["dram_per_algorithmic_byte"] * roof["bytes_per_launch"]
-                    roof["traffic_source"] = tj.get("source")
-            except Exception:
-                pass
+    roof = _roofline(prof, prof_ms, cfg)
     breakdown = _breakdown(prof, args.steps)
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(cfg)
+
+    # sub-records (N = 1): config 3, the HBM-scale p = 20 case, and config 5, the real-time stream
+    # (BASELINE.json configs[2], configs[4]); parity-test workloads, reported beside the headline
+    sub = None
+    if rank == 0 and world == 1 and not args.no_sub and cfg == 4:
+        import copy
+        sub = {"cfg3": quick_fit(3, local, 10, 3)}
+        sa = copy.copy(args)
+        sa.steps, sa.warmup, sa.no_cpu_baseline, sa.no_e2e = args.stream_batches, 3, True, False
+        sl = run_stream(sa, local)
+        sub["cfg5_stream"] = {k: sl[k] for k in ("value", "unit", "ms_per_step", "latency_ms", "warm_start", "e2e",
+                                                 "gpu_launches", "cub_sorts", "roofline")}
+        sub["cfg5_stream"]["batches"] = sa.steps
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "obs/s", "n_gpus": world, "steps": args.steps,
@@ -514,7 +588,8 @@ def main():
                 "gpu_launches": int((k1 - k0)), "cub_sorts": int(s1 - s0),
                 "clocks": clk.summary(), "breakdown": breakdown,
                 "fit": {"block_chosen": [int(x) for x in res.block_chosen] if hasattr(res, "block_chosen") else None,
-                        "start_steps": [int(x) for x in res.start_steps] if hasattr(res, "start_steps") else None}}
+                        "start_steps": [int(x) for x in res.start_steps] if hasattr(res, "start_steps") else None},
+                "sub": sub}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -340,6 +340,12 @@ bool dist_tma(cudaStream_t st, const CStepBufs& b, const double* Z, long long bl
     if (pair) s++;
   }
   h2d(st, b.pairs, pr.data(), pr.size() * sizeof(int));
+  // algorithmic bytes of this launch: every item's block read once (a pair's two starts share it) and one
+  // d^2 per row and start; flops: the triangular operator and the squared norm, p(p+1) + 2p per row and
+  // start; eff_bytes: what the paper's per-start C-steps would stream, (8p + 8) per row and start
+  const double fm = (double)b.m, pp = (double)b.p, ni = (double)pr.size() / 2;
+  ProfScope ps("dist", ni * fm * 8.0 * pp + nact * fm * 8.0, nact * fm * (pp * (pp + 1.0) + 2.0 * pp),
+               nact * fm * (8.0 * pp + 8.0));
   launch_dist_tma(b.p, Z, b.m, nblk, b.pairs, (int)pr.size() / 2, b.inst_dev, nstart, b.cstage, cstride, b.d2, st);
   return true;
 }
@@ -356,10 +362,10 @@ void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long
     launch_dist_inv(b.p, Z, b.m, blk_stride, b.inst_dev, nstart, nact, b.cstage, cstride, b.d2, st);
     return;
   }
+  if (dist_tma(st, b, Z, blk_stride, nstart, ids, cstride)) return;  // TMA-fed, two starts per tile
   if (dist_mma_supported(b.p)) {  // FP64 tensor-pipe kernel: operator read from cstage, all instances at once
     ProfScope ps("dist", (double)nact * fm * (8.0 * pp + 8.0), (double)nact * fm * (pp * (pp + 1.0) + 2.0 * pp),
                  (double)nact * fm * (8.0 * pp + 8.0));
-    if (dist_tma(st, b, Z, blk_stride, nstart, ids, cstride)) return;
     launch_dist_mma(b.p, Z, b.m, blk_stride, b.inst_dev, nstart, nact, b.cstage, cstride, b.d2, st);
     return;
   }
@@ -1046,11 +1052,10 @@ void phase_reweight_blocks(cudaStream_t st, FitBufs& f, int p, int q, long long 
   std::vector<int> blocks(q);
   for (int b = 0; b < q; b++) blocks[b] = b;
   h2d(st, f.cb.inst_dev, blocks.data(), q * sizeof(int));
-  {
+  if (!dist_tma(st, f.cb, f.Z, blk_stride, 1, blocks, 0)) {
     ProfScope ps("dist", (double)q * m * (8.0 * p + 8.0), (double)q * m * ((double)p * (p + 1.0) + 2.0 * p),
                  (double)q * m * (8.0 * p + 8.0));
-    if (dist_tma(st, f.cb, f.Z, blk_stride, 1, blocks, 0)) {
-    } else if (dist_mma_supported(p)) {
+    if (dist_mma_supported(p)) {
       launch_dist_mma(p, f.Z, m, blk_stride, f.cb.inst_dev, 1, q, f.cb.cstage, 0, f.cb.d2, st);
     } else {
       ConstLease lease(f.cb.cstage, cstride, st);

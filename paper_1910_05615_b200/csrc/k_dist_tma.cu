@@ -44,10 +44,10 @@ __device__ __forceinline__ void dmma_t(double& c0, double& c1, double a, double 
 template <int P, int V>
 struct DistTmaCfg {
   static constexpr int NCW = 8;                              // consumer warps (+ 1 producer warp)
-  static constexpr int G = V == 1 ? 15 : (V == 2 ? 23 : 31);               // 8-row groups per tile (odd: TR = 8 mod 16)
+  static constexpr int G = V == 1 ? 15 : (V == 2 ? (P <= 24 ? 15 : 23) : 31);  // 8-row groups per tile (odd: TR = 8 mod 16)
   static constexpr bool JOINT = V == 2;                      // both starts of a pair in one register pass
   static constexpr int MB = (G + NCW - 1) / NCW;             // groups per consumer warp
-  static constexpr int MINB = V == 1 ? 2 : 1;                // CTAs per SM
+  static constexpr int MINB = (V == 1 || (V == 2 && P <= 24)) ? 2 : 1;  // CTAs per SM
   // V = 2: G = 23 (TR = 184), MB = 3, one CTA per SM, and the two starts of a pair contracted together from the same raw A fragments: the
   //        centring enters the accumulators (y = M z - M mu, the same arithmetic object)
   static constexpr int TR = 8 * G;
