@@ -400,7 +400,8 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
   steps_h.assign(ninst, 0);
   std::vector<int> act, changed(ninst);
   static const bool no_small = getenv("RTD_NO_SMALL_CSTEPS") != nullptr;
-  if (dist_mode == RTD_DIST_CHOLESKY && csteps_small_supported(m, p) && !no_small) {
+  const bool use_cluster = dist_mode == RTD_DIST_CHOLESKY && !no_small && csteps_cluster_supported(m, p);
+  if (dist_mode == RTD_DIST_CHOLESKY && (csteps_small_supported(m, p) || use_cluster) && !no_small) {
     // short blocks: the whole loop of every active instance in one launch (k_csteps_small), dense
     // moments every step (exact for the final subset), no host round trip per step
     for (int i = 0; i < ninst; i++)
@@ -409,7 +410,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     h2d(st, b.inst_dev, act.data(), act.size() * sizeof(int));
     {
       ProfScope ps("csteps_small", (double)act.size() * m * (8.0 * p + 8.0));
-      launch_csteps_small(Z, m, p, blk_stride, nstart, b.inst_dev, (int)act.size(), h, kappa_max, max_steps, b.mu,
+      (use_cluster ? launch_csteps_cluster : launch_csteps_small)(Z, m, p, blk_stride, nstart, b.inst_dev, (int)act.size(), h, kappa_max, max_steps, b.mu,
                           b.sigma, b.status, b.changed, b.logdet, b.traj, b.traj_stride, b.memA, st);
     }
     std::vector<int> steps_all(ninst);

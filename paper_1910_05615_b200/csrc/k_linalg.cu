@@ -11,6 +11,8 @@
 //   k_aggregate entrywise median, KL ranking, ceil(q/2) kept, pooling.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "rtd_internal.h"
 #include "rtd_linalg.h"
 #include <cstdio>
@@ -481,6 +483,413 @@ __global__ void __launch_bounds__(CS_T, 1) k_csteps_small(const double* __restri
     status_all[id] = stat;
     steps_all[id] = step;
     logdet_all[id] = s_logdet;
+  }
+}
+
+// ------------------------------------------------------------------ the C-step loop of a mid-size block
+// on a thread-block CLUSTER (config 5: 20,000 rows, p = 8): the loop of k_csteps_small with the rows of the
+// block split over the CL CTAs of a cluster (one instance per cluster), so every per-step pass runs on CL
+// SMs, and the three couplings go through distributed shared memory (DSMEM) instead of kernel launches
+// and host round trips:
+//   - the radix select: each CTA histograms its rows' composite keys, every CTA reads the CL histograms
+//     of the cluster (map_shared_rank) and takes the same decision;
+//   - the changed-row count: CL partial counts summed in rank order;
+//   - the moments of H_new: each CTA's fixed-order warp-reduced partial sums, folded in rank order by every
+//     CTA (identical (mu, Sigma) on all of them, deterministic).
+// The Cholesky / condition / log det of the (tiny) p x p scatter is recomputed by every CTA.
+static constexpr int CSC_CL = 8;                       // CTAs per cluster (one instance)
+__device__ unsigned long long g_csc_prof[64 * 8];      // RTD_DEBUG_CSC: phase timestamps of cluster 0, rank 0
+__device__ __forceinline__ void csc_mark(int step, int ph, bool on) {
+  if (on && step < 64) {
+    unsigned long long tt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+    g_csc_prof[step * 8 + ph] = tt;
+  }
+}
+static constexpr int CSC_ROWS = 2560;                  // rows per CTA at most (m <= 20480)
+
+template <int NB>
+__global__ void __cluster_dims__(CSC_CL, 1, 1) __launch_bounds__(CS_T, 1)
+    k_csteps_cluster(const double* __restrict__ Zall, int m, int p, long long blk_stride, int nstart,
+                     const int* __restrict__ inst, int h, double kappa_max, int max_steps,
+                     double* __restrict__ mu_all, double* __restrict__ sigma_all, int* __restrict__ status_all,
+                     int* __restrict__ steps_all, double* __restrict__ logdet_all, double* __restrict__ traj,
+                     int traj_stride, uint8_t* __restrict__ mem_all) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int NBLK = NB * (NB + 1) / 2;
+  constexpr int NRED = NBLK * 64 + 8 * NB + 1;
+  extern __shared__ double dsm[];  // A, L, Li (block_* layout), then d^2 of this CTA's rows / warp partials
+  double* A = dsm;
+  double* L = dsm + RTD_MAXP * LD;
+  double* Li = dsm + 2 * RTD_MAXP * LD;
+  double* dyn = dsm + 3 * RTD_MAXP * LD;
+  __shared__ double red[RTD_MAXP];
+  __shared__ double mu_s[16], sg_s[16 * 16];
+  __shared__ double part[NRED];                      // this CTA's moment partial (read by the cluster)
+  __shared__ __align__(16) unsigned int hist[4096];  // this CTA's histogram (read by the cluster)
+  __shared__ __align__(16) unsigned int tot[4096];   // the cluster's histogram
+  __shared__ unsigned int cur[CSC_ROWS / 32], prv[CSC_ROWS / 32];
+  __shared__ long long wsum[CS_W];
+  __shared__ int s_fail, s_stat, s_found, s_done, s_chg_local;
+  __shared__ long long s_before, s_cnt;
+  __shared__ unsigned long long s_pre_hi, s_pre_lo;
+  __shared__ double s_logdet;
+  const int cr = (int)cluster.block_rank();
+  const int id = inst[blockIdx.x / CSC_CL];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, g = lane >> 2, tq = lane & 3;
+  const double* __restrict__ Z = Zall + (long long)(id / nstart) * blk_stride;
+  const int mloc = (m + CSC_CL - 1) / CSC_CL;
+  const int r0 = min(m, cr * mloc), r1 = min(m, r0 + mloc), nl = r1 - r0;
+  const int nwords = (nl + 31) / 32;
+  for (int e = t; e < p; e += CS_T) mu_s[e] = mu_all[(long long)id * RTD_MAXP + e];
+  for (int e = t; e < p * p; e += CS_T) sg_s[e] = sigma_all[(long long)id * RTD_MAXP * RTD_MAXP + e];
+  for (int w = t; w < CSC_ROWS / 32; w += CS_T) prv[w] = cur[w] = 0u;
+  if (t == 0) s_stat = ST_ACTIVE;
+  __syncthreads();
+  int step = 1;
+  const bool prof = blockIdx.x == 0 && t == 0;
+  for (; step <= max_steps; step++) {
+    csc_mark(step, 0, prof);
+    // ---- factor (every CTA, identical)
+    for (int e = t; e < p * p; e += CS_T) A[(e / p) * LD + e % p] = sg_s[e];
+    __syncthreads();
+    if (!block_cholesky(A, L, p, &s_fail)) {
+      if (t == 0) s_stat = ST_NOT_PD;
+      break;
+    }
+    block_tri_inverse(L, Li, p);
+    const double n1 = block_max_colsum_abs(A, p, red);
+    block_inv_from_li(Li, A, p);
+    const double kappa = n1 * block_max_colsum_abs(A, p, red);
+    if (t == 0) {
+      double ld = 0.0;
+      for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
+      ld *= 2.0;
+      s_logdet = ld;
+      if (traj && cr == 0) traj[(long long)id * traj_stride + step] = ld;
+      if (!(kappa < kappa_max)) s_stat = ST_COND;
+    }
+    __syncthreads();
+    if (s_stat != ST_ACTIVE) break;
+    csc_mark(step, 1, prof);
+    // ---- distances of this CTA's rows
+    constexpr int CS_R = 4;
+    for (int i0 = r0 + t; i0 < r1; i0 += CS_T * CS_R) {
+      double u[CS_R][8 * NB];
+#pragma unroll
+      for (int r = 0; r < CS_R; r++) {
+        const int i = i0 + r * CS_T;
+#pragma unroll
+        for (int k = 0; k < 8 * NB; k++) u[r][k] = (k < p && i < r1) ? __ldg(Z + (long long)k * m + i) : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < CS_R; r++) {
+        const int i = i0 + r * CS_T;
+        if (i >= r1) continue;
+        double d = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8 * NB; j++) {
+          if (j < p) {
+            double y = 0.0;
+#pragma unroll
+            for (int k = 0; k <= j; k++) y = fma(Li[j * LD + k], __dsub_rn(u[r][k], mu_s[k]), y);
+            d = fma(y, y, d);
+          }
+        }
+        dyn[i - r0] = d;
+      }
+    }
+    // ---- exact selection of the h smallest composite keys (bits(d^2) << 32 | row) over the cluster
+    if (t == 0) {
+      s_pre_hi = 0ull;
+      s_pre_lo = 0ull;
+      s_done = 0;
+      s_before = h;
+    }
+    int plen = 0;
+    __syncthreads();
+    csc_mark(step, 2, prof);
+    while (true) {
+      for (int b = t; b < 4096; b += CS_T) hist[b] = 0u;
+      __syncthreads();
+      const unsigned __int128 pre = ((unsigned __int128)s_pre_hi << 64) | s_pre_lo;
+      for (int i0 = 0; i0 < nl; i0 += CS_T) {
+        const int il = i0 + t;
+        bool take = false;
+        unsigned dig = 0;
+        if (il < nl) {
+          const unsigned __int128 C =
+              ((unsigned __int128)(unsigned long long)__double_as_longlong(dyn[il]) << 32) | (unsigned)(r0 + il);
+          take = plen == 0 || (C >> (96 - plen)) == pre;
+          dig = (unsigned)(C >> (96 - plen - 12)) & 4095u;
+        }
+        const unsigned act = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const unsigned same = __match_any_sync(act, dig);
+          if ((__ffs(same) - 1) == lane) atomicAdd(&hist[dig], (unsigned)__popc(same));
+        }
+      }
+      if (plen == 0) csc_mark(step, 6, prof);
+      cluster.sync();  // every CTA's histogram is complete
+      if (plen == 0) csc_mark(step, 7, prof);
+      constexpr int BPT = 4096 / CS_T;
+      // the cluster's histogram: coalesced 16-byte DSMEM reads of the CL histograms (rank order) into tot
+      for (int v = t; v < 4096 / 4; v += CS_T) {
+        uint4 sum = make_uint4(0u, 0u, 0u, 0u);
+        for (int q = 0; q < CSC_CL; q++) {
+          const uint4 r = reinterpret_cast<const uint4*>(cluster.map_shared_rank(hist, q))[v];
+          sum.x += r.x;
+          sum.y += r.y;
+          sum.z += r.z;
+          sum.w += r.w;
+        }
+        reinterpret_cast<uint4*>(tot)[v] = sum;
+      }
+      __syncthreads();
+      long long c[BPT], loc = 0;
+#pragma unroll
+      for (int e = 0; e < BPT; e++) {
+        c[e] = tot[t * BPT + e];
+        loc += c[e];
+      }
+      long long inc = loc;
+      for (int d = 1; d < 32; d <<= 1) {
+        const long long v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      cluster.sync();  // all remote reads of the histograms done (they are reset next round)
+      if (t == 0) {
+        long long acc = 0;
+        for (int w = 0; w < CS_W; w++) {
+          const long long v = wsum[w];
+          wsum[w] = acc;
+          acc += v;
+        }
+      }
+      __syncthreads();
+      const long long rank = s_before;
+      long long before = wsum[warp] + inc - loc;
+#pragma unroll
+      for (int e = 0; e < BPT; e++) {
+        if (c[e] > 0 && before < rank && rank <= before + c[e]) {
+          s_found = t * BPT + e;
+          s_cnt = c[e];
+          s_pre_lo = (unsigned long long)before;
+        }
+        before += c[e];
+      }
+      __syncthreads();
+      if (t == 0) {
+        const long long bef = (long long)s_pre_lo;
+        const unsigned __int128 np = (pre << 12) | (unsigned __int128)s_found;
+        s_pre_hi = (unsigned long long)(np >> 64);
+        s_pre_lo = (unsigned long long)np;
+        s_before = rank - bef;
+        s_done = (s_cnt == s_before || plen + 12 >= 96) ? 1 : 0;
+      }
+      plen += 12;
+      __syncthreads();
+      if (s_done) break;
+    }
+    csc_mark(step, 3, prof);
+    // ---- membership bits of this CTA's rows and the cluster's changed-row count
+    {
+      const unsigned __int128 pre = ((unsigned __int128)s_pre_hi << 64) | s_pre_lo;
+      if (t == 0) s_chg_local = 0;
+      __syncthreads();
+      int chg = 0;
+      for (int i0 = 0; i0 < nl; i0 += CS_T) {
+        const int il = i0 + t;
+        bool in = false;
+        if (il < nl) {
+          const unsigned __int128 C =
+              ((unsigned __int128)(unsigned long long)__double_as_longlong(dyn[il]) << 32) | (unsigned)(r0 + il);
+          in = (C >> (96 - plen)) <= pre;
+        }
+        const unsigned wb = __ballot_sync(0xffffffffu, in);
+        if (lane == 0 && i0 / 32 + warp < nwords) {
+          const int w = i0 / 32 + warp;
+          cur[w] = wb;
+          chg += __popc(wb ^ prv[w]);
+        }
+      }
+      if (lane == 0 && chg) atomicAdd(&s_chg_local, chg);
+      cluster.sync();
+      long long changed = 0;
+      for (int q = 0; q < CSC_CL; q++) changed += *cluster.map_shared_rank(&s_chg_local, q);
+      if (step > 1 && changed == 0) {
+        if (t == 0) s_stat = ST_CONVERGED;
+        cluster.sync();  // no CTA resets s_chg_local before every CTA read it
+        break;
+      }
+    }
+    csc_mark(step, 4, prof);
+    // ---- moments of H_new about the current centre: this CTA's rows on DMMA, folded in rank order
+    {
+      double acc[NBLK][2], s1[NB];
+#pragma unroll
+      for (int k = 0; k < NBLK; k++) acc[k][0] = acc[k][1] = 0.0;
+#pragma unroll
+      for (int b = 0; b < NB; b++) s1[b] = 0.0;
+      constexpr int CS_G = 8;
+      for (int rb = warp * 4 * CS_G; rb < nl; rb += CS_W * 4 * CS_G) {
+        double w[CS_G], u[CS_G][NB];
+#pragma unroll
+        for (int q = 0; q < CS_G; q++) {
+          const int rl = rb + 4 * q + tq;
+          w[q] = (rl < nl && ((cur[rl >> 5] >> (rl & 31)) & 1u)) ? 1.0 : 0.0;
+#pragma unroll
+          for (int b = 0; b < NB; b++) {
+            const int col = 8 * b + g;
+            u[q][b] = (w[q] != 0.0 && col < p) ? __ldg(Z + (long long)col * m + r0 + rl) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < CS_G; q++) {
+          if (!__any_sync(0xffffffffu, w[q] != 0.0)) continue;
+          double uu[NB], wu[NB];
+#pragma unroll
+          for (int b = 0; b < NB; b++) {
+            const int col = 8 * b + g;
+            uu[b] = (w[q] != 0.0 && col < p) ? __dsub_rn(u[q][b], mu_s[col]) : 0.0;
+            wu[b] = w[q] * uu[b];
+            s1[b] += wu[b];
+          }
+          int k = 0;
+#pragma unroll
+          for (int jb = 0; jb < NB; jb++)
+#pragma unroll
+            for (int kb = 0; kb <= jb; kb++) {
+              cs_dmma(acc[k][0], acc[k][1], wu[jb], uu[kb]);
+              k++;
+            }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 1);
+        s1[b] += __shfl_xor_sync(0xffffffffu, s1[b], 2);
+      }
+      double* rw = dyn + (size_t)warp * NRED;  // d^2 no longer needed this step
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < NBLK; k++) {
+        rw[k * 64 + g * 8 + 2 * tq] = acc[k][0];
+        rw[k * 64 + g * 8 + 2 * tq + 1] = acc[k][1];
+      }
+      if (tq == 0) {
+#pragma unroll
+        for (int b = 0; b < NB; b++) rw[NBLK * 64 + 8 * b + g] = s1[b];
+      }
+      __syncthreads();
+      for (int e = t; e < NRED - 1; e += CS_T) {  // this CTA's partial: fixed-order sum over its warps
+        double v = 0.0;
+        for (int w = 0; w < CS_W; w++) v += dyn[(size_t)w * NRED + e];
+        part[e] = v;
+      }
+      cluster.sync();  // every CTA's partial is complete
+      const double hd = (double)h;
+      double sg_new = 0.0, s1j = 0.0;
+      if (t < p * p) {
+        const int j = t / p, k = t - j * p;
+        const int a = j > k ? j : k, bq = j > k ? k : j;
+        const int ja = a >> 3, kbq = bq >> 3;
+        const int blk = ja * (ja + 1) / 2 + kbq;
+        const int e = blk * 64 + (a & 7) * 8 + (bq & 7);
+        double s2 = 0.0, sa = 0.0, sb = 0.0;
+        for (int q = 0; q < CSC_CL; q++) {  // rank order
+          const double* rr = cluster.map_shared_rank(part, q);
+          s2 += rr[e];
+          sa += rr[NBLK * 64 + a];
+          sb += rr[NBLK * 64 + bq];
+        }
+        sg_new = (s2 - sa * sb / hd) / (hd - 1.0);
+        s1j = sa;
+      }
+      cluster.sync();  // all remote reads of the partials done
+      if (t < p * p) {
+        const int j = t / p, k = t - j * p;
+        sg_s[t] = sg_new;
+        if (j == k) A[j] = s1j;
+      }
+      __syncthreads();
+      if (t < p) mu_s[t] = mu_s[t] + A[t] / hd;
+      for (int w = t; w < nwords; w += CS_T) prv[w] = cur[w];
+      __syncthreads();
+      csc_mark(step, 5, prof);
+    }
+  }
+  if (step > max_steps) {
+    step = max_steps;
+    if (t == 0) s_stat = ST_MAXSTEPS;
+  }
+  __syncthreads();
+  const int stat = s_stat;
+  if (stat == ST_MAXSTEPS) {
+    for (int e = t; e < p * p; e += CS_T) A[(e / p) * LD + e % p] = sg_s[e];
+    __syncthreads();
+    if (block_cholesky(A, L, p, &s_fail) && t == 0) {
+      double ld = 0.0;
+      for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
+      s_logdet = 2.0 * ld;
+    }
+    __syncthreads();
+  }
+  for (int il = t; il < nl; il += CS_T)
+    mem_all[(long long)id * m + r0 + il] = (uint8_t)((cur[il >> 5] >> (il & 31)) & 1u);
+  if (cr == 0) {
+    for (int e = t; e < p; e += CS_T) mu_all[(long long)id * RTD_MAXP + e] = mu_s[e];
+    for (int e = t; e < p * p; e += CS_T) sigma_all[(long long)id * RTD_MAXP * RTD_MAXP + e] = sg_s[e];
+    if (t == 0) {
+      status_all[id] = stat;
+      steps_all[id] = step;
+      logdet_all[id] = s_logdet;
+    }
+  }
+  cluster.sync();  // no CTA leaves while another may still read its shared memory
+}
+
+bool csteps_cluster_supported(long long m, int p) {
+  static const bool off = getenv("RTD_NO_CLUSTER_CSTEPS") != nullptr;
+  return !off && m > 4096 && m <= (long long)CSC_CL * CSC_ROWS && p >= 1 && p <= 16;
+}
+
+void launch_csteps_cluster(const double* Zall, long long m, int p, long long blk_stride, int nstart, const int* inst,
+                           int ninst, long long h, double kappa_max, int max_steps, double* mu_all, double* sigma_all,
+                           int* status_all, int* steps_all, double* logdet_all, double* traj, int traj_stride,
+                           uint8_t* mem_all, cudaStream_t st) {
+  const int nb = (p + 7) / 8;
+  const int nred = (nb * (nb + 1) / 2) * 64 + 8 * nb + 1;
+  const size_t dyn = (3 * (size_t)RTD_MAXP * LD + std::max<size_t>((size_t)CSC_ROWS, (size_t)CS_W * nred)) *
+                     sizeof(double);
+  if (nb == 1) {
+    RTD_CU(cudaFuncSetAttribute(k_csteps_cluster<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    k_csteps_cluster<1><<<ninst * CSC_CL, CS_T, dyn, st>>>(Zall, (int)m, p, blk_stride, nstart, inst, (int)h,
+                                                           kappa_max, max_steps, mu_all, sigma_all, status_all,
+                                                           steps_all, logdet_all, traj, traj_stride, mem_all);
+  } else {
+    RTD_CU(cudaFuncSetAttribute(k_csteps_cluster<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    k_csteps_cluster<2><<<ninst * CSC_CL, CS_T, dyn, st>>>(Zall, (int)m, p, blk_stride, nstart, inst, (int)h,
+                                                           kappa_max, max_steps, mu_all, sigma_all, status_all,
+                                                           steps_all, logdet_all, traj, traj_stride, mem_all);
+  }
+  RTD_LAUNCHED();
+  static const bool dbg = getenv("RTD_DEBUG_CSC") != nullptr;
+  if (dbg) {
+    static int calls = 0;
+    unsigned long long pr[64 * 8];
+    RTD_CU(cudaStreamSynchronize(st));
+    RTD_CU(cudaMemcpyFromSymbol(pr, g_csc_prof, sizeof(pr)));
+    if (calls++ < 3) {
+      for (int s = 1; s < 12 && pr[s * 8 + 5] > pr[s * 8]; s++)
+        fprintf(stderr, "[csc] step %d: factor %.1f dist %.1f select %.1f (hist1 %.1f sync1 %.1f) member %.1f moments %.1f us\n", s,
+                (pr[s * 8 + 1] - pr[s * 8]) * 1e-3, (pr[s * 8 + 2] - pr[s * 8 + 1]) * 1e-3,
+                (pr[s * 8 + 6] - pr[s * 8 + 2]) * 1e-3, (pr[s * 8 + 7] - pr[s * 8 + 6]) * 1e-3,
+                (pr[s * 8 + 3] - pr[s * 8 + 2]) * 1e-3, (pr[s * 8 + 4] - pr[s * 8 + 3]) * 1e-3,
+                (pr[s * 8 + 5] - pr[s * 8 + 4]) * 1e-3);
+    }
   }
 }
 

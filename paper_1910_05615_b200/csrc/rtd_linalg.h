@@ -20,6 +20,12 @@ void launch_smw_stage(const int* inst, int ninst, const double* mu_all, const do
                       double kappa_max, double* cstage, int cstride, double* sinv_all, int* smw_valid,
                       double* cond_out, int* status, cudaStream_t st);
 // the whole C-step loop of short blocks (m <= 20480, p <= 16) in one CTA per instance (k_linalg.cu)
+// 4096 < m <= 20480, p <= 16: the same loop on a cluster of 8 CTAs per instance (DSMEM couplings)
+bool csteps_cluster_supported(long long m, int p);
+void launch_csteps_cluster(const double* Zall, long long m, int p, long long blk_stride, int nstart, const int* inst,
+                           int ninst, long long h, double kappa_max, int max_steps, double* mu_all, double* sigma_all,
+                           int* status_all, int* steps_all, double* logdet_all, double* traj, int traj_stride,
+                           uint8_t* mem_all, cudaStream_t st);
 bool csteps_small_supported(long long m, int p);
 void launch_csteps_small(const double* Zall, long long m, int p, long long blk_stride, int nstart, const int* inst,
                          int ninst, long long h, double kappa_max, int max_steps, double* mu_all, double* sigma_all,
