@@ -9,6 +9,7 @@
 //   loc = round(sum kept)/k, scale^2 = c(.975,1) sum_kept (y-loc)^2/(k-1).
 // Prefix sums are never materialised: each window CTA rebuilds the two
 // prefix streams it needs (P(s) and P(s+h)) from per-chunk totals.
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cstdlib>
@@ -492,6 +493,130 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
   out[col] = o;
 }
 
+// ------------------------------------------------------------------ cluster radix sort of short columns
+// Columns of up to UCS_CL * UCS_CAP = 32768 rows (config 5: 20,000) are sorted by one 8-CTA thread-block
+// cluster each, instead of by two device-wide CUB radix sorts: every CTA holds a contiguous eighth of the
+// column as order-preserving 64-bit keys in shared memory; 8 stable LSD passes of 8 bits, each: per-warp
+// digit counts (match_any ranking), the cluster's per-(digit, CTA) offsets from the 8 CTAs' counts
+// (DSMEM), and a scatter of every key straight into the destination CTA's receive buffer (DSMEM stores);
+// passes whose digit is the same for every key of the column are skipped.  The sorted column is written
+// back as doubles for the window kernels below.  Stable and exact: the same order as any correct sort.
+static constexpr int UCS_CL = 8;      // CTAs per cluster (one column)
+static constexpr int UCS_CAP = 4096;  // keys per CTA
+static constexpr int UCS_T = 512;
+static constexpr int UCS_W = UCS_T / 32;
+
+__device__ __forceinline__ unsigned long long ucs_key(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ucs_val(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+__global__ void __cluster_dims__(UCS_CL, 1, 1) __launch_bounds__(UCS_T, 1)
+    k_uni_cluster_sort(const double* __restrict__ cols, long long len, double* __restrict__ sorted) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ unsigned long long ucs_dyn[];  // [2][UCS_CAP] key buffers (receive buffers of the scatter)
+  unsigned long long* buf[2] = {ucs_dyn, ucs_dyn + UCS_CAP};
+  __shared__ unsigned int whist[UCS_W][256];   // per-warp digit counts, then running offsets
+  __shared__ __align__(16) unsigned int ccnt[256];  // this CTA's digit counts (read by the cluster)
+  __shared__ unsigned int base[256];           // destination of this CTA's first key of each digit
+  __shared__ int s_skip;
+  const int r = (int)cluster.block_rank();
+  const int col = blockIdx.x / UCS_CL;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nloc = (int)((len + UCS_CL - 1) / UCS_CL);
+  const int r0 = min((int)len, r * nloc), cnt = min((int)len, r0 + nloc) - r0;
+  const double* y = cols + (long long)col * len;
+  for (int i = t; i < cnt; i += UCS_T) buf[0][i] = ucs_key(y[r0 + i]);
+  // warp w owns the local items [w per_w, (w+1) per_w), processed 32 at a time in order (stability)
+  const int per_w = (cnt + UCS_W - 1) / UCS_W;
+  const int w0 = min(cnt, warp * per_w), w1 = min(cnt, w0 + per_w);
+  int cur = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 8; pass++) {
+    const int sh = 8 * pass;
+    const unsigned long long* src = buf[cur];
+    for (int d = lane; d < 256; d += 32) whist[warp][d] = 0u;
+    __syncwarp();
+    for (int i0 = w0; i0 < w1; i0 += 32) {
+      const int i = i0 + lane;
+      const bool in = i < w1;
+      const unsigned dig = in ? (unsigned)(src[i] >> sh) & 255u : 0u;
+      const unsigned act = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const unsigned same = __match_any_sync(act, dig);
+        if ((__ffs(same) - 1) == lane) whist[warp][dig] += (unsigned)__popc(same);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    if (t < 256) {  // this CTA's count of digit t, warp prefixes (running offsets start there)
+      unsigned acc = 0;
+      for (int w = 0; w < UCS_W; w++) {
+        const unsigned v = whist[w][t];
+        whist[w][t] = acc;
+        acc += v;
+      }
+      ccnt[t] = acc;
+    }
+    cluster.sync();  // every CTA's counts are published
+    if (t < 256) {
+      // total of each digit over the cluster, keys of this digit in lower-ranked CTAs
+      unsigned tot = 0, before = 0;
+      for (int q = 0; q < UCS_CL; q++) {
+        const unsigned v = cluster.map_shared_rank(ccnt, q)[t];
+        tot += v;
+        if (q < r) before += v;
+      }
+      base[t] = before;
+      // exclusive scan of the totals over digits (block-wide, 256 values)
+      unsigned inc = tot;
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+      }
+      __shared__ unsigned wtot[8];
+      if (lane == 31) wtot[warp] = inc;
+      asm volatile("bar.sync 2, 256;\n" ::: "memory");
+      unsigned off = 0;
+      for (int w = 0; w < warp; w++) off += wtot[w];
+      base[t] += off + inc - tot;
+      if (t == 0) s_skip = 0;
+      asm volatile("bar.sync 2, 256;\n" ::: "memory");
+      if (tot == (unsigned)len) s_skip = 1;  // every key of the column has this digit: nothing moves
+    }
+    cluster.sync();  // every CTA read the counts (ccnt is rewritten next pass); base / s_skip ready
+    if (s_skip) continue;
+    unsigned long long* dstbuf = buf[cur ^ 1];
+    for (int i0 = w0; i0 < w1; i0 += 32) {
+      const int i = i0 + lane;
+      const bool in = i < w1;
+      const unsigned long long k = in ? src[i] : 0ull;
+      const unsigned dig = (unsigned)(k >> sh) & 255u;
+      const unsigned act = __ballot_sync(0xffffffffu, in);
+      unsigned same = 0, rank = 0;
+      if (in) {
+        same = __match_any_sync(act, dig);
+        rank = whist[warp][dig] + (unsigned)__popc(same & ((1u << lane) - 1u));
+        const unsigned pos = base[dig] + rank;
+        const int dq = (int)(pos / (unsigned)nloc), doff = (int)(pos - (unsigned)dq * (unsigned)nloc);
+        cluster.map_shared_rank(dstbuf, dq)[doff] = k;
+      }
+      __syncwarp();
+      if (in && (__ffs(same) - 1) == lane) whist[warp][dig] += (unsigned)__popc(same);
+      __syncwarp();
+    }
+    cur ^= 1;
+    cluster.sync();  // every key landed in its destination CTA
+  }
+  double* out = sorted + (long long)col * len;
+  for (int i = t; i < cnt; i += UCS_T) out[r0 + i] = ucs_val(buf[cur][i]);
+  cluster.sync();  // no CTA leaves while another may still write into its buffers
+}
+
 struct UniScratch {
   double* sorted;
   double* tmpk;
@@ -577,12 +702,19 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
     if (done) return;
   }
   if (A.base == nullptr) return;  // dry run
+  static const bool no_csort = getenv("RTD_UNI_NOCLUSTERSORT") != nullptr;
+  const bool csort = !no_csort && len <= (long long)UCS_CL * UCS_CAP;
   for (int c0 = 0; c0 < ncols; c0 += USORT) {
     const int nc = std::min(USORT, ncols - c0);
     const double* cc = cols + (long long)c0 * len;
     const long long Nc = len * nc;
     size_t bytes = s.cub_bytes;
-    if (nc == 1) {
+    if (csort) {  // one 8-CTA cluster per column, no library sort
+      const int dyn = 2 * UCS_CAP * (int)sizeof(unsigned long long);
+      RTD_CU(cudaFuncSetAttribute(k_uni_cluster_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+      k_uni_cluster_sort<<<nc * UCS_CL, UCS_T, dyn, st>>>(cc, len, s.sorted);
+      RTD_LAUNCHED();
+    } else if (nc == 1) {
       count_sort();
       RTD_CU(cub::DeviceRadixSort::SortKeys(s.cub_tmp, bytes, cc, s.sorted, (int)Nc, 0, 64, st));
     } else {
