@@ -493,20 +493,25 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
   out[col] = o;
 }
 
-// ------------------------------------------------------------------ cluster radix sort of short columns
+// ------------------------------------------------------------------ cluster sort of short columns
 // Columns of up to UCS_CL * UCS_CAP = 32768 rows (config 5: 20,000) are sorted by one 8-CTA thread-block
-// cluster each, instead of by two device-wide CUB radix sorts: every CTA holds a contiguous eighth of the
-// column as order-preserving 64-bit keys in shared memory; 8 stable LSD passes of 8 bits, each: per-warp
-// digit counts (match_any ranking), the cluster's per-(digit, CTA) offsets from the 8 CTAs' counts
-// (DSMEM), and a scatter of every key straight into the destination CTA's receive buffer (DSMEM stores);
-// passes whose digit is the same for every key of the column are skipped.  The sorted column is written
-// back as doubles for the window kernels below.  Stable and exact: the same order as any correct sort.
+// cluster each, instead of by two device-wide CUB radix sorts:
+//   1. every CTA sorts a contiguous eighth of the column, padded to 4096 with keys above all others, by a
+//      bitonic network held in registers (4 values per thread): strides < 4 inside a thread, < 128 by warp
+//      shuffles,
+//      larger ones through shared memory;
+//   2. three merge rounds pair the sorted runs (8 -> 4 -> 2 -> 1 per cluster): each CTA finds where its
+//      stretch of the merged run starts and ends in the two input runs (merge path, a 32-ary search by
+//      one warp over the runs where they live -- the shared memory of the other CTAs, DSMEM), copies the
+//      two sub-ranges into its own shared memory and merges them there, every thread a stretch of its own
+//      (merge path again, stable: ties take the left run first).
+// The sorted column is written back for the window kernels below.
 static constexpr int UCS_CL = 8;      // CTAs per cluster (one column)
-static constexpr int UCS_CAP = 4096;  // keys per CTA
-static constexpr int UCS_T = 512;
-static constexpr int UCS_W = UCS_T / 32;
+static constexpr int UCS_CAP = 4096;  // values per CTA
+static constexpr int UCS_T = 1024;
+static constexpr int UCS_V = UCS_CAP / UCS_T;  // values per thread in the local sort (4)
 
-__device__ __forceinline__ unsigned long long ucs_key(double x) {
+__device__ __forceinline__ unsigned long long ucs_key(double x) {  // order-preserving key of x
   const unsigned long long u = (unsigned long long)__double_as_longlong(x);
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
@@ -514,107 +519,153 @@ __device__ __forceinline__ double ucs_val(unsigned long long k) {
   return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
 }
 
+// smallest i in [lo, hi] with A(i) > B(o - i - 1) (hi if none) -- the merge-path split of output o, stable;
+// evaluated by the 32 lanes of one warp (32-ary search), A / B read through `elem`
+template <class F>
+__device__ __forceinline__ int ucs_split(int o, int lo, int hi, int gA, int gB, F elem, int lane) {
+  while (lo < hi) {
+    const int step = (hi - lo + 31) / 32;
+    const int i = lo + lane * step;
+    const bool pr = i < hi ? (elem(gA + i) > elem(gB + o - i - 1)) : true;
+    const unsigned bal = __ballot_sync(0xffffffffu, pr);
+    if (bal == 0u) {  // the split lies beyond the last probe
+      lo = lo + 31 * step + 1;
+      continue;
+    }
+    const int f = __ffs(bal) - 1;  // first lane whose probe is at or past the split
+    const int nhi = min(hi, lo + f * step);
+    const int nlo = f == 0 ? lo : lo + (f - 1) * step + 1;
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
+// a bitonic stage whose pairs lie inside a thread (stride S < UCS_V, compile time: x stays in registers)
+template <int S>
+__device__ __forceinline__ void ucs_reg_stage(unsigned long long (&x)[UCS_V], int t, int size) {
+#pragma unroll
+  for (int k = 0; k < UCS_V; k++) {
+    if ((k & S) == 0) {
+      const int e = t * UCS_V + k;
+      const bool up = (e & size) == 0;
+      const unsigned long long a = x[k], b = x[k + S];
+      const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
+      x[k] = up ? lo : hi;
+      x[k + S] = up ? hi : lo;
+    }
+  }
+}
+
 __global__ void __cluster_dims__(UCS_CL, 1, 1) __launch_bounds__(UCS_T, 1)
     k_uni_cluster_sort(const double* __restrict__ cols, long long len, double* __restrict__ sorted) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ unsigned long long ucs_dyn[];  // [2][UCS_CAP] key buffers (receive buffers of the scatter)
-  unsigned long long* buf[2] = {ucs_dyn, ucs_dyn + UCS_CAP};
-  __shared__ unsigned int whist[UCS_W][256];   // per-warp digit counts, then running offsets
-  __shared__ __align__(16) unsigned int ccnt[256];  // this CTA's digit counts (read by the cluster)
-  __shared__ unsigned int base[256];           // destination of this CTA's first key of each digit
-  __shared__ int s_skip;
+  extern __shared__ unsigned long long ucs_dyn[];  // [2][UCS_CAP] runs (read remotely), [2][UCS_CAP] local copies
+  // values as order-preserving 64-bit keys (integer compares in the network and the merges)
+  __shared__ int s_split[2];
   const int r = (int)cluster.block_rank();
   const int col = blockIdx.x / UCS_CL;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int nloc = (int)((len + UCS_CL - 1) / UCS_CL);
-  const int r0 = min((int)len, r * nloc), cnt = min((int)len, r0 + nloc) - r0;
+  const int t = threadIdx.x, lane = t & 31;
+  const int n = (int)len;
+  const int nloc = (n + UCS_CL - 1) / UCS_CL;
+  const int r0 = min(n, r * nloc), cnt = min(n, r0 + nloc) - r0;
   const double* y = cols + (long long)col * len;
-  for (int i = t; i < cnt; i += UCS_T) buf[0][i] = ucs_key(y[r0 + i]);
-  // warp w owns the local items [w per_w, (w+1) per_w), processed 32 at a time in order (stability)
-  const int per_w = (cnt + UCS_W - 1) / UCS_W;
-  const int w0 = min(cnt, warp * per_w), w1 = min(cnt, w0 + per_w);
-  int cur = 0;
-  __syncthreads();
-  for (int pass = 0; pass < 8; pass++) {
-    const int sh = 8 * pass;
-    const unsigned long long* src = buf[cur];
-    for (int d = lane; d < 256; d += 32) whist[warp][d] = 0u;
-    __syncwarp();
-    for (int i0 = w0; i0 < w1; i0 += 32) {
-      const int i = i0 + lane;
-      const bool in = i < w1;
-      const unsigned dig = in ? (unsigned)(src[i] >> sh) & 255u : 0u;
-      const unsigned act = __ballot_sync(0xffffffffu, in);
-      if (in) {
-        const unsigned same = __match_any_sync(act, dig);
-        if ((__ffs(same) - 1) == lane) whist[warp][dig] += (unsigned)__popc(same);
+  unsigned long long* xs = ucs_dyn + UCS_CAP;  // exchange buffer of the local sort
+  // ---- 1. local bitonic sort in registers: element e = t * UCS_V + k
+  unsigned long long x[UCS_V];
+#pragma unroll
+  for (int k = 0; k < UCS_V; k++) {
+    const int e = t * UCS_V + k;
+    x[k] = e < cnt ? ucs_key(y[r0 + e]) : ~0ull;  // padding above every key
+  }
+  for (int size = 2; size <= UCS_CAP; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride < UCS_V) {
+        if (stride == 4) ucs_reg_stage<4>(x, t, size);
+        else if (stride == 2) ucs_reg_stage<2>(x, t, size);
+        else ucs_reg_stage<1>(x, t, size);
+      } else if (stride < UCS_V * 32) {
+        const int lm = stride / UCS_V;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int k = 0; k < UCS_V; k++) {
+          const int e = t * UCS_V + k;
+          const unsigned long long o = __shfl_xor_sync(0xffffffffu, x[k], lm);
+          const bool keep_min = ((e & size) == 0) == lower;
+          x[k] = keep_min ? (x[k] < o ? x[k] : o) : (x[k] < o ? o : x[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < UCS_V; k++) xs[t * UCS_V + k] = x[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < UCS_V; k++) {
+          const int e = t * UCS_V + k;
+          const unsigned long long o = xs[e ^ stride];
+          const bool keep_min = ((e & size) == 0) == ((e & stride) == 0);
+          x[k] = keep_min ? (x[k] < o ? x[k] : o) : (x[k] < o ? o : x[k]);
+        }
+        __syncthreads();
       }
-      __syncwarp();
+    }
+  }
+  unsigned long long* v = ucs_dyn;
+#pragma unroll
+  for (int k = 0; k < UCS_V; k++) {
+    const int e = t * UCS_V + k;
+    if (e < cnt) v[e] = x[k];
+  }
+  cluster.sync();
+  // ---- 2. merge rounds over the cluster
+  int cur = 0;
+  unsigned long long* la = ucs_dyn + 2 * UCS_CAP;
+  unsigned long long* lb = ucs_dyn + 3 * UCS_CAP;
+  for (int span = 1; span < UCS_CL; span <<= 1) {
+    const unsigned long long* src = ucs_dyn + cur * UCS_CAP;
+    unsigned long long* dst = ucs_dyn + (cur ^ 1) * UCS_CAP;
+    const int grp = r / (2 * span);
+    const int gs = min(n, grp * 2 * span * nloc), gm = min(n, gs + span * nloc), ge = min(n, gm + span * nloc);
+    const int na = gm - gs, nb = ge - gm;
+    auto elem = [&](int g) -> unsigned long long {  // global position g of the current runs, in CTA g / nloc
+      const int q = g / nloc;
+      return cluster.map_shared_rank(src, q)[g - q * nloc];
+    };
+    const int olo = r0 - gs, ohi = olo + cnt;  // this CTA's outputs, relative to the group
+    if (t < 64) {
+      const int o = t < 32 ? olo : ohi;
+      const int sp = ucs_split(o, max(0, o - nb), min(o, na), gs, gm, elem, lane);
+      if (lane == 0) s_split[t >> 5] = sp;
     }
     __syncthreads();
-    if (t < 256) {  // this CTA's count of digit t, warp prefixes (running offsets start there)
-      unsigned acc = 0;
-      for (int w = 0; w < UCS_W; w++) {
-        const unsigned v = whist[w][t];
-        whist[w][t] = acc;
-        acc += v;
+    const int ia = s_split[0], ib = s_split[1];
+    const int ja = olo - ia, jb = ohi - ib;  // B sub-range [ja, jb)
+    const int nla = ib - ia, nlb = jb - ja;
+    for (int e = t; e < nla; e += UCS_T) la[e] = elem(gs + ia + e);
+    for (int e = t; e < nlb; e += UCS_T) lb[e] = elem(gm + ja + e);
+    __syncthreads();
+    const int ept = (cnt + UCS_T - 1) / UCS_T;
+    const int o0 = min(cnt, t * ept), o1 = min(cnt, o0 + ept);
+    if (o0 < o1) {
+      int lo = max(0, o0 - nlb), hi = min(o0, nla);
+      while (lo < hi) {
+        const int i = (lo + hi) >> 1;
+        if (la[i] <= lb[o0 - i - 1]) lo = i + 1;
+        else hi = i;
       }
-      ccnt[t] = acc;
-    }
-    cluster.sync();  // every CTA's counts are published
-    if (t < 256) {
-      // total of each digit over the cluster, keys of this digit in lower-ranked CTAs
-      unsigned tot = 0, before = 0;
-      for (int q = 0; q < UCS_CL; q++) {
-        const unsigned v = cluster.map_shared_rank(ccnt, q)[t];
-        tot += v;
-        if (q < r) before += v;
+      int i = lo, j = o0 - lo;
+      for (int o = o0; o < o1; o++) {
+        const bool takeA = j >= nlb || (i < nla && la[i] <= lb[j]);
+        dst[o] = takeA ? la[i++] : lb[j++];
       }
-      base[t] = before;
-      // exclusive scan of the totals over digits (block-wide, 256 values)
-      unsigned inc = tot;
-      for (int d = 1; d < 32; d <<= 1) {
-        const unsigned v = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += v;
-      }
-      __shared__ unsigned wtot[8];
-      if (lane == 31) wtot[warp] = inc;
-      asm volatile("bar.sync 2, 256;\n" ::: "memory");
-      unsigned off = 0;
-      for (int w = 0; w < warp; w++) off += wtot[w];
-      base[t] += off + inc - tot;
-      if (t == 0) s_skip = 0;
-      asm volatile("bar.sync 2, 256;\n" ::: "memory");
-      if (tot == (unsigned)len) s_skip = 1;  // every key of the column has this digit: nothing moves
-    }
-    cluster.sync();  // every CTA read the counts (ccnt is rewritten next pass); base / s_skip ready
-    if (s_skip) continue;
-    unsigned long long* dstbuf = buf[cur ^ 1];
-    for (int i0 = w0; i0 < w1; i0 += 32) {
-      const int i = i0 + lane;
-      const bool in = i < w1;
-      const unsigned long long k = in ? src[i] : 0ull;
-      const unsigned dig = (unsigned)(k >> sh) & 255u;
-      const unsigned act = __ballot_sync(0xffffffffu, in);
-      unsigned same = 0, rank = 0;
-      if (in) {
-        same = __match_any_sync(act, dig);
-        rank = whist[warp][dig] + (unsigned)__popc(same & ((1u << lane) - 1u));
-        const unsigned pos = base[dig] + rank;
-        const int dq = (int)(pos / (unsigned)nloc), doff = (int)(pos - (unsigned)dq * (unsigned)nloc);
-        cluster.map_shared_rank(dstbuf, dq)[doff] = k;
-      }
-      __syncwarp();
-      if (in && (__ffs(same) - 1) == lane) whist[warp][dig] += (unsigned)__popc(same);
-      __syncwarp();
     }
     cur ^= 1;
-    cluster.sync();  // every key landed in its destination CTA
+    cluster.sync();  // the round's outputs are complete everywhere (and nobody still reads src)
   }
+  const unsigned long long* fin = ucs_dyn + cur * UCS_CAP;
   double* out = sorted + (long long)col * len;
-  for (int i = t; i < cnt; i += UCS_T) out[r0 + i] = ucs_val(buf[cur][i]);
-  cluster.sync();  // no CTA leaves while another may still write into its buffers
+  for (int i = t; i < cnt; i += UCS_T) out[r0 + i] = ucs_val(fin[i]);
+  cluster.sync();  // no CTA leaves while another may still read its buffers
 }
 
 struct UniScratch {
@@ -710,7 +761,7 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
     const long long Nc = len * nc;
     size_t bytes = s.cub_bytes;
     if (csort) {  // one 8-CTA cluster per column, no library sort
-      const int dyn = 2 * UCS_CAP * (int)sizeof(unsigned long long);
+      const int dyn = 4 * UCS_CAP * (int)sizeof(unsigned long long);
       RTD_CU(cudaFuncSetAttribute(k_uni_cluster_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
       k_uni_cluster_sort<<<nc * UCS_CL, UCS_T, dyn, st>>>(cc, len, s.sorted);
       RTD_LAUNCHED();
