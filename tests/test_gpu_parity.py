@@ -30,7 +30,8 @@ def _cuda(a):
 
 
 # ------------------------------------------------------------------ K1 univariate MCD
-@pytest.mark.parametrize("n", [2, 3, 5, 17, 1000, 1023, 1024, 1025, 4097, 100_003])
+# 4097 .. 32768: the 8-CTA cluster sort (k_uni_cluster_sort), incl. lengths not divisible by 8 and the cap
+@pytest.mark.parametrize("n", [2, 3, 5, 17, 1000, 1023, 1024, 1025, 4097, 20_000, 20_001, 32_767, 32_768, 100_003])
 def test_unimcd_sizes(n):
     rng = np.random.default_rng(n)
     cols = np.stack([rng.standard_normal(n), rng.standard_normal(n) * 3 + 100, rng.exponential(size=n)])
@@ -43,6 +44,27 @@ def test_unimcd_sizes(n):
         assert g["start"][j] == r.start
         assert g["raw_loc"][j] == pytest.approx(r.loc, rel=1e-15, abs=1e-300)
         assert g["raw_var"][j] == pytest.approx(r.var_raw, rel=1e-14)
+        assert g["loc"][j] == pytest.approx(o.loc, rel=1e-14, abs=1e-14)
+        assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13)
+
+
+@pytest.mark.parametrize("n", [8_191, 20_000])
+def test_unimcd_cluster_sort_ties_signed_zeros(n):
+    # heavy ties, signed zeros and duplicated extremes across the 8 CTA slices of the cluster sort:
+    # the window start / locations must still be the exact ones (ties -> lowest start, reading R2)
+    rng = np.random.default_rng(n)
+    a = np.round(rng.standard_normal(n), 1)
+    a[::7] = 0.0
+    a[1::7] = -0.0
+    a[: n // 50] = 1e6
+    b = np.repeat(rng.standard_normal(n // 10 + 1), 10)[:n]
+    cols = np.stack([a, b, -a])
+    g = api.unimcd(_cuda(cols))
+    for j in range(cols.shape[0]):
+        o = unimcd_reweighted(cols[j])
+        r = unimcd_raw(cols[j], n // 2 + 1)
+        assert g["start"][j] == r.start
+        assert g["raw_loc"][j] == pytest.approx(r.loc, rel=1e-15, abs=1e-300)
         assert g["loc"][j] == pytest.approx(o.loc, rel=1e-14, abs=1e-14)
         assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13)
 
@@ -189,8 +211,11 @@ def test_refinement_ill_conditioned():
 
 
 # ------------------------------------------------------------------ C-steps
+# 4096 < n <= 20480 with p <= 16: the loop on an 8-CTA cluster (k_csteps_cluster); 12_345 at p = 40 and
+# 30_001: the multi-launch loop
 @pytest.mark.parametrize("cfg,n,refresh", [(1, 1000, 32), (2, 20_000, 32), (3, 30_001, 32), (3, 30_001, 1),
-                                           (4, 12_345, 32), (5, 20_000, 3)])
+                                           (4, 12_345, 32), (5, 20_000, 3), (2, 4_097, 32), (2, 20_480, 32),
+                                           (5, 9_999, 32)])
 def test_csteps(cfg, n, refresh):
     d, Z = _zblock(cfg, n)
     h = (d.h * n) // d.meta["n"] if d.meta["n"] != n else d.h
