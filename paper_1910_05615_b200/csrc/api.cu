@@ -10,6 +10,7 @@
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/rtdetmcd.h"
 #include "rtd_internal.h"
@@ -127,6 +128,7 @@ struct ProfScope {
   double bytes, flops, eff_bytes;
   ProfScope(const char* name, double algorithmic_bytes, double algorithmic_flops = 0.0, double effective_bytes = 0.0)
       : bytes(algorithmic_bytes), flops(algorithmic_flops), eff_bytes(effective_bytes) {
+    nvtxRangePushA(name);  // host-side range of the launches of this kernel class (nsys / ncu --nvtx)
     if (!g_prof || !g_prof->on) return;
     idx = g_prof->index(name);
     a = g_prof->ev();
@@ -134,10 +136,17 @@ struct ProfScope {
     cudaEventRecord(a, g_prof_stream);
   }
   ~ProfScope() {
+    nvtxRangePop();
     if (idx < 0) return;
     cudaEventRecord(b, g_prof_stream);
     g_prof->pending.push_back({idx, a, b, bytes, flops, eff_bytes});
   }
+};
+
+// NVTX range over a phase of the fit (the steps of PAPER.md §4)
+struct NvtxPhase {
+  explicit NvtxPhase(const char* name) { nvtxRangePushA(name); }
+  ~NvtxPhase() { nvtxRangePop(); }
 };
 
 struct rtdetmcd_ctx {
@@ -1125,7 +1134,10 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
   phase_columns(st, Xdev, n, p, d.log, f.Xc, f.bad);
 
   // H1: global column standardisation
-  run_unimcd(st, f.uscratch, f.uscratch_bytes, f.Xc, n, p, f.uni);
+  {
+    NvtxPhase ph("H1 standardise");
+    run_unimcd(st, f.uscratch, f.uscratch_bytes, f.Xc, n, p, f.uni);
+  }
   std::vector<UniOut> uni(p);
   d2h(st, uni.data(), f.uni, p * sizeof(UniOut));
   for (int j = 0; j < p; j++)
@@ -1146,15 +1158,26 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     h2d(st, f.warm_mu, wm.data(), RTD_MAXP * sizeof(double));
     h2d(st, f.warm_sig, ws.data(), M2 * sizeof(double));
   }
-  BlockResult br = phase_blocks(st, f, d, o, warm);
+  BlockResult br;
+  {
+    NvtxPhase ph("H2-H9 blocks");
+    br = phase_blocks(st, f, d, o, warm);
+  }
   warnings |= br.warnings;
-  const int n_kept = phase_raw(st, f, p, q, m, br.valid_ids);
+  int n_kept;
+  {
+    NvtxPhase ph("H10 aggregate");
+    n_kept = phase_raw(st, f, p, q, m, br.valid_ids);
+  }
 
   // H11: reweighting over the fitted rows, per block then pooled
   const double c2 = chi2_quantile(o.quantile, p);
   const int cstride = p + p * (p + 1) / 2;
-  phase_reweight_blocks(st, f, p, q, m, c2, true);
-  phase_pool(st, f, p, q, o.quantile, f.sums_rw, true);
+  {
+    NvtxPhase ph("H11 reweight");
+    phase_reweight_blocks(st, f, p, q, m, c2, true);
+    phase_pool(st, f, p, q, o.quantile, f.sums_rw, true);
+  }
   // de-standardise raw and reweighted fits (H13)
   launch_destandardize(f.uni, f.mu_raw, f.sig_raw, p, f.muX, f.sigX, st);
   launch_destandardize(f.uni, f.mu_rew, f.sig_rew, p, f.muX + RTD_MAXP, f.sigX + M2, st);
