@@ -18,7 +18,10 @@
 //   5. the gathered sets are sorted (shared-memory bitonic chunks + merge path), prefix-summed in
 //      double-double, and h*SQ(s) is evaluated exactly for every candidate s:
 //      argmin, ties -> lowest s (reading R2);
-//   6. one pass sums the kept points of the reweighting step (reading R4).
+//   6. one pass sums the kept points of the reweighting step (reading R4).  Optional (RTD_UNI_FUSEDKEEP):
+//      fused into pass 4 -- the raw fit is bracketed by the bounds of step 3, so the values certainly kept
+//      are summed there and only the two narrow bands around the kept interval's ends are gathered and
+//      decided once the raw fit is known (k_pr_final_fused); measured slower (FP64-bound), off by default.
 // A column whose candidate sets do not fit (massive ties, extreme shapes)
 // makes the caller fall back to the full radix-sort path (same result).
 #include <cstdio>
@@ -47,7 +50,10 @@ struct PrunedCol {
   int bs_lo, bs_hi, be_lo, be_hi;  // gathered bucket ranges (start side / end side)
   long long cs_lo, ce_lo;    // C[bs_lo], C[be_lo]
   int status;                // 0 ok, 1 fall back
-  int pad;
+  int kfused;                // 1: the reweighting sums are taken in the gather pass (step 6 fused into 4)
+  double kc;                 // shift of the fused reweighting sums (centre of the raw location's interval)
+  double kin_lo, kin_hi;     // values certainly kept by the reweighting, whatever the exact raw fit
+  double kout_lo, kout_hi;   // outside [kout_lo, kout_hi]: certainly dropped; between: decided in k_pr_final
 };
 
 __device__ __forceinline__ int bucket_of(double y, const PrunedCol& c) {
@@ -596,10 +602,34 @@ __device__ __forceinline__ T block_reduce(T v, Op op, T* red) {
 //       buckets -> the range of starts whose chunk may hold the minimum;
 //    d. per-start lower bounds inside that range -> the candidate range [smin, smax];
 //    e. the gathered bucket ranges of the candidate window ends (k_pr_gather).
+// bounds on the window sum S1(s) (the raw location is S1(s*) / h): the r1 largest elements of the start
+// bucket are at least its mean, the r2 smallest of the end bucket at most its mean, the buckets between
+// contribute their sum intervals
+__device__ __forceinline__ void window_sum_bounds(long long s, long long h, const PrunedCol& c, const long long* C,
+                                                  const double* A1, const double* sb, double E1, double& lo,
+                                                  double& hi) {
+  const int b = rank_bucket(C, s), be = rank_bucket(C, s + h - 1);
+  const double hd = (double)h;
+  if (b == be) {
+    lo = hd * bucket_lo(b, c);
+    hi = hd * bucket_hi(b, c);
+    return;
+  }
+  const double r1 = (double)(C[b + 1] - s), r2 = (double)(s + h - C[be]);
+  const double n1 = (double)(C[b + 1] - C[b]), n2 = (double)(C[be + 1] - C[be]);
+  const double t1lo = fmax(r1 * bucket_lo(b, c), r1 * (sb[b] / n1)), t1hi = r1 * bucket_hi(b, c);
+  const double t2lo = r2 * bucket_lo(be, c), t2hi = fmin(r2 * bucket_hi(be, c), r2 * (sb[NBK + be] / n2));
+  lo = t1lo + (A1[be] - A1[b + 1]) + t2lo - E1;
+  hi = t1hi + (A1[NBK + 1 + be] - A1[NBK + 1 + b + 1]) + t2hi + E1;
+  const double pad = 1e-12 * (fabs(lo) + fabs(hi)) + 1e-300;  // rounding of these fp64 evaluations
+  lo -= pad;
+  hi += pad;
+}
+
 __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, PrunedCol* __restrict__ pc,
                                                   const int* __restrict__ cnt, const unsigned long long* __restrict__ tq,
                                                   const double* __restrict__ esum,
-                                                  const unsigned long long* __restrict__ mm) {
+                                                  const unsigned long long* __restrict__ mm, UniConst uc) {
   extern __shared__ __align__(16) unsigned char loc_raw[];
   LocSmem& S = *reinterpret_cast<LocSmem*>(loc_raw);
   __shared__ BucketScan bs;
@@ -727,9 +757,11 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
   const long long lo_s = block_reduce(cmin, [](long long x, long long y) { return min(x, y); }, redl);
   const long long hi_s = block_reduce(cmax, [](long long x, long long y) { return max(x, y); }, redl);
 
-  // d. per-start lower bounds inside [lo_s, hi_s]: the thread's contiguous range, run by run
+  // d. per-start lower bounds inside [lo_s, hi_s]: the thread's contiguous range, run by run (and the
+  //    smallest lower bound of a candidate: h SQ(s*) lies in [vmin, bub])
   cmin = 0x7fffffffffffffffLL;
   cmax = -1;
+  double vmin = INFINITY;
   if (lo_s <= hi_s) {
     const long long cnt_s = hi_s - lo_s + 1;
     const long long per = (cnt_s + LT - 1) / LT;
@@ -742,17 +774,21 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
         while (C[be + 1] <= sa + h - 1) be++;
         const long long sb = min(min(s1e, C[b + 1]), C[be + 1] - h + 1) - 1;  // same (b, be) on [sa, sb]
         const RunConst rc = run_const(b, be, c, C, S.A1, S.Q2lo, S.Q2hi, S.sb);
-        for (long long s = sa; s <= sb; s++)
-          if (start_bounds(rc, s, h, m).lo <= bub) {
+        for (long long s = sa; s <= sb; s++) {
+          const double lb = start_bounds(rc, s, h, m).lo;
+          if (lb <= bub) {
             cmin = min(cmin, s);
             cmax = max(cmax, s);
+            vmin = fmin(vmin, lb);
           }
+        }
         sa = sb + 1;
       }
     }
   }
   const long long smin = block_reduce(cmin, [](long long x, long long y) { return min(x, y); }, redl);
   const long long smax = block_reduce(cmax, [](long long x, long long y) { return max(x, y); }, redl);
+  const double vlb = block_reduce(vmin, [](double x, double y) { return fmin(x, y); }, redd);
 
   // e. gathered bucket ranges
   if (t == 0) {
@@ -775,6 +811,27 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
       c.tS1 = bucket_threshold(c.bs_hi + 1, c);
       c.tE0 = bucket_threshold(c.be_lo, c);
       c.tE1 = bucket_threshold(c.be_hi + 1, c);
+      // the reweighting step (reading R4) keeps x iff (x - loc0)^2 <= q1 var0; the
+      // raw fit is not known yet, but loc0 = S1(s*) / h with s* in [smin, smax] (the window mean is
+      // monotone in s) and h SQ(s*) in [vlb, bub] bound it: values well inside the kept interval for
+      // every such (loc0, var0) are summed in the gather pass, values in the two narrow bands around its
+      // ends are gathered and decided exactly once the raw fit is known
+      double l0lo, l0hi, l1lo, l1hi;
+      window_sum_bounds(smin, h, c, C, S.A1, S.sb, m.E1, l0lo, l0hi);
+      window_sum_bounds(smax, h, c, C, S.A1, S.sb, m.E1, l1lo, l1hi);
+      const double hd = (double)h;
+      const double mlo = l0lo / hd, mhi = l1hi / hd;
+      const double vden = hd * (hd - 1.0);
+      const double v0lo = uc.c_raw * vlb / vden * (1.0 - 1e-9), v0hi = uc.c_raw * bub / vden * (1.0 + 1e-9);
+      const double Rlo = sqrt(uc.q1 * v0lo) * (1.0 - 1e-9), Rhi = sqrt(uc.q1 * v0hi) * (1.0 + 1e-9);
+      const double eps = 1e-9 * (Rhi + fabs(mlo) + fabs(mhi));
+      c.kc = 0.5 * (mlo + mhi);
+      c.kin_lo = mhi - Rlo + eps;
+      c.kin_hi = mlo + Rlo - eps;
+      c.kout_lo = mlo - Rhi - eps;
+      c.kout_hi = mhi + Rhi + eps;
+      c.kfused = (vlb > 0.0 && isfinite(mlo) && isfinite(mhi) && isfinite(Rhi) && mlo <= mhi &&
+                  c.kin_lo < c.kin_hi && (mhi - mlo) < 0.01 * Rlo && (Rhi - Rlo) < 0.01 * Rlo) ? 1 : 0;
     }
     pc[col] = c;
   }
@@ -787,9 +844,17 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
 static constexpr int GST = 3;  // k_pr_gather: cp.async stages of ILP elements per thread in flight
 static constexpr int GBUF = 1024;  // k_pr_gather: per-CTA shared buffer of gathered elements per side
 
+static constexpr int BCAP = 65536;  // band elements of the fused reweighting per column
+
+// FUSED: also the reweighting step's sums over the values certainly kept (kin_lo <= x <= kin_hi: sum x and
+// sum (x - kc)^2, kc rounded away as in k_pr_keep) and the values of the two bands around the kept
+// interval's ends, for k_pr_final_fused
+template <bool FUSED>
 __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ cols, long long len,
                                                   const PrunedCol* __restrict__ pc, double* __restrict__ g,
-                                                  int* __restrict__ gcount, dd2* __restrict__ below) {
+                                                  int* __restrict__ gcount, dd2* __restrict__ below,
+                                                  double* __restrict__ band, int* __restrict__ bcount,
+                                                  dd2* __restrict__ kpart, long long* __restrict__ kcnt) {
   __shared__ dd2 sm[33];
   __shared__ double sbuf[2][GBUF];  // this CTA's gathered elements, flushed with one global atomic per side
   __shared__ int scnt[2], sbase[2];
@@ -804,6 +869,14 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
   ddacc acc[NACC];
 #pragma unroll
   for (int q = 0; q < NACC; q++) acc[q] = ddacc_zero();
+  constexpr int NKA = FUSED ? 2 : 1;
+  ddacc kacc[NKA];
+#pragma unroll
+  for (int q = 0; q < NKA; q++) kacc[q] = ddacc_zero();
+  long long kn = 0;
+  __shared__ double bbuf[FUSED ? 512 : 1];
+  __shared__ int bcnt_s, bbase_s;
+  if (FUSED && threadIdx.x == 0) bcnt_s = 0;
   const long long per = (len + PCTA - 1) / PCTA;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
   const unsigned lane = threadIdx.x & 31, lt_mask = (1u << lane) - 1u;
@@ -836,6 +909,27 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
       const double x = src[k * PT];
       const bool geS = x >= c.tS0, geE = x >= c.tE0;
       ddacc_add(acc[k % NACC], (geS && !geE) ? x : 0.0);  // [bs_lo, be_lo); branch-free: adding 0 is exact
+      if (FUSED) {
+        const bool kin = x >= c.kin_lo && x <= c.kin_hi;
+        const double xv = kin ? x : 0.0;
+        ddacc_add_dev(kacc[k % NKA], xv, kin ? __dsub_rn(x, c.kc) : 0.0);
+        kn += kin ? 1 : 0;
+        const bool inb = !kin && x >= c.kout_lo && x <= c.kout_hi;
+        if (__any_sync(0xffffffffu, inb)) {  // rare: the bands hold ~1e-4 of the values
+          const unsigned mb = __ballot_sync(0xffffffffu, inb);
+          int pos = 0;
+          if (lane == (unsigned)(__ffs(mb) - 1)) pos = atomicAdd(&bcnt_s, __popc(mb));
+          pos = __shfl_sync(0xffffffffu, pos, __ffs(mb) - 1) + __popc(mb & lt_mask);
+          if (inb) {
+            if (pos < 512) {
+              bbuf[pos] = x;
+            } else {
+              const int gp = atomicAdd(&bcount[col], 1);
+              if (gp < BCAP) band[(long long)col * BCAP + gp] = x;
+            }
+          }
+        }
+      }
       const bool inS = geS && x < c.tS1, inE = geE && x < c.tE1;
       if (!__any_sync(0xffffffffu, inS || inE)) continue;  // the common case: one vote, no candidate
       const unsigned ms = __ballot_sync(0xffffffffu, inS), me = __ballot_sync(0xffffffffu, inE);
@@ -880,6 +974,30 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
   if (threadIdx.x == 0) {
     below[((long long)col * PCTA + blockIdx.x) * 2] = dd2_zero();
     below[((long long)col * PCTA + blockIdx.x) * 2 + 1] = te;
+  }
+  if (FUSED) {
+    __syncthreads();  // sm reused
+    dd2 kt = ddacc_dd2(kacc[0]);
+#pragma unroll
+    for (int q = 1; q < NKA; q++) kt = dd2_add(kt, ddacc_dd2(kacc[q]));
+    const dd2 ktot = block_sum_dd2(kt, sm);
+    __shared__ long long kred[PT / 32];
+    for (int d = 16; d > 0; d >>= 1) kn += __shfl_down_sync(0xffffffffu, kn, d);
+    if (lane == 0) kred[threadIdx.x >> 5] = kn;
+    if (threadIdx.x == 0) {
+      const int nbl = min(bcnt_s, 512);
+      bbase_s = nbl ? atomicAdd(&bcount[col], nbl) : 0;
+    }
+    __syncthreads();
+    const int nbl = min(bcnt_s, 512);
+    for (int i = threadIdx.x; i < nbl; i += PT)
+      if (bbase_s + i < BCAP) band[(long long)col * BCAP + bbase_s + i] = bbuf[i];
+    if (threadIdx.x == 0) {
+      long long kt2 = 0;
+      for (int q = 0; q < PT / 32; q++) kt2 += kred[q];
+      kpart[(long long)col * PCTA + blockIdx.x] = ktot;
+      kcnt[(long long)col * PCTA + blockIdx.x] = kt2;
+    }
   }
 }
 
@@ -1135,6 +1253,58 @@ __global__ void k_pr_final(UniConst uc, const dd2* __restrict__ part, const long
   out[col] = o;
 }
 
+// 6'. the fused reweighting: the certainly-kept sums of the gather pass (fixed order over its CTAs) plus
+//     the band values that pass the exact test (x - loc0)^2 <= q1 var0 under the raw fit (reading R4),
+//     all about the shift kc
+__global__ void __launch_bounds__(PT) k_pr_final_fused(UniConst uc, const PrunedCol* __restrict__ pc,
+                                                       const dd2* __restrict__ part, const long long* __restrict__ kcnt,
+                                                       const double* __restrict__ band, const int* __restrict__ bcount,
+                                                       UniOut* __restrict__ out) {
+  __shared__ dd2 sm[33];
+  __shared__ long long kred[PT / 32];
+  const int col = blockIdx.x;
+  const PrunedCol c = pc[col];
+  UniOut o = out[col];
+  const double loc0 = o.raw_loc, thresh = uc.q1 * o.var0;
+  const int nb = min(bcount[col], BCAP);
+  ddacc acc = ddacc_zero();
+  long long kb = 0;
+  for (int i = threadIdx.x; i < nb; i += PT) {
+    const double x = band[(long long)col * BCAP + i];
+    const double d = __dsub_rn(x, loc0);
+    if (__dmul_rn(d, d) <= thresh) {
+      ddacc_add_dev(acc, x, __dsub_rn(x, c.kc));
+      kb++;
+    }
+  }
+  const dd2 btot = block_sum_dd2(ddacc_dd2(acc), sm);
+  for (int d = 16; d > 0; d >>= 1) kb += __shfl_down_sync(0xffffffffu, kb, d);
+  if ((threadIdx.x & 31) == 0) kred[threadIdx.x >> 5] = kb;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  dd2 K = dd2_zero();
+  long long k = 0;
+  for (int q = 0; q < PCTA; q++) {
+    K = dd2_add(K, part[(long long)col * PCTA + q]);
+    k += kcnt[(long long)col * PCTA + q];
+  }
+  K = dd2_add(K, btot);
+  for (int q = 0; q < PT / 32; q++) k += kred[q];
+  o.kept = k;
+  if (o.status || k < 2) {
+    o.status = 1;
+  } else {
+    const double Sd = dd_to_d(K.s1);
+    const double loc = Sd / (double)k;
+    const dd qq = kept_sq_about_loc(K, c.kc, loc, (double)k);
+    const double var = uc.c_rew * (dd_to_d(qq) / (double)(k - 1));
+    o.loc = loc;
+    o.scale = sqrt(var);
+    if (!(var > 0.0)) o.status = 1;
+  }
+  out[col] = o;
+}
+
 struct PrScratch {
   PrunedCol* pc;
   int* cnt;
@@ -1148,6 +1318,8 @@ struct PrScratch {
   WinBest* part;
   dd2* kpart;
   long long* kcnt;
+  double* band;
+  int* bcount;
   int nch;
 };
 
@@ -1167,6 +1339,8 @@ static void carve_pr(Arena& A, PrScratch& s, int ncols) {
   s.part = A.take<WinBest>((size_t)ncols * s.nch);
   s.kpart = A.take<dd2>((size_t)ncols * PCTA);
   s.kcnt = A.take<long long>((size_t)ncols * PCTA);
+  s.band = A.take<double>((size_t)ncols * BCAP);
+  s.bcount = A.take<int>((size_t)ncols);
 }
 
 // Returns true when every column was resolved by the pruned path (out_dev filled);
@@ -1181,6 +1355,7 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   RTD_CU(cudaMemsetAsync(s.tq, 0, (size_t)ncols * NBK * sizeof(unsigned long long), st));
   RTD_CU(cudaMemsetAsync(s.esum, 0, (size_t)ncols * 4 * sizeof(double), st));
   RTD_CU(cudaMemsetAsync(s.gcount, 0, 2 * (size_t)ncols * sizeof(int), st));
+  RTD_CU(cudaMemsetAsync(s.bcount, 0, (size_t)ncols * sizeof(int), st));
   k_pr_sample<<<ncols, 1024, 0, st>>>(cols, len, s.pc, s.mm);
   RTD_LAUNCHED();
   // ~64K elements per CTA: many CTAs per column so the 4-CTA/SM waves quantise finely (a CTA flushes its
@@ -1193,18 +1368,33 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
     return true;
   }();
   (void)loc_attr;
-  k_pr_locate<<<ncols, LT, LOC_SMEM, st>>>(len, h, s.pc, s.cnt, s.tq, s.esum, s.mm);
+  k_pr_locate<<<ncols, LT, LOC_SMEM, st>>>(len, h, s.pc, s.cnt, s.tq, s.esum, s.mm, uc);
   RTD_LAUNCHED();
+  // RTD_UNI_FUSEDKEEP=1: the reweighting sums fused into the gather pass (a column whose bounds are too
+  // loose, kfused = 0, sends the batch to k_pr_keep).  Measured on config 4: the fused pass is FP64-bound
+  // (two double-double accumulations per value) and takes 7.2 ms per fit against 6.5 ms for the gather
+  // and keep passes apart, so it is off by default.
+  static const bool no_fused = getenv("RTD_UNI_FUSEDKEEP") == nullptr;
   static const int gsmem = [] {
     const int b = GST * ILP * PT * (int)sizeof(double);
-    RTD_CU(cudaFuncSetAttribute(k_pr_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    RTD_CU(cudaFuncSetAttribute(k_pr_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    RTD_CU(cudaFuncSetAttribute(k_pr_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
     return b;
   }();
-  k_pr_gather<<<dim3(PCTA, ncols), PT, gsmem, st>>>(cols, len, s.pc, s.g, s.gcount, s.below);
+  if (no_fused)
+    k_pr_gather<false><<<dim3(PCTA, ncols), PT, gsmem, st>>>(cols, len, s.pc, s.g, s.gcount, s.below, s.band,
+                                                             s.bcount, s.kpart, s.kcnt);
+  else
+    k_pr_gather<true><<<dim3(PCTA, ncols), PT, gsmem, st>>>(cols, len, s.pc, s.g, s.gcount, s.below, s.band,
+                                                            s.bcount, s.kpart, s.kcnt);
   RTD_LAUNCHED();
   std::vector<PrunedCol> hc(ncols);
-  std::vector<int> gc(2 * ncols);
-  fetch(st, {{hc.data(), s.pc, ncols * sizeof(PrunedCol)}, {gc.data(), s.gcount, 2 * ncols * sizeof(int)}});
+  std::vector<int> gc(2 * ncols), bc(ncols);
+  fetch(st, {{hc.data(), s.pc, ncols * sizeof(PrunedCol)}, {gc.data(), s.gcount, 2 * ncols * sizeof(int)},
+             {bc.data(), s.bcount, ncols * sizeof(int)}});
+  bool fused = !no_fused;
+  for (int j = 0; j < ncols; j++)
+    if (!hc[j].kfused || bc[j] > BCAP) fused = false;
   static const bool dbg = getenv("RTD_DEBUG_PRUNED") != nullptr;
   if (dbg) {
     for (int j = 0; j < ncols; j++)
@@ -1247,6 +1437,11 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   RTD_LAUNCHED();
   k_pr_raw<<<ncols, 32, 0, st>>>(h, s.pc, s.pref, s.part, s.nch, uc, out_dev);
   RTD_LAUNCHED();
+  if (fused) {
+    k_pr_final_fused<<<ncols, PT, 0, st>>>(uc, s.pc, s.kpart, s.kcnt, s.band, s.bcount, out_dev);
+    RTD_LAUNCHED();
+    return true;
+  }
   k_pr_keep<<<dim3(PCTA, ncols), PT, 0, st>>>(cols, len, uc, out_dev, s.kpart, s.kcnt);
   RTD_LAUNCHED();
   k_pr_final<<<ncols, 32, 0, st>>>(uc, s.kpart, s.kcnt, out_dev);
