@@ -24,6 +24,8 @@ void launch_dist_inv(int p, const double* Zall, long long m, long long blk_strid
 void launch_scale_median(const double* sig_all, const int* chosen_inst, const double* qv, int q, long long m, int p,
                          double chi2half, double* out_all, cudaStream_t st);
 bool dist_tma_supported(int p, long long m);
+void launch_matmul_tma(int p, const double* Zall, long long m, int nblk, const int* slot_of, const int* blk_of_slot,
+                       const int* pairs, int npairs, const double* W_all, double* out_all, cudaStream_t st);
 bool moments_tma_supported(int mode, const MomArgs& a);
 void launch_moments_tma(int mode, const MomArgs& a, int ninst, cudaStream_t st);
 void launch_dist_tma(int p, const double* Zall, long long m, int nblk, const int* pairs, int npairs, const int* inst,
@@ -636,6 +638,22 @@ static void refine_matmul(cudaStream_t st, RefineBufs& r, const double* Zall, lo
                           const std::vector<int>& blk) {
   ProfScope ps("matmul", (double)nitems * m * p * 16.0);
   static const bool no_pair = getenv("RTD_MATMUL_NOPAIR") != nullptr;
+  static const bool no_tma = getenv("RTD_MATMUL_NOTMA") != nullptr;
+  if (use_mma() && !no_pair && !no_tma && dist_tma_supported(p, m) && blk_stride == (long long)p * m) {
+    // TMA-fed, the two starts of a block per CTA row (Z read once)
+    std::vector<int> pr;
+    int nblk = 0;
+    for (int i = 0; i < nitems;) {
+      const bool two = i + 1 < nitems && blk[items[i]] == blk[items[i + 1]];
+      nblk = std::max(nblk, blk[items[i]] + 1);
+      pr.push_back(i);
+      pr.push_back(two ? i + 1 : -1);
+      i += two ? 2 : 1;
+    }
+    h2d(st, r.pairs, pr.data(), pr.size() * sizeof(int));
+    launch_matmul_tma(p, Zall, m, nblk, r.slot_of, r.blk_of_slot, r.pairs, (int)pr.size() / 2, W_all, r.T, st);
+    return;
+  }
   if (use_mma() && p > 24 && !no_pair) {  // consecutive items of one block share a CTA (Z read once)
     std::vector<int> pr;
     for (int i = 0; i < nitems;) {

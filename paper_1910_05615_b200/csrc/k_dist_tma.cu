@@ -243,6 +243,167 @@ __global__ void __launch_bounds__((DistTmaCfg<P, V>::NCW + 1) * 32, DistTmaCfg<P
   }
 }
 
+// ------------------------------------------------------------------ refinement GEMMs, TMA-fed
+// out = Z W for the two starts of a block at once (the scores T = Z V and the
+// sphered data Z~ = Z Sigma^-1/2 of the refinement): tiles of G = 23 row groups of 8 (TR = 184 rows) in a
+// 3-stage ring loaded by TMA, every one of the 8 warps contracting its groups (w, w + 8, w + 16) -- lane 0
+// of warp 0 also issues the loads, so the CTA has 8 warps and 255 registers per thread (a separate
+// producer warp would make one SM sub-partition hold 3 warps: 168 registers, spills) -- each raw A
+// fragment of Z feeding the DMMAs of both W (full p x p operators, B fragments in shared memory), the
+// accumulators stored straight to the column-major outputs.  grid (ctas_per_item, nitems); item y =
+// work items pairs[2y], pairs[2y+1] (-1: a lone item).
+template <int P>
+struct MatTmaCfg {
+  static constexpr int NW = 8, G = 23, MB = 3, TR = 8 * G;
+  static constexpr int KB = (P + 3) / 4, NB = (P + 7) / 8;
+  static constexpr int TILE = TR * P, STG = (TILE + 15) / 16 * 16;
+  static constexpr int OPW = KB * NB * 32;
+  static constexpr int NS = std::max(3, std::min(8, (200 * 1024 - 2 * OPW * 8) / (STG * 8)));
+  static constexpr size_t SMEM = (size_t)NS * STG * 8 + 2 * (size_t)OPW * 8 + 2 * NS * 8 + 128;
+};
+
+template <int P>
+__global__ void __launch_bounds__(MatTmaCfg<P>::NW * 32, 1)
+    k_matmul_tma(const __grid_constant__ CUtensorMap zmap, long long m, const int* __restrict__ pairs,
+                 const int* __restrict__ slot_of, const int* __restrict__ blk_of_slot, const double* __restrict__ W_all,
+                 double* __restrict__ out_all, int tiles_per_cta) {
+  using C = MatTmaCfg<P>;
+  constexpr int MB = C::MB, NW = C::NW, G = C::G, TR = C::TR, KB = C::KB, NB = C::NB, NS = C::NS,
+                TILE = C::TILE, STG = C::STG, OPW = C::OPW;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* tiles = reinterpret_cast<double*>(smraw);
+  double* ops = tiles + (size_t)NS * STG;  // [2][OPW]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ops + 2 * OPW);
+  uint64_t* empty = full + NS;
+  const int i0 = pairs[2 * blockIdx.y], i1 = pairs[2 * blockIdx.y + 1];
+  const bool two = i1 >= 0;
+  const int s0 = slot_of[i0], s1 = two ? slot_of[i1] : s0;
+  const int blk = blk_of_slot[s0];
+  const long long ntiles = (m + TR - 1) / TR;
+  const long long t_begin = (long long)blockIdx.x * tiles_per_cta;
+  const long long t_end = min(ntiles, t_begin + tiles_per_cta);
+  const int nt = (int)max(0LL, t_end - t_begin);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int w = 0; w < 2; w++) {  // B[k][j] = W[k][j] lane-major per 8x4 block (a lone item: W twice)
+    const double* W = W_all + (long long)(w ? s1 : s0) * RTD_MAXP * RTD_MAXP;
+    for (int e = threadIdx.x; e < OPW; e += blockDim.x) {
+      const int ln = e & 31, b = e >> 5, kb = b / NB, nb = b - kb * NB;
+      const int k = 4 * kb + (ln & 3), j = 8 * nb + (ln >> 2);
+      ops[w * OPW + e] = (k < P && j < P) ? W[k * P + j] : 0.0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < NS; q++) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int j) {  // tile j into stage j % NS once every warp released its previous use
+    if (j >= nt) return;
+    const int q = j % NS;
+    mbar_wait(&empty[q], (uint32_t)(((j / NS) & 1) ^ 1));
+    mbar_expect_tx(&full[q], (uint32_t)(TILE * 8));
+    tma_load_3d(tiles + (size_t)q * STG, &zmap, &full[q], (int)((t_begin + j) * TR), 0, blk);
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&zmap)) : "memory");
+    for (int j = 0; j < NS - 1; j++) issue(j);
+  }
+  const int g = lane >> 2, t = lane & 3;
+  double* __restrict__ out0 = out_all + (long long)i0 * P * m;
+  double* __restrict__ out1 = out_all + (long long)(two ? i1 : i0) * P * m;
+  for (int it = 0; it < nt; it++) {
+    const int q = it % NS;
+    if (threadIdx.x == 0 && it >= 1) issue(it + NS - 2);  // the stage of tile it - 2
+    mbar_wait(&full[q], (uint32_t)((it / NS) & 1));
+    const double* T = tiles + (size_t)q * STG;
+    const long long tr0 = (t_begin + it) * TR;
+    double acc[2][MB][NB][2];
+#pragma unroll
+    for (int w = 0; w < 2; w++)
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++)
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) acc[w][mb][nb][0] = acc[w][mb][nb][1] = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < KB; kb++) {
+      const int k = 4 * kb + t;
+      double a[MB];
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++) {
+        const int grp = warp + NW * mb;
+        a[mb] = (k < P && grp < G) ? T[k * TR + grp * 8 + g] : 0.0;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; nb++) {
+        const double bv0 = ops[(kb * NB + nb) * 32 + lane], bv1 = ops[OPW + (kb * NB + nb) * 32 + lane];
+#pragma unroll
+        for (int mb = 0; mb < MB; mb++)
+          if (MB * NW == G || warp + NW * mb < G) {
+            dmma_t(acc[0][mb][nb][0], acc[0][mb][nb][1], a[mb], bv0);
+            dmma_t(acc[1][mb][nb][0], acc[1][mb][nb][1], a[mb], bv1);  // a lone item: a discarded copy
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[q]);  // the tile is no longer read
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+      double* __restrict__ out = w ? out1 : out0;
+#pragma unroll
+      for (int mb = 0; mb < MB; mb++) {
+        const int grp = warp + NW * mb;
+        const long long row = tr0 + grp * 8 + g;
+        if (grp >= G || row >= m || (w == 1 && !two)) continue;
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) {
+          const int j = 8 * nb + 2 * t;
+          if (j < P) out[(long long)j * m + row] = acc[w][mb][nb][0];
+          if (j + 1 < P) out[(long long)(j + 1) * m + row] = acc[w][mb][nb][1];
+        }
+      }
+    }
+  }
+}
+
+namespace {
+
+template <int P>
+void matmul_tma_launch(const double* Zall, long long m, int nblk, const int* slot_of, const int* blk_of_slot,
+                       const int* pairs, int npairs, const double* W_all, double* out_all, cudaStream_t st) {
+  using C = MatTmaCfg<P>;
+  CUtensorMap map;
+  if (!encode_blocks(&map, Zall, m, P, nblk, C::TR)) throw std::string("cuTensorMapEncodeTiled failed for the GEMM");
+  const long long ntiles = (m + C::TR - 1) / C::TR;
+  const long long per_item = std::max<long long>(1, 148LL / npairs);
+  const int tpc = (int)std::max<long long>(1, (ntiles + per_item - 1) / per_item);
+  const unsigned gx = (unsigned)((ntiles + tpc - 1) / tpc);
+  RTD_CU(cudaFuncSetAttribute(k_matmul_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  k_matmul_tma<P><<<dim3(gx, npairs), C::NW * 32, C::SMEM, st>>>(map, m, pairs, slot_of, blk_of_slot, W_all, out_all,
+                                                                  tpc);
+}
+
+}  // namespace
+
+void launch_matmul_tma(int p, const double* Zall, long long m, int nblk, const int* slot_of, const int* blk_of_slot,
+                       const int* pairs, int npairs, const double* W_all, double* out_all, cudaStream_t st) {
+  switch (p) {
+#define RTD_MT_CASE(P) \
+  case P: matmul_tma_launch<P>(Zall, m, nblk, slot_of, blk_of_slot, pairs, npairs, W_all, out_all, st); break;
+    RTD_MT_CASE(8) RTD_MT_CASE(9) RTD_MT_CASE(10) RTD_MT_CASE(11) RTD_MT_CASE(12) RTD_MT_CASE(13)
+    RTD_MT_CASE(14) RTD_MT_CASE(15) RTD_MT_CASE(16) RTD_MT_CASE(17) RTD_MT_CASE(18) RTD_MT_CASE(19)
+    RTD_MT_CASE(20) RTD_MT_CASE(21) RTD_MT_CASE(22) RTD_MT_CASE(23) RTD_MT_CASE(24) RTD_MT_CASE(25)
+    RTD_MT_CASE(26) RTD_MT_CASE(27) RTD_MT_CASE(28) RTD_MT_CASE(29) RTD_MT_CASE(30) RTD_MT_CASE(31)
+    RTD_MT_CASE(32) RTD_MT_CASE(33) RTD_MT_CASE(34) RTD_MT_CASE(35) RTD_MT_CASE(36) RTD_MT_CASE(37)
+    RTD_MT_CASE(38) RTD_MT_CASE(39) RTD_MT_CASE(40)
+#undef RTD_MT_CASE
+    default: throw std::string("matmul_tma: p out of range");
+  }
+  RTD_LAUNCHED();
+}
+
 namespace {
 
 template <int P, int V>
