@@ -187,24 +187,30 @@ __global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
       }
       // psi: identity / zero branches in place; the tanh branch (1.5 < |z| <= 4, ~13 %
       // of the entries) compacted into a warp-private list, evaluated by all 32 lanes, scattered back
+      // (the branch tests on the magnitude's bit pattern -- integer compares, IEEE order -- so the FP64
+      // pipe the DMMAs share only evaluates the compacted tanh entries)
+      constexpr unsigned long long B15 = 0x3FF8000000000000ull, C40 = 0x4010000000000000ull;  // 1.5, 4.0
       int pos[NB];
       int n = 0;
 #pragma unroll
       for (int b = 0; b < NB; b++) {
-        const double az = fabs(u[b]);
-        const bool need = az > 1.5 && az <= 4.0;
+        const unsigned long long ab = (unsigned long long)__double_as_longlong(u[b]) & 0x7FFFFFFFFFFFFFFFull;
+        const bool need = ab > B15 && ab <= C40;
         const unsigned bal = __ballot_sync(0xffffffffu, need);
         pos[b] = need ? n + __popc(bal & ((1u << lane) - 1u)) : -1;
-        if (need) scr[pos[b]] = __dmul_rn(0.862, __dsub_rn(4.0, az));
+        if (need) scr[pos[b]] = __longlong_as_double((long long)ab);  // |z|
         n += __popc(bal);
-        if (!need && az > 4.0) u[b] = 0.0;
+        if (ab > C40) u[b] = 0.0;
       }
       __syncwarp();
-      for (int i = lane; i < n; i += 32) scr[i] = __dmul_rn(1.541, tanh(scr[i]));
+      for (int i = lane; i < n; i += 32) scr[i] = __dmul_rn(1.541, tanh(__dmul_rn(0.862, __dsub_rn(4.0, scr[i]))));
       __syncwarp();
 #pragma unroll
       for (int b = 0; b < NB; b++)
-        if (pos[b] >= 0) u[b] = u[b] > 0 ? scr[pos[b]] : -scr[pos[b]];
+        if (pos[b] >= 0) {
+          const double v = scr[pos[b]];
+          u[b] = (__double_as_longlong(u[b]) < 0) ? -v : v;  // |z| > 1.5: the sign bit is the sign
+        }
       __syncwarp();
     } else if (MODE >= MOM_MEMBER) {
 #pragma unroll
