@@ -314,6 +314,7 @@ static constexpr int USMALL = 16384;  // shared-memory capacity bound
 static constexpr int USMALL_USE = 4096;  // measured: faster than the radix-sort path up to here (config 1:
                                          // 3 calls 1.06 -> 0.21 ms), slower at 20,000 rows (config 5)
 static constexpr int UST = 1024;
+static constexpr int USORTED = 24576;  // presorted columns up to here fit k_uni_small's shared memory
 
 __device__ __forceinline__ void u_cmpswap(double* v, int i, int j) {
   const double a = v[i], b = v[j];
@@ -331,6 +332,9 @@ __device__ __forceinline__ dd2 u_prefix(const double* v, const dd2* cpre, int pe
   return acc;
 }
 
+// PRESORTED: the columns arrive sorted (k_uni_cluster_sort) and only the scans, the window objective and
+// the reweighting run here -- up to USORTED rows (the column and the chunk prefixes in shared memory)
+template <bool PRESORTED>
 __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ cols, int len, int h, UniConst uc,
                                                    UniOut* __restrict__ out) {
   extern __shared__ double usm[];
@@ -342,9 +346,9 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
   const double* y = cols + (long long)col * len;
   for (int i = t; i < len; i += UST) v[i] = y[i];
   int N = 1;
-  while (N < len) N <<= 1;
+  while (N < len && !PRESORTED) N <<= 1;
   __syncthreads();
-  for (int lk = 1; (1 << lk) <= N; lk++) {
+  for (int lk = 1; (1 << lk) <= N && !PRESORTED; lk++) {
     const int k = 1 << lk;
     for (int q = t; q < N / 2; q += UST) {  // flip step: i in the lower half of its k-block
       const int i = ((q >> (lk - 1)) << lk) | (q & (k / 2 - 1)), j = i ^ (k - 1);
@@ -716,12 +720,12 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
     if (A.base == nullptr) return;  // no scratch
     const int smem = (int)((((len + 3) & ~3LL) * sizeof(double)) + (UST + 1) * sizeof(dd2));
     static const bool attr = [] {
-      cudaFuncSetAttribute(k_uni_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_uni_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(USMALL * sizeof(double) + (UST + 1) * sizeof(dd2)));
       return true;
     }();
     (void)attr;
-    k_uni_small<<<ncols, UST, smem, st>>>(cols, (int)len, (int)(len / 2 + 1), uc, out_dev);
+    k_uni_small<false><<<ncols, UST, smem, st>>>(cols, (int)len, (int)(len / 2 + 1), uc, out_dev);
     RTD_LAUNCHED();
     return;
   }
@@ -765,6 +769,13 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
       RTD_CU(cudaFuncSetAttribute(k_uni_cluster_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
       k_uni_cluster_sort<<<nc * UCS_CL, UCS_T, dyn, st>>>(cc, len, s.sorted);
       RTD_LAUNCHED();
+      if (len <= USORTED) {  // the scans, windows and reweighting of each sorted column in one CTA
+        const int smem = (int)((((len + 3) & ~3LL) * sizeof(double)) + (UST + 1) * sizeof(dd2));
+        RTD_CU(cudaFuncSetAttribute(k_uni_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_uni_small<true><<<nc, UST, smem, st>>>(s.sorted, (int)len, (int)h, uc, out_dev + c0);
+        RTD_LAUNCHED();
+        continue;
+      }
     } else if (nc == 1) {
       count_sort();
       RTD_CU(cub::DeviceRadixSort::SortKeys(s.cub_tmp, bytes, cc, s.sorted, (int)Nc, 0, 64, st));
