@@ -139,6 +139,10 @@ def shard_layout(n_global: int, q: int, world: int, rank: int) -> tuple:
     return r0.value, nl.value, b0.value, ql.value
 
 
+def _error(rc: int, ctx) -> "RTDError | None":
+    return RTDError(rc, lib().rtdetmcd_last_error(ctx["h"]).decode()) if rc else None
+
+
 def _check(rc: int, ctx) -> None:
     if rc != 0:
         raise RTDError(rc, lib().rtdetmcd_last_error(ctx["h"]).decode())
@@ -288,9 +292,11 @@ def fit(X, h: int | None = None, alpha: float = 0.5, q: int = 1, seed: int = 0, 
         wS = np.ascontiguousarray(warm_start[1], dtype=np.float64).reshape(p, p)
         rc = L.rtdetmcd_fit_warm(ctx["h"], C.c_void_p(ptr), n, p, C.byref(o), C.c_void_p(wm.ctypes.data),
                                  C.c_void_p(wS.ctypes.data), C.byref(r))
+    err = _error(rc, ctx)          # read before the workspace reset (every library call clears the message)
     if torch_workspace:
         L.rtdetmcd_set_workspace(ctx["h"], None, 0)
-    _check(rc, ctx)
+    if err:
+        raise err
     return _make_fit(r, host, rows)
 
 
@@ -351,9 +357,11 @@ def fit_batches(batches, h: int | None = None, alpha: float = 0.5, q: int = 1, s
         res[b] = per[b][0]
     ptrs = (C.c_void_p * nb)(*[a[0] for a in arrs])
     rc = L.rtdetmcd_fit_batches(ctx["h"], ptrs, nb, n, p, C.byref(o), res)
+    err = _error(rc, ctx)          # read before the workspace reset (every library call clears the message)
     if torch_workspace:
         L.rtdetmcd_set_workspace(ctx["h"], None, 0)
-    _check(rc, ctx)
+    if err:
+        raise err
     return [_make_fit(res[b], per[b][1], per[b][2]) for b in range(nb)]
 
 

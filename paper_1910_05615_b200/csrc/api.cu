@@ -395,7 +395,7 @@ void dist_groups(cudaStream_t st, const CStepBufs& b, const double* Z, long long
 // mu/sigma = mean / covariance of the final h-subset (in memA; update-based, reading R12), logdet.
 void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_stride, int nstart, int ninst, long long h,
                 double kappa_max, int max_steps, int refresh, std::vector<int>& status_h, std::vector<int>& steps_h,
-                int dist_mode = RTD_DIST_CHOLESKY) {
+                int dist_mode = RTD_DIST_CHOLESKY, std::vector<double>* logdet_h = nullptr) {
   const int p = b.p;
   const long long m = b.m;
   const bool full_inv = dist_mode == RTD_DIST_INVERSE || dist_mode == RTD_DIST_SMW;
@@ -425,7 +425,9 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
                           b.sigma, b.status, b.changed, b.logdet, b.traj, b.traj_stride, b.memA, st);
     }
     std::vector<int> steps_all(ninst);
-    fetch(st, {{status_h.data(), b.status, ninst * sizeof(int)}, {steps_all.data(), b.changed, ninst * sizeof(int)}});
+    if (logdet_h) logdet_h->resize(ninst);
+    fetch(st, {{status_h.data(), b.status, ninst * sizeof(int)}, {steps_all.data(), b.changed, ninst * sizeof(int)},
+               {logdet_h ? logdet_h->data() : nullptr, b.logdet, logdet_h ? ninst * sizeof(double) : 0}});
     for (int i : act) steps_h[i] = steps_all[i];
     return;
   }
@@ -918,17 +920,25 @@ struct BlockResult {
   int warnings = 0;
 };
 
-// H0: X (device) -> validated, optionally ln, column-major Xc; throws RTD_E_NONFINITE
+// H0: X (device) -> validated, optionally ln, column-major Xc; *bad = first bad row (or ~0) on the device
+void phase_columns_async(cudaStream_t st, const double* Xdev, long long n, int p, int log, double* Xc,
+                         unsigned long long* bad) {
+  RTD_CU(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  ProfScope ps("transpose", (double)n * p * 16.0);
+  launch_transpose(Xdev, n, p, log, Xc, bad, st);
+}
+
+void throw_if_bad_row(unsigned long long b, int log) {
+  if (b != ~0ull) throw Fail{RTD_E_NONFINITE, "row " + std::to_string(b) + (log ? " is not finite and > 0" : " is not finite")};
+}
+
+// H0 with its check; throws RTD_E_NONFINITE
 void phase_columns(cudaStream_t st, const double* Xdev, long long n, int p, int log, double* Xc,
                    unsigned long long* bad) {
-  RTD_CU(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
-  {
-    ProfScope ps("transpose", (double)n * p * 16.0);
-    launch_transpose(Xdev, n, p, log, Xc, bad, st);
-  }
+  phase_columns_async(st, Xdev, n, p, log, Xc, bad);
   unsigned long long b = 0;
   d2h(st, &b, bad, sizeof(b));
-  if (b != ~0ull) throw Fail{RTD_E_NONFINITE, "row " + std::to_string(b) + (log ? " is not finite and > 0" : " is not finite")};
+  throw_if_bad_row(b, log);
 }
 
 // H2-H9 for the q blocks already in f.Z: starts, refinement, C-steps, start choice, c(alpha) scaling.
@@ -964,10 +974,13 @@ BlockResult phase_csteps_choose(cudaStream_t st, FitBufs& f, const Dims& d, cons
   const int p = d.p, q = d.q;
   const long long m = d.m, blk_stride = (long long)p * m;
   const int ninst = 2 * q;
+  r.logdet.clear();
   run_csteps(st, f.cb, f.Z, blk_stride, 2, ninst, d.hb, o.kappa_max, o.max_csteps, o.refresh_every, r.status,
-             r.steps, o.distance);
-  r.logdet.resize(ninst);
-  d2h(st, r.logdet.data(), f.cb.logdet, ninst * sizeof(double));
+             r.steps, o.distance, &r.logdet);
+  if ((int)r.logdet.size() != ninst) {  // the multi-launch loop: one more read
+    r.logdet.resize(ninst);
+    d2h(st, r.logdet.data(), f.cb.logdet, ninst * sizeof(double));
+  }
   const double calpha = consistency_factor((double)d.hb / (double)m, p);
   r.chosen.assign(q, -1);
   r.chosen_inst.assign(q, -1);
@@ -1149,7 +1162,10 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     h2d(st, f.Xd, X, (size_t)n * p * sizeof(double));
     Xdev = f.Xd;
   }
-  phase_columns(st, Xdev, n, p, d.log, f.Xc, f.bad);
+  // The input check (a bad row) and the standardisation's (a degenerate column) are read back with the
+  // final results instead of one synchronisation each; a failure in between is reported as the bad input
+  // it came from (deferred_checks first).
+  phase_columns_async(st, Xdev, n, p, d.log, f.Xc, f.bad);
 
   // H1: global column standardisation
   {
@@ -1157,9 +1173,12 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     run_unimcd(st, f.uscratch, f.uscratch_bytes, f.Xc, n, p, f.uni);
   }
   std::vector<UniOut> uni(p);
-  d2h(st, uni.data(), f.uni, p * sizeof(UniOut));
-  for (int j = 0; j < p; j++)
-    if (uni[j].status) throw Fail{RTD_E_DEGENERATE_COLUMN, "column " + std::to_string(j)};
+  auto deferred_checks = [&](unsigned long long b) {
+    throw_if_bad_row(b, d.log);
+    for (int j = 0; j < p; j++)
+      if (uni[j].status) throw Fail{RTD_E_DEGENERATE_COLUMN, "column " + std::to_string(j)};
+  };
+  try {
 
   // partition + Z = (X - loc)/scale per block, column-major
   {
@@ -1219,12 +1238,16 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     launch_weights_from_d2(f.cb.d2, (long long)q * m, c2, f.rowmap, f.weights_d, st);
     launch_hsub_from_mem(f.cb.memA, f.chosen_dev, q, m, f.rowmap, f.hsub_d, st);
   }
-  // one synchronisation: deferred status words (raw / reweighted scatter PD), weighted count, estimates
+  // one synchronisation: deferred status words (input, columns, raw / reweighted scatter PD), weighted
+  // count, estimates
   std::vector<double> mx(4 * RTD_MAXP), sx(4 * M2);
   int pd[2] = {0, 0};
   double kw = 0.0;
+  unsigned long long badrow = 0;
   fetch(st, {{pd, f.st1, 2 * sizeof(int)}, {&kw, f.pooled + (mom_np(p) - 1), sizeof(double)},
-             {mx.data(), f.muX, 2 * RTD_MAXP * sizeof(double)}, {sx.data(), f.sigX, 2 * M2 * sizeof(double)}});
+             {mx.data(), f.muX, 2 * RTD_MAXP * sizeof(double)}, {sx.data(), f.sigX, 2 * M2 * sizeof(double)},
+             {&badrow, f.bad, sizeof(badrow)}, {uni.data(), f.uni, p * sizeof(UniOut)}});
+  deferred_checks(badrow);
   if (pd[0] == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "raw scatter is not positive definite"};
   if (!(kw > p)) throw Fail{RTD_E_NOT_PD, "too few reweighted inliers"};
   if (pd[1] == ST_NOT_PD) throw Fail{RTD_E_NOT_PD, "reweighted scatter is not positive definite"};
@@ -1265,6 +1288,12 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
     output_copy(st, out->weights, f.weights_d, n);
     output_copy(st, out->hsubset, f.hsub_d, n);
     RTD_CU(cudaStreamSynchronize(st));
+  }
+  } catch (const Fail&) {  // a failure after bad input: report the input
+    unsigned long long b = 0;
+    fetch(st, {{&b, f.bad, sizeof(b)}, {uni.data(), f.uni, p * sizeof(UniOut)}});
+    deferred_checks(b);
+    throw;
   }
 }
 

@@ -361,6 +361,25 @@ def test_fit_errors():
     assert e.value.name == "RTD_E_INVALID_ARG"
 
 
+@pytest.mark.parametrize("n", [20_000, 100_000])
+def test_fit_errors_deferred_checks(n):
+    # the input check and the standardisation check are read back with the results (one synchronisation):
+    # whatever the kernels do with the bad values in between, the error is the input's
+    X = datagen.gaussian(n, 8, seed=24)
+    Y = X.copy()
+    Y[n // 3, 5] = np.inf
+    with pytest.raises(api.RTDError) as e:
+        api.fit(_cuda(Y), alpha=0.75, q=2)
+    assert e.value.name == "RTD_E_NONFINITE" and f"row {n // 3}" in str(e.value)
+    Y = X.copy()
+    Y[:, 4] = 2.5
+    with pytest.raises(api.RTDError) as e:
+        api.fit(_cuda(Y), alpha=0.75)
+    assert e.value.name == "RTD_E_DEGENERATE_COLUMN" and "column 4" in str(e.value)
+    g = api.fit(_cuda(X), alpha=0.75)          # the context is still usable
+    assert g.n_weighted > 0
+
+
 def test_fit_minimal_size():
     X = datagen.gaussian(7, 3, seed=23)       # n = 2p + 1
     o = ofit.fit(X, h=5)
