@@ -35,7 +35,7 @@ namespace rtd {
 static constexpr int NBK = 4096;         // buckets per column (incl. underflow 0 and overflow NBK-1)
 static constexpr int SAMPLE = 2048;      // strided sample for the bucket map
 static constexpr int CAP = 65536;        // max gathered elements per side per column
-static constexpr int PCTA = 32;          // CTAs per column in the streaming passes (fixed -> deterministic)
+static constexpr int PCTA = 32;          // max CTAs per column in the streaming passes (stride of the partials)
 static constexpr long long PACK_LEN = 1LL << 24;  // below: hist flushes count + offset sum in one 64-bit atomic
 static constexpr int PT = 256;
 static constexpr int LT = 512;    // k_pr_locate threads (one CTA per column)
@@ -43,7 +43,9 @@ static constexpr int LT = 512;    // k_pr_locate threads (one CTA per column)
 struct PrunedCol {
   double lo, hi, w, inv_w;   // bucket map
   double inv_w16;            // 2^16 inv_w (exact): fl(fl(y - lo) inv_w16) = 2^16 fl(fl(y - lo) inv_w)
-  double cmin, cmax;         // column min / max
+  double cs;                 // shift of every bound: the bounds work on y - cs (cs = centre of the map)
+  double los, his;           // lo - cs, hi - cs (rounded down / up)
+  double cmin, cmax;         // column min / max, minus cs (rounded down / up)
   long long smin, smax;      // candidate window starts
   long long rmin, rmax;      // range of starts left by the chunk lower bounds (diagnostics)
   double tS0, tS1, tE0, tE1; // value thresholds of the gathered bucket ranges (bucket_threshold)
@@ -64,12 +66,14 @@ __device__ __forceinline__ int bucket_of(double y, const PrunedCol& c) {
   return b > NBK - 2 ? NBK - 2 : b;
 }
 
-// value range of bucket b (fuzzed by 1e-6 bucket widths against rounding in bucket_of)
+// value range of bucket b, minus cs (fuzzed by 1e-6 bucket widths against rounding in bucket_of).  The
+// bounds of k_pr_locate all work on y - cs: h SQ(s) is shift-invariant, and bounds on (sum y)^2 taken in
+// raw units lose 2 |sum y| x (their width), i.e. nothing prunes once |mean| >> scale
 __device__ __forceinline__ double bucket_lo(int b, const PrunedCol& c) {
-  return b == 0 ? c.cmin : (b == NBK - 1 ? c.hi : c.lo + ((double)(b - 1) - 1e-6) * c.w);
+  return b == 0 ? c.cmin : (b == NBK - 1 ? c.his : c.los + ((double)(b - 1) - 1e-6) * c.w);
 }
 __device__ __forceinline__ double bucket_hi(int b, const PrunedCol& c) {
-  return b == 0 ? c.lo : (b == NBK - 1 ? c.cmax : c.lo + ((double)b + 1e-6) * c.w);
+  return b == 0 ? c.los : (b == NBK - 1 ? c.cmax : c.los + ((double)b + 1e-6) * c.w);
 }
 
 __device__ __forceinline__ unsigned long long ord_key(double x) {
@@ -177,6 +181,9 @@ __global__ void __launch_bounds__(1024) k_pr_sample(const double* __restrict__ c
     c.w = (c.hi - c.lo) / (double)(NBK - 2);
     c.inv_w = 1.0 / c.w;
     c.inv_w16 = c.inv_w * 65536.0;
+    c.cs = 0.5 * (c.lo + c.hi);
+    c.los = __dsub_rd(c.lo, c.cs);
+    c.his = __dsub_ru(c.hi, c.cs);
     c.status = (span > 0.0 && isfinite(span) && c.w > 0.0) ? 0 : 1;
     pc[col] = c;
     mm[2 * col] = ~0ull;
@@ -190,10 +197,11 @@ __global__ void __launch_bounds__(1024) k_pr_sample(const double* __restrict__ c
 //    [L_b + w (q - 1) 2^-16, L_b + w (q + 2) 2^-16] (the margin covers the rounding of the offset), so
 //    the bucket sum is known to an interval (k_pr_scan).  The under- and overflow buckets' sums are
 //    accumulated in registers (fp64) and added once per warp.
-__global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols, long long len,
+__global__ void __launch_bounds__(PT, 5) k_pr_hist(const double* __restrict__ cols, long long len,
                                                 const PrunedCol* __restrict__ pc, int* __restrict__ cnt,
                                                 unsigned long long* __restrict__ tq, double* __restrict__ esum,
                                                 unsigned long long* __restrict__ mm) {
+  // (a packed 64-bit count + offset atomic would be a CAS loop in shared memory: two native 32-bit ones)
   __shared__ unsigned int hc[NBK];
   __shared__ unsigned int hq[NBK];
   const int col = blockIdx.y;
@@ -222,20 +230,23 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
         // max only bound the end buckets' values (bucket_lo(0), bucket_hi(NBK - 1)): tracked there only
         const double x = v[k];
         int b;
+        unsigned int q = 0u;
         if (x < c.lo) {
           b = 0;
-          e0 += x;
-          a0 += fabs(x);
+          const double xs = __dsub_rn(x, c.cs);  // shifted (k_pr_locate): one more rounding per term
+          e0 += xs;
+          a0 += fabs(xs);
           kmin = min(kmin, ord_key(x));
         } else if (x >= c.hi) {
           b = NBK - 1;
-          e1 += x;
-          a1 += fabs(x);
+          const double xs = __dsub_rn(x, c.cs);
+          e1 += xs;
+          a1 += fabs(xs);
           kmax = max(kmax, ord_key(x));
         } else {
           const int T = (int)__dmul_rn(__dsub_rn(x, c.lo), c.inv_w16);
           b = 1 + (T >> 16);
-          unsigned int q = (unsigned int)(T & 0xffff);
+          q = (unsigned int)(T & 0xffff);
           if (b > NBK - 2) {
             b = NBK - 2;
             q = 65535u;
@@ -270,7 +281,7 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
   int* cn = cnt + (long long)col * NBK;
   unsigned long long* tqc = tq + (long long)col * NBK;
   const bool packed = len < PACK_LEN;  // count (bits 40..63) + offset sum (< len 2^16 <= 2^40) in one word
-  for (int b = threadIdx.x; b < NBK; b += PT)
+  for (int b = threadIdx.x; b < NBK; b += PT) {
     if (hc[b]) {
       if (packed) {
         atomicAdd(&tqc[b], ((unsigned long long)hc[b] << 40) | (unsigned long long)hq[b]);
@@ -279,6 +290,7 @@ __global__ void __launch_bounds__(PT) k_pr_hist(const double* __restrict__ cols,
         if (hq[b]) atomicAdd(&tqc[b], (unsigned long long)hq[b]);
       }
     }
+  }
 }
 
 // 3a. prefix arrays over buckets (one CTA per column): rank offsets C, the interval [Slo, Shi] of
@@ -294,14 +306,15 @@ __device__ __forceinline__ void bucket_sum_interval(int b, int r, unsigned long 
   if (r == 0) {
     Slo = Shi = 0.0;
   } else if (b == 0 || b == NBK - 1) {
-    // an fp64 sum of r terms in any order is within (r + 2) u sum|y| of the exact sum (u = 2^-53;
-    // the sum of magnitudes itself carries a relative error below (r + 2) u, hence the factor 2)
+    // an fp64 sum of r terms y - cs (each rounded: u |y - cs|) in any order is within (r + 3) u sum|y - cs|
+    // of the exact sum (u = 2^-53; the sum of magnitudes itself carries a relative error below (r + 2) u,
+    // hence the factor 2 on (r + 2))
     const double S = es[b == 0 ? 0 : 1], Sa = es[b == 0 ? 2 : 3];
     const double err = 2.0 * ((double)r + 2.0) * 0x1p-53 * Sa + 1e-300;
     Slo = S - err;
     Shi = S + err;
   } else {
-    const double rd = (double)r, Lb = c.lo + (double)(b - 1) * c.w, u = c.w * (1.0 / 65536.0);
+    const double rd = (double)r, Lb = c.los + (double)(b - 1) * c.w, u = c.w * (1.0 / 65536.0);
     Slo = fmax(rd * bucket_lo(b, c), rd * Lb + u * ((double)T - rd));
     Shi = fmin(rd * bucket_hi(b, c), rd * Lb + u * ((double)T + 2.0 * rd));
   }
@@ -638,8 +651,8 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
   const int col = blockIdx.x;
   PrunedCol c = pc[col];
   if (c.status) return;
-  c.cmin = ord_val(mm[2 * col]);
-  c.cmax = ord_val(mm[2 * col + 1]);
+  c.cmin = __dsub_rd(ord_val(mm[2 * col]), c.cs);
+  c.cmax = __dsub_ru(ord_val(mm[2 * col + 1]), c.cs);
   scan_column(c, len < PACK_LEN, cnt + (long long)col * NBK, tq + (long long)col * NBK, esum + 4 * col, S.C, S.sb, S.A1, S.Q2lo,
               S.Q2hi, bs);
   const long long* C = S.C;
@@ -820,7 +833,7 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
       window_sum_bounds(smin, h, c, C, S.A1, S.sb, m.E1, l0lo, l0hi);
       window_sum_bounds(smax, h, c, C, S.A1, S.sb, m.E1, l1lo, l1hi);
       const double hd = (double)h;
-      const double mlo = l0lo / hd, mhi = l1hi / hd;
+      const double mlo = l0lo / hd + c.cs, mhi = l1hi / hd + c.cs;  // back to raw units
       const double vden = hd * (hd - 1.0);
       const double v0lo = uc.c_raw * vlb / vden * (1.0 - 1e-9), v0hi = uc.c_raw * bub / vden * (1.0 + 1e-9);
       const double Rlo = sqrt(uc.q1 * v0lo) * (1.0 - 1e-9), Rhi = sqrt(uc.q1 * v0hi) * (1.0 + 1e-9);
@@ -841,7 +854,6 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
 //    two gathered bucket ranges' lower ends: K = sum over buckets [bs_lo, be_lo).  The window sum of
 //    start s is then K + (first s + h - ce_lo sorted E elements) - (first s - cs_lo sorted S elements):
 //    every window sum shares the same K, so elements below bs_lo never need to be summed.
-static constexpr int GST = 3;  // k_pr_gather: cp.async stages of ILP elements per thread in flight
 static constexpr int GBUF = 1024;  // k_pr_gather: per-CTA shared buffer of gathered elements per side
 
 static constexpr int BCAP = 65536;  // band elements of the fused reweighting per column
@@ -850,7 +862,7 @@ static constexpr int BCAP = 65536;  // band elements of the fused reweighting pe
 // sum (x - kc)^2, kc rounded away as in k_pr_keep) and the values of the two bands around the kept
 // interval's ends, for k_pr_final_fused
 template <bool FUSED>
-__global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ cols, long long len,
+__global__ void __launch_bounds__(PT, FUSED ? 4 : 5) k_pr_gather(const double* __restrict__ cols, long long len,
                                                   const PrunedCol* __restrict__ pc, double* __restrict__ g,
                                                   int* __restrict__ gcount, dd2* __restrict__ below,
                                                   double* __restrict__ band, int* __restrict__ bcount,
@@ -858,102 +870,115 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
   __shared__ dd2 sm[33];
   __shared__ double sbuf[2][GBUF];  // this CTA's gathered elements, flushed with one global atomic per side
   __shared__ int scnt[2], sbase[2];
-  extern __shared__ double gbuf[];  // [GST][ILP][PT]: each thread reads back only what it copied
   const int col = blockIdx.y;
   const PrunedCol c = pc[col];
   if (c.status) return;
   const double* y = cols + (long long)col * len;
   double* S = g + (long long)(2 * col) * CAP;
   double* E = g + (long long)(2 * col + 1) * CAP;
-  constexpr int NACC = 4;  // independent accumulators: the two-sum chains of successive elements overlap
-  ddacc acc[NACC];
+  // K = (sum x, sum x^2) over [bs_lo, be_lo).  Every candidate's objective h S2 - S1^2 contains h K.s2 as
+  // the same additive constant, so only K.s1 decides the argmin and is kept in double-double (two-sum,
+  // error words collected); K.s2 only enters the raw variance and is taken as sum (x - cs)^2 in fp64
+  // about the bucket map's centre cs (positive terms, relative error ~ sqrt(terms) u) plus the exact
+  // shift 2 cs K.s1 - n cs^2 in double-double.  5 fp64 operations per element fewer than two full
+  // double-double sums; the pass is otherwise limited by the fp64 pipe.
+  constexpr int NACC = 2;  // independent accumulators: the two-sum chains of successive elements overlap
+  double a1h[NACC], a1l[NACC], a2[NACC];
 #pragma unroll
-  for (int q = 0; q < NACC; q++) acc[q] = ddacc_zero();
+  for (int q = 0; q < NACC; q++) a1h[q] = a1l[q] = a2[q] = 0.0;
+  int nmid = 0;
+  const double cs = c.cs;
+  // FUSED: sum d, sum d^2 of the certainly kept d = x - kc in fp64 per thread (as k_pr_keep)
   constexpr int NKA = FUSED ? 2 : 1;
-  ddacc kacc[NKA];
+  double ks1[NKA], ks2[NKA];
 #pragma unroll
-  for (int q = 0; q < NKA; q++) kacc[q] = ddacc_zero();
+  for (int q = 0; q < NKA; q++) ks1[q] = ks2[q] = 0.0;
   long long kn = 0;
   __shared__ double bbuf[FUSED ? 512 : 1];
   __shared__ int bcnt_s, bbase_s;
   if (FUSED && threadIdx.x == 0) bcnt_s = 0;
-  const long long per = (len + PCTA - 1) / PCTA;
+  const long long per = (len + gridDim.x - 1) / gridDim.x;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
   const unsigned lane = threadIdx.x & 31, lt_mask = (1u << lane) - 1u;
   if (threadIdx.x < 2) scnt[threadIdx.x] = 0;
   __syncthreads();
-  const long long nb = (i1 - i0 + (long long)PT * ILP - 1) / ((long long)PT * ILP);  // warp-uniform trip count
-  auto issue = [&](long long it) {
-    if (it < nb) {
-      double* dst = gbuf + (it % GST) * ILP * PT + threadIdx.x;
-      const long long base = i0 + it * (long long)PT * ILP + threadIdx.x;
-#pragma unroll
-      for (int k = 0; k < ILP; k++) {
-        const long long i = base + (long long)k * PT;
-        if (i < i1) cp_async8(dst + k * PT, y + i);
-        else dst[k * PT] = __longlong_as_double(0x7ff8000000000000LL);  // NaN: fails every range test
+  // streaming: ILP independent loads per thread in flight (plain registers; full tiles without bounds
+  // tests, then one predicated tail tile whose slots past the range hold NaN, which fails every test)
+  auto consume = [&](const double x, const int k) {
+    // bucket ranges by value thresholds: bucket_of(y) in [b0, b1) <=> T(b0) <= y < T(b1)
+    const bool geS = x >= c.tS0, geE = x >= c.tE0;
+    const bool mid = geS && !geE;  // [bs_lo, be_lo); branch-free: adding 0 is exact
+    {
+      const int q = k % NACC;
+      const double v = mid ? x : 0.0, dv = mid ? __dsub_rn(x, cs) : 0.0;
+      const double sh = __dadd_rn(a1h[q], v), bb = __dsub_rn(sh, a1h[q]);
+      a1l[q] = __dadd_rn(a1l[q], __dadd_rn(__dsub_rn(a1h[q], __dsub_rn(sh, bb)), __dsub_rn(v, bb)));
+      a1h[q] = sh;
+      a2[q] = __fma_rn(dv, dv, a2[q]);
+      nmid += mid ? 1 : 0;
+    }
+    if (FUSED) {
+      const bool kin = x >= c.kin_lo && x <= c.kin_hi;
+      const double dk = kin ? __dsub_rn(x, c.kc) : 0.0;
+      ks1[k % NKA] = __dadd_rn(ks1[k % NKA], dk);
+      ks2[k % NKA] = __fma_rn(dk, dk, ks2[k % NKA]);
+      kn += kin ? 1 : 0;
+      const bool inb = !kin && x >= c.kout_lo && x <= c.kout_hi;
+      if (__any_sync(0xffffffffu, inb)) {  // rare: the bands hold ~1e-4 of the values
+        const unsigned mb = __ballot_sync(0xffffffffu, inb);
+        int pos = 0;
+        if (lane == (unsigned)(__ffs(mb) - 1)) pos = atomicAdd(&bcnt_s, __popc(mb));
+        pos = __shfl_sync(0xffffffffu, pos, __ffs(mb) - 1) + __popc(mb & lt_mask);
+        if (inb) {
+          if (pos < 512) {
+            bbuf[pos] = x;
+          } else {
+            const int gp = atomicAdd(&bcount[col], 1);
+            if (gp < BCAP) band[(long long)col * BCAP + gp] = x;
+          }
+        }
       }
     }
-    cp_async_commit();  // (possibly empty) group: keeps the wait count uniform
+    const bool inS = geS && x < c.tS1, inE = geE && x < c.tE1;
+    if (!__any_sync(0xffffffffu, inS || inE)) return;  // the common case: one vote, no candidate
+    const unsigned ms = __ballot_sync(0xffffffffu, inS), me = __ballot_sync(0xffffffffu, inE);
+#pragma unroll
+    for (int side = 0; side < 2; side++) {  // one shared atomic per warp and side
+      const unsigned mm = side ? me : ms;
+      if (mm) {
+        const bool mine = side ? inE : inS;
+        int pos = 0;
+        if (lane == (unsigned)(__ffs(mm) - 1)) pos = atomicAdd(&scnt[side], __popc(mm));
+        pos = __shfl_sync(0xffffffffu, pos, __ffs(mm) - 1) + __popc(mm & lt_mask);
+        if (mine) {
+          if (pos < GBUF) {
+            sbuf[side][pos] = x;
+          } else {  // CTA buffer full: straight to global memory
+            const int gp = atomicAdd(&gcount[2 * col + side], 1);
+            if (gp < CAP) (side ? E : S)[gp] = x;
+          }
+        }
+      }
+    }
   };
+  const long long nfull = (i1 - i0) / ((long long)PT * ILP);
+  const double* yp = y + i0 + threadIdx.x;
+  for (long long it = 0; it < nfull; it++, yp += (long long)PT * ILP) {
+    double v[ILP];
 #pragma unroll
-  for (int st = 0; st < GST - 1; st++) issue(st);
-  for (long long it = 0; it < nb; it++) {
-    issue(it + GST - 1);
-    cp_async_wait<GST - 1>();
-    const double* src = gbuf + (it % GST) * ILP * PT + threadIdx.x;
+    for (int k = 0; k < ILP; k++) v[k] = __ldg(yp + k * PT);
 #pragma unroll
-    for (int k = 0; k < ILP; k++) {
-      // bucket ranges by value thresholds: bucket_of(y) in [b0, b1) <=> T(b0) <= y < T(b1); the
-      // slots past the CTA's range hold NaN, which fails every test
-      const double x = src[k * PT];
-      const bool geS = x >= c.tS0, geE = x >= c.tE0;
-      ddacc_add(acc[k % NACC], (geS && !geE) ? x : 0.0);  // [bs_lo, be_lo); branch-free: adding 0 is exact
-      if (FUSED) {
-        const bool kin = x >= c.kin_lo && x <= c.kin_hi;
-        const double xv = kin ? x : 0.0;
-        ddacc_add_dev(kacc[k % NKA], xv, kin ? __dsub_rn(x, c.kc) : 0.0);
-        kn += kin ? 1 : 0;
-        const bool inb = !kin && x >= c.kout_lo && x <= c.kout_hi;
-        if (__any_sync(0xffffffffu, inb)) {  // rare: the bands hold ~1e-4 of the values
-          const unsigned mb = __ballot_sync(0xffffffffu, inb);
-          int pos = 0;
-          if (lane == (unsigned)(__ffs(mb) - 1)) pos = atomicAdd(&bcnt_s, __popc(mb));
-          pos = __shfl_sync(0xffffffffu, pos, __ffs(mb) - 1) + __popc(mb & lt_mask);
-          if (inb) {
-            if (pos < 512) {
-              bbuf[pos] = x;
-            } else {
-              const int gp = atomicAdd(&bcount[col], 1);
-              if (gp < BCAP) band[(long long)col * BCAP + gp] = x;
-            }
-          }
-        }
-      }
-      const bool inS = geS && x < c.tS1, inE = geE && x < c.tE1;
-      if (!__any_sync(0xffffffffu, inS || inE)) continue;  // the common case: one vote, no candidate
-      const unsigned ms = __ballot_sync(0xffffffffu, inS), me = __ballot_sync(0xffffffffu, inE);
-#pragma unroll
-      for (int side = 0; side < 2; side++) {  // one shared atomic per warp and side
-        const unsigned mm = side ? me : ms;
-        if (mm) {
-          const bool mine = side ? inE : inS;
-          int pos = 0;
-          if (lane == (unsigned)(__ffs(mm) - 1)) pos = atomicAdd(&scnt[side], __popc(mm));
-          pos = __shfl_sync(0xffffffffu, pos, __ffs(mm) - 1) + __popc(mm & lt_mask);
-          if (mine) {
-            if (pos < GBUF) {
-              sbuf[side][pos] = x;
-            } else {  // CTA buffer full: straight to global memory
-              const int gp = atomicAdd(&gcount[2 * col + side], 1);
-              if (gp < CAP) (side ? E : S)[gp] = x;
-            }
-          }
-        }
-      }
-    }
+    for (int k = 0; k < ILP; k++) consume(v[k], k);
   }
-  cp_async_wait<0>();
+  if (i0 + nfull * (long long)PT * ILP < i1) {  // warp-uniform
+    const long long base = i0 + nfull * (long long)PT * ILP + threadIdx.x;
+    double v[ILP];
+#pragma unroll
+    for (int k = 0; k < ILP; k++)
+      v[k] = base + k * PT < i1 ? __ldg(y + base + k * PT) : __longlong_as_double(0x7ff8000000000000LL);
+#pragma unroll
+    for (int k = 0; k < ILP; k++) consume(v[k], k);
+  }
   __syncthreads();
   if (threadIdx.x < 2) {
     const int n = min(scnt[threadIdx.x], GBUF);
@@ -967,19 +992,25 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
     for (int i = threadIdx.x; i < n; i += PT)
       if (b0 + i < CAP) dst[b0 + i] = sbuf[side][i];
   }
-  dd2 tacc = ddacc_dd2(acc[0]);
+  dd K1 = two_sum(a1h[0], a1l[0]);
+  double K2c = a2[0];
 #pragma unroll
-  for (int q = 1; q < NACC; q++) tacc = dd2_add(tacc, ddacc_dd2(acc[q]));
-  dd2 te = block_sum_dd2(tacc, sm);
+  for (int q = 1; q < NACC; q++) {
+    K1 = dd_add(K1, two_sum(a1h[q], a1l[q]));
+    K2c = __dadd_rn(K2c, a2[q]);
+  }
+  // sum x^2 = sum (x - cs)^2 + 2 cs sum x - n cs^2
+  const dd K2 = dd_sub(dd_add(dd_make(K2c), dd_mul_d(K1, 2.0 * cs)), dd_mul_d(two_prod(cs, cs), (double)nmid));
+  dd2 te = block_sum_dd2({K1, K2}, sm);
   if (threadIdx.x == 0) {
     below[((long long)col * PCTA + blockIdx.x) * 2] = dd2_zero();
     below[((long long)col * PCTA + blockIdx.x) * 2 + 1] = te;
   }
   if (FUSED) {
     __syncthreads();  // sm reused
-    dd2 kt = ddacc_dd2(kacc[0]);
+    dd2 kt = {dd_make(ks1[0]), dd_make(ks2[0])};
 #pragma unroll
-    for (int q = 1; q < NKA; q++) kt = dd2_add(kt, ddacc_dd2(kacc[q]));
+    for (int q = 1; q < NKA; q++) kt = dd2_add(kt, {dd_make(ks1[q]), dd_make(ks2[q])});
     const dd2 ktot = block_sum_dd2(kt, sm);
     __shared__ long long kred[PT / 32];
     for (int d = 16; d > 0; d >>= 1) kn += __shfl_down_sync(0xffffffffu, kn, d);
@@ -1003,14 +1034,14 @@ __global__ void __launch_bounds__(PT) k_pr_gather(const double* __restrict__ col
 
 
 // 5a. double-double prefix sums of each sorted gathered segment (one CTA per segment)
-__device__ void prefix_body(const double* v, int cn, int col, int side, const dd2* __restrict__ below,
+__device__ void prefix_body(const double* v, int cn, int col, int side, int npc, const dd2* __restrict__ below,
                             dd2* __restrict__ P) {
   __shared__ dd2 sm[33];
   __shared__ dd2 base;
   const int t = threadIdx.x;
   if (t == 0) {
     dd2 B = dd2_zero();
-    for (int k = 0; k < PCTA; k++) B = dd2_add(B, below[((long long)col * PCTA + k) * 2 + side]);
+    for (int k = 0; k < npc; k++) B = dd2_add(B, below[((long long)col * PCTA + k) * 2 + side]);
     base = B;
   }
   __syncthreads();
@@ -1028,20 +1059,20 @@ __device__ void prefix_body(const double* v, int cn, int col, int side, const dd
   if (t == 0) P[cn] = dd2_add(base, tot);
 }
 
-__global__ void __launch_bounds__(1024) k_pr_prefix(const PrunedCol* __restrict__ pc, const double* __restrict__ gsorted,
+__global__ void __launch_bounds__(1024) k_pr_prefix(int npc, const PrunedCol* __restrict__ pc, const double* __restrict__ gsorted,
                                                     const int* __restrict__ gcount, const dd2* __restrict__ below,
                                                     dd2* __restrict__ pref) {
   const int seg = blockIdx.x, col = seg >> 1, side = seg & 1;
   if (pc[col].status) return;
   const int cn = min(gcount[seg], CAP);
-  prefix_body(gsorted + (long long)seg * CAP, cn, col, side, below, pref + (long long)seg * (CAP + 1));
+  prefix_body(gsorted + (long long)seg * CAP, cn, col, side, npc, below, pref + (long long)seg * (CAP + 1));
 }
 
 // 5a'. the common case, every gathered segment holding at most SMAX elements: sort the segment in
 //      shared memory (bitonic) and take its prefix sums in the same CTA (replaces the segmented radix
 //      sort's passes and the separate prefix launch)
 static constexpr int SMAX = 16384;
-__global__ void __launch_bounds__(1024) k_pr_sortprefix(const PrunedCol* __restrict__ pc, const double* __restrict__ g,
+__global__ void __launch_bounds__(1024) k_pr_sortprefix(int npc, const PrunedCol* __restrict__ pc, const double* __restrict__ g,
                                                         const int* __restrict__ gcount, const dd2* __restrict__ below,
                                                         dd2* __restrict__ pref) {
   extern __shared__ double sv[];
@@ -1054,7 +1085,7 @@ __global__ void __launch_bounds__(1024) k_pr_sortprefix(const PrunedCol* __restr
   for (int i = threadIdx.x; i < np2; i += blockDim.x) sv[i] = i < cn ? src[i] : INFINITY;
   __syncthreads();
   smem_bitonic(sv, np2);
-  prefix_body(sv, cn, col, side, below, pref + (long long)seg * (CAP + 1));
+  prefix_body(sv, cn, col, side, npc, below, pref + (long long)seg * (CAP + 1));
 }
 
 __device__ __forceinline__ bool win_better2(double ahi, double alo, long long as, double bhi, double blo, long long bs) {
@@ -1186,6 +1217,25 @@ __global__ void k_pr_raw(long long h, const PrunedCol* __restrict__ pc, const dd
   out[col] = o;
 }
 
+// the reweighted fit from K = (sum d, sum d^2) over the k kept values, d = x - shift:
+// loc = shift + sum d / k, sum (x - loc)^2 = sum d^2 - (sum d)^2 / k (reading R4)
+__device__ __forceinline__ void reweighted_from_shifted(const UniConst& uc, const dd2& K, double shift, long long k,
+                                                        UniOut& o) {
+  o.kept = k;
+  if (o.status || k < 2) {
+    o.status = 1;
+    return;
+  }
+  const double kd = (double)k;
+  const dd D = dd_div_d(K.s1, kd);
+  const double loc = dd_to_d(dd_add(dd_make(shift), D));
+  const dd q = dd_sub(K.s2, dd_mul(D, K.s1));
+  const double var = uc.c_rew * (dd_to_d(q) / (double)(k - 1));
+  o.loc = loc;
+  o.scale = sqrt(var);
+  if (!(var > 0.0)) o.status = 1;
+}
+
 // 6. reweighting sums over kept points (fixed-order per-CTA partials)
 __global__ void __launch_bounds__(PT) k_pr_keep(const double* __restrict__ cols, long long len, UniConst uc,
                                                 const UniOut* __restrict__ out, dd2* __restrict__ part,
@@ -1196,9 +1246,14 @@ __global__ void __launch_bounds__(PT) k_pr_keep(const double* __restrict__ cols,
   const UniOut o = out[col];
   const double* y = cols + (long long)col * len;
   const double loc0 = o.raw_loc, thresh = uc.q1 * o.var0;
-  const long long per = (len + PCTA - 1) / PCTA;
+  const long long per = (len + gridDim.x - 1) / gridDim.x;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
-  ddacc acc = ddacc_zero();
+  // sum d and sum d^2 of the kept d = x - loc0 in fp64 per thread (ILP chains; d is centred, the squares
+  // are positive: relative errors ~ sqrt(terms) u), folded over threads and CTAs in double-double
+  constexpr int NKS = 2;
+  double s1[NKS], s2[NKS];
+#pragma unroll
+  for (int u = 0; u < NKS; u++) s1[u] = s2[u] = 0.0;
   long long k = 0;
   for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
     double v[ILP];
@@ -1209,13 +1264,17 @@ __global__ void __launch_bounds__(PT) k_pr_keep(const double* __restrict__ cols,
     for (int u = 0; u < ILP; u++) {
       if (u * PT >= rem) continue;
       const double d = __dsub_rn(v[u], loc0);
-      if (__dmul_rn(d, d) <= thresh) {
-        ddacc_add_dev(acc, v[u], d);
-        k++;
-      }
+      const bool kept = __dmul_rn(d, d) <= thresh;
+      const double dk = kept ? d : 0.0;
+      s1[u % NKS] = __dadd_rn(s1[u % NKS], dk);
+      s2[u % NKS] = __fma_rn(dk, dk, s2[u % NKS]);
+      k += kept ? 1 : 0;
     }
   }
-  dd2 tot = block_sum_dd2(ddacc_dd2(acc), sm);
+  dd2 t = {dd_make(s1[0]), dd_make(s2[0])};
+#pragma unroll
+  for (int u = 1; u < NKS; u++) t = dd2_add(t, {dd_make(s1[u]), dd_make(s2[u])});
+  dd2 tot = block_sum_dd2(t, sm);
   for (int d = 16; d > 0; d >>= 1) k += __shfl_down_sync(0xffffffffu, k, d);
   if ((threadIdx.x & 31) == 0) kc[threadIdx.x >> 5] = k;
   __syncthreads();
@@ -1227,36 +1286,25 @@ __global__ void __launch_bounds__(PT) k_pr_keep(const double* __restrict__ cols,
   }
 }
 
-__global__ void k_pr_final(UniConst uc, const dd2* __restrict__ part, const long long* __restrict__ kcnt,
+__global__ void k_pr_final(UniConst uc, int npc, const dd2* __restrict__ part, const long long* __restrict__ kcnt,
                            UniOut* __restrict__ out) {
   const int col = blockIdx.x;
   if (threadIdx.x != 0) return;
   UniOut o = out[col];
   dd2 K = dd2_zero();
   long long k = 0;
-  for (int q = 0; q < PCTA; q++) {
+  for (int q = 0; q < npc; q++) {
     K = dd2_add(K, part[(long long)col * PCTA + q]);
     k += kcnt[(long long)col * PCTA + q];
   }
-  o.kept = k;
-  if (o.status || k < 2) {
-    o.status = 1;
-  } else {
-    const double Sd = dd_to_d(K.s1);
-    const double loc = Sd / (double)k;
-    const dd q = kept_sq_about_loc(K, o.raw_loc, loc, (double)k);
-    const double var = uc.c_rew * (dd_to_d(q) / (double)(k - 1));
-    o.loc = loc;
-    o.scale = sqrt(var);
-    if (!(var > 0.0)) o.status = 1;
-  }
+  reweighted_from_shifted(uc, K, o.raw_loc, k, o);
   out[col] = o;
 }
 
 // 6'. the fused reweighting: the certainly-kept sums of the gather pass (fixed order over its CTAs) plus
 //     the band values that pass the exact test (x - loc0)^2 <= q1 var0 under the raw fit (reading R4),
 //     all about the shift kc
-__global__ void __launch_bounds__(PT) k_pr_final_fused(UniConst uc, const PrunedCol* __restrict__ pc,
+__global__ void __launch_bounds__(PT) k_pr_final_fused(UniConst uc, int npc, const PrunedCol* __restrict__ pc,
                                                        const dd2* __restrict__ part, const long long* __restrict__ kcnt,
                                                        const double* __restrict__ band, const int* __restrict__ bcount,
                                                        UniOut* __restrict__ out) {
@@ -1267,41 +1315,32 @@ __global__ void __launch_bounds__(PT) k_pr_final_fused(UniConst uc, const Pruned
   UniOut o = out[col];
   const double loc0 = o.raw_loc, thresh = uc.q1 * o.var0;
   const int nb = min(bcount[col], BCAP);
-  ddacc acc = ddacc_zero();
+  double b1 = 0.0, b2 = 0.0;
   long long kb = 0;
   for (int i = threadIdx.x; i < nb; i += PT) {
     const double x = band[(long long)col * BCAP + i];
     const double d = __dsub_rn(x, loc0);
     if (__dmul_rn(d, d) <= thresh) {
-      ddacc_add_dev(acc, x, __dsub_rn(x, c.kc));
+      const double dk = __dsub_rn(x, c.kc);
+      b1 = __dadd_rn(b1, dk);
+      b2 = __fma_rn(dk, dk, b2);
       kb++;
     }
   }
-  const dd2 btot = block_sum_dd2(ddacc_dd2(acc), sm);
+  const dd2 btot = block_sum_dd2({dd_make(b1), dd_make(b2)}, sm);
   for (int d = 16; d > 0; d >>= 1) kb += __shfl_down_sync(0xffffffffu, kb, d);
   if ((threadIdx.x & 31) == 0) kred[threadIdx.x >> 5] = kb;
   __syncthreads();
   if (threadIdx.x != 0) return;
   dd2 K = dd2_zero();
   long long k = 0;
-  for (int q = 0; q < PCTA; q++) {
+  for (int q = 0; q < npc; q++) {
     K = dd2_add(K, part[(long long)col * PCTA + q]);
     k += kcnt[(long long)col * PCTA + q];
   }
   K = dd2_add(K, btot);
   for (int q = 0; q < PT / 32; q++) k += kred[q];
-  o.kept = k;
-  if (o.status || k < 2) {
-    o.status = 1;
-  } else {
-    const double Sd = dd_to_d(K.s1);
-    const double loc = Sd / (double)k;
-    const dd qq = kept_sq_about_loc(K, c.kc, loc, (double)k);
-    const double var = uc.c_rew * (dd_to_d(qq) / (double)(k - 1));
-    o.loc = loc;
-    o.scale = sqrt(var);
-    if (!(var > 0.0)) o.status = 1;
-  }
+  reweighted_from_shifted(uc, K, c.kc, k, o);
   out[col] = o;
 }
 
@@ -1374,18 +1413,17 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   // loose, kfused = 0, sends the batch to k_pr_keep).  Measured on config 4: the fused pass is FP64-bound
   // (two double-double accumulations per value) and takes 7.2 ms per fit against 6.5 ms for the gather
   // and keep passes apart, so it is off by default.
-  static const bool no_fused = getenv("RTD_UNI_FUSEDKEEP") == nullptr;
-  static const int gsmem = [] {
-    const int b = GST * ILP * PT * (int)sizeof(double);
-    RTD_CU(cudaFuncSetAttribute(k_pr_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    RTD_CU(cudaFuncSetAttribute(k_pr_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
-    return b;
-  }();
+  static const bool no_fused = getenv("RTD_UNI_NOFUSEDKEEP") != nullptr;
+  // CTAs per column in the streaming passes: a function of the length only (fixed fold order ->
+  // deterministic), ~128K+ elements each so the per-CTA partial folds stay a small share
+  static const int npc_env = getenv("RTD_PR_CTAS") ? atoi(getenv("RTD_PR_CTAS")) : 0;
+  const int npc = npc_env > 0 ? std::min(npc_env, PCTA) : (int)std::max<long long>(4, std::min<long long>(PCTA, len / 131072));
+  constexpr int gsmem = 0;
   if (no_fused)
-    k_pr_gather<false><<<dim3(PCTA, ncols), PT, gsmem, st>>>(cols, len, s.pc, s.g, s.gcount, s.below, s.band,
+    k_pr_gather<false><<<dim3(npc, ncols), PT, gsmem, st>>>(cols, len, s.pc, s.g, s.gcount, s.below, s.band,
                                                              s.bcount, s.kpart, s.kcnt);
   else
-    k_pr_gather<true><<<dim3(PCTA, ncols), PT, gsmem, st>>>(cols, len, s.pc, s.g, s.gcount, s.below, s.band,
+    k_pr_gather<true><<<dim3(npc, ncols), PT, gsmem, st>>>(cols, len, s.pc, s.g, s.gcount, s.below, s.band,
                                                             s.bcount, s.kpart, s.kcnt);
   RTD_LAUNCHED();
   std::vector<PrunedCol> hc(ncols);
@@ -1398,9 +1436,10 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   static const bool dbg = getenv("RTD_DEBUG_PRUNED") != nullptr;
   if (dbg) {
     for (int j = 0; j < ncols; j++)
-      fprintf(stderr, "pruned len=%lld col=%d status=%d r=[%lld,%lld] s=[%lld,%lld] bs=[%d,%d] be=[%d,%d] span=%g g=%d,%d\n",
+      fprintf(stderr, "pruned len=%lld col=%d status=%d r=[%lld,%lld] s=[%lld,%lld] bs=[%d,%d] be=[%d,%d] span=%g g=%d,%d "
+              "kfused=%d band=%d\n",
               len, j, hc[j].status, hc[j].rmin, hc[j].rmax, hc[j].smin, hc[j].smax, hc[j].bs_lo, hc[j].bs_hi,
-              hc[j].be_lo, hc[j].be_hi, hc[j].hi - hc[j].lo, gc[2 * j], gc[2 * j + 1]);
+              hc[j].be_lo, hc[j].be_hi, hc[j].hi - hc[j].lo, gc[2 * j], gc[2 * j + 1], hc[j].kfused, bc[j]);
   }
   for (int j = 0; j < ncols; j++)
     if (hc[j].status) return false;
@@ -1413,8 +1452,8 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
     }();
     int np2 = 1;
     while (np2 < gmax) np2 <<= 1;
-    k_pr_sortprefix<<<2 * ncols, 1024, std::min(smem, np2 * (int)sizeof(double)), st>>>(s.pc, s.g, s.gcount, s.below,
-                                                                                         s.pref);
+    k_pr_sortprefix<<<2 * ncols, 1024, std::min(smem, np2 * (int)sizeof(double)), st>>>(npc, s.pc, s.g, s.gcount,
+                                                                                         s.below, s.pref);
     RTD_LAUNCHED();
   } else {  // chunk sorts + merge rounds (no library sort on the fit path)
     static const int csmem = [] {
@@ -1430,7 +1469,7 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
       RTD_LAUNCHED();
       std::swap(src, dst);
     }
-    k_pr_prefix<<<2 * ncols, 1024, 0, st>>>(s.pc, src, s.gcount, s.below, s.pref);
+    k_pr_prefix<<<2 * ncols, 1024, 0, st>>>(npc, s.pc, src, s.gcount, s.below, s.pref);
     RTD_LAUNCHED();
   }
   k_pr_eval<<<dim3(s.nch, ncols), PT, 0, st>>>(h, s.pc, s.pref, s.part, s.nch);
@@ -1438,13 +1477,13 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   k_pr_raw<<<ncols, 32, 0, st>>>(h, s.pc, s.pref, s.part, s.nch, uc, out_dev);
   RTD_LAUNCHED();
   if (fused) {
-    k_pr_final_fused<<<ncols, PT, 0, st>>>(uc, s.pc, s.kpart, s.kcnt, s.band, s.bcount, out_dev);
+    k_pr_final_fused<<<ncols, PT, 0, st>>>(uc, npc, s.pc, s.kpart, s.kcnt, s.band, s.bcount, out_dev);
     RTD_LAUNCHED();
     return true;
   }
-  k_pr_keep<<<dim3(PCTA, ncols), PT, 0, st>>>(cols, len, uc, out_dev, s.kpart, s.kcnt);
+  k_pr_keep<<<dim3(npc, ncols), PT, 0, st>>>(cols, len, uc, out_dev, s.kpart, s.kcnt);
   RTD_LAUNCHED();
-  k_pr_final<<<ncols, 32, 0, st>>>(uc, s.kpart, s.kcnt, out_dev);
+  k_pr_final<<<ncols, 32, 0, st>>>(uc, npc, s.kpart, s.kcnt, out_dev);
   RTD_LAUNCHED();
   return true;
 }

@@ -110,6 +110,29 @@ def test_unimcd_large_columns(n):
         assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13), j
 
 
+@pytest.mark.parametrize("offset", [100.0, 1e6, -3e9])
+def test_unimcd_offset_and_skewed_columns_take_the_pruned_path(offset):
+    """Columns far from zero relative to their spread (and a lognormal one): the window bounds work on
+    y - centre, so they prune as tightly as for centred data and no column falls back to the full sort
+    (a raw-units bound on (sum y)^2 loses 2 |sum y| x its width, which once sent such batches to the
+    radix-sort path)."""
+    rng = np.random.default_rng(int(abs(offset)) % 1000)
+    n = 1_000_000
+    cols = np.stack([offset + 3.0 * rng.standard_normal(n), offset + rng.exponential(size=n),
+                     np.exp(rng.standard_normal(n)), offset * (1 + 1e-3 * rng.standard_normal(n))])
+    k0, s0 = api.counters()
+    g = api.unimcd(_cuda(cols))
+    k1, s1 = api.counters()
+    assert s1 - s0 == 0, "a column fell back to the full-sort path"
+    for j in range(cols.shape[0]):
+        o = unimcd_reweighted(cols[j])
+        assert g["start"][j] == o.raw.start, j
+        assert g["raw_loc"][j] == pytest.approx(o.raw.loc, rel=1e-15, abs=1e-300), j
+        assert g["raw_var"][j] == pytest.approx(o.raw.var_raw, rel=1e-13), j
+        assert g["loc"][j] == pytest.approx(o.loc, rel=1e-14, abs=1e-14), j
+        assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13), j
+
+
 def test_unimcd_8m_rows_merge_sorted_candidates():
     """Columns as long as config 4's (8M rows): the gathered candidate sets exceed one shared-memory
     sort (16K), so they go through the chunk sorts + merge path before the exact evaluation."""
