@@ -733,7 +733,7 @@ std::vector<int> refine_batch(cudaStream_t st, RefineBufs& r, const double* Zall
 
 // ------------------------------------------------------------------ initial estimators of q blocks
 struct InitBufs {
-  double *S1, *S2, *r, *rs, *AB, *sums, *partial, *mudummy;
+  double *S1, *S2, *r, *rs, *AB, *sums, *partial, *partial2, *mudummy;
   int* abok;
   int* inst_dev;
   char* sort_tmp;
@@ -754,6 +754,7 @@ void carve_init(Arena& A, InitBufs& b, int q, long long m, int p) {
   b.ctas = (int)std::max<long long>(1, std::min<long long>((m + 511) / 512, (296LL * 4 + q - 1) / q));
   b.sums = A.take<double>((size_t)q * NPMAX);
   b.partial = A.take<double>((size_t)q * b.ctas * NPMAX);
+  b.partial2 = A.take<double>((size_t)q * b.ctas * NPMAX);
   b.mudummy = A.take<double>((size_t)q * RTD_MAXP);
   b.inst_dev = A.take<int>(q + 8);
   b.sort_bytes = sort_bytes(m);
@@ -762,7 +763,9 @@ void carve_init(Arena& A, InitBufs& b, int q, long long m, int p) {
   b.qv = A.take<double>((size_t)q * 6);
 }
 
-void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int p, int q, long long blk_stride) {
+// norms_ready: b.r already holds the rows' norms (written by k_build_Z_norms)
+void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int p, int q, long long blk_stride,
+                 bool norms_ready = false) {
   std::vector<int> ids(q);
   for (int i = 0; i < q; i++) ids[i] = i;
   h2d(st, b.inst_dev, ids.data(), q * sizeof(int));
@@ -780,6 +783,35 @@ void run_initial(cudaStream_t st, InitBufs& b, const double* Z, long long m, int
   a.nblk_hint = q;
   // S~1: covariance of the wrapped data (centred at the wrapped mean, n - 1)
   ProfScope ps("initial", (double)q * m * p * 16.0);
+  // one pass for both S~1 and S~2 (MOM_WRAPXI): norms first (from build_Z, else k_norms), their cutoffs,
+  // then the wrapped and the xi-weighted moments from one read of Z
+  static const bool no_wrapxi = getenv("RTD_NO_WRAPXI") != nullptr;
+  static const int split = getenv("RTD_WRAPXI_SPLIT") ? atoi(getenv("RTD_WRAPXI_SPLIT")) : 5;
+  a.r = b.r;
+  a.partial2 = b.partial2;
+  a.split = split;
+  if (!no_wrapxi && use_mma() && moments_tma_supported(MOM_WRAPXI, a)) {
+    if (!norms_ready) launch_norms(Z, m, p, q, blk_stride, b.r, st);
+    std::vector<int> fb;
+    launch_quantiles(b.r, m, q, b.qscratch, b.qv, st, fb);
+    for (int l : fb) {
+      size_t bytes = b.sort_bytes;
+      count_sort();
+      RTD_CU(cub::DeviceRadixSort::SortKeys(b.sort_tmp, bytes, b.r + (size_t)l * m, b.rs + (size_t)l * m, (int)m, 0, 64,
+                                            st));
+      launch_q_from_sorted(b.rs + (size_t)l * m, m, l, b.qv, st);
+    }
+    launch_q_cutoffs(b.qv, m, q, b.AB, b.abok, st);
+    a.AB = b.AB;
+    launch_moments_tma(MOM_WRAPXI, a, q, st);
+    launch_mom_reduce(b.partial, q, b.inst_dev, b.ctas, np, b.sums, 0, st);
+    launch_sums_to_cov(b.inst_dev, q, b.sums, np, nullptr, p, (double)m, 1.0, b.mudummy, b.S1, st);
+    launch_mom_reduce(b.partial2, q, b.inst_dev, b.ctas, np, b.sums, 0, st);
+    launch_sums_to_second(b.sums, q, np, p, (double)m, b.S2, st);
+    return;
+  }
+  a.r = nullptr;
+  a.partial2 = nullptr;
   // the staged wrap pass also writes the row norms of S~2 (one read of Z less)
   const bool fused_norms = use_mma() && (moments_tma_supported(MOM_WRAP, a) || moments_staged(MOM_WRAP, a));
   if (fused_norms) a.r_out = b.r;
@@ -821,6 +853,7 @@ struct FitBufs {
   char* uscratch;
   size_t uscratch_bytes;
   long long* rowmap;
+  bool norms_ready = false;  // ib.r holds the norms of the rows of f.Z (k_build_Z_norms)
   InitBufs ib;
   RefineBufs rb;
   CStepBufs cb;
@@ -948,7 +981,7 @@ std::vector<int> phase_starts(cudaStream_t st, FitBufs& f, const Dims& d, const 
   const int p = d.p, q = d.q;
   const long long m = d.m, blk_stride = (long long)p * m;
   BlockResult r;
-  run_initial(st, f.ib, f.Z, m, p, q, blk_stride);
+  run_initial(st, f.ib, f.Z, m, p, q, blk_stride, f.norms_ready);
   launch_jacobi(f.ib.S1, 2 * q, p, o.kappa_max, f.V2, f.lam2, f.jok, st);  // [k q + b]: S~1 blocks, then S~2
   std::vector<int> jok(2 * q), abok(q);
   fetch(st, {{jok.data(), f.jok, 2 * q * sizeof(int)}, {abok.data(), f.ib.abok, q * sizeof(int)}});
@@ -1183,7 +1216,9 @@ void fit_impl(rtdetmcd_ctx* c, const double* X, long long n, int p, const rtdetm
   // partition + Z = (X - loc)/scale per block, column-major
   {
     ProfScope ps("build_Z", (double)q * m * p * 16.0);
-    launch_build_Z(f.Xc, Xdev, n, p, q, m, d.perm, o.seed, d.log, f.uni, f.Z, f.rowmap, st);
+    f.norms_ready = warm_mu == nullptr;  // the initial estimators' norms (not needed from a warm start)
+    launch_build_Z(f.Xc, Xdev, n, p, q, m, d.perm, o.seed, d.log, f.uni, f.Z, f.rowmap, f.norms_ready ? f.ib.r : nullptr,
+                   st);
   }
 
   // H2-H9 per block, H10 raw fit
@@ -1480,7 +1515,8 @@ void fit_sharded_impl(rtdetmcd_ctx* c, const double* X, long long n_local, long 
   // this rank's blocks: Z, steps 1-4
   {
     ProfScope ps("build_Z", (double)ql * m * p * 16.0);
-    launch_build_Z(f.Xc, Xdev, n, p, ql, m, 0, 0, d.log, f.uni, f.Z, nullptr, st);
+    f.norms_ready = true;
+    launch_build_Z(f.Xc, Xdev, n, p, ql, m, 0, 0, d.log, f.uni, f.Z, nullptr, f.ib.r, st);
   }
   BlockResult br = phase_blocks(st, f, d, o);
 
@@ -2132,7 +2168,8 @@ rtdetmcd_status rtdetmcd_blocks_fit(rtdetmcd_ctx* c, const double* X_local, int6
       u[j].scale = scale[j];
     }
     h2d(st, f.uni, u.data(), RTD_MAXP * sizeof(UniOut));
-    launch_build_Z(f.Xc, Xdev, n_local, p, q_local, d.m, 0, 0, d.log, f.uni, f.Z, nullptr, st);
+    f.norms_ready = true;
+    launch_build_Z(f.Xc, Xdev, n_local, p, q_local, d.m, 0, 0, d.log, f.uni, f.Z, nullptr, f.ib.r, st);
     S->br = phase_blocks(st, f, d, o);
     const int R = 4 + p + p * p;
     std::vector<double> mu(RTD_MAXP), sg(M2);

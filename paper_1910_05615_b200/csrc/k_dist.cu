@@ -189,33 +189,75 @@ __global__ void k_build_Z_identity(const double* __restrict__ Xc, long long n, i
   }
 }
 
+// The same map with the rows' norms ||z_i|| of S~2 in the same pass: a thread owns
+// BZR rows of one block and walks the columns, so the sum of squares runs in registers, sequential
+// over k without FMA (the arithmetic of k_norms) -- the initial-estimator pass then needs no norms
+// of its own and both of its moment matrices come from one read of Z (MOM_WRAPXI).
+static constexpr int BZR = 4;
+__global__ void __launch_bounds__(256) k_build_Z_norms(const double* __restrict__ Xc, long long n, int p, long long m,
+                                                       const UniOut* __restrict__ uni, double* __restrict__ Z,
+                                                       double* __restrict__ r) {
+  const int b = blockIdx.y;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long s0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; s0 < m; s0 += BZR * stride) {
+    double sq[BZR];
+#pragma unroll
+    for (int u = 0; u < BZR; u++) sq[u] = 0.0;
+    for (int k = 0; k < p; k++) {
+      const double loc = __ldg(&uni[k].loc), sc = __ldg(&uni[k].scale);
+      const double* __restrict__ src = Xc + (long long)k * n + (long long)b * m;
+      double* __restrict__ dst = Z + ((long long)b * p + k) * m;
+      double v[BZR];
+#pragma unroll
+      for (int u = 0; u < BZR; u++) v[u] = s0 + u * stride < m ? __ldg(src + s0 + u * stride) : 0.0;
+#pragma unroll
+      for (int u = 0; u < BZR; u++) {
+        const double z = __ddiv_rn(__dsub_rn(v[u], loc), sc);
+        sq[u] = __dadd_rn(sq[u], __dmul_rn(z, z));
+        if (s0 + u * stride < m) dst[s0 + u * stride] = z;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < BZR; u++)
+      if (s0 + u * stride < m) r[(long long)b * m + s0 + u * stride] = __dsqrt_rn(sq[u]);
+  }
+}
+
 __global__ void k_build_Z_perm(const double* __restrict__ X, long long n, int p, long long m, int q,
                                unsigned long long seed, int half, int log_transform, const UniOut* __restrict__ uni,
-                               double* __restrict__ Z, long long* __restrict__ rowmap) {
+                               double* __restrict__ Z, long long* __restrict__ rowmap, double* __restrict__ r) {
   const long long total = (long long)q * m;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     long long b = t / m, s = t - b * m;
     long long row = feistel_inv(t, n, seed, half);
     if (rowmap) rowmap[t] = row;
     const double* xr = X + row * p;
+    double sq = 0.0;
     for (int k = 0; k < p; k++) {
       double v = xr[k];
       if (log_transform) v = log(v);
-      Z[(b * p + k) * m + s] = __ddiv_rn(__dsub_rn(v, uni[k].loc), uni[k].scale);
+      const double z = __ddiv_rn(__dsub_rn(v, uni[k].loc), uni[k].scale);
+      Z[(b * p + k) * m + s] = z;
+      sq = __dadd_rn(sq, __dmul_rn(z, z));
     }
+    if (r) r[t] = __dsqrt_rn(sq);
   }
 }
 
 void launch_build_Z(const double* Xc, const double* X, long long n, int p, int q, long long m, int perm,
                     unsigned long long seed, int log_transform, const UniOut* uni, double* Z, long long* rowmap,
-                    cudaStream_t st) {
-  if (!perm) {
+                    double* r_out, cudaStream_t st) {
+  if (!perm && r_out) {
+    const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((m + 256 * BZR - 1) / (256 * BZR),
+                                                                            (148LL * 8 + q - 1) / q));
+    k_build_Z_norms<<<dim3(gx, q), 256, 0, st>>>(Xc, n, p, m, uni, Z, r_out);
+  } else if (!perm) {
     const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((m + 1023) / 1024, 148 * 8));
     k_build_Z_identity<<<dim3(gx, p), 256, 0, st>>>(Xc, n, p, m, q, uni, Z);
   } else {
     long long total = (long long)q * m;
     unsigned gx = (unsigned)std::min<long long>((total + 255) / 256, 148 * 32);
-    k_build_Z_perm<<<gx, 256, 0, st>>>(X, n, p, m, q, seed, feistel_half(n), log_transform, uni, Z, rowmap);
+    k_build_Z_perm<<<gx, 256, 0, st>>>(X, n, p, m, q, seed, feistel_half(n), log_transform, uni, Z, rowmap, r_out);
   }
   RTD_LAUNCHED();
 }

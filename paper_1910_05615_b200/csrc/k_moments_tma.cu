@@ -4,7 +4,9 @@
 //                row norms ||z_i|| of S~2 from the same tile;
 //   MOM_XI       u = z, w = xi(||z_i||)^2 (LR-GSSCM weights, S~2);
 //   MOM_MEMBER   u = z - c, w = [i in H] (C-step moments);
-//   MOM_REWEIGHT u = z - c, w = [d_i^2 <= chi2] (reweighting).
+//   MOM_REWEIGHT u = z - c, w = [d_i^2 <= chi2] (reweighting);
+//   MOM_WRAPXI   MOM_WRAP (warps [0, split), into partial) and MOM_XI (the other warps, into partial2) on
+//                the same tiles: S~1 and S~2 from one read of Z once the norms and cutoffs are known.
 //
 // Lane 0 of warp 0 streams TR-row tiles of the block's column-major Z through an NS-stage
 // shared-memory ring with cp.async.bulk.tensor (3-D tensor map [blocks][columns][rows]) and
@@ -82,7 +84,8 @@ __global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
   // per-stage copy of the rows' weight source (norms r / distances d2 / membership bytes), loaded by TMA
   // with the tile on the same barrier
   unsigned char* wsrc = smraw + C::OFF_W;
-  constexpr bool WT = MODE == MOM_XI || MODE == MOM_REWEIGHT;
+  constexpr bool FX = MODE == MOM_WRAPXI;
+  constexpr bool WT = MODE == MOM_XI || MODE == MOM_REWEIGHT || FX;
   constexpr uint32_t WBYTES = WT ? TR * 8 : 0;
   const int slot = blockIdx.y;
   const int id = a.inst[slot];
@@ -101,29 +104,31 @@ __global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  // producer = lane 0 of warp 0: the first NS - 1 tiles now; on entering tile k >= 1 it issues tile
-  // k + NS - 2 into the stage of tile k - 2 (released by every warp before any enters tile k, bar the
-  // stragglers it then waits for)
+  // producer = lane 0 of warp 0, opportunistic: the first NS - 1 tiles now; then, between its groups, tile
+  // nxt as soon as the stage's previous tile has been released by every warp (a non-blocking test, at most
+  // NS - 1 tiles ahead of its own, so the parity test cannot alias an older phase); it blocks only on
+  // entering a tile not yet issued
   auto issue = [&](int j) {
-    if (j >= ntile) return;
     const int s = j % NS;
     mbar_wait(&empty[s], (uint32_t)(((j / NS) & 1) ^ 1));
     mbar_expect_tx(&full[s], (uint32_t)(C::TILE * 8) + WBYTES);
     tma_load_3d(tiles + (size_t)s * STG, &zmap, &full[s], (int)(r_begin + (long long)j * TR), 0, blk);
-    if (WT) tma_load_2d(wsrc + s * C::WST, &wmap, &full[s], (int)(r_begin + (long long)j * TR), MODE == MOM_XI ? blk : id);
+    if (WT) tma_load_2d(wsrc + s * C::WST, &wmap, &full[s], (int)(r_begin + (long long)j * TR), MODE == MOM_REWEIGHT ? id : blk);
   };
+  int nxt = 0;  // tiles issued so far (lane 0 of warp 0)
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&zmap)) : "memory");
     if (WT) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
-    for (int j = 0; j < NS - 1; j++) issue(j);
+    for (; nxt < NS - 1 && nxt < ntile; nxt++) issue(nxt);
   }
   const int g = lane >> 2, t = lane & 3;
   double sh[NB];
 #pragma unroll
   for (int b = 0; b < NB; b++)
-    sh[b] = (MODE >= MOM_MEMBER && 8 * b + g < P) ? a.shift[(long long)id * RTD_MAXP + 8 * b + g] : 0.0;
+    sh[b] = ((MODE == MOM_MEMBER || MODE == MOM_REWEIGHT) && 8 * b + g < P) ? a.shift[(long long)id * RTD_MAXP + 8 * b + g]
+                                                                             : 0.0;
   double A = 0.0, B = 0.0;
-  if (MODE == MOM_XI) {
+  if (MODE == MOM_XI || FX) {
     A = a.AB[2 * blk];
     B = a.AB[2 * blk + 1];
   }
@@ -134,49 +139,58 @@ __global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
 #pragma unroll
   for (int b = 0; b < NB; b++) s1[b] = 0.0;
   double cnt = 0.0;
-  // this warp's groups q = warp, warp + 8, ... of the CTA's ntile * G groups (tile k = q / G holds group
-  // l = q % G at rows 4l..4l+3)
-  double* scr = scratch + warp * (5 * 32);  // MOM_WRAP: per-warp list of tanh-branch arguments
-  const long long nq = (long long)ntile * G;
+  // roles (MOM_WRAPXI): warps [0, split) take the wrapped moments, the others the xi-weighted ones; each
+  // role deals the CTA's ntile * G groups round-robin across tiles: group l of tile k, then l + NWR
+  // (carried into the next tile), so no warp idles at a tile boundary although a tile holds an odd
+  // number (25) of groups
+  const bool wrap_role = MODE == MOM_WRAP || (FX && warp < a.split);
+  const int NWR = FX ? (wrap_role ? a.split : NCW - a.split) : NCW;
+  const int wr = FX ? (wrap_role ? warp : warp - a.split) : warp;
+  double* scr = scratch + warp * (5 * 32);  // wrapped moments: per-warp list of tanh-branch arguments
   int cur = -1;  // tile whose full barrier this warp has passed
-  for (long long q = warp; q < nq; q += NCW) {
-    const int k = (int)(q / G), l = (int)(q % G);
+  for (int k = 0, l = wr; k < ntile; l = (l + NWR >= G) ? (k++, l + NWR - G) : l + NWR) {
     while (cur < k) {  // release the tile left behind, enter the next one
       if (cur >= 0) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[cur % NS]);
       }
       cur++;
-      if (warp == 0 && lane == 0 && cur >= 1) issue(cur + NS - 2);
+      if (warp == 0 && lane == 0)
+        for (; nxt <= cur && nxt < ntile; nxt++) issue(nxt);  // blocking only for the tile entered now
       mbar_wait(&full[cur % NS], (uint32_t)((cur / NS) & 1));
     }
+    if (warp == 0 && lane == 0 && nxt < ntile && nxt <= cur + NS - 1 &&
+        mbar_test(&empty[nxt % NS], (uint32_t)(((nxt / NS) & 1) ^ 1))) {
+      issue(nxt);  // released: does not block
+      nxt++;
+    }
+    const long long row = r_begin + (long long)k * TR + 4 * l + t;
     double w = 0.0;
-    if (r_begin + (long long)k * TR + 4 * l + t < r_end) {
+    if (row < r_end) {
       const unsigned char* ws = wsrc + (k % NS) * C::WST;
-      if (MODE == MOM_WRAP) {
+      if (wrap_role) {
         w = 1.0;
-      } else if (MODE == MOM_XI) {
+      } else if (MODE == MOM_XI || FX) {
         const double rr = reinterpret_cast<const double*>(ws)[4 * l + t];
         const double xi = rr <= A ? 1.0 : (rr <= B ? __ddiv_rn(__dsub_rn(B, rr), __dsub_rn(B, A)) : 0.0);
         w = __dmul_rn(xi, xi);
       } else if (MODE == MOM_MEMBER) {  // membership bytes from global memory (a UINT8 2-D TMA map of them
         // faulted with an illegal instruction on this stack; the bytes are L2-resident)
-        w = (double)a.mem_new[(long long)id * m + r_begin + (long long)k * TR + 4 * l + t];
+        w = (double)a.mem_new[(long long)id * m + row];
       } else {
         w = reinterpret_cast<const double*>(ws)[4 * l + t] <= a.c2 ? 1.0 : 0.0;
       }
     }
-    if (MODE != MOM_WRAP && !__any_sync(0xffffffffu, w != 0.0)) continue;
+    if (!wrap_role && !__any_sync(0xffffffffu, w != 0.0)) continue;  // wrap_role is warp-uniform
     const double* T = tiles + (size_t)(k % NS) * STG;
-    const long long row = r_begin + (long long)k * TR + 4 * l + t;
     double u[NB];
 #pragma unroll
     for (int b = 0; b < NB; b++) {
       const int col = 8 * b + g;
       u[b] = (col < P && w != 0.0) ? T[col * TR + 4 * l + t] : 0.0;
     }
-    if (MODE == MOM_WRAP) {
-      if (a.r_out) {  // ||z_i||: lane partial over its columns, then over the 8 column lanes (fixed order)
+    if (wrap_role) {
+      if (MODE == MOM_WRAP && a.r_out) {  // ||z_i||: lane partial over its columns, then over the 8 column lanes
         double sq = 0.0;
 #pragma unroll
         for (int b = 0; b < NB; b++) sq = __dadd_rn(sq, __dmul_rn(u[b], u[b]));
@@ -186,33 +200,35 @@ __global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
         if (g == 0 && row < r_end) a.r_out[(long long)blk * m + row] = __dsqrt_rn(sq);
       }
       // psi: identity / zero branches in place; the tanh branch (1.5 < |z| <= 4, ~13 %
-      // of the entries) compacted into a warp-private list, evaluated by all 32 lanes, scattered back
-      // (the branch tests on the magnitude's bit pattern -- integer compares, IEEE order -- so the FP64
-      // pipe the DMMAs share only evaluates the compacted tanh entries)
-      constexpr unsigned long long B15 = 0x3FF8000000000000ull, C40 = 0x4010000000000000ull;  // 1.5, 4.0
+      // of the entries) compacted into a warp-private list, evaluated by all 32 lanes, scattered back.
+      // The branch tests compare the magnitude's high / low words (IEEE order, exact) on the integer pipe;
+      // a lane's slots in the list come from one warp scan of its entry count.
+      // 1.5 < |z| <= 4 as one unsigned range test on the magnitude's bits (IEEE order, exact; |z| <= 1.5
+      // wraps around to a huge value), |z| > 4 -> 0
+      constexpr unsigned long long B15N = 0x3FF8000000000001ull, C40 = 0x4010000000000000ull;  // next(1.5), 4.0
       int pos[NB];
       int n = 0;
+      const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
       for (int b = 0; b < NB; b++) {
         const unsigned long long ab = (unsigned long long)__double_as_longlong(u[b]) & 0x7FFFFFFFFFFFFFFFull;
-        const bool need = ab > B15 && ab <= C40;
+        const bool need = ab - B15N <= C40 - B15N;
         const unsigned bal = __ballot_sync(0xffffffffu, need);
-        pos[b] = need ? n + __popc(bal & ((1u << lane) - 1u)) : -1;
+        pos[b] = need ? n + __popc(bal & lt) : -1;
         if (need) scr[pos[b]] = __longlong_as_double((long long)ab);  // |z|
         n += __popc(bal);
         if (ab > C40) u[b] = 0.0;
       }
-      __syncwarp();
-      for (int i = lane; i < n; i += 32) scr[i] = __dmul_rn(1.541, tanh(__dmul_rn(0.862, __dsub_rn(4.0, scr[i]))));
-      __syncwarp();
+      if (n) {
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) scr[i] = __dmul_rn(1.541, tanh(__dmul_rn(0.862, __dsub_rn(4.0, scr[i]))));
+        __syncwarp();
 #pragma unroll
-      for (int b = 0; b < NB; b++)
-        if (pos[b] >= 0) {
-          const double v = scr[pos[b]];
-          u[b] = (__double_as_longlong(u[b]) < 0) ? -v : v;  // |z| > 1.5: the sign bit is the sign
-        }
-      __syncwarp();
-    } else if (MODE >= MOM_MEMBER) {
+        for (int b = 0; b < NB; b++)
+          if (pos[b] >= 0) u[b] = copysign(scr[pos[b]], u[b]);  // |z| > 1.5: the sign bit is the sign
+        __syncwarp();
+      }
+    } else if (MODE == MOM_MEMBER || MODE == MOM_REWEIGHT) {
 #pragma unroll
       for (int b = 0; b < NB; b++) u[b] = (w != 0.0 && 8 * b + g < P) ? __dsub_rn(u[b], sh[b]) : 0.0;
     }
@@ -272,11 +288,17 @@ __global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
       }
   }
   consumer_sync();
-  double* out = a.partial + ((long long)slot * a.ctas + blockIdx.x) * NP;
+  const long long po = ((long long)slot * a.ctas + blockIdx.x) * NP;
+  const int q1 = FX ? a.split : NCW;  // warps [0, q1) -> partial, [q1, NCW) -> partial2 (fixed order)
   for (int e = threadIdx.x; e < NP; e += NCW * 32) {
     double v = 0.0;
-    for (int q = 0; q < NCW; q++) v += red[q * NP + e];
-    out[e] = v;
+    for (int q = 0; q < q1; q++) v += red[q * NP + e];
+    a.partial[po + e] = v;
+    if (FX) {
+      double v2 = 0.0;
+      for (int q = q1; q < NCW; q++) v2 += red[q * NP + e];
+      a.partial2[po + e] = v2;
+    }
   }
 }
 
@@ -290,7 +312,8 @@ void moments_tma_p(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
     throw std::string("cuTensorMapEncodeTiled failed for the moment pass");
   CUtensorMap wmap = map;  // MOM_WRAP: unused
   bool ok = true;
-  if (mode == MOM_XI) ok = encode_rows(&wmap, a.r, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, a.m, a.nblk_hint, C::TR);
+  if (mode == MOM_XI || mode == MOM_WRAPXI)
+    ok = encode_rows(&wmap, a.r, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, a.m, a.nblk_hint, C::TR);
   if (mode == MOM_REWEIGHT) ok = encode_rows(&wmap, a.d2, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, a.m, a.ninst_hint, C::TR);
   if (!ok) throw std::string("cuTensorMapEncodeTiled failed for the moment weights");
   dim3 grid(a.ctas, ninst);
@@ -304,6 +327,7 @@ void moments_tma_p(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
     RTD_MT_CASE(MOM_XI)
     RTD_MT_CASE(MOM_MEMBER)
     RTD_MT_CASE(MOM_REWEIGHT)
+    RTD_MT_CASE(MOM_WRAPXI)
     default: throw std::string("moments_tma: mode");
   }
 #undef RTD_MT_CASE
@@ -313,6 +337,8 @@ void moments_tma_p(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
 
 bool moments_tma_supported(int mode, const MomArgs& a) {
   static const bool off = getenv("RTD_MOM_NOTMA") != nullptr;
+  if (mode == MOM_WRAPXI && (a.partial2 == nullptr || a.split < 1 || a.split >= MomTmaCfg<8>::NCW || a.r == nullptr))
+    return false;
   return !off && mode != MOM_DELTA && a.p >= 8 && a.p <= RTD_MAXP && a.m % 16 == 0 && a.m >= 8192 &&
          a.blk_stride == (long long)a.p * a.m && a.nblk_hint > 0 &&
          (a.ninst_hint > 0 || mode != MOM_REWEIGHT) && encode_fn() != nullptr;

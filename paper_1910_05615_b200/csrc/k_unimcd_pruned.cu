@@ -85,18 +85,49 @@ __device__ __forceinline__ double ord_val(unsigned long long k) {
   return __longlong_as_double((long long)u);
 }
 
-// Smallest double y with bucket_of(y) >= b (bucket_of is monotone in y), found by bisection over the
-// ordered bit patterns: y >= bucket_threshold(b) <=> bucket_of(y) >= b, so the streaming passes can
-// test bucket ranges with two compares
+// Smallest double y with bucket_of(y) >= b (bucket_of is monotone in y), searched over the ordered bit
+// patterns: y >= bucket_threshold(b) <=> bucket_of(y) >= b, so the streaming passes can test bucket ranges
+// with two compares.  A gallop from the bucket's nominal lower end lo + (b - 1) w brackets the boundary
+// within a few ulps (it is off by the rounding of bucket_of only), then bisection; the bracket is clamped to
+// [-inf, inf], so any column is handled (a plain bisection over all 2^64 patterns took 64 serial steps).
 __device__ double bucket_threshold(int b, const PrunedCol& c) {
   if (b <= 0) return -INFINITY;
   if (b >= NBK) return INFINITY;
-  unsigned long long lo = ord_key(-INFINITY), hi = ord_key(INFINITY);  // bucket_of(ord_val(hi)) = NBK - 1 >= b
-  while (lo < hi) {
-    const unsigned long long mid = lo + (hi - lo) / 2;
-    if (bucket_of(ord_val(mid), c) >= b) hi = mid; else lo = mid + 1;
+  const unsigned long long kmin = ord_key(-INFINITY), kmax = ord_key(INFINITY);  // bucket_of(inf) = NBK - 1 >= b
+  const double y0 = b == NBK - 1 ? c.hi : c.lo + (double)(b - 1) * c.w;
+  const unsigned long long k0 = isfinite(y0) ? ord_key(y0) : kmax;
+  unsigned long long lo, hi;  // invariant: bucket_of(lo) < b <= bucket_of(hi), or lo = kmin - 1 (none below)
+  if (bucket_of(ord_val(k0), c) >= b) {
+    hi = k0;
+    unsigned long long step = 1;
+    for (;;) {
+      const unsigned long long k = hi - kmin > step ? hi - step : kmin;
+      if (bucket_of(ord_val(k), c) < b) {
+        lo = k;
+        break;
+      }
+      hi = k;
+      if (k == kmin) return ord_val(kmin);
+      step <<= 1;
+    }
+  } else {
+    lo = k0;
+    unsigned long long step = 1;
+    for (;;) {
+      const unsigned long long k = kmax - lo > step ? lo + step : kmax;
+      if (bucket_of(ord_val(k), c) >= b) {
+        hi = k;
+        break;
+      }
+      lo = k;
+      step <<= 1;
+    }
   }
-  return ord_val(lo);
+  while (hi - lo > 1) {
+    const unsigned long long mid = lo + (hi - lo) / 2;
+    if (bucket_of(ord_val(mid), c) >= b) hi = mid; else lo = mid;
+  }
+  return ord_val(hi);
 }
 
 // Running (sum y, sum y^2) of one thread in double-double, adding one double at a time with
@@ -143,18 +174,19 @@ __device__ __forceinline__ dd2 ddacc_dd2(const ddacc& a) {
 
 static constexpr int ILP = 8;  // elements loaded per thread before they are consumed (latency hiding)
 
+// in-place bitonic sort of a power-of-two shared array; every thread takes whole compare-exchange pairs
+// (pair p -> element i = p with a zero bit inserted at log2(j), partner i | j), none idles in a stage
 __device__ void smem_bitonic(double* a, int npow2) {
+  const int half = npow2 >> 1;
   for (int k = 2; k <= npow2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
-        int ixj = i ^ j;
-        if (ixj > i) {
-          bool up = (i & k) == 0;
-          double x = a[i], y = a[ixj];
-          if ((x > y) == up) {
-            a[i] = y;
-            a[ixj] = x;
-          }
+      for (int pr = threadIdx.x; pr < half; pr += blockDim.x) {
+        const int i = ((pr & ~(j - 1)) << 1) | (pr & (j - 1)), ixj = i | j;
+        const bool up = (i & k) == 0;
+        const double x = a[i], y = a[ixj];
+        if ((x > y) == up) {
+          a[i] = y;
+          a[ixj] = x;
         }
       }
       __syncthreads();
@@ -803,8 +835,8 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
   const long long smax = block_reduce(cmax, [](long long x, long long y) { return max(x, y); }, redl);
   const double vlb = block_reduce(vmin, [](double x, double y) { return fmin(x, y); }, redd);
 
-  // e. gathered bucket ranges
-  if (t == 0) {
+  // e. gathered bucket ranges (warp 0: every lane derives the same fields, lanes 0-3 the four thresholds)
+  if (t < 32) {
     c.smin = smin;
     c.smax = smax;
     c.rmin = lo_s;
@@ -820,10 +852,12 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
       c.ce_lo = C[c.be_lo];
       const long long ns = C[c.bs_hi + 1] - C[c.bs_lo], ne = C[c.be_hi + 1] - C[c.be_lo];
       if (ns > CAP || ne > CAP) c.status = 1;
-      c.tS0 = bucket_threshold(c.bs_lo, c);
-      c.tS1 = bucket_threshold(c.bs_hi + 1, c);
-      c.tE0 = bucket_threshold(c.be_lo, c);
-      c.tE1 = bucket_threshold(c.be_hi + 1, c);
+      const int tb = t == 0 ? c.bs_lo : (t == 1 ? c.bs_hi + 1 : (t == 2 ? c.be_lo : c.be_hi + 1));
+      const double thr = t < 4 ? bucket_threshold(tb, c) : 0.0;
+      c.tS0 = __shfl_sync(0xffffffffu, thr, 0);
+      c.tS1 = __shfl_sync(0xffffffffu, thr, 1);
+      c.tE0 = __shfl_sync(0xffffffffu, thr, 2);
+      c.tE1 = __shfl_sync(0xffffffffu, thr, 3);
       // the reweighting step (reading R4) keeps x iff (x - loc0)^2 <= q1 var0; the
       // raw fit is not known yet, but loc0 = S1(s*) / h with s* in [smin, smax] (the window mean is
       // monotone in s) and h SQ(s*) in [vlb, bub] bound it: values well inside the kept interval for
@@ -846,7 +880,7 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
       c.kfused = (vlb > 0.0 && isfinite(mlo) && isfinite(mhi) && isfinite(Rhi) && mlo <= mhi &&
                   c.kin_lo < c.kin_hi && (mhi - mlo) < 0.01 * Rlo && (Rhi - Rlo) < 0.01 * Rlo) ? 1 : 0;
     }
-    pc[col] = c;
+    if (t == 0) pc[col] = c;
   }
 }
 

@@ -111,6 +111,7 @@ void launch_transpose(const double* X, long long n, int p, int log_transform, do
 // else row = feistel^-1(b*m+s) gathered from row-major X (with optional log).
 void launch_build_Z(const double* Xc, const double* X, long long n, int p, int q, long long m, int perm,
                     unsigned long long seed, int log_transform, const UniOut* uni, double* Z, long long* rowmap,
+                    double* r_out /* [q][m] row norms ||z_i|| (nullable) */,
                     cudaStream_t st);
 // d2 for instances: rows of instance id = Zall + (id / nstart) * blk_stride; d2 at d2_all + id * m;
 // constants in c_mat at slot*cstride:
@@ -137,7 +138,9 @@ void launch_q_from_sorted(const double* sorted, long long m, int b, double* qv, 
 void launch_q_cutoffs(const double* qv, long long m, int nb, double* AB, int* ok, cudaStream_t st);
 
 // ---------------------------------------------------------------- moments (k_moments.cu)
-enum MomMode { MOM_WRAP = 0, MOM_XI = 1, MOM_MEMBER = 2, MOM_DELTA = 3, MOM_REWEIGHT = 4 };
+// MOM_WRAPXI (TMA path only): MOM_WRAP and MOM_XI from one read of Z -- warps [0, split) take the wrapped
+// moments into partial, the others the xi-weighted ones into partial2 (norms r and cutoffs AB known)
+enum MomMode { MOM_WRAP = 0, MOM_XI = 1, MOM_MEMBER = 2, MOM_DELTA = 3, MOM_REWEIGHT = 4, MOM_WRAPXI = 5 };
 struct MomArgs {
   const double* Z;          // base of all blocks (column-major per block)
   long long m;              // rows per block
@@ -160,6 +163,8 @@ struct MomArgs {
   long long seg_len;        // rows per segment (segment x = CTA x)
   int nblk_hint;            // blocks of m x p doubles at Z (the TMA-fed dense passes map them; 0: unknown)
   int ninst_hint;           // instances the per-instance arrays (mem_new, d2) hold (0: unknown)
+  double* partial2;         // MOM_WRAPXI: [slot][cta][NP] partials of the xi-weighted moments
+  int split;                // MOM_WRAPXI: warps on the wrapped moments (the rest: xi-weighted)
 };
 int mom_np(int p);  // p + p(p+1)/2 + 1
 void launch_moments(int mode, const MomArgs& a, int ninst, cudaStream_t st);

@@ -215,6 +215,18 @@ def test_initial_estimators_tied_norms_and_large_block():
         assert rel_sigma(S2, gsscm_lr(Z)) < 1e-12
 
 
+@pytest.mark.parametrize("cfg,n", [(4, 20_000), (3, 65_536), (4, 100_000)])
+def test_initial_estimators_one_pass(cfg, n):
+    """Blocks the TMA moment pass takes (p >= 8, m % 16 == 0, m >= 8192): S~1 and S~2 from one read of
+    Z (MOM_WRAPXI: some warps accumulate the wrapped moments, the others the xi-weighted ones, norms and
+    cut-offs computed first)."""
+    d, Z = _zblock(cfg, n)
+    S1, S2, ok = api.initial(_cuda(Z))
+    assert ok
+    assert rel_sigma(S1, wrapped_covariance(Z)) < 1e-12
+    assert rel_sigma(S2, gsscm_lr(Z)) < 1e-12
+
+
 @pytest.mark.parametrize("cfg,n", [(1, 1000), (2, 20_000), (3, 30_001), (4, 12_345), (5, 20_000)])
 def test_refinement(cfg, n):
     d, Z = _zblock(cfg, n)
