@@ -34,12 +34,11 @@ static constexpr int LD = RTD_MAXP + 1;
 // column and no dependent chain longer than one FMA (the left-looking form had a length-j dot product
 // on one thread per column: ~64 us per launch at p = 40, dominated by barrier waits).
 __device__ __noinline__ bool block_cholesky(const double* A, double* L, int p, int* s_fail) {
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
   if (t == 0) *s_fail = 0;
-  for (int e = t; e < RTD_MAXP * LD; e += blockDim.x) {
-    const int i = e / LD, k = e - i * LD;
-    L[e] = (i < p && k <= i) ? A[i * LD + k] : 0.0;
-  }
+  // rows to warps, columns to lanes: no integer division in the index maps
+  for (int i = wid; i < RTD_MAXP; i += nw)
+    for (int k = lane; k < LD; k += 32) L[i * LD + k] = (i < p && k <= i) ? A[i * LD + k] : 0.0;
   __syncthreads();
   bool ok = true;
   for (int j = 0; j < p; j++) {
@@ -53,13 +52,9 @@ __device__ __noinline__ bool block_cholesky(const double* A, double* L, int p, i
     if (t == 0) L[j * LD + j] = r;
     for (int i = j + 1 + t; i < p; i += blockDim.x) L[i * LD + j] /= r;
     __syncthreads();
-    const int nr = p - j - 1;
-    for (int e = t; e < nr * nr; e += blockDim.x) {
-      const int ii = e / nr, kk = e - ii * nr;
-      if (kk <= ii) {
-        const int i = j + 1 + ii, k = j + 1 + kk;
-        L[i * LD + k] = fma(-L[i * LD + j], L[k * LD + j], L[i * LD + k]);
-      }
+    for (int i = j + 1 + wid; i < p; i += nw) {
+      const double lij = L[i * LD + j];
+      for (int k = j + 1 + lane; k <= i; k += 32) L[i * LD + k] = fma(-lij, L[k * LD + j], L[i * LD + k]);
     }
     __syncthreads();
   }
@@ -71,19 +66,16 @@ __device__ __noinline__ bool block_cholesky(const double* A, double* L, int p, i
 // Li = L^-1 (lower triangular): row-wise forward substitution L X = I, right-looking -- row k of X
 // is final once divided by L_kk, then its contribution is removed from the rows below in parallel.
 __device__ __noinline__ void block_tri_inverse(const double* L, double* Li, int p) {
-  const int t = threadIdx.x;
-  for (int e = t; e < RTD_MAXP * LD; e += blockDim.x) {
-    const int i = e / LD, k = e - i * LD;
-    Li[e] = (i == k && i < p) ? 1.0 : 0.0;
-  }
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  for (int i = wid; i < RTD_MAXP; i += nw)
+    for (int k = lane; k < LD; k += 32) Li[i * LD + k] = (i == k && i < p) ? 1.0 : 0.0;
   __syncthreads();
   for (int k = 0; k < p; k++) {
     for (int c = t; c <= k; c += blockDim.x) Li[k * LD + c] /= L[k * LD + k];
     __syncthreads();
-    const int nr = p - k - 1, nc = k + 1;
-    for (int e = t; e < nr * nc; e += blockDim.x) {
-      const int i = k + 1 + e / nc, c = e % nc;
-      Li[i * LD + c] = fma(-L[i * LD + k], Li[k * LD + c], Li[i * LD + c]);
+    for (int i = k + 1 + wid; i < p; i += nw) {
+      const double lik = L[i * LD + k];
+      for (int c = lane; c <= k; c += 32) Li[i * LD + c] = fma(-lik, Li[k * LD + c], Li[i * LD + c]);
     }
     __syncthreads();
   }
@@ -105,13 +97,14 @@ __device__ __noinline__ double block_max_colsum_abs(const double* A, int p, doub
 
 // Sigma^-1 = Li^T Li into B
 __device__ __noinline__ void block_inv_from_li(const double* Li, double* B, int p) {
-  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
-    int i = e / p, j = e - i * p;
-    int k0 = i > j ? i : j;
-    double s = 0.0;
-    for (int k = k0; k < p; k++) s += Li[k * LD + i] * Li[k * LD + j];
-    B[i * LD + j] = s;
-  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = wid; i < p; i += nw)
+    for (int j = lane; j < p; j += 32) {
+      const int k0 = i > j ? i : j;
+      double s = 0.0;
+      for (int k = k0; k < p; k++) s += Li[k * LD + i] * Li[k * LD + j];
+      B[i * LD + j] = s;
+    }
   __syncthreads();
 }
 

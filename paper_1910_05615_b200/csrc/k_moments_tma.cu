@@ -49,14 +49,17 @@ __device__ __forceinline__ double psi_wrap(double z) {  // PAPER.md:478-486, con
 
 __device__ __forceinline__ void consumer_sync() { __syncthreads(); }
 
-template <int P>
+// W = 8: two CTAs of 8 warps per SM, a 96 KB ring each; W = 16: one CTA of 16 warps per SM, a 192 KB ring
+// (the producer runs twice as far ahead of the slowest warp)
+template <int P, int W = 8>
 struct MomTmaCfg {
-  static constexpr int NCW = 8;                  // warps (lane 0 of warp 0 also issues the TMA loads)
+  static constexpr int NCW = W;                  // warps (lane 0 of warp 0 also issues the TMA loads)
+  static constexpr int CPS = 16 / W;             // CTAs per SM
   static constexpr int TR = 100;                 // rows per tile: 4 (mod 16) doubles, 25 groups of 4 rows
   static constexpr int G = TR / 4;
   static constexpr int TILE = TR * P;
   static constexpr int STG = (TILE + 15) / 16 * 16;
-  static constexpr int NS = std::max(3, std::min(8, (96 * 1024) / (STG * 8)));  // two CTAs per SM
+  static constexpr int NS = std::max(3, std::min(8, (96 * 1024 * (W / 8)) / (STG * 8)));
   static constexpr int NP = P + P * (P + 1) / 2 + 1;
   static constexpr size_t RING = (size_t)NS * STG * 8;
   static constexpr size_t RED = (size_t)NCW * NP * 8;  // epilogue: per-warp sums (reuses the ring)
@@ -70,10 +73,10 @@ struct MomTmaCfg {
 
 }  // namespace
 
-template <int P, int MODE>
-__global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
+template <int P, int MODE, int W>
+__global__ void __launch_bounds__(W * 32, 16 / W)
     k_moments_tma(const __grid_constant__ CUtensorMap zmap, const __grid_constant__ CUtensorMap wmap, MomArgs a) {
-  using C = MomTmaCfg<P>;
+  using C = MomTmaCfg<P, W>;
   constexpr int NB = (P + 7) / 8, NBLK = NB * (NB + 1) / 2, NCW = C::NCW, TR = C::TR, G = C::G, NS = C::NS,
                 STG = C::STG, NP = C::NP;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -143,9 +146,10 @@ __global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
   // role deals the CTA's ntile * G groups round-robin across tiles: group l of tile k, then l + NWR
   // (carried into the next tile), so no warp idles at a tile boundary although a tile holds an odd
   // number (25) of groups
-  const bool wrap_role = MODE == MOM_WRAP || (FX && warp < a.split);
-  const int NWR = FX ? (wrap_role ? a.split : NCW - a.split) : NCW;
-  const int wr = FX ? (wrap_role ? warp : warp - a.split) : warp;
+  const int split = a.split * (W / 8);  // a.split counts eighths of the CTA's warps
+  const bool wrap_role = MODE == MOM_WRAP || (FX && warp < split);
+  const int NWR = FX ? (wrap_role ? split : NCW - split) : NCW;
+  const int wr = FX ? (wrap_role ? warp : warp - split) : warp;
   double* scr = scratch + warp * (5 * 32);  // wrapped moments: per-warp list of tanh-branch arguments
   int cur = -1;  // tile whose full barrier this warp has passed
   for (int k = 0, l = wr; k < ntile; l = (l + NWR >= G) ? (k++, l + NWR - G) : l + NWR) {
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
   }
   consumer_sync();
   const long long po = ((long long)slot * a.ctas + blockIdx.x) * NP;
-  const int q1 = FX ? a.split : NCW;  // warps [0, q1) -> partial, [q1, NCW) -> partial2 (fixed order)
+  const int q1 = FX ? split : NCW;  // warps [0, q1) -> partial, [q1, NCW) -> partial2 (fixed order)
   for (int e = threadIdx.x; e < NP; e += NCW * 32) {
     double v = 0.0;
     for (int q = 0; q < q1; q++) v += red[q * NP + e];
@@ -304,9 +308,9 @@ __global__ void __launch_bounds__(MomTmaCfg<P>::NCW * 32, 2)
 
 namespace {
 
-template <int P>
-void moments_tma_p(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
-  using C = MomTmaCfg<P>;
+template <int P, int W>
+void moments_tma_pw(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
+  using C = MomTmaCfg<P, W>;
   CUtensorMap map;  // blocks addressed by the 3rd coordinate: a.nblk_hint blocks of m x p doubles at a.Z
   if (!encode_blocks(&map, a.Z, a.m, P, a.nblk_hint, C::TR))
     throw std::string("cuTensorMapEncodeTiled failed for the moment pass");
@@ -319,8 +323,8 @@ void moments_tma_p(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
   dim3 grid(a.ctas, ninst);
 #define RTD_MT_CASE(M)                                                                                        \
   case M:                                                                                                     \
-    RTD_CU(cudaFuncSetAttribute(k_moments_tma<P, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM)); \
-    k_moments_tma<P, M><<<grid, C::NCW * 32, C::SMEM, st>>>(map, wmap, a);                                   \
+    RTD_CU(cudaFuncSetAttribute(k_moments_tma<P, M, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM)); \
+    k_moments_tma<P, M, W><<<grid, C::NCW * 32, C::SMEM, st>>>(map, wmap, a);                                   \
     break;
   switch (mode) {
     RTD_MT_CASE(MOM_WRAP)
@@ -333,11 +337,18 @@ void moments_tma_p(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
 #undef RTD_MT_CASE
 }
 
+// W = 16 (one CTA of 16 warps and a 192 KB ring per SM) measured slower on config 4 (wrapped + xi pass
+// 1.94 -> 1.98 ms, member moments 1.36 -> 1.52 ms): two CTAs of 8 warps
+template <int P>
+void moments_tma_p(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
+  moments_tma_pw<P, 8>(mode, a, ninst, st);
+}
+
 }  // namespace
 
 bool moments_tma_supported(int mode, const MomArgs& a) {
   static const bool off = getenv("RTD_MOM_NOTMA") != nullptr;
-  if (mode == MOM_WRAPXI && (a.partial2 == nullptr || a.split < 1 || a.split >= MomTmaCfg<8>::NCW || a.r == nullptr))
+  if (mode == MOM_WRAPXI && (a.partial2 == nullptr || a.split < 1 || a.split >= 8 || a.r == nullptr))
     return false;
   return !off && mode != MOM_DELTA && a.p >= 8 && a.p <= RTD_MAXP && a.m % 16 == 0 && a.m >= 8192 &&
          a.blk_stride == (long long)a.p * a.m && a.nblk_hint > 0 &&

@@ -164,7 +164,7 @@ struct MomArgs {
   int nblk_hint;            // blocks of m x p doubles at Z (the TMA-fed dense passes map them; 0: unknown)
   int ninst_hint;           // instances the per-instance arrays (mem_new, d2) hold (0: unknown)
   double* partial2;         // MOM_WRAPXI: [slot][cta][NP] partials of the xi-weighted moments
-  int split;                // MOM_WRAPXI: warps on the wrapped moments (the rest: xi-weighted)
+  int split;                // MOM_WRAPXI: eighths of the CTA's warps on the wrapped moments (the rest: xi-weighted)
 };
 int mom_np(int p);  // p + p(p+1)/2 + 1
 void launch_moments(int mode, const MomArgs& a, int ninst, cudaStream_t st);
