@@ -152,6 +152,11 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
   const int wr = FX ? (wrap_role ? warp : warp - split) : warp;
   double* scr = scratch + warp * (5 * 32);  // wrapped moments: per-warp list of tanh-branch arguments
   int cur = -1;  // tile whose full barrier this warp has passed
+  // MOM_MEMBER: the membership byte of the warp's next group is loaded one group ahead (an L2 round trip
+  // per group otherwise stalls the warp before every group)
+  unsigned int mb_next = 0u;
+  if (MODE == MOM_MEMBER && wr < G && r_begin + 4 * wr + t < r_end)
+    mb_next = a.mem_new[(long long)id * m + r_begin + 4 * wr + t];
   for (int k = 0, l = wr; k < ntile; l = (l + NWR >= G) ? (k++, l + NWR - G) : l + NWR) {
     while (cur < k) {  // release the tile left behind, enter the next one
       if (cur >= 0) {
@@ -169,6 +174,13 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
       nxt++;
     }
     const long long row = r_begin + (long long)k * TR + 4 * l + t;
+    unsigned int mb = 0u;
+    if (MODE == MOM_MEMBER) {
+      mb = mb_next;
+      const int l2 = l + NWR >= G ? l + NWR - G : l + NWR, k2 = l + NWR >= G ? k + 1 : k;
+      const long long row2 = r_begin + (long long)k2 * TR + 4 * l2 + t;
+      mb_next = (k2 < ntile && row2 < r_end) ? a.mem_new[(long long)id * m + row2] : 0u;
+    }
     double w = 0.0;
     if (row < r_end) {
       const unsigned char* ws = wsrc + (k % NS) * C::WST;
@@ -180,7 +192,7 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
         w = __dmul_rn(xi, xi);
       } else if (MODE == MOM_MEMBER) {  // membership bytes from global memory (a UINT8 2-D TMA map of them
         // faulted with an illegal instruction on this stack; the bytes are L2-resident)
-        w = (double)a.mem_new[(long long)id * m + row];
+        w = (double)mb;
       } else {
         w = reinterpret_cast<const double*>(ws)[4 * l + t] <= a.c2 ? 1.0 : 0.0;
       }
