@@ -249,45 +249,50 @@ __global__ void __launch_bounds__(PT, 5) k_pr_hist(const double* __restrict__ co
   double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;  // end-bucket sums and sums of magnitudes
   const long long per = (len + gridDim.x - 1) / gridDim.x;
   const long long i0 = blockIdx.x * per, i1 = min(len, i0 + per);
-  for (long long base = i0 + threadIdx.x; base < i1; base += (long long)PT * ILP) {
-    double v[ILP];
-    const int rem = (int)min(i1 - base, (long long)PT * ILP);  // elements k with k PT < rem are in range
-#pragma unroll
-    for (int k = 0; k < ILP; k++) v[k] = k * PT < rem ? __ldg(y + base + k * PT) : 0.0;
-#pragma unroll
-    for (int k = 0; k < ILP; k++) {
-      if (k * PT < rem) {
-        // bucket_of and the offset in one product: T = floor(2^16 t), t = fl(fl(y - lo) inv_w), so
-        // b = 1 + floor(t) = 1 + (T >> 16) and q = floor(2^16 frac(t)) = T & 0xffff.  The column min /
-        // max only bound the end buckets' values (bucket_lo(0), bucket_hi(NBK - 1)): tracked there only
-        const double x = v[k];
-        int b;
-        unsigned int q = 0u;
-        if (x < c.lo) {
-          b = 0;
-          const double xs = __dsub_rn(x, c.cs);  // shifted (k_pr_locate): one more rounding per term
-          e0 += xs;
-          a0 += fabs(xs);
-          kmin = min(kmin, ord_key(x));
-        } else if (x >= c.hi) {
-          b = NBK - 1;
-          const double xs = __dsub_rn(x, c.cs);
-          e1 += xs;
-          a1 += fabs(xs);
-          kmax = max(kmax, ord_key(x));
-        } else {
-          const int T = (int)__dmul_rn(__dsub_rn(x, c.lo), c.inv_w16);
-          b = 1 + (T >> 16);
-          q = (unsigned int)(T & 0xffff);
-          if (b > NBK - 2) {
-            b = NBK - 2;
-            q = 65535u;
-          }
-          atomicAdd(&hq[b], q);
-        }
-        atomicAdd(&hc[b], 1u);
+  // bucket_of and the offset in one product: T = floor(2^16 t), t = fl(fl(y - lo) inv_w), so
+  // b = 1 + floor(t) = 1 + (T >> 16) and q = floor(2^16 frac(t)) = T & 0xffff.  The column min /
+  // max only bound the end buckets' values (bucket_lo(0), bucket_hi(NBK - 1)): tracked there only
+  auto consume = [&](const double x) {
+    int b;
+    if (x < c.lo) {
+      b = 0;
+      const double xs = __dsub_rn(x, c.cs);  // shifted (k_pr_locate): one more rounding per term
+      e0 += xs;
+      a0 += fabs(xs);
+      kmin = min(kmin, ord_key(x));
+    } else if (x >= c.hi) {
+      b = NBK - 1;
+      const double xs = __dsub_rn(x, c.cs);
+      e1 += xs;
+      a1 += fabs(xs);
+      kmax = max(kmax, ord_key(x));
+    } else {
+      const int T = (int)__dmul_rn(__dsub_rn(x, c.lo), c.inv_w16);
+      b = 1 + (T >> 16);
+      unsigned int q = (unsigned int)(T & 0xffff);
+      if (b > NBK - 2) {
+        b = NBK - 2;
+        q = 65535u;
       }
+      atomicAdd(&hq[b], q);
     }
+    atomicAdd(&hc[b], 1u);
+  };
+  // full tiles of ILP loads per thread without bounds tests, then one predicated tail tile
+  const long long nfull = (i1 - i0) / ((long long)PT * ILP);
+  const double* yp = y + i0 + threadIdx.x;
+  for (long long it = 0; it < nfull; it++, yp += (long long)PT * ILP) {
+    double v[ILP];
+#pragma unroll
+    for (int k = 0; k < ILP; k++) v[k] = __ldg(yp + k * PT);
+#pragma unroll
+    for (int k = 0; k < ILP; k++) consume(v[k]);
+  }
+  {
+    const long long base = i0 + nfull * (long long)PT * ILP + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < ILP; k++)
+      if (base + k * PT < i1) consume(__ldg(y + base + k * PT));
   }
   for (int d = 16; d > 0; d >>= 1) {
     kmin = min(kmin, __shfl_down_sync(0xffffffffu, kmin, d));
