@@ -81,6 +81,51 @@ __device__ __noinline__ void block_tri_inverse(const double* L, double* Li, int 
   }
 }
 
+// Cholesky Sigma = L L^T and Li = L^-1 in ONE right-looking loop (same quantities as block_cholesky +
+// block_tri_inverse): at step j the pivot r = sqrt(L_jj) is read by every thread (a uniform decision), column j
+// of L and row j of Li (final after the earlier steps) are scaled by 1 / r, then the trailing triangle of L
+// and the rows below j of Li are updated in one phase -- two barriers per step instead of five, the
+// reciprocal computed once per thread instead of a division per element.  r is kept in rd[] until the loop
+// ends (the pivot entry is read unsynchronised at the top of the step).
+__device__ __noinline__ bool block_chol_inv(const double* A, double* L, double* Li, double* rd, int p, int* s_fail) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  if (t == 0) *s_fail = 0;
+  for (int i = wid; i < RTD_MAXP; i += nw)
+    for (int k = lane; k < LD; k += 32) {
+      L[i * LD + k] = (i < p && k <= i) ? A[i * LD + k] : 0.0;
+      Li[i * LD + k] = (i == k && i < p) ? 1.0 : 0.0;
+    }
+  __syncthreads();
+  bool ok = true;
+  for (int j = 0; j < p; j++) {
+    const double d = L[j * LD + j];
+    if (!(d > 0.0) || !isfinite(d)) {
+      ok = false;
+      break;
+    }
+    const double r = sqrt(d), ri = 1.0 / r;
+    if (t == 0) rd[j] = r;
+    for (int e = t; e < p; e += blockDim.x) {
+      if (e > j) L[e * LD + j] *= ri;        // column j of L below the pivot
+      else Li[j * LD + e] *= ri;             // row j of Li (columns 0..j)
+    }
+    __syncthreads();
+    for (int i = j + 1 + wid; i < p; i += nw) {
+      const double lij = L[i * LD + j];
+      for (int k = lane; k <= i; k += 32) {
+        if (k <= j) Li[i * LD + k] = fma(-lij, Li[j * LD + k], Li[i * LD + k]);
+        else L[i * LD + k] = fma(-lij, L[k * LD + j], L[i * LD + k]);
+      }
+    }
+    __syncthreads();
+  }
+  if (ok)
+    for (int j = t; j < p; j += blockDim.x) L[j * LD + j] = rd[j];
+  if (!ok && t == 0) *s_fail = 1;
+  __syncthreads();
+  return ok;
+}
+
 __device__ __noinline__ double block_max_colsum_abs(const double* A, int p, double* red) {
   const int t = threadIdx.x;
   if (t < p) {
@@ -125,19 +170,20 @@ __global__ void __launch_bounds__(512) k_prepare(const int* __restrict__ inst, c
   const double* sg = sigma_all + (long long)id * RTD_MAXP * RTD_MAXP;
   for (int e = t; e < p * p; e += blockDim.x) A[(e / p) * LD + e % p] = sg[e];
   __syncthreads();
-  const bool ok = block_cholesky(A, L, p, &s_fail);
+  const bool ok = block_chol_inv(A, L, Li, red, p, &s_fail);
   if (!ok) {
     if (t == 0 && status_out) status_out[id] = ST_NOT_PD;
     return;
   }
-  block_tri_inverse(L, Li, p);
   const double n1 = block_max_colsum_abs(A, p, red);
   block_inv_from_li(Li, A, p);  // A <- Sigma^-1
   const double n1i = block_max_colsum_abs(A, p, red);
   const double kappa = n1 * n1i;
+  if (t < p) red[t] = log(L[t * LD + t]);  // the logs in parallel, summed in row order by thread 0
+  __syncthreads();
   if (t == 0) {
     double ld = 0.0;
-    for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
+    for (int j = 0; j < p; j++) ld += red[j];
     ld *= 2.0;
     if (logdet_out) logdet_out[id] = ld;
     if (cond_out) cond_out[id] = kappa;
@@ -150,13 +196,10 @@ __global__ void __launch_bounds__(512) k_prepare(const int* __restrict__ inst, c
     for (int k = t; k < p; k += blockDim.x) cs[k] = mu[k];
     if (full_inverse) {  // [mu | Sigma^-1 row-major]: variant I of Table 1 (distances by the inverse)
       for (int e = t; e < p * p; e += blockDim.x) cs[p + e] = A[(e / p) * LD + e % p];
-    } else {             // [mu | L^-1 packed lower]: §3.4 (distances by the Cholesky factor)
-      for (int e = t; e < p * (p + 1) / 2; e += blockDim.x) {
-        int j = 0;
-        while ((j + 1) * (j + 2) / 2 <= e) j++;
-        int k = e - j * (j + 1) / 2;
-        cs[p + e] = Li[j * LD + k];
-      }
+    } else {             // [mu | L^-1 packed lower]: §3.4 (distances by the Cholesky factor); row j per warp
+      const int lane = t & 31, nw = blockDim.x >> 5;
+      for (int j = t >> 5; j < p; j += nw)
+        for (int k = lane; k <= j; k += 32) cs[p + j * (j + 1) / 2 + k] = Li[j * LD + k];
     }
   }
 }
@@ -218,11 +261,10 @@ __global__ void __launch_bounds__(CS_T, 1) k_csteps_small(const double* __restri
     // ---- factor: Cholesky, condition monitor, log det (k_prepare)
     for (int e = t; e < p * p; e += CS_T) A[(e / p) * LD + e % p] = sg_s[e];
     __syncthreads();
-    if (!block_cholesky(A, L, p, &s_fail)) {
+    if (!block_chol_inv(A, L, Li, red, p, &s_fail)) {
       if (t == 0) s_stat = ST_NOT_PD;
       break;
     }
-    block_tri_inverse(L, Li, p);
     const double n1 = block_max_colsum_abs(A, p, red);
     block_inv_from_li(Li, A, p);
     const double kappa = n1 * block_max_colsum_abs(A, p, red);
@@ -547,11 +589,10 @@ __global__ void __cluster_dims__(CSC_CL, 1, 1) __launch_bounds__(CS_T, 1)
     // ---- factor (every CTA, identical)
     for (int e = t; e < p * p; e += CS_T) A[(e / p) * LD + e % p] = sg_s[e];
     __syncthreads();
-    if (!block_cholesky(A, L, p, &s_fail)) {
+    if (!block_chol_inv(A, L, Li, red, p, &s_fail)) {
       if (t == 0) s_stat = ST_NOT_PD;
       break;
     }
-    block_tri_inverse(L, Li, p);
     const double n1 = block_max_colsum_abs(A, p, red);
     block_inv_from_li(Li, A, p);
     const double kappa = n1 * block_max_colsum_abs(A, p, red);
@@ -1286,9 +1327,138 @@ __global__ void __launch_bounds__(LT) k_jacobi(const double* __restrict__ A_all,
   }
 }
 
+// One-sided (Hestenes) Jacobi for the symmetric positive semi-definite inputs (S~1, S~2, Sigma_k: Gram
+// matrices): the columns of A are rotated in place, A <- A J, V <- V J, until every pair is orthogonal to
+// |a_P . a_Q| <= tol ||a_P|| ||a_Q||; then A V = V diag(lambda) and lambda_j = v_j . a_j (the
+// eigenvectors of the initial estimates).  One warp per pair of the round-robin schedule computes the pair's
+// three dot products (butterfly shuffles: every lane holds the same sums), the rotation in registers and
+// the two column updates, so a round is one barrier and one chain of slow fp64 operations (the two-sided
+// form needed four barriers and a shared-memory hand-off of (c, s) per round: 0.83 ms for the 16 40 x 40
+// matrices of config 4, 57 us for config 5's two 8 x 8).
+static constexpr int JCS = 64;  // column stride of the column-major copies (rows lane and lane + 32)
+__global__ void __launch_bounds__(32 * (RTD_MAXP / 2)) k_jacobi_os(const double* __restrict__ A_all, int p,
+                                                                   double kappa_max, double* __restrict__ V_all,
+                                                                   double* __restrict__ lam_all,
+                                                                   int* __restrict__ ok_all) {
+  __shared__ double Ac[RTD_MAXP][JCS], Vc[RTD_MAXP][JCS];
+  __shared__ double lam_s[RTD_MAXP];
+  __shared__ int order[RTD_MAXP];
+  __shared__ int s_rot[3];
+  const int b = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+  const double* Ain = A_all + (long long)b * RTD_MAXP * RTD_MAXP;
+  for (int j = w; j < RTD_MAXP; j += nw)
+    for (int i = lane; i < JCS; i += 32) {
+      const bool in = i < p && j < p;
+      Ac[j][i] = in ? 0.5 * (Ain[i * p + j] + Ain[j * p + i]) : 0.0;
+      Vc[j][i] = (in && i == j) ? 1.0 : 0.0;
+    }
+  if (t < 3) s_rot[t] = 0;
+  const int n2 = p + (p & 1);
+  constexpr double tol = 1e-15;
+  __syncthreads();
+  for (int sweep = 0; sweep < 60; sweep++) {
+    const int fs = sweep % 3;
+    if (t == 0) s_rot[(sweep + 1) % 3] = 0;  // the next sweep's flag (triple-buffered: no reader races)
+    for (int round = 0; round < n2 - 1; round++) {
+      if (w < n2 / 2) {
+        auto ord = [&](int k) { return k == 0 ? 0 : 1 + ((k - 1 - round) % (n2 - 1) + (n2 - 1)) % (n2 - 1); };
+        int P = ord(w), Q = ord(n2 - 1 - w);
+        if (P > Q) { const int tmp = P; P = Q; Q = tmp; }
+        if (Q < p) {
+          double aP0 = Ac[P][lane], aP1 = Ac[P][lane + 32], aQ0 = Ac[Q][lane], aQ1 = Ac[Q][lane + 32];
+          double al = fma(aP0, aP0, aP1 * aP1), be = fma(aQ0, aQ0, aQ1 * aQ1), ga = fma(aP0, aQ0, aP1 * aQ1);
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            al += __shfl_xor_sync(0xffffffffu, al, d);
+            be += __shfl_xor_sync(0xffffffffu, be, d);
+            ga += __shfl_xor_sync(0xffffffffu, ga, d);
+          }
+          if (ga != 0.0 && ga * ga > tol * tol * al * be) {
+            // zeta = (be - al) / (2 ga), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)) written without the first
+            // division: t = sign(h ga) |ga| / (|h| + sqrt(h^2 + ga^2)), h = (be - al) / 2; c = rsqrt(1 + t^2)
+            const double hh = 0.5 * (be - al);
+            const bool pos = hh == 0.0 || ((hh > 0.0) == (ga > 0.0));
+            const double tt = (pos ? fabs(ga) : -fabs(ga)) / (fabs(hh) + sqrt(fma(hh, hh, ga * ga)));
+            const double c = rsqrt(fma(tt, tt, 1.0)), s = tt * c;
+            Ac[P][lane] = c * aP0 - s * aQ0;
+            Ac[Q][lane] = s * aP0 + c * aQ0;
+            Ac[P][lane + 32] = c * aP1 - s * aQ1;
+            Ac[Q][lane + 32] = s * aP1 + c * aQ1;
+            const double vP0 = Vc[P][lane], vP1 = Vc[P][lane + 32], vQ0 = Vc[Q][lane], vQ1 = Vc[Q][lane + 32];
+            Vc[P][lane] = c * vP0 - s * vQ0;
+            Vc[Q][lane] = s * vP0 + c * vQ0;
+            Vc[P][lane + 32] = c * vP1 - s * vQ1;
+            Vc[Q][lane + 32] = s * vP1 + c * vQ1;
+            if (lane == 0) s_rot[fs] = 1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (!s_rot[fs]) break;  // a sweep without a rotation: converged
+  }
+  // lambda_j = v_j . (A v_j), the rotated column a_j = A v_j (one warp per column)
+  for (int j = w; j < p; j += nw) {
+    double v = fma(Vc[j][lane], Ac[j][lane], Vc[j][lane + 32] * Ac[j][lane + 32]);
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (lane == 0) lam_s[j] = v;
+  }
+  __syncthreads();
+  // sort eigenvalues descending (stable), normalise signs (largest |component| positive)
+  if (t == 0) {
+    int idx[RTD_MAXP];
+    for (int k = 0; k < p; k++) idx[k] = k;
+    for (int i = 1; i < p; i++) {
+      const int v = idx[i];
+      int j = i - 1;
+      while (j >= 0 && lam_s[idx[j]] < lam_s[v]) {
+        idx[j + 1] = idx[j];
+        j--;
+      }
+      idx[j + 1] = v;
+    }
+    for (int k = 0; k < p; k++) order[k] = idx[k];
+    const double lmax = lam_s[idx[0]], lmin = lam_s[idx[p - 1]];
+    ok_all[b] = (lmin > 0.0 && lmax / lmin <= kappa_max) ? 1 : 0;
+  }
+  __syncthreads();
+  double* Vo = V_all + (long long)b * RTD_MAXP * RTD_MAXP;
+  double* lo = lam_all + (long long)b * RTD_MAXP;
+  for (int k = w; k < p; k += nw) {  // output column k = eigenvector order[k]
+    const int src = order[k];
+    const double x0 = Vc[src][lane], x1 = lane + 32 < p ? Vc[src][lane + 32] : 0.0;
+    // row index of the largest |component| (lowest row on ties, as the serial scan)
+    double vm = fabs(x0);
+    int km = lane < p ? lane : RTD_MAXP;
+    if (lane + 32 < p && fabs(x1) > vm) {
+      vm = fabs(x1);
+      km = lane + 32;
+    }
+    if (lane >= p) vm = -1.0;
+    for (int d = 16; d > 0; d >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, vm, d);
+      const int ok = __shfl_xor_sync(0xffffffffu, km, d);
+      if (ov > vm || (ov == vm && ok < km)) {
+        vm = ov;
+        km = ok;
+      }
+    }
+    const double sg = Vc[src][km] < 0 ? -1.0 : 1.0;
+    if (lane < p) Vo[lane * p + k] = sg * x0;
+    if (lane + 32 < p) Vo[(lane + 32) * p + k] = sg * x1;
+    if (lane == 0) lo[k] = lam_s[src];
+  }
+}
+
 void launch_jacobi(const double* A_all, int nb, int p, double kappa_max, double* V_all, double* lam_all, int* ok_all,
                    cudaStream_t st) {
-  k_jacobi<<<nb, LT, 0, st>>>(A_all, p, kappa_max, V_all, lam_all, ok_all);
+  static const bool two_sided = getenv("RTD_JACOBI_TWOSIDED") != nullptr;
+  if (two_sided) {
+    k_jacobi<<<nb, LT, 0, st>>>(A_all, p, kappa_max, V_all, lam_all, ok_all);
+  } else {
+    const int npr = std::max(1, (p + (p & 1)) / 2);
+    k_jacobi_os<<<nb, 32 * npr, 0, st>>>(A_all, p, kappa_max, V_all, lam_all, ok_all);
+  }
   RTD_LAUNCHED();
 }
 

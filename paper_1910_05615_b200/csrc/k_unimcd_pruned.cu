@@ -1275,13 +1275,21 @@ __device__ __forceinline__ void reweighted_from_shifted(const UniConst& uc, cons
   if (!(var > 0.0)) o.status = 1;
 }
 
-// 6. reweighting sums over kept points (fixed-order per-CTA partials)
+// a column whose reweighting sums were taken by the fused gather pass (kfused, band within BCAP)
+__device__ __forceinline__ bool col_fused(const PrunedCol* pc, const int* bcount, int col) {
+  return pc != nullptr && pc[col].kfused && bcount[col] <= BCAP;
+}
+
+// 6. reweighting sums over kept points (fixed-order per-CTA partials).  pc != nullptr: the gather pass ran
+//    fused, and only the columns it could not take (col_fused false) are summed here
 __global__ void __launch_bounds__(PT) k_pr_keep(const double* __restrict__ cols, long long len, UniConst uc,
                                                 const UniOut* __restrict__ out, dd2* __restrict__ part,
-                                                long long* __restrict__ kcnt) {
+                                                long long* __restrict__ kcnt, const PrunedCol* __restrict__ pc,
+                                                const int* __restrict__ bcount) {
   __shared__ dd2 sm[33];
   __shared__ long long kc[PT / 32];
   const int col = blockIdx.y;
+  if (col_fused(pc, bcount, col)) return;
   const UniOut o = out[col];
   const double* y = cols + (long long)col * len;
   const double loc0 = o.raw_loc, thresh = uc.q1 * o.var0;
@@ -1326,9 +1334,9 @@ __global__ void __launch_bounds__(PT) k_pr_keep(const double* __restrict__ cols,
 }
 
 __global__ void k_pr_final(UniConst uc, int npc, const dd2* __restrict__ part, const long long* __restrict__ kcnt,
-                           UniOut* __restrict__ out) {
+                           UniOut* __restrict__ out, const PrunedCol* __restrict__ pc, const int* __restrict__ bcount) {
   const int col = blockIdx.x;
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x != 0 || col_fused(pc, bcount, col)) return;
   UniOut o = out[col];
   dd2 K = dd2_zero();
   long long k = 0;
@@ -1350,6 +1358,7 @@ __global__ void __launch_bounds__(PT) k_pr_final_fused(UniConst uc, int npc, con
   __shared__ dd2 sm[33];
   __shared__ long long kred[PT / 32];
   const int col = blockIdx.x;
+  if (!col_fused(pc, bcount, col)) return;  // summed by k_pr_keep / k_pr_final
   const PrunedCol c = pc[col];
   UniOut o = out[col];
   const double loc0 = o.raw_loc, thresh = uc.q1 * o.var0;
@@ -1469,9 +1478,11 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   std::vector<int> gc(2 * ncols), bc(ncols);
   fetch(st, {{hc.data(), s.pc, ncols * sizeof(PrunedCol)}, {gc.data(), s.gcount, 2 * ncols * sizeof(int)},
              {bc.data(), s.bcount, ncols * sizeof(int)}});
-  bool fused = !no_fused;
+  // columns whose bounds were too loose for the fused sums (kfused = 0: e.g. a flat or bimodal projection
+  // with a wide candidate range) get the separate keep pass; the others finish from the gather's sums
+  int nfused = 0;
   for (int j = 0; j < ncols; j++)
-    if (!hc[j].kfused || bc[j] > BCAP) fused = false;
+    if (!no_fused && hc[j].kfused && bc[j] <= BCAP) nfused++;
   static const bool dbg = getenv("RTD_DEBUG_PRUNED") != nullptr;
   if (dbg) {
     for (int j = 0; j < ncols; j++)
@@ -1518,15 +1529,17 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
   RTD_LAUNCHED();
   k_pr_raw<<<ncols, 32, 0, st>>>(h, s.pc, s.pref, s.part, s.nch, uc, out_dev);
   RTD_LAUNCHED();
-  if (fused) {
+  if (nfused > 0) {
     k_pr_final_fused<<<ncols, PT, 0, st>>>(uc, npc, s.pc, s.kpart, s.kcnt, s.band, s.bcount, out_dev);
     RTD_LAUNCHED();
-    return true;
   }
-  k_pr_keep<<<dim3(npc, ncols), PT, 0, st>>>(cols, len, uc, out_dev, s.kpart, s.kcnt);
-  RTD_LAUNCHED();
-  k_pr_final<<<ncols, 32, 0, st>>>(uc, npc, s.kpart, s.kcnt, out_dev);
-  RTD_LAUNCHED();
+  if (nfused < ncols) {  // the fused columns' CTAs exit at once
+    const PrunedCol* fpc = no_fused ? nullptr : s.pc;
+    k_pr_keep<<<dim3(npc, ncols), PT, 0, st>>>(cols, len, uc, out_dev, s.kpart, s.kcnt, fpc, s.bcount);
+    RTD_LAUNCHED();
+    k_pr_final<<<ncols, 32, 0, st>>>(uc, npc, s.kpart, s.kcnt, out_dev, fpc, s.bcount);
+    RTD_LAUNCHED();
+  }
   return true;
 }
 
