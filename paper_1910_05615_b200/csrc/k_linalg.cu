@@ -103,7 +103,7 @@ __device__ __noinline__ bool block_chol_inv(const double* A, double* L, double* 
       ok = false;
       break;
     }
-    const double r = sqrt(d), ri = 1.0 / r;
+    const double ri = rsqrt(d), r = d * ri;  // one slow fp64 operation on the chain (rsqrt ~55 cycles)
     if (t == 0) rd[j] = r;
     for (int e = t; e < p; e += blockDim.x) {
       if (e > j) L[e * LD + j] *= ri;        // column j of L below the pivot
@@ -268,9 +268,11 @@ __global__ void __launch_bounds__(CS_T, 1) k_csteps_small(const double* __restri
     const double n1 = block_max_colsum_abs(A, p, red);
     block_inv_from_li(Li, A, p);
     const double kappa = n1 * block_max_colsum_abs(A, p, red);
+    if (t < p) red[t] = log(L[t * LD + t]);  // the logs in parallel (a dependent fp64 log is ~280 cycles)
+    __syncthreads();
     if (t == 0) {
       double ld = 0.0;
-      for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
+      for (int j = 0; j < p; j++) ld += red[j];
       ld *= 2.0;
       s_logdet = ld;
       if (traj) traj[(long long)id * traj_stride + step] = ld;
@@ -542,6 +544,7 @@ __device__ __forceinline__ void csc_mark(int step, int ph, bool on) {
   }
 }
 static constexpr int CSC_ROWS = 2560;                  // rows per CTA at most (m <= 20480)
+static constexpr int CSC_CAND = 64;                    // rows of the h-th key's bin resolved by counting
 
 template <int NB>
 __global__ void __cluster_dims__(CSC_CL, 1, 1) __launch_bounds__(CS_T, 1)
@@ -566,9 +569,10 @@ __global__ void __cluster_dims__(CSC_CL, 1, 1) __launch_bounds__(CS_T, 1)
   __shared__ __align__(16) unsigned int tot[4096];   // the cluster's histogram
   __shared__ unsigned int cur[CSC_ROWS / 32], prv[CSC_ROWS / 32];
   __shared__ long long wsum[CS_W];
-  __shared__ int s_fail, s_stat, s_found, s_done, s_chg_local;
+  __shared__ int s_fail, s_stat, s_found, s_done, s_chg_local, s_ncand, s_have_prev;
   __shared__ long long s_before, s_cnt;
-  __shared__ unsigned long long s_pre_hi, s_pre_lo;
+  __shared__ unsigned long long s_pre_hi, s_pre_lo, s_cbase;
+  __shared__ unsigned __int128 cand[CSC_CAND];  // this CTA's rows of the h-th key's bin (read by the cluster)
   __shared__ double s_logdet;
   const int cr = (int)cluster.block_rank();
   const int id = inst[blockIdx.x / CSC_CL];
@@ -580,7 +584,11 @@ __global__ void __cluster_dims__(CSC_CL, 1, 1) __launch_bounds__(CS_T, 1)
   for (int e = t; e < p; e += CS_T) mu_s[e] = mu_all[(long long)id * RTD_MAXP + e];
   for (int e = t; e < p * p; e += CS_T) sg_s[e] = sigma_all[(long long)id * RTD_MAXP * RTD_MAXP + e];
   for (int w = t; w < CSC_ROWS / 32; w += CS_T) prv[w] = cur[w] = 0u;
-  if (t == 0) s_stat = ST_ACTIVE;
+  if (t == 0) {
+    s_stat = ST_ACTIVE;
+    s_have_prev = 0;
+    s_cbase = 0ull;
+  }
   __syncthreads();
   int step = 1;
   const bool prof = blockIdx.x == 0 && t == 0;
@@ -596,9 +604,11 @@ __global__ void __cluster_dims__(CSC_CL, 1, 1) __launch_bounds__(CS_T, 1)
     const double n1 = block_max_colsum_abs(A, p, red);
     block_inv_from_li(Li, A, p);
     const double kappa = n1 * block_max_colsum_abs(A, p, red);
+    if (t < p) red[t] = log(L[t * LD + t]);  // the logs in parallel (a dependent fp64 log is ~280 cycles)
+    __syncthreads();
     if (t == 0) {
       double ld = 0.0;
-      for (int j = 0; j < p; j++) ld += log(L[j * LD + j]);
+      for (int j = 0; j < p; j++) ld += red[j];
       ld *= 2.0;
       s_logdet = ld;
       if (traj && cr == 0) traj[(long long)id * traj_stride + step] = ld;
@@ -634,7 +644,13 @@ __global__ void __cluster_dims__(CSC_CL, 1, 1) __launch_bounds__(CS_T, 1)
         dyn[i - r0] = d;
       }
     }
-    // ---- exact selection of the h smallest composite keys (bits(d^2) << 32 | row) over the cluster
+    // ---- exact selection of the h smallest composite keys (bits(d^2) << 32 | row) over the cluster.
+    //      From the second step on, the first level is CENTRED on the previous step's h-th key (as
+    //      k_sel_level): its top 24 bits minus 2048 give 4094 bins of relative width 2^-12, everything below /
+    //      above in the two end bins (a miss falls back to the plain 12-bit levels).  Once the bin holding the
+    //      h-th key has at most CSC_CAND rows, the rows of that bin are collected (every CTA's few, through
+    //      DSMEM) and the h-th key is found among them by counting -- instead of further histogram levels
+    //      (each one a 4096-bin clear, two cluster barriers and 128 KB of DSMEM reads per CTA).
     if (t == 0) {
       s_pre_hi = 0ull;
       s_pre_lo = 0ull;
@@ -642,26 +658,49 @@ __global__ void __cluster_dims__(CSC_CL, 1, 1) __launch_bounds__(CS_T, 1)
       s_before = h;
     }
     int plen = 0;
+    bool centred = s_have_prev != 0;
+    const unsigned long long cbase = s_cbase;
     __syncthreads();
     csc_mark(step, 2, prof);
     while (true) {
       for (int b = t; b < 4096; b += CS_T) hist[b] = 0u;
       __syncthreads();
       const unsigned __int128 pre = ((unsigned __int128)s_pre_hi << 64) | s_pre_lo;
+      unsigned below = 0, above = 0;
       for (int i0 = 0; i0 < nl; i0 += CS_T) {
         const int il = i0 + t;
         bool take = false;
         unsigned dig = 0;
         if (il < nl) {
-          const unsigned __int128 C =
-              ((unsigned __int128)(unsigned long long)__double_as_longlong(dyn[il]) << 32) | (unsigned)(r0 + il);
-          take = plen == 0 || (C >> (96 - plen)) == pre;
-          dig = (unsigned)(C >> (96 - plen - 12)) & 4095u;
+          const unsigned long long kb = (unsigned long long)__double_as_longlong(dyn[il]);
+          if (centred) {
+            const unsigned long long top24 = kb >> 40;
+            if (top24 < cbase) below++;
+            else if (top24 >= cbase + 4094) above++;
+            else {
+              take = true;
+              dig = (unsigned)(top24 - cbase + 1);
+            }
+          } else {
+            const unsigned __int128 C = ((unsigned __int128)kb << 32) | (unsigned)(r0 + il);
+            take = plen == 0 || (C >> (96 - plen)) == pre;
+            dig = (unsigned)(C >> (96 - plen - 12)) & 4095u;
+          }
         }
         const unsigned act = __ballot_sync(0xffffffffu, take);
         if (take) {
           const unsigned same = __match_any_sync(act, dig);
           if ((__ffs(same) - 1) == lane) atomicAdd(&hist[dig], (unsigned)__popc(same));
+        }
+      }
+      if (centred) {
+        for (int d = 16; d > 0; d >>= 1) {
+          below += __shfl_down_sync(0xffffffffu, below, d);
+          above += __shfl_down_sync(0xffffffffu, above, d);
+        }
+        if (lane == 0) {
+          if (below) atomicAdd(&hist[0], below);
+          if (above) atomicAdd(&hist[4095], above);
         }
       }
       if (plen == 0) csc_mark(step, 6, prof);
@@ -715,17 +754,78 @@ __global__ void __cluster_dims__(CSC_CL, 1, 1) __launch_bounds__(CS_T, 1)
         before += c[e];
       }
       __syncthreads();
-      if (t == 0) {
-        const long long bef = (long long)s_pre_lo;
-        const unsigned __int128 np = (pre << 12) | (unsigned __int128)s_found;
-        s_pre_hi = (unsigned long long)(np >> 64);
-        s_pre_lo = (unsigned long long)np;
-        s_before = rank - bef;
-        s_done = (s_cnt == s_before || plen + 12 >= 96) ? 1 : 0;
+      if (centred) {
+        const bool miss = s_found == 0 || s_found == 4095;
+        __syncthreads();  // every thread has read s_found before thread 0 rewrites the state
+        if (t == 0) {
+          if (miss) {  // the h-th key left the window: plain levels from the top
+            s_pre_hi = 0ull;
+            s_pre_lo = 0ull;
+          } else {
+            const long long bef = (long long)s_pre_lo;
+            s_pre_hi = 0ull;
+            s_pre_lo = cbase + (unsigned long long)s_found - 1ull;
+            s_before = rank - bef;
+            s_done = s_cnt == s_before ? 1 : 0;
+          }
+        }
+        if (!miss) plen = 24;
+        centred = false;
+      } else {
+        if (t == 0) {
+          const long long bef = (long long)s_pre_lo;
+          const unsigned __int128 np = (pre << 12) | (unsigned __int128)s_found;
+          s_pre_hi = (unsigned long long)(np >> 64);
+          s_pre_lo = (unsigned long long)np;
+          s_before = rank - bef;
+          s_done = (s_cnt == s_before || plen + 12 >= 96) ? 1 : 0;
+        }
+        plen += 12;
       }
-      plen += 12;
       __syncthreads();
       if (s_done) break;
+      if (plen >= 24 && s_cnt <= CSC_CAND) {
+        // candidate resolution: the bin's rows (at most CSC_CAND over the cluster) collected per CTA
+        const unsigned __int128 bp = ((unsigned __int128)s_pre_hi << 64) | s_pre_lo;
+        if (t == 0) s_ncand = 0;
+        __syncthreads();
+        for (int il = t; il < nl; il += CS_T) {
+          const unsigned __int128 C =
+              ((unsigned __int128)(unsigned long long)__double_as_longlong(dyn[il]) << 32) | (unsigned)(r0 + il);
+          if ((C >> (96 - plen)) == bp) cand[atomicAdd(&s_ncand, 1)] = C;  // < CSC_CAND: a subset of the bin
+        }
+        cluster.sync();  // every CTA's candidates are listed
+        const long long need = s_before;  // rank of the h-th key inside the bin (1-based)
+        const int ntot = (int)s_cnt;
+        if (t < ntot) {
+          int q = 0, j = t;  // candidate t of the concatenation in rank order
+          while (j >= *cluster.map_shared_rank(&s_ncand, q)) {
+            j -= *cluster.map_shared_rank(&s_ncand, q);
+            q++;
+          }
+          const unsigned __int128 mine = cluster.map_shared_rank(cand, q)[j];
+          int less = 0;
+          for (int qq = 0; qq < CSC_CL; qq++) {
+            const int nq = *cluster.map_shared_rank(&s_ncand, qq);
+            const unsigned __int128* cq = cluster.map_shared_rank(cand, qq);
+            for (int k = 0; k < nq; k++) less += cq[k] < mine ? 1 : 0;
+          }
+          if (less == need - 1) {  // the h-th key (keys are unique: the row index is part of them)
+            s_pre_hi = (unsigned long long)(mine >> 64);
+            s_pre_lo = (unsigned long long)mine;
+          }
+        }
+        plen = 96;
+        // (the lists are rewritten only in the next step's select, after the member phase's cluster barrier)
+        __syncthreads();
+        break;
+      }
+    }
+    if (t == 0) {  // centre the next step's first level on this step's h-th key
+      const unsigned __int128 fp = ((unsigned __int128)s_pre_hi << 64) | s_pre_lo;
+      const unsigned long long top24 = plen >= 24 ? (unsigned long long)(fp >> (plen - 24)) : 0ull;
+      s_have_prev = plen >= 24 ? 1 : 0;
+      s_cbase = top24 > 2048 ? top24 - 2048 : 0ull;
     }
     csc_mark(step, 3, prof);
     // ---- membership bits of this CTA's rows and the cluster's changed-row count

@@ -209,6 +209,17 @@ __device__ __forceinline__ bool uni_keep(double y, double loc0, double thresh) {
   return __dmul_rn(d, d) <= thresh;
 }
 
+// (d, d^2) of the SHIFTED value d = y - c, d exact as a double-double (two-sum): the window objective
+// h S2 - S1^2 is shift-invariant, and with c = the column's median its terms are of the size of the spread,
+// not of the offset -- a column 1e8 + 1e-6 N(0,1) keeps its argmin (unshifted, S2 ~ h 1e16 and S1^2 cancel
+// to ~30 digits, past what double-double holds)
+__device__ __forceinline__ dd2 dd2_sh(double y, double c) {
+  const dd d = two_sum(y, -c);
+  dd p = two_prod(d.hi, d.hi);
+  p = quick_two_sum(p.hi, __fma_rn(2.0 * d.hi, d.lo, p.lo));
+  return {d, p};
+}
+
 __global__ void __launch_bounds__(UTH) k_uni_final(const double* __restrict__ sorted, long long len, long long h,
                                                    int nchunks, const dd2* __restrict__ coff, int nwchunks,
                                                    const WinPartial* __restrict__ part, UniConst uc,
@@ -325,10 +336,10 @@ __device__ __forceinline__ void u_cmpswap(double* v, int i, int j) {
 }
 
 // P(t) = sum_{i<t} (y_i, y_i^2) from the chunk prefixes cpre (chunk c = [c per, (c+1) per))
-__device__ __forceinline__ dd2 u_prefix(const double* v, const dd2* cpre, int per, int t) {
+__device__ __forceinline__ dd2 u_prefix(const double* v, const dd2* cpre, int per, int t, double cm) {
   const int c = t / per;
   dd2 acc = cpre[c];
-  for (int i = c * per; i < t; i++) acc = dd2_add(acc, dd2_of(v[i]));
+  for (int i = c * per; i < t; i++) acc = dd2_add(acc, dd2_sh(v[i], cm));
   return acc;
 }
 
@@ -364,11 +375,12 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
       __syncthreads();
     }
   }
-  // chunk totals and their exclusive scan
+  // chunk totals and their exclusive scan (values shifted by the median cm, see dd2_sh)
   const int per = (len + UST - 1) / UST;
   const int c0 = t * per, c1 = min(len, c0 + per);
+  const double cm = v[len / 2];
   dd2 loc = dd2_zero();
-  for (int i = c0; i < c1; i++) loc = dd2_add(loc, dd2_of(v[i]));
+  for (int i = c0; i < c1; i++) loc = dd2_add(loc, dd2_sh(v[i], cm));
   // prefixes anchored at chunk UST/2 (see k_uni_chunkscan): cpre[c] = P(c per) - P(UST/2 per)
   constexpr int AN = UST / 2;
   dd2 tot;
@@ -394,7 +406,7 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
   const double hd = (double)h;
   if (c0 < nwin) {
     dd2 Pl = ex;
-    dd2 Pr = u_prefix(v, cpre, per, c0 + h);
+    dd2 Pr = u_prefix(v, cpre, per, c0 + h, cm);
     const int e1 = min(c1, nwin);
     for (int s = c0; s < e1; s++) {
       const dd S1 = dd_sub(Pr.s1, Pl.s1);
@@ -405,8 +417,8 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
         blo = w.lo;
         bs = s;
       }
-      Pl = dd2_add(Pl, dd2_of(v[s]));
-      if (s + h < len) Pr = dd2_add(Pr, dd2_of(v[s + h]));
+      Pl = dd2_add(Pl, dd2_sh(v[s], cm));
+      if (s + h < len) Pr = dd2_add(Pr, dd2_sh(v[s + h], cm));
     }
   }
   for (int d = 16; d > 0; d >>= 1) {
@@ -428,8 +440,8 @@ __global__ void __launch_bounds__(UST) k_uni_small(const double* __restrict__ co
   for (int w = 1; w < UST / 32; w++)
     if (win_better(wsm[w].vhi, wsm[w].vlo, wsm[w].s, best.vhi, best.vlo, best.s)) best = wsm[w];
   const int s = (int)best.s;
-  const dd S1 = dd_sub(u_prefix(v, cpre, per, s + h).s1, u_prefix(v, cpre, per, s).s1);
-  const double loc0 = dd_to_d(dd_div_d(S1, hd));
+  const dd S1 = dd_sub(u_prefix(v, cpre, per, s + h, cm).s1, u_prefix(v, cpre, per, s, cm).s1);
+  const double loc0 = dd_to_d(dd_add(dd_div_d(S1, hd), dd_make(cm)));
   const dd wv = {best.vhi, best.vlo};
   const double var_raw = h > 1 ? dd_to_d(dd_div_d(dd_div_d(wv, hd), (double)(h - 1))) : 0.0;
   const double var0 = uc.c_raw * var_raw;
@@ -672,6 +684,331 @@ __global__ void __cluster_dims__(UCS_CL, 1, 1) __launch_bounds__(UCS_T, 1)
   cluster.sync();  // no CTA leaves while another may still read its buffers
 }
 
+// ------------------------------------------------------------------ the whole estimator of a short column
+// on one cluster: k_uni_cluster_sort's sort (512 threads x 8 keys per CTA, 96 KB of shared memory, so two
+// CTAs -- and twice the clusters -- fit per SM; 16 columns no longer take two waves) followed, in the same
+// kernel, by k_uni_small's scans, window objective and reweighting on the sorted column spread over the 8
+// CTAs (readings R2-R4):
+//   - chunk c = (CTA q, thread t) holds local positions [t per, (t+1) per) of the CTA's sorted run; chunk
+//     totals (sum y, sum y^2) in double-double, scanned per CTA forwards and backwards, and the CTA totals
+//     exchanged through DSMEM: prefixes ANCHORED at the first position of CTA 4 (~ the median, as
+//     k_uni_small's anchor: no window sum ever reaches into the tails);
+//   - every thread evaluates h S2 - S1^2 for the starts of its chunk, P(s + h) read from the CTA that holds
+//     position s + h (its chunk prefix + at most `per` values, DSMEM); argmin per CTA, then over the cluster
+//     in rank order (ties -> lowest s);
+//   - the raw fit from the best window (every CTA, the same arithmetic), the kept values summed per CTA and
+//     folded in rank order by CTA 0, which writes the column's UniOut.
+// One launch per call instead of two, and the tail work runs on 8 SMs instead of one.
+static constexpr int UCM_T = 512;
+static constexpr int UCM_V = UCS_CAP / UCM_T;  // 8 keys per thread in the local sort
+
+template <int S>
+__device__ __forceinline__ void ucm_reg_stage(unsigned long long (&x)[UCM_V], int t, int size) {
+#pragma unroll
+  for (int k = 0; k < UCM_V; k++) {
+    if ((k & S) == 0) {
+      const int e = t * UCM_V + k;
+      const bool up = (e & size) == 0;
+      const unsigned long long a = x[k], b = x[k + S];
+      const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
+      x[k] = up ? lo : hi;
+      x[k + S] = up ? hi : lo;
+    }
+  }
+}
+
+__global__ void __cluster_dims__(UCS_CL, 1, 1) __launch_bounds__(UCM_T, 2)
+    k_uni_cluster_mcd(const double* __restrict__ cols, long long len, long long hl, UniConst uc,
+                      UniOut* __restrict__ out) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ unsigned long long ucm_dyn[];  // [3][UCS_CAP]: runs 0 / 1, the merge inputs (la | lb)
+  __shared__ int s_split[2];
+  __shared__ dd2 sm[33];
+  __shared__ dd2 s_tot;           // this CTA's total, read by the cluster
+  __shared__ WinPartial s_best;   // this CTA's best window, read by the cluster
+  __shared__ dd2 s_kept;          // this CTA's kept sums, read by CTA 0
+  __shared__ long long s_kcnt;
+  __shared__ double s_fin[4];     // loc0, var_raw, var0, s*
+  const int r = (int)cluster.block_rank();
+  const int col = blockIdx.x / UCS_CL;
+  const int t = threadIdx.x, lane = t & 31;
+  const int n = (int)len, h = (int)hl;
+  const int nloc = (n + UCS_CL - 1) / UCS_CL;
+  const int r0 = min(n, r * nloc), cnt = min(n, r0 + nloc) - r0;
+  const double* y = cols + (long long)col * len;
+  unsigned long long* xs = ucm_dyn + UCS_CAP;
+  // ---- 1. local bitonic sort in registers (element e = t * UCM_V + k)
+  unsigned long long x[UCM_V];
+#pragma unroll
+  for (int k = 0; k < UCM_V; k++) {
+    const int e = t * UCM_V + k;
+    x[k] = e < cnt ? ucs_key(y[r0 + e]) : ~0ull;
+  }
+  for (int size = 2; size <= UCS_CAP; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride < UCM_V) {
+        if (stride == 4) ucm_reg_stage<4>(x, t, size);
+        else if (stride == 2) ucm_reg_stage<2>(x, t, size);
+        else ucm_reg_stage<1>(x, t, size);
+      } else if (stride < UCM_V * 32) {
+        const int lm = stride / UCM_V;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int k = 0; k < UCM_V; k++) {
+          const int e = t * UCM_V + k;
+          const unsigned long long o = __shfl_xor_sync(0xffffffffu, x[k], lm);
+          const bool keep_min = ((e & size) == 0) == lower;
+          x[k] = keep_min ? (x[k] < o ? x[k] : o) : (x[k] < o ? o : x[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < UCM_V; k++) xs[t * UCM_V + k] = x[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < UCM_V; k++) {
+          const int e = t * UCM_V + k;
+          const unsigned long long o = xs[e ^ stride];
+          const bool keep_min = ((e & size) == 0) == ((e & stride) == 0);
+          x[k] = keep_min ? (x[k] < o ? x[k] : o) : (x[k] < o ? o : x[k]);
+        }
+        __syncthreads();
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < UCM_V; k++) {
+    const int e = t * UCM_V + k;
+    if (e < cnt) ucm_dyn[e] = x[k];
+  }
+  cluster.sync();
+  // ---- 2. merge rounds over the cluster (as k_uni_cluster_sort; la | lb share one buffer: nla + nlb = cnt)
+  int cur = 0;
+  unsigned long long* la = ucm_dyn + 2 * UCS_CAP;
+  for (int span = 1; span < UCS_CL; span <<= 1) {
+    const unsigned long long* src = ucm_dyn + cur * UCS_CAP;
+    unsigned long long* dst = ucm_dyn + (cur ^ 1) * UCS_CAP;
+    const int grp = r / (2 * span);
+    const int gs = min(n, grp * 2 * span * nloc), gm = min(n, gs + span * nloc), ge = min(n, gm + span * nloc);
+    const int na = gm - gs, nb = ge - gm;
+    auto elem = [&](int g) -> unsigned long long {
+      const int q = g / nloc;
+      return cluster.map_shared_rank(src, q)[g - q * nloc];
+    };
+    const int olo = r0 - gs, ohi = olo + cnt;
+    if (t < 64) {
+      const int o = t < 32 ? olo : ohi;
+      const int sp = ucs_split(o, max(0, o - nb), min(o, na), gs, gm, elem, lane);
+      if (lane == 0) s_split[t >> 5] = sp;
+    }
+    __syncthreads();
+    const int ia = s_split[0], ib = s_split[1];
+    const int ja = olo - ia, jb = ohi - ib;
+    const int nla = ib - ia, nlb = jb - ja;
+    unsigned long long* lb = la + nla;
+    for (int e = t; e < nla; e += UCM_T) la[e] = elem(gs + ia + e);
+    for (int e = t; e < nlb; e += UCM_T) lb[e] = elem(gm + ja + e);
+    __syncthreads();
+    const int ept = (cnt + UCM_T - 1) / UCM_T;
+    const int o0 = min(cnt, t * ept), o1 = min(cnt, o0 + ept);
+    if (o0 < o1) {
+      int lo = max(0, o0 - nlb), hi = min(o0, nla);
+      while (lo < hi) {
+        const int i = (lo + hi) >> 1;
+        if (la[i] <= lb[o0 - i - 1]) lo = i + 1;
+        else hi = i;
+      }
+      int i = lo, j = o0 - lo;
+      for (int o = o0; o < o1; o++) {
+        const bool takeA = j >= nlb || (i < nla && la[i] <= lb[j]);
+        dst[o] = takeA ? la[i++] : lb[j++];
+      }
+    }
+    cur ^= 1;
+    cluster.sync();
+  }
+  // ---- 3. the sorted values (into the last round's source buffer: the keys stay readable), chunk totals
+  //         of the values shifted by the column's median (dd2_sh) and anchored chunk prefixes
+  const unsigned long long* kfin = ucm_dyn + cur * UCS_CAP;
+  double* v = reinterpret_cast<double*>(ucm_dyn + (cur ^ 1) * UCS_CAP);
+  dd2* cpre = reinterpret_cast<dd2*>(ucm_dyn + 2 * UCS_CAP);  // [UCM_T] (the merge buffer is free now)
+  __shared__ double s_cm;
+  for (int i = t; i < cnt; i += UCM_T) v[i] = ucs_val(kfin[i]);
+  if (t == 0) {
+    const int qm = (n / 2) / nloc;
+    s_cm = ucs_val(*cluster.map_shared_rank(kfin + (n / 2 - qm * nloc), qm));
+  }
+  __syncthreads();
+  const double cm = s_cm;
+  const int per = (nloc + UCM_T - 1) / UCM_T;  // the same chunk geometry in every CTA
+  const int c0 = min(cnt, t * per), c1 = min(cnt, c0 + per);
+  dd2 loc = dd2_zero();
+  for (int i = c0; i < c1; i++) loc = dd2_add(loc, dd2_sh(v[i], cm));
+  constexpr int AQ = UCS_CL / 2;  // anchor: the first position of CTA AQ
+  dd2 ctot;
+  const dd2 fex = block_exscan_dd2(loc, &ctot, sm);  // chunks [0, t) of this CTA
+  cpre[t] = loc;
+  __syncthreads();
+  const dd2 rin = cpre[UCM_T - 1 - t];
+  dd2 btot;
+  const dd2 bex = block_exscan_dd2(rin, &btot, sm);  // chunks above UCM_T - 1 - t
+  __syncthreads();
+  // local parts: forward prefix for CTAs >= AQ, minus the suffix (from the chunk start on) below AQ
+  if (r >= AQ) cpre[t] = fex;
+  else cpre[UCM_T - 1 - t] = dd2_add(bex, rin);  // (negated with the cross-CTA part below)
+  if (t == 0) s_tot = ctot;
+  cluster.sync();  // every CTA's total is published
+  dd2 off = dd2_zero(), Pn = dd2_zero();  // cross-CTA part of this CTA's prefixes; anchored P(n)
+  if (r >= AQ) {
+    for (int q = AQ; q < r; q++) off = dd2_add(off, *cluster.map_shared_rank(&s_tot, q));
+  } else {
+    for (int q = r + 1; q < AQ; q++) off = dd2_add(off, *cluster.map_shared_rank(&s_tot, q));
+  }
+  for (int q = AQ; q < UCS_CL; q++) Pn = dd2_add(Pn, *cluster.map_shared_rank(&s_tot, q));
+  {
+    const dd2 lp = cpre[t];
+    if (r >= AQ) {
+      cpre[t] = dd2_add(off, lp);
+    } else {
+      const dd2 b = dd2_add(off, lp);
+      cpre[t] = {dd_neg(b.s1), dd_neg(b.s2)};
+    }
+  }
+  cluster.sync();  // every CTA's anchored chunk prefixes are final
+  // anchored P(G) for a global position G in [0, n] (remote chunk prefix + the chunk's values before G)
+  auto prefix_at = [&](int G) -> dd2 {
+    if (G >= n) return Pn;
+    const int q = G / nloc, l = G - q * nloc, tc = l / per;
+    const dd2* cq = reinterpret_cast<const dd2*>(cluster.map_shared_rank(ucm_dyn + 2 * UCS_CAP, q));
+    dd2 acc = cq[tc];
+    const double* vq = cluster.map_shared_rank(v, q);
+    for (int i = tc * per; i < l; i++) acc = dd2_add(acc, dd2_sh(vq[i], cm));
+    return acc;
+  };
+  // ---- 4. window objective of the starts in this thread's chunk
+  const int nwin = n - h + 1;
+  const double hd = (double)h;
+  double bhi = __longlong_as_double(0x7ff0000000000000LL), blo = 0.0;
+  long long bs = 0x7fffffffffffffffLL;
+  {
+    const int ga = r0 + c0, gb = min(r0 + c1, nwin);
+    if (ga < gb) {
+      dd2 Pl = cpre[t];
+      dd2 Pr = prefix_at(ga + h);
+      int G = ga + h, q = G / nloc, l = G - q * nloc;
+      const double* vq = cluster.map_shared_rank(v, q < UCS_CL ? q : UCS_CL - 1);
+      for (int sg = ga; sg < gb; sg++) {
+        const dd S1 = dd_sub(Pr.s1, Pl.s1);
+        const dd S2 = dd_sub(Pr.s2, Pl.s2);
+        const dd w = dd_sub(dd_mul_d(S2, hd), dd_mul(S1, S1));
+        if (win_better(w.hi, w.lo, sg, bhi, blo, bs)) {
+          bhi = w.hi;
+          blo = w.lo;
+          bs = sg;
+        }
+        Pl = dd2_add(Pl, dd2_sh(v[sg - r0], cm));
+        if (G < n) {
+          Pr = dd2_add(Pr, dd2_sh(vq[l], cm));
+          G++;
+          if (++l == nloc && G < n) {
+            q++;
+            l = 0;
+            vq = cluster.map_shared_rank(v, q);
+          }
+        }
+      }
+    }
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    const double ohi = __shfl_down_sync(0xffffffffu, bhi, d);
+    const double olo = __shfl_down_sync(0xffffffffu, blo, d);
+    const long long os = __shfl_down_sync(0xffffffffu, bs, d);
+    if (win_better(ohi, olo, os, bhi, blo, bs)) {
+      bhi = ohi;
+      blo = olo;
+      bs = os;
+    }
+  }
+  __shared__ WinPartial wsm[UCM_T / 32];
+  if (lane == 0) wsm[t >> 5] = {bhi, blo, bs};
+  __syncthreads();
+  if (t == 0) {
+    WinPartial best = wsm[0];
+    for (int w = 1; w < UCM_T / 32; w++)
+      if (win_better(wsm[w].vhi, wsm[w].vlo, wsm[w].s, best.vhi, best.vlo, best.s)) best = wsm[w];
+    s_best = best;
+  }
+  cluster.sync();  // every CTA's best window is published
+  // ---- 5. the raw fit (every CTA, identical) and the kept sums
+  if (t == 0) {
+    WinPartial best = *cluster.map_shared_rank(&s_best, 0);
+    for (int q = 1; q < UCS_CL; q++) {
+      const WinPartial w = *cluster.map_shared_rank(&s_best, q);
+      if (win_better(w.vhi, w.vlo, w.s, best.vhi, best.vlo, best.s)) best = w;
+    }
+    const int sb = (int)best.s;
+    const dd S1 = dd_sub(prefix_at(sb + h).s1, prefix_at(sb).s1);
+    const double loc0 = dd_to_d(dd_add(dd_div_d(S1, hd), dd_make(cm)));
+    const dd wv = {best.vhi, best.vlo};
+    const double var_raw = h > 1 ? dd_to_d(dd_div_d(dd_div_d(wv, hd), (double)(h - 1))) : 0.0;
+    s_fin[0] = loc0;
+    s_fin[1] = var_raw;
+    s_fin[2] = uc.c_raw * var_raw;
+    s_fin[3] = (double)sb;
+  }
+  __syncthreads();
+  const double loc0 = s_fin[0], var0 = s_fin[2], thresh = uc.q1 * var0;
+  dd2 kacc = dd2_zero();
+  long long kc = 0;
+  for (int i = c0; i < c1; i++)
+    if (uni_keep(v[i], loc0, thresh)) {
+      kacc = dd2_add(kacc, dd2_of_dev(v[i], __dsub_rn(v[i], loc0)));
+      kc++;
+    }
+  const dd2 Kc = block_sum_dd2(kacc, sm);
+  for (int d = 16; d > 0; d >>= 1) kc += __shfl_down_sync(0xffffffffu, kc, d);
+  __shared__ long long kred[UCM_T / 32];
+  if (lane == 0) kred[t >> 5] = kc;
+  __syncthreads();
+  if (t == 0) {
+    long long k = 0;
+    for (int w = 0; w < UCM_T / 32; w++) k += kred[w];
+    s_kept = Kc;
+    s_kcnt = k;
+  }
+  cluster.sync();  // every CTA's kept sums are published
+  if (r == 0 && t == 0) {
+    dd2 K = dd2_zero();
+    long long k = 0;
+    for (int q = 0; q < UCS_CL; q++) {
+      K = dd2_add(K, *cluster.map_shared_rank(&s_kept, q));
+      k += *cluster.map_shared_rank(&s_kcnt, q);
+    }
+    UniOut o;
+    o.raw_loc = loc0;
+    o.raw_var = s_fin[1];
+    o.var0 = var0;
+    o.start = (long long)s_fin[3];
+    o.kept = k;
+    o.pad = 0;
+    o.status = 0;
+    o.loc = 0.0;
+    o.scale = 0.0;
+    if (!(var0 > 0.0) || k < 2) {
+      o.status = 1;
+    } else {
+      const double lc = dd_to_d(K.s1) / (double)k;
+      const dd qv = kept_sq_about_loc(K, loc0, lc, (double)k);
+      const double var = uc.c_rew * (dd_to_d(qv) / (double)(k - 1));
+      o.loc = lc;
+      o.scale = sqrt(var);
+      if (!(var > 0.0)) o.status = 1;
+    }
+    out[col] = o;
+  }
+  cluster.sync();  // no CTA leaves while another may still read its shared memory
+}
+
 struct UniScratch {
   double* sorted;
   double* tmpk;
@@ -764,6 +1101,15 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
     const double* cc = cols + (long long)c0 * len;
     const long long Nc = len * nc;
     size_t bytes = s.cub_bytes;
+    static const bool split = getenv("RTD_UNI_CLUSTER_SPLIT") != nullptr;  // r02 path: sort, then k_uni_small
+    if (csort && !split && len <= (long long)UCS_CL * UCS_CAP && len / 2 + 1 <= (long long)UCS_CL * UCS_CAP) {
+      // sort + scans + window + reweighting in one cluster launch per batch of columns
+      const int dyn = 3 * UCS_CAP * (int)sizeof(unsigned long long);
+      RTD_CU(cudaFuncSetAttribute(k_uni_cluster_mcd, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+      k_uni_cluster_mcd<<<nc * UCS_CL, UCM_T, dyn, st>>>(cc, len, h, uc, out_dev + c0);
+      RTD_LAUNCHED();
+      continue;
+    }
     if (csort) {  // one 8-CTA cluster per column, no library sort
       const int dyn = 4 * UCS_CAP * (int)sizeof(unsigned long long);
       RTD_CU(cudaFuncSetAttribute(k_uni_cluster_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));

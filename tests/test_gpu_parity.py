@@ -69,6 +69,34 @@ def test_unimcd_cluster_sort_ties_signed_zeros(n):
         assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13)
 
 
+@pytest.mark.parametrize("n", [4_097, 20_000, 32_768])
+def test_unimcd_cluster_estimator_many_columns_and_tails(n):
+    """k_uni_cluster_mcd (sort + anchored double-double scans + windows + reweighting on one 8-CTA cluster per
+    column): 24 columns in one launch (more clusters than fit at once before), huge tails of both signs and
+    an offset column, each against the oracle's exact window."""
+    rng = np.random.default_rng(n + 5)
+    cols = []
+    for j in range(24):
+        x = rng.standard_normal(n) * (1.0 + j) + 10.0 * j
+        if j % 3 == 1:
+            k = n // 100
+            x[:k] = rng.choice([-1.0, 1.0], size=k) * 10.0 ** rng.uniform(0, 12, size=k)
+            x = rng.permutation(x)
+        if j % 3 == 2:
+            x = 1e8 + 1e-6 * rng.standard_normal(n)
+        cols.append(x)
+    cols = np.stack(cols)
+    g = api.unimcd(_cuda(cols))
+    for j in range(cols.shape[0]):
+        o = unimcd_reweighted(cols[j])
+        r = unimcd_raw(cols[j], n // 2 + 1)
+        assert g["start"][j] == r.start, j
+        assert g["raw_loc"][j] == pytest.approx(r.loc, rel=1e-15, abs=1e-300), j
+        assert g["raw_var"][j] == pytest.approx(r.var_raw, rel=1e-14), j
+        assert g["loc"][j] == pytest.approx(o.loc, rel=1e-14, abs=1e-14), j
+        assert g["scale"][j] == pytest.approx(o.scale, rel=1e-13), j
+
+
 def test_unimcd_exact_ties_and_symmetry():
     rng = np.random.default_rng(7)
     a = np.sort(np.abs(rng.standard_normal(2000))) + 0.01
