@@ -273,6 +273,8 @@ struct CStepBufs {
   int* pairs;     // [inst][2] slots of the distance pass's CTA rows (two starts of a block share one)
   int* list;      // [inst][m] ordered changed rows per segment (update-based C-step)
   int* seg_cnt;   // [inst][ctas]
+  SelCand* cand;  // [inst][SEL_CAND] candidate-mode rows of the select
+  int* cand_cnt;  // [inst]
   long long seg_len;
   int traj_stride;
   int ctas;
@@ -307,6 +309,8 @@ void carve_cstep(Arena& A, CStepBufs& b, int ninst, long long m, int p, int max_
   b.selcnt = A.take<unsigned int>(ninst);
   b.list = A.take<int>((size_t)ninst * m);
   b.seg_cnt = A.take<int>((size_t)ninst * b.ctas);
+  b.cand = A.take<SelCand>((size_t)ninst * SEL_CAND);
+  b.cand_cnt = A.take<int>(ninst);
   b.seg_len = ((m + b.ctas - 1) / b.ctas + 255) / 256 * 256;
 }
 
@@ -454,7 +458,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     {
       ProfScope ps("select", (double)na * m * 9.0);
       launch_select(b.d2, m, h, b.inst_dev, na, b.sel, b.hist, b.selcnt, memB, memA, b.changed, b.list, b.seg_cnt,
-                    b.ctas, b.seg_len, st);
+                    b.ctas, b.seg_len, b.cand, b.cand_cnt, st);
       fetch(st, {{changed.data(), b.changed, ninst * sizeof(int)}, {status_h.data(), b.status, ninst * sizeof(int)}});
       std::vector<int> more;
       for (int i : act)
@@ -463,7 +467,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
         h2d(st, b.inst_dev, more.data(), more.size() * sizeof(int));
         RTD_CU(cudaMemsetAsync(b.changed, 0, ninst * sizeof(int), st));
         launch_select_finish(b.d2, m, b.inst_dev, (int)more.size(), b.sel, b.hist, b.selcnt, memB, memA, b.changed,
-                             b.list, b.seg_cnt, b.ctas, b.seg_len, st);
+                             b.list, b.seg_cnt, b.ctas, b.seg_len, b.cand, b.cand_cnt, st);
         std::vector<int> ch2(ninst);
         d2h(st, ch2.data(), b.changed, ninst * sizeof(int));
         for (int i : more) changed[i] = ch2[i];

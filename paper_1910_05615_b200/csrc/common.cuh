@@ -178,4 +178,161 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// Order-preserving 64-bit key of a double (NaN-free input) and back.
+__device__ __forceinline__ unsigned long long ord_key64(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val64(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+// In-register bitonic sort of N = V * blockDim.x keys (N a power of two), element e = threadIdx.x * V + k in
+// x[k]: strides below V inside a thread, below 32 V by warp shuffles, the rest through xs[N] (two barriers
+// per such stage).  For 4096 keys and 1024 threads: 15 shared-memory stages instead of the 78 barriers of
+// a shared-memory network (k_q_sample 43 -> ~6 us).
+template <int V>
+__device__ __forceinline__ void bitonic_inreg_stage(unsigned long long (&x)[V], int stride, int size) {
+#pragma unroll
+  for (int k = 0; k < V; k++) {
+#pragma unroll
+    for (int S = 1; S < V; S <<= 1) {
+      if (S == stride && (k & S) == 0) {
+        const int e = threadIdx.x * V + k;
+        const bool up = (e & size) == 0;
+        const unsigned long long a = x[k], b = x[k + S];
+        const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
+        x[k] = up ? lo : hi;
+        x[k + S] = up ? hi : lo;
+      }
+    }
+  }
+}
+template <int V>
+__device__ void block_bitonic_keys(unsigned long long (&x)[V], unsigned long long* xs) {
+  const int lane = threadIdx.x & 31;
+  const int N = V * (int)blockDim.x;
+  for (int size = 2; size <= N; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride < V) {
+        bitonic_inreg_stage<V>(x, stride, size);
+      } else if (stride < V * 32) {
+        const int lm = stride / V;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int k = 0; k < V; k++) {
+          const int e = threadIdx.x * V + k;
+          const unsigned long long o = __shfl_xor_sync(0xffffffffu, x[k], lm);
+          const bool keep_min = ((e & size) == 0) == lower;
+          x[k] = keep_min ? (x[k] < o ? x[k] : o) : (x[k] < o ? o : x[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < V; k++) xs[threadIdx.x * V + k] = x[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < V; k++) {
+          const int e = threadIdx.x * V + k;
+          const unsigned long long o = xs[e ^ stride];
+          const bool keep_min = ((e & size) == 0) == ((e & stride) == 0);
+          x[k] = keep_min ? (x[k] < o ? x[k] : o) : (x[k] < o ? o : x[k]);
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+// Two order statistics (ranks ra, rb, 0-based) of N = V * blockDim.x ordered 64-bit keys x, without sorting:
+// radix levels of 12 bits (sign + exponent first), a 4096-bin histogram per rank and level among the keys
+// that share the rank's prefix so far, until the rank's bin holds a single key (then that key is the order
+// statistic, exactly) or 60 bits are fixed (then the prefix, low bits cleared for ra / set for rb).  Normal
+// columns stop after two or three levels; a column 1e9 + N(0,1) needs four.  Used for routing maps (bucket
+// ranges) only.  hist: shared, 2 x 4096 unsigned; blockDim.x == 1024.
+__device__ __forceinline__ void rank_bin_4096(const unsigned* h, long long rank, int* s_bin, long long* s_bef,
+                                              long long* wsum) {
+  // thread t owns bins 4t .. 4t+3; block exclusive scan of the per-thread sums
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  long long c[4], loc = 0;
+#pragma unroll
+  for (int e = 0; e < 4; e++) {
+    c[e] = h[4 * t + e];
+    loc += c[e];
+  }
+  long long inc = loc;
+  for (int d = 1; d < 32; d <<= 1) {
+    const long long v = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += v;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (t < 32) {
+    long long v = wsum[t], x = v;
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    wsum[t] = x - v;
+  }
+  __syncthreads();
+  long long before = wsum[w] + inc - loc;
+#pragma unroll
+  for (int e = 0; e < 4; e++) {
+    if (c[e] > 0 && before <= rank && rank < before + c[e]) {
+      *s_bin = 4 * t + e;
+      *s_bef = before;
+    }
+    before += c[e];
+  }
+  __syncthreads();
+}
+template <int V>
+__device__ void block_quantile_keys2(const unsigned long long (&x)[V], long long ra, long long rb, unsigned* hist,
+                                     unsigned long long* out) {
+  __shared__ long long wsum[32];
+  __shared__ int s_bin[2];
+  __shared__ long long s_bef[2];
+  __shared__ unsigned long long s_key[2];
+  const int t = threadIdx.x;
+  unsigned long long pre[2] = {0ull, 0ull};
+  long long rk[2] = {ra, rb};
+  bool done[2] = {false, false};
+  for (int lev = 0; lev < 5 && !(done[0] && done[1]); lev++) {
+    const int sh = 52 - 12 * lev;  // this level's digit: bits [sh, sh + 12)
+    for (int i = t; i < 2 * 4096; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < V; k++) {
+      const unsigned dig = (unsigned)(x[k] >> sh) & 4095u;
+#pragma unroll
+      for (int j = 0; j < 2; j++)
+        if (!done[j] && (lev == 0 || (x[k] >> (sh + 12)) == pre[j])) atomicAdd(&hist[4096 * j + dig], 1u);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      if (done[j]) continue;  // (uniform)
+      rank_bin_4096(hist + 4096 * j, rk[j], &s_bin[j], &s_bef[j], wsum);
+      const unsigned cnt = hist[4096 * j + s_bin[j]];
+      pre[j] = (pre[j] << 12) | (unsigned)s_bin[j];
+      rk[j] -= s_bef[j];
+      if (cnt == 1u) {  // the rank's key is the only one with this prefix
+#pragma unroll
+        for (int k = 0; k < V; k++)
+          if ((x[k] >> sh) == pre[j]) s_key[j] = x[k];
+        done[j] = true;
+      } else if (lev == 4) {
+        s_key[j] = j == 0 ? (pre[j] << 4) : ((pre[j] << 4) | 15ull);
+        done[j] = true;
+      }
+      __syncthreads();
+    }
+  }
+  if (t == 0) {
+    out[0] = s_key[0];
+    out[1] = s_key[1];
+  }
+  __syncthreads();
+}
+
 }  // namespace rtd

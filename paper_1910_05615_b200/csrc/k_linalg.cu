@@ -1099,7 +1099,10 @@ __global__ void __launch_bounds__(64) k_smw_update(const int* __restrict__ inst,
     int k = 0;
     for (int sgi = 0; sgi < nseg && k < 2; sgi++) {
       const int c = seg_cnt_all[(long long)id * nseg + sgi];
-      for (int j = 0; j < c && k < 2; j++) rows[k++] = list_all[(long long)id * m + (long long)sgi * seg_len + j];
+      for (int j = 0; j < c && k < 2; j++) {
+        const int e = list_all[(long long)id * m + (long long)sgi * seg_len + j];
+        if (e != 0) rows[k++] = e;  // (0: a reserved slot of an unchanged candidate row)
+      }
     }
     s_ok = k == 2;
   }
@@ -1435,6 +1438,7 @@ __global__ void __launch_bounds__(LT) k_jacobi(const double* __restrict__ A_all,
 // the two column updates, so a round is one barrier and one chain of slow fp64 operations (the two-sided
 // form needed four barriers and a shared-memory hand-off of (c, s) per round: 0.83 ms for the 16 40 x 40
 // matrices of config 4, 57 us for config 5's two 8 x 8).
+__device__ int g_jacobi_sweeps[64];  // RTD_DEBUG_JACOBI: sweeps of the first 64 matrices of the last launch
 static constexpr int JCS = 64;  // column stride of the column-major copies (rows lane and lane + 32)
 __global__ void __launch_bounds__(32 * (RTD_MAXP / 2)) k_jacobi_os(const double* __restrict__ A_all, int p,
                                                                    double kappa_max, double* __restrict__ V_all,
@@ -1444,6 +1448,7 @@ __global__ void __launch_bounds__(32 * (RTD_MAXP / 2)) k_jacobi_os(const double*
   __shared__ double lam_s[RTD_MAXP];
   __shared__ int order[RTD_MAXP];
   __shared__ int s_rot[3];
+  __shared__ unsigned char pq[RTD_MAXP - 1][RTD_MAXP / 2][2];  // round-robin schedule: (P, Q) of pair w in a round
   const int b = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
   const double* Ain = A_all + (long long)b * RTD_MAXP * RTD_MAXP;
   for (int j = w; j < RTD_MAXP; j += nw)
@@ -1454,32 +1459,46 @@ __global__ void __launch_bounds__(32 * (RTD_MAXP / 2)) k_jacobi_os(const double*
     }
   if (t < 3) s_rot[t] = 0;
   const int n2 = p + (p & 1);
-  constexpr double tol = 1e-15;
+  // positions: 0 fixed, 1..n2-1 rotated right by one per round (period n2 - 1: every sweep starts from the
+  // identity); tabulated once (the integer modulo per round and lane was on the critical path)
+  for (int e = t; e < (n2 - 1) * (n2 / 2); e += blockDim.x) {
+    const int round = e / (n2 / 2), k = e - round * (n2 / 2);
+    auto ord = [&](int x) { return x == 0 ? 0 : 1 + ((x - 1 - round) % (n2 - 1) + (n2 - 1)) % (n2 - 1); };
+    int P = ord(k), Q = ord(n2 - 1 - k);
+    if (P > Q) { const int tmp = P; P = Q; Q = tmp; }
+    pq[round][k][0] = (unsigned char)P;
+    pq[round][k][1] = (unsigned char)Q;
+  }
+  // rotate while |a_P . a_Q| > tol ||a_P|| ||a_Q||: the rounding of a rotation leaves a few eps of relative
+  // non-orthogonality, so tol must sit above it or the sweeps never end (LAPACK's dgesvj: sqrt(m) eps)
+  constexpr double tol = 1e-14;
+  int lanes = 1;  // lanes holding rows (rows lane and lane + 32)
+  while (lanes < 32 && lanes < p) lanes <<= 1;
   __syncthreads();
   for (int sweep = 0; sweep < 60; sweep++) {
     const int fs = sweep % 3;
     if (t == 0) s_rot[(sweep + 1) % 3] = 0;  // the next sweep's flag (triple-buffered: no reader races)
     for (int round = 0; round < n2 - 1; round++) {
       if (w < n2 / 2) {
-        auto ord = [&](int k) { return k == 0 ? 0 : 1 + ((k - 1 - round) % (n2 - 1) + (n2 - 1)) % (n2 - 1); };
-        int P = ord(w), Q = ord(n2 - 1 - w);
-        if (P > Q) { const int tmp = P; P = Q; Q = tmp; }
+        const int P = pq[round][w][0], Q = pq[round][w][1];
         if (Q < p) {
           double aP0 = Ac[P][lane], aP1 = Ac[P][lane + 32], aQ0 = Ac[Q][lane], aQ1 = Ac[Q][lane + 32];
           double al = fma(aP0, aP0, aP1 * aP1), be = fma(aQ0, aQ0, aQ1 * aQ1), ga = fma(aP0, aQ0, aP1 * aQ1);
-#pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
+          // butterfly over the lanes that hold rows (the others hold zeros): every such lane gets the sums
+          for (int d = 1; d < lanes; d <<= 1) {
             al += __shfl_xor_sync(0xffffffffu, al, d);
             be += __shfl_xor_sync(0xffffffffu, be, d);
             ga += __shfl_xor_sync(0xffffffffu, ga, d);
           }
           if (ga != 0.0 && ga * ga > tol * tol * al * be) {
-            // zeta = (be - al) / (2 ga), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)) written without the first
-            // division: t = sign(h ga) |ga| / (|h| + sqrt(h^2 + ga^2)), h = (be - al) / 2; c = rsqrt(1 + t^2)
+            // the rotation zeroing a_P . a_Q (zeta = (be - al) / (2 ga), t = tan theta = sign(zeta) / (|zeta| +
+            // sqrt(1 + zeta^2))) from two rsqrt and no division: with h = (be - al) / 2, r = sqrt(h^2 + ga^2),
+            // cos^2 theta = (1 + |h| / r) / 2 (>= 1/2: no cancellation), sin theta = sign(h ga) |ga| / (2 r cos theta)
             const double hh = 0.5 * (be - al);
             const bool pos = hh == 0.0 || ((hh > 0.0) == (ga > 0.0));
-            const double tt = (pos ? fabs(ga) : -fabs(ga)) / (fabs(hh) + sqrt(fma(hh, hh, ga * ga)));
-            const double c = rsqrt(fma(tt, tt, 1.0)), s = tt * c;
+            const double ir = rsqrt(fma(hh, hh, ga * ga));
+            const double c2 = 0.5 * fma(fabs(hh), ir, 1.0), rc = rsqrt(c2);
+            const double c = c2 * rc, s = (pos ? fabs(ga) : -fabs(ga)) * ir * 0.5 * rc;
             Ac[P][lane] = c * aP0 - s * aQ0;
             Ac[Q][lane] = s * aP0 + c * aQ0;
             Ac[P][lane + 32] = c * aP1 - s * aQ1;
@@ -1495,7 +1514,10 @@ __global__ void __launch_bounds__(32 * (RTD_MAXP / 2)) k_jacobi_os(const double*
       }
       __syncthreads();
     }
-    if (!s_rot[fs]) break;  // a sweep without a rotation: converged
+    if (!s_rot[fs]) {  // a sweep without a rotation: converged
+      if (t == 0 && b < 64) g_jacobi_sweeps[b] = sweep + 1;
+      break;
+    }
   }
   // lambda_j = v_j . (A v_j), the rotated column a_j = A v_j (one warp per column)
   for (int j = w; j < p; j += nw) {
@@ -1560,6 +1582,15 @@ void launch_jacobi(const double* A_all, int nb, int p, double kappa_max, double*
     k_jacobi_os<<<nb, 32 * npr, 0, st>>>(A_all, p, kappa_max, V_all, lam_all, ok_all);
   }
   RTD_LAUNCHED();
+  static const bool dbg = getenv("RTD_DEBUG_JACOBI") != nullptr;
+  if (dbg && !two_sided) {
+    int sw[64];
+    RTD_CU(cudaStreamSynchronize(st));
+    RTD_CU(cudaMemcpyFromSymbol(sw, g_jacobi_sweeps, sizeof(sw)));
+    fprintf(stderr, "[jacobi] p=%d nb=%d sweeps:", p, nb);
+    for (int i = 0; i < std::min(nb, 64); i++) fprintf(stderr, " %d", sw[i]);
+    fprintf(stderr, "\n");
+  }
 }
 
 // ------------------------------------------------------------------ refinement matrices

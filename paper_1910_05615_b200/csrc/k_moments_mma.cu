@@ -306,9 +306,9 @@ __global__ void __launch_bounds__(MW * 32, 2) k_moments_mma(MomArgs a) {
       w[q] = 0.0;
       if (MODE == MOM_DELTA) {
         if (row[q] < r_end) {
-          const int e = lst[row[q]];
-          w[q] = e > 0 ? 1.0 : -1.0;
-          row[q] = (e > 0 ? e : -e) - 1;
+          const int e = lst[row[q]];  // 0: a reserved slot of an unchanged candidate row (k_sel_fixup)
+          w[q] = e > 0 ? 1.0 : (e < 0 ? -1.0 : 0.0);
+          row[q] = e != 0 ? (e > 0 ? e : -e) - 1 : 0;
         }
       } else if (row[q] < r_end) {
         if (MODE == MOM_WRAP) {

@@ -58,15 +58,22 @@ __global__ void __launch_bounds__(1024) k_q_sample(const double* __restrict__ r_
   __shared__ double s[QSAMPLE];
   const int b = blockIdx.x;
   const double* r = r_all + (long long)b * m;
-  for (int i = threadIdx.x; i < QSAMPLE; i += blockDim.x) s[i] = r[(long long)i * m / QSAMPLE];
+  constexpr int V = QSAMPLE / 1024;  // blockDim.x == 1024
+  unsigned long long x[V];
+#pragma unroll
+  for (int k = 0; k < V; k++) {
+    const double y = r[(long long)(threadIdx.x * V + k) * m / QSAMPLE];
+    x[k] = y == y ? ord_key64(y) : ~0ull;  // (a NaN norm sorts last; the input check rejects it anyway)
+  }
   for (int i = threadIdx.x; i < QNB; i += blockDim.x) cnt_all[(long long)b * QNB + i] = 0u;
   if (threadIdx.x < QTARGETS) gcount[b * QTARGETS + threadIdx.x] = 0;
-  __syncthreads();
-  q_bitonic(s, QSAMPLE);
+  // the sample's [0.5%, 99.5%] quantiles to 12 mantissa bits (the map only routes: any monotone map is exact)
+  __shared__ unsigned long long qk[2];
+  block_quantile_keys2<V>(x, QSAMPLE / 200, QSAMPLE - 1 - QSAMPLE / 200, reinterpret_cast<unsigned*>(s), qk);
   if (threadIdx.x == 0) {
     QMap c;
     memset(&c, 0, sizeof(c));
-    const double ql = s[QSAMPLE / 200], qh = s[QSAMPLE - 1 - QSAMPLE / 200];
+    const double ql = ord_val64(qk[0]), qh = ord_val64(qk[1]);
     const double span = qh - ql;
     c.lo = ql - 0.05 * span;
     c.hi = qh + 0.05 * span;

@@ -197,16 +197,23 @@ __device__ void smem_bitonic(double* a, int npow2) {
 // 1. bucket map from a strided sample
 __global__ void __launch_bounds__(1024) k_pr_sample(const double* __restrict__ cols, long long len,
                                                     PrunedCol* __restrict__ pc, unsigned long long* __restrict__ mm) {
-  __shared__ double s[SAMPLE];
+  __shared__ unsigned s[2 * 4096];  // block_quantile_keys2's two histograms
   const int col = blockIdx.x;
   const double* y = cols + (long long)col * len;
-  for (int i = threadIdx.x; i < SAMPLE; i += blockDim.x) s[i] = y[(long long)i * len / SAMPLE];
-  __syncthreads();
-  smem_bitonic(s, SAMPLE);
+  constexpr int V = SAMPLE / 1024;  // blockDim.x == 1024: the in-register network (common.cuh)
+  unsigned long long x[V];
+#pragma unroll
+  for (int k = 0; k < V; k++) {
+    const double v = y[(long long)(threadIdx.x * V + k) * len / SAMPLE];
+    x[k] = v == v ? ord_key64(v) : ~0ull;
+  }
+  // the sample's [0.5%, 99.5%] quantiles to 12 mantissa bits (routing only; block_quantile_keys2)
+  __shared__ unsigned long long qk[2];
+  block_quantile_keys2<V>(x, SAMPLE / 200, SAMPLE - 1 - SAMPLE / 200, s, qk);
   if (threadIdx.x == 0) {
     PrunedCol c;
     memset(&c, 0, sizeof(c));
-    double ql = s[SAMPLE / 200], qh = s[SAMPLE - 1 - SAMPLE / 200];
+    double ql = ord_val64(qk[0]), qh = ord_val64(qk[1]);
     double span = qh - ql;
     c.lo = ql - 0.05 * span;
     c.hi = qh + 0.05 * span;

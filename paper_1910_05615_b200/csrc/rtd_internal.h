@@ -183,17 +183,30 @@ struct SelState {
   int done;
   int valid;                     // done and prefix usable to centre the next step's first level
   int centred;                   // the next level is the centred 24-bit level
+  int candok;                    // not done, but the h-th key's bin (plen >= 24) holds <= SEL_CAND rows:
+                                 // they are listed by k_sel_member and resolved by k_sel_fixup
+  long long bincnt;              // rows in the bin of the current prefix
+};
+// a row of the h-th key's bin (candidate mode): its d^2 bits, row and reserved changed-list position
+struct SelCand {
+  unsigned long long kb;
+  int row;
+  int listpos;
 };
 // Selection of the h smallest (d^2, row) per instance + membership + ordered changed-row lists:
 // list_all[id][seg x at x seg_len] (+-(row+1)), seg_cnt_all[id][nseg]; changed[id] must be zero on
 // entry; changed[id] == -1 on exit means the selection needs launch_select_finish.
 // st_all must be zeroed before the first step of a trajectory (no centring then).
+// cand_all[inst][SEL_CAND] / cand_cnt[inst]: the candidate-mode buffers (a list entry 0 is a reserved slot of
+// a candidate row that did not change: consumers skip it).
+constexpr int SEL_CAND = 4096;
 void launch_select(const double* d2_all, long long m, long long h, const int* inst, int ninst, SelState* st_all,
                    unsigned int* hist_all, unsigned int* cnt_all, uint8_t* mem_new_all, const uint8_t* mem_old_all,
-                   int* changed, int* list_all, int* seg_cnt_all, int nseg, long long seg_len, cudaStream_t st);
+                   int* changed, int* list_all, int* seg_cnt_all, int nseg, long long seg_len, SelCand* cand_all,
+                   int* cand_cnt, cudaStream_t st);
 void launch_select_finish(const double* d2_all, long long m, const int* inst, int ninst, SelState* st_all,
                           unsigned int* hist_all, unsigned int* cnt_all, uint8_t* mem_new_all,
                           const uint8_t* mem_old_all, int* changed, int* list_all, int* seg_cnt_all, int nseg,
-                          long long seg_len, cudaStream_t st);
+                          long long seg_len, SelCand* cand_all, int* cand_cnt, cudaStream_t st);
 
 }  // namespace rtd
