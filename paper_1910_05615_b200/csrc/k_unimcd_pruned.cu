@@ -564,8 +564,23 @@ __device__ __forceinline__ VBound window_bounds(long long s, long long h, int b,
   return start_bounds(run_const(b, be, c, C, A1, Q2lo, Q2hi, sb), s, h, m);
 }
 
-__device__ __forceinline__ int rank_bucket(const long long* C, long long r) {  // largest b with C[b] <= r
+// k_pr_locate's rank -> bucket index: RT_N coarse cells of 2^sh ranks (sh in entry RT_N), cell k holding
+// rank_bucket(k 2^sh); a query searches only between the buckets of its cell's two ends (a few instead of
+// the 12 dependent shared-memory loads of a search over all NBK buckets -- the search was ~25 % of the
+// kernel).  The table lives right after C in LocSmem: every caller passes LocSmem::C.
+static constexpr int RT_N = 256;  // (LocSmem + static shared must stay within the 228 KB of an SM)
+__device__ __forceinline__ int rank_bucket_full(const long long* C, long long r) {  // largest b with C[b] <= r
   int lo = 0, hi = NBK - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (C[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ int rank_bucket(const long long* C, long long r) {  // largest b with C[b] <= r
+  const unsigned short* R = reinterpret_cast<const unsigned short*>(C + NBK + 1);
+  const long long k = r >> R[RT_N];
+  int lo = R[k], hi = k + 1 < RT_N ? R[k + 1] : NBK - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
     if (C[mid] <= r) lo = mid; else hi = mid - 1;
@@ -635,6 +650,7 @@ static constexpr int UB1 = 4096;      // strided starts of the first upper-bound
 
 struct LocSmem {  // one column's bucket prefix arrays (the layout of window_bounds' arguments)
   long long C[NBK + 1];
+  unsigned short rt[RT_N + 4];  // rank_bucket's cell table (must follow C), rt[RT_N] = the cell shift
   double sb[2 * NBK];          // [lo | hi] bucket sum intervals
   double A1[2 * (NBK + 1)];    // [lo | hi] prefix sums of the bucket sums
   double Q2lo[NBK + 1], Q2hi[NBK + 1];
@@ -699,6 +715,13 @@ __global__ void __launch_bounds__(LT) k_pr_locate(long long len, long long h, Pr
   c.cmax = __dsub_ru(ord_val(mm[2 * col + 1]), c.cs);
   scan_column(c, len < PACK_LEN, cnt + (long long)col * NBK, tq + (long long)col * NBK, esum + 4 * col, S.C, S.sb, S.A1, S.Q2lo,
               S.Q2hi, bs);
+  {  // rank_bucket's cell table (scan_column ended with a barrier: C is complete)
+    int sh = 0;
+    while (((long long)RT_N << sh) < len) sh++;
+    for (int k = threadIdx.x; k < RT_N; k += LT) S.rt[k] = (unsigned short)rank_bucket_full(S.C, (long long)k << sh);
+    if (threadIdx.x == 0) S.rt[RT_N] = (unsigned short)sh;
+    __syncthreads();
+  }
   const long long* C = S.C;
   const BucketScan m = bs;
   const long long nwin = len - h + 1;
@@ -1120,11 +1143,12 @@ __global__ void __launch_bounds__(1024) k_pr_prefix(int npc, const PrunedCol* __
 static constexpr int SMAX = 16384;
 __global__ void __launch_bounds__(1024) k_pr_sortprefix(int npc, const PrunedCol* __restrict__ pc, const double* __restrict__ g,
                                                         const int* __restrict__ gcount, const dd2* __restrict__ below,
-                                                        dd2* __restrict__ pref) {
+                                                        dd2* __restrict__ pref, int cmin, int cmax) {
   extern __shared__ double sv[];
   const int seg = blockIdx.x, col = seg >> 1, side = seg & 1;
   if (pc[col].status) return;
   const int cn = min(gcount[seg], CAP);
+  if (cn < cmin || cn > cmax) return;  // this launch's class of segment lengths
   int np2 = 1;
   while (np2 < cn) np2 <<= 1;
   const double* src = g + (long long)seg * CAP;
@@ -1510,11 +1534,24 @@ bool unimcd_pruned(Arena& A, cudaStream_t st, const double* cols, long long len,
     int np2 = 1;
     while (np2 < gmax) np2 <<= 1;
     // 256 threads: many segments (2 per column) share each SM; measured 0.43 -> 0.34 ms per 640-column call
-    // against 1024 threads (a CTA-wide barrier per bitonic stage costs more than the pairs per thread)
-    constexpr int spt = 256;
-    k_pr_sortprefix<<<2 * ncols, spt, std::min(smem, np2 * (int)sizeof(double)), st>>>(npc, s.pc, s.g, s.gcount,
-                                                                                         s.below, s.pref);
+    // against 1024 threads (a CTA-wide barrier per bitonic stage costs more than the pairs per thread).
+    // The shared memory of a launch is sized by its largest segment, so a few long segments (a column
+    // with a wide candidate range) would cut every CTA's occupancy: segments up to SPLIT go in a launch
+    // sized for them, the longer ones (if any) in a second launch (each skips the other's).
+    constexpr int spt = 256, SPLIT = 4096;
+    int np2s = 1;
+    for (int v : gc)
+      if (v <= SPLIT)
+        while (np2s < v) np2s <<= 1;
+    k_pr_sortprefix<<<2 * ncols, spt, np2s * (int)sizeof(double), st>>>(npc, s.pc, s.g, s.gcount, s.below, s.pref,
+                                                                         0, SPLIT);
     RTD_LAUNCHED();
+    if (gmax > SPLIT) {
+      k_pr_sortprefix<<<2 * ncols, spt, std::min(smem, np2 * (int)sizeof(double)), st>>>(npc, s.pc, s.g, s.gcount,
+                                                                                           s.below, s.pref, SPLIT + 1,
+                                                                                           SMAX);
+      RTD_LAUNCHED();
+    }
   } else {  // chunk sorts + merge rounds (no library sort on the fit path)
     static const int csmem = [] {
       cudaFuncSetAttribute(k_pr_chunksort, cudaFuncAttributeMaxDynamicSharedMemorySize, SMAX * (int)sizeof(double));

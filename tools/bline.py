@@ -13,6 +13,6 @@ for line in open(sys.argv[1]):
         print("latency", d["latency_ms"], "warm", d.get("warm_start", {}).get("latency_ms"))
     for k, v in d.get("breakdown", {}).items():
         print(f"  {k:16s} {v['ms_per_step']:8.3f} ms  x{v['launches_per_step']}")
-    for k, v in d.get("sub", {}).items():
+    for k, v in (d.get("sub") or {}).items():
         print(f"sub {k}: value {v.get('value', 0) / 1e6:.2f} M ms/step {v.get('ms_per_step')}",
               "latency", v.get("latency_ms"), "warm", v.get("warm_start", {}).get("latency_ms"))
