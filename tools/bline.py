@@ -8,7 +8,7 @@ for line in open(sys.argv[1]):
         continue
     d = json.loads(line)
     print(f"value {d.get('value', 0) / 1e6:.1f} M {d.get('unit')}  ms/step {d.get('ms_per_step', 0):.3f}  "
-          f"e2e {d.get('e2e', {}).get('value', 0) / 1e6:.1f} M  roofline {d.get('roofline', {}).get('frac')}")
+          f"e2e {(d.get('e2e') or {}).get('value', 0) / 1e6:.1f} M  roofline {(d.get('roofline') or {}).get('frac')}")
     if "latency_ms" in d:
         print("latency", d["latency_ms"], "warm", d.get("warm_start", {}).get("latency_ms"))
     for k, v in d.get("breakdown", {}).items():
