@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -223,9 +225,15 @@ size_t uni_bytes(long long len, int ncols) {
   return a.off + 4096;
 }
 
-size_t sort_bytes(long long len) {
+size_t sort_bytes(long long len) {  // memoised (CUB's query does host-side occupancy queries)
+  static std::mutex mu;
+  static std::map<long long, size_t> memo;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = memo.find(len);
+  if (it != memo.end()) return it->second;
   size_t b = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, b, (const double*)nullptr, (double*)nullptr, (int)len);
+  memo[len] = b;
   return b;
 }
 
@@ -407,10 +415,7 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
   const int cstride = p + (full_inv ? p * p : p * (p + 1) / 2);
   if (smw) RTD_CU(cudaMemsetAsync(b.smw_valid, 0, ninst * sizeof(int), st));
   const int np = mom_np(p);
-  RTD_CU(cudaMemsetAsync(b.memA, 0, (size_t)ninst * m, st));
-  RTD_CU(cudaMemsetAsync(b.memB, 0, (size_t)ninst * m, st));
-  RTD_CU(cudaMemsetAsync(b.hist, 0, (size_t)ninst * 4096 * sizeof(unsigned int), st));
-  RTD_CU(cudaMemsetAsync(b.sel, 0, (size_t)ninst * sizeof(SelState), st));
+  RTD_CU(cudaMemsetAsync(b.memA, 0, (size_t)ninst * m, st));  // (instances not launched keep an empty subset)
   h2d(st, b.status, status_h.data(), ninst * sizeof(int));
   steps_h.assign(ninst, 0);
   std::vector<int> act, changed(ninst);
@@ -435,6 +440,10 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     for (int i : act) steps_h[i] = steps_all[i];
     return;
   }
+  // (the one-launch loops above keep their state on chip: these only serve the multi-launch loop)
+  RTD_CU(cudaMemsetAsync(b.memB, 0, (size_t)ninst * m, st));
+  RTD_CU(cudaMemsetAsync(b.hist, 0, (size_t)ninst * 4096 * sizeof(unsigned int), st));
+  RTD_CU(cudaMemsetAsync(b.sel, 0, (size_t)ninst * sizeof(SelState), st));
   MomArgs ma = mom_args(b, Z, blk_stride, nstart);
   uint8_t* memA = b.memA;  // latest membership
   uint8_t* memB = b.memB;

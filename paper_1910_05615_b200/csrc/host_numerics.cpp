@@ -8,12 +8,52 @@
 // last representable double.
 #include <cmath>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace rtd {
 
 static std::atomic<long long> g_launches{0}, g_sorts{0};
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// RTD_TRACE_HOST=1: host timestamp and call site of every launch, the last TRACE_N printed at exit as deltas
+// (where the host spends its time between launches on a latency-bound fit)
+static constexpr int TRACE_N = 4096;
+struct TraceEnt {
+  long long ns;
+  const char* file;
+  int line;
+};
+static TraceEnt g_trace[TRACE_N];
+static std::atomic<long long> g_ntrace{0};
+static void dump_trace() {
+  const long long n = g_ntrace.load(), n0 = n > 400 ? n - 400 : 0;
+  for (long long i = n0 + 1; i < n; i++) {
+    const TraceEnt& a = g_trace[(i - 1) % TRACE_N];
+    const TraceEnt& b = g_trace[i % TRACE_N];
+    std::fprintf(stderr, "[trace] %8.1f us  %s:%d\n", (b.ns - a.ns) * 1e-3, std::strrchr(b.file, '/') ? std::strrchr(b.file, '/') + 1 : b.file, b.line);
+  }
+}
+static bool trace_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RTD_TRACE_HOST");
+    v = (e && e[0] == '1') ? 1 : 0;
+    if (v) std::atexit(dump_trace);
+  }
+  return v == 1;
+}
+void count_launch(const char* file, int line) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (trace_on()) {
+    const long long k = g_ntrace.fetch_add(1);
+    g_trace[k % TRACE_N] = {std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                std::chrono::steady_clock::now().time_since_epoch()).count(), file, line};
+  }
+}
 void count_sort() { g_sorts.fetch_add(1, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(); }
 long long sort_count() { return g_sorts.load(); }
@@ -60,7 +100,25 @@ static double gamma_p(double a, double x) {
 
 double chi2_cdf(double x, int dof) { return gamma_p(0.5 * dof, 0.5 * x); }
 
+// The quantile and the consistency factor are memoised per argument pair: a bisection to the last double over
+// the incomplete-gamma series costs tens of microseconds, and a fit asks for the same few values every call
+// (on a latency-bound 20,000-row fit that host time left the GPU idle between launches).
+static double chi2_quantile_raw(double prob, int dof);
+static std::mutex g_memo_mu;
+static std::map<std::pair<double, int>, double> g_q_memo, g_c_memo;
 double chi2_quantile(double prob, int dof) {
+  {
+    std::lock_guard<std::mutex> lk(g_memo_mu);
+    auto it = g_q_memo.find({prob, dof});
+    if (it != g_q_memo.end()) return it->second;
+  }
+  const double v = chi2_quantile_raw(prob, dof);
+  std::lock_guard<std::mutex> lk(g_memo_mu);
+  g_q_memo[{prob, dof}] = v;
+  return v;
+}
+
+static double chi2_quantile_raw(double prob, int dof) {
   double lo = 0.0, hi = std::fmax(1.0, (double)dof);
   while (chi2_cdf(hi, dof) < prob) hi *= 2.0;
   for (int it = 0; it < 2000; it++) {
@@ -74,7 +132,15 @@ double chi2_quantile(double prob, int dof) {
 
 double consistency_factor(double alpha, int p) {
   if (alpha >= 1.0) return 1.0;
-  return alpha / chi2_cdf(chi2_quantile(alpha, p), p + 2);
+  {
+    std::lock_guard<std::mutex> lk(g_memo_mu);
+    auto it = g_c_memo.find({alpha, p});
+    if (it != g_c_memo.end()) return it->second;
+  }
+  const double v = alpha / chi2_cdf(chi2_quantile(alpha, p), p + 2);
+  std::lock_guard<std::mutex> lk(g_memo_mu);
+  g_c_memo[{alpha, p}] = v;
+  return v;
 }
 
 }  // namespace rtd

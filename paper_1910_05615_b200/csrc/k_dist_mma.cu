@@ -310,7 +310,7 @@ static void flag_mma_launch(const double* X, long long n, int log_transform, con
   constexpr int MB = 1, S = P + 1, TR = 8 * MB;
   const int smem = 8 * 2 * TR * S * (int)sizeof(double);
   static const bool attr = [&] {
-    RTD_CU(cudaFuncSetAttribute(k_flag_mma<P, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    set_max_dyn_smem(reinterpret_cast<const void*>(k_flag_mma<P, MB>), smem);
     return true;
   }();
   (void)attr;

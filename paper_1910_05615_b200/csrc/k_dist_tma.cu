@@ -380,7 +380,7 @@ void matmul_tma_launch(const double* Zall, long long m, int nblk, const int* slo
   const long long per_item = std::max<long long>(1, 148LL / npairs);
   const int tpc = (int)std::max<long long>(1, (ntiles + per_item - 1) / per_item);
   const unsigned gx = (unsigned)((ntiles + tpc - 1) / tpc);
-  RTD_CU(cudaFuncSetAttribute(k_matmul_tma<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  set_max_dyn_smem(reinterpret_cast<const void*>(k_matmul_tma<P>), (int)C::SMEM);
   k_matmul_tma<P><<<dim3(gx, npairs), C::NW * 32, C::SMEM, st>>>(map, m, pairs, slot_of, blk_of_slot, W_all, out_all,
                                                                   tpc);
 }
@@ -416,7 +416,7 @@ void dist_tma_launch_v(const CUtensorMap& map, long long m, const int* pairs, in
   const long long per_item = std::max<long long>(1, 148LL * C::MINB / npairs);
   const int tpc = (int)std::max<long long>(1, (ntiles + per_item - 1) / per_item);
   const unsigned gx = (unsigned)((ntiles + tpc - 1) / tpc);
-  RTD_CU(cudaFuncSetAttribute(k_dist_tma<P, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  set_max_dyn_smem(reinterpret_cast<const void*>(k_dist_tma<P, V>), (int)C::SMEM);
   k_dist_tma<P, V><<<dim3(gx, npairs), (C::NCW + 1) * 32, C::SMEM, st>>>(map, m, pairs, inst, nstart, cstage, cstride,
                                                                          d2_all, tpc);
 }

@@ -999,12 +999,12 @@ void launch_csteps_cluster(const double* Zall, long long m, int p, long long blk
   const size_t dyn = (3 * (size_t)RTD_MAXP * LD + std::max<size_t>((size_t)CSC_ROWS, (size_t)CS_W * nred)) *
                      sizeof(double);
   if (nb == 1) {
-    RTD_CU(cudaFuncSetAttribute(k_csteps_cluster<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    set_max_dyn_smem(reinterpret_cast<const void*>(k_csteps_cluster<1>), (int)dyn);
     k_csteps_cluster<1><<<ninst * CSC_CL, CS_T, dyn, st>>>(Zall, (int)m, p, blk_stride, nstart, inst, (int)h,
                                                            kappa_max, max_steps, mu_all, sigma_all, status_all,
                                                            steps_all, logdet_all, traj, traj_stride, mem_all);
   } else {
-    RTD_CU(cudaFuncSetAttribute(k_csteps_cluster<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    set_max_dyn_smem(reinterpret_cast<const void*>(k_csteps_cluster<2>), (int)dyn);
     k_csteps_cluster<2><<<ninst * CSC_CL, CS_T, dyn, st>>>(Zall, (int)m, p, blk_stride, nstart, inst, (int)h,
                                                            kappa_max, max_steps, mu_all, sigma_all, status_all,
                                                            steps_all, logdet_all, traj, traj_stride, mem_all);

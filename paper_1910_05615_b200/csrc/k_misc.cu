@@ -5,12 +5,28 @@
 #include <cstring>
 #include <vector>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "rtd_internal.h"
 
 namespace rtd {
 
 // Several device -> host reads behind ONE stream synchronisation: the copies land in a pinned staging
 // buffer (a copy into pageable memory would synchronise by itself), then are unpacked.
+void set_max_dyn_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  RTD_CU(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = done[{dev, func}];
+  if (bytes <= cur) return;
+  RTD_CU(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  cur = bytes;
+}
+
 void fetch(cudaStream_t st, std::initializer_list<Fetch> items) {
   static thread_local char* stage = nullptr;
   static thread_local size_t cap = 0;

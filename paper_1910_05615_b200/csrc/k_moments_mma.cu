@@ -374,7 +374,7 @@ static void moments_mma_nb(int mode, const MomArgs& a, int ninst, cudaStream_t s
                                  (size_t)a.p * SR * sizeof(int));
 #define RTD_ST_CASE(M)                                                                                   \
   case M:                                                                                                \
-    RTD_CU(cudaFuncSetAttribute(k_moments_st<NB, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    set_max_dyn_smem(reinterpret_cast<const void*>(k_moments_st<NB, M>), (int)smem); \
     k_moments_st<NB, M><<<grid, MW * 32, smem, st>>>(a);                                                 \
     break;
     switch (mode) {
@@ -389,8 +389,7 @@ static void moments_mma_nb(int mode, const MomArgs& a, int ninst, cudaStream_t s
   const size_t smem = (size_t)MW * NP * sizeof(double);
 #define RTD_MM_CASE(M)                                                                                   \
   case M:                                                                                                \
-    RTD_CU(cudaFuncSetAttribute(k_moments_mma<NB, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                (int)smem));                                                             \
+    set_max_dyn_smem(reinterpret_cast<const void*>(k_moments_mma<NB, M>), (int)smem);                   \
     k_moments_mma<NB, M><<<grid, MW * 32, smem, st>>>(a);                                                \
     break;
   switch (mode) {

@@ -335,7 +335,7 @@ void moments_tma_pw(int mode, const MomArgs& a, int ninst, cudaStream_t st) {
   dim3 grid(a.ctas, ninst);
 #define RTD_MT_CASE(M)                                                                                        \
   case M:                                                                                                     \
-    RTD_CU(cudaFuncSetAttribute(k_moments_tma<P, M, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM)); \
+    set_max_dyn_smem(reinterpret_cast<const void*>(k_moments_tma<P, M, W>), (int)C::SMEM); \
     k_moments_tma<P, M, W><<<grid, C::NCW * 32, C::SMEM, st>>>(map, wmap, a);                                   \
     break;
   switch (mode) {

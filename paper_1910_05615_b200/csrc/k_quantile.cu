@@ -9,6 +9,8 @@
 // The values returned are the exact order statistics (the bucket map only routes).
 // A block whose target bucket holds more than QCAP elements (massive ties) is flagged
 // and the caller sorts that block instead (same result).
+#include <cstdlib>
+
 #include "rtd_internal.h"
 
 namespace rtd {
@@ -211,6 +213,77 @@ __global__ void k_q_from_sorted(const double* __restrict__ sorted, long long m, 
   if (threadIdx.x < QTARGETS) qv[b * QTARGETS + threadIdx.x] = sorted[q_target(m, threadIdx.x)];
 }
 
+// Fallback for a flagged block (a target bucket over QCAP elements: massive ties, or a degenerate sample span),
+// on the device: the six order statistics by an exact radix select over all m norms (ordered 64-bit keys,
+// digits of 12 bits from the top, a 4096-bin shared histogram per level among the keys that share the
+// target's prefix, the last level 4 bits) -- one CTA per block, exits at once for an unflagged one.  No host
+// round trip decides whether it is needed (the bucketed path used to read the flags back).
+__global__ void __launch_bounds__(1024) k_q_exact(const double* __restrict__ r_all, long long m,
+                                                  const QMap* __restrict__ maps, double* __restrict__ qv) {
+  __shared__ unsigned int h[4096];
+  __shared__ long long wsum[32];
+  __shared__ int s_bin;
+  __shared__ long long s_bef;
+  const int b = blockIdx.x;
+  if (!maps[b].status) return;
+  const double* r = r_all + (long long)b * m;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int k = 0; k < QTARGETS; k++) {
+    long long rank = q_target(m, k);  // 0-based
+    unsigned long long pre = 0ull;
+    int plen = 0;
+    while (plen < 64) {
+      const int dig = plen + 12 <= 64 ? 12 : 64 - plen, sh = 64 - plen - dig;
+      for (int i = t; i < 4096; i += blockDim.x) h[i] = 0u;
+      __syncthreads();
+      for (long long i = t; i < m; i += blockDim.x) {
+        const unsigned long long key = ord_key64(r[i]);
+        if (plen == 0 || (key >> (64 - plen)) == pre) atomicAdd(&h[(unsigned)(key >> sh) & ((1u << dig) - 1u)], 1u);
+      }
+      __syncthreads();
+      // thread t owns bins 4t .. 4t+3 (1024 threads)
+      long long c[4], loc = 0;
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        c[e] = h[4 * t + e];
+        loc += c[e];
+      }
+      long long inc = loc;
+      for (int d = 1; d < 32; d <<= 1) {
+        const long long v = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += v;
+      }
+      if (lane == 31) wsum[w] = inc;
+      __syncthreads();
+      if (t < 32) {
+        const long long v = wsum[t];
+        long long x = v;
+        for (int d = 1; d < 32; d <<= 1) {
+          const long long y = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane >= d) x += y;
+        }
+        wsum[t] = x - v;
+      }
+      __syncthreads();
+      long long before = wsum[w] + inc - loc;
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        if (c[e] > 0 && before <= rank && rank < before + c[e]) {
+          s_bin = 4 * t + e;
+          s_bef = before;
+        }
+        before += c[e];
+      }
+      __syncthreads();
+      pre = (pre << dig) | (unsigned long long)s_bin;
+      rank -= s_bef;
+      plen += dig;
+      __syncthreads();
+    }
+    if (t == 0) qv[b * QTARGETS + k] = ord_val64(pre);
+  }
+}
+
 // A = median, B = A + 1.5 IQR from the six order statistics (type-7 interpolation)
 __global__ void k_q_cutoffs(const double* __restrict__ qv, long long m, int nb, double* __restrict__ AB,
                             int* __restrict__ ok) {
@@ -285,10 +358,16 @@ void launch_quantiles(const double* r_all, long long m, int nb, char* scratch, d
   (void)attr;
   k_q_pick<<<dim3(QTARGETS, nb), 1024, QCAP * sizeof(double), st>>>(maps, gbuf, gcount, qv);
   RTD_LAUNCHED();
+  fallback.clear();
+  static const bool host_fb = getenv("RTD_Q_HOSTFALLBACK") != nullptr;  // r02: flags read back, CUB sort
+  if (!host_fb) {
+    k_q_exact<<<nb, 1024, 0, st>>>(r_all, m, maps, qv);
+    RTD_LAUNCHED();
+    return;
+  }
   std::vector<QMap> h(nb);
   RTD_CU(cudaMemcpyAsync(h.data(), maps, nb * sizeof(QMap), cudaMemcpyDeviceToHost, st));
   RTD_CU(cudaStreamSynchronize(st));
-  fallback.clear();
   for (int b = 0; b < nb; b++)
     if (h[b].status) fallback.push_back(b);
 }

@@ -13,6 +13,9 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "rtd_internal.h"
 
@@ -1036,7 +1039,23 @@ static int id_bits(int ncols) {
 // by column id, which leaves every column sorted and contiguous.
 static constexpr int USORT = 256;  // columns per pass of the sort path (8-bit segment ids)
 
+static size_t cub_sort_bytes_raw(long long len, int ncols);
+// memoised: CUB's temporary-storage query runs occupancy queries on the host (~40 us per call, three calls
+// per fit, with the GPU idle behind them on a latency-bound fit)
 static size_t cub_sort_bytes(long long len, int ncols) {
+  static std::mutex mu;
+  static std::map<std::pair<long long, int>, size_t> memo;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find({len, ncols});
+    if (it != memo.end()) return it->second;
+  }
+  const size_t v = cub_sort_bytes_raw(len, ncols);
+  std::lock_guard<std::mutex> lk(mu);
+  memo[{len, ncols}] = v;
+  return v;
+}
+static size_t cub_sort_bytes_raw(long long len, int ncols) {
   const long long N = len * ncols;
   size_t b1 = 0, b2 = 0;
   if (ncols == 1) {
@@ -1105,19 +1124,19 @@ void unimcd_batch(Arena& A, cudaStream_t st, const double* cols, long long len, 
     if (csort && !split && len <= (long long)UCS_CL * UCS_CAP && len / 2 + 1 <= (long long)UCS_CL * UCS_CAP) {
       // sort + scans + window + reweighting in one cluster launch per batch of columns
       const int dyn = 3 * UCS_CAP * (int)sizeof(unsigned long long);
-      RTD_CU(cudaFuncSetAttribute(k_uni_cluster_mcd, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+      set_max_dyn_smem(reinterpret_cast<const void*>(k_uni_cluster_mcd), dyn);
       k_uni_cluster_mcd<<<nc * UCS_CL, UCM_T, dyn, st>>>(cc, len, h, uc, out_dev + c0);
       RTD_LAUNCHED();
       continue;
     }
     if (csort) {  // one 8-CTA cluster per column, no library sort
       const int dyn = 4 * UCS_CAP * (int)sizeof(unsigned long long);
-      RTD_CU(cudaFuncSetAttribute(k_uni_cluster_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+      set_max_dyn_smem(reinterpret_cast<const void*>(k_uni_cluster_sort), dyn);
       k_uni_cluster_sort<<<nc * UCS_CL, UCS_T, dyn, st>>>(cc, len, s.sorted);
       RTD_LAUNCHED();
       if (len <= USORTED) {  // the scans, windows and reweighting of each sorted column in one CTA
         const int smem = (int)((((len + 3) & ~3LL) * sizeof(double)) + (UST + 1) * sizeof(dd2));
-        RTD_CU(cudaFuncSetAttribute(k_uni_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        set_max_dyn_smem(reinterpret_cast<const void*>(k_uni_small<true>), smem);
         k_uni_small<true><<<nc, UST, smem, st>>>(s.sorted, (int)len, (int)h, uc, out_dev + c0);
         RTD_LAUNCHED();
         continue;

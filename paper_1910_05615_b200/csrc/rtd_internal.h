@@ -22,11 +22,14 @@ struct CudaError {
     if (e__ != cudaSuccess) throw ::rtd::CudaError{e__, #x};              \
   } while (0)
 bool debug_sync();  // RTD_DEBUG_SYNC=1: synchronise and check after every launch
-void count_launch();  // kernels launched by this library (hand-written kernels)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size): the runtime call costs
+// microseconds of host time, on the critical path of a latency-bound fit when made before every launch
+void set_max_dyn_smem(const void* func, int bytes);
+void count_launch(const char* file, int line);  // kernels launched by this library (hand-written kernels)
 void count_sort();    // CUB radix-sort invocations
 #define RTD_LAUNCHED()                                                      \
   do {                                                                      \
-    ::rtd::count_launch();                                                  \
+    ::rtd::count_launch(__FILE__, __LINE__);                                \
     RTD_CU(cudaGetLastError());                                             \
     if (::rtd::debug_sync()) {                                              \
       cudaError_t e2__ = cudaDeviceSynchronize();                           \
