@@ -986,13 +986,19 @@ __global__ void __launch_bounds__(PT, FUSED ? 4 : 5) k_pr_gather(const double* _
       a2[q] = __fma_rn(dv, dv, a2[q]);
       nmid += mid ? 1 : 0;
     }
+    bool kin = false;
     if (FUSED) {
-      const bool kin = x >= c.kin_lo && x <= c.kin_hi;
+      kin = x >= c.kin_lo && x <= c.kin_hi;
       const double dk = kin ? __dsub_rn(x, c.kc) : 0.0;
       ks1[k % NKA] = __dadd_rn(ks1[k % NKA], dk);
       ks2[k % NKA] = __fma_rn(dk, dk, ks2[k % NKA]);
       kn += kin ? 1 : 0;
-      const bool inb = !kin && x >= c.kout_lo && x <= c.kout_hi;
+    }
+    const bool inb = FUSED && !kin && x >= c.kout_lo && x <= c.kout_hi;
+    const bool inS = geS && x < c.tS1, inE = geE && x < c.tE1;
+    // one vote for both rare cases (band values of the fused reweighting, candidate window ends)
+    if (!__any_sync(0xffffffffu, inS || inE || inb)) return;
+    if (FUSED) {
       if (__any_sync(0xffffffffu, inb)) {  // rare: the bands hold ~1e-4 of the values
         const unsigned mb = __ballot_sync(0xffffffffu, inb);
         int pos = 0;
@@ -1008,8 +1014,7 @@ __global__ void __launch_bounds__(PT, FUSED ? 4 : 5) k_pr_gather(const double* _
         }
       }
     }
-    const bool inS = geS && x < c.tS1, inE = geE && x < c.tE1;
-    if (!__any_sync(0xffffffffu, inS || inE)) return;  // the common case: one vote, no candidate
+    if (!__any_sync(0xffffffffu, inS || inE)) return;
     const unsigned ms = __ballot_sync(0xffffffffu, inS), me = __ballot_sync(0xffffffffu, inE);
 #pragma unroll
     for (int side = 0; side < 2; side++) {  // one shared atomic per warp and side
