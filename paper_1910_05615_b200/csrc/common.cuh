@@ -191,22 +191,27 @@ __device__ __forceinline__ double ord_val64(unsigned long long k) {
 // x[k]: strides below V inside a thread, below 32 V by warp shuffles, the rest through xs[N] (two barriers
 // per such stage).  For 4096 keys and 1024 threads: 15 shared-memory stages instead of the 78 barriers of
 // a shared-memory network (k_q_sample 43 -> ~6 us).
-template <int V>
-__device__ __forceinline__ void bitonic_inreg_stage(unsigned long long (&x)[V], int stride, int size) {
+template <int V, int S>
+__device__ __forceinline__ void bitonic_inreg_s(unsigned long long (&x)[V], int size) {
 #pragma unroll
   for (int k = 0; k < V; k++) {
-#pragma unroll
-    for (int S = 1; S < V; S <<= 1) {
-      if (S == stride && (k & S) == 0) {
-        const int e = threadIdx.x * V + k;
-        const bool up = (e & size) == 0;
-        const unsigned long long a = x[k], b = x[k + S];
-        const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
-        x[k] = up ? lo : hi;
-        x[k + S] = up ? hi : lo;
-      }
+    if ((k & S) == 0) {  // compile-time: only the V/2 pairs of this stride
+      const int e = threadIdx.x * V + k;
+      const bool up = (e & size) == 0;
+      const unsigned long long a = x[k], b = x[k + S];
+      const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
+      x[k] = up ? lo : hi;
+      x[k + S] = up ? hi : lo;
     }
   }
+}
+template <int V>
+__device__ __forceinline__ void bitonic_inreg_stage(unsigned long long (&x)[V], int stride, int size) {
+  if constexpr (V > 1) if (stride == 1) { bitonic_inreg_s<V, 1>(x, size); return; }
+  if constexpr (V > 2) if (stride == 2) { bitonic_inreg_s<V, (V > 2 ? 2 : 1)>(x, size); return; }
+  if constexpr (V > 4) if (stride == 4) { bitonic_inreg_s<V, (V > 4 ? 4 : 1)>(x, size); return; }
+  if constexpr (V > 8) if (stride == 8) { bitonic_inreg_s<V, (V > 8 ? 8 : 1)>(x, size); return; }
+  if constexpr (V > 16) if (stride == 16) { bitonic_inreg_s<V, (V > 16 ? 16 : 1)>(x, size); return; }
 }
 template <int V>
 __device__ void block_bitonic_keys(unsigned long long (&x)[V], unsigned long long* xs) {
