@@ -110,12 +110,10 @@ __device__ __noinline__ bool block_chol_inv(const double* A, double* L, double* 
       else Li[j * LD + e] *= ri;             // row j of Li (columns 0..j)
     }
     __syncthreads();
-    for (int i = j + 1 + wid; i < p; i += nw) {
+    for (int i = j + 1 + wid; i < p; i += nw) {  // (two loops: no lane divergence between the L and Li parts)
       const double lij = L[i * LD + j];
-      for (int k = lane; k <= i; k += 32) {
-        if (k <= j) Li[i * LD + k] = fma(-lij, Li[j * LD + k], Li[i * LD + k]);
-        else L[i * LD + k] = fma(-lij, L[k * LD + j], L[i * LD + k]);
-      }
+      for (int k = lane; k <= j; k += 32) Li[i * LD + k] = fma(-lij, Li[j * LD + k], Li[i * LD + k]);
+      for (int k = j + 1 + lane; k <= i; k += 32) L[i * LD + k] = fma(-lij, L[k * LD + j], L[i * LD + k]);
     }
     __syncthreads();
   }
@@ -134,8 +132,11 @@ __device__ __noinline__ double block_max_colsum_abs(const double* A, int p, doub
     red[t] = s;
   }
   __syncthreads();
-  double mx = 0.0;
-  for (int j = 0; j < p; j++) mx = fmax(mx, red[j]);
+  // every warp takes the max of the p column sums by a butterfly (max is exact: any order gives the same value)
+  const int lane = t & 31;
+  double mx = lane < p ? red[lane] : 0.0;
+  if (lane + 32 < p) mx = fmax(mx, red[lane + 32]);
+  for (int d = 16; d > 0; d >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
   __syncthreads();
   return mx;
 }
