@@ -1446,7 +1446,7 @@ __global__ void __launch_bounds__(32 * (RTD_MAXP / 2)) k_jacobi_os(const double*
                                                                    double* __restrict__ lam_all,
                                                                    int* __restrict__ ok_all) {
   __shared__ double Ac[RTD_MAXP][JCS], Vc[RTD_MAXP][JCS];
-  __shared__ double lam_s[RTD_MAXP];
+  __shared__ double lam_s[RTD_MAXP], nrm[RTD_MAXP];
   __shared__ int order[RTD_MAXP];
   __shared__ int s_rot[3];
   __shared__ unsigned char pq[RTD_MAXP - 1][RTD_MAXP / 2][2];  // round-robin schedule: (P, Q) of pair w in a round
@@ -1479,18 +1479,24 @@ __global__ void __launch_bounds__(32 * (RTD_MAXP / 2)) k_jacobi_os(const double*
   for (int sweep = 0; sweep < 60; sweep++) {
     const int fs = sweep % 3;
     if (t == 0) s_rot[(sweep + 1) % 3] = 0;  // the next sweep's flag (triple-buffered: no reader races)
+    // squared column norms, recomputed at every sweep and carried through the rotations of the sweep
+    // (a_P' = c a_P - s a_Q: alpha' = c^2 alpha - 2 c s gamma + s^2 beta, beta' = s^2 alpha + 2 c s gamma +
+    // c^2 beta), so a round reduces one dot product instead of three
+    for (int j = w; j < p; j += nw) {
+      double v = fma(Ac[j][lane], Ac[j][lane], Ac[j][lane + 32] * Ac[j][lane + 32]);
+      for (int d = 1; d < lanes; d <<= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+      if (lane == 0) nrm[j] = v;
+    }
+    __syncthreads();
     for (int round = 0; round < n2 - 1; round++) {
       if (w < n2 / 2) {
         const int P = pq[round][w][0], Q = pq[round][w][1];
         if (Q < p) {
           double aP0 = Ac[P][lane], aP1 = Ac[P][lane + 32], aQ0 = Ac[Q][lane], aQ1 = Ac[Q][lane + 32];
-          double al = fma(aP0, aP0, aP1 * aP1), be = fma(aQ0, aQ0, aQ1 * aQ1), ga = fma(aP0, aQ0, aP1 * aQ1);
-          // butterfly over the lanes that hold rows (the others hold zeros): every such lane gets the sums
-          for (int d = 1; d < lanes; d <<= 1) {
-            al += __shfl_xor_sync(0xffffffffu, al, d);
-            be += __shfl_xor_sync(0xffffffffu, be, d);
-            ga += __shfl_xor_sync(0xffffffffu, ga, d);
-          }
+          const double al = nrm[P], be = nrm[Q];
+          double ga = fma(aP0, aQ0, aP1 * aQ1);
+          // butterfly over the lanes that hold rows (the others hold zeros): every such lane gets the sum
+          for (int d = 1; d < lanes; d <<= 1) ga += __shfl_xor_sync(0xffffffffu, ga, d);
           if (ga != 0.0 && ga * ga > tol * tol * al * be) {
             // the rotation zeroing a_P . a_Q (zeta = (be - al) / (2 ga), t = tan theta = sign(zeta) / (|zeta| +
             // sqrt(1 + zeta^2))) from two rsqrt and no division: with h = (be - al) / 2, r = sqrt(h^2 + ga^2),
@@ -1509,7 +1515,12 @@ __global__ void __launch_bounds__(32 * (RTD_MAXP / 2)) k_jacobi_os(const double*
             Vc[Q][lane] = s * vP0 + c * vQ0;
             Vc[P][lane + 32] = c * vP1 - s * vQ1;
             Vc[Q][lane + 32] = s * vP1 + c * vQ1;
-            if (lane == 0) s_rot[fs] = 1;
+            if (lane == 0) {
+              s_rot[fs] = 1;
+              const double cc = c * c, ss = s * s, cs2 = 2.0 * c * s * ga;
+              nrm[P] = fma(cc, al, fma(ss, be, -cs2));
+              nrm[Q] = fma(ss, al, fma(cc, be, cs2));
+            }
           }
         }
       }
