@@ -97,23 +97,57 @@ __device__ __noinline__ bool block_chol_inv(const double* A, double* L, double* 
     }
   __syncthreads();
   bool ok = true;
-  for (int j = 0; j < p; j++) {
-    const double d = L[j * LD + j];
-    if (!(d > 0.0) || !isfinite(d)) {
+  // two columns per step (a 2 x 2 pivot block, every thread computing it redundantly from the same shared
+  // values): half the barriers of the one-column loop; a last single column when p is odd
+  int j = 0;
+  for (; j + 1 < p; j += 2) {
+    const double d0 = L[j * LD + j];
+    if (!(d0 > 0.0) || !isfinite(d0)) {
       ok = false;
       break;
     }
-    const double ri = rsqrt(d), r = d * ri;  // one slow fp64 operation on the chain (rsqrt ~55 cycles)
-    if (t == 0) rd[j] = r;
+    const double r0i = rsqrt(d0), r0 = d0 * r0i;
+    const double l10 = L[(j + 1) * LD + j] * r0i;
+    const double d1 = fma(-l10, l10, L[(j + 1) * LD + j + 1]);
+    if (!(d1 > 0.0) || !isfinite(d1)) {
+      ok = false;
+      break;
+    }
+    const double r1i = rsqrt(d1), r1 = d1 * r1i;
+    if (t == 0) {
+      rd[j] = r0;
+      rd[j + 1] = r1;
+    }
     for (int e = t; e < p; e += blockDim.x) {
-      if (e > j) L[e * LD + j] *= ri;        // column j of L below the pivot
-      else Li[j * LD + e] *= ri;             // row j of Li (columns 0..j)
+      if (e >= j + 2) {  // columns j, j+1 of L below the pivot block
+        const double li0 = L[e * LD + j] * r0i;
+        L[e * LD + j] = li0;
+        L[e * LD + j + 1] = fma(-li0, l10, L[e * LD + j + 1]) * r1i;
+      } else {           // rows j, j+1 of Li (columns 0..j+1; Li[j][j+1] = 0)
+        const double a0 = Li[j * LD + e] * r0i;
+        Li[j * LD + e] = a0;
+        Li[(j + 1) * LD + e] = fma(-l10, a0, Li[(j + 1) * LD + e]) * r1i;
+      }
     }
     __syncthreads();
-    for (int i = j + 1 + wid; i < p; i += nw) {  // (two loops: no lane divergence between the L and Li parts)
-      const double lij = L[i * LD + j];
-      for (int k = lane; k <= j; k += 32) Li[i * LD + k] = fma(-lij, Li[j * LD + k], Li[i * LD + k]);
-      for (int k = j + 1 + lane; k <= i; k += 32) L[i * LD + k] = fma(-lij, L[k * LD + j], L[i * LD + k]);
+    if (t == 0) L[(j + 1) * LD + j] = l10;
+    for (int i = j + 2 + wid; i < p; i += nw) {  // rank-2 updates of the rows below the block
+      const double a0 = L[i * LD + j], a1 = L[i * LD + j + 1];
+      for (int k = lane; k <= j + 1; k += 32)
+        Li[i * LD + k] = fma(-a1, Li[(j + 1) * LD + k], fma(-a0, Li[j * LD + k], Li[i * LD + k]));
+      for (int k = j + 2 + lane; k <= i; k += 32)
+        L[i * LD + k] = fma(-a1, L[k * LD + j + 1], fma(-a0, L[k * LD + j], L[i * LD + k]));
+    }
+    __syncthreads();
+  }
+  if (ok && j < p) {  // the last column (p odd): its pivot and row j of Li
+    const double d = L[j * LD + j];
+    if (!(d > 0.0) || !isfinite(d)) {
+      ok = false;
+    } else {
+      const double ri = rsqrt(d);
+      if (t == 0) rd[j] = d * ri;
+      for (int e = t; e <= j; e += blockDim.x) Li[j * LD + e] *= ri;
     }
     __syncthreads();
   }
