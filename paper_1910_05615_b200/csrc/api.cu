@@ -466,8 +466,10 @@ void run_csteps(cudaStream_t st, CStepBufs& b, const double* Z, long long blk_st
     RTD_CU(cudaMemsetAsync(b.changed, 0, ninst * sizeof(int), st));
     {
       ProfScope ps("select", (double)na * m * 9.0);
+      // levels launched before the membership pass: the first step's plain levels need two or three; later
+      // steps' centred level is normally enough (candidate mode); a miss goes through launch_select_finish
       launch_select(b.d2, m, h, b.inst_dev, na, b.sel, b.hist, b.selcnt, memB, memA, b.changed, b.list, b.seg_cnt,
-                    b.ctas, b.seg_len, b.cand, b.cand_cnt, st);
+                    b.ctas, b.seg_len, b.cand, b.cand_cnt, st, step == 1 || !sel_cand_mode() ? 3 : 1);
       fetch(st, {{changed.data(), b.changed, ninst * sizeof(int)}, {status_h.data(), b.status, ninst * sizeof(int)}});
       std::vector<int> more;
       for (int i : act)

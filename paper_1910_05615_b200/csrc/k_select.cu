@@ -374,7 +374,7 @@ static unsigned sel_grid(long long m, int ninst) {
   return (unsigned)std::min<long long>((m + SEL_T - 1) / SEL_T, std::max(1, 148 * per_sm / std::max(1, ninst)));
 }
 
-static bool sel_cand_mode() {
+bool sel_cand_mode() {
   static const bool off = getenv("RTD_SEL_NOCAND") != nullptr;  // r02 path: radix levels to the end
   return !off;
 }
@@ -397,12 +397,12 @@ static void launch_fixup(long long m, const int* inst, int ninst, SelState* st_a
 void launch_select(const double* d2_all, long long m, long long h, const int* inst, int ninst, SelState* st_all,
                    unsigned int* hist_all, unsigned int* cnt_all, uint8_t* mem_new_all, const uint8_t* mem_old_all,
                    int* changed, int* list_all, int* seg_cnt_all, int nseg, long long seg_len, SelCand* cand_all,
-                   int* cand_cnt, cudaStream_t st) {
+                   int* cand_cnt, cudaStream_t st, int nfast) {
   k_sel_init<<<ninst, 32, 0, st>>>(inst, st_all, cnt_all, h, cand_cnt);
   RTD_LAUNCHED();
   const unsigned gx = sel_grid(m, ninst);
   const int cm = sel_cand_mode() ? 1 : 0;
-  for (int L = 0; L < SEL_FAST; L++) {  // (a level exits at once once the instance is done or in candidate mode)
+  for (int L = 0; L < nfast; L++) {  // (a level exits at once once the instance is done or in candidate mode)
     k_sel_level<<<dim3(gx, ninst), SEL_T, 0, st>>>(d2_all, m, inst, st_all, hist_all, cnt_all, cm);
     RTD_LAUNCHED();
   }
@@ -419,7 +419,7 @@ void launch_select_finish(const double* d2_all, long long m, const int* inst, in
                           long long seg_len, SelCand* cand_all, int* cand_cnt, cudaStream_t st) {
   const unsigned gx = sel_grid(m, ninst);
   const int cm = sel_cand_mode() ? 1 : 0;
-  for (int L = SEL_FAST; L < SEL_MAXLEV; L++) {
+  for (int L = 0; L < SEL_MAXLEV - 1; L++) {  // (as many as the state may still need; done levels exit at once)
     k_sel_level<<<dim3(gx, ninst), SEL_T, 0, st>>>(d2_all, m, inst, st_all, hist_all, cnt_all, cm);
     RTD_LAUNCHED();
   }

@@ -203,10 +203,11 @@ struct SelCand {
 // cand_all[inst][SEL_CAND] / cand_cnt[inst]: the candidate-mode buffers (a list entry 0 is a reserved slot of
 // a candidate row that did not change: consumers skip it).
 constexpr int SEL_CAND = 4096;
+bool sel_cand_mode();  // RTD_SEL_NOCAND unset
 void launch_select(const double* d2_all, long long m, long long h, const int* inst, int ninst, SelState* st_all,
                    unsigned int* hist_all, unsigned int* cnt_all, uint8_t* mem_new_all, const uint8_t* mem_old_all,
                    int* changed, int* list_all, int* seg_cnt_all, int nseg, long long seg_len, SelCand* cand_all,
-                   int* cand_cnt, cudaStream_t st);
+                   int* cand_cnt, cudaStream_t st, int nfast = 3);
 void launch_select_finish(const double* d2_all, long long m, const int* inst, int ninst, SelState* st_all,
                           unsigned int* hist_all, unsigned int* cnt_all, uint8_t* mem_new_all,
                           const uint8_t* mem_old_all, int* changed, int* list_all, int* seg_cnt_all, int nseg,
