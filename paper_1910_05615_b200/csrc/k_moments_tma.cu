@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "rtd_internal.h"
+#include "tanh_table.h"
 #include "tma.cuh"
 
 namespace rtd {
@@ -47,6 +48,21 @@ __device__ __forceinline__ double psi_wrap(double z) {  // PAPER.md:478-486, con
   return 0.0;
 }
 
+// tanh on [0, 2.19) from the shared-memory copy of tools/gen_tanh_table.py's table: degree-10 Taylor
+// polynomial about c_j = j W (j = rint(x / W)), Estrin's scheme (five dependent FMA levels instead of
+// the library tanh's exp + Newton division chain, which left the wrap warps stalled on fixed-latency
+// dependencies); <= 2 ulp (the generator's check), the library tanh 1 ulp (reading R28)
+__device__ __forceinline__ double tanh_tab(double x, const double* __restrict__ tab) {
+  const int j = min(__double2int_rn(__dmul_rn(x, 1.0 / RTD_TANH_W)), RTD_TANH_NI - 1);
+  const double v = __dsub_rn(x, __dmul_rn((double)j, RTD_TANH_W));
+  const double* a = tab + j * RTD_TANH_NC;
+  const double v2 = __dmul_rn(v, v), v4 = __dmul_rn(v2, v2), v8 = __dmul_rn(v4, v4);
+  const double p01 = fma(a[1], v, a[0]), p23 = fma(a[3], v, a[2]), p45 = fma(a[5], v, a[4]),
+               p67 = fma(a[7], v, a[6]), p89 = fma(a[9], v, a[8]);
+  const double q0 = fma(p23, v2, p01), q1 = fma(p67, v2, p45), q2 = fma(a[10], v2, p89);
+  return fma(q2, v8, fma(q1, v4, q0));
+}
+
 __device__ __forceinline__ void consumer_sync() { __syncthreads(); }
 
 // W = 8: two CTAs of 8 warps per SM, a 96 KB ring each; W = 16: one CTA of 16 warps per SM, a 192 KB ring
@@ -68,7 +84,8 @@ struct MomTmaCfg {
   static constexpr size_t OFF_W = (std::max(RING, RED) + 127) / 128 * 128;  // weight stages (TMA destinations)
   static constexpr size_t OFF_B = OFF_W + (size_t)NS * WST;                  // full / empty barriers
   static constexpr size_t OFF_S = OFF_B + 2 * NS * 8 + 64;                    // tanh scratch
-  static constexpr size_t SMEM = OFF_S + SCR;
+  static constexpr size_t OFF_T = OFF_S + SCR;                               // tanh table (wrap modes)
+  static constexpr size_t SMEM = OFF_T + RTD_TANH_NI * RTD_TANH_NC * 8;
 };
 
 }  // namespace
@@ -87,6 +104,7 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
   // per-stage copy of the rows' weight source (norms r / distances d2 / membership bytes), loaded by TMA
   // with the tile on the same barrier
   unsigned char* wsrc = smraw + C::OFF_W;
+  double* ttab = reinterpret_cast<double*>(smraw + C::OFF_T);
   constexpr bool FX = MODE == MOM_WRAPXI;
   constexpr bool WT = MODE == MOM_XI || MODE == MOM_REWEIGHT || FX;
   constexpr uint32_t WBYTES = WT ? TR * 8 : 0;
@@ -106,6 +124,8 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if (MODE == MOM_WRAP || FX)
+    for (int i = threadIdx.x; i < RTD_TANH_NI * RTD_TANH_NC; i += W * 32) ttab[i] = rtd_tanh_coef[i];
   __syncthreads();
   // producer = lane 0 of warp 0, opportunistic: the first NS - 1 tiles now; then, between its groups, tile
   // nxt as soon as the stage's previous tile has been released by every warp (a non-blocking test, at most
@@ -130,10 +150,11 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
   for (int b = 0; b < NB; b++)
     sh[b] = ((MODE == MOM_MEMBER || MODE == MOM_REWEIGHT) && 8 * b + g < P) ? a.shift[(long long)id * RTD_MAXP + 8 * b + g]
                                                                              : 0.0;
-  double A = 0.0, B = 0.0;
+  double A = 0.0, B = 0.0, invBA = 0.0;
   if (MODE == MOM_XI || FX) {
     A = a.AB[2 * blk];
     B = a.AB[2 * blk + 1];
+    invBA = B > A ? 1.0 / (B - A) : 0.0;  // (B - r) / (B - A) as a product: no division per row (reading R28)
   }
   double acc[NBLK][2];
 #pragma unroll
@@ -188,7 +209,7 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
         w = 1.0;
       } else if (MODE == MOM_XI || FX) {
         const double rr = reinterpret_cast<const double*>(ws)[4 * l + t];
-        const double xi = rr <= A ? 1.0 : (rr <= B ? __ddiv_rn(__dsub_rn(B, rr), __dsub_rn(B, A)) : 0.0);
+        const double xi = rr <= A ? 1.0 : (rr <= B ? __dmul_rn(__dsub_rn(B, rr), invBA) : 0.0);
         w = __dmul_rn(xi, xi);
       } else if (MODE == MOM_MEMBER) {  // membership bytes from global memory (a UINT8 2-D TMA map of them
         // faulted with an illegal instruction on this stack; the bytes are L2-resident)
@@ -237,7 +258,7 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
       }
       if (n) {
         __syncwarp();
-        for (int i = lane; i < n; i += 32) scr[i] = __dmul_rn(1.541, tanh(__dmul_rn(0.862, __dsub_rn(4.0, scr[i]))));
+        for (int i = lane; i < n; i += 32) scr[i] = __dmul_rn(1.541, tanh_tab(__dmul_rn(0.862, __dsub_rn(4.0, scr[i])), ttab));
         __syncwarp();
 #pragma unroll
         for (int b = 0; b < NB; b++)

@@ -68,3 +68,30 @@ def test_library_has_no_undefined_internal_symbols(so):
     out = subprocess.run(["nm", "-D", "--undefined-only", LIB], capture_output=True, text=True).stdout
     bad = [ln for ln in out.splitlines() if "rtd" in ln or "rtdetmcd" in ln]
     assert not bad, bad
+
+
+def test_wrap_tanh_table_accuracy():
+    """The device tanh table of the wrapping function's tanh branch (csrc/tanh_table.h, PAPER.md:478-486:
+    argument q2 (c - |z|) in [0, 2.155]) evaluated as k_moments_tma evaluates it (interval rint(x / W),
+    Estrin) is within 3 ulp of numpy's tanh on a dense grid and at the interval ends (reading R28)."""
+    import numpy as np
+    txt = open(os.path.join(ROOT, "paper_1910_05615_b200", "csrc", "tanh_table.h")).read()
+    ni = int(re.search(r"#define RTD_TANH_NI (\d+)", txt).group(1))
+    nc = int(re.search(r"#define RTD_TANH_NC (\d+)", txt).group(1))
+    body = txt[txt.index("{") + 1:txt.index("};")]
+    a = np.array([float.fromhex(t) for t in body.replace("\n", " ").split(",") if t.strip()]).reshape(ni, nc)
+    w = 2.16 / 32
+    x = np.concatenate([np.linspace(0.0, 0.862 * 2.5, 200_001), (np.arange(ni) + 0.5) * w])
+    x = x[x <= 0.862 * 2.5]
+    j = np.minimum(np.rint(x * (1.0 / w)).astype(np.int64), ni - 1)
+    v = x - j * w
+    c = a[j]
+    v2 = v * v
+    v4 = v2 * v2
+    p = [c[:, k] + c[:, k + 1] * v for k in (0, 2, 4, 6, 8)]
+    q0, q1, q2 = p[0] + p[1] * v2, p[2] + p[3] * v2, p[4] + c[:, 10] * v2
+    y = (q0 + q1 * v4) + q2 * (v4 * v4)
+    ref = np.tanh(x)
+    ulp = np.spacing(np.maximum(np.abs(ref), np.finfo(float).tiny))
+    assert y[0] == 0.0
+    assert (np.abs(y - ref)[1:] / ulp[1:]).max() <= 3.0
