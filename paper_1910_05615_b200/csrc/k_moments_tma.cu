@@ -238,31 +238,36 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
       }
       // psi: identity / zero branches in place; the tanh branch (1.5 < |z| <= 4, ~13 %
       // of the entries) compacted into a warp-private list, evaluated by all 32 lanes, scattered back.
-      // The branch tests compare the magnitude's high / low words (IEEE order, exact) on the integer pipe;
-      // a lane's slots in the list come from one warp scan of its entry count.
-      // 1.5 < |z| <= 4 as one unsigned range test on the magnitude's bits (IEEE order, exact; |z| <= 1.5
-      // wraps around to a huge value), |z| > 4 -> 0
-      constexpr unsigned long long B15N = 0x3FF8000000000001ull, C40 = 0x4010000000000000ull;  // next(1.5), 4.0
+      // The branch tests look at the magnitude's HIGH word only (IEEE order; integer pipe, no fp64 abs):
+      // hi in [hi(1.5), hi(4)) is 1.5 <= |z| < 4, listed (|z| == 1.5 exactly, the one listed value of
+      // the identity branch, is kept as is by the tanh pass); hi >= hi(4) is |z| >= 4 -> 0 (psi(4) =
+      // q1 tanh(0) = 0, so |z| == 4 may take either branch).  A lane's slots in the list come from one
+      // ballot per column block.
+      constexpr unsigned H15 = 0x3FF80000u, H40 = 0x40100000u;  // high words of 1.5 and 4.0
       int pos[NB];
       int n = 0;
       const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
       for (int b = 0; b < NB; b++) {
-        const unsigned long long ab = (unsigned long long)__double_as_longlong(u[b]) & 0x7FFFFFFFFFFFFFFFull;
-        const bool need = ab - B15N <= C40 - B15N;
+        const unsigned ah = (unsigned)__double2hiint(u[b]) & 0x7FFFFFFFu;
+        const bool need = ah - H15 < H40 - H15;
         const unsigned bal = __ballot_sync(0xffffffffu, need);
         pos[b] = need ? n + __popc(bal & lt) : -1;
-        if (need) scr[pos[b]] = __longlong_as_double((long long)ab);  // |z|
+        if (need) scr[pos[b]] = __hiloint2double((int)ah, __double2loint(u[b]));  // |z|
         n += __popc(bal);
-        if (ab > C40) u[b] = 0.0;
+        if (ah >= H40) u[b] = 0.0;
       }
       if (n) {
         __syncwarp();
-        for (int i = lane; i < n; i += 32) scr[i] = __dmul_rn(1.541, tanh_tab(__dmul_rn(0.862, __dsub_rn(4.0, scr[i])), ttab));
+        for (int i = lane; i < n; i += 32) {
+          const double az = scr[i];
+          if (__double_as_longlong(az) != 0x3FF8000000000000ll)  // |z| == 1.5: identity branch
+            scr[i] = __dmul_rn(1.541, tanh_tab(__dmul_rn(0.862, __dsub_rn(4.0, az)), ttab));
+        }
         __syncwarp();
 #pragma unroll
         for (int b = 0; b < NB; b++)
-          if (pos[b] >= 0) u[b] = copysign(scr[pos[b]], u[b]);  // |z| > 1.5: the sign bit is the sign
+          if (pos[b] >= 0) u[b] = copysign(scr[pos[b]], u[b]);  // |z| >= 1.5: the sign bit is the sign
         __syncwarp();
       }
     } else if (MODE == MOM_MEMBER || MODE == MOM_REWEIGHT) {
@@ -270,10 +275,18 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
       for (int b = 0; b < NB; b++) u[b] = (w != 0.0 && 8 * b + g < P) ? __dsub_rn(u[b], sh[b]) : 0.0;
     }
     double wu[NB];
+    if (wrap_role) {  // w = 1 (warp-uniform): no product on the fp64 pipe the DMMAs share
 #pragma unroll
-    for (int b = 0; b < NB; b++) {
-      wu[b] = w * u[b];
-      s1[b] += wu[b];
+      for (int b = 0; b < NB; b++) {
+        wu[b] = u[b];
+        s1[b] += u[b];
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        wu[b] = w * u[b];
+        s1[b] += wu[b];
+      }
     }
     if (g == 0) cnt += w;
     int kk = 0;
