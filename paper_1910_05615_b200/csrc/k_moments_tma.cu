@@ -275,7 +275,9 @@ __global__ void __launch_bounds__(W * 32, 16 / W)
       for (int b = 0; b < NB; b++) u[b] = (w != 0.0 && 8 * b + g < P) ? __dsub_rn(u[b], sh[b]) : 0.0;
     }
     double wu[NB];
-    if (wrap_role) {  // w = 1 (warp-uniform): no product on the fp64 pipe the DMMAs share
+    // w = 1 (wrap warps; warp-uniform) or w in {0, 1} with u already 0 where w = 0 (member / reweight
+    // modes): w u = u exactly, so no product on the fp64 pipe the DMMAs share
+    if (wrap_role || MODE == MOM_MEMBER || MODE == MOM_REWEIGHT) {
 #pragma unroll
       for (int b = 0; b < NB; b++) {
         wu[b] = u[b];
