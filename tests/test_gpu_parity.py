@@ -255,6 +255,24 @@ def test_initial_estimators_one_pass(cfg, n):
     assert rel_sigma(S2, gsscm_lr(Z)) < 1e-12
 
 
+def test_initial_estimators_one_pass_psi_branch_edges():
+    """The one-pass wrap warps classify psi's branches by the magnitude's high word and evaluate the tanh
+    branch from a table (reading R28): entries exactly at b = 1.5 and c = 4 (psi(1.5) = 1.5, psi(4) = 0),
+    one ulp either side of them, the high-word boundaries 1.5 (1 + 2^-20) and 4 (1 - 2^-52), signed
+    zeros and huge values, on a block the TMA pass takes."""
+    rng = np.random.default_rng(5)
+    m, p = 16_384, 12
+    Z = rng.standard_normal((m, p)) * 1.7
+    edges = np.array([1.5, np.nextafter(1.5, 0), np.nextafter(1.5, 9), 1.5 * (1 + 2.0 ** -20), 4.0,
+                      np.nextafter(4.0, 0), np.nextafter(4.0, 9), 4.0 * (1 - 2.0 ** -52), 0.0, 1e6, 2.0, 3.999])
+    pick = rng.random((m, p)) < 0.3
+    vals = edges[rng.integers(0, edges.size, size=(m, p))] * rng.choice([-1.0, 1.0], size=(m, p))
+    Z[pick] = vals[pick]
+    S1, S2, ok = api.initial(_cuda(Z))
+    assert ok
+    assert rel_sigma(S1, wrapped_covariance(Z)) < 1e-12
+
+
 @pytest.mark.parametrize("cfg,n", [(1, 1000), (2, 20_000), (3, 30_001), (4, 12_345), (5, 20_000)])
 def test_refinement(cfg, n):
     d, Z = _zblock(cfg, n)
