@@ -95,3 +95,17 @@ def test_wrap_tanh_table_accuracy():
     ulp = np.spacing(np.maximum(np.abs(ref), np.finfo(float).tiny))
     assert y[0] == 0.0
     assert (np.abs(y - ref)[1:] / ulp[1:]).max() <= 3.0
+
+
+def test_wrap_tanh_table_matches_its_generator():
+    """csrc/tanh_table.h holds exactly the coefficients tools/gen_tanh_table.py derives (mpmath Taylor
+    coefficients about c_j = j W rounded to fp64): the table is not hand-edited."""
+    import importlib.util
+    import numpy as np
+    spec = importlib.util.spec_from_file_location("gen_tanh_table", os.path.join(ROOT, "tools", "gen_tanh_table.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    txt = open(os.path.join(ROOT, "paper_1910_05615_b200", "csrc", "tanh_table.h")).read()
+    body = txt[txt.index("{") + 1:txt.index("};")]
+    a = np.array([float.fromhex(t) for t in body.replace("\n", " ").split(",") if t.strip()])
+    assert np.array_equal(a, gen.coeffs().ravel())
